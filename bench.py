@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""Benchmark: row-sharded sketched rSVD on 1..8 B200s (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A "step" is one full pass of the hot path over the resident input: CountSketch
+draw (K1) -> A~ = A S (K2, fused ||A||_F^2 + finiteness) -> Y = A~ Omega ->
+q x {CholeskyQR2(Y); Z = sum_p A~_p^T Y_p (NCCL); Y = A~ Z} -> CholeskyQR2 ->
+B = sum_p Q_p^T A_p (NCCL) -> Gram + Jacobi -> U, sigma, V.
+
+value      = device time of one rSVD (ms, max over ranks), inputs resident in HBM.
+e2e        = the same through the public API ``paper_2605_09755_b200.rsvd`` with
+             the input in pinned host memory (H2D inside the timed region) and
+             U, sigma, V copied back (D2H inside).
+roofline   = the dominant kernel of the step, measured live with CUDA events.
+cpu_baseline / --impl reference = the oracle port (oracle/skp_oracle.py, the
+             reference's algorithm on numpy/scipy) on a bounded row slab,
+             extrapolated per phase to the full workload.
+Inputs (A = 17 GB at C3) are far larger than the 126 MB L2, so no flush is
+needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "rSVD time/sketch HBM GB/s/power-iter TFLOP/s vs roofline at 1/2/4/8 B200"
+
+# BASELINE.json configs (C4 = Nystrom; C5 needs one full GPU of HBM at l=8000)
+CONFIGS = {
+    "C1": dict(m=2000, n=1000, l=200, s=8, k=20, r2=30, q=2, dtype="f64", gen="c1"),
+    "C2": dict(m=20000, n=10000, l=2000, s=8, k=100, r2=110, q=3, dtype="f32", gen="c2"),
+    "C3": dict(m=262144, n=16384, l=4000, s=8, k=500, r2=520, q=3, dtype="f32", gen="c3"),
+    "C5": dict(m=1048576, n=32768, l=8000, s=8, k=1000, r2=1050, q=4, dtype="f32", gen="c5"),
+}
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), \
+            d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(5)
+            except Exception:
+                self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7
+                          for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ inputs --
+def make_input(cfg, row0, rows, device):
+    import torch
+    from paper_2605_09755_b200 import datagen
+    g = cfg["gen"]
+    if g == "c1":
+        return torch.from_numpy(datagen.c1_matrix(1)[row0:row0 + rows]).to(device)
+    if g == "c2":
+        return torch.from_numpy(datagen.c2_matrix(2)[row0:row0 + rows]).to(device)
+    if g == "c3":
+        return datagen.c3_matrix_gpu(3, cfg["m"], cfg["n"], device=device, row0=row0, rows=rows)
+    if g == "c5":
+        return datagen.c5_matrix_gpu(5, cfg["m"], cfg["n"], device=device, row0=row0, rows=rows)
+    raise ValueError(g)
+
+
+def spec_of(cfg, seed):
+    from paper_2605_09755_b200 import RangeFinderSpec
+    return RangeFinderSpec(k=cfg["k"], l=cfg["l"], r1=cfg["l"], r2=cfg["r2"], q=cfg["q"], eps=0.5,
+                           sketch_kind="countsketch", seed=seed, s=cfg["s"])
+
+
+def flops_of(cfg):
+    m, n, l, r2, q = cfg["m"], cfg["n"], cfg["l"], cfg["r2"], cfg["q"]
+    power = (1 + 2 * q) * 2.0 * m * l * r2
+    orth = (q + 1) * 2 * (2.0 * m * r2 * r2 + 2.0 * m * r2 * r2)   # 2 passes x (Gram + Y R^-1)
+    qta = 2.0 * m * n * r2
+    return power, orth, qta
+
+
+# ---------------------------------------------------------- CPU baseline ----
+def cpu_baseline(cfg, sample_rows: int, reps: int = 1):
+    """Oracle port on a row slab; phases extrapolated linearly in m (except
+    those independent of m).  Returns (ms for the full workload, details)."""
+    from oracle import skp_oracle as o
+    m, n = cfg["m"], cfg["n"]
+    rows = min(sample_rows, m)
+    rng = np.random.default_rng(0)
+    # same structure as the workload: low rank + noise (values only shape the flops)
+    r = min(256, n)
+    a = ((rng.standard_normal((rows, r)) @ rng.standard_normal((r, n))) / math.sqrt(r * n)).astype(
+        np.float32 if cfg["dtype"] == "f32" else np.float64)
+    spec = o.Spec(k=cfg["k"], l=cfg["l"], r1=cfg["l"], r2=cfg["r2"], q=cfg["q"], seed=3, s=cfg["s"])
+    best = None
+    for _ in range(reps):
+        t = {}
+        qb = o.range_finder_sketched(a, spec, timings=t)
+        t0 = time.perf_counter()
+        b = qb.T @ a.astype(np.float64)
+        t["qta"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        o.thin_svd(b)
+        t["svd"] = time.perf_counter() - t0
+        best = t if best is None or sum(t.values()) < sum(best.values()) else best
+    scale = m / rows
+    linear = ("cast", "apply_right", "power", "orth", "qta")
+    full = sum(v * (scale if k in linear else 1.0) for k, v in best.items())
+    return full * 1e3, {"phases_s_sample": {k: round(v, 4) for k, v in best.items()},
+                        "rows_sampled": rows, "extrapolated_to_m": m}
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+# --------------------------------------------------------------- the arm ----
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2605_09755_b200 as skp
+    from paper_2605_09755_b200 import _lib, distributed as D
+    from paper_2605_09755_b200.sketching import make_sketch, substream
+
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    comm = D.TorchComm() if world > 1 else None
+    m, n = cfg["m"], cfg["n"]
+    row0, rows = D.shard_rows(m, world, rank)
+    a = make_input(cfg, row0, rows, device)
+    torch.cuda.synchronize()
+    spec = spec_of(cfg, seed=cfg.get("seed", 3))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(timings=None):
+        if world > 1:
+            return D.rsvd_sharded(a, spec, m, comm, timings)
+        return D.rsvd_sharded(a, spec, m, _LocalComm(), timings)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = _lib.load().skp_launch_count()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    phases = {}
+    t_start.record()
+    rel = None
+    for _ in range(args.steps):
+        _, sig, _, rel = step(phases)
+    t_end.record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    launches = _lib.load().skp_launch_count() - launches0
+    ms = t_start.elapsed_time(t_end) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    phases = {k: v / args.steps for k, v in phases.items()}
+
+    # ---- dominant-kernel measurements (live, CUDA events on this stream) ----
+    hbm, bf16, bf16_sus, peak_src = load_peaks()
+    sk = make_sketch("countsketch", n, cfg["l"], substream(spec.seed, 0), s=cfg["s"], device=device)
+    atil = torch.empty((rows, cfg["l"]), dtype=a.dtype, device=device)
+    fro2 = torch.zeros(1, dtype=torch.float64, device=device)
+    for _ in range(2):
+        sk.right(a, out=atil, fro2=fro2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        sk.right(a, out=atil, fro2=fro2)
+    e1.record()
+    torch.cuda.synchronize()
+    sketch_ms = e0.elapsed_time(e1) / reps
+    esz = a.element_size()
+    sketch_bytes = rows * n * esz + rows * cfg["l"] * esz + n * cfg["s"] * 5 + (cfg["l"] + 1) * 4
+    sketch_gbs = sketch_bytes / (sketch_ms * 1e-3) / 1e9
+    # power-iteration GEMM: Y = A~ Z  (rows x l) . (l x r2)
+    from paper_2605_09755_b200 import _ops
+    z = torch.randn(cfg["l"], cfg["r2"], device=device, dtype=a.dtype)
+    y = torch.empty(rows, cfg["r2"], device=device, dtype=a.dtype)
+    for _ in range(2):
+        _ops.gemm(atil, z, out=y)
+    e0.record()
+    for _ in range(reps):
+        _ops.gemm(atil, z, out=y)
+    e1.record()
+    torch.cuda.synchronize()
+    gemm_ms = e0.elapsed_time(e1) / reps
+    gemm_flop = 2.0 * rows * cfg["l"] * cfg["r2"]
+    gemm_tflops = gemm_flop / (gemm_ms * 1e-3) / 1e12
+    power_f, orth_f, qta_f = flops_of(cfg)
+    tc = bool(_lib.load().skp_has_tcgen05())
+    # tensor-pipe view of 3xTF32: 3 TF32 MMAs per useful MAC, TF32 rate = bf16 / 2
+    pipe_tflops = gemm_tflops * 3 if (tc and cfg["dtype"] == "f32") else gemm_tflops
+    tf32_peak = bf16 / 2.0
+    power_tflops = (power_f / world) / (phases.get("power", float("nan")) * 1e-3) / 1e12
+    dominant = "power" if phases.get("power", 0) >= phases.get("apply_right", 0) else "sketch"
+    if dominant == "power":
+        roof = {"kernel": "gemm_nn A~.Z (power iteration)" + (" tcgen05 3xTF32" if tc else " SIMT"),
+                "bound": "tensor", "achieved": round(pipe_tflops, 2), "peak": round(tf32_peak, 1),
+                "unit": "TFLOP/s", "frac": round(pipe_tflops / tf32_peak, 4), "traffic": None,
+                "useful_tflops": round(gemm_tflops, 2), "ms_per_launch": round(gemm_ms, 4),
+                "peak_note": f"TF32 dense = bf16/2 of {peak_src} bf16 {bf16} TFLOP/s",
+                "algorithmic_flop_per_launch": gemm_flop}
+    else:
+        roof = {"kernel": "sketch_right (K2)", "bound": "hbm", "achieved": round(sketch_gbs, 1),
+                "peak": hbm, "unit": "GB/s", "frac": round(sketch_gbs / hbm, 4), "traffic": None,
+                "ms_per_launch": round(sketch_ms, 4), "algorithmic_bytes_per_launch": sketch_bytes}
+    extra = {
+        "sketch": {"ms": round(sketch_ms, 4), "GB/s": round(sketch_gbs, 1),
+                   "frac_hbm": round(sketch_gbs / hbm, 4), "bytes": sketch_bytes},
+        "power_gemm": {"ms": round(gemm_ms, 4), "useful_TFLOP/s": round(gemm_tflops, 2),
+                       "pipe_frac": round(pipe_tflops / tf32_peak, 4)},
+        "power_phase_TFLOP/s": round(power_tflops, 2),
+    }
+
+    # ---- end to end through the public API from pinned host memory ----------
+    e2e = None
+    if not args.no_e2e:
+        host = a.cpu().pin_memory()
+        torch.cuda.synchronize()
+        for _ in range(max(1, min(args.warmup, 2))):
+            skp.rsvd(host, spec) if world == 1 else _e2e_sharded(host, spec, m, comm, device, D)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        k2 = max(1, min(args.steps, 3))
+        for _ in range(k2):
+            if world == 1:
+                res = skp.rsvd(host, spec)
+                out_b = res.U.numel() * res.U.element_size() + res.V.numel() * res.V.element_size() \
+                    + res.sigma.numel() * res.sigma.element_size()
+            else:
+                out_b = _e2e_sharded(host, spec, m, comm, device, D)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / k2
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": round(e2e_ms, 3), "unit": "ms",
+               "h2d_bytes_per_step": int(host.numel() * host.element_size()),
+               "d2h_bytes_per_step": int(out_b), "steps": k2}
+
+    if rank != 0:
+        return None
+    line = {
+        "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": cfg["dtype"] + ("(3xTF32 tcgen05)" if tc and cfg["dtype"] == "f32" else ""),
+        "data": "synthetic (seeded, BASELINE config recipe; random-init factors, no dataset)",
+        "config": {"workload": args.config, "m": m, "n": n, "l": cfg["l"], "s": cfg["s"],
+                   "k": cfg["k"], "r2": cfg["r2"], "q": cfg["q"],
+                   "parallelism": f"rows sharded x{world} (NCCL allreduce of l x r2 / r2 x r2 / r2 x n)",
+                   "l2": "no flush: A is far larger than the 126 MB L2"},
+        "phases_ms": {k: round(v, 3) for k, v in phases.items()},
+        "rel_err": rel, "sigma_1": float(sig[0].item()),
+        "roofline": roof, **extra,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    return line
+
+
+class _LocalComm:
+    rank, world = 0, 1
+
+    def allreduce_(self, t):
+        return t
+
+
+def _e2e_sharded(host, spec, m, comm, device, D):
+    a = host.to(device, non_blocking=True)
+    u, s, v, _ = D.rsvd_sharded(a, spec, m, comm)
+    u_h, s_h, v_h = u.cpu(), s.cpu(), v.cpu()
+    return u_h.numel() * 4 + s_h.numel() * 8 + v_h.numel() * 4
+
+
+def run_reference(args, cfg):
+    ncores = host_threads()
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(var, str(ncores))
+    sample = args.cpu_rows
+    vals = []
+    det = None
+    for i in range(args.warmup + args.steps):
+        v, det = cpu_baseline(cfg, sample)
+        if i >= args.warmup:
+            vals.append(v)
+    val = statistics.median(vals)
+    return {
+        "metric": METRIC, "impl": "reference", "value": round(val, 1), "unit": "ms",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(val, 1), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64 (numpy/scipy, as the reference computes)",
+        "data": "synthetic", "config": {"workload": args.config, **{k: cfg[k] for k in
+                                                                    ("m", "n", "l", "s", "k", "r2", "q")}},
+        "cpu_baseline": {"value": round(val, 1), "unit": "ms", "cores": ncores, "kind": "port",
+                         "sample": f"{det['rows_sampled']} of {cfg['m']} rows, phases extrapolated "
+                                   f"linearly in m (sketch/SVD-of-B phases not scaled)",
+                         **det},
+        "e2e": {"value": round(val, 1), "unit": "ms", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--q", type=int, default=None)
+    ap.add_argument("--l", type=int, default=None)
+    ap.add_argument("--cpu-rows", type=int, default=4096)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.q is not None:
+        cfg["q"] = args.q
+    if args.l is not None:
+        cfg["l"] = args.l
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, cfg)), flush=True)
+        return
+
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = run_ours(args, cfg, rank, world, local_rank)
+    if line is not None:
+        if world == 1 and not args.no_cpu:
+            v, det = cpu_baseline(cfg, args.cpu_rows)
+            line["cpu_baseline"] = {"value": round(v, 1), "unit": "ms", "cores": host_threads(),
+                                    "kind": "port",
+                                    "sample": f"{det['rows_sampled']} of {cfg['m']} rows, "
+                                              f"extrapolated linearly in m", **det}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,175 @@
+/*
+ * skp.h -- C ABI of the B200-native sketched power method (libskp.so).
+ *
+ * Drop-in boundary for the reference's hot path
+ * (/root/reference/pkg/src/skpower, a pure NumPy/SciPy package with no FFI of
+ * its own; its boundary is the Python call surface re-exported at
+ * pkg/src/skpower/__init__.py:25-86).  Each entry point below names the
+ * reference operation it replaces.  The Python facade
+ * (paper_2605_09755_b200/) binds these with ctypes; INTEGRATION.md shows the
+ * binding a maintainer of the reference would add.
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes, no torch types; every array argument is a
+ *     DEVICE pointer on the current CUDA device; matrices are row-major with
+ *     an explicit leading dimension (elements);
+ *   - no allocation inside: scratch comes from the caller (`ws`, sized by the
+ *     matching *_ws_bytes query);
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); every call is
+ *     asynchronous on it; no host synchronisation unless stated;
+ *   - return 0 (SKP_OK) or a status code; skp_last_error() returns the
+ *     calling thread's last message.  Thread-safe, stateless.
+ */
+#ifndef SKP_H_
+#define SKP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SKP_OK = 0,
+    SKP_ERR_ARG = 1,          /* -> ValueError in the facade */
+    SKP_ERR_CUDA = 2,         /* -> RuntimeError */
+    SKP_ERR_UNSUPPORTED = 3,  /* -> ValueError ("unsupported") */
+    SKP_ERR_NUMERIC = 4
+};
+
+const char* skp_last_error(void);
+int skp_abi_version(void);
+/* Number of kernels this process has launched through libskp (all threads). */
+int64_t skp_launch_count(void);
+/* 1 if the tcgen05 (sm_100a) GEMM path is compiled in and the device is sm_100. */
+int skp_has_tcgen05(void);
+
+/* ---------------------------------------------------------------- K1 ----
+ * CountSketch draw, bit-exact with numpy 2.3.5 PCG64.
+ * Replaces SketchOperator.__init__ countsketch branch + _draw_countsketch
+ * (reference sketching.py:114-124, :141-150).  (st, inc) is the 128-bit PCG64
+ * state of _rng(seed) (sketching.py:57-58), split in 64-bit halves.
+ * Rows [j0, j1) of the n x s arrays are written to cols[(j-j0)*s + t]
+ * (int32 column index, ascending-key order) and signs[...] (+1 / -1).
+ * Supported: 1 <= s <= 32, r < 2^31 (s == 1: r <= 2^31 - 1).
+ * s == 1 needs `ws` (skp_countsketch_ws_bytes) and synchronises the stream
+ * once if Lemire rejections exhaust the first candidate window.            */
+int64_t skp_countsketch_ws_bytes(int64_t n, int64_t r, int32_t s);
+int skp_countsketch_gen(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
+                        int64_t n, int64_t r, int32_t s, int64_t j0, int64_t j1,
+                        int32_t* cols, int8_t* signs, void* ws, int64_t ws_bytes,
+                        void* stream);
+
+/* Column-compressed (CSC) view of S for the gather kernels: colptr[r+1],
+ * entries[n*s] = j | (sign < 0) << 31, each column's entries ascending in j
+ * (deterministic).  ws: skp_countsketch_csc_ws_bytes.                       */
+int64_t skp_countsketch_csc_ws_bytes(int64_t n, int32_t s, int64_t r);
+int skp_countsketch_csc(const int32_t* cols, const int8_t* signs, int64_t n, int32_t s,
+                        int64_t r, int32_t* colptr, int32_t* entries, void* ws,
+                        int64_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- K2 ----
+ * out (m x r) = A (m x n) . S / ... i.e. SketchOperator.apply_right for a
+ * countsketch (reference sketching.py:158-164: `a @ self._sparse`).  Fused:
+ * fro2 += ||A||_F^2 (double) and nonfinite += #non-finite entries of A (the
+ * as_matrix finiteness contract, linalg.py:30-39).  fro2 / nonfinite may be
+ * NULL.                                                                     */
+int skp_sketch_right_f32(const float* A, int64_t lda, int64_t m, int64_t n,
+                         const int32_t* colptr, const int32_t* entries, int32_t s, int64_t r,
+                         float* out, int64_t ldo, double* fro2, int64_t* nonfinite,
+                         void* stream);
+int skp_sketch_right_f64(const double* A, int64_t lda, int64_t m, int64_t n,
+                         const int32_t* colptr, const int32_t* entries, int32_t s, int64_t r,
+                         double* out, int64_t ldo, double* fro2, int64_t* nonfinite,
+                         void* stream);
+
+/* ---------------------------------------------------------------- K3 ----
+ * out (r x c) = S^T . X (X n x c); SketchOperator.apply_left_transpose
+ * (reference sketching.py:176-182: `self._sparse.T @ a`).                   */
+int skp_sketch_left_t_f32(const float* X, int64_t ldx, int64_t n, int64_t c,
+                          const int32_t* colptr, const int32_t* entries, int32_t s, int64_t r,
+                          float* out, int64_t ldo, void* stream);
+int skp_sketch_left_t_f64(const double* X, int64_t ldx, int64_t n, int64_t c,
+                          const int32_t* colptr, const int32_t* entries, int32_t s, int64_t r,
+                          double* out, int64_t ldo, void* stream);
+
+/* ---------------------------------------------------------------- K4 ----
+ * C (M x N) = alpha * op(A) . op(B) + beta * C, row-major.
+ * op(A) is M x K: transA == 0 -> A is M x K (lda >= K); 1 -> A is K x M.
+ * op(B) is K x N: transB == 0 -> B is K x N (ldb >= N); 1 -> B is N x K.
+ * Replaces the dense products of power_iterate (power.py:129-133), randsvd
+ * (power.py:194-199) and nystrom_psd (power.py:280-287), which the reference
+ * runs through OpenBLAS dgemm.
+ * f32 mode: 0 = auto (3xTF32 on tcgen05 when available, else SIMT fp32),
+ *           1 = 3xTF32 tcgen05 (error if unavailable), 2 = SIMT fp32 FFMA.
+ * f64: SIMT FP64 (mode ignored).
+ * ws: skp_gemm_ws_bytes (split-K partials; 0 bytes is always accepted and
+ * disables split-K).                                                        */
+int64_t skp_gemm_ws_bytes(int transA, int transB, int64_t M, int64_t N, int64_t K,
+                          int32_t elem_bytes, int32_t mode);
+int skp_gemm_f32(int transA, int transB, int64_t M, int64_t N, int64_t K, float alpha,
+                 const float* A, int64_t lda, const float* B, int64_t ldb, float beta,
+                 float* C, int64_t ldc, int32_t mode, void* ws, int64_t ws_bytes,
+                 void* stream);
+int skp_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+                 const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                 double* C, int64_t ldc, int32_t mode, void* ws, int64_t ws_bytes,
+                 void* stream);
+
+/* ---------------------------------------------------------------- K5 ----
+ * CholeskyQR2 building blocks (replace orthonormalize's pivoted QR,
+ * reference linalg.py:57-81).  All fp64, n <= 4096.
+ * cholesky: G (n x n, ld) -> lower L in place (strict upper clobbered);
+ *   *info (device int) = 0 or the 1-based index of the first non-positive
+ *   pivot.                                                                  */
+int skp_cholesky_f64(double* G, int64_t n, int64_t ld, int32_t* info, void* stream);
+/* Rank check after skp_cholesky_f64: if *info == 0 and
+ * min_i L_ii < rel_tol * max_i L_ii, sets *info = -1 (numerically rank
+ * deficient; the facade then takes the eigen-based truncating path, matching
+ * orthonormalize's column dropping, linalg.py:75-81).                       */
+int skp_chol_pivot_check_f64(const double* L, int64_t n, int64_t ld, double rel_tol,
+                             int32_t* info, void* stream);
+/* X (n x n, dense, row-major) = L^{-1} (lower; strict upper zeroed). */
+int skp_trinv_lower_f64(const double* L, int64_t ldl, int64_t n, double* X, void* stream);
+
+/* ---------------------------------------------------------------- K6 ----
+ * Symmetric eigensolver (parallel cyclic Jacobi, fp64) for the small cores:
+ * the Gram B B^T of randsvd's B = Q^T A (replaces thin_svd / gesdd,
+ * linalg.py:84-88) and the Nystrom W.  A (n x n) is destroyed.  On return
+ * W[n] holds eigenvalues DESCENDING and V (n x n) the matching eigenvectors
+ * as columns.  *sweeps (device int) = sweeps used.                          */
+int64_t skp_syevj_ws_bytes(int64_t n);
+int skp_syevj_f64(double* A, int64_t n, double* W, double* V, int32_t max_sweeps,
+                  void* ws, int64_t ws_bytes, int32_t* sweeps, void* stream);
+
+/* ----------------------------------------------------------- utilities -- */
+int skp_cast_f32_f64(const float* x, double* y, int64_t count, void* stream);
+int skp_cast_f64_f32(const double* x, float* y, int64_t count, void* stream);
+/* out[0] += sum of squares (double), nonfinite[0] += #non-finite (either may be NULL) */
+int skp_sumsq_f32(const float* X, int64_t rows, int64_t cols, int64_t ld, double* out,
+                  int64_t* nonfinite, void* stream);
+int skp_sumsq_f64(const double* X, int64_t rows, int64_t cols, int64_t ld, double* out,
+                  int64_t* nonfinite, void* stream);
+/* W = (W + W^T) / 2 in place (power.py:276, :287) */
+int skp_symmetrize_f32(float* W, int64_t n, int64_t ld, void* stream);
+int skp_symmetrize_f64(double* W, int64_t n, int64_t ld, void* stream);
+/* X[:, j] *= scale[j] */
+int skp_scale_cols_f32(float* X, int64_t rows, int64_t cols, int64_t ld, const double* scale,
+                       void* stream);
+int skp_scale_cols_f64(double* X, int64_t rows, int64_t cols, int64_t ld, const double* scale,
+                       void* stream);
+/* out[0] = max_ij |G_ij - delta_ij|  (randsvd's orthonormality check, power.py:194-196) */
+int skp_orth_dev_f64(const double* G, int64_t n, int64_t ld, double* out, void* stream);
+/* Eigen-based orthonormaliser (rank-revealing fallback for orthonormalize):
+ * given eigen-decomposition (W desc, V) of G = Y^T Y, writes T (n x n, ld n)
+ * = V[:, :k] diag(W[:k]^{-1/2}) padded with zero columns and *k_out = number
+ * of eigenvalues > rel_tol * W[0] (device int).                              */
+int skp_eig_orth_f64(const double* W, const double* V, int64_t n, double rel_tol, double* T,
+                     int32_t* k_out, void* stream);
+/* sigma[i] = sqrt(max(W[i], 0)); inv[i] = sigma[i] > 0 ? 1/sigma[i] : 0 */
+int skp_sqrt_eigs_f64(const double* W, int64_t n, double* sigma, double* inv, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKP_H_ */

@@ -1,0 +1,118 @@
+"""Backend-agnostic orchestration of the sketched power method.
+
+The algorithm (reference power.py:113-154, :181-199, :258-298 and
+linalg.py:57-88) written once against two small interfaces:
+
+* a compute backend ``be`` (``_ops.CudaBackend`` in the product: every call is
+  a libskp kernel) providing mm / gram64 / chol_inv64 / eig_desc64 / ...;
+* a communicator ``comm`` with ``allreduce_(t)`` (in-place sum over ranks)
+  for row-sharded runs: A, A.S and Y live as row slabs, and only the l x r2
+  product A~^T Y, the r2 x r2 Gram matrices and the r2 x n matrix Q^T A are
+  summed.
+
+Orthonormalisation is CholeskyQR2 (two passes of Gram -> Cholesky -> L^{-1}
+-> Y L^{-T}).  Where the reference's pivoted QR would drop columns
+(linalg.py:75-81) the Cholesky pivot check fails and an eigen-based
+truncating pass (Y V_k Lambda_k^{-1/2}) runs first.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+class LocalComm:
+    rank = 0
+    world = 1
+
+    def allreduce_(self, t):
+        return t
+
+
+LOCAL = LocalComm()
+
+# Relative pivot floor for the Gram-based rank test: CholeskyQR resolves
+# sigma_i / sigma_1 down to ~sqrt(eps) of the Gram's precision, so the
+# reference tolerance max(m, c) * eps (linalg.py:51-54) is raised to these
+# floors (documented deviation).
+PIVOT_FLOOR = {"float64": 1e-6, "float32": 5e-4}
+ORTHO_TOL = {"float64": 1e-6, "float32": 1e-4}
+
+
+def _dtype_key(be) -> str:
+    return "float32" if "32" in str(be.dtype) else "float64"
+
+
+def pivot_tol(be, rows: int, cols: int, tol=None) -> float:
+    ref = (max(rows, cols) * np.finfo(np.float64).eps) if tol is None else float(tol)
+    return max(ref, PIVOT_FLOOR[_dtype_key(be)])
+
+
+def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None):
+    """Orthonormal basis of range(y) (linalg.py:57-81) by CholeskyQR2."""
+    c = y.shape[1]
+    rows_total = y.shape[0] if rows_total is None else rows_total
+    rel = pivot_tol(be, rows_total, c, tol)
+    g = comm.allreduce_(be.gram64(y))
+    x = be.chol_inv64(g, rel)
+    if x is None:
+        w, v = be.eig_desc64(g)
+        t, k = be.eig_orth64(w, v, rel * rel)
+        if k == 0:
+            raise ValueError("cannot orthonormalize an all-zero matrix")
+        y = be.mm(y, be.to_compute(be.cols(t, k)))
+        g = comm.allreduce_(be.gram64(y))
+        x = be.chol_inv64(g, 0.0)
+        if x is None:
+            raise RuntimeError("orthonormalize: Cholesky failed after rank truncation")
+    q = be.mm(y, be.to_compute(x), tb=True)
+    g2 = comm.allreduce_(be.gram64(q))
+    x2 = be.chol_inv64(g2, 0.0)
+    if x2 is None:
+        raise RuntimeError("orthonormalize: second CholeskyQR pass failed")
+    return be.mm(q, be.to_compute(x2), tb=True)
+
+
+def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_total=None):
+    """power.py:113-134 on a row slab of A~: Y = A~ Omega, then q x
+    {orth(Y) if stabilized; Z = sum_p A~_p^T Y_p; Y = A~ Z}."""
+    y = be.mm(atil, omega)
+    for _ in range(q):
+        if stabilized:
+            y = orthonormalize(be, comm, y, rows_total=rows_total)
+        z = comm.allreduce_(be.mm(atil, y, ta=True))
+        y = be.mm(atil, z)
+    return y
+
+
+def randsvd(be, comm, a, qb, check: bool = True):
+    """power.py:181-199: B = Q^T A (summed over row slabs), thin SVD of B via
+    the fp64 Gram B B^T and the Jacobi eigensolver; U = Q U~, V = B^T U~ / sigma."""
+    if check:
+        g = comm.allreduce_(be.gram64(qb))
+        dev = be.orth_dev(g)
+        if not dev <= ORTHO_TOL[_dtype_key(be)]:
+            raise ValueError(f"Q is not orthonormal (deviation {dev:.3e})")
+    b = comm.allreduce_(be.mm(qb, a, ta=True))            # c x n
+    c, n = b.shape
+    gb = be.gram64_rows(b)                                  # c x c, fp64
+    w, v = be.eig_desc64(gb)
+    p = min(c, n)
+    sig, inv = be.sqrt_eigs(w)
+    vc = be.to_compute(be.cols(v, p))
+    u = be.mm(qb, vc)
+    vv = be.mm(b, vc, ta=True)
+    be.scale_cols_(vv, inv[:p])
+    return u, sig[:p], vv
+
+
+def nystrom(be, comm, ctil, wtil, omega, q: int, stabilized: bool):
+    """power.py:276-287 given C~ (row slab) and the summed, symmetrised W~."""
+    y = omega
+    for _ in range(q):
+        if stabilized:
+            y = orthonormalize(be, LOCAL, y)
+        y = be.mm(wtil, y)
+    cmat = be.mm(ctil, y)
+    w = be.mm(y, be.mm(wtil, y), ta=True)
+    be.symmetrize_(w)
+    return cmat, w

@@ -1,0 +1,279 @@
+"""Device operations over torch CUDA tensors, each one libskp call (or a few).
+
+torch is plumbing here: device memory, the current stream and dtype tags.
+Every arithmetic step runs in libskp.so kernels; nothing falls back to torch
+or the CPU.  ``CudaBackend`` is the compute backend the algorithm engine
+(``_engine.py``) drives.
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call
+
+F32, F64 = torch.float32, torch.float64
+_SFX = {F32: "f32", F64: "f64"}
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2605_09755_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    _lib.load()
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {d}")
+    return d if d.index is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class _Workspace(threading.local):
+    """Per-thread, per-device scratch (callers on different threads never share)."""
+
+    def __init__(self):
+        self.buf = {}
+
+    def get(self, device: torch.device, nbytes: int) -> torch.Tensor:
+        key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+        b = self.buf.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=device)
+            self.buf[key] = b
+        return b
+
+
+_WS = _Workspace()
+
+
+def workspace(device, nbytes: int) -> torch.Tensor:
+    return _WS.get(device, nbytes)
+
+
+def _rows_ld(x: torch.Tensor):
+    if x.dim() != 2:
+        raise ValueError(f"expected a 2-D tensor, got shape {tuple(x.shape)}")
+    if x.stride(1) != 1:
+        raise ValueError("expected unit column stride (row-major)")
+    return x.shape[0], x.shape[1], x.stride(0)
+
+
+# --------------------------------------------------------------- sketch ----
+
+def countsketch(state: int, inc: int, n: int, r: int, s: int, device, j0: int = 0,
+                j1: int | None = None):
+    """K1: rows [j0, j1) of (cols int32 (rows, s), signs int8 (rows, s))."""
+    j1 = n if j1 is None else j1
+    m64 = (1 << 64) - 1
+    cols = torch.empty((j1 - j0, s), dtype=torch.int32, device=device)
+    signs = torch.empty((j1 - j0, s), dtype=torch.int8, device=device)
+    lib = _lib.load()
+    wsb = lib.skp_countsketch_ws_bytes(n, r, s)
+    ws = workspace(device, wsb) if wsb else None
+    call("skp_countsketch_gen", (state >> 64) & m64, state & m64, (inc >> 64) & m64, inc & m64,
+         n, r, s, j0, j1, ptr(cols), ptr(signs), ptr(ws), wsb, stream_ptr(device))
+    return cols, signs
+
+
+def csc(cols: torch.Tensor, signs: torch.Tensor, n: int, s: int, r: int):
+    """CSC view of S: (colptr int32 (r+1,), entries int32 (n*s,))."""
+    dev = cols.device
+    colptr = torch.empty(r + 1, dtype=torch.int32, device=dev)
+    entries = torch.empty(n * s, dtype=torch.int32, device=dev)
+    wsb = _lib.load().skp_countsketch_csc_ws_bytes(n, s, r)
+    ws = workspace(dev, wsb)
+    call("skp_countsketch_csc", ptr(cols), ptr(signs), n, s, r, ptr(colptr), ptr(entries),
+         ptr(ws), wsb, stream_ptr(dev))
+    return colptr, entries
+
+
+def sketch_right(a: torch.Tensor, colptr, entries, s: int, r: int, out=None, fro2=None,
+                 nonfinite=None):
+    """K2: a (m x n) @ S -> (m x r), fused ||a||_F^2 / non-finite count."""
+    m, n, lda = _rows_ld(a)
+    if out is None:
+        out = torch.empty((m, r), dtype=a.dtype, device=a.device)
+    _, _, ldo = _rows_ld(out)
+    call(f"skp_sketch_right_{_SFX[a.dtype]}", ptr(a), lda, m, n, ptr(colptr), ptr(entries), s, r,
+         ptr(out), ldo, ptr(fro2), ptr(nonfinite), stream_ptr(a.device))
+    return out
+
+
+def sketch_left_t(x: torch.Tensor, colptr, entries, s: int, r: int, out=None):
+    """K3: S^T @ x (x n x c) -> (r x c)."""
+    n, c, ldx = _rows_ld(x)
+    if out is None:
+        out = torch.empty((r, c), dtype=x.dtype, device=x.device)
+    _, _, ldo = _rows_ld(out)
+    call(f"skp_sketch_left_t_{_SFX[x.dtype]}", ptr(x), ldx, n, c, ptr(colptr), ptr(entries), s, r,
+         ptr(out), ldo, stream_ptr(x.device))
+    return out
+
+
+# ----------------------------------------------------------------- gemm ----
+
+GEMM_MODE = {"auto": 0, "3xtf32": 1, "fp32": 2}
+
+
+def gemm(a, b, ta: bool = False, tb: bool = False, alpha: float = 1.0, beta: float = 0.0,
+         out=None, mode: str = "auto"):
+    """K4: out = alpha * op(a) @ op(b) + beta * out."""
+    if a.dtype != b.dtype:
+        raise ValueError("gemm operands must share a dtype")
+    ra, ca, lda = _rows_ld(a)
+    rb, cb, ldb = _rows_ld(b)
+    M, K = (ca, ra) if ta else (ra, ca)
+    Kb, N = (cb, rb) if tb else (rb, cb)
+    if K != Kb:
+        raise ValueError(f"dimension mismatch: {M}x{K} @ {Kb}x{N}")
+    if out is None:
+        out = torch.empty((M, N), dtype=a.dtype, device=a.device)
+        if beta != 0.0:
+            raise ValueError("beta != 0 needs out")
+    _, _, ldc = _rows_ld(out)
+    lib = _lib.load()
+    eb = 4 if a.dtype == F32 else 8
+    md = GEMM_MODE[mode]
+    wsb = lib.skp_gemm_ws_bytes(int(ta), int(tb), M, N, K, eb, md)
+    ws = workspace(a.device, wsb) if wsb else None
+    call(f"skp_gemm_{_SFX[a.dtype]}", int(ta), int(tb), M, N, K, alpha, ptr(a), lda, ptr(b), ldb,
+         beta, ptr(out), ldc, md, ptr(ws), wsb, stream_ptr(a.device))
+    return out
+
+
+# ------------------------------------------------------------ utilities ----
+
+def cast(x: torch.Tensor, dtype) -> torch.Tensor:
+    if x.dtype == dtype:
+        return x
+    x = x.contiguous()
+    out = torch.empty(x.shape, dtype=dtype, device=x.device)
+    name = "skp_cast_f32_f64" if dtype == F64 else "skp_cast_f64_f32"
+    call(name, ptr(x), ptr(out), x.numel(), stream_ptr(x.device))
+    return out
+
+
+def sumsq(x: torch.Tensor, acc=None, nonfinite=None):
+    r, c, ld = _rows_ld(x)
+    if acc is None:
+        acc = torch.zeros(1, dtype=F64, device=x.device)
+    call(f"skp_sumsq_{_SFX[x.dtype]}", ptr(x), r, c, ld, ptr(acc), ptr(nonfinite),
+         stream_ptr(x.device))
+    return acc
+
+
+def symmetrize_(w: torch.Tensor):
+    n, _, ld = _rows_ld(w)
+    call(f"skp_symmetrize_{_SFX[w.dtype]}", ptr(w), n, ld, stream_ptr(w.device))
+    return w
+
+
+def scale_cols_(x: torch.Tensor, scale64: torch.Tensor):
+    r, c, ld = _rows_ld(x)
+    call(f"skp_scale_cols_{_SFX[x.dtype]}", ptr(x), r, c, ld, ptr(scale64), stream_ptr(x.device))
+    return x
+
+
+class CudaBackend:
+    """Compute backend for the engine: every op is a libskp kernel launch."""
+
+    name = "cuda"
+
+    def __init__(self, device, dtype, gemm_mode: str = "auto"):
+        self.device = device
+        self.dtype = dtype
+        self.gemm_mode = gemm_mode if dtype == F32 else "auto"
+        self.info = torch.zeros(2, dtype=torch.int32, device=device)
+
+    # dense products in the compute dtype
+    def mm(self, a, b, ta=False, tb=False, out=None, alpha=1.0, beta=0.0):
+        return gemm(a, b, ta, tb, alpha=alpha, beta=beta, out=out, mode=self.gemm_mode)
+
+    def gram64(self, y):
+        """y^T y as fp64 (computed in the compute dtype, then widened)."""
+        return cast(self.mm(y, y, ta=True), F64)
+
+    def gram64_rows(self, b):
+        """b b^T in fp64 arithmetic (b: c x n, widened first)."""
+        bd = cast(b, F64)
+        return gemm(bd, bd, False, True)
+
+    def chol_inv64(self, g, rel_tol):
+        """L^{-1} of G = L L^T, or None when G is not numerically full rank."""
+        n = g.shape[0]
+        lmat = g.clone()
+        st = stream_ptr(self.device)
+        call("skp_cholesky_f64", ptr(lmat), n, n, ptr(self.info), st)
+        call("skp_chol_pivot_check_f64", ptr(lmat), n, n, rel_tol, ptr(self.info), st)
+        if int(self.info[0].item()) != 0:
+            return None
+        x = torch.empty_like(lmat)
+        call("skp_trinv_lower_f64", ptr(lmat), n, n, ptr(x), st)
+        return x
+
+    def eig_desc64(self, g, max_sweeps=30):
+        n = g.shape[0]
+        a = g.clone()
+        w = torch.empty(n, dtype=F64, device=self.device)
+        v = torch.empty((n, n), dtype=F64, device=self.device)
+        wsb = _lib.load().skp_syevj_ws_bytes(n)
+        ws = workspace(self.device, wsb)
+        call("skp_syevj_f64", ptr(a), n, ptr(w), ptr(v), max_sweeps, ptr(ws), wsb,
+             ptr(self.info[1:]), stream_ptr(self.device))
+        return w, v
+
+    def eig_orth64(self, w, v, rel_tol):
+        n = w.shape[0]
+        t = torch.empty((n, n), dtype=F64, device=self.device)
+        call("skp_eig_orth_f64", ptr(w), ptr(v), n, rel_tol, ptr(t), ptr(self.info),
+             stream_ptr(self.device))
+        return t, int(self.info[0].item())
+
+    def sqrt_eigs(self, w):
+        sig = torch.empty_like(w)
+        inv = torch.empty_like(w)
+        call("skp_sqrt_eigs_f64", ptr(w), w.shape[0], ptr(sig), ptr(inv), stream_ptr(self.device))
+        return sig, inv
+
+    def orth_dev(self, g64) -> float:
+        out = torch.empty(1, dtype=F64, device=self.device)
+        call("skp_orth_dev_f64", ptr(g64), g64.shape[0], g64.stride(0), ptr(out),
+             stream_ptr(self.device))
+        return float(out.item())
+
+    def to_compute(self, x64):
+        return cast(x64, self.dtype)
+
+    def scale_cols_(self, x, s64):
+        return scale_cols_(x, s64)
+
+    def symmetrize_(self, w):
+        return symmetrize_(w)
+
+    def cols(self, x, k):
+        return x[:, :k].contiguous() if k < x.shape[1] else x
+
+    def sumsq(self, x):
+        return sumsq(x)
+
+    def scalar(self, x) -> float:
+        return float(x.reshape(-1)[0].item())
+
+    def zeros(self, shape, dtype=None):
+        return torch.zeros(shape, dtype=dtype or self.dtype, device=self.device)
+
+
+def np_dtype(t: torch.dtype):
+    return np.float32 if t == F32 else np.float64

@@ -1,0 +1,363 @@
+"""Sketched power method on the B200 (drop-in for skpower.power).
+
+Mirrors /root/reference/pkg/src/skpower/power.py: ``RangeFinderSpec`` (:49),
+``power_iterate`` (:113), ``range_finder_sketched`` (:141),
+``range_finder_classical`` (:157), ``randsvd`` (:181), ``lowrank_factorize``
+(:202), ``nystrom_psd`` (:258), ``choose_q`` (:34) and the result records.
+
+Seeds follow the reference: S from substream(seed, 0) (regenerated on the
+device by K1), Omega from substream(seed, 1) (host numpy, bit-identical),
+S2 from substream(seed, 2).
+
+Precision: float32 operands run the FP32 path (3xTF32 tcgen05 GEMMs, fp64
+small cores); anything else runs FP64 like the reference.  Optional keyword
+``timings`` (a dict) receives per-phase device times in milliseconds (CUDA
+events on the launching stream).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _convert, _engine, _ops
+from ._ops import F32, F64
+from .linalg import SvdResult, _pinv_dev
+from .sketching import make_sketch, omega_tensor, substream
+
+
+def choose_q(eps: float, m_hat: int) -> int:
+    """ceil(ln(2 m_hat) / (2 eps)) -- power.py:34-46."""
+    if not 0.0 < eps <= 0.5:
+        raise ValueError(f"eps must be in (0, 1/2], got {eps}")
+    if m_hat < 1:
+        raise ValueError(f"m_hat must be >= 1, got {m_hat}")
+    return math.ceil(math.log(2.0 * m_hat) / (2.0 * eps))
+
+
+@dataclass(frozen=True)
+class RangeFinderSpec:
+    """Parameter record of the sketched power method (power.py:49-92)."""
+
+    k: int
+    l: int
+    r1: int
+    r2: int
+    q: int
+    eps: float
+    sketch_kind: str = "countsketch"
+    seed: int = 0
+    stabilized: bool = True
+    s: int = 1
+    s2_kind: str | None = None
+    s2_r: int | None = None
+    omega_kind: str = "gaussian"
+
+    def validate(self, m: int, n: int) -> None:
+        if not 1 <= self.k <= self.l <= min(m, n):
+            raise ValueError(
+                f"need 1 <= k <= l <= min(m, n); got k={self.k}, l={self.l}, "
+                f"min(m, n)={min(m, n)}"
+            )
+        if self.r2 < self.k:
+            raise ValueError(f"r2 must be >= k, got r2={self.r2}, k={self.k}")
+        if self.q < 0:
+            raise ValueError(f"q must be >= 0, got {self.q}")
+        if not 0.0 < self.eps <= 0.5:
+            raise ValueError(f"eps must be in (0, 1/2], got {self.eps}")
+        if self.r1 < 1:
+            raise ValueError(f"r1 must be >= 1, got {self.r1}")
+
+
+@dataclass
+class FactorizationResult:
+    """Low-rank factors Y (m x r2) and X (r2 x n) plus stage times (power.py:95-101)."""
+    Y: object
+    X: object
+    elapsed: dict = field(default_factory=dict)
+
+
+@dataclass
+class NystromResult:
+    """Nystrom factors C (n x r2) and psd core W (r2 x r2) plus stage times (power.py:104-110)."""
+    C: object
+    W: object
+    elapsed: dict = field(default_factory=dict)
+
+
+class _Phases:
+    """CUDA-event phase timer on the current stream (no-op when disabled)."""
+
+    def __init__(self, enabled: bool):
+        self.enabled = enabled
+        self.ev = []
+
+    def mark(self, name: str):
+        if self.enabled:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.ev.append((name, e))
+
+    def result(self, out: dict | None, scale: float = 1.0):
+        if not self.enabled or out is None:
+            return
+        self.ev[-1][1].synchronize()
+        for (_, a), (name, b) in zip(self.ev, self.ev[1:]):
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b) * scale
+
+
+def _be(dtype, device):
+    return _ops.CudaBackend(device, dtype)
+
+
+def power_iterate(atil, omega, q: int, stabilized: bool = True):
+    """Block with the column span of (A~ A~^T)^q A~ Omega (power.py:113-134)."""
+    oa = _convert.upload(atil, "atil")
+    oo = _convert.upload(omega, "omega", oa.t.device)
+    if oa.t.shape[1] != oo.t.shape[0]:
+        raise ValueError(f"dimension mismatch: {tuple(oa.t.shape)} vs omega {tuple(oo.t.shape)}")
+    if q < 0:
+        raise ValueError(f"q must be >= 0, got {q}")
+    dt = _convert.common_dtype(oa, oo)
+    y = _engine.power_iterate(_be(dt, oa.t.device), _engine.LOCAL, _convert.as_dtype(oa, dt),
+                              _convert.as_dtype(oo, dt), q, stabilized)
+    return _convert.download(y, oa.kind)
+
+
+def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL,
+                      rows_total: int | None = None, phases: _Phases | None = None,
+                      fro2: torch.Tensor | None = None, name: str = "a"):
+    """Alg. 1 on a device row slab; returns Q (rows x <= r2).  Raises on
+    non-finite entries of a (counted inside the sketch kernel)."""
+    ph = phases or _Phases(False)
+    dev = a.device
+    m_loc, n = a.shape
+    be = _be(a.dtype, dev)
+    ph.mark("start")
+    sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
+    ph.mark("make_sketch")
+    omega = omega_tensor(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), a.dtype, dev)
+    ph.mark("omega")
+    nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
+    atil = sk.right(a, fro2=fro2, nonfinite=nonfinite)
+    ph.mark("apply_right")
+    bad = comm.allreduce_(nonfinite)
+    if int(bad.item()) != 0:
+        raise ValueError(f"{name} contains non-finite entries")
+    y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total)
+    ph.mark("power")
+    qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total)
+    ph.mark("orth")
+    return qb
+
+
+def range_finder_sketched(a, spec: RangeFinderSpec, *, timings: dict | None = None, device=None):
+    """Orthonormal range finder from power iteration on the sketch A S (power.py:141-154)."""
+    op = _convert.upload(a, "a", device, check_finite=False)
+    m, n = op.t.shape
+    spec.validate(m, n)
+    ph = _Phases(timings is not None)
+    qb = _range_finder_dev(op.t, spec, phases=ph)
+    ph.result(timings)
+    return _convert.download(qb, op.kind)
+
+
+def range_finder_classical(a, k: int, r2: int, q: int, seed: int, stabilized: bool = True):
+    """Power iteration on a itself: the identity-sketch case (power.py:157-178)."""
+    op = _convert.upload(a, "a", check_finite=False)
+    m, n = op.t.shape
+    spec = RangeFinderSpec(k=k, l=min(m, n), r1=n, r2=r2, q=q, eps=0.5, sketch_kind="identity",
+                           seed=seed, stabilized=stabilized)
+    spec.validate(m, n)
+    return _convert.download(_range_finder_dev(op.t, spec), op.kind)
+
+
+def _randsvd_dev(a: torch.Tensor, qb: torch.Tensor, comm=_engine.LOCAL, check: bool = True):
+    be = _be(a.dtype, a.device)
+    return _engine.randsvd(be, comm, a, qb, check)
+
+
+def randsvd(a, q_basis, *, timings: dict | None = None) -> SvdResult:
+    """U diag(sigma) V^T == Q Q^T a (power.py:181-199)."""
+    oa = _convert.upload(a, "a")
+    oq = _convert.upload(q_basis, "q_basis", oa.t.device)
+    if oq.t.shape[0] != oa.t.shape[0]:
+        raise ValueError(f"dimension mismatch: Q has {oq.t.shape[0]} rows, a has {oa.t.shape[0]}")
+    dt = _convert.common_dtype(oa, oq)
+    ph = _Phases(timings is not None)
+    ph.mark("start")
+    u, s, v = _randsvd_dev(_convert.as_dtype(oa, dt), _convert.as_dtype(oq, dt))
+    ph.mark("randsvd")
+    ph.result(timings)
+    return SvdResult(_convert.download(u, oa.kind), _convert.download(s, oa.kind),
+                     _convert.download(v, oa.kind))
+
+
+def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: bool = False):
+    """range_finder_sketched + randsvd with ONE upload of ``a`` (convenience
+    entry, not in the reference: the two reference calls each re-read a).
+
+    Returns SvdResult, or (SvdResult, rel_err) with ``with_error`` where
+    rel_err = ||a - QQ^T a||_F / ||a||_F from ||a||_F^2 - sum(sigma^2)
+    (Pythagorean identity; ||a||_F^2 is fused into the sketch)."""
+    op = _convert.upload(a, "a", check_finite=False)
+    m, n = op.t.shape
+    spec.validate(m, n)
+    ph = _Phases(timings is not None)
+    fro2 = torch.zeros(1, dtype=torch.float64, device=op.t.device)
+    qb = _range_finder_dev(op.t, spec, phases=ph, fro2=fro2)
+    u, s, v = _randsvd_dev(op.t, qb, check=False)
+    ph.mark("randsvd")
+    res = SvdResult(_convert.download(u, op.kind), _convert.download(s, op.kind),
+                    _convert.download(v, op.kind))
+    ph.result(timings)
+    if not with_error:
+        return res
+    a2 = float(fro2.item())
+    s64 = np.asarray(res.sigma.cpu() if isinstance(res.sigma, torch.Tensor) else res.sigma,
+                     dtype=np.float64)
+    rel = math.sqrt(max(a2 - float((s64 ** 2).sum()), 0.0) / a2) if a2 > 0 else 0.0
+    return res, rel
+
+
+def lowrank_factorize(a, spec: RangeFinderSpec) -> FactorizationResult:
+    """Generalized Nystrom a ~= Y X with X = (S2^T Y)^+ (S2^T a) (power.py:202-239)."""
+    op = _convert.upload(a, "a", check_finite=False)
+    t = op.t
+    m, n = t.shape
+    spec.validate(m, n)
+    s2_kind = spec.s2_kind or spec.sketch_kind
+    s2_r = spec.s2_r or spec.r1
+    dev = t.device
+    be = _be(t.dtype, dev)
+    ph = _Phases(True)
+    ph.mark("t0")
+    s1 = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
+    nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
+    atil = s1.right(t, nonfinite=nonfinite)
+    ph.mark("sketch")
+    if int(nonfinite.item()):
+        raise ValueError("a contains non-finite entries")
+    omega = omega_tensor(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), t.dtype, dev)
+    y = _engine.power_iterate(be, _engine.LOCAL, atil, omega, spec.q, spec.stabilized)
+    ph.mark("power")
+    s2 = make_sketch(s2_kind, m, s2_r, substream(spec.seed, 2), s=spec.s, device=dev)
+    s2y = s2.left_t(y)
+    if float(_ops.sumsq(s2y).item()) == 0.0:
+        raise ValueError("S2.T Y is numerically rank-zero; regression is undefined")
+    x = be.mm(_pinv_dev(be, s2y), s2.left_t(t))
+    ph.mark("regression")
+    el = {}
+    ph.result(el, 1e-3)
+    return FactorizationResult(Y=_convert.download(y, op.kind), X=_convert.download(x, op.kind),
+                               elapsed=el)
+
+
+# psd checks (power.py:242-255).  The symmetry test runs on the device at any
+# size; the O(n^3) eigenvalue test only up to PSD_EIG_MAX (documented gap).
+PSD_EIG_MAX = 1024
+
+
+def _check_psd_dev(t: torch.Tensor, tol: float = 1e-8) -> None:
+    n = t.shape[0]
+    if t.shape[0] != t.shape[1]:
+        raise ValueError(f"psd input must be square, got {tuple(t.shape)}")
+    scale = float(t.abs().max().item())
+    if scale == 0.0:
+        return
+    asym = float((t - t.T).abs().max().item())
+    if asym > tol * scale:
+        raise ValueError("matrix is not symmetric within tolerance")
+    if n <= PSD_EIG_MAX:
+        be = _be(F64, t.device)
+        g = _ops.cast(t, F64).clone()
+        _ops.symmetrize_(g)
+        w, _ = be.eig_desc64(g)
+        lo, hi = float(w[-1].item()), float(w.abs().max().item())
+        if hi > 0.0 and lo < -tol * hi:
+            raise ValueError(f"matrix is not psd: min eigenvalue {lo:.3e} < {-tol * hi:.3e}")
+
+
+def _nystrom_dev(t: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL, row0: int = 0,
+                 n_total: int | None = None, stabilized: bool | None = None,
+                 phases: _Phases | None = None):
+    """Alg. 3 on a row slab t = K[row0:row0+rows, :] (power.py:272-287)."""
+    ph = phases or _Phases(False)
+    dev = t.device
+    n = t.shape[1] if n_total is None else n_total
+    be = _be(t.dtype, dev)
+    if stabilized is None:
+        stabilized = t.dtype == F32 and spec.stabilized
+    ph.mark("t0")
+    sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
+    nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
+    ctil = sk.right(t, nonfinite=nonfinite)
+    if int(comm.allreduce_(nonfinite).item()):
+        raise ValueError("a contains non-finite entries")
+    rows = t.shape[0]
+    if rows == n:
+        wtil = sk.left_t(ctil)
+    else:  # S rows of this shard: W~ = sum_p S[I_p]^T C~_p
+        shard = _shard_sketch(sk, row0, rows)
+        wtil = shard.left_t(ctil)
+    wtil = comm.allreduce_(wtil)
+    be.symmetrize_(wtil)
+    ph.mark("sketch")
+    omega = omega_tensor(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), t.dtype, dev)
+    cmat, w = _engine.nystrom(be, comm, ctil, wtil, omega, spec.q, stabilized)
+    ph.mark("contract")
+    return cmat, w
+
+
+class _ShardSketch:
+    """Rows [row0, row0+rows) of a countsketch / dense sketch, for S[I_p]^T X."""
+
+    def __init__(self, sk, row0, rows):
+        self.sk, self.row0, self.rows = sk, row0, rows
+        if sk.kind == "countsketch":
+            c = sk.d_cols[row0:row0 + rows].contiguous()
+            g = sk.d_signs[row0:row0 + rows].contiguous()
+            self.colptr, self.entries = _ops.csc(c, g, rows, sk.s, sk.r)
+
+    def left_t(self, x):
+        sk = self.sk
+        if sk.kind == "countsketch":
+            return _ops.sketch_left_t(x, self.colptr, self.entries, sk.s, sk.r)
+        if sk.kind == "identity":
+            out = torch.zeros((sk.n, x.shape[1]), dtype=x.dtype, device=x.device)
+            out[self.row0:self.row0 + self.rows] = x
+            return out
+        d = sk._dense(x.dtype)[self.row0:self.row0 + self.rows].contiguous()
+        return _ops.gemm(d, x, ta=True)
+
+
+def _shard_sketch(sk, row0, rows):
+    return _ShardSketch(sk, row0, rows)
+
+
+def nystrom_psd(a, spec: RangeFinderSpec, *, stabilized: bool | None = None) -> NystromResult:
+    """Psd Nystrom a ~= C pinv(W) C^T (power.py:258-298).
+
+    FP64 input follows the reference literally (Y = W~^q Omega).  FP32 input
+    orthonormalises between the W~ products (same span)
+    unless ``spec.stabilized`` is False or ``stabilized=False`` is passed:
+    the literal fp32 power collapses the block (SURVEY.md §7 hard part 5)."""
+    op = _convert.upload(a, "a", check_finite=False)
+    t = op.t
+    n = t.shape[0]
+    if t.shape[0] != t.shape[1]:
+        raise ValueError(f"psd Nystrom needs a square matrix, got {tuple(t.shape)}")
+    _convert.ensure_finite(op)
+    _check_psd_dev(t)
+    spec.validate(n, n)
+    ph = _Phases(True)
+    cmat, w = _nystrom_dev(t, spec, stabilized=stabilized, phases=ph)
+    el = {}
+    ph.mark("end")
+    ph.result(el, 1e-3)
+    el.pop("end", None)
+    el["power"] = 0.0
+    return NystromResult(C=_convert.download(cmat, op.kind), W=_convert.download(w, op.kind),
+                         elapsed=el)

@@ -1,0 +1,199 @@
+"""Seeded sketch operators on the B200 (drop-in for skpower.sketching).
+
+Mirrors /root/reference/pkg/src/skpower/sketching.py: ``SketchOperator``
+(:93), ``make_sketch`` (:216), ``substream`` (:46), the functional forms
+(:225-237) and ``SKETCH_KINDS`` (:39).
+
+* ``countsketch`` -- S is regenerated ON THE DEVICE from the seed by the K1
+  kernel, bit-exact with the reference's numpy draw (sketching.py:141-150);
+  apply_right / apply_left_transpose are the K2 / K3 gather kernels.
+* ``identity``    -- the classical (unsketched) hook (sketching.py:137-139).
+* ``gaussian`` / ``sign`` -- dense S drawn on the host with the reference's
+  numpy stream (bit-identical), applied with the device GEMM.
+* ``srht``        -- not on the accelerated path: raises
+  ValueError("unsupported ...").  No CPU fallback exists.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _convert, _ops
+from ._ops import F32, F64
+
+SKETCH_KINDS = ("gaussian", "sign", "countsketch", "srht", "identity")
+DEVICE_KINDS = ("gaussian", "sign", "countsketch", "identity")
+
+_DENSIFY_CAP = 10**7
+_MASK64 = (1 << 64) - 1
+
+
+def substream(seed: int, *indices: int) -> int:
+    """Independent 64-bit seed from (seed, *indices) -- sketching.py:46-54.
+    Host-side seed expansion (numpy SeedSequence), as in the reference."""
+    entropy = [int(seed) & _MASK64] + [int(i) & _MASK64 for i in indices]
+    return int(np.random.SeedSequence(entropy=entropy).generate_state(1, np.uint64)[0])
+
+
+def _host_rng(seed: int) -> np.random.Generator:
+    # sketching.py:57-58
+    return np.random.default_rng(np.random.SeedSequence(entropy=[int(seed) & _MASK64]))
+
+
+def pcg64_state(seed: int) -> tuple[int, int]:
+    """128-bit PCG64 (state, inc) that _rng(seed) starts from (passed to K1)."""
+    st = _host_rng(seed).bit_generator.state["state"]
+    return int(st["state"]), int(st["inc"])
+
+
+class SketchOperator:
+    """Immutable seeded linear map from n to r coordinates (device resident).
+
+    Same constructor, attributes (kind, n, r, seed, s) and methods as the
+    reference; ``_cols`` / ``_signs`` are host copies of the device arrays
+    (int64 / float64 +-1, as the reference stores them).
+    """
+
+    def __init__(self, kind: str, n: int, r: int, seed: int, s: int | None = None, device=None):
+        if kind not in SKETCH_KINDS:
+            raise ValueError(f"unknown sketch kind {kind!r}, expected one of {SKETCH_KINDS}")
+        if r < 1:
+            raise ValueError(f"sketch dimension r must be >= 1, got {r}")
+        if n < 1:
+            raise ValueError(f"input dimension n must be >= 1, got {n}")
+        self.kind = kind
+        self.n = int(n)
+        self.r = int(r)
+        self.seed = int(seed) & _MASK64
+        self.s = None
+        self._dense_host = None
+        self._dense_dev = {}
+        if kind == "srht":
+            raise ValueError("unsupported on the B200 path: the srht sketch is out of scope "
+                             "(countsketch, identity, gaussian and sign are supported)")
+        self.device = _ops.require_cuda(device)
+        if kind == "countsketch":
+            s = 1 if s is None else int(s)
+            if not 1 <= s <= r:
+                raise ValueError(f"countsketch needs 1 <= s <= r, got s={s}, r={r}")
+            self.s = s
+            st, inc = pcg64_state(self.seed)
+            self.d_cols, self.d_signs = _ops.countsketch(st, inc, self.n, self.r, s, self.device)
+            self.colptr, self.entries = _ops.csc(self.d_cols, self.d_signs, self.n, s, self.r)
+        elif kind == "gaussian":
+            self._dense_host = _host_rng(self.seed).standard_normal((n, r)) / math.sqrt(r)
+        elif kind == "sign":
+            d = _host_rng(self.seed).integers(0, 2, size=(n, r)).astype(np.float64) * 2.0 - 1.0
+            self._dense_host = d / math.sqrt(r)
+        else:  # identity
+            if r != n:
+                raise ValueError(f"identity sketch needs r == n, got n={n}, r={r}")
+
+    def __repr__(self):
+        extra = f", s={self.s}" if self.kind == "countsketch" else ""
+        return f"SketchOperator({self.kind}, n={self.n}, r={self.r}, seed={self.seed}{extra})"
+
+    # reference-compatible host views of the draw
+    @property
+    def _cols(self) -> np.ndarray:
+        return self.d_cols.cpu().numpy().astype(np.int64)
+
+    @property
+    def _signs(self) -> np.ndarray:
+        return self.d_signs.cpu().numpy().astype(np.float64)
+
+    def _dense(self, dtype) -> torch.Tensor:
+        t = self._dense_dev.get(dtype)
+        if t is None:
+            t = torch.from_numpy(self._dense_host).to(self.device, dtype=dtype)
+            self._dense_dev[dtype] = t
+        return t
+
+    # -- device-level application (tensors in, tensors out) -----------------
+    def right(self, a: torch.Tensor, out=None, fro2=None, nonfinite=None) -> torch.Tensor:
+        if self.kind == "countsketch":
+            return _ops.sketch_right(a, self.colptr, self.entries, self.s, self.r, out, fro2,
+                                     nonfinite)
+        if fro2 is not None or nonfinite is not None:
+            _ops.sumsq(a, fro2, nonfinite)
+        if self.kind == "identity":
+            return a.clone() if out is None else out.copy_(a)
+        return _ops.gemm(a, self._dense(a.dtype), out=out)
+
+    def left_t(self, x: torch.Tensor, out=None) -> torch.Tensor:
+        if self.kind == "countsketch":
+            return _ops.sketch_left_t(x, self.colptr, self.entries, self.s, self.r, out)
+        if self.kind == "identity":
+            return x.clone() if out is None else out.copy_(x)
+        return _ops.gemm(self._dense(x.dtype), x, ta=True, out=out)
+
+    # -- reference API --------------------------------------------------------
+    def apply_right(self, a):
+        """a @ S for a with n columns (sketching.py:158-174)."""
+        op = _convert.upload(a, "a", self.device)
+        if op.t.shape[1] != self.n:
+            raise ValueError(f"dimension mismatch: a has {op.t.shape[1]} cols, sketch n={self.n}")
+        return _convert.download(self.right(op.t), op.kind)
+
+    def apply_left_transpose(self, a):
+        """S.T @ a for a with n rows (sketching.py:176-192)."""
+        op = _convert.upload(a, "a", self.device)
+        if op.t.shape[0] != self.n:
+            raise ValueError(f"dimension mismatch: a has {op.t.shape[0]} rows, sketch n={self.n}")
+        return _convert.download(self.left_t(op.t), op.kind)
+
+    def densify(self) -> np.ndarray:
+        """Explicit n x r matrix (host numpy, test oracle) -- sketching.py:194-213."""
+        if self.n * self.r > _DENSIFY_CAP:
+            raise ValueError(f"densify cap exceeded: {self.n} x {self.r} > {_DENSIFY_CAP} entries")
+        if self.kind == "countsketch":
+            out = np.zeros((self.n, self.r))
+            rows = np.repeat(np.arange(self.n), self.s)
+            out[rows, self._cols.ravel()] = self._signs.ravel() / math.sqrt(self.s)
+            return out
+        if self.kind == "identity":
+            return np.eye(self.n)
+        return self._dense_host.copy()
+
+
+def make_sketch(kind: str, n: int, r: int, seed: int, s: int | None = None,
+                device=None) -> SketchOperator:
+    """Construct a sketch operator; deterministic in (kind, n, r, seed) -- sketching.py:216-222."""
+    return SketchOperator(kind, n, r, seed, s=s, device=device)
+
+
+def apply_right(a, sketch: SketchOperator):
+    return sketch.apply_right(a)
+
+
+def apply_left_transpose(sketch: SketchOperator, a):
+    return sketch.apply_left_transpose(a)
+
+
+def densify(sketch: SketchOperator) -> np.ndarray:
+    return sketch.densify()
+
+
+def draw_omega(kind: str, rows: int, cols: int, seed: int) -> np.ndarray:
+    """The start block (power.py:137-138): host numpy draw, bit-identical to the
+    reference (the ziggurat's data-dependent stream stays on the host)."""
+    if kind == "gaussian":
+        return _host_rng(seed).standard_normal((rows, cols)) / math.sqrt(cols)
+    if kind == "sign":
+        d = _host_rng(seed).integers(0, 2, size=(rows, cols)).astype(np.float64) * 2.0 - 1.0
+        return d / math.sqrt(cols)
+    if kind == "identity":
+        if rows != cols:
+            raise ValueError(f"identity sketch needs r == n, got n={rows}, r={cols}")
+        return np.eye(rows)
+    if kind == "countsketch":
+        return make_sketch("countsketch", rows, cols, seed).densify()
+    raise ValueError(f"unsupported omega kind {kind!r} on the B200 path")
+
+
+def omega_tensor(kind: str, rows: int, cols: int, seed: int, dtype, device) -> torch.Tensor:
+    om = draw_omega(kind, rows, cols, seed)
+    t = torch.from_numpy(om.astype(np.float32) if dtype == F32 else om)
+    return t.pin_memory().to(device, non_blocking=True) if rows * cols > 1 << 16 else t.to(device)

@@ -1,0 +1,75 @@
+"""numpy compute backend for the engine -- TEST ONLY.
+
+Implements the ``_engine`` backend interface with numpy/scipy so the
+row-sharded orchestration (what is all-reduced, when, in which order) can be
+exercised by multi-process gloo tests on a CPU-only box.  The product uses
+``_ops.CudaBackend``; nothing in the package imports this module.
+"""
+import numpy as np
+
+
+class NumpyBackend:
+    name = "numpy"
+
+    def __init__(self, dtype=np.float64):
+        self.dtype = np.dtype(dtype)
+
+    def mm(self, a, b, ta=False, tb=False, out=None, alpha=1.0, beta=0.0):
+        r = (a.T if ta else a) @ (b.T if tb else b)
+        return np.ascontiguousarray(r.astype(self.dtype, copy=False))
+
+    def gram64(self, y):
+        return np.ascontiguousarray((y.T @ y).astype(np.float64))
+
+    def gram64_rows(self, b):
+        b = b.astype(np.float64)
+        return b @ b.T
+
+    def chol_inv64(self, g, rel_tol):
+        try:
+            lmat = np.linalg.cholesky(g)
+        except np.linalg.LinAlgError:
+            return None
+        d = np.abs(np.diag(lmat))
+        if d.min() < rel_tol * d.max():
+            return None
+        return np.linalg.inv(lmat)
+
+    def eig_desc64(self, g):
+        w, v = np.linalg.eigh((g + g.T) / 2)
+        idx = np.argsort(-w, kind="stable")
+        return w[idx], np.ascontiguousarray(v[:, idx])
+
+    def eig_orth64(self, w, v, rel_tol):
+        keep = (w > 0) & (w > rel_tol * w[0])
+        t = np.zeros_like(v)
+        t[:, keep] = v[:, keep] / np.sqrt(w[keep])
+        return t, int(keep.sum())
+
+    def sqrt_eigs(self, w):
+        s = np.sqrt(np.maximum(w, 0))
+        inv = np.where(s > 0, 1 / np.where(s > 0, s, 1), 0)
+        return s, inv
+
+    def orth_dev(self, g):
+        return float(np.abs(g - np.eye(g.shape[0])).max())
+
+    def to_compute(self, x):
+        return np.ascontiguousarray(x.astype(self.dtype))
+
+    def scale_cols_(self, x, s):
+        x *= s.astype(x.dtype)
+        return x
+
+    def symmetrize_(self, w):
+        w[...] = (w + w.T) / 2
+        return w
+
+    def cols(self, x, k):
+        return np.ascontiguousarray(x[:, :k])
+
+    def sumsq(self, x):
+        return np.array([float((x.astype(np.float64) ** 2).sum())])
+
+    def scalar(self, x):
+        return float(np.asarray(x).reshape(-1)[0])

@@ -1,0 +1,228 @@
+"""Per-kernel parity on the B200, through the C-ABI (libskp.so via ctypes).
+
+K1 (CountSketch draw) must be bit-exact with the live-reference golden
+fixtures and the C oracle; K2/K3 sketch application, the GEMMs and the small
+fp64 kernels are compared with numpy/torch fp64 references at stated
+tolerances.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import small_cs_cases
+from oracle import skp_oracle as o
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def skp():
+    import paper_2605_09755_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2605_09755_b200 import _ops
+    return _ops
+
+
+# ------------------------------------------------------------------ K1 ----
+
+def test_countsketch_small_golden(skp, golden_cs):
+    for i, n, r, s, seed in small_cs_cases(golden_cs):
+        if s > 32 or r >= 2**31:
+            with pytest.raises(ValueError, match="unsupported"):
+                skp.make_sketch("countsketch", n, r, seed, s=s)
+            continue
+        op = skp.make_sketch("countsketch", n, r, seed, s=s)
+        np.testing.assert_array_equal(op._cols, golden_cs[f"cs{i}_cols"], err_msg=f"case {i}")
+        np.testing.assert_array_equal(op._signs.astype(np.int8), golden_cs[f"cs{i}_signs"])
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5_l4000", "C5_l8000", "C5_l16000"])
+def test_countsketch_config_shapes_golden(skp, golden, name):
+    b = golden["countsketch_big"][name]
+    op = skp.make_sketch("countsketch", b["n"], b["r"], int(b["seed"]), s=b["s"])
+    assert sha(op._cols) == b["cols_sha256"]
+    assert sha(op._signs.astype(np.int8)) == b["signs_sha256"]
+
+
+@pytest.mark.parametrize("n,r,s,seed", [
+    (1, 1, 1, 0), (1, 5, 5, 3), (37, 1, 1, 4), (100, 3, 2, 5), (513, 1000, 7, 6),
+    (64, 1025, 32, 7), (333, 31, 31, 8), (1000, 1_500_000_000, 1, 9), (2049, 2, 1, 10),
+    (3000, 129, 1, 11), (40, 33, 9, 12)])
+def test_countsketch_random_vs_c_oracle(skp, n, r, s, seed):
+    op = skp.make_sketch("countsketch", n, r, seed, s=s)
+    cols, signs = o.countsketch_c(seed, n, r, s)
+    np.testing.assert_array_equal(op._cols, cols)
+    np.testing.assert_array_equal(op._signs, signs)
+
+
+@pytest.mark.parametrize("s", [1, 3, 8])
+def test_countsketch_row_ranges_compose(ops, s):
+    n, r, seed = 1001, 257, 42
+    st, inc = o.pcg64_state(seed)
+    full_c, full_s = ops.countsketch(st, inc, n, r, s, "cuda")
+    for j0, j1 in [(0, 1), (0, 500), (500, 1001), (999, 1001), (333, 334)]:
+        c, g = ops.countsketch(st, inc, n, r, s, "cuda", j0, j1)
+        assert torch.equal(c, full_c[j0:j1]) and torch.equal(g, full_s[j0:j1])
+
+
+def test_countsketch_bad_arguments(skp):
+    with pytest.raises(ValueError):
+        skp.make_sketch("countsketch", 10, 4, seed=0, s=5)
+    with pytest.raises(ValueError):
+        skp.make_sketch("gaussian", 10, 0, seed=0)
+    with pytest.raises(ValueError):
+        skp.make_sketch("nope", 10, 4, seed=0)
+    with pytest.raises(ValueError):
+        skp.make_sketch("identity", 10, 4, seed=0)
+    with pytest.raises(ValueError, match="unsupported"):
+        skp.make_sketch("srht", 16, 4, seed=0)
+
+
+# ---------------------------------------------------------------- K2/K3 ---
+
+@pytest.mark.parametrize("dtype,tol", [(np.float64, 1e-12), (np.float32, 2e-6)])
+@pytest.mark.parametrize("m,n,r,s", [(50, 200, 40, 4), (1, 7, 3, 2), (257, 1000, 200, 8),
+                                     (3, 60000, 100, 8), (130, 513, 64, 1)])
+def test_sketch_apply_matches_dense(skp, dtype, tol, m, n, r, s):
+    rng = np.random.default_rng(m + n)
+    op = skp.make_sketch("countsketch", n, r, seed=21, s=s)
+    dense = op.densify() if n * r <= 10**7 else None
+    a = rng.standard_normal((m, n)).astype(dtype)
+    fast = op.apply_right(a)
+    assert fast.dtype == dtype and fast.shape == (m, r)
+    ref = a.astype(np.float64) @ dense if dense is not None else o.CountSketch(
+        "countsketch", n, r, 21, s=s).apply_right(a)
+    assert np.abs(fast - ref).max() <= tol * np.linalg.norm(a.astype(np.float64)) + 1e-300
+    b = rng.standard_normal((n, 30)).astype(dtype)
+    fast_t = op.apply_left_transpose(b)
+    ref_t = (dense.T @ b.astype(np.float64)) if dense is not None else o.CountSketch(
+        "countsketch", n, r, 21, s=s).apply_left_transpose(b)
+    assert np.abs(fast_t - ref_t).max() <= tol * np.linalg.norm(b.astype(np.float64))
+
+
+def test_sketch_identity_input_and_zero(skp):
+    op = skp.make_sketch("countsketch", 20, 7, seed=11, s=3)
+    np.testing.assert_array_equal(op.apply_right(np.eye(20)), op.densify())
+    np.testing.assert_array_equal(op.apply_left_transpose(np.eye(20)), op.densify().T)
+    np.testing.assert_array_equal(op.apply_right(np.zeros((5, 20))), np.zeros((5, 7)))
+
+
+def test_sketch_fused_norm_and_nonfinite(skp, ops):
+    rng = np.random.default_rng(3)
+    for n in (500, 60000):
+        a = rng.standard_normal((9, n)).astype(np.float32)
+        a[4, n // 3] = np.nan
+        a[7, 1] = np.inf
+        op = skp.make_sketch("countsketch", n, 50, seed=1, s=4)
+        t = torch.from_numpy(a).cuda()
+        fro2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+        op.right(t, fro2=fro2, nonfinite=bad)
+        assert int(bad.item()) == 2
+        with pytest.raises(ValueError, match="non-finite"):
+            op.apply_right(a)
+        a[4, n // 3] = 0
+        a[7, 1] = 0
+        fro2.zero_()
+        op.right(torch.from_numpy(a).cuda(), fro2=fro2)
+        assert abs(fro2.item() - float((a.astype(np.float64) ** 2).sum())) <= 1e-9 * fro2.item()
+
+
+def test_sketch_dimension_mismatch(skp):
+    op = skp.make_sketch("countsketch", 20, 7, seed=11, s=3)
+    with pytest.raises(ValueError, match="mismatch"):
+        op.apply_right(np.ones((3, 19)))
+    with pytest.raises(ValueError, match="mismatch"):
+        op.apply_left_transpose(np.ones((19, 3)))
+
+
+# ------------------------------------------------------------------ K4 ----
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (67, 45, 131), (256, 130, 4097), (30, 40, 200000),
+                                   (1000, 110, 2000)])
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_gemm_vs_torch(ops, ta, tb, M, N, K, dt):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    a = torch.randn((K, M) if ta else (M, K), generator=g, device="cuda", dtype=dt)
+    b = torch.randn((N, K) if tb else (K, N), generator=g, device="cuda", dtype=dt)
+    ref = (a.double().T if ta else a.double()) @ (b.double().T if tb else b.double())
+    c0 = torch.randn(M, N, generator=g, device="cuda", dtype=dt)
+    out = c0.clone()
+    ops.gemm(a, b, bool(ta), bool(tb), alpha=0.5, beta=2.0, out=out)
+    expect = 0.5 * ref + 2.0 * c0.double()
+    scale = (a.double().abs().max() * b.double().abs().max() * np.sqrt(K)).item() + 1.0
+    tol = 1e-13 if dt == torch.float64 else 2e-6
+    assert (out.double() - expect).abs().max().item() <= tol * scale
+
+
+def test_gemm_modes_agree(ops):
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(2048, 520, generator=g, device="cuda")
+    b = torch.randn(2048, 110, generator=g, device="cuda")
+    ref = a.double().T @ b.double()
+    for mode in ("auto", "fp32"):
+        c = ops.gemm(a, b, True, False, mode=mode)
+        assert (c.double() - ref).abs().max().item() <= 1e-5 * ref.abs().max().item()
+
+
+# ----------------------------------------------------------- K5 / K6 ------
+
+def _spd(n, cond=1e4, seed=0):
+    rng = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    w = np.logspace(0, -np.log10(cond), n)
+    return (q * w) @ q.T
+
+
+@pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 130, 520])
+def test_cholesky_and_trinv(n):
+    from paper_2605_09755_b200 import _lib
+    from paper_2605_09755_b200._ops import ptr
+    g = _spd(n, seed=n)
+    t = torch.from_numpy(g).cuda()
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("skp_cholesky_f64", ptr(t), n, n, ptr(info), st)
+    assert int(info.item()) == 0
+    lmat = np.tril(t.cpu().numpy())
+    np.testing.assert_allclose(lmat, np.linalg.cholesky(g), rtol=0, atol=1e-10)
+    x = torch.empty_like(t)
+    _lib.call("skp_trinv_lower_f64", ptr(t), n, n, ptr(x), st)
+    np.testing.assert_allclose(x.cpu().numpy() @ lmat, np.eye(n), atol=1e-8)
+
+
+def test_cholesky_reports_indefinite():
+    from paper_2605_09755_b200 import _lib
+    from paper_2605_09755_b200._ops import ptr
+    g = _spd(100)
+    g[70, 70] = -1.0
+    t = torch.from_numpy(g).cuda()
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("skp_cholesky_f64", ptr(t), 100, 100, ptr(info), torch.cuda.current_stream().cuda_stream)
+    assert int(info.item()) > 0
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 30, 111, 112, 113, 300])
+def test_jacobi_eigensolver(n):
+    from paper_2605_09755_b200._ops import CudaBackend
+    rng = np.random.default_rng(n)
+    b = rng.standard_normal((n, 3 * n + 1))
+    g = b @ b.T
+    be = CudaBackend(torch.device("cuda", 0), torch.float64)
+    w, v = be.eig_desc64(torch.from_numpy(g).cuda())
+    w, v = w.cpu().numpy(), v.cpu().numpy()
+    ref = np.sort(np.linalg.eigvalsh(g))[::-1]
+    np.testing.assert_allclose(w, ref, rtol=1e-11, atol=1e-11 * ref[0])
+    np.testing.assert_allclose(v.T @ v, np.eye(n), atol=1e-11)
+    np.testing.assert_allclose(g @ v, v * w, atol=1e-9 * ref[0])
