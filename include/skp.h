@@ -69,19 +69,22 @@ int skp_countsketch_csc(const int32_t* cols, const int8_t* signs, int64_t n, int
                         int64_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- K2 ----
- * out (m x r) = A (m x n) . S / ... i.e. SketchOperator.apply_right for a
+ * out (m x r) = A (m x n) . S, i.e. SketchOperator.apply_right for a
  * countsketch (reference sketching.py:158-164: `a @ self._sparse`).  Fused:
  * fro2 += ||A||_F^2 (double) and nonfinite += #non-finite entries of A (the
  * as_matrix finiteness contract, linalg.py:30-39).  fro2 / nonfinite may be
- * NULL.                                                                     */
+ * NULL.  With ws (skp_sketch_right_ws_bytes) and 16-byte aligned rows the
+ * rows-in-lanes kernel runs (32 rows per warp, chunked CSC in smem); without
+ * it a slab kernel gathers per output column.                              */
+int64_t skp_sketch_right_ws_bytes(int64_t n, int32_t s, int64_t r, int32_t elem_bytes);
 int skp_sketch_right_f32(const float* A, int64_t lda, int64_t m, int64_t n,
                          const int32_t* colptr, const int32_t* entries, int32_t s, int64_t r,
-                         float* out, int64_t ldo, double* fro2, int64_t* nonfinite,
-                         void* stream);
+                         float* out, int64_t ldo, double* fro2, int64_t* nonfinite, void* ws,
+                         int64_t ws_bytes, void* stream);
 int skp_sketch_right_f64(const double* A, int64_t lda, int64_t m, int64_t n,
                          const int32_t* colptr, const int32_t* entries, int32_t s, int64_t r,
-                         double* out, int64_t ldo, double* fro2, int64_t* nonfinite,
-                         void* stream);
+                         double* out, int64_t ldo, double* fro2, int64_t* nonfinite, void* ws,
+                         int64_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- K3 ----
  * out (r x c) = S^T . X (X n x c); SketchOperator.apply_left_transpose
@@ -145,6 +148,11 @@ int skp_syevj_f64(double* A, int64_t n, double* W, double* V, int32_t max_sweeps
 /* ----------------------------------------------------------- utilities -- */
 int skp_cast_f32_f64(const float* x, double* y, int64_t count, void* stream);
 int skp_cast_f64_f32(const double* x, float* y, int64_t count, void* stream);
+/* 2-D strided casts: y[i*ldy + j] = x[i*ldx + j] for i < rows, j < cols */
+int skp_cast2d_f32_f64(const float* x, int64_t ldx, double* y, int64_t ldy, int64_t rows,
+                       int64_t cols, void* stream);
+int skp_cast2d_f64_f32(const double* x, int64_t ldx, float* y, int64_t ldy, int64_t rows,
+                       int64_t cols, void* stream);
 /* out[0] += sum of squares (double), nonfinite[0] += #non-finite (either may be NULL) */
 int skp_sumsq_f32(const float* X, int64_t rows, int64_t cols, int64_t ld, double* out,
                   int64_t* nonfinite, void* stream);

@@ -258,6 +258,18 @@ def randsvd(a, qb):
     return qb @ u, s, v
 
 
+def lowrank_factorize(a, spec: Spec):
+    """power.py:202-239: Y = powered block, X = pinv(S2^T Y) (S2^T a), S2 ~ substream(seed, 2)."""
+    a = as_matrix(a)
+    m, n = a.shape
+    s1 = CountSketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s)
+    atil = s1.apply_right(a)
+    omega = draw_omega(spec.r1, spec.r2, substream(spec.seed, 1))
+    y = power_iterate(atil, omega, spec.q, stabilized=spec.stabilized)
+    s2 = CountSketch(spec.sketch_kind, m, spec.r1, substream(spec.seed, 2), s=spec.s)
+    return y, pinv(s2.apply_left_transpose(y)) @ s2.apply_left_transpose(a)
+
+
 def nystrom_core(a, spec: Spec, stabilized: bool = False):
     """power.py:272-287 without _check_psd (O(n^3), infeasible at C4).
 

@@ -31,10 +31,11 @@ SIGNATURES = {
                                    _vp, _vp, _vp, _i64, _vp]),
     "skp_countsketch_csc_ws_bytes": (_i64, [_i64, _i32, _i64]),
     "skp_countsketch_csc": (_int, [_vp, _vp, _i64, _i32, _i64, _vp, _vp, _vp, _i64, _vp]),
+    "skp_sketch_right_ws_bytes": (_i64, [_i64, _i32, _i64, _i32]),
     "skp_sketch_right_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _i64,
-                                    _vp, _vp, _vp]),
+                                    _vp, _vp, _vp, _i64, _vp]),
     "skp_sketch_right_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _i64,
-                                    _vp, _vp, _vp]),
+                                    _vp, _vp, _vp, _i64, _vp]),
     "skp_sketch_left_t_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _i64,
                                      _vp]),
     "skp_sketch_left_t_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _i64,
@@ -50,6 +51,8 @@ SIGNATURES = {
     "skp_syevj_f64": (_int, [_vp, _i64, _vp, _vp, _i32, _vp, _i64, _vp, _vp]),
     "skp_cast_f32_f64": (_int, [_vp, _vp, _i64, _vp]),
     "skp_cast_f64_f32": (_int, [_vp, _vp, _i64, _vp]),
+    "skp_cast2d_f32_f64": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
+    "skp_cast2d_f64_f32": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
     "skp_sumsq_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "skp_sumsq_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "skp_symmetrize_f32": (_int, [_vp, _i64, _i64, _vp]),

@@ -62,6 +62,24 @@ def workspace(device, nbytes: int) -> torch.Tensor:
     return _WS.get(device, nbytes)
 
 
+def empty2d(rows: int, cols: int, dtype, device) -> torch.Tensor:
+    """rows x cols view of a buffer whose rows start on 16-byte boundaries
+    (leading dimension rounded up to 4 fp32 / 2 fp64), as TMA requires."""
+    per = 16 // torch.empty((), dtype=dtype).element_size()
+    ld = max(per, (cols + per - 1) // per * per)
+    return torch.empty((rows, ld), dtype=dtype, device=device)[:, :cols]
+
+
+def aligned2d(t: torch.Tensor) -> torch.Tensor:
+    """t itself if its rows are 16-byte aligned, else a padded copy."""
+    es = t.element_size()
+    if t.stride(1) == 1 and (t.stride(0) * es) % 16 == 0 and t.data_ptr() % 16 == 0:
+        return t
+    out = empty2d(t.shape[0], t.shape[1], t.dtype, t.device)
+    out.copy_(t)
+    return out
+
+
 def _rows_ld(x: torch.Tensor):
     if x.dim() != 2:
         raise ValueError(f"expected a 2-D tensor, got shape {tuple(x.shape)}")
@@ -104,10 +122,12 @@ def sketch_right(a: torch.Tensor, colptr, entries, s: int, r: int, out=None, fro
     """K2: a (m x n) @ S -> (m x r), fused ||a||_F^2 / non-finite count."""
     m, n, lda = _rows_ld(a)
     if out is None:
-        out = torch.empty((m, r), dtype=a.dtype, device=a.device)
+        out = empty2d(m, r, a.dtype, a.device)
     _, _, ldo = _rows_ld(out)
+    wsb = _lib.load().skp_sketch_right_ws_bytes(n, s, r, a.element_size())
+    ws = workspace(a.device, wsb)
     call(f"skp_sketch_right_{_SFX[a.dtype]}", ptr(a), lda, m, n, ptr(colptr), ptr(entries), s, r,
-         ptr(out), ldo, ptr(fro2), ptr(nonfinite), stream_ptr(a.device))
+         ptr(out), ldo, ptr(fro2), ptr(nonfinite), ptr(ws), wsb, stream_ptr(a.device))
     return out
 
 
@@ -115,7 +135,7 @@ def sketch_left_t(x: torch.Tensor, colptr, entries, s: int, r: int, out=None):
     """K3: S^T @ x (x n x c) -> (r x c)."""
     n, c, ldx = _rows_ld(x)
     if out is None:
-        out = torch.empty((r, c), dtype=x.dtype, device=x.device)
+        out = empty2d(r, c, x.dtype, x.device)
     _, _, ldo = _rows_ld(out)
     call(f"skp_sketch_left_t_{_SFX[x.dtype]}", ptr(x), ldx, n, c, ptr(colptr), ptr(entries), s, r,
          ptr(out), ldo, stream_ptr(x.device))
@@ -139,7 +159,7 @@ def gemm(a, b, ta: bool = False, tb: bool = False, alpha: float = 1.0, beta: flo
     if K != Kb:
         raise ValueError(f"dimension mismatch: {M}x{K} @ {Kb}x{N}")
     if out is None:
-        out = torch.empty((M, N), dtype=a.dtype, device=a.device)
+        out = empty2d(M, N, a.dtype, a.device)
         if beta != 0.0:
             raise ValueError("beta != 0 needs out")
     _, _, ldc = _rows_ld(out)
@@ -156,12 +176,18 @@ def gemm(a, b, ta: bool = False, tb: bool = False, alpha: float = 1.0, beta: flo
 # ------------------------------------------------------------ utilities ----
 
 def cast(x: torch.Tensor, dtype) -> torch.Tensor:
+    """fp32 <-> fp64 (device kernel); 2-D results keep 16-byte rows."""
     if x.dtype == dtype:
         return x
+    sfx = "f32_f64" if dtype == F64 else "f64_f32"
+    if x.dim() == 2:
+        r, c, ld = _rows_ld(x)
+        out = empty2d(r, c, dtype, x.device)
+        call(f"skp_cast2d_{sfx}", ptr(x), ld, ptr(out), out.stride(0), r, c, stream_ptr(x.device))
+        return out
     x = x.contiguous()
     out = torch.empty(x.shape, dtype=dtype, device=x.device)
-    name = "skp_cast_f32_f64" if dtype == F64 else "skp_cast_f64_f32"
-    call(name, ptr(x), ptr(out), x.numel(), stream_ptr(x.device))
+    call(f"skp_cast_{sfx}", ptr(x), ptr(out), x.numel(), stream_ptr(x.device))
     return out
 
 

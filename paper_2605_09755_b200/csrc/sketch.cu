@@ -9,9 +9,19 @@
 //     ~200 KB) a slab-free variant gathers straight from L2.
 // K3  out = S^T . X  (reference sketching.py:181-182)
 //     Row gather: out[c][:] = sum_{(j,sg) in col c} sg * X[j][:] / sqrt(s).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace skp {
+
+template <typename T>
+int sketch_right_rows(const T* A, int64_t lda, int64_t m, int64_t n, const int32_t* colptr,
+                      const int32_t* entries, int32_t s, int64_t r, T* out, int64_t ldo,
+                      double* fro2, int64_t* nonfinite, void* ws, int64_t ws_bytes,
+                      cudaStream_t st);
+int64_t sketch_rows_ws_bytes(int64_t n, int32_t s, int64_t r, int elem);
+
 namespace {
 
 constexpr int kSketchThreads = 512;
@@ -80,8 +90,9 @@ __global__ void sketch_right_direct_kernel(const T* __restrict__ A, int64_t lda,
                                            const int32_t* __restrict__ colptr,
                                            const int32_t* __restrict__ entries, T scale,
                                            int64_t r, T* __restrict__ out, int64_t ldo) {
-    const int64_t i = blockIdx.y;
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t cblocks = (r + blockDim.x - 1) / blockDim.x;
+    const int64_t i = (int64_t)blockIdx.x / cblocks;
+    const int64_t c = ((int64_t)blockIdx.x % cblocks) * blockDim.x + threadIdx.x;
     if (c >= r || i >= m) return;
     const T* row = A + i * lda;
     T acc = T(0);
@@ -139,10 +150,15 @@ __global__ void sketch_left_t_kernel(const T* __restrict__ X, int64_t ldx, int64
 template <typename T>
 int sketch_right(const T* A, int64_t lda, int64_t m, int64_t n, const int32_t* colptr,
                  const int32_t* entries, int32_t s, int64_t r, T* out, int64_t ldo, double* fro2,
-                 int64_t* nonfinite, void* stream) {
+                 int64_t* nonfinite, void* ws, int64_t ws_bytes, void* stream) {
     SKP_ARG(m >= 1 && n >= 1 && r >= 1 && s >= 1, "sketch_right: bad sizes");
     SKP_ARG(lda >= n && ldo >= r, "sketch_right: bad leading dimension");
     cudaStream_t st = SKP_STREAM(stream);
+    if (ws && !getenv("SKP_SKETCH_SLAB")) {
+        int rc = sketch_right_rows<T>(A, lda, m, n, colptr, entries, s, r, out, ldo, fro2,
+                                      nonfinite, ws, ws_bytes, st);
+        if (rc != SKP_ERR_UNSUPPORTED) return rc;
+    }
     const T scale = T(1) / sqrt(T(s));
     const int64_t row_bytes = n * (int64_t)sizeof(T);
     if (row_bytes <= kSlabBytes) {
@@ -158,8 +174,8 @@ int sketch_right(const T* A, int64_t lda, int64_t m, int64_t n, const int32_t* c
         SKP_LAUNCHED(sketch_right_slab_kernel);
         return SKP_OK;
     }
-    SKP_ARG(m < 65536 * 1024LL, "sketch_right: m too large for the direct path");
-    dim3 grid((unsigned)cdiv(r, 256), (unsigned)m);
+    SKP_ARG(cdiv(r, 256) * m < INT32_MAX, "sketch_right: m too large for the direct path");
+    dim3 grid((unsigned)(cdiv(r, 256) * m));
     sketch_right_direct_kernel<T><<<grid, 256, 0, st>>>(A, lda, m, colptr, entries, scale, r, out,
                                                         ldo);
     SKP_LAUNCHED(sketch_right_direct_kernel);
@@ -207,19 +223,25 @@ int sumsq(const T* X, int64_t rows, int64_t cols, int64_t ld, double* out, int64
 
 using namespace skp;
 
+extern "C" int64_t skp_sketch_right_ws_bytes(int64_t n, int32_t s, int64_t r,
+                                             int32_t elem_bytes) {
+    return sketch_rows_ws_bytes(n, s, r, elem_bytes);
+}
 extern "C" int skp_sketch_right_f32(const float* A, int64_t lda, int64_t m, int64_t n,
                                     const int32_t* colptr, const int32_t* entries, int32_t s,
                                     int64_t r, float* out, int64_t ldo, double* fro2,
-                                    int64_t* nonfinite, void* stream) {
+                                    int64_t* nonfinite, void* ws, int64_t ws_bytes,
+                                    void* stream) {
     return sketch_right<float>(A, lda, m, n, colptr, entries, s, r, out, ldo, fro2, nonfinite,
-                               stream);
+                               ws, ws_bytes, stream);
 }
 extern "C" int skp_sketch_right_f64(const double* A, int64_t lda, int64_t m, int64_t n,
                                     const int32_t* colptr, const int32_t* entries, int32_t s,
                                     int64_t r, double* out, int64_t ldo, double* fro2,
-                                    int64_t* nonfinite, void* stream) {
+                                    int64_t* nonfinite, void* ws, int64_t ws_bytes,
+                                    void* stream) {
     return sketch_right<double>(A, lda, m, n, colptr, entries, s, r, out, ldo, fro2, nonfinite,
-                                stream);
+                                ws, ws_bytes, stream);
 }
 extern "C" int skp_sketch_left_t_f32(const float* X, int64_t ldx, int64_t n, int64_t c,
                                      const int32_t* colptr, const int32_t* entries, int32_t s,

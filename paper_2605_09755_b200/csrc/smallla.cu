@@ -360,6 +360,16 @@ __global__ void cast_f64_f32_kernel(const double* x, float* y, int64_t cnt) {
         y[t] = (float)x[t];
 }
 
+template <typename S, typename D>
+__global__ void cast2d_kernel(const S* __restrict__ x, int64_t ldx, D* __restrict__ y, int64_t ldy,
+                              int64_t rows, int64_t cols) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows * cols;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = t / cols, j = t - i * cols;
+        y[i * ldy + j] = (D)x[i * ldx + j];
+    }
+}
+
 template <typename T>
 __global__ void symmetrize_kernel(T* W, int64_t n, int64_t ld) {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * n;
@@ -568,6 +578,25 @@ extern "C" int skp_cast_f64_f32(const double* x, float* y, int64_t count, void* 
     SKP_LAUNCHED(cast);
     return SKP_OK;
 }
+extern "C" int skp_cast2d_f32_f64(const float* x, int64_t ldx, double* y, int64_t ldy,
+                                  int64_t rows, int64_t cols, void* stream) {
+    SKP_ARG(rows >= 0 && cols >= 0 && ldx >= cols && ldy >= cols, "cast2d: bad sizes");
+    if (!rows || !cols) return SKP_OK;
+    cast2d_kernel<float, double><<<grid_for(rows * cols), 256, 0, SKP_STREAM(stream)>>>(
+        x, ldx, y, ldy, rows, cols);
+    SKP_LAUNCHED(cast2d);
+    return SKP_OK;
+}
+extern "C" int skp_cast2d_f64_f32(const double* x, int64_t ldx, float* y, int64_t ldy,
+                                  int64_t rows, int64_t cols, void* stream) {
+    SKP_ARG(rows >= 0 && cols >= 0 && ldx >= cols && ldy >= cols, "cast2d: bad sizes");
+    if (!rows || !cols) return SKP_OK;
+    cast2d_kernel<double, float><<<grid_for(rows * cols), 256, 0, SKP_STREAM(stream)>>>(
+        x, ldx, y, ldy, rows, cols);
+    SKP_LAUNCHED(cast2d);
+    return SKP_OK;
+}
+
 extern "C" int skp_symmetrize_f32(float* W, int64_t n, int64_t ld, void* stream) {
     SKP_ARG(n >= 1 && ld >= n, "symmetrize: bad sizes");
     symmetrize_kernel<float><<<grid_for(n * n), 256, 0, SKP_STREAM(stream)>>>(W, n, ld);

@@ -194,6 +194,11 @@ def draw_omega(kind: str, rows: int, cols: int, seed: int) -> np.ndarray:
 
 
 def omega_tensor(kind: str, rows: int, cols: int, seed: int, dtype, device) -> torch.Tensor:
+    """Omega on the device with 16-byte-aligned rows (TMA operand)."""
     om = draw_omega(kind, rows, cols, seed)
-    t = torch.from_numpy(om.astype(np.float32) if dtype == F32 else om)
-    return t.pin_memory().to(device, non_blocking=True) if rows * cols > 1 << 16 else t.to(device)
+    out = _ops.empty2d(rows, cols, dtype, device)
+    host = torch.from_numpy(om.astype(np.float32) if dtype == F32 else om)
+    if rows * cols > 1 << 16:
+        host = host.pin_memory()
+    out.copy_(host, non_blocking=True)
+    return out

@@ -1,0 +1,5 @@
+python scripts/gemm_one.py nn > gpurun_out/g1.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 1 -c 1 -o gpurun_out/gemm_nn python scripts/gemm_one.py nn > gpurun_out/ncu_gemm.log 2>&1; echo "ncu rc=$?"
+timeout 300 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/b1.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo "ncu2 rc=$?"
+ls -la gpurun_out

@@ -239,5 +239,8 @@ def test_lowrank_factorize(skp):
     res = skp.lowrank_factorize(a, spec)
     assert res.Y.shape == (200, 20) and res.X.shape == (20, 120)
     err = np.linalg.norm(a - res.Y @ res.X) / np.linalg.norm(a)
-    assert err < 0.2
+    y_o, x_o = o.lowrank_factorize(a, o.Spec(k=10, l=20, r1=40, r2=20, q=2, seed=7, s=3))
+    err_o = np.linalg.norm(a - y_o @ x_o) / np.linalg.norm(a)   # 0.2923756... (reference)
+    assert abs(err - err_o) <= 1e-10 * err_o
+    np.testing.assert_allclose(res.Y @ res.X, y_o @ x_o, atol=1e-9 * np.abs(a).max())
     assert set(res.elapsed) >= {"sketch", "power", "regression"}
