@@ -114,24 +114,28 @@ __global__ void chol_trsm_kernel(double* G, int64_t ld, int64_t n, int64_t k0, i
         if (j < b) row[j] = x[j];
 }
 
-// X = L^{-1}: thread per column j, forward substitution down the column.
-__global__ void trinv_kernel(const double* __restrict__ L, int64_t ldl, int64_t n,
-                             double* __restrict__ X) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// X = L^{-1}: one warp per column j, forward substitution down the column.
+// x_i = (delta_ij - sum_{k=j}^{i-1} L_ik x_k) / L_ii; the dot product is split
+// across the 32 lanes (warp shuffle reduction), x lives in shared memory.
+constexpr int kTrinvWarps = 8;
+__global__ void __launch_bounds__(kTrinvWarps * 32)
+trinv_kernel(const double* __restrict__ L, int64_t ldl, int64_t n, double* __restrict__ X) {
+    extern __shared__ double xs_all[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t j = (int64_t)blockIdx.x * kTrinvWarps + warp;
     if (j >= n) return;
-    for (int64_t i = 0; i < j; ++i) X[i * n + j] = 0.0;
+    double* xs = xs_all + (int64_t)warp * n;
+    for (int64_t i = lane; i < j; i += 32) X[i * n + j] = 0.0;
     for (int64_t i = j; i < n; ++i) {
-        double s0 = (i == j) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         const double* li = L + i * ldl;
-        int64_t k = j;
-        for (; k + 3 < i; k += 4) {
-            s0 -= li[k] * X[k * n + j];
-            s1 -= li[k + 1] * X[(k + 1) * n + j];
-            s2 -= li[k + 2] * X[(k + 2) * n + j];
-            s3 -= li[k + 3] * X[(k + 3) * n + j];
-        }
-        for (; k < i; ++k) s0 -= li[k] * X[k * n + j];
-        X[i * n + j] = ((s0 + s1) + (s2 + s3)) / li[i];
+        double acc = 0.0;
+        for (int64_t k = j + lane; k < i; k += 32) acc += li[k] * xs[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        const double xi = ((i == j ? 1.0 : 0.0) - acc) / li[i];
+        if (lane == 0) xs[i] = xi;
+        __syncwarp();
+        if (lane == (int)(i & 31)) X[i * n + j] = xi;
     }
 }
 
@@ -511,8 +515,12 @@ extern "C" int skp_chol_pivot_check_f64(const double* L, int64_t n, int64_t ld, 
 
 extern "C" int skp_trinv_lower_f64(const double* L, int64_t ldl, int64_t n, double* X,
                                    void* stream) {
-    SKP_ARG(n >= 1 && ldl >= n && L && X, "trinv: bad arguments");
-    trinv_kernel<<<(unsigned)cdiv(n, 64), 64, 0, SKP_STREAM(stream)>>>(L, ldl, n, X);
+    SKP_ARG(n >= 1 && n <= 3000 && ldl >= n && L && X, "trinv: bad arguments (n <= 3000)");
+    const size_t smem = (size_t)kTrinvWarps * n * sizeof(double);
+    SKP_CUDA(cudaFuncSetAttribute(trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    trinv_kernel<<<(unsigned)cdiv(n, kTrinvWarps), kTrinvWarps * 32, smem, SKP_STREAM(stream)>>>(
+        L, ldl, n, X);
     SKP_LAUNCHED(trinv_kernel);
     return SKP_OK;
 }

@@ -138,11 +138,13 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     ph.mark("start")
     sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
     ph.mark("make_sketch")
-    omega = omega_tensor(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), a.dtype, dev)
-    ph.mark("omega")
     nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
     atil = sk.right(a, fro2=fro2, nonfinite=nonfinite)
     ph.mark("apply_right")
+    # the host-side Omega draw (numpy ziggurat, bit-identical to the reference)
+    # runs while the device executes K1 + K2 queued above
+    omega = omega_tensor(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), a.dtype, dev)
+    ph.mark("omega")
     bad = comm.allreduce_(nonfinite)
     if int(bad.item()) != 0:
         raise ValueError(f"{name} contains non-finite entries")
