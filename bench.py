@@ -175,7 +175,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     from paper_2605_09755_b200 import _lib, distributed as D
     from paper_2605_09755_b200.sketching import make_sketch, substream
 
-    device = torch.device("cuda", local_rank)
+    device = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(device)
     comm = D.TorchComm() if world > 1 else None
     m, n = cfg["m"], cfg["n"]
@@ -197,7 +197,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
     launches0 = _lib.load().skp_launch_count()
-    clk = ClockSampler(local_rank)
+    clk = ClockSampler(device.index)
     clk.start()
     barrier()
     torch.cuda.synchronize()
@@ -383,6 +383,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional multi-rank check with ranks sharing a GPU")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.q is not None:
@@ -401,8 +403,12 @@ def main():
     import torch
     if world > 1:
         import torch.distributed as dist
+        local_rank = local_rank % torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     line = run_ours(args, cfg, rank, world, local_rank)
     if line is not None:
         if world == 1 and not args.no_cpu:

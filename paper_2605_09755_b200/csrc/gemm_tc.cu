@@ -1,15 +1,20 @@
 // K4: FP32 GEMM on the sm_100a tensor cores by the 3xTF32 split, tcgen05/TMEM.
 //
-//   C = alpha * op(A) op(B) + beta * C,   a = a_hi + a_lo (both TF32),
-//   a.b ~= a_hi.b_hi + a_hi.b_lo + a_lo.b_hi   (error ~2^-22 relative per term)
+//   C = alpha * op(A) op(B) + beta * C,   a = a_hi + a_lo,
+//   a.b ~= a_hi.b_hi + a_hi.b_lo + a_lo.b_hi   (error ~2^-20 relative per term,
+//   below the fp32 accumulation error of the TMEM accumulator for K >~ 100)
+// kind::tf32 reads fp32 containers and TRUNCATES to the TF32 grid (measured on
+// B200: raw-operand products match truncated inputs to accumulation noise and
+// miss round-to-nearest by ~500x), so the raw tile IS a_hi and only
+// a_lo = a - trunc(a) (exact in fp32) is materialised beside it.
 //
 // One persistent CTA per SM, warp-specialised (10 warps):
 //   warp 0      TMA producer: raw fp32 tiles -> smem ring (SWIZZLE_64B, BK=16)
 //   warp 1      MMA issuer: one elected lane issues 6 tcgen05.mma.kind::tf32 per
 //               stage (2 K-steps x 3 products) into a TMEM accumulator; owns the
 //               TMEM allocation (2 x 256 columns = double-buffered accumulators)
-//   warps 2-5   split: raw -> (hi in place, lo beside it), cvt.rna.tf32
-//   warps 6-9   epilogue: tcgen05.ld 32x32b -> alpha/beta -> global (or split-K
+//   warps 2-9   split: lo = x - trunc_tf32(x) beside each raw tile
+//   warps 10-13 epilogue: tcgen05.ld 32x32b -> alpha/beta -> global (or split-K
 //               partials), overlapping the next tile's main loop
 // Operands may be K-major (K contiguous, one 2-D TMA box per tile) or MN-major
 // (MN contiguous, one 16-wide box per 16 MN elements); the UMMA descriptors
@@ -19,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "gemm.h"
@@ -44,6 +50,7 @@ struct TcParams {
     int stages;
     uint32_t a_bytes, b_bytes, stage_bytes;
     uint32_t idesc;
+    int xf_mode;  // 0: 3xTF32 (split in smem); 1: debug -- raw operands, one product
 };
 
 // ------------------------------------------------------------ PTX helpers --
@@ -128,10 +135,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 __device__ __forceinline__ uint32_t tf32_round_bits(uint32_t u) {
     return (u + 0x1000u) & 0xFFFFE000u;
 }
-// x -> (hi, lo) with hi, lo on the TF32 grid and x - hi exact.
-__device__ __forceinline__ void split_tf32(uint32_t x, uint32_t& hi, uint32_t& lo) {
-    hi = tf32_round_bits(x);
-    lo = tf32_round_bits(__float_as_uint(__uint_as_float(x) - __uint_as_float(hi)));
+// lo = x - trunc_tf32(x): exact in fp32; the tensor core truncates it again.
+__device__ __forceinline__ uint32_t tf32_lo(uint32_t x) {
+    return __float_as_uint(__uint_as_float(x) - __uint_as_float(x & 0xFFFFE000u));
 }
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
     uint4 v;
@@ -287,6 +293,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         const uint64_t dbh = operand_desc(bh, p.b_kmajor, j);
                         const uint64_t dbl = operand_desc(bl, p.b_kmajor, j);
                         const uint32_t acc = (kb > w.kb0 || j > 0) ? 1u : 0u;
+                        if (p.xf_mode == 1) {
+                            tc_mma_tf32(d, dah, dbh, p.idesc, acc);
+                            continue;
+                        }
                         tc_mma_tf32(d, dal, dbh, p.idesc, acc);
                         tc_mma_tf32(d, dah, dbl, p.idesc, 1u);
                         tc_mma_tf32(d, dah, dbh, p.idesc, 1u);
@@ -308,6 +318,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const int s = it % S;
                 const uint32_t ph = (it / S) & 1;
                 mbar_wait(&full[s], ph);
+                if (p.xf_mode == 1) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&split[s]);
+                    continue;
+                }
                 // layout per stage: [A_hi | A_lo | B_hi | B_lo]; lo sits one buffer
                 // past its hi, so each 16-B granule maps to (src, src + bytes)
                 const uint32_t a0 = smem_u32(stage_a(s)), b0 = smem_u32(stage_b(s));
@@ -315,13 +330,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     const bool isa = i < nA;
                     const uint32_t src = isa ? a0 + 16u * i : b0 + 16u * (i - nA);
                     const uint32_t dlo = src + (isa ? p.a_bytes : p.b_bytes);
-                    uint4 v = lds128(src), h, l;
-                    split_tf32(v.x, h.x, l.x);
-                    split_tf32(v.y, h.y, l.y);
-                    split_tf32(v.z, h.z, l.z);
-                    split_tf32(v.w, h.w, l.w);
-                    sts128(src, h);
-                    sts128(dlo, l);
+                    const uint4 v = lds128(src);
+                    sts128(dlo, make_uint4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w)));
                 }
                 fence_proxy_async();
                 __syncwarp();
@@ -522,6 +532,7 @@ int gemm_tc_3xtf32(int ta, int tb, int64_t M, int64_t N, int64_t K, float alpha,
     p.ws = pl.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
     p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
     p.stage_bytes = pl.stage_bytes;
+    p.xf_mode = getenv("SKP_TC_RAW1") ? 1 : 0;
     p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(!p.a_kmajor) << 15) |
               ((uint32_t)(!p.b_kmajor) << 16) | ((uint32_t)(p.bn >> 3) << 17) |
               ((uint32_t)(BM >> 4) << 24);

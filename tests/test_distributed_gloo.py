@@ -105,3 +105,30 @@ def test_shard_rows_partition():
             for (a0, ar), (b0, _) in zip(parts, parts[1:]):
                 assert a0 + ar == b0
             assert max(p[1] for p in parts) - min(p[1] for p in parts) <= 1
+
+
+def _pad_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        base = torch.full((5, 8), float(rank + 1))
+        view = base[:, :6]                      # row-padded view, like _ops.empty2d
+        TorchComm().allreduce_(view)
+        out[rank] = view.clone().numpy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduce_padded_views():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_pad_worker, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    for r in range(2):
+        np.testing.assert_array_equal(out[r], np.full((5, 6), 3.0))
