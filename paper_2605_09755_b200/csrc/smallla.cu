@@ -20,6 +20,9 @@ namespace cg = cooperative_groups;
 
 // ----------------------------------------------------------- errors ------
 namespace skp {
+int64_t syev_tri_ws_bytes(int64_t n);
+int syev_tri(const double* A, int64_t n, double* W, double* V, void* ws, int64_t ws_bytes,
+             int32_t* sweeps, cudaStream_t st);
 static thread_local char g_err[512] = "";
 void set_error(const char* fmt, ...) {
     va_list ap;
@@ -779,7 +782,10 @@ extern "C" int64_t skp_syevj_ws_bytes(int64_t n) {
     const int64_t nb0 = cdiv(n, 32), nb = nb0 + (nb0 & 1), np = nb * 32;
     const int64_t blk = (3 * np * np + (nb / 2) * 64 * 64 + n * n) * (int64_t)sizeof(double);
     const int64_t small = 2 * n * n * (int64_t)sizeof(double);
-    return (blk > small ? blk : small) + 64 * sizeof(int32_t) + 256;
+    int64_t b = blk > small ? blk : small;
+    const int64_t tri = syev_tri_ws_bytes(n);
+    b = b > tri ? b : tri;
+    return b + 64 * sizeof(int32_t) + 256;
 }
 
 extern "C" int skp_syevj_f64(double* A, int64_t n, double* W, double* V, int32_t max_sweeps,
@@ -804,10 +810,12 @@ extern "C" int skp_syevj_f64(double* A, int64_t n, double* W, double* V, int32_t
         SKP_LAUNCHED(eig_sort_kernel);
         return SKP_OK;
     }
-    // 112 < n < 700: 2x2 cooperative (cheaper rounds); n >= 700: block Jacobi
-    // (2.3x faster at n = 1050).  SKP_SYEVJ=coop|block forces a variant.
+    // n > 112: tridiagonal reduction + bisection + inverse iteration (default);
+    // SKP_SYEVJ=coop|block selects the Jacobi variants (2x2 cooperative rounds /
+    // 64x64 block rotations) kept for cross-checking.
     const char* force = getenv("SKP_SYEVJ");
-    const bool use_coop = force ? force[0] == 'c' : n < 700;
+    if (!force || force[0] == 't') return syev_tri(A, n, W, V, ws, ws_bytes, sweeps, st);
+    const bool use_coop = force[0] == 'c';
     {
         if (use_coop) {
             SKP_CUDA(cudaMemsetAsync(counters, 0, 64 * sizeof(int32_t), st));

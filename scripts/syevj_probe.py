@@ -19,7 +19,7 @@ for n in (520, 1050):
     err = np.abs(np.sort(w.cpu().numpy())[::-1] - np.sort(np.linalg.eigvalsh(g))[::-1]).max() / lam[0]
     print(f"n={n} time={e0.elapsed_time(e1):.2f} ms sweeps={sw} eigerr={err:.1e}", flush=True)
 '''
-for variant in ("block", "coop"):
+for variant in ("tri", "coop"):
     env = dict(os.environ, SKP_SYEVJ=variant)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     print(variant, r.stdout, r.stderr[-400:], flush=True)
