@@ -47,12 +47,29 @@ def pivot_tol(be, rows: int, cols: int, tol=None) -> float:
     return max(ref, PIVOT_FLOOR[_dtype_key(be)])
 
 
-def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None):
-    """Orthonormal basis of range(y) (linalg.py:57-81) by CholeskyQR2."""
+def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: bool = False,
+                   passes: int = 2):
+    """Orthonormal basis of range(y) (linalg.py:57-81) by CholeskyQR2.
+
+    ``lazy``: no host synchronisation; a Cholesky failure (rank deficiency)
+    is only flagged on the device (``be.lazy_failed()``) and the caller must
+    redo the computation eagerly, where the truncating eigen path runs.
+    ``passes=1`` (lazy only): one CholeskyQR pass -- same span, orthogonality
+    ~eps * cond(Y)^2; used for the stabilisations inside the power iteration,
+    whose only job is to keep the block well conditioned (the final Q always
+    gets two passes)."""
     c = y.shape[1]
     rows_total = y.shape[0] if rows_total is None else rows_total
     rel = pivot_tol(be, rows_total, c, tol)
     g = comm.allreduce_(be.gram64(y))
+    if lazy:
+        x = be.chol_inv64(g, rel, lazy=True)
+        q = be.mm(y, be.to_compute(x), tb=True)
+        if passes == 1:
+            return q
+        g2 = comm.allreduce_(be.gram64(q))
+        x2 = be.chol_inv64(g2, 0.0, lazy=True)
+        return be.mm(q, be.to_compute(x2), tb=True)
     x = be.chol_inv64(g, rel)
     if x is None:
         w, v = be.eig_desc64(g)
@@ -72,13 +89,15 @@ def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None):
     return be.mm(q, be.to_compute(x2), tb=True)
 
 
-def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_total=None):
+def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_total=None,
+                  lazy: bool = False):
     """power.py:113-134 on a row slab of A~: Y = A~ Omega, then q x
     {orth(Y) if stabilized; Z = sum_p A~_p^T Y_p; Y = A~ Z}."""
     y = be.mm(atil, omega)
     for _ in range(q):
         if stabilized:
-            y = orthonormalize(be, comm, y, rows_total=rows_total)
+            y = orthonormalize(be, comm, y, rows_total=rows_total, lazy=lazy,
+                               passes=1 if lazy else 2)
         z = comm.allreduce_(be.mm(atil, y, ta=True))
         y = be.mm(atil, z)
     return y

@@ -222,6 +222,7 @@ class CudaBackend:
         self.dtype = dtype
         self.gemm_mode = gemm_mode if dtype == F32 else "auto"
         self.info = torch.zeros(2, dtype=torch.int32, device=device)
+        self.fail = torch.zeros(2, dtype=torch.int32, device=device)
 
     # dense products in the compute dtype
     def mm(self, a, b, ta=False, tb=False, out=None, alpha=1.0, beta=0.0):
@@ -236,18 +237,33 @@ class CudaBackend:
         bd = cast(b, F64)
         return gemm(bd, bd, False, True)
 
-    def chol_inv64(self, g, rel_tol):
-        """L^{-1} of G = L L^T, or None when G is not numerically full rank."""
+    def chol_inv64(self, g, rel_tol, lazy: bool = False):
+        """L^{-1} of G = L L^T (fused cooperative kernel).
+
+        Eager: zeroes the status, then one 4-byte device->host read; returns
+        None when G is not numerically full rank.  Lazy: no host sync; a failure
+        is OR-ed into ``self.fail`` (checked once by the caller, see
+        ``lazy_failed``) and the returned X is then meaningless."""
         n = g.shape[0]
-        lmat = g.clone()
+        x = torch.empty((n, n), dtype=F64, device=self.device)
+        wsb = _lib.load().skp_cholinv_ws_bytes(n)
+        ws = workspace(self.device, wsb)
         st = stream_ptr(self.device)
-        call("skp_cholesky_f64", ptr(lmat), n, n, ptr(self.info), st)
-        call("skp_chol_pivot_check_f64", ptr(lmat), n, n, rel_tol, ptr(self.info), st)
+        flag = self.fail if lazy else self.info
+        if not lazy:
+            self.info.zero_()
+        call("skp_cholinv_f64", ptr(g), n, g.stride(0), rel_tol, ptr(x), ptr(flag), ptr(ws), wsb, st)
+        if lazy:
+            return x
         if int(self.info[0].item()) != 0:
             return None
-        x = torch.empty_like(lmat)
-        call("skp_trinv_lower_f64", ptr(lmat), n, n, ptr(x), st)
         return x
+
+    def lazy_reset(self):
+        self.fail.zero_()
+
+    def lazy_failed(self) -> bool:
+        return int(self.fail[0].item()) != 0
 
     def eig_desc64(self, g, max_sweeps=30):
         n = g.shape[0]

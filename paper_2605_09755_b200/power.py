@@ -146,12 +146,21 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     omega = omega_tensor(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), a.dtype, dev)
     ph.mark("omega")
     bad = comm.allreduce_(nonfinite)
+    # Fast path: no host synchronisation until the end -- CholeskyQR failures
+    # (numerical rank deficiency) are flagged on the device and checked once,
+    # together with the non-finite count; only then is the eager,
+    # rank-truncating path run.
+    be.lazy_reset()
+    y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total,
+                              lazy=True)
+    ph.mark("power")
+    qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total, lazy=True)
+    ph.mark("orth")
     if int(bad.item()) != 0:
         raise ValueError(f"{name} contains non-finite entries")
-    y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total)
-    ph.mark("power")
-    qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total)
-    ph.mark("orth")
+    if be.lazy_failed():
+        y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total)
+        qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total)
     return qb
 
 

@@ -25,13 +25,17 @@ class NumpyBackend:
         b = b.astype(np.float64)
         return b @ b.T
 
-    def chol_inv64(self, g, rel_tol):
+    def chol_inv64(self, g, rel_tol, lazy=False):
         try:
             lmat = np.linalg.cholesky(g)
+            d = np.abs(np.diag(lmat))
+            ok = d.min() >= rel_tol * d.max()
         except np.linalg.LinAlgError:
-            return None
-        d = np.abs(np.diag(lmat))
-        if d.min() < rel_tol * d.max():
+            lmat, ok = None, False
+        if not ok:
+            if lazy:
+                self._fail = True
+                return np.eye(g.shape[0])
             return None
         return np.linalg.inv(lmat)
 
@@ -73,3 +77,10 @@ class NumpyBackend:
 
     def scalar(self, x):
         return float(np.asarray(x).reshape(-1)[0])
+
+    # lazy (sync-free) protocol of the CUDA backend: numpy never defers
+    def lazy_reset(self):
+        self._fail = False
+
+    def lazy_failed(self):
+        return getattr(self, "_fail", False)

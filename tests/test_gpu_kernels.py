@@ -226,3 +226,29 @@ def test_jacobi_eigensolver(n):
     np.testing.assert_allclose(w, ref, rtol=1e-11, atol=1e-11 * ref[0])
     np.testing.assert_allclose(v.T @ v, np.eye(n), atol=1e-11)
     np.testing.assert_allclose(g @ v, v * w, atol=1e-9 * ref[0])
+
+
+@pytest.mark.parametrize("n", [1, 5, 32, 33, 64, 110, 520, 1050])
+def test_fused_cholinv(n):
+    from paper_2605_09755_b200 import _lib
+    from paper_2605_09755_b200._ops import ptr, workspace
+    g = _spd(n, cond=1e6, seed=n)
+    t = torch.from_numpy(g).cuda()
+    x = torch.empty_like(t)
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    wsb = _lib.load().skp_cholinv_ws_bytes(n)
+    ws = workspace(t.device, wsb)
+    _lib.call("skp_cholinv_f64", ptr(t), n, n, 1e-9, ptr(x), ptr(info), ptr(ws), wsb,
+              torch.cuda.current_stream().cuda_stream)
+    assert int(info.item()) == 0
+    xi = x.cpu().numpy()
+    lmat = np.linalg.cholesky(g)
+    np.testing.assert_allclose(xi @ lmat, np.eye(n), atol=1e-7)
+    assert np.all(np.triu(xi, 1) == 0)
+    # rank check and indefinite detection
+    g2 = g.copy()
+    g2[n // 2, n // 2] = -1.0 if n > 1 else -1.0
+    t2 = torch.from_numpy(g2).cuda()
+    _lib.call("skp_cholinv_f64", ptr(t2), n, n, 1e-9, ptr(x), ptr(info), ptr(ws), wsb,
+              torch.cuda.current_stream().cuda_stream)
+    assert int(info.item()) != 0
