@@ -105,21 +105,25 @@ def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_t
 
 def randsvd(be, comm, a, qb, check: bool = True):
     """power.py:181-199: B = Q^T A (summed over row slabs), thin SVD of B via
-    the fp64 Gram B B^T and the Jacobi eigensolver; U = Q U~, V = B^T U~ / sigma."""
+    the fp64 Gram B B^T and the eigensolver; U = Q U~, V = B^T U~ / sigma.
+
+    B is formed transposed, B^T = A^T Q (n x c): the long dimension n then
+    sits on the GEMM's M side (full 256-row CTA-pair tiles) instead of the
+    short c, and B B^T = (B^T)^T B^T, V = B^T U~ read it directly."""
     if check:
         g = comm.allreduce_(be.gram64(qb))
         dev = be.orth_dev(g)
         if not dev <= ORTHO_TOL[_dtype_key(be)]:
             raise ValueError(f"Q is not orthonormal (deviation {dev:.3e})")
-    b = comm.allreduce_(be.mm(qb, a, ta=True))            # c x n
-    c, n = b.shape
-    gb = be.gram64_rows(b)                                  # c x c, fp64
+    bt = comm.allreduce_(be.mm(a, qb, ta=True))           # n x c
+    n, c = bt.shape
+    gb = be.gram64_rows_t(bt)                               # c x c, fp64
     w, v = be.eig_desc64(gb)
     p = min(c, n)
     sig, inv = be.sqrt_eigs(w)
     vc = be.to_compute(be.cols(v, p))
     u = be.mm(qb, vc)
-    vv = be.mm(b, vc, ta=True)
+    vv = be.mm(bt, vc)
     be.scale_cols_(vv, inv[:p])
     return u, sig[:p], vv
 

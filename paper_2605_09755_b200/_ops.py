@@ -63,9 +63,11 @@ def workspace(device, nbytes: int) -> torch.Tensor:
 
 
 def empty2d(rows: int, cols: int, dtype, device) -> torch.Tensor:
-    """rows x cols view of a buffer whose rows start on 16-byte boundaries
-    (leading dimension rounded up to 4 fp32 / 2 fp64), as TMA requires."""
-    per = 16 // torch.empty((), dtype=dtype).element_size()
+    """rows x cols view of a buffer whose rows start on 128-byte boundaries
+    (leading dimension rounded up to 32 fp32 / 16 fp64): TMA needs 16-byte
+    aligned rows, and the GEMM's one-box-per-stage 3-D view of an MN-major
+    operand needs 32-element chunks that never cross a row."""
+    per = 128 // torch.empty((), dtype=dtype).element_size()
     ld = max(per, (cols + per - 1) // per * per)
     return torch.empty((rows, ld), dtype=dtype, device=device)[:, :cols]
 
@@ -236,6 +238,11 @@ class CudaBackend:
         """b b^T in fp64 arithmetic (b: c x n, widened first)."""
         bd = cast(b, F64)
         return gemm(bd, bd, False, True)
+
+    def gram64_rows_t(self, bt):
+        """(bt^T bt) in fp64 arithmetic, i.e. b b^T for b = bt^T (bt: n x c)."""
+        bd = cast(bt, F64)
+        return gemm(bd, bd, True, False)
 
     def chol_inv64(self, g, rel_tol, lazy: bool = False):
         """L^{-1} of G = L L^T (fused cooperative kernel).

@@ -5,26 +5,39 @@
 //   below the fp32 accumulation error of the TMEM accumulator for K >~ 100)
 // kind::tf32 reads fp32 containers and TRUNCATES to the TF32 grid (measured on
 // B200: raw-operand products match truncated inputs to accumulation noise and
-// miss round-to-nearest by ~500x), so the raw tile IS a_hi and only
-// a_lo = a - trunc(a) (exact in fp32) is materialised beside it.
+// miss round-to-nearest by ~500x), so a raw fp32 value IS its hi part and only
+// lo = x - trunc(x) (exact in fp32) is materialised.
 //
-// One persistent CTA per SM, warp-specialised (10 warps):
-//   warp 0      TMA producer: raw fp32 tiles -> smem ring (SWIZZLE_64B, BK=16)
-//   warp 1      MMA issuer: one elected lane issues 6 tcgen05.mma.kind::tf32 per
-//               stage (2 K-steps x 3 products) into a TMEM accumulator; owns the
-//               TMEM allocation (2 x 256 columns = double-buffered accumulators)
-//   warps 2-9   split: lo = x - trunc_tf32(x) beside each raw tile
+// The A operand lives in TENSOR MEMORY (tcgen05.mma A-from-TMEM): with both
+// operands in shared memory the six MMAs of a stage re-read A and B from smem
+// (60 KB/stage) and, with the TMA writes and the split, shared memory
+// (128 B/clk) -- not the tensor pipe -- bounded the kernel.  Now the split
+// warps read each A row once and store hi|lo straight into TMEM, and the MMAs
+// only stream B from smem.
+//
+// One persistent CTA per SM, warp-specialised (14 warps):
+//   warp 0      TMA producer: raw fp32 A and B tiles -> smem ring (BK = 32)
+//   warp 1      MMA issuer: tcgen05.mma.kind::tf32 [acc], [A tmem], B desc,
+//               12 per stage (4 K-steps x 3 products); owns the TMEM allocation
+//   warps 2-5   A split: thread = tile row; smem row -> (hi, lo) -> tcgen05.st
+//               into the stage's TMEM A slot (64 columns: 32 hi | 32 lo)
+//   warps 6-9   B split: b_lo = b - trunc(b) beside each raw B tile in smem
 //   warps 10-13 epilogue: tcgen05.ld 32x32b -> alpha/beta -> global (or split-K
 //               partials), overlapping the next tile's main loop
-// Operands may be K-major (K contiguous, one 2-D TMA box per tile) or MN-major
-// (MN contiguous, one 16-wide box per 16 MN elements); the UMMA descriptors
-// carry the major-ness, so no transposes are ever materialised.
-// Tiles: BM = 128 (UMMA M), BN = runtime multiple of 16 <= 256, BK = 16.
+// TMEM columns: [acc buffer 0 | acc buffer 1 | A slot 0..S-1].
+// All issuing is warp-convergent (elect.sync inside the asm): a divergent
+// `if (lane == 0)` issue path costs ~300 cycles per tcgen05/TMA instruction.
+// Operands may be K-major or MN-major: B's UMMA descriptor carries its
+// major-ness; A is re-laid row-per-lane by the split warps either way.
+// Tiles: BM = 128 (UMMA M), BN = runtime multiple of 16 (32 for one-box MN
+// loads) <= 192, BK = 32 (a stage carries 12 MMAs, ~1150 tensor cycles, so
+// the per-stage barrier / TMA-issue / split costs stay off the critical path).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <stdlib.h>
+#include <stdio.h>
 
 #include "common.cuh"
 #include "gemm.h"
@@ -33,11 +46,15 @@ namespace skp {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 16;
-constexpr int kWarpTma = 0, kWarpMma = 1, kWarpXf = 2, kNumXf = 8, kWarpEpi = 10, kNumEpi = 4;
+constexpr int BK = 32;
+constexpr int kKSteps = BK / 8;      // tf32 UMMA K = 8
+constexpr uint32_t kASlotCols = 2 * BK;  // TMEM columns per A slot: hi | lo
+constexpr int kWarpTma = 0, kWarpMma = 1, kWarpAx = 2, kWarpBx = 6, kWarpEpi = 10, kNumEpi = 4;
+constexpr int kNumXf = 8;  // A-split + B-split warps arriving on split[s]
+constexpr int kMaxBn = 192;
 constexpr int kThreads = 32 * (kWarpEpi + kNumEpi);
 constexpr uint32_t kTmemCols = 512;
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 12;
 
 struct TcParams {
     int M, N, K;
@@ -50,6 +67,11 @@ struct TcParams {
     int stages;
     uint32_t a_bytes, b_bytes, stage_bytes;
     uint32_t idesc;
+    int a_mn3d, b_mn3d;  // MN-major operand loaded by ONE 3-D box per stage
+    int acc_stride;      // TMEM columns per accumulator buffer
+    int nacc;            // accumulator buffers (2: epilogue overlaps the next tile)
+    unsigned long long* prof;  // debug (SKP_TC_PROF): per-role cycle counters, summed over CTAs
+    int dbg;      // debug: bit0 A / bit1 B re-read a 4-block k window (L2-resident)
     int xf_mode;  // 0: 3xTF32 (split in smem); 1: debug -- raw operands, one product
 };
 
@@ -68,18 +90,27 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, bool spin = false) {
     const uint32_t a = smem_u32(bar);
     long long t0 = 0;
     for (int it = 0;; ++it) {
         uint32_t ok;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(a), "r"(parity)
-            : "memory");
+        if (spin)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(a), "r"(parity)
+                : "memory");
+        else
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(a), "r"(parity)
+                : "memory");
         if (ok) return;
         // watchdog: a protocol bug becomes a trap (error), never a hung GPU
         if (it == 64) t0 = clock64();
@@ -94,6 +125,144 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+// Warp-convergent issue: every lane executes the asm, elect.sync picks one to
+// issue.  (A divergent `if (lane == 0)` issue path compiles to ELECT/R2UR
+// loops costing ~300 cycles per tcgen05/TMA instruction -- 3.4x the MMA time.)
+__device__ __forceinline__ void mbar_expect_tx_e(uint64_t* bar, uint32_t bytes) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+                 "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_e(uint64_t* bar) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+                 "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_e(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                              int c0, int c1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_e(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                              int c0, int c1, int c2) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+// Arrive on a barrier in another CTA of the cluster.  Default (.release.cta)
+// semantics: the data being published is already complete (tcgen05.wait::st,
+// fence.proxy.async) and lives in the peer SM's own smem/TMEM; a .cluster
+// release fence here measured ~1250 cycles per arrive under TMA load.
+__device__ __forceinline__ void mbar_arrive_cluster_e(uint32_t cl_addr) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+                 "@p mbarrier.arrive.shared::cluster.b64 _, [%0];\n\t}" ::"r"(cl_addr)
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                     "memory");
+}
+// wait with cluster-scope acquire (barrier arrived on from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    long long t0 = 0;
+    for (int it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it == 64) t0 = clock64();
+        if (it > 64 && (it & 1023) == 0 && clock64() - t0 > (long long)40e9) __trap();
+    }
+}
+template <bool kPair>
+__device__ __forceinline__ void mbar_wait_k(uint64_t* bar, uint32_t parity, bool cl_scope = false) {
+    if (kPair && cl_scope) mbar_wait_cl(bar, parity);
+    else mbar_wait(bar, parity);
+}
+// commit to the barrier at this smem offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair_e(uint64_t* bar) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+                 "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                 " [%0], %1;\n\t}" ::"r"(smem_u32(bar)), "h"((uint16_t)3)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_ts_pair_e(uint32_t d, uint32_t a_tmem, uint64_t b,
+                                                      uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t.reg .b32 r;\n\t"
+        "setp.ne.b32 q, %4, 0;\n\t"
+        "elect.sync r|p, 0xffffffff;\n\t"
+        "@p tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, q;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_e(uint64_t* bar) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+                 "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+                 ::"r"(smem_u32(bar))
+                 : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem desc]
+__device__ __forceinline__ void tc_mma_tf32_ts_e(uint32_t d, uint32_t a_tmem, uint64_t b,
+                                                 uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t.reg .b32 r;\n\t"
+        "setp.ne.b32 q, %4, 0;\n\t"
+        "elect.sync r|p, 0xffffffff;\n\t"
+        "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, q;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+        "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -107,15 +276,6 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      smem_u32(bar))
                  : "memory");
-}
-__device__ __forceinline__ void tc_mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                            uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     uint32_t r[16];
@@ -153,14 +313,14 @@ __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
 }
 
 // UMMA shared-memory descriptors (sm_100, version 1).
-//  K-major : SWIZZLE_64B, rows of 64 B (16 fp32 of K), 8-row atoms (SBO 512 B);
+//  K-major : SWIZZLE_128B, rows of 128 B (32 fp32 of K), 8-row atoms (SBO 1 KB);
 //            K-step of 8 = +32 B inside the atom.
 //  MN-major: SWIZZLE_128B_BASE32B -- the only MN-major layout tf32 accepts:
 //            atoms of 32 MN-elements (128 B) x 4 K-rows, 32-B chunks swizzled
 //            (TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B); LBO = MN-chunk stride
 //            (BK rows x 128 B), SBO = 4-row atom stride (512 B); K-step of 8 =
 //            +1 KB.
-constexpr uint32_t kLayoutSW64 = 4, kLayoutSW128Base32B = 1;
+constexpr uint32_t kLayoutSW128 = 2, kLayoutSW128Base32B = 1;
 constexpr uint32_t kMnChunkBytes = 32 * BK * 4;  // one TMA box: 32 MN x BK K
 
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
@@ -174,7 +334,7 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
     return d;
 }
 __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int kmajor, int j) {
-    return kmajor ? make_desc(base + 32u * j, 16u, 512u, kLayoutSW64)
+    return kmajor ? make_desc(base + 32u * j, 16u, 1024u, kLayoutSW128)
                   : make_desc(base + 1024u * j, kMnChunkBytes, 512u, kLayoutSW128Base32B);
 }
 
@@ -194,6 +354,22 @@ __device__ __forceinline__ Work unit_of(const TcParams& p, int u) {
     return w;
 }
 
+// ring position: stage index and its phase bit, advanced without div/mod
+struct Ring {
+    int s = 0;
+    uint32_t ph = 0;
+    __device__ __forceinline__ void next(int S) {
+        if (++s == S) { s = 0; ph ^= 1; }
+    }
+};
+
+// kPair: a CTA pair (cluster of 2, tcgen05 cta_group::2) computes a 256-row
+// tile: each CTA holds its own 128 A rows (in its TMEM) and HALF of the B tile
+// (bn/2 columns) in its smem; the leader's MMA warp issues M=256 MMAs that
+// read both halves, so each SM streams ~30% fewer operand bytes from L2 and
+// reads half as much B from smem.  Split / epilogue warps of both CTAs arrive
+// on the leader's barriers; MMA commits multicast to both CTAs.
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const TcParams p) {
@@ -211,144 +387,254 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int units = p.tiles_m * p.tiles_n * p.splits;
+    const uint32_t rank = kPair ? cluster_rank() : 0u;
+    const bool leader = rank == 0;
+    const int ustart = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int ustride = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    constexpr int kRowsPerUnit = kPair ? 2 * BM : BM;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&split[s], kNumXf);
+            // paired: the peer's split warps arrive locally and its MMA warp
+            // forwards ONE cluster-scope arrive per stage to the leader (a
+            // release.cluster arrive from every split warp cost ~1000 cycles/stage)
+            mbar_init(&split[s], (kPair && leader) ? kNumXf + 1 : kNumXf);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], kNumEpi);
+            mbar_init(&tempty[b], kPair ? 2 * kNumEpi : kNumEpi);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kWarpMma) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_slot)),
-                     "r"(kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (kPair) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if (kPair) cluster_sync_all();
+    else __syncthreads();
     tc_fence_after();
+    // arrival targets on the leader (own barriers when not paired)
+    const uint32_t split_cl0 = kPair ? mapa_shared(smem_u32(split), 0) : 0u;
+    const uint32_t tempty_cl0 = kPair ? mapa_shared(smem_u32(tempty), 0) : 0u;
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t acol0 = (uint32_t)(p.nacc * p.acc_stride);  // first A slot column
 
+    // stage layout: [A raw (a_bytes) | B raw (b_bytes) | B lo (b_bytes)]
+    const uint32_t smem0 = smem_u32(smem);
     auto stage_a = [&](int s) { return smem + (size_t)s * p.stage_bytes; };
-    auto stage_alo = [&](int s) { return stage_a(s) + p.a_bytes; };
-    auto stage_b = [&](int s) { return stage_a(s) + 2 * p.a_bytes; };
-    auto stage_blo = [&](int s) { return stage_b(s) + p.b_bytes; };
+    auto stage_b = [&](int s) { return stage_a(s) + p.a_bytes; };
+    long long pw0 = 0, pw1 = 0;
+    const long long role_t0 = p.prof ? clock64() : 0;
+#define SKP_TIMED_WAIT(acc, call)                 \
+    do {                                          \
+        if (p.prof) {                             \
+            const long long t_ = clock64();       \
+            call;                                 \
+            acc += clock64() - t_;                \
+        } else {                                  \
+            call;                                 \
+        }                                         \
+    } while (0)
 
     if (warp == kWarpTma) {
-        if (lane == 0) {
-            int it = 0;
-            for (int u = blockIdx.x; u < units; u += gridDim.x) {
-                Work w = unit_of(p, u);
-                const int m0 = w.tm * BM, n0 = w.tn * p.bn;
-                for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
-                    const int s = it % S;
-                    const uint32_t ph = (it / S) & 1;
-                    mbar_wait(&empty[s], ph ^ 1);
-                    mbar_expect_tx(&full[s], p.a_bytes + p.b_bytes);
-                    const int k0 = kb * BK;
-                    if (p.a_kmajor) {
-                        tma_load_2d(&map_a, &full[s], stage_a(s), k0, m0);
-                    } else {
-                        for (int c = 0; c < BM / 32; ++c)
-                            tma_load_2d(&map_a, &full[s], stage_a(s) + c * kMnChunkBytes,
-                                        m0 + 32 * c, k0);
-                    }
-                    if (p.b_kmajor) {
-                        tma_load_2d(&map_b, &full[s], stage_b(s), k0, n0);
-                    } else {
-                        for (int c = 0; c < (p.bn + 31) / 32; ++c)
-                            tma_load_2d(&map_b, &full[s], stage_b(s) + c * kMnChunkBytes,
-                                        n0 + 32 * c, k0);
-                    }
+        Ring r;
+        for (int u = ustart; u < units; u += ustride) {
+            Work w = unit_of(p, u);
+            const int m0 = w.tm * kRowsPerUnit + (int)rank * BM;
+            const int n0 = w.tn * p.bn + (kPair ? (int)rank * (p.bn / 2) : 0);
+            for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
+                const int s = r.s;
+                SKP_TIMED_WAIT(pw0, mbar_wait_k<kPair>(&empty[s], r.ph ^ 1, (p.dbg & 128) != 0));
+                mbar_expect_tx_e(&full[s], p.a_bytes + p.b_bytes);
+                const int k0 = ((p.dbg & 1) ? (kb & 3) : kb) * BK;
+                const int k0b = ((p.dbg & 2) ? (kb & 3) : kb) * BK;
+                if (p.a_kmajor) {
+                    tma_load_2d_e(&map_a, &full[s], stage_a(s), k0, m0);
+                } else if (p.a_mn3d) {
+                    tma_load_3d_e(&map_a, &full[s], stage_a(s), 0, k0, m0 / 32);
+                } else {
+                    for (int c = 0; c < BM / 32; ++c)
+                        tma_load_2d_e(&map_a, &full[s], stage_a(s) + c * kMnChunkBytes, m0 + 32 * c,
+                                      k0);
+                }
+                if (p.b_kmajor) {
+                    tma_load_2d_e(&map_b, &full[s], stage_b(s), k0b, n0);
+                } else if (p.b_mn3d) {
+                    tma_load_3d_e(&map_b, &full[s], stage_b(s), 0, k0b, n0 / 32);
+                } else {
+                    const int bcols = kPair ? p.bn / 2 : p.bn;
+                    for (int c = 0; c < (bcols + 31) / 32; ++c)
+                        tma_load_2d_e(&map_b, &full[s], stage_b(s) + c * kMnChunkBytes, n0 + 32 * c,
+                                      k0b);
                 }
             }
         }
-    } else if (warp == kWarpMma) {
-        int it = 0, ul = 0;
-        for (int u = blockIdx.x; u < units; u += gridDim.x, ++ul) {
+    } else if (warp == kWarpMma && leader) {
+        // B descriptors: stage 0 / K-step 0, plus per-stage, per-K-step and
+        // hi->lo offsets (the 14-bit start-address field never carries:
+        // smem addresses < 228 KB)
+        const uint64_t bdesc0 = operand_desc(smem_u32(stage_b(0)), p.b_kmajor, 0);
+        const uint64_t sstep = p.stage_bytes >> 4;
+        const uint64_t jstep = p.b_kmajor ? (32u >> 4) : (1024u >> 4);
+        const uint64_t lostep = p.b_bytes >> 4;
+        const bool raw = p.xf_mode == 1;
+        Ring r;
+        int ul = 0;
+        for (int u = ustart; u < units; u += ustride, ++ul) {
             Work w = unit_of(p, u);
-            const int buf = ul & 1;
-            const uint32_t aph = (ul >> 1) & 1;
-            mbar_wait(&tempty[buf], aph ^ 1);
+            const int buf = p.nacc == 2 ? (ul & 1) : 0;
+            const uint32_t aph = (uint32_t)(p.nacc == 2 ? (ul >> 1) : ul) & 1u;
+            SKP_TIMED_WAIT(pw1, mbar_wait_k<kPair>(&tempty[buf], aph ^ 1, (p.dbg & 128) != 0));
             tc_fence_after();
-            const uint32_t d = tmem_base + (uint32_t)(buf * 256);
-            for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
-                const int s = it % S;
-                const uint32_t ph = (it / S) & 1;
-                mbar_wait(&split[s], ph);
+            const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
+            for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
+                const int s = r.s;
+                SKP_TIMED_WAIT(pw0, mbar_wait_k<kPair>(&split[s], r.ph, (p.dbg & 128) != 0));
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t ah = smem_u32(stage_a(s)), al = smem_u32(stage_alo(s));
-                    const uint32_t bh = smem_u32(stage_b(s)), bl = smem_u32(stage_blo(s));
+                const uint64_t bh = bdesc0 + (uint64_t)s * sstep;
+                // A slot: hi at +0..BK-1, lo at +BK..2BK-1
+                const uint32_t ah = tmem_base + acol0 + kASlotCols * (uint32_t)s;
+                auto mma = [&](uint32_t a_t, uint64_t b_d, uint32_t acc) {
+                    if (kPair) tc_mma_tf32_ts_pair_e(d, a_t, b_d, p.idesc, acc);
+                    else tc_mma_tf32_ts_e(d, a_t, b_d, p.idesc, acc);
+                };
 #pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const uint64_t dah = operand_desc(ah, p.a_kmajor, j);
-                        const uint64_t dal = operand_desc(al, p.a_kmajor, j);
-                        const uint64_t dbh = operand_desc(bh, p.b_kmajor, j);
-                        const uint64_t dbl = operand_desc(bl, p.b_kmajor, j);
-                        const uint32_t acc = (kb > w.kb0 || j > 0) ? 1u : 0u;
-                        if (p.xf_mode == 1) {
-                            tc_mma_tf32(d, dah, dbh, p.idesc, acc);
-                            continue;
-                        }
-                        tc_mma_tf32(d, dal, dbh, p.idesc, acc);
-                        tc_mma_tf32(d, dah, dbl, p.idesc, 1u);
-                        tc_mma_tf32(d, dah, dbh, p.idesc, 1u);
+                for (int j = 0; j < kKSteps; ++j) {
+                    const uint32_t acc = (kb > w.kb0 || j > 0) ? 1u : 0u;
+                    const uint32_t a_hi = ah + 8u * j, a_lo = a_hi + BK;
+                    const uint64_t b_hi = bh + (uint64_t)j * jstep;
+                    if (raw) {
+                        mma(a_hi, b_hi, acc);
+                    } else {
+                        mma(a_lo, b_hi, acc);          // a_lo b_hi
+                        mma(a_hi, b_hi + lostep, 1u);  // a_hi b_lo
+                        mma(a_hi, b_hi, 1u);           // a_hi b_hi
                     }
-                    tc_commit(&empty[s]);
                 }
-                __syncwarp();
+                // frees the smem stage and the TMEM A slot (in both CTAs)
+                if (kPair) tc_commit_pair_e(&empty[s]);
+                else tc_commit_e(&empty[s]);
             }
-            if (lane == 0) tc_commit(&tfull[buf]);
-            __syncwarp();
+            if (kPair) tc_commit_pair_e(&tfull[buf]);
+            else tc_commit_e(&tfull[buf]);
         }
-    } else if (warp >= kWarpXf && warp < kWarpXf + kNumXf) {
-        const int t = threadIdx.x - kWarpXf * 32;
-        int it = 0;
-        const uint32_t nA = p.a_bytes / 16, nB = p.b_bytes / 16;
-        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    } else if (kPair && warp == kWarpMma) {
+        // peer CTA: forward "stage s split done" to the leader's split[s]
+        Ring r;
+        for (int u = ustart; u < units; u += ustride) {
             Work w = unit_of(p, u);
-            for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
-                const int s = it % S;
-                const uint32_t ph = (it / S) & 1;
-                mbar_wait(&full[s], ph);
-                if (p.xf_mode == 1) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&split[s]);
-                    continue;
+            for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
+                SKP_TIMED_WAIT(pw0, mbar_wait(&split[r.s], r.ph));
+                mbar_arrive_cluster_e(split_cl0 + 8u * (uint32_t)r.s);
+            }
+        }
+    } else if (warp >= kWarpAx && warp < kWarpBx) {
+        // A split: thread = tile row (TMEM lane); TMEM lane quadrant = warp % 4
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const uint32_t tlane = (uint32_t)(q * 32) << 16;
+        const bool raw = p.xf_mode == 1;
+        Ring r;
+        for (int u = ustart; u < units; u += ustride) {
+            Work w = unit_of(p, u);
+            for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
+                const int s = r.s;
+                SKP_TIMED_WAIT(pw0, mbar_wait(&full[s], r.ph));
+                const uint32_t a0 = smem0 + (uint32_t)s * p.stage_bytes;
+                uint32_t hi[BK], lo[BK];
+                if (p.a_kmajor) {
+                    // SWIZZLE_128B: 16-B chunk c of row r sits at r*128 + 16*(c ^ (r & 7));
+                    // conflict-free across a warp
+                    const uint32_t rb = a0 + (uint32_t)row * 128u;
+                    const uint32_t sw = (uint32_t)row & 7u;
+#pragma unroll
+                    for (int c = 0; c < BK / 4; ++c) {
+                        const uint4 v = lds128(rb + 16u * ((uint32_t)c ^ sw));
+                        hi[4 * c + 0] = v.x; hi[4 * c + 1] = v.y;
+                        hi[4 * c + 2] = v.z; hi[4 * c + 3] = v.w;
+                    }
+                } else {
+                    // unswizzled MN-major chunks [m/32][k][32]: lanes read 128 contiguous B
+                    const uint32_t cb = a0 + (uint32_t)q * kMnChunkBytes + (uint32_t)lane * 4u;
+#pragma unroll
+                    for (int k = 0; k < BK; ++k) hi[k] = lds32(cb + 128u * k);
                 }
-                // layout per stage: [A_hi | A_lo | B_hi | B_lo]; lo sits one buffer
-                // past its hi, so each 16-B granule maps to (src, src + bytes)
-                const uint32_t a0 = smem_u32(stage_a(s)), b0 = smem_u32(stage_b(s));
-                for (uint32_t i = t; i < nA + nB; i += kNumXf * 32) {
-                    const bool isa = i < nA;
-                    const uint32_t src = isa ? a0 + 16u * i : b0 + 16u * (i - nA);
-                    const uint32_t dlo = src + (isa ? p.a_bytes : p.b_bytes);
-                    const uint4 v = lds128(src);
-                    sts128(dlo, make_uint4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w)));
+                const uint32_t ta = tmem_base + tlane + acol0 + kASlotCols * (uint32_t)s;
+                tmem_st16(ta, hi);
+                tmem_st16(ta + 16, hi + 16);
+                if (!raw) {
+#pragma unroll
+                    for (int k = 0; k < BK; ++k) lo[k] = tf32_lo(hi[k]);
+                    tmem_st16(ta + BK, lo);
+                    tmem_st16(ta + BK + 16, lo + 16);
                 }
-                fence_proxy_async();
+                tmem_st_wait();
+                tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&split[s]);
+                mbar_arrive_e(&split[s]);
+            }
+        }
+    } else if (warp >= kWarpBx && warp < kWarpEpi) {
+        // B split: b_lo beside the raw B tile
+        const int t = threadIdx.x - kWarpBx * 32;
+        const uint32_t nB = p.b_bytes / 16;
+        const bool raw = p.xf_mode == 1;
+        Ring r;
+        for (int u = ustart; u < units; u += ustride) {
+            Work w = unit_of(p, u);
+            for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
+                const int s = r.s;
+                SKP_TIMED_WAIT(pw0, mbar_wait(&full[s], r.ph));
+                if (!raw) {
+                    const uint32_t b0 = smem0 + (uint32_t)s * p.stage_bytes + p.a_bytes;
+                    // 4 loads in flight before the stores (the asm loads/stores
+                    // are not reordered by the compiler)
+                    for (uint32_t i0 = t; i0 < nB; i0 += 4 * 128) {
+                        uint4 v[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t i = i0 + 128u * k;
+                            if (i < nB) v[k] = lds128(b0 + 16u * i);
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t i = i0 + 128u * k;
+                            if (i < nB)
+                                sts128(b0 + p.b_bytes + 16u * i,
+                                       make_uint4(tf32_lo(v[k].x), tf32_lo(v[k].y), tf32_lo(v[k].z),
+                                                  tf32_lo(v[k].w)));
+                        }
+                    }
+                    fence_proxy_async();
+                }
+                __syncwarp();
+                mbar_arrive_e(&split[s]);
             }
         }
     } else if (warp >= kWarpEpi) {
         const int q = warp & 3;  // TMEM lane quadrant this warp may access
         int ul = 0;
-        for (int u = blockIdx.x; u < units; u += gridDim.x, ++ul) {
+        for (int u = ustart; u < units; u += ustride, ++ul) {
             Work w = unit_of(p, u);
-            const int buf = ul & 1;
-            const uint32_t aph = (ul >> 1) & 1;
-            mbar_wait(&tfull[buf], aph);
+            const int buf = p.nacc == 2 ? (ul & 1) : 0;
+            const uint32_t aph = (uint32_t)(p.nacc == 2 ? (ul >> 1) : ul) & 1u;
+            SKP_TIMED_WAIT(pw0, mbar_wait_k<kPair>(&tfull[buf], aph, (p.dbg & 128) != 0));
             tc_fence_after();
-            const int row = w.tm * BM + q * 32 + lane;
-            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256);
+            const int row = w.tm * kRowsPerUnit + (int)rank * BM + q * 32 + lane;
+            const uint32_t tbase =
+                tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * p.acc_stride);
             for (int c0 = 0; c0 < p.bn; c0 += 16) {
                 float v[16];
                 tmem_ld16(tbase + c0, v);
@@ -387,15 +673,34 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[buf]);
+            if (kPair) mbar_arrive_cluster_e(tempty_cl0 + 8u * (uint32_t)buf);
+            else mbar_arrive_e(&tempty[buf]);
+        }
+    }
+#undef SKP_TIMED_WAIT
+    if (p.prof && lane == 0) {
+        // slots: role*4 + {0 total, 1 wait0, 2 wait1}; roles 0 tma, 1 mma, 2 a-split, 3 b-split, 4 epi
+        const int role = warp == kWarpTma ? 0 : warp == kWarpMma ? (leader ? 1 : 5) : warp < kWarpBx ? 2
+                       : warp < kWarpEpi ? 3 : 4;
+        const bool first = warp == kWarpTma || warp == kWarpMma || warp == kWarpAx ||
+                           warp == kWarpBx || warp == kWarpEpi;
+        if (first) {
+            atomicAdd(&p.prof[role * 4 + 0], (unsigned long long)(clock64() - role_t0));
+            atomicAdd(&p.prof[role * 4 + 1], (unsigned long long)pw0);
+            atomicAdd(&p.prof[role * 4 + 2], (unsigned long long)pw1);
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if (kPair) cluster_sync_all();
+    else __syncthreads();
     if (warp == kWarpMma) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(kTmemCols));
+        if (kPair)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(kTmemCols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(kTmemCols));
     }
 }
 
@@ -452,44 +757,85 @@ bool encode_2d(CUtensorMap* map, const float* base, uint64_t cols, uint64_t rows
     return r == CUDA_SUCCESS;
 }
 
+// 3-D view of a row-major [rows x cols] MN-major operand as
+// {32 elements, rows, cols/32 chunks} so one box {32, BK, nchunk} lands in smem
+// as [chunk][k-row][32] (with swz = SWIZZLE_128B_ATOM_32B: the UMMA
+// SWIZZLE_128B_BASE32B layout B needs; unswizzled for A, which the split warps
+// read row-per-lane).  Needs ld % 32 == 0 (chunks never cross a row) -- see
+// _ops.empty2d.
+bool encode_mn3d(CUtensorMap* map, const float* base, uint64_t cols, uint64_t rows, uint64_t ld,
+                 uint32_t nchunk, CUtensorMapSwizzle swz) {
+    cuuint64_t dims[3] = {32, rows, cdiv(cols, 32)};
+    cuuint64_t strides[2] = {ld * sizeof(float), 32 * sizeof(float)};
+    cuuint32_t box[3] = {32, (cuuint32_t)BK, nchunk};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
+                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 struct Plan {
-    int bn, tiles_m, tiles_n, splits, num_kb, kb_per_split, stages;
+    int bn, tiles_m, tiles_n, splits, num_kb, kb_per_split, stages, acc_stride, nacc;
     uint32_t a_bytes, b_bytes, stage_bytes;
     size_t smem;
 };
 
-Plan plan_for(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool b_mn) {
+// pair: CTA-pair plan (256-row units, each CTA loads half of the B tile)
+Plan plan_for(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool b_mn, bool b_mn3d,
+              bool pair) {
     Plan pl;
-    pl.tiles_n = (int)cdiv(N, 256);
-    pl.bn = (int)(cdiv(cdiv(N, pl.tiles_n), 16) * 16);
-    pl.tiles_m = (int)cdiv(M, BM);
+    pl.tiles_n = (int)cdiv(N, kMaxBn);
+    // MN-major B is addressed in whole 32-column chunks (per CTA half when paired)
+    const int gran = b_mn ? (pair ? 64 : (b_mn3d ? 32 : 16)) : (pair ? 32 : 16);
+    pl.bn = (int)(cdiv(cdiv(N, pl.tiles_n), gran) * gran);
+    pl.tiles_m = (int)cdiv(M, pair ? 2 * BM : BM);
     pl.num_kb = (int)cdiv(K, BK);
+    const int slots_machine = pair ? g_sms / 2 : g_sms;
     int64_t base = (int64_t)pl.tiles_m * pl.tiles_n;
     int splits = 1;
-    if (base < 4 * g_sms) {
+    if (base < 4 * slots_machine) {
         double best = 0;
         int maxs = (int)std::max<int64_t>(1, pl.num_kb / 8);
         for (int s = 1; s <= std::min(64, maxs); ++s) {
             int64_t units = base * s;
             if (s > 1 && (int64_t)s * M * N > ws_cap_elems) break;
-            double waves = (double)cdiv(units, g_sms);
-            double eff = (double)units / (waves * g_sms);
+            double waves = (double)cdiv(units, slots_machine);
+            double eff = (double)units / (waves * slots_machine);
             // prefer enough units to fill the machine, then balanced waves
-            double score = std::min(1.0, (double)units / g_sms) * eff;
+            double score = std::min(1.0, (double)units / slots_machine) * eff;
             if (score > best + 0.02) { best = score; splits = s; }
         }
     }
     pl.kb_per_split = (int)cdiv(pl.num_kb, splits);
     pl.splits = (int)cdiv(pl.num_kb, pl.kb_per_split);
     pl.a_bytes = BM * BK * 4;
-    // MN-major B is loaded in 32-wide chunks (a partial last chunk is padded)
-    pl.b_bytes = b_mn ? (uint32_t)cdiv(pl.bn, 32) * kMnChunkBytes : (uint32_t)pl.bn * BK * 4;
-    pl.stage_bytes = 2 * pl.a_bytes + 2 * pl.b_bytes;
+    // B columns held per CTA; MN-major B is loaded in 32-wide chunks (a partial
+    // last chunk is padded)
+    const int bcols = pair ? pl.bn / 2 : pl.bn;
+    pl.b_bytes = b_mn ? (uint32_t)cdiv(bcols, 32) * kMnChunkBytes : (uint32_t)bcols * BK * 4;
+    pl.stage_bytes = pl.a_bytes + 2 * pl.b_bytes;
+    // TMEM: two accumulator buffers, then one 32-column A slot per stage
+    pl.acc_stride = (int)cdiv(pl.bn, 32) * 32;
+    // double-buffer the accumulator (epilogue overlaps the next tile) only when
+    // that still leaves room for 4 A slots
+    pl.nacc = ((int)kTmemCols - 2 * pl.acc_stride) / (int)kASlotCols >= 4 ? 2 : 1;
+    if (getenv("SKP_TC_NACC")) pl.nacc = std::max(1, std::min(2, atoi(getenv("SKP_TC_NACC"))));
+    const int slots = ((int)kTmemCols - pl.nacc * pl.acc_stride) / (int)kASlotCols;
     const size_t budget = 220 * 1024;
     int st = (int)((budget - 1024 - 256) / pl.stage_bytes);
-    pl.stages = std::max(2, std::min(kMaxStages, st));
+    pl.stages = std::max(2, std::min({kMaxStages, st, slots}));
+    if (getenv("SKP_TC_STAGES")) pl.stages = std::max(2, std::min(pl.stages, atoi(getenv("SKP_TC_STAGES"))));
     pl.smem = 1024 + (size_t)pl.stages * pl.stage_bytes + (3 * pl.stages + 4) * 8 + 16;
     return pl;
+}
+
+// CTA pairs pay off once there are enough 256-row units to fill the machine
+bool use_pair(int64_t M) {
+    if (getenv("SKP_TC_NO2CTA")) return false;
+    if (getenv("SKP_TC_FORCE2CTA")) return true;  // test hook: pairs at any M
+    return M > BM;
 }
 
 }  // namespace
@@ -500,7 +846,7 @@ int64_t gemm_tc_ws_bytes(int ta, int tb, int64_t M, int64_t N, int64_t K) {
     (void)ta;
     (void)tb;
     if (!init_tc()) return 0;
-    Plan pl = plan_for(M, N, K, INT64_MAX, tb == 0);
+    Plan pl = plan_for(M, N, K, INT64_MAX, tb == 0, false, use_pair(M));
     return pl.splits > 1 ? (int64_t)pl.splits * M * N * 4 : 0;
 }
 
@@ -518,9 +864,14 @@ int gemm_tc_3xtf32(int ta, int tb, int64_t M, int64_t N, int64_t K, float alpha,
         return SKP_ERR_UNSUPPORTED;
     }
     const int64_t cap = ws ? ws_bytes / 4 : 0;
-    Plan pl = plan_for(M, N, K, cap, tb == 0);
+    // one 3-D box per MN-major operand per stage when rows are 128-byte padded
+    const bool no3d = getenv("SKP_TC_NO3D") != nullptr;
+    const bool a_mn3d = ta && (lda % 32 == 0) && !no3d;
+    const bool b_mn3d = !tb && (ldb % 32 == 0) && !no3d;
+    const bool pair = use_pair(M);
+    Plan pl = plan_for(M, N, K, cap, tb == 0, b_mn3d, pair);
     if (pl.splits > 1 && (!ws || (int64_t)pl.splits * M * N * 4 > ws_bytes)) {
-        pl = plan_for(M, N, K, 0, tb == 0);  // no split-K without workspace
+        pl = plan_for(M, N, K, 0, tb == 0, b_mn3d, pair);  // no split-K without workspace
     }
     TcParams p;
     p.M = (int)M; p.N = (int)N; p.K = (int)K;
@@ -532,26 +883,81 @@ int gemm_tc_3xtf32(int ta, int tb, int64_t M, int64_t N, int64_t K, float alpha,
     p.ws = pl.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
     p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
     p.stage_bytes = pl.stage_bytes;
+    p.acc_stride = pl.acc_stride;
+    p.nacc = pl.nacc;
     p.xf_mode = getenv("SKP_TC_RAW1") ? 1 : 0;
-    p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(!p.a_kmajor) << 15) |
+    p.dbg = getenv("SKP_TC_DBG") ? atoi(getenv("SKP_TC_DBG")) : 0;
+    static unsigned long long* prof_buf = nullptr;
+    p.prof = nullptr;
+    if (getenv("SKP_TC_PROF")) {
+        if (!prof_buf) SKP_CUDA(cudaMalloc(&prof_buf, 24 * sizeof(unsigned long long)));
+        SKP_CUDA(cudaMemsetAsync(prof_buf, 0, 24 * sizeof(unsigned long long), st));
+        p.prof = prof_buf;
+    }
+    // A comes from TMEM (always K-major there); B's major-ness from its layout
+    p.idesc = (1u << 4) | (2u << 7) | (2u << 10) |
               ((uint32_t)(!p.b_kmajor) << 16) | ((uint32_t)(p.bn >> 3) << 17) |
-              ((uint32_t)(BM >> 4) << 24);
+              ((uint32_t)((pair ? 2 * BM : BM) >> 4) << 24);
     CUtensorMap ma, mb;
-    const CUtensorMapSwizzle kSw = CU_TENSOR_MAP_SWIZZLE_64B, mSw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-    bool ok = p.a_kmajor ? encode_2d(&ma, A, (uint64_t)K, (uint64_t)M, lda, BK, BM, kSw)
-                         : encode_2d(&ma, A, (uint64_t)M, (uint64_t)K, lda, 32, BK, mSw);
-    ok = ok && (p.b_kmajor ? encode_2d(&mb, B, (uint64_t)K, (uint64_t)N, ldb, BK, (uint32_t)p.bn, kSw)
-                           : encode_2d(&mb, B, (uint64_t)N, (uint64_t)K, ldb, 32, BK, mSw));
+    const CUtensorMapSwizzle kSw = CU_TENSOR_MAP_SWIZZLE_128B, mSw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+    p.a_mn3d = a_mn3d;
+    p.b_mn3d = b_mn3d;
+    bool ok;
+    if (p.a_kmajor) ok = encode_2d(&ma, A, (uint64_t)K, (uint64_t)M, lda, BK, BM, kSw);
+    else if (p.a_mn3d)
+        ok = encode_mn3d(&ma, A, (uint64_t)M, (uint64_t)K, lda, BM / 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+    else ok = encode_2d(&ma, A, (uint64_t)M, (uint64_t)K, lda, 32, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (!ok) {
+    }
+    const int bcols = pair ? p.bn / 2 : p.bn;  // B columns loaded per CTA
+    if (!ok) {
+    } else if (p.b_kmajor) ok = encode_2d(&mb, B, (uint64_t)K, (uint64_t)N, ldb, BK, (uint32_t)bcols, kSw);
+    else if (p.b_mn3d) ok = encode_mn3d(&mb, B, (uint64_t)N, (uint64_t)K, ldb, (uint32_t)cdiv(bcols, 32), mSw);
+    else ok = encode_2d(&mb, B, (uint64_t)N, (uint64_t)K, ldb, 32, BK, mSw);
     if (!ok) {
         set_error("cuTensorMapEncodeTiled failed");
         return SKP_ERR_UNSUPPORTED;
     }
-    SKP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)pl.smem));
     const int units = p.tiles_m * p.tiles_n * p.splits;
-    const int grid = std::min(units, g_sms);
-    gemm_tc_kernel<<<grid, kThreads, pl.smem, st>>>(ma, mb, p);
-    SKP_LAUNCHED(gemm_tc_kernel);
+    int grid;
+    if (pair) {
+        SKP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        grid = 2 * std::min(units, g_sms / 2);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = pl.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SKP_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<true>, ma, mb, p));
+        SKP_LAUNCHED(gemm_tc_kernel_pair);
+    } else {
+        SKP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        grid = std::min(units, g_sms);
+        gemm_tc_kernel<false><<<grid, kThreads, pl.smem, st>>>(ma, mb, p);
+        SKP_LAUNCHED(gemm_tc_kernel);
+    }
+    if (p.prof) {
+        unsigned long long h[24];
+        SKP_CUDA(cudaStreamSynchronize(st));
+        SKP_CUDA(cudaMemcpy(h, p.prof, sizeof(h), cudaMemcpyDeviceToHost));
+        const char* names[6] = {"tma", "mma", "asp", "bsp", "epi", "fwd"};
+        fprintf(stderr, "[gemm_tc prof] M=%lld N=%lld K=%lld bn=%d stages=%d units=%d grid=%d pair=%d\n",
+                (long long)M, (long long)N, (long long)K, p.bn, p.stages, units, grid, (int)pair);
+        for (int r = 0; r < (pair ? 6 : 5); ++r) {
+            const double n = (pair && (r == 1 || r == 5)) ? grid / 2 : grid;  // leader / peer only
+            fprintf(stderr, "  %-4s total %10.0f  wait0 %10.0f  wait1 %10.0f  (cycles per CTA)\n", names[r],
+                    (double)h[r * 4] / n, (double)h[r * 4 + 1] / n, (double)h[r * 4 + 2] / n);
+        }
+    }
     if (p.splits > 1) {
         int64_t blocks = std::min<int64_t>(cdiv(M * N, 256), (int64_t)g_sms * 8);
         tc_splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(p.ws, p.splits, M, N, alpha, beta, C,

@@ -9,9 +9,16 @@ print("tcgen05:", lib.skp_has_tcgen05(), flush=True)
 torch.manual_seed(0)
 dev = "cuda"
 
-def check(M, N, K, ta, tb, beta=0.0):
-    a = torch.randn((K, M) if ta else (M, K), device=dev)
-    b = torch.randn((N, K) if tb else (K, N), device=dev)
+def rnd(r, c, padded):
+    if not padded:
+        return torch.randn(r, c, device=dev)
+    t = _ops.empty2d(r, c, torch.float32, dev)
+    t.copy_(torch.randn(r, c, device=dev))
+    return t
+
+def check(M, N, K, ta, tb, beta=0.0, padded=False):
+    a = rnd(*((K, M) if ta else (M, K)), padded)
+    b = rnd(*((N, K) if tb else (K, N)), padded)
     ref = (a.double().T if ta else a.double()) @ (b.double().T if tb else b.double())
     c0 = torch.randn(M, N, device=dev)
     out = c0.clone()
@@ -25,8 +32,9 @@ for (M, N, K) in [(128, 16, 16), (128, 128, 64), (256, 176, 1000), (300, 110, 77
     for ta in (0, 1):
         for tb in (0, 1):
             try:
-                e = check(M, N, K, ta, tb, beta=0.5 if (M + ta) % 2 else 0.0)
-                print(f"M={M} N={N} K={K} ta={ta} tb={tb} relerr={e:.2e}", flush=True)
+                for pad in (False, True):
+                    e = check(M, N, K, ta, tb, beta=0.5 if (M + ta) % 2 else 0.0, padded=pad)
+                    print(f"M={M} N={N} K={K} ta={ta} tb={tb} pad={int(pad)} relerr={e:.2e}", flush=True)
             except Exception as ex:
                 print(f"M={M} N={N} K={K} ta={ta} tb={tb} EXC {ex}", flush=True)
 

@@ -25,6 +25,10 @@ class NumpyBackend:
         b = b.astype(np.float64)
         return b @ b.T
 
+    def gram64_rows_t(self, bt):
+        bt = bt.astype(np.float64)
+        return bt.T @ bt
+
     def chol_inv64(self, g, rel_tol, lazy=False):
         try:
             lmat = np.linalg.cholesky(g)
