@@ -86,6 +86,25 @@ int skp_sketch_right_f64(const double* A, int64_t lda, int64_t m, int64_t n,
                          double* out, int64_t ldo, double* fro2, int64_t* nonfinite, void* ws,
                          int64_t ws_bytes, void* stream);
 
+/* K2 v2 (fp32, range-finder path): the same product written with PERMUTED
+ * output columns, out = (A . S) P, by a row gather with a register-resident,
+ * bank-conflict-free schedule.  P sorts the columns of each 768-column slice
+ * by entry count; its table is plan[0 .. slices*768) (int32 column of S, -1
+ * past r).  Build the plan once per sketch (skp_sketch_gather_plan, from the
+ * CSC view); it is usable iff the int32 at byte offset
+ * skp_sketch_gather_plan_fail_offset(r) is 0 after the build.  Requires
+ * n <= 24576 and 16-byte aligned rows padded to a multiple of 4 floats;
+ * returns SKP_ERR_UNSUPPORTED otherwise (callers keep skp_sketch_right).
+ * Replaces the same `a @ self._sparse` (sketching.py:158-164) inside
+ * range_finder_sketched (power.py:141-154): Y = (A S) Omega = (A S P)(P^T Omega). */
+int64_t skp_sketch_gather_plan_bytes(int64_t r);
+int64_t skp_sketch_gather_plan_fail_offset(int64_t r);
+int skp_sketch_gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n, int64_t r,
+                           void* plan, int64_t plan_bytes, void* stream);
+int skp_sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
+                          const void* plan, float scale, float* out, int64_t ldo, double* fro2,
+                          int64_t* nonfinite, void* stream);
+
 /* ---------------------------------------------------------------- K3 ----
  * out (r x c) = S^T . X (X n x c); SketchOperator.apply_left_transpose
  * (reference sketching.py:176-182: `self._sparse.T @ a`).                   */
@@ -160,6 +179,12 @@ int skp_cast2d_f32_f64(const float* x, int64_t ldx, double* y, int64_t ldy, int6
                        int64_t cols, void* stream);
 int skp_cast2d_f64_f32(const double* x, int64_t ldx, float* y, int64_t ldy, int64_t rows,
                        int64_t cols, void* stream);
+/* Row gather y[v, :] = x[perm[v], :], v < rows (P^T Omega for the K2 v2
+ * column permutation; perm = the first `rows` int32 of a gather plan).       */
+int skp_permute_rows_f32(const float* x, int64_t ldx, const int32_t* perm, float* y, int64_t ldy,
+                         int64_t rows, int64_t cols, void* stream);
+int skp_permute_rows_f64(const double* x, int64_t ldx, const int32_t* perm, double* y,
+                         int64_t ldy, int64_t rows, int64_t cols, void* stream);
 /* out[0] += sum of squares (double), nonfinite[0] += #non-finite (either may be NULL) */
 int skp_sumsq_f32(const float* X, int64_t rows, int64_t cols, int64_t ld, double* out,
                   int64_t* nonfinite, void* stream);

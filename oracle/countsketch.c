@@ -15,7 +15,11 @@
  *     first s entries is ascending-key on numpy 2.3.5 (SURVEY.md §7 hard part 2;
  *     pinned by tests/golden against the live reference).
  *   - Generator.integers(0, R): Lemire's nearly-divisionless bounded draw on
- *     32-bit halves of 64-bit draws (low half first), one local buffer per call.
+ *     32-bit values; PCG64's next_uint32 returns the low half of a 64-bit draw
+ *     and keeps the high half in the BIT GENERATOR (has_uint32 / uinteger),
+ *     so the buffer persists across integers() calls: after an odd number of
+ *     32-bit column draws (s == 1) the first sign is that buffered half.
+ *     64-bit draws (random()) neither use nor clear it.
  * Ties between equal 53-bit keys are broken by the lower column index.
  */
 #include <stdint.h>
@@ -30,7 +34,8 @@ static const u128 PCG_MULT =
 typedef struct {
     u128 state;
     u128 inc;
-    /* Generator.integers' 32-bit buffer lives in a local of one fill call */
+    /* PCG64's 32-bit buffer (numpy pcg64_state.has_uint32 / uinteger):
+     * part of the bit generator, persists across integers() calls */
     uint64_t buf;
     int bcnt;
 } pcg64_t;
@@ -73,8 +78,6 @@ static inline uint32_t lemire_u32(pcg64_t* g, uint32_t rng) {
 /* Generator.integers(0, hi, size=cnt) into out[] (int64 path, use_masked=False). */
 static void integers_fill(pcg64_t* g, uint64_t hi, int64_t cnt, int64_t* out) {
     uint64_t rng = hi - 1;
-    g->bcnt = 0;
-    g->buf = 0;
     if (rng == 0) {
         for (int64_t i = 0; i < cnt; ++i) out[i] = 0;
         return;

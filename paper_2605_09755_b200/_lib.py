@@ -36,6 +36,11 @@ SIGNATURES = {
                                     _vp, _vp, _vp, _i64, _vp]),
     "skp_sketch_right_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _i64,
                                     _vp, _vp, _vp, _i64, _vp]),
+    "skp_sketch_gather_plan_bytes": (_i64, [_i64]),
+    "skp_sketch_gather_plan_fail_offset": (_i64, [_i64]),
+    "skp_sketch_gather_plan": (_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "skp_sketch_gather_f32": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, ctypes.c_float, _vp, _i64,
+                                     _vp, _vp, _vp]),
     "skp_sketch_left_t_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _i64,
                                      _vp]),
     "skp_sketch_left_t_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _i64,
@@ -53,6 +58,8 @@ SIGNATURES = {
     "skp_syevj_f64": (_int, [_vp, _i64, _vp, _vp, _i32, _vp, _i64, _vp, _vp]),
     "skp_cast_f32_f64": (_int, [_vp, _vp, _i64, _vp]),
     "skp_cast_f64_f32": (_int, [_vp, _vp, _i64, _vp]),
+    "skp_permute_rows_f32": (_int, [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "skp_permute_rows_f64": (_int, [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp]),
     "skp_cast2d_f32_f64": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
     "skp_cast2d_f64_f32": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
     "skp_sumsq_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),

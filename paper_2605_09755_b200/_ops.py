@@ -133,6 +133,55 @@ def sketch_right(a: torch.Tensor, colptr, entries, s: int, r: int, out=None, fro
     return out
 
 
+GATHER_COLS = 768  # output columns per slice of the K2 v2 plan (sketch_gather.cu)
+
+
+def gather_plan(colptr, entries, n: int, r: int, device):
+    """K2 v2 plan (once per sketch): (plan bytes on the device, perm) where
+    perm[v] = the column of S written at position v by sketch_gather; None when
+    the shape is outside the kernel (n > 24576, or a column / warp needing more
+    than 56 schedule steps) -- the caller then keeps sketch_right."""
+    lib = _lib.load()
+    nb = int(lib.skp_sketch_gather_plan_bytes(r))
+    plan = torch.empty(nb, dtype=torch.uint8, device=device)
+    rc = lib.skp_sketch_gather_plan(ptr(colptr), ptr(entries), n, r, ptr(plan), nb,
+                                    stream_ptr(device))
+    if rc == _lib.SKP_ERR_UNSUPPORTED:
+        return None
+    _lib.check(rc, "skp_sketch_gather_plan")
+    off = int(lib.skp_sketch_gather_plan_fail_offset(r))
+    if int(plan[off:off + 4].view(torch.int32).item()) != 0:
+        return None
+    nslice = -(-r // GATHER_COLS)
+    perm = plan[:nslice * GATHER_COLS * 4].view(torch.int32).cpu().numpy()
+    perm = perm[perm >= 0].astype(np.int64)
+    return plan, perm
+
+
+def sketch_gather(a: torch.Tensor, plan: torch.Tensor, r: int, s: int, out=None, fro2=None,
+                  nonfinite=None):
+    """K2 v2: (a @ S) with the plan's column permutation, fused ||a||_F^2 and
+    non-finite test; fp32, a with 16-byte aligned rows (empty2d)."""
+    m, n, lda = _rows_ld(a)
+    if out is None:
+        out = empty2d(m, r, a.dtype, a.device)
+    _, _, ldo = _rows_ld(out)
+    call("skp_sketch_gather_f32", ptr(a), lda, m, n, r, ptr(plan), 1.0 / float(np.sqrt(s)),
+         ptr(out), ldo, ptr(fro2), ptr(nonfinite), stream_ptr(a.device))
+    return out
+
+
+def permute_rows(x: torch.Tensor, perm_dev: torch.Tensor, out=None) -> torch.Tensor:
+    """out[v, :] = x[perm_dev[v], :] for v < x.shape[0] (perm_dev: int32 on the device)."""
+    rows, cols, ldx = _rows_ld(x)
+    if out is None:
+        out = empty2d(rows, cols, x.dtype, x.device)
+    _, _, ldy = _rows_ld(out)
+    call(f"skp_permute_rows_{_SFX[x.dtype]}", ptr(x), ldx, ptr(perm_dev), ptr(out), ldy, rows,
+         cols, stream_ptr(x.device))
+    return out
+
+
 def sketch_left_t(x: torch.Tensor, colptr, entries, s: int, r: int, out=None):
     """K3: S^T @ x (x n x c) -> (r x c)."""
     n, c, ldx = _rows_ld(x)

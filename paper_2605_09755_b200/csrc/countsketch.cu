@@ -131,29 +131,38 @@ cs_keys_kernel(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
     }
 }
 
-// Signs: element e = j*s + t uses 32-bit half e of the stream starting at
-// draw index d0 (low half first); bit 31 set -> +1 (Lemire with range 2
-// never rejects).  Each thread owns kSignDraws consecutive 64-bit draws.
+// Signs: element e = j*s + t is 32-bit value u0 + e of the generator's uint32
+// stream (value h = half h&1 of 64-bit draw h>>1, low half first); bit 31 set
+// -> +1 (Lemire with range 2 never rejects).  u0 = the uint32 values the
+// column phase consumed: numpy's PCG64 keeps the unused high half of a draw in
+// the bit generator (has_uint32) across integers() calls, so after an odd
+// number of Lemire-32 column draws (s == 1) the first sign is that buffered
+// high half.  Each thread owns kSignDraws consecutive 64-bit draws.
 constexpr int kSignDraws = 16;
 
 __global__ void cs_signs_kernel(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
-                                const int64_t* __restrict__ d0_dev, uint64_t d0_host, int64_t e0,
+                                const int64_t* __restrict__ u0_dev, uint64_t u0_host, int64_t e0,
                                 int64_t e1, int8_t* __restrict__ signs) {
     const u128 inc = mk128(inc_hi, inc_lo);
-    const uint64_t d0 = d0_dev ? (uint64_t)(*d0_dev) : d0_host;
+    const int64_t u0 = u0_dev ? *u0_dev : (int64_t)u0_host;
     // first and last draw covering elements [e0, e1)
-    const int64_t dfirst = e0 >> 1, dlast = (e1 - 1) >> 1;
+    const int64_t dfirst = (u0 + e0) >> 1, dlast = (u0 + e1 - 1) >> 1;
     int64_t d = dfirst + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kSignDraws;
     if (d > dlast) return;
-    u128 x = apply(affine(jpow(d0 + (uint64_t)d + 1), inc), mk128(st_hi, st_lo));
+    u128 x = apply(affine(jpow((uint64_t)d + 1), inc), mk128(st_hi, st_lo));
     const Affine one{pcg_mult(), inc};
     for (int k = 0; k < kSignDraws && d <= dlast; ++k, ++d) {
         uint64_t v = xsl_rr(x);
         x = apply(one, x);
-        int64_t e = 2 * d;
+        const int64_t e = 2 * d - u0;  // element of the low half
         if (e >= e0 && e < e1) signs[e - e0] = ((uint32_t)v >> 31) ? 1 : -1;
         if (e + 1 >= e0 && e + 1 < e1) signs[e + 1 - e0] = ((uint32_t)(v >> 32) >> 31) ? 1 : -1;
     }
+}
+// grid for cs_signs_kernel over elements [e0, e1) (any u0)
+inline int sign_blocks(int64_t e0, int64_t e1) {
+    const int64_t draws = (e1 - e0) / 2 + 2;
+    return (int)cdiv(cdiv(draws, (int64_t)kSignDraws), (int64_t)256);
 }
 
 // ---- s == 1: cols = integers(0, r) by Lemire-32 with rejection --------------
@@ -257,7 +266,7 @@ __global__ void s1_write_kernel(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi,
         if (rank >= j0 && rank < j1) cols[rank - j0] = (int32_t)val[k];
         if (rank == n - 1) {
             int64_t halves_used = h0 + k + 1;
-            *sign_d0 = (halves_used + 1) >> 1;  // fresh 64-bit draw for the signs call
+            *sign_d0 = halves_used;  // uint32 values consumed: the signs continue from here
         }
         ++rank;
     }
@@ -305,11 +314,8 @@ extern "C" int skp_countsketch_gen(uint64_t st_hi, uint64_t st_lo, uint64_t inc_
         if (r == 1) {
             // rng == 0: all zeros, no draws consumed (numpy random_bounded_uint64_fill)
             SKP_CUDA(cudaMemsetAsync(cols, 0, sizeof(int32_t) * (j1 - j0), st));
-            int64_t e0 = j0, e1 = j1;
-            int64_t draws = ((e1 - 1) >> 1) - (e0 >> 1) + 1;
-            int blocks = (int)cdiv(cdiv(draws, kSignDraws), 256);
-            cs_signs_kernel<<<blocks, 256, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo, nullptr, 0, e0,
-                                                   e1, signs);
+            cs_signs_kernel<<<sign_blocks(j0, j1), 256, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo,
+                                                                 nullptr, 0, j0, j1, signs);
             SKP_LAUNCHED(cs_signs_kernel);
             return SKP_OK;
         }
@@ -333,11 +339,8 @@ extern "C" int skp_countsketch_gen(uint64_t st_hi, uint64_t st_lo, uint64_t inc_
         s1_write_kernel<<<(int)ntiles, 256, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo, H, excl, thr,
                                                     tiles, n, j0, j1, cols, d_sign0);
         SKP_LAUNCHED(s1_write_kernel);
-        int64_t e0 = j0, e1 = j1;
-        int64_t draws = ((e1 - 1) >> 1) - (e0 >> 1) + 1;
-        int blocks = (int)cdiv(cdiv(draws, kSignDraws), 256);
-        cs_signs_kernel<<<blocks, 256, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo, d_sign0, 0, e0, e1,
-                                               signs);
+        cs_signs_kernel<<<sign_blocks(j0, j1), 256, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo, d_sign0,
+                                                             0, j0, j1, signs);
         SKP_LAUNCHED(cs_signs_kernel);
         return SKP_OK;
     }
@@ -358,11 +361,11 @@ extern "C" int skp_countsketch_gen(uint64_t st_hi, uint64_t st_lo, uint64_t inc_
         cs_keys_kernel<32><<<(int)blocks, kWarps * 32, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo, r,
                                                               s, j0, j1, cols);
     SKP_LAUNCHED(cs_keys_kernel);
+    // the key phase consumed n*r 64-bit draws (2*n*r uint32 values, none buffered)
     int64_t e0 = j0 * s, e1 = j1 * s;
-    int64_t draws = ((e1 - 1) >> 1) - (e0 >> 1) + 1;
-    int sblocks = (int)cdiv(cdiv(draws, kSignDraws), 256);
-    cs_signs_kernel<<<sblocks, 256, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo, nullptr,
-                                            (uint64_t)n * (uint64_t)r, e0, e1, signs);
+    cs_signs_kernel<<<sign_blocks(e0, e1), 256, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo, nullptr,
+                                                         2 * (uint64_t)n * (uint64_t)r, e0, e1,
+                                                         signs);
     SKP_LAUNCHED(cs_signs_kernel);
     return SKP_OK;
 }

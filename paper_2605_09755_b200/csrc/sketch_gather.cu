@@ -1,0 +1,454 @@
+// K2 v2 (fp32): A~ = A . S as a ROW GATHER with a register-resident,
+// bank-conflict-free schedule.
+//
+// Output column c of A~ is  sum_e sign_e * A[:, j_e]  over the ~n*s/l (C3:
+// 33) CountSketch entries of column c.  Lane = output column: each thread keeps
+// its column's entries in registers as smem byte addresses (bit 31 = negate),
+// and every row of A is streamed whole into a double-buffered shared-memory
+// row by 1-D bulk copies.  One step = 4 instructions for the warp's 32 columns:
+//     LOP3 (address) -> LDS -> LOP3 (sign xor) -> FADD
+// No per-(chunk, column) metadata, no padding slots, no transposes, and the
+// warp's 32 results of a row are one coalesced 128-byte store.
+//
+// Bank conflicts: the 32 lanes of a warp load 32 data-dependent words of the
+// row; the order of each lane's entries is scheduled offline (per sketch, on
+// the device) so that at every step the warp touches 32 distinct banks -- a
+// greedy edge colouring of the lane x bank multigraph, lanes with the most
+// remaining entries served first (a lane that would otherwise lengthen the
+// schedule accepts a conflict).  Lanes without an entry at a step read a zero
+// word in a free bank.  Columns are sorted by entry count inside each slice,
+// so the 32 lanes of a warp need about the same number of steps (C3: ~34
+// steps for ~33 entries).  The sort permutes the OUTPUT COLUMNS: the kernel
+// writes A~ P, and the range finder multiplies by P^T Omega instead of Omega
+// (Y = A~ Omega = (A~ P)(P^T Omega)); apply_right keeps K2 v1's column order.
+//
+// CTA = one slice of kGCols = 768 output columns (24 warps); the last warp to
+// finish a row refills its buffer (bulk copy of the row two ahead).  Grid = G row groups x P slices; CTAs of a row
+// group walk the same rows at the same time, so the P-fold reuse of each row
+// is served by L2 and A is read from HBM once.  ||A||_F^2 (fp64) and the
+// non-finite test are fused: the compute threads of slice p square this
+// slice's 1/P share of each row.
+#include <cuda.h>
+
+#include <algorithm>
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace skp {
+
+namespace {
+
+constexpr int kGW = 24;                   // compute warps per CTA
+constexpr int kGCols = kGW * 32;          // output columns per slice
+// no producer warp: 24 warps x 80 registers is the most a 4-way register file
+// split allows (a 25th warp puts 7 warps on one SMSP: 17920 > 16384); the last
+// warp to finish a row issues the bulk copy of the row two ahead instead
+constexpr int kGThreads = 32 * kGW;
+constexpr int kGTReg = 56;                // schedule steps held in registers
+constexpr int kGTMax = 128;               // schedule steps per warp (the rest: L1/global)
+constexpr int kGBufWords = 24608;         // row buffer: n <= 24576 floats + 32 zero words
+constexpr uint32_t kGBufBytes = kGBufWords * 4;  // 98432, a multiple of 128
+constexpr size_t kGSmem = 2 * (size_t)kGBufBytes + 32 + kGW * 8;
+
+__device__ __forceinline__ uint32_t g_smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void g_mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(g_smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void g_mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = g_smem_u32(bar);
+    long long t0 = 0;
+    for (int it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) return;
+        // watchdog: a protocol bug becomes a trap (error), never a hung GPU
+        if (it == 64) t0 = clock64();
+        if (it > 64 && (it & 1023) == 0 && clock64() - t0 > (long long)40e9) __trap();
+    }
+}
+__device__ __forceinline__ void g_mbar_arrive_e(uint64_t* bar) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+                 "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(g_smem_u32(bar))
+                 : "memory");
+}
+// elected lane: expect `bytes` on bar, then bulk-copy them global -> smem
+__device__ __forceinline__ void g_bulk_load_e(uint32_t dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n\t"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %3, "
+        "[%2];\n\t}" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(g_smem_u32(bar)), "r"(bytes)
+        : "memory");
+}
+
+// ---- plan 1: per-slice column order, sorted by entry count (descending) -----
+// perm[p*kGCols + v] = output column, or -1 past the end; one block per slice.
+__global__ void gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r,
+                                   int32_t* __restrict__ perm) {
+    __shared__ int key[kGCols];
+    const int64_t c0 = (int64_t)blockIdx.x * kGCols;
+    const int nc = (int)(r - c0 < kGCols ? r - c0 : kGCols);
+    for (int v = threadIdx.x; v < kGCols; v += blockDim.x)
+        key[v] = v < nc ? colptr[c0 + v + 1] - colptr[c0 + v] : -1;
+    __syncthreads();
+    for (int v = threadIdx.x; v < kGCols; v += blockDim.x) {
+        const int kv = key[v];
+        int rank = 0;
+        for (int u = 0; u < kGCols; ++u) {
+            const int ku = key[u];
+            rank += (ku > kv) || (ku == kv && u < v);
+        }
+        perm[c0 + rank] = v < nc ? (int32_t)(c0 + v) : -1;
+    }
+}
+
+// ---- plan 2: greedy bank-conflict-free step schedule, one WARP per warp ------
+// sched[(wg*kGTMax + t)*32 + lane] = byte offset into the row buffer (bit 31:
+// negate); tw[wg] = steps (a multiple of 4); fail |= 1 when a column or a
+// warp needs more than kGTMax steps (the caller then keeps K2 v1).
+// Per step: rounds in which every unserved lane proposes the bank of its first
+// unscheduled entry whose bank is still free; per bank the lane with the most
+// remaining entries wins (ties: lower lane).  Then critical lanes (as many
+// remaining entries as the warp maximum) take an entry even if its bank is
+// taken (a 2-way conflict rather than a longer schedule), and lanes left
+// without an entry read a zero word in a distinct free bank.
+__global__ void gather_sched_kernel(const int32_t* __restrict__ colptr,
+                                    const int32_t* __restrict__ entries,
+                                    const int32_t* __restrict__ perm, int nwarps, int64_t n,
+                                    uint32_t* __restrict__ sched, int32_t* __restrict__ tw,
+                                    int32_t* __restrict__ fail) {
+    const int wg = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (wg >= nwarps) return;
+    const uint32_t zero_word = (uint32_t)((n + 31) / 32 * 32);  // 32 zero words after the row
+    const int c = perm[wg * 32 + lane];
+    const int beg = c >= 0 ? colptr[c] : 0;
+    const int cnt = c >= 0 ? colptr[c + 1] - colptr[c] : 0;
+    if (__any_sync(0xffffffffu, cnt > kGTMax)) {
+        if (lane == 0) {
+            atomicOr(fail, 1);
+            tw[wg] = 0;
+        }
+        return;
+    }
+    uint32_t usedm[kGTMax / 32] = {0, 0, 0, 0};  // bit k: entry k already scheduled
+    int rem = cnt;
+    int t = 0;
+    while (__any_sync(0xffffffffu, rem > 0) || (t & 3)) {
+        if (t >= kGTMax) {
+            if (lane == 0) {
+                atomicOr(fail, 1);
+                tw[wg] = 0;
+            }
+            return;
+        }
+        uint32_t taken = 0;
+        bool served = false;
+        uint32_t val = 0;
+        int maxrem = rem;
+        for (int o = 16; o; o >>= 1) maxrem = max(maxrem, __shfl_xor_sync(0xffffffffu, maxrem, o));
+        for (int round = 0; round < 32; ++round) {
+            int pick = -1, bank = -1;
+            if (!served && rem > 0) {
+                for (int k = 0; k < cnt; ++k) {
+                    if ((usedm[k >> 5] >> (k & 31)) & 1) continue;
+                    const int bk = (int)(((uint32_t)entries[beg + k]) & 31u);
+                    if (!((taken >> bk) & 1)) {
+                        pick = k;
+                        bank = bk;
+                        break;
+                    }
+                }
+            }
+            const unsigned grp = __match_any_sync(0xffffffffu, bank);
+            const unsigned key = bank >= 0 ? ((unsigned)rem << 5) | (31u - (unsigned)lane) : 0u;
+            const unsigned best = __reduce_max_sync(grp, key);
+            const bool win = bank >= 0 && key == best;
+            if (win) {
+                const uint32_t v = (uint32_t)entries[beg + pick];
+                usedm[pick >> 5] |= 1u << (pick & 31);
+                --rem;
+                served = true;
+                val = ((v & 0x7fffffffu) * 4u) | (v & 0x80000000u);
+            }
+            const unsigned won = __reduce_or_sync(0xffffffffu, win ? 1u << bank : 0u);
+            if (!won) break;
+            taken |= won;
+        }
+        // critical lanes accept a conflict rather than lengthen the schedule
+        if (!served && rem > 0 && rem >= maxrem) {
+            for (int k = 0; k < cnt; ++k)
+                if (!((usedm[k >> 5] >> (k & 31)) & 1)) {
+                    const uint32_t v = (uint32_t)entries[beg + k];
+                    usedm[k >> 5] |= 1u << (k & 31);
+                    --rem;
+                    served = true;
+                    val = ((v & 0x7fffffffu) * 4u) | (v & 0x80000000u);
+                    taken |= 1u << (v & 31u);
+                    break;
+                }
+        }
+        for (int o = 16; o; o >>= 1) taken |= __shfl_xor_sync(0xffffffffu, taken, o);
+        // unserved lanes: distinct free banks for their zero-word reads
+        const unsigned idle = __ballot_sync(0xffffffffu, !served);
+        if (!served) {
+            const int rank = __popc(idle & ((1u << lane) - 1u));
+            uint32_t freeb = ~taken;
+            int bk = 0;
+            for (int q = 0; q <= rank && freeb; ++q) {
+                bk = __ffs(freeb) - 1;
+                freeb &= freeb - 1;
+            }
+            val = (zero_word + (uint32_t)bk) * 4u;
+        }
+        sched[((int64_t)wg * kGTMax + t) * 32 + lane] = val;
+        ++t;
+    }
+    if (lane == 0) tw[wg] = t;
+}
+
+// ---- the gather ----------------------------------------------------------------
+template <bool kNorms>
+__global__ void __maxnreg__(80)
+sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n, int P,
+                     const uint32_t* __restrict__ sched, const int32_t* __restrict__ tw,
+                     const int32_t* __restrict__ perm, float scale, float* __restrict__ out,
+                     int64_t ldo, double* fro2, int64_t* nonfinite) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * (size_t)kGBufBytes);
+    uint32_t* done = reinterpret_cast<uint32_t*>(full + 2);  // warps finished with a buffer
+    double* red = reinterpret_cast<double*>(full + 4);       // [kGW] per-warp norm partials
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int slice = blockIdx.x % P;
+    const int g = blockIdx.x / P, G = gridDim.x / P;
+    const uint32_t base = g_smem_u32(sm);
+    const uint32_t zero_word = (uint32_t)((n + 31) / 32 * 32);
+    const uint32_t row_bytes = (uint32_t)((n + 3) / 4 * 16);
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            g_mbar_init(&full[b], 1);
+            done[b] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < 64) {  // zero words (targets of idle lanes) of both buffers
+        float* z = reinterpret_cast<float*>(sm + (threadIdx.x >> 5) * (size_t)kGBufBytes);
+        z[zero_word + (threadIdx.x & 31)] = 0.f;
+    }
+    __syncthreads();
+    if (warp == 0) {  // first two rows of this group
+        if (g < m) g_bulk_load_e(base, A + (int64_t)g * lda, row_bytes, &full[0]);
+        if (g + G < m)
+            g_bulk_load_e(base + kGBufBytes, A + (int64_t)(g + G) * lda, row_bytes, &full[1]);
+    }
+
+    // compute warps: this warp's schedule -> registers (absolute smem addresses)
+    const int wg = slice * kGW + warp;
+    const int T = tw[wg];
+    uint32_t e[kGTReg];
+#pragma unroll
+    for (int t = 0; t < kGTReg; ++t) {
+        const uint32_t v =
+            t < T ? __ldg(sched + ((int64_t)wg * kGTMax + t) * 32 + lane) : zero_word * 4u;
+        // (steps >= kGTReg, if any, are read per row below)
+        e[t] = v + base;  // absolute smem address in buffer 0; bit 31 (sign) kept
+    }
+    const int v_out = slice * kGCols + warp * 32 + lane;
+    const bool valid = perm[v_out] >= 0;
+    // norm share of this slice: float4 units [q0, q1) of the row, one per thread
+    const int64_t nq = (n + 3) / 4;
+    const int64_t qper = (nq + P - 1) / P;
+    const int64_t q0 = (int64_t)slice * qper, q1 = q0 + qper < nq ? q0 + qper : nq;
+    double ss = 0.0;
+
+    auto do_row = [&](int64_t i, int b, uint32_t ph, auto boff_c) {
+        constexpr uint32_t boff = decltype(boff_c)::value;
+        g_mbar_wait(&full[b], ph);
+        // opaque per row: stops the compiler from hoisting the per-entry masks
+        // out of the row loop (3x the registers, spills) and orders the loads
+        // below after the wait
+#pragma unroll
+        for (int t = 0; t < kGTReg; ++t) asm volatile("" : "+r"(e[t]));
+        float acc = 0.f;
+#pragma unroll
+        for (int t4 = 0; t4 < kGTReg; t4 += 4) {
+            if (t4 >= T) break;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t ev = e[t4 + u];
+                float x;  // buffer offset as the LDS immediate
+                asm("ld.shared.f32 %0, [%1+%2];" : "=f"(x) : "r"(ev & 0x7fffffffu), "n"(boff));
+                acc += __int_as_float(__float_as_int(x) ^ (int)(ev & 0x80000000u));
+            }
+        }
+        // rare heavy warps: the steps past the register-resident ones stream
+        // from the (L1-resident) schedule
+        for (int t = kGTReg; t < T; ++t) {
+            const uint32_t ev = __ldg(sched + ((int64_t)wg * kGTMax + t) * 32 + lane) + base;
+            float x;
+            asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(x) : "r"(ev & 0x7fffffffu), "n"(boff));
+            acc += __int_as_float(__float_as_int(x) ^ (int)(ev & 0x80000000u));
+        }
+        if (kNorms) {
+            for (int64_t q = q0 + threadIdx.x; q < q1; q += kGCols) {
+                float4 v;
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                             : "r"(base + boff + (uint32_t)q * 16u)
+                             : "memory");
+                const int64_t c = q * 4;
+                ss += (c + 0 < n ? (double)v.x * v.x : 0.0) + (c + 1 < n ? (double)v.y * v.y : 0.0) +
+                      (c + 2 < n ? (double)v.z * v.z : 0.0) + (c + 3 < n ? (double)v.w * v.w : 0.0);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            // the last warp done with this buffer refills it with row i + 2G
+            if (atomicAdd(&done[b], 1u) == kGW - 1) {
+                done[b] = 0;
+                const int64_t nx = i + 2 * (int64_t)G;
+                if (nx < m) {
+                    asm volatile(
+                        "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                            g_smem_u32(&full[b])),
+                        "r"(row_bytes)
+                        : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+                        "[%1], %2, [%3];" ::"r"(base + (uint32_t)b * kGBufBytes),
+                        "l"(reinterpret_cast<uint64_t>(A + nx * lda)), "r"(row_bytes),
+                        "r"(g_smem_u32(&full[b]))
+                        : "memory");
+                }
+            }
+        }
+        if (valid) out[i * ldo + v_out] = acc * scale;
+    };
+
+    int it = 0;
+    for (int64_t i = g; i < m; i += 2 * G, it += 2) {
+        do_row(i, 0, (uint32_t)((it >> 1) & 1), std::integral_constant<uint32_t, 0>());
+        if (i + G < m)
+            do_row(i + G, 1, (uint32_t)((it >> 1) & 1),
+                   std::integral_constant<uint32_t, kGBufBytes>());
+    }
+
+    if (kNorms) {
+        // ss is finite iff every entry of the share is (squares in fp64 cannot overflow)
+        for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (lane == 0) red[warp] = ss;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < kGW; ++w) tot += red[w];
+            if (fro2) atomicAdd(fro2, tot);
+            if (nonfinite && !isfinite(tot)) atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), 1ull);
+        }
+    }
+}
+
+}  // namespace
+
+// plan layout (bytes): perm int32[P*kGCols] | tw int32[P*kGW] | fail int32 |
+//                      pad to 16 | sched uint32[P*kGW*kGTMax*32]
+int gather_slices(int64_t r) { return (int)cdiv(r, (int64_t)kGCols); }
+int64_t gather_plan_bytes(int64_t r) {
+    const int64_t P = gather_slices(r);
+    const int64_t head = (P * kGCols + P * kGW + 1) * 4;
+    return (head + 15) / 16 * 16 + P * kGW * kGTMax * 32 * 4;
+}
+
+int gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n, int64_t r, void* plan,
+                int64_t plan_bytes, cudaStream_t st) {
+    SKP_ARG(n >= 1 && r >= 1 && plan, "sketch_gather_plan: bad sizes");
+    SKP_ARG(plan_bytes >= gather_plan_bytes(r), "sketch_gather_plan: plan buffer too small");
+    if (n > kGBufWords - 32) {
+        set_error("unsupported: sketch_gather needs n <= %d", kGBufWords - 32);
+        return SKP_ERR_UNSUPPORTED;
+    }
+    const int P = gather_slices(r);
+    int32_t* perm = reinterpret_cast<int32_t*>(plan);
+    int32_t* tw = perm + (int64_t)P * kGCols;
+    int32_t* fail = tw + (int64_t)P * kGW;
+    const int64_t head = ((int64_t)P * kGCols + P * kGW + 1) * 4;
+    uint32_t* sched =
+        reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(plan) + (head + 15) / 16 * 16);
+    SKP_CUDA(cudaMemsetAsync(fail, 0, 4, st));
+    gather_sort_kernel<<<P, 256, 0, st>>>(colptr, r, perm);
+    SKP_LAUNCHED(gather_sort_kernel);
+    const int nw = P * kGW;
+    gather_sched_kernel<<<(unsigned)cdiv(nw, 4), 128, 0, st>>>(colptr, entries, perm, nw, n,
+                                                                sched, tw, fail);
+    SKP_LAUNCHED(gather_sched_kernel);
+    return SKP_OK;
+}
+
+int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
+                      const void* plan, float scale, float* out, int64_t ldo, double* fro2,
+                      int64_t* nonfinite, cudaStream_t st) {
+    SKP_ARG(m >= 0 && n >= 1 && r >= 1 && ldo >= r, "sketch_gather: bad sizes");
+    if (n > kGBufWords - 32 || (reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3) ||
+        lda < (n + 3) / 4 * 4) {
+        set_error("unsupported: sketch_gather needs n <= %d and 16-byte aligned, padded rows",
+                  kGBufWords - 32);
+        return SKP_ERR_UNSUPPORTED;
+    }
+    if (m == 0) return SKP_OK;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int P = gather_slices(r);
+    const int G = std::max(1, std::min<int>(sms / P, (int)std::min<int64_t>(m, 1 << 20)));
+    const int32_t* perm = reinterpret_cast<const int32_t*>(plan);
+    const int32_t* tw = perm + (int64_t)P * kGCols;
+    const int64_t head = ((int64_t)P * kGCols + P * kGW + 1) * 4;
+    const uint32_t* sched = reinterpret_cast<const uint32_t*>(
+        reinterpret_cast<const char*>(plan) + (head + 15) / 16 * 16);
+    const bool norms = fro2 || nonfinite;
+    if (norms) {
+        SKP_CUDA(cudaFuncSetAttribute(sketch_gather_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
+        sketch_gather_kernel<true><<<G * P, kGThreads, kGSmem, st>>>(
+            A, lda, m, n, P, sched, tw, perm, scale, out, ldo, fro2, nonfinite);
+    } else {
+        SKP_CUDA(cudaFuncSetAttribute(sketch_gather_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
+        sketch_gather_kernel<false><<<G * P, kGThreads, kGSmem, st>>>(
+            A, lda, m, n, P, sched, tw, perm, scale, out, ldo, fro2, nonfinite);
+    }
+    SKP_LAUNCHED(sketch_gather_kernel);
+    return SKP_OK;
+}
+
+}  // namespace skp
+
+using namespace skp;
+
+extern "C" int64_t skp_sketch_gather_plan_bytes(int64_t r) { return gather_plan_bytes(r); }
+extern "C" int64_t skp_sketch_gather_plan_fail_offset(int64_t r) {
+    const int64_t P = gather_slices(r);
+    return (P * kGCols + P * kGW) * 4;
+}
+extern "C" int skp_sketch_gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n,
+                                      int64_t r, void* plan, int64_t plan_bytes, void* stream) {
+    return gather_plan(colptr, entries, n, r, plan, plan_bytes, (cudaStream_t)stream);
+}
+extern "C" int skp_sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
+                                     const void* plan, float scale, float* out, int64_t ldo,
+                                     double* fro2, int64_t* nonfinite, void* stream) {
+    return sketch_gather_f32(A, lda, m, n, r, plan, scale, out, ldo, fro2, nonfinite,
+                             (cudaStream_t)stream);
+}

@@ -224,17 +224,39 @@ sketch_rows_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n, i
         }
         const int4* rec = ell_s + b * SW + cl0;
         const int32_t* ovk = ovf_s + b * C::OVMAX;
+        // columns in batches of KB: all record loads, then all slot loads, no
+        // per-column branch (ILP across columns); unused slots (zero row) are
+        // predicated off so they cost no shared-memory wavefront; the rare
+        // >3-entry overflow is one warp-uniform check per batch
+        constexpr int KB = 4;
+        const int zo = (int)C::zero_off;
 #pragma unroll
-        for (int kc = 0; kc < CW; ++kc) {
-            const int4 d = rec[kc];
-            T a = lds_t<T>(x_base + (uint32_t)d.x) + lds_t<T>(x_base + (uint32_t)d.y) +
-                  lds_t<T>(x_base + (uint32_t)d.z);
-            if (d.w) {
-                const int o = d.w & 0xffff, e = o + (d.w >> 16);
-#pragma unroll 1
-                for (int i = o; i < e; ++i) a += lds_t<T>(x_base + (uint32_t)ovk[i]);
+        for (int kb0 = 0; kb0 < CW; kb0 += KB) {
+            int4 d[KB];
+#pragma unroll
+            for (int i = 0; i < KB; ++i) d[i] = rec[kb0 + i];
+            int ovf_any = 0;
+#pragma unroll
+            for (int i = 0; i < KB; ++i) {
+                T a = T(0);
+                if (d[i].x != zo) a += lds_t<T>(x_base + (uint32_t)d[i].x);
+                if (d[i].y != zo) a += lds_t<T>(x_base + (uint32_t)d[i].y);
+                if (d[i].z != zo) a += lds_t<T>(x_base + (uint32_t)d[i].z);
+                acc[kb0 + i] += a;
+                ovf_any |= d[i].w;
             }
-            acc[kc] += a;
+            if (ovf_any) {
+#pragma unroll
+                for (int i = 0; i < KB; ++i) {
+                    if (d[i].w) {
+                        const int o = d[i].w & 0xffff, e = o + (d[i].w >> 16);
+                        T a = T(0);
+#pragma unroll 1
+                        for (int t = o; t < e; ++t) a += lds_t<T>(x_base + (uint32_t)ovk[t]);
+                        acc[kb0 + i] += a;
+                    }
+                }
+            }
         }
         __syncthreads();
     }

@@ -627,6 +627,17 @@ __global__ void cast2d_kernel(const S* __restrict__ x, int64_t ldx, D* __restric
     }
 }
 
+// y[v, :] = x[perm[v], :] (row gather; one block-row per output row)
+template <typename T>
+__global__ void permute_rows_kernel(const T* __restrict__ x, int64_t ldx, const int32_t* __restrict__ perm,
+                                    T* __restrict__ y, int64_t ldy, int64_t rows, int64_t cols) {
+    for (int64_t v = blockIdx.x; v < rows; v += gridDim.x) {
+        const T* src = x + (int64_t)perm[v] * ldx;
+        T* dst = y + v * ldy;
+        for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) dst[j] = src[j];
+    }
+}
+
 template <typename T>
 __global__ void symmetrize_kernel(T* W, int64_t n, int64_t ld) {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * n;
@@ -893,6 +904,25 @@ extern "C" int skp_cast2d_f32_f64(const float* x, int64_t ldx, double* y, int64_
         x, ldx, y, ldy, rows, cols);
     SKP_LAUNCHED(cast2d);
     return SKP_OK;
+}
+template <typename T>
+static int permute_rows(const T* x, int64_t ldx, const int32_t* perm, T* y, int64_t ldy,
+                        int64_t rows, int64_t cols, void* stream) {
+    SKP_ARG(rows >= 0 && cols >= 0 && ldx >= cols && ldy >= cols, "permute_rows: bad sizes");
+    if (!rows || !cols) return SKP_OK;
+    const int64_t grid = rows < 65535 ? rows : 65535;
+    permute_rows_kernel<T><<<(unsigned)grid, 128, 0, SKP_STREAM(stream)>>>(x, ldx, perm, y, ldy,
+                                                                           rows, cols);
+    SKP_LAUNCHED(permute_rows);
+    return SKP_OK;
+}
+extern "C" int skp_permute_rows_f32(const float* x, int64_t ldx, const int32_t* perm, float* y,
+                                    int64_t ldy, int64_t rows, int64_t cols, void* stream) {
+    return permute_rows<float>(x, ldx, perm, y, ldy, rows, cols, stream);
+}
+extern "C" int skp_permute_rows_f64(const double* x, int64_t ldx, const int32_t* perm, double* y,
+                                    int64_t ldy, int64_t rows, int64_t cols, void* stream) {
+    return permute_rows<double>(x, ldx, perm, y, ldy, rows, cols, stream);
 }
 extern "C" int skp_cast2d_f64_f32(const double* x, int64_t ldx, float* y, int64_t ldy,
                                   int64_t rows, int64_t cols, void* stream) {

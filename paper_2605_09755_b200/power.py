@@ -25,7 +25,7 @@ import torch
 from . import _convert, _engine, _ops
 from ._ops import F32, F64
 from .linalg import SvdResult, _pinv_dev
-from .sketching import make_sketch, omega_tensor, substream
+from .sketching import OmegaDraw, make_sketch, omega_tensor, substream
 
 
 def choose_q(eps: float, m_hat: int) -> int:
@@ -136,14 +136,22 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     m_loc, n = a.shape
     be = _be(a.dtype, dev)
     ph.mark("start")
+    # the host-side Omega draw (numpy ziggurat, bit-identical to the reference)
+    # runs on a thread while the device executes K1 + K2
+    om_job = OmegaDraw(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), a.dtype)
     sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
     ph.mark("make_sketch")
     nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
-    atil = sk.right(a, fro2=fro2, nonfinite=nonfinite)
+    # K2 v2 writes A~ with its columns permuted (A S P); the power iteration
+    # then uses P^T Omega, so Y = (A S P)(P^T Omega) = A S Omega exactly as in
+    # the reference.  K2 v1 (natural column order) where v2 does not apply.
+    got = sk.right_permuted(a, fro2=fro2, nonfinite=nonfinite)
+    if got is not None:
+        atil, perm = got
+    else:
+        atil, perm = sk.right(a, fro2=fro2, nonfinite=nonfinite), None
     ph.mark("apply_right")
-    # the host-side Omega draw (numpy ziggurat, bit-identical to the reference)
-    # runs while the device executes K1 + K2 queued above
-    omega = omega_tensor(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), a.dtype, dev)
+    omega = om_job.to_device(dev, perm)
     ph.mark("omega")
     bad = comm.allreduce_(nonfinite)
     # Fast path: no host synchronisation until the end -- CholeskyQR failures

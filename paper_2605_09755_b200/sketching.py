@@ -16,6 +16,7 @@ Mirrors /root/reference/pkg/src/skpower/sketching.py: ``SketchOperator``
 from __future__ import annotations
 
 import math
+import threading
 
 import numpy as np
 import torch
@@ -122,6 +123,28 @@ class SketchOperator:
             return a.clone() if out is None else out.copy_(a)
         return _ops.gemm(a, self._dense(a.dtype), out=out)
 
+    def gather_plan(self):
+        """Cached K2 v2 plan (plan, perm) for this countsketch, or None."""
+        if self.kind != "countsketch":
+            return None
+        if not hasattr(self, "_gather"):
+            self._gather = _ops.gather_plan(self.colptr, self.entries, self.n, self.r, self.device)
+        return self._gather
+
+    def right_permuted(self, a: torch.Tensor, out=None, fro2=None, nonfinite=None):
+        """(a @ S P, perm) with perm[v] (int32, on the device) = the column of
+        a @ S at position v, via the row-gather kernel (fp32, n <= 24576); None
+        when it does not apply.
+        Range-finder use: (a S P)(P^T Omega) == (a S) Omega."""
+        if a.dtype != torch.float32 or (a.stride(0) * 4) % 16 or a.data_ptr() % 16:
+            return None
+        plan = self.gather_plan()
+        if plan is None:
+            return None
+        g, _ = plan
+        perm_dev = g[:4 * self.r].view(torch.int32)   # the first r entries are the valid ones
+        return _ops.sketch_gather(a, g, self.r, self.s, out, fro2, nonfinite), perm_dev
+
     def left_t(self, x: torch.Tensor, out=None) -> torch.Tensor:
         if self.kind == "countsketch":
             return _ops.sketch_left_t(x, self.colptr, self.entries, self.s, self.r, out)
@@ -193,9 +216,45 @@ def draw_omega(kind: str, rows: int, cols: int, seed: int) -> np.ndarray:
     raise ValueError(f"unsupported omega kind {kind!r} on the B200 path")
 
 
-def omega_tensor(kind: str, rows: int, cols: int, seed: int, dtype, device) -> torch.Tensor:
-    """Omega on the device with 16-byte-aligned rows (TMA operand)."""
+class OmegaDraw:
+    """The host-side Omega draw (numpy, bit-identical to the reference) on a
+    background thread -- numpy's generator fills release the GIL -- so it
+    overlaps the device's sketch; to_device() joins, uploads (pinned,
+    asynchronous) and optionally applies P^T on the device."""
+
+    def __init__(self, kind: str, rows: int, cols: int, seed: int, dtype):
+        self.rows, self.cols, self.dtype = rows, cols, dtype
+        self._host = None
+        self._err = None
+        self._t = threading.Thread(target=self._run, args=(kind, seed), daemon=True)
+        self._t.start()
+
+    def _run(self, kind, seed):
+        try:
+            om = draw_omega(kind, self.rows, self.cols, seed)
+            host = torch.from_numpy(om.astype(np.float32) if self.dtype == F32 else om)
+            self._host = host.pin_memory() if self.rows * self.cols > 1 << 16 else host
+        except BaseException as e:  # re-raised on the caller's thread
+            self._err = e
+
+    def to_device(self, device, perm_dev: torch.Tensor | None = None) -> torch.Tensor:
+        self._t.join()
+        if self._err is not None:
+            raise self._err
+        out = _ops.empty2d(self.rows, self.cols, self.dtype, device)
+        out.copy_(self._host, non_blocking=True)
+        if perm_dev is not None:
+            out = _ops.permute_rows(out, perm_dev)
+        return out
+
+
+def omega_tensor(kind: str, rows: int, cols: int, seed: int, dtype, device,
+                 row_perm: np.ndarray | None = None) -> torch.Tensor:
+    """Omega on the device with 16-byte-aligned rows (TMA operand); with
+    row_perm, P^T Omega (rows reordered on the host before the upload)."""
     om = draw_omega(kind, rows, cols, seed)
+    if row_perm is not None:
+        om = om[row_perm]
     out = _ops.empty2d(rows, cols, dtype, device)
     host = torch.from_numpy(om.astype(np.float32) if dtype == F32 else om)
     if rows * cols > 1 << 16:

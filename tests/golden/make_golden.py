@@ -46,6 +46,9 @@ SMALL_CS = [  # (n, r, s, seed)
     (1000, 200, 8, None),  # C1 primary sketch: seed = substream(1, 0)
     (1000, 3_000_000_000, 1, 17),  # s=1 with frequent Lemire rejections
     (64, 64, 64, 3), (50, 40, 33, 8), (33, 1000, 17, 12),
+    # s=1 with an odd number of 32-bit column draws: the first sign is the
+    # high half PCG64 kept buffered from the column phase
+    (513, 64, 1, 13), (1025, 64, 1, 5), (7, 3, 1, 1), (999, 37, 1, 77), (2049, 2, 1, 10),
 ]
 # BASELINE config shapes; seed = substream(config spec seed, 0)
 BIG_CS = {

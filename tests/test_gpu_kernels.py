@@ -57,12 +57,17 @@ def test_countsketch_config_shapes_golden(skp, golden, name):
 @pytest.mark.parametrize("n,r,s,seed", [
     (1, 1, 1, 0), (1, 5, 5, 3), (37, 1, 1, 4), (100, 3, 2, 5), (513, 1000, 7, 6),
     (64, 1025, 32, 7), (333, 31, 31, 8), (1000, 1_500_000_000, 1, 9), (2049, 2, 1, 10),
-    (3000, 129, 1, 11), (40, 33, 9, 12)])
+    (3000, 129, 1, 11), (40, 33, 9, 12), (513, 64, 1, 13), (1025, 4000, 1, 5),
+    (16385, 4000, 1, 2), (999, 37, 1, 77)])
 def test_countsketch_random_vs_c_oracle(skp, n, r, s, seed):
     op = skp.make_sketch("countsketch", n, r, seed, s=s)
     cols, signs = o.countsketch_c(seed, n, r, s)
     np.testing.assert_array_equal(op._cols, cols)
     np.testing.assert_array_equal(op._signs, signs)
+    if r < 10**6 and n * r < 10**7:   # and numpy itself (the reference's generator)
+        cn, sn = o.countsketch_numpy(seed, n, r, s)
+        np.testing.assert_array_equal(op._cols, cn)
+        np.testing.assert_array_equal(op._signs, sn)
 
 
 @pytest.mark.parametrize("s", [1, 3, 8])
@@ -136,6 +141,76 @@ def test_sketch_fused_norm_and_nonfinite(skp, ops):
         fro2.zero_()
         op.right(torch.from_numpy(a).cuda(), fro2=fro2)
         assert abs(fro2.item() - float((a.astype(np.float64) ** 2).sum())) <= 1e-9 * fro2.item()
+
+
+@pytest.mark.parametrize("m,n,r,s", [(67, 16384, 4000, 8), (5, 1000, 300, 8), (130, 513, 64, 1),
+                                     (40, 2050, 1600, 3), (1, 24576, 4000, 8)])
+def test_sketch_gather_permuted(skp, ops, m, n, r, s):
+    """K2 v2: (A S) P from the row-gather kernel == the oracle's A S with its
+    columns taken in plan order; fused fp64 ||A||_F^2 and the non-finite test."""
+    rng = np.random.default_rng(n + r)
+    op = skp.make_sketch("countsketch", n, r, seed=13, s=s)
+    plan = op.gather_plan()
+    assert plan is not None
+    g, perm = plan
+    assert sorted(perm.tolist()) == list(range(r))      # a permutation of the columns
+    a = rng.standard_normal((m, n)).astype(np.float32)
+    t = ops.empty2d(m, n, torch.float32, "cuda")
+    t.copy_(torch.from_numpy(a))
+    fro2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out, perm2 = op.right_permuted(t, fro2=fro2, nonfinite=bad)
+    assert (perm2.cpu().numpy() == perm).all()
+    ref = o.CountSketch("countsketch", n, r, 13, s=s).apply_right(a.astype(np.float64))
+    got = out.cpu().numpy().astype(np.float64)
+    scale = np.abs(ref).max()
+    assert np.abs(got - ref[:, perm]).max() <= 4e-7 * np.sqrt(n * s / r) * scale + 1e-30
+    assert int(bad.item()) == 0
+    want = float((a.astype(np.float64) ** 2).sum())
+    assert abs(fro2.item() - want) <= 1e-12 * want
+    # a single non-finite entry is reported
+    a[m // 2, n // 3] = np.nan
+    t.copy_(torch.from_numpy(a))
+    bad.zero_()
+    op.right_permuted(t, nonfinite=bad)
+    assert int(bad.item()) >= 1
+
+
+def test_sketch_gather_declines_outside_its_envelope(skp, ops):
+    """No plan (and right_permuted -> None, the caller keeps K2 v1) when rows do
+    not fit the smem row buffer or a column needs more than 128 steps."""
+    assert skp.make_sketch("countsketch", 24577, 4000, seed=1, s=8).gather_plan() is None
+    op = skp.make_sketch("countsketch", 4096, 64, seed=1, s=8)     # ~512 entries per column
+    assert op.gather_plan() is None
+    t = ops.empty2d(3, 4096, torch.float32, "cuda").zero_()
+    assert op.right_permuted(t) is None
+    assert op.right_permuted(t.double()) is None
+
+
+def test_sketch_gather_range_finder_matches_v1(skp, ops, monkeypatch):
+    """The range finder on (A S P, P^T Omega) (K2 v2) gives the same sigma and
+    projection error as on (A S, Omega) (K2 v1): both fp32 on the device, they
+    differ only in the sketch's summation order."""
+    from paper_2605_09755_b200 import sketching
+    rng = np.random.default_rng(5)
+    m, n = 600, 3000
+    u = np.linalg.qr(rng.standard_normal((m, 40)))[0]
+    v = np.linalg.qr(rng.standard_normal((n, 40)))[0]
+    # noise floor ~8% of sigma_1: inside the fp32 CholeskyQR envelope (DESIGN.md)
+    a = ((u * np.logspace(0, -1, 40)) @ v.T + 1e-3 * rng.standard_normal((m, n))).astype(np.float32)
+    spec = skp.RangeFinderSpec(k=20, l=400, r1=400, r2=60, q=2, eps=0.5, s=8, seed=9)
+    assert skp.make_sketch("countsketch", n, 400, seed=0, s=8).gather_plan() is not None
+    q2 = skp.range_finder_sketched(a, spec)                       # K2 v2
+    monkeypatch.setattr(sketching.SketchOperator, "right_permuted", lambda *x, **k: None)
+    q1 = skp.range_finder_sketched(a, spec)                       # K2 v1
+    a64 = a.astype(np.float64)
+    s1 = np.linalg.svd(q1.T.astype(np.float64) @ a64, compute_uv=False)
+    s2 = np.linalg.svd(q2.T.astype(np.float64) @ a64, compute_uv=False)
+    assert np.abs(s1[:20] - s2[:20]).max() <= 2e-6 * s1[0]
+    e1, e2 = o.proj_rel_error(a64, q1.astype(np.float64)), o.proj_rel_error(a64, q2.astype(np.float64))
+    ref = o.range_finder_sketched(a, o.Spec(k=20, l=400, r1=400, r2=60, q=2, s=8, seed=9))
+    e0 = o.proj_rel_error(a64, ref)
+    assert abs(e2 - e1) <= 1e-4 * e1 and abs(e2 - e0) <= 1e-3 * e0
 
 
 def test_sketch_dimension_mismatch(skp):
