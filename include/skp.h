@@ -92,7 +92,10 @@ int skp_sketch_right_f64(const double* A, int64_t lda, int64_t m, int64_t n,
  * by entry count; its table is plan[0 .. slices*768) (int32 column of S, -1
  * past r).  Build the plan once per sketch (skp_sketch_gather_plan, from the
  * CSC view); it is usable iff the int32 at byte offset
- * skp_sketch_gather_plan_fail_offset(r) is 0 after the build.  Requires
+ * skp_sketch_gather_plan_fail_offset(r) is 0 after the build -- or, without a
+ * host check, run skp_sketch_gather_f32 anyway: with a failed plan it writes
+ * nothing and adds 2^40 to *nonfinite (the caller then uses skp_sketch_right).
+ * Requires
  * n <= 24576 and 16-byte aligned rows padded to a multiple of 4 floats;
  * returns SKP_ERR_UNSUPPORTED otherwise (callers keep skp_sketch_right).
  * Replaces the same `a @ self._sparse` (sketching.py:158-164) inside

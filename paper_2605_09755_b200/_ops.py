@@ -136,11 +136,17 @@ def sketch_right(a: torch.Tensor, colptr, entries, s: int, r: int, out=None, fro
 GATHER_COLS = 768  # output columns per slice of the K2 v2 plan (sketch_gather.cu)
 
 
-def gather_plan(colptr, entries, n: int, r: int, device):
-    """K2 v2 plan (once per sketch): (plan bytes on the device, perm) where
-    perm[v] = the column of S written at position v by sketch_gather; None when
-    the shape is outside the kernel (n > 24576, or a column / warp needing more
-    than 56 schedule steps) -- the caller then keeps sketch_right."""
+GATHER_PLAN_FAIL_MARK = 1 << 40   # added to the non-finite counter by a failed plan
+
+
+def gather_plan(colptr, entries, n: int, r: int, device, check: bool = True):
+    """K2 v2 plan (once per sketch): (plan bytes on the device, perm or None).
+
+    None when the shape is outside the kernel (n > 24576).  With check=True the
+    schedule is verified on the host (one sync; None if a column / warp needs
+    more than 128 steps) and perm[v] (numpy) = the column written at position v.
+    With check=False nothing is read back: a failed schedule surfaces as
+    GATHER_PLAN_FAIL_MARK in the non-finite counter of sketch_gather."""
     lib = _lib.load()
     nb = int(lib.skp_sketch_gather_plan_bytes(r))
     plan = torch.empty(nb, dtype=torch.uint8, device=device)
@@ -149,13 +155,19 @@ def gather_plan(colptr, entries, n: int, r: int, device):
     if rc == _lib.SKP_ERR_UNSUPPORTED:
         return None
     _lib.check(rc, "skp_sketch_gather_plan")
-    off = int(lib.skp_sketch_gather_plan_fail_offset(r))
+    if not check:
+        return plan, None
+    return gather_plan_checked(plan, r)
+
+
+def gather_plan_checked(plan: torch.Tensor, r: int):
+    """(plan, perm) after the host check of a built plan, or None if it failed."""
+    off = int(_lib.load().skp_sketch_gather_plan_fail_offset(r))
     if int(plan[off:off + 4].view(torch.int32).item()) != 0:
         return None
     nslice = -(-r // GATHER_COLS)
     perm = plan[:nslice * GATHER_COLS * 4].view(torch.int32).cpu().numpy()
-    perm = perm[perm >= 0].astype(np.int64)
-    return plan, perm
+    return plan, perm[perm >= 0].astype(np.int64)
 
 
 def sketch_gather(a: torch.Tensor, plan: torch.Tensor, r: int, s: int, out=None, fro2=None,

@@ -47,6 +47,7 @@ constexpr int kGCols = kGW * 32;          // output columns per slice
 constexpr int kGThreads = 32 * kGW;
 constexpr int kGTReg = 56;                // schedule steps held in registers
 constexpr int kGTMax = 128;               // schedule steps per warp (the rest: L1/global)
+constexpr unsigned long long kGPlanFailMark = 1ull << 40;  // added to *nonfinite
 constexpr int kGBufWords = 24608;         // row buffer: n <= 24576 floats + 32 zero words
 constexpr uint32_t kGBufBytes = kGBufWords * 4;  // 98432, a multiple of 128
 constexpr size_t kGSmem = 2 * (size_t)kGBufBytes + 32 + kGW * 8;
@@ -123,11 +124,11 @@ __global__ void gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r
 // remaining entries as the warp maximum) take an entry even if its bank is
 // taken (a 2-way conflict rather than a longer schedule), and lanes left
 // without an entry read a zero word in a distinct free bank.
-__global__ void gather_sched_kernel(const int32_t* __restrict__ colptr,
-                                    const int32_t* __restrict__ entries,
-                                    const int32_t* __restrict__ perm, int nwarps, int64_t n,
-                                    uint32_t* __restrict__ sched, int32_t* __restrict__ tw,
-                                    int32_t* __restrict__ fail) {
+__global__ void __launch_bounds__(128)
+gather_sched_kernel(const int32_t* __restrict__ colptr, const int32_t* __restrict__ entries,
+                    const int32_t* __restrict__ perm, int nwarps, int64_t n,
+                    uint32_t* __restrict__ sched, int32_t* __restrict__ tw,
+                    int32_t* __restrict__ fail) {
     const int wg = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (wg >= nwarps) return;
@@ -142,8 +143,35 @@ __global__ void gather_sched_kernel(const int32_t* __restrict__ colptr,
         }
         return;
     }
-    uint32_t usedm[kGTMax / 32] = {0, 0, 0, 0};  // bit k: entry k already scheduled
+    // this lane's entries bucketed by bank (counting sort, local memory)
+    uint32_t ent[kGTMax];
+    uint8_t bstart[33], bptr[32];
+    {
+        uint8_t bc[32];
+        for (int b = 0; b < 32; ++b) bc[b] = 0;
+        for (int k = 0; k < cnt; ++k) ++bc[(uint32_t)entries[beg + k] & 31u];
+        int acc = 0;
+        for (int b = 0; b < 32; ++b) {
+            bstart[b] = (uint8_t)acc;
+            bptr[b] = (uint8_t)acc;
+            acc += bc[b];
+        }
+        bstart[32] = (uint8_t)acc;
+        for (int k = 0; k < cnt; ++k) {
+            const uint32_t v = (uint32_t)entries[beg + k];
+            ent[bptr[v & 31u]++] = v;
+        }
+        for (int b = 0; b < 32; ++b) bptr[b] = bstart[b];
+    }
+    uint32_t avail = 0;  // banks with an unscheduled entry
+    for (int b = 0; b < 32; ++b) avail |= (bstart[b + 1] > bstart[b] ? 1u : 0u) << b;
     int rem = cnt;
+    auto take = [&](int bk) -> uint32_t {
+        const uint32_t v = ent[bptr[bk]++];
+        if (bptr[bk] == bstart[bk + 1]) avail &= ~(1u << bk);
+        --rem;
+        return ((v & 0x7fffffffu) * 4u) | (v & 0x80000000u);
+    };
     int t = 0;
     while (__any_sync(0xffffffffu, rem > 0) || (t & 3)) {
         if (t >= kGTMax) {
@@ -159,28 +187,15 @@ __global__ void gather_sched_kernel(const int32_t* __restrict__ colptr,
         int maxrem = rem;
         for (int o = 16; o; o >>= 1) maxrem = max(maxrem, __shfl_xor_sync(0xffffffffu, maxrem, o));
         for (int round = 0; round < 32; ++round) {
-            int pick = -1, bank = -1;
-            if (!served && rem > 0) {
-                for (int k = 0; k < cnt; ++k) {
-                    if ((usedm[k >> 5] >> (k & 31)) & 1) continue;
-                    const int bk = (int)(((uint32_t)entries[beg + k]) & 31u);
-                    if (!((taken >> bk) & 1)) {
-                        pick = k;
-                        bank = bk;
-                        break;
-                    }
-                }
-            }
+            const uint32_t cand = served ? 0u : (avail & ~taken);
+            const int bank = cand ? __ffs(cand) - 1 : -1;
             const unsigned grp = __match_any_sync(0xffffffffu, bank);
             const unsigned key = bank >= 0 ? ((unsigned)rem << 5) | (31u - (unsigned)lane) : 0u;
             const unsigned best = __reduce_max_sync(grp, key);
             const bool win = bank >= 0 && key == best;
             if (win) {
-                const uint32_t v = (uint32_t)entries[beg + pick];
-                usedm[pick >> 5] |= 1u << (pick & 31);
-                --rem;
+                val = take(bank);
                 served = true;
-                val = ((v & 0x7fffffffu) * 4u) | (v & 0x80000000u);
             }
             const unsigned won = __reduce_or_sync(0xffffffffu, win ? 1u << bank : 0u);
             if (!won) break;
@@ -188,16 +203,10 @@ __global__ void gather_sched_kernel(const int32_t* __restrict__ colptr,
         }
         // critical lanes accept a conflict rather than lengthen the schedule
         if (!served && rem > 0 && rem >= maxrem) {
-            for (int k = 0; k < cnt; ++k)
-                if (!((usedm[k >> 5] >> (k & 31)) & 1)) {
-                    const uint32_t v = (uint32_t)entries[beg + k];
-                    usedm[k >> 5] |= 1u << (k & 31);
-                    --rem;
-                    served = true;
-                    val = ((v & 0x7fffffffu) * 4u) | (v & 0x80000000u);
-                    taken |= 1u << (v & 31u);
-                    break;
-                }
+            const int bk = __ffs(avail) - 1;
+            val = take(bk);
+            served = true;
+            taken |= 1u << bk;
         }
         for (int o = 16; o; o >>= 1) taken |= __shfl_xor_sync(0xffffffffu, taken, o);
         // unserved lanes: distinct free banks for their zero-word reads
@@ -223,9 +232,17 @@ template <bool kNorms>
 __global__ void __maxnreg__(80)
 sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n, int P,
                      const uint32_t* __restrict__ sched, const int32_t* __restrict__ tw,
-                     const int32_t* __restrict__ perm, float scale, float* __restrict__ out,
-                     int64_t ldo, double* fro2, int64_t* nonfinite) {
+                     const int32_t* __restrict__ perm, const int32_t* __restrict__ plan_fail,
+                     float scale, float* __restrict__ out, int64_t ldo, double* fro2,
+                     int64_t* nonfinite) {
     extern __shared__ __align__(128) unsigned char sm[];
+    if (*plan_fail) {
+        // the plan's schedule overflowed: report it through the non-finite
+        // counter (the caller re-runs with K2 v1; no host sync at plan time)
+        if (blockIdx.x == 0 && threadIdx.x == 0 && nonfinite)
+            atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), kGPlanFailMark);
+        return;
+    }
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * (size_t)kGBufBytes);
     uint32_t* done = reinterpret_cast<uint32_t*>(full + 2);  // warps finished with a buffer
     double* red = reinterpret_cast<double*>(full + 4);       // [kGW] per-warp norm partials
@@ -414,6 +431,7 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
     const int G = std::max(1, std::min<int>(sms / P, (int)std::min<int64_t>(m, 1 << 20)));
     const int32_t* perm = reinterpret_cast<const int32_t*>(plan);
     const int32_t* tw = perm + (int64_t)P * kGCols;
+    const int32_t* pfail = tw + (int64_t)P * kGW;
     const int64_t head = ((int64_t)P * kGCols + P * kGW + 1) * 4;
     const uint32_t* sched = reinterpret_cast<const uint32_t*>(
         reinterpret_cast<const char*>(plan) + (head + 15) / 16 * 16);
@@ -422,12 +440,12 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
         SKP_CUDA(cudaFuncSetAttribute(sketch_gather_kernel<true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
         sketch_gather_kernel<true><<<G * P, kGThreads, kGSmem, st>>>(
-            A, lda, m, n, P, sched, tw, perm, scale, out, ldo, fro2, nonfinite);
+            A, lda, m, n, P, sched, tw, perm, pfail, scale, out, ldo, fro2, nonfinite);
     } else {
         SKP_CUDA(cudaFuncSetAttribute(sketch_gather_kernel<false>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
         sketch_gather_kernel<false><<<G * P, kGThreads, kGSmem, st>>>(
-            A, lda, m, n, P, sched, tw, perm, scale, out, ldo, fro2, nonfinite);
+            A, lda, m, n, P, sched, tw, perm, pfail, scale, out, ldo, fro2, nonfinite);
     }
     SKP_LAUNCHED(sketch_gather_kernel);
     return SKP_OK;

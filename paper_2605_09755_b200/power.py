@@ -17,6 +17,8 @@ events on the launching stream).
 from __future__ import annotations
 
 import math
+import os
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -93,12 +95,14 @@ class _Phases:
     def __init__(self, enabled: bool):
         self.enabled = enabled
         self.ev = []
+        self.host = []
 
     def mark(self, name: str):
         if self.enabled:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
             self.ev.append((name, e))
+            self.host.append(time.perf_counter())
 
     def result(self, out: dict | None, scale: float = 1.0):
         if not self.enabled or out is None:
@@ -106,6 +110,9 @@ class _Phases:
         self.ev[-1][1].synchronize()
         for (_, a), (name, b) in zip(self.ev, self.ev[1:]):
             out[name] = out.get(name, 0.0) + a.elapsed_time(b) * scale
+        if os.environ.get("SKP_HOST_TRACE"):   # debug: host-side time per phase
+            for (name, _), h0, h1 in zip(self.ev[1:], self.host, self.host[1:]):
+                out["host_" + name] = out.get("host_" + name, 0.0) + (h1 - h0) * 1e3 * scale
 
 
 def _be(dtype, device):
@@ -145,7 +152,9 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     # K2 v2 writes A~ with its columns permuted (A S P); the power iteration
     # then uses P^T Omega, so Y = (A S P)(P^T Omega) = A S Omega exactly as in
     # the reference.  K2 v1 (natural column order) where v2 does not apply.
-    got = sk.right_permuted(a, fro2=fro2, nonfinite=nonfinite)
+    # (deferred: no host sync for the plan check; a failed plan shows up as a
+    # marker in the non-finite count checked at the end)
+    got = sk.right_permuted(a, fro2=fro2, nonfinite=nonfinite, deferred=True)
     if got is not None:
         atil, perm = got
     else:
@@ -164,9 +173,19 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     ph.mark("power")
     qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total, lazy=True)
     ph.mark("orth")
-    if int(bad.item()) != 0:
+    nbad = int(bad.item())
+    redo = False
+    if nbad >= _ops.GATHER_PLAN_FAIL_MARK:
+        # K2 v2's schedule overflowed (very uneven sketch columns): K2 v1 in
+        # the natural column order with the unpermuted Omega
+        nonfinite.zero_()
+        atil = sk.right(a, fro2=fro2, nonfinite=nonfinite)
+        nbad = int(comm.allreduce_(nonfinite).item())
+        omega = om_job.to_device(dev, None)
+        redo = True
+    if nbad != 0:
         raise ValueError(f"{name} contains non-finite entries")
-    if be.lazy_failed():
+    if redo or be.lazy_failed():
         y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total)
         qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total)
     return qb

@@ -123,25 +123,35 @@ class SketchOperator:
             return a.clone() if out is None else out.copy_(a)
         return _ops.gemm(a, self._dense(a.dtype), out=out)
 
-    def gather_plan(self):
-        """Cached K2 v2 plan (plan, perm) for this countsketch, or None."""
+    def gather_plan(self, check: bool = True):
+        """Cached K2 v2 plan: (plan, perm) -- perm (numpy) only after the host
+        check -- or None when the kernel does not apply (check=True also
+        returns None for a schedule that overflowed)."""
         if self.kind != "countsketch":
             return None
         if not hasattr(self, "_gather"):
-            self._gather = _ops.gather_plan(self.colptr, self.entries, self.n, self.r, self.device)
+            self._gather = _ops.gather_plan(self.colptr, self.entries, self.n, self.r,
+                                            self.device, check=check)
+        if check and self._gather is not None and self._gather[1] is None:
+            self._gather = _ops.gather_plan_checked(self._gather[0], self.r)
         return self._gather
 
-    def right_permuted(self, a: torch.Tensor, out=None, fro2=None, nonfinite=None):
+    def right_permuted(self, a: torch.Tensor, out=None, fro2=None, nonfinite=None,
+                       deferred: bool = False):
         """(a @ S P, perm) with perm[v] (int32, on the device) = the column of
         a @ S at position v, via the row-gather kernel (fp32, n <= 24576); None
-        when it does not apply.
+        when it does not apply.  deferred=True skips the plan's host check: a
+        failed schedule then adds _ops.GATHER_PLAN_FAIL_MARK to *nonfinite
+        (required) and writes nothing -- the caller falls back to right().
         Range-finder use: (a S P)(P^T Omega) == (a S) Omega."""
         if a.dtype != torch.float32 or (a.stride(0) * 4) % 16 or a.data_ptr() % 16:
             return None
-        plan = self.gather_plan()
+        if deferred and nonfinite is None:
+            raise ValueError("right_permuted(deferred=True) needs the nonfinite counter")
+        plan = self.gather_plan(check=not deferred)
         if plan is None:
             return None
-        g, _ = plan
+        g = plan[0]
         perm_dev = g[:4 * self.r].view(torch.int32)   # the first r entries are the valid ones
         return _ops.sketch_gather(a, g, self.r, self.s, out, fro2, nonfinite), perm_dev
 

@@ -187,6 +187,31 @@ def test_sketch_gather_declines_outside_its_envelope(skp, ops):
     assert op.right_permuted(t.double()) is None
 
 
+def test_sketch_gather_deferred_failure_falls_back(skp, ops):
+    """A plan whose schedule overflows (here ~512 entries per column) is not
+    checked on the host in the range finder: the kernel flags it through the
+    non-finite counter and the range finder re-runs on K2 v1 -- same result as
+    the oracle, and a genuinely non-finite input still raises."""
+    rng = np.random.default_rng(8)
+    m, n = 300, 4096
+    a = (rng.standard_normal((m, 30)) @ rng.standard_normal((30, n))).astype(np.float32)
+    spec = skp.RangeFinderSpec(k=10, l=64, r1=64, r2=20, q=1, eps=0.5, s=8, seed=4)
+    op = skp.make_sketch("countsketch", n, 64, seed=0, s=8)
+    t = ops.empty2d(m, n, torch.float32, "cuda")
+    t.copy_(torch.from_numpy(a))
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    got = op.right_permuted(t, nonfinite=bad, deferred=True)
+    assert got is not None and int(bad.item()) >= ops.GATHER_PLAN_FAIL_MARK
+    q = skp.range_finder_sketched(a, spec)
+    ref = o.range_finder_sketched(a, o.Spec(k=10, l=64, r1=64, r2=20, q=1, s=8, seed=4))
+    a64 = a.astype(np.float64)
+    assert abs(o.proj_rel_error(a64, q.astype(np.float64)) - o.proj_rel_error(a64, ref)) \
+        <= 1e-3 * o.proj_rel_error(a64, ref) + 1e-6
+    a[5, 7] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        skp.range_finder_sketched(a, spec)
+
+
 def test_sketch_gather_range_finder_matches_v1(skp, ops, monkeypatch):
     """The range finder on (A S P, P^T Omega) (K2 v2) gives the same sigma and
     projection error as on (A S, Omega) (K2 v1): both fp32 on the device, they
