@@ -108,6 +108,24 @@ int skp_sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int
                           const void* plan, float scale, float* out, int64_t ldo, double* fro2,
                           int64_t* nonfinite, void* stream);
 
+/* ----------------------------------------------------------- Omega ----
+ * out (rows x cols) = Generator(PCG64 (state, inc)).standard_normal((rows,
+ * cols)) / divisor, computed on the device, cast to fp32 for _f32 -- the
+ * reference's Gaussian start block (power.py:137-138: divisor = sqrt(cols)).
+ * numpy's ziggurat is reproduced draw for draw (the wedge test's exp and the
+ * tail's log1p are CUDA's: ~2^-52 chance per wedge test of a different accept
+ * decision, rare 1-ulp differences in tail values).  A generation that cannot
+ * complete (a tail beyond the tracked window: astronomically rare) writes
+ * nothing and adds 2^50 to *fail_counter (may be NULL).
+ * ws: skp_gaussian_ws_bytes(rows*cols).                                    */
+int64_t skp_gaussian_ws_bytes(int64_t count);
+int skp_gaussian_f32(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
+                     int64_t rows, int64_t cols, double divisor, float* out, int64_t ldo,
+                     int64_t* fail_counter, void* ws, int64_t ws_bytes, void* stream);
+int skp_gaussian_f64(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
+                     int64_t rows, int64_t cols, double divisor, double* out, int64_t ldo,
+                     int64_t* fail_counter, void* ws, int64_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- K3 ----
  * out (r x c) = S^T . X (X n x c); SketchOperator.apply_left_transpose
  * (reference sketching.py:176-182: `self._sparse.T @ a`).                   */

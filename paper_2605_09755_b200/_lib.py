@@ -36,6 +36,11 @@ SIGNATURES = {
                                     _vp, _vp, _vp, _i64, _vp]),
     "skp_sketch_right_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _i64,
                                     _vp, _vp, _vp, _i64, _vp]),
+    "skp_gaussian_ws_bytes": (_i64, [_i64]),
+    "skp_gaussian_f32": (_int, [_u64, _u64, _u64, _u64, _i64, _i64, _f64, _vp, _i64, _vp, _vp,
+                                _i64, _vp]),
+    "skp_gaussian_f64": (_int, [_u64, _u64, _u64, _u64, _i64, _i64, _f64, _vp, _i64, _vp, _vp,
+                                _i64, _vp]),
     "skp_sketch_gather_plan_bytes": (_i64, [_i64]),
     "skp_sketch_gather_plan_fail_offset": (_i64, [_i64]),
     "skp_sketch_gather_plan": (_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),

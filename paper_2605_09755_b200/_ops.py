@@ -183,6 +183,25 @@ def sketch_gather(a: torch.Tensor, plan: torch.Tensor, r: int, s: int, out=None,
     return out
 
 
+OMEGA_FAIL_MARK = 1 << 50   # added to a counter by a device Gaussian draw that failed
+
+
+def gaussian(st: int, inc: int, rows: int, cols: int, divisor: float, dtype, device,
+             fail_counter=None, out=None) -> torch.Tensor:
+    """numpy Generator(PCG64(st, inc)).standard_normal((rows, cols)) / divisor
+    on the device (the reference's Gaussian Omega), fp32 or fp64."""
+    if out is None:
+        out = empty2d(rows, cols, dtype, device)
+    _, _, ldo = _rows_ld(out)
+    lib = _lib.load()
+    wsb = int(lib.skp_gaussian_ws_bytes(rows * cols))
+    ws = workspace(out.device, wsb) if wsb else None
+    m64 = (1 << 64) - 1
+    call(f"skp_gaussian_{_SFX[dtype]}", st >> 64, st & m64, inc >> 64, inc & m64, rows, cols,
+         float(divisor), ptr(out), ldo, ptr(fail_counter), ptr(ws), wsb, stream_ptr(out.device))
+    return out
+
+
 def permute_rows(x: torch.Tensor, perm_dev: torch.Tensor, out=None) -> torch.Tensor:
     """out[v, :] = x[perm_dev[v], :] for v < x.shape[0] (perm_dev: int32 on the device)."""
     rows, cols, ldx = _rows_ld(x)

@@ -11,51 +11,10 @@
 // prefix order on numpy 2.3.5, pinned by tests/golden).
 // Signs kernel: draws n*r ... as 32-bit halves (low first), bit 31 -> +1.
 #include "common.cuh"
+#include "pcg.cuh"
 
 namespace skp {
 namespace {
-
-typedef unsigned __int128 u128;
-
-__host__ __device__ inline u128 mk128(uint64_t hi, uint64_t lo) { return ((u128)hi << 64) | lo; }
-
-struct Jump {  // k steps: x -> m * x + g * inc
-    u128 m, g;
-};
-
-__host__ __device__ inline u128 pcg_mult() {
-    return mk128(2549297995355413924ULL, 4865540595714422341ULL);
-}
-
-__host__ __device__ inline Jump jcompose(Jump a, Jump b) {  // a then b (commutative)
-    Jump r;
-    r.m = a.m * b.m;
-    r.g = b.m * a.g + b.g;
-    return r;
-}
-
-__host__ __device__ inline Jump jpow(uint64_t k) {
-    Jump acc{1, 0}, cur{pcg_mult(), 1};
-    while (k) {
-        if (k & 1) acc = jcompose(acc, cur);
-        cur = jcompose(cur, cur);
-        k >>= 1;
-    }
-    return acc;
-}
-
-struct Affine {  // precombined with inc: x -> m * x + c
-    u128 m, c;
-};
-__host__ __device__ inline Affine affine(Jump j, u128 inc) { return Affine{j.m, j.g * inc}; }
-__host__ __device__ inline u128 apply(Affine a, u128 x) { return a.m * x + a.c; }
-
-__device__ __forceinline__ uint64_t xsl_rr(u128 x) {
-    uint64_t hi = (uint64_t)(x >> 64), lo = (uint64_t)x;
-    unsigned rot = (unsigned)(hi >> 58);
-    uint64_t v = hi ^ lo;
-    return (v >> rot) | (v << ((64u - rot) & 63u));
-}
 
 constexpr int kWarps = 8;  // rows in flight per CTA
 

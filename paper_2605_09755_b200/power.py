@@ -27,7 +27,7 @@ import torch
 from . import _convert, _engine, _ops
 from ._ops import F32, F64
 from .linalg import SvdResult, _pinv_dev
-from .sketching import OmegaDraw, make_sketch, omega_tensor, substream
+from .sketching import OmegaDraw, make_sketch, omega_device, omega_tensor, substream
 
 
 def choose_q(eps: float, m_hat: int) -> int:
@@ -143,9 +143,11 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     m_loc, n = a.shape
     be = _be(a.dtype, dev)
     ph.mark("start")
-    # the host-side Omega draw (numpy ziggurat, bit-identical to the reference)
-    # runs on a thread while the device executes K1 + K2
-    om_job = OmegaDraw(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), a.dtype)
+    # Omega: the Gaussian kind is drawn on the device (omega_device, queued
+    # after K2); the other kinds on a host thread while the device runs K1 + K2
+    om_seed = substream(spec.seed, 1)
+    om_job = None if spec.omega_kind == "gaussian" else \
+        OmegaDraw(spec.omega_kind, spec.r1, spec.r2, om_seed, a.dtype)
     sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
     ph.mark("make_sketch")
     nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -160,7 +162,15 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     else:
         atil, perm = sk.right(a, fro2=fro2, nonfinite=nonfinite), None
     ph.mark("apply_right")
-    omega = om_job.to_device(dev, perm)
+
+    def omega_for(perm_dev, host: bool = False):
+        if om_job is None and not host:
+            return omega_device(spec.omega_kind, spec.r1, spec.r2, om_seed, a.dtype, dev,
+                                perm_dev, nonfinite)
+        job = om_job or OmegaDraw(spec.omega_kind, spec.r1, spec.r2, om_seed, a.dtype)
+        return job.to_device(dev, perm_dev)
+
+    omega = omega_for(perm)
     ph.mark("omega")
     bad = comm.allreduce_(nonfinite)
     # Fast path: no host synchronisation until the end -- CholeskyQR failures
@@ -174,18 +184,22 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total, lazy=True)
     ph.mark("orth")
     nbad = int(bad.item())
-    redo = False
-    if nbad >= _ops.GATHER_PLAN_FAIL_MARK:
+    omega_failed = nbad >= _ops.OMEGA_FAIL_MARK
+    plan_failed = nbad % _ops.OMEGA_FAIL_MARK >= _ops.GATHER_PLAN_FAIL_MARK
+    nbad %= _ops.GATHER_PLAN_FAIL_MARK
+    if plan_failed:
         # K2 v2's schedule overflowed (very uneven sketch columns): K2 v1 in
-        # the natural column order with the unpermuted Omega
+        # the natural column order, with Omega unpermuted
         nonfinite.zero_()
         atil = sk.right(a, fro2=fro2, nonfinite=nonfinite)
-        nbad = int(comm.allreduce_(nonfinite).item())
-        omega = om_job.to_device(dev, None)
-        redo = True
+        nbad = int(comm.allreduce_(nonfinite).item()) % _ops.GATHER_PLAN_FAIL_MARK
+        perm = None
     if nbad != 0:
         raise ValueError(f"{name} contains non-finite entries")
-    if redo or be.lazy_failed():
+    if plan_failed or omega_failed:
+        # (a device Omega that could not complete is redrawn by numpy itself)
+        omega = omega_for(perm, host=omega_failed)
+    if plan_failed or omega_failed or be.lazy_failed():
         y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total)
         qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total)
     return qb

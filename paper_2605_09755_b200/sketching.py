@@ -226,6 +226,19 @@ def draw_omega(kind: str, rows: int, cols: int, seed: int) -> np.ndarray:
     raise ValueError(f"unsupported omega kind {kind!r} on the B200 path")
 
 
+def omega_device(kind: str, rows: int, cols: int, seed: int, dtype, device, perm_dev=None,
+                 fail_counter=None):
+    """The Gaussian start block drawn ON THE DEVICE (numpy's ziggurat
+    reproduced draw for draw, omega.cu), with P^T applied when perm_dev is
+    given; None for the other kinds (drawn on the host).  A generation that
+    could not complete adds _ops.OMEGA_FAIL_MARK to fail_counter."""
+    if kind != "gaussian":
+        return None
+    st, inc = pcg64_state(seed)
+    om = _ops.gaussian(st, inc, rows, cols, math.sqrt(cols), dtype, device, fail_counter)
+    return _ops.permute_rows(om, perm_dev) if perm_dev is not None else om
+
+
 class OmegaDraw:
     """The host-side Omega draw (numpy, bit-identical to the reference) on a
     background thread -- numpy's generator fills release the GIL -- so it

@@ -352,3 +352,25 @@ def test_fused_cholinv(n):
     _lib.call("skp_cholinv_f64", ptr(t2), n, n, 1e-9, ptr(x), ptr(info), ptr(ws), wsb,
               torch.cuda.current_stream().cuda_stream)
     assert int(info.item()) != 0
+
+
+# ---------------------------------------------------------------- Omega ----
+
+@pytest.mark.parametrize("rows,cols,seed", [(4000, 520, 1), (2000, 110, 2), (13, 7, 5),
+                                            (8000, 1050, 3), (1, 1, 9)])
+def test_gaussian_omega_matches_numpy(ops, rows, cols, seed):
+    """Device Omega == numpy's standard_normal((rows, cols)) / sqrt(cols): the
+    fp32 matrix bit for bit; fp64 to 1 ulp (CUDA's log1p in a few tail values)."""
+    import math
+    from paper_2605_09755_b200.sketching import _host_rng, pcg64_state
+    st, inc = pcg64_state(seed)
+    fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+    g32 = ops.gaussian(st, inc, rows, cols, math.sqrt(cols), torch.float32, "cuda", fail)
+    g64 = ops.gaussian(st, inc, rows, cols, math.sqrt(cols), torch.float64, "cuda", fail)
+    ref = _host_rng(seed).standard_normal((rows, cols)) / math.sqrt(cols)
+    assert int(fail.item()) == 0
+    np.testing.assert_array_equal(g32.cpu().numpy(), ref.astype(np.float32))
+    d64 = g64.cpu().numpy()
+    ulp = np.spacing(np.abs(ref))
+    assert (np.abs(d64 - ref) <= ulp).all()
+    assert np.count_nonzero(d64 != ref) <= max(3, rows * cols // 100000)

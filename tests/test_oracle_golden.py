@@ -85,3 +85,14 @@ def test_nystrom_literal_oracle(golden):
     np.testing.assert_allclose(np.linalg.eigvalsh(w), g["W_eigs"], rtol=1e-8,
                                atol=1e-10 * max(abs(x) for x in g["W_eigs"]))
     assert abs(o.nystrom_rel_error(k, c, w) - g["rel_err_literal"]) <= 1e-6
+
+
+@pytest.mark.parametrize("seed", [0, 7, 2**40 + 3])
+def test_ziggurat_restatement_matches_numpy(seed):
+    """The ziggurat constants compiled into csrc/omega.cu reproduce numpy's
+    standard_normal draw for draw (rectangles, wedges and the tail)."""
+    from oracle import ziggurat
+    n = 120_000
+    ref = np.random.Generator(np.random.PCG64(seed)).standard_normal(n)
+    raw = np.random.PCG64(seed).random_raw(n + n // 16 + 64)
+    np.testing.assert_array_equal(ziggurat.standard_normal_from_raw(raw, n), ref)
