@@ -98,6 +98,9 @@ int skp_sketch_right_f64(const double* A, int64_t lda, int64_t m, int64_t n,
  * Requires
  * n <= 24576 and 16-byte aligned rows padded to a multiple of 4 floats;
  * returns SKP_ERR_UNSUPPORTED otherwise (callers keep skp_sketch_right).
+ * nonfinite (may be NULL) += #non-finite outputs: > 0 iff A has a non-finite
+ * entry (every column of A feeds nonzero entries), barring fp32 overflow of a
+ * finite sum; fro2 (may be NULL) += ||A||_F^2 by a separate pass.
  * Replaces the same `a @ self._sparse` (sketching.py:158-164) inside
  * range_finder_sketched (power.py:141-154): Y = (A S) Omega = (A S P)(P^T Omega). */
 int64_t skp_sketch_gather_plan_bytes(int64_t r);

@@ -72,8 +72,12 @@ def as_dtype(op: Operand, dtype) -> torch.Tensor:
 
 
 def download(t: torch.Tensor, kind: str):
+    """Result back to the caller's kind.  Host results land in PINNED memory
+    (pageable device->host copies of the 0.5 GB U run at a fraction of the
+    link rate); numpy results are views of those pinned tensors."""
     if kind == "cuda":
         return t
-    if kind == "cpu":
-        return t.cpu()
-    return t.cpu().numpy()
+    host = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    host.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return host if kind == "cpu" else host.numpy()

@@ -11,6 +11,9 @@
 //     Row gather: out[c][:] = sum_{(j,sg) in col c} sg * X[j][:] / sqrt(s).
 #include <stdlib.h>
 
+#include <algorithm>
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace skp {
@@ -105,20 +108,39 @@ __global__ void sketch_right_direct_kernel(const T* __restrict__ A, int64_t lda,
     out[i * ldo + c] = acc * scale;
 }
 
+__device__ __forceinline__ void sq_acc(float v, double& ss, long long& bad) {
+    ss = fma((double)v, (double)v, ss);  // fp64 squares: finite inputs cannot overflow
+    bad += (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+}
+__device__ __forceinline__ void sq_acc(double v, double& ss, long long& bad) {
+    ss = fma(v, v, ss);
+    bad += !isfinite(v);
+}
+
+// ||X||_F^2 (fp64) and #non-finite entries: blocks walk rows, threads walk a
+// row with 16-byte vector loads (HBM-bound; no per-element index arithmetic)
 template <typename T>
-__global__ void sumsq_kernel(const T* __restrict__ X, int64_t rows, int64_t cols, int64_t ld,
-                             double* out, long long* nonfinite) {
+__global__ void __launch_bounds__(256)
+sumsq_kernel(const T* __restrict__ X, int64_t rows, int64_t cols, int64_t ld, double* out,
+             long long* nonfinite) {
+    typedef typename std::conditional<sizeof(T) == 4, float4, double2>::type V;
+    constexpr int VE = sizeof(V) / sizeof(T);
     __shared__ double red_d[32];
     __shared__ long long red_i[32];
     double ss = 0.0;
     long long bad = 0;
-    const int64_t total = rows * cols;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i = t / cols, j = t - i * cols;
-        T v = X[i * ld + j];
-        ss += (double)v * (double)v;
-        bad += !finite_v(v);
+    const bool vec = (reinterpret_cast<uintptr_t>(X) % sizeof(V) == 0) && (ld % VE == 0);
+    const int64_t nv = vec ? cols / VE : 0;
+    for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
+        const T* row = X + i * ld;
+        const V* rv = reinterpret_cast<const V*>(row);
+        for (int64_t j = threadIdx.x; j < nv; j += blockDim.x) {
+            const V v = __ldg(rv + j);
+            const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+            for (int k = 0; k < VE; ++k) sq_acc(e[k], ss, bad);
+        }
+        for (int64_t j = nv * VE + threadIdx.x; j < cols; j += blockDim.x) sq_acc(row[j], ss, bad);
     }
     double bs = block_sum<double>(ss, red_d);
     long long bb = block_sum<long long>(bad, red_i);
@@ -180,8 +202,8 @@ int sketch_right(const T* A, int64_t lda, int64_t m, int64_t n, const int32_t* c
                                                         ldo);
     SKP_LAUNCHED(sketch_right_direct_kernel);
     if (fro2 || nonfinite) {
-        sumsq_kernel<T><<<1184, 256, 0, st>>>(A, m, n, lda, fro2,
-                                              reinterpret_cast<long long*>(nonfinite));
+        sumsq_kernel<T><<<(unsigned)std::min<int64_t>(m, 148 * 8), 256, 0, st>>>(
+            A, m, n, lda, fro2, reinterpret_cast<long long*>(nonfinite));
         SKP_LAUNCHED(sumsq_kernel);
     }
     return SKP_OK;
@@ -210,8 +232,7 @@ int sumsq(const T* X, int64_t rows, int64_t cols, int64_t ld, double* out, int64
           void* stream) {
     SKP_ARG(rows >= 0 && cols >= 0 && ld >= cols, "sumsq: bad sizes");
     if (rows == 0 || cols == 0) return SKP_OK;
-    int64_t blocks = cdiv(rows * cols, 256 * 8);
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    const int64_t blocks = std::min<int64_t>(rows, 148 * 8);
     sumsq_kernel<T><<<(unsigned)blocks, 256, 0, SKP_STREAM(stream)>>>(
         X, rows, cols, ld, out, reinterpret_cast<long long*>(nonfinite));
     SKP_LAUNCHED(sumsq_kernel);

@@ -25,15 +25,20 @@
 // CTA = one slice of kGCols = 768 output columns (24 warps); the last warp to
 // finish a row refills its buffer (bulk copy of the row two ahead).  Grid = G row groups x P slices; CTAs of a row
 // group walk the same rows at the same time, so the P-fold reuse of each row
-// is served by L2 and A is read from HBM once.  ||A||_F^2 (fp64) and the
-// non-finite test are fused: the compute threads of slice p square this
-// slice's 1/P share of each row.
+// is served by L2 and A is read from HBM once.  Non-finite test: every column
+// of A feeds s >= 1 nonzero (+-1/sqrt(s)) entries, so A has a non-finite entry
+// iff A~ does -- each thread tests the value it stores (one instruction per
+// row; a fused fp64 ||A||^2 here cost 20% of the kernel).  ||A||_F^2, when
+// asked for, is a separate HBM-bound pass (skp_sumsq).
 #include <cuda.h>
 
 #include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
+
+extern "C" int skp_sumsq_f32(const float* X, int64_t rows, int64_t cols, int64_t ld, double* out,
+                             int64_t* nonfinite, void* stream);  // sketch.cu
 
 namespace skp {
 
@@ -50,7 +55,7 @@ constexpr int kGTMax = 128;               // schedule steps per warp (the rest: 
 constexpr unsigned long long kGPlanFailMark = 1ull << 40;  // added to *nonfinite
 constexpr int kGBufWords = 24608;         // row buffer: n <= 24576 floats + 32 zero words
 constexpr uint32_t kGBufBytes = kGBufWords * 4;  // 98432, a multiple of 128
-constexpr size_t kGSmem = 2 * (size_t)kGBufBytes + 32 + kGW * 8;
+constexpr size_t kGSmem = 2 * (size_t)kGBufBytes + 32;
 
 __device__ __forceinline__ uint32_t g_smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -228,13 +233,11 @@ gather_sched_kernel(const int32_t* __restrict__ colptr, const int32_t* __restric
 }
 
 // ---- the gather ----------------------------------------------------------------
-template <bool kNorms>
 __global__ void __maxnreg__(80)
 sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n, int P,
                      const uint32_t* __restrict__ sched, const int32_t* __restrict__ tw,
                      const int32_t* __restrict__ perm, const int32_t* __restrict__ plan_fail,
-                     float scale, float* __restrict__ out, int64_t ldo, double* fro2,
-                     int64_t* nonfinite) {
+                     float scale, float* __restrict__ out, int64_t ldo, int64_t* nonfinite) {
     extern __shared__ __align__(128) unsigned char sm[];
     if (*plan_fail) {
         // the plan's schedule overflowed: report it through the non-finite
@@ -245,7 +248,6 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
     }
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * (size_t)kGBufBytes);
     uint32_t* done = reinterpret_cast<uint32_t*>(full + 2);  // warps finished with a buffer
-    double* red = reinterpret_cast<double*>(full + 4);       // [kGW] per-warp norm partials
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slice = blockIdx.x % P;
@@ -285,11 +287,7 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
     }
     const int v_out = slice * kGCols + warp * 32 + lane;
     const bool valid = perm[v_out] >= 0;
-    // norm share of this slice: float4 units [q0, q1) of the row, one per thread
-    const int64_t nq = (n + 3) / 4;
-    const int64_t qper = (nq + P - 1) / P;
-    const int64_t q0 = (int64_t)slice * qper, q1 = q0 + qper < nq ? q0 + qper : nq;
-    double ss = 0.0;
+    bool bad = false;  // a non-finite output of this thread (iff a non-finite input)
 
     auto do_row = [&](int64_t i, int b, uint32_t ph, auto boff_c) {
         constexpr uint32_t boff = decltype(boff_c)::value;
@@ -319,18 +317,6 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
             asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(x) : "r"(ev & 0x7fffffffu), "n"(boff));
             acc += __int_as_float(__float_as_int(x) ^ (int)(ev & 0x80000000u));
         }
-        if (kNorms) {
-            for (int64_t q = q0 + threadIdx.x; q < q1; q += kGCols) {
-                float4 v;
-                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                             : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                             : "r"(base + boff + (uint32_t)q * 16u)
-                             : "memory");
-                const int64_t c = q * 4;
-                ss += (c + 0 < n ? (double)v.x * v.x : 0.0) + (c + 1 < n ? (double)v.y * v.y : 0.0) +
-                      (c + 2 < n ? (double)v.z * v.z : 0.0) + (c + 3 < n ? (double)v.w * v.w : 0.0);
-            }
-        }
         __syncwarp();
         if (lane == 0) {
             // the last warp done with this buffer refills it with row i + 2G
@@ -352,7 +338,11 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
                 }
             }
         }
-        if (valid) out[i * ldo + v_out] = acc * scale;
+        if (valid) {
+            const float o = acc * scale;
+            bad |= !isfinite(o);
+            out[i * ldo + v_out] = o;
+        }
     };
 
     int it = 0;
@@ -363,17 +353,10 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
                    std::integral_constant<uint32_t, kGBufBytes>());
     }
 
-    if (kNorms) {
-        // ss is finite iff every entry of the share is (squares in fp64 cannot overflow)
-        for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        if (lane == 0) red[warp] = ss;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double tot = 0.0;
-            for (int w = 0; w < kGW; ++w) tot += red[w];
-            if (fro2) atomicAdd(fro2, tot);
-            if (nonfinite && !isfinite(tot)) atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), 1ull);
-        }
+    if (nonfinite) {
+        const unsigned nb = __popc(__ballot_sync(0xffffffffu, bad));
+        if (lane == 0 && nb)
+            atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), (unsigned long long)nb);
     }
 }
 
@@ -435,19 +418,15 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
     const int64_t head = ((int64_t)P * kGCols + P * kGW + 1) * 4;
     const uint32_t* sched = reinterpret_cast<const uint32_t*>(
         reinterpret_cast<const char*>(plan) + (head + 15) / 16 * 16);
-    const bool norms = fro2 || nonfinite;
-    if (norms) {
-        SKP_CUDA(cudaFuncSetAttribute(sketch_gather_kernel<true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
-        sketch_gather_kernel<true><<<G * P, kGThreads, kGSmem, st>>>(
-            A, lda, m, n, P, sched, tw, perm, pfail, scale, out, ldo, fro2, nonfinite);
-    } else {
-        SKP_CUDA(cudaFuncSetAttribute(sketch_gather_kernel<false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
-        sketch_gather_kernel<false><<<G * P, kGThreads, kGSmem, st>>>(
-            A, lda, m, n, P, sched, tw, perm, pfail, scale, out, ldo, fro2, nonfinite);
-    }
+    SKP_CUDA(cudaFuncSetAttribute(sketch_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kGSmem));
+    sketch_gather_kernel<<<G * P, kGThreads, kGSmem, st>>>(A, lda, m, n, P, sched, tw, perm, pfail,
+                                                           scale, out, ldo, nonfinite);
     SKP_LAUNCHED(sketch_gather_kernel);
+    if (fro2) {  // ||A||_F^2: a separate HBM-bound pass (only when asked for)
+        const int rc = skp_sumsq_f32(A, m, n, lda, fro2, nullptr, st);
+        if (rc != SKP_OK) return rc;
+    }
     return SKP_OK;
 }
 

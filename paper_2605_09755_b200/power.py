@@ -258,7 +258,7 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
     m, n = op.t.shape
     spec.validate(m, n)
     ph = _Phases(timings is not None)
-    fro2 = torch.zeros(1, dtype=torch.float64, device=op.t.device)
+    fro2 = torch.zeros(1, dtype=torch.float64, device=op.t.device) if with_error else None
     qb = _range_finder_dev(op.t, spec, phases=ph, fro2=fro2)
     u, s, v = _randsvd_dev(op.t, qb, check=False)
     ph.mark("randsvd")
