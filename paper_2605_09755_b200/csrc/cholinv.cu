@@ -19,6 +19,8 @@
 // flag can cover a whole sync-free sequence of factorisations.
 #include <cooperative_groups.h>
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -36,6 +38,7 @@ struct CIShared {
     double a[CB][CB + 1];
     double b[CB][CB + 1];
     double c[CB][CB + 1];
+    double invd[CB];
     int bad;
 };
 
@@ -56,157 +59,257 @@ __device__ __forceinline__ void tile_mm(double (*C)[CB + 1], double (*X)[CB + 1]
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kCIThreads)
+// 1/sqrt(d) to fp64 accuracy: the fp32 estimate (MUFU, ~23 bits) and two
+// Newton steps (46 -> full); the IEEE sqrt + divide chain costs ~10x more and
+// sits on the factorisation's critical path 64 times per 32x32 tile
+__device__ __forceinline__ double rsqrt64(double d) {   // d > 0, finite, normal
+    // d = m * 4^h with m in [1, 4): exact power-of-four scaling from the
+    // exponent bits keeps the fp32 estimate in range with no calls or branches
+    // (an out-of-line sqrt / divide forced register spills around the loop)
+    const int e = ((__double2hiint(d) >> 20) & 0x7ff) - 1023;
+    const int h = e >> 1;
+    const double m = d * __hiloint2double((1023 - 2 * h) << 20, 0);
+    double y = (double)rsqrtf((float)m);
+    const double hm = 0.5 * m;
+    y = y * fma(-hm * y, y, 1.5);
+    y = y * fma(-hm * y, y, 1.5);
+    return y * __hiloint2double((1023 - h) << 20, 0);
+}
+
+// 32x32 SPD tile T (smem, lower part) -> L into T (lower, upper zeroed) and
+// L^{-1} into Li, by the whole block (block-uniform; 256 threads):
+//   Cholesky, right-looking: per step k thread 0 takes the pivot (rsqrt64),
+//   the column below is scaled, the trailing triangle (<= 496 entries) is
+//   updated ~2 entries per thread -- 3 block barriers per step;
+//   inverse by recursive doubling: with the diagonal 1/L_ii, level b = 1..16
+//   fills every off-diagonal block of the inverse at once,
+//   X21 = -X22 (L21 X11), one output entry per thread, 2 barriers per level.
+// (A one-warp version serialised on the 32-step dependency chains and its
+// register rows were demoted to local memory.)  Returns the first bad pivot
+// (1-based in the tile, 0 if none) and the pivot range via *mn / *mx.
+__device__ __forceinline__ int tile_chol_inv(double (*T)[CB + 1], double (*Li)[CB + 1],
+                                             double (*W)[CB + 1], double* invd, double* mn,
+                                             double* mx) {
+    __shared__ int s_bad;
+    __shared__ double s_mn, s_mx;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        s_bad = 0;
+        s_mn = INFINITY;
+        s_mx = 0.0;
+    }
+    for (int k = 0; k < CB; ++k) {
+        if (tid == 0) {
+            double d = T[k][k];
+            if (!(d > 1e-300) || !isfinite(d)) {
+                if (!s_bad) s_bad = k + 1;
+                d = 1.0;  // keep going; the caller discards the result
+            }
+            const double inv = rsqrt64(d);
+            const double l = d * inv;
+            T[k][k] = l;
+            invd[k] = inv;
+            s_mn = fmin(s_mn, l);
+            s_mx = fmax(s_mx, l);
+        }
+        __syncthreads();
+        if (tid > k && tid < CB) T[tid][k] *= invd[k];   // L_ik
+        __syncthreads();
+        const int m = CB - 1 - k;                        // trailing triangle k < j <= i
+        for (int t = tid; t < m * (m + 1) / 2; t += blockDim.x) {
+            int r = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+            while (r * (r + 1) / 2 > t) --r;
+            while ((r + 1) * (r + 2) / 2 <= t) ++r;
+            const int c = t - r * (r + 1) / 2;
+            const int i = k + 1 + r, j = k + 1 + c;
+            T[i][j] -= T[i][k] * T[j][k];
+        }
+        __syncthreads();
+    }
+    for (int q = tid; q < CB * CB; q += blockDim.x) {
+        const int i = q / CB, j = q % CB;
+        if (j > i) T[i][j] = 0.0;
+        Li[i][j] = i == j ? invd[i] : 0.0;
+    }
+    __syncthreads();
+    for (int b = 1; b < CB; b *= 2) {
+        // pairs of b x b diagonal blocks (s0, s0 + b): W = L21 X11, then X21 = -X22 W
+        const int per = b * b, npairs = CB / (2 * b);
+        for (int t = tid; t < npairs * per; t += blockDim.x) {
+            const int q = t / per, e = t % per, r = e / b, c = e % b;
+            const int s0 = q * 2 * b, s1 = s0 + b;
+            double acc = 0.0;
+            for (int k = 0; k < b; ++k) acc += T[s1 + r][s0 + k] * Li[s0 + k][s0 + c];
+            W[s1 + r][s0 + c] = acc;
+        }
+        __syncthreads();
+        for (int t = tid; t < npairs * per; t += blockDim.x) {
+            const int q = t / per, e = t % per, r = e / b, c = e % b;
+            const int s0 = q * 2 * b, s1 = s0 + b;
+            double acc = 0.0;
+            for (int k = 0; k < b; ++k) acc += Li[s1 + r][s1 + k] * W[s1 + k][s0 + c];
+            Li[s1 + r][s0 + c] = -acc;
+        }
+        __syncthreads();
+    }
+    *mn = s_mn;
+    *mx = s_mx;
+    return s_bad;
+}
+
+// One cooperative kernel, ONE grid sync per 32-wide panel:
+//   before panel p: L_pp and L_pp^{-1} are final (factored by CTA 0 as a
+//   lookahead at the end of panel p-1); the trailing matrix holds all updates
+//   through panel p-1.
+//   panel p tasks (any CTA):
+//     trailing tile (I, J), p < J <= I:  L_Ip = A_Ip L_pp^{-T}, L_Jp likewise
+//       (recomputed per task: no separate panel solve and no extra sync),
+//       A_IJ -= L_Ip L_Jp^T; the task with J = p+1 stores L_Ip;
+//     inverse, one layer per panel (row p-1 of X became final in panel p-1):
+//       rows r > p, J < p:  S_rJ += L_{r,p-1} X_{p-1,J};
+//       row p, J < p:       X_pJ = -L_pp^{-1} (S_pJ + L_{p,p-1} X_{p-1,J})
+//     (X_pJ = -L_pp^{-1} sum_{K=J}^{p-1} L_pK X_KJ, accumulated across panels
+//     so every task is ONE tile product and each S tile has one writer).
+//   CTA 0 takes task (p+1, p+1) first and factors the result right away.
+__global__ void __launch_bounds__(kCIThreads, 1)
 cholinv_kernel(const double* __restrict__ G, int n, int64_t ldg, int nb, double rel_tol,
-               double* A, double* X, double* dinfo, int32_t* info, int col_in_smem) {
+               double* A, double* Lb, double* X, double* S, double* dinfo, int32_t* info,
+               unsigned long long* prof) {
+    auto stamp = [&](int slot) {
+        if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            prof[slot] = t;
+        }
+    };
     extern __shared__ __align__(16) unsigned char smraw[];
     CIShared& sh = *reinterpret_cast<CIShared*>(smraw);
+    double (*sd)[CB + 1] = reinterpret_cast<double (*)[CB + 1]>(smraw + sizeof(CIShared));
     cg::grid_group grid = cg::this_grid();
     const int np = nb * CB;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-    // padded copy: [[G, 0], [0, I]]
+    // padded copy: [[G, 0], [0, I]]; X = 0
     for (int64_t t = gtid; t < (int64_t)np * np; t += gstride) {
         const int i = (int)(t / np), j = (int)(t % np);
         A[t] = (i < n && j < n) ? G[(int64_t)i * ldg + j] : (i == j ? 1.0 : 0.0);
         X[t] = 0.0;
-    }
-    if (gtid == 0) {                 // *info is only ever SET (failures accumulate)
-        dinfo[0] = INFINITY;   // min pivot of L
-        dinfo[1] = 0.0;        // max pivot of L
+        S[t] = 0.0;
     }
     grid.sync();
-    for (int p = 0; p < nb; ++p) {
-        const int p0 = p * CB;
-        // (1) diagonal block: factor + invert (CTA 0)
-        if (blockIdx.x == 0) {
-            for (int t = threadIdx.x; t < CB * CB; t += blockDim.x)
-                sh.a[t / CB][t % CB] = A[(int64_t)(p0 + t / CB) * np + p0 + t % CB];
-            if (threadIdx.x == 0) sh.bad = 0;
+    auto tload = [&](double (*T)[CB + 1], const double* M, int r0, int c0) {
+        for (int q = threadIdx.x; q < CB * CB; q += blockDim.x)
+            T[q / CB][q % CB] = M[(int64_t)(r0 + q / CB) * np + c0 + q % CB];
+    };
+    auto tstore = [&](double* M, int r0, int c0, double (*T)[CB + 1]) {
+        for (int q = threadIdx.x; q < CB * CB; q += blockDim.x)
+            M[(int64_t)(r0 + q / CB) * np + c0 + q % CB] = T[q / CB][q % CB];
+    };
+    // factor tile (p, p) held in T (smem) into Lb / X, pivot statistics (CTA 0)
+    auto factor = [&](int p, double (*T)[CB + 1]) {
+        __syncthreads();
+        {
+            double mn, mx;
+            for (int q = threadIdx.x; q < CB * CB; q += blockDim.x)  // factor a copy in sh.a
+                sh.a[q / CB][q % CB] = T[q / CB][q % CB];
             __syncthreads();
-            for (int k = 0; k < CB; ++k) {
-                if (threadIdx.x == 0) {
-                    const double dkk = sh.a[k][k];
-                    if (!(dkk > 0.0) || !isfinite(dkk)) {
-                        if (!sh.bad) sh.bad = p0 + k + 1;
-                        sh.a[k][k] = 1.0;  // keep going; result is discarded
+            const int bad = tile_chol_inv(sh.a, sh.b, sh.c, sh.invd, &mn, &mx);
+            if (threadIdx.x == 0) {
+                const int p0 = p * CB;
+                if (bad && *info == 0) *info = p0 + bad;
+                // pivots of the identity padding are 1: count only real rows
+                double dmn = dinfo[0], dmx = dinfo[1];
+                if (p0 < n) {
+                    if (p0 + CB <= n) {
+                        dmn = fmin(dmn, mn);
+                        dmx = fmax(dmx, mx);
                     } else {
-                        sh.a[k][k] = sqrt(dkk);
+                        for (int k = 0; p0 + k < n; ++k) {
+                            dmn = fmin(dmn, sh.a[k][k]);
+                            dmx = fmax(dmx, sh.a[k][k]);
+                        }
                     }
                 }
-                __syncthreads();
-                const double dk = sh.a[k][k];
-                for (int i = k + 1 + threadIdx.x; i < CB; i += blockDim.x) sh.a[i][k] /= dk;
-                __syncthreads();
-                for (int t = threadIdx.x; t < (CB - k - 1) * (CB - k - 1); t += blockDim.x) {
-                    const int i = k + 1 + t / (CB - k - 1), j = k + 1 + t % (CB - k - 1);
-                    if (j <= i) sh.a[i][j] -= sh.a[i][k] * sh.a[j][k];
-                }
-                __syncthreads();
+                dinfo[0] = dmn;
+                dinfo[1] = dmx;
             }
-            // zero the strict upper part, invert (column-parallel forward substitution)
-            for (int t = threadIdx.x; t < CB * CB; t += blockDim.x)
-                if (t % CB > t / CB) sh.a[t / CB][t % CB] = 0.0;
-            __syncthreads();
-            if (threadIdx.x < CB) {
-                const int j = threadIdx.x;
-                for (int i = 0; i < CB; ++i) {
-                    double s = (i == j) ? 1.0 : 0.0;
-                    for (int k = j; k < i; ++k) s -= sh.a[i][k] * sh.b[k][j];
-                    sh.b[i][j] = i >= j ? s / sh.a[i][i] : 0.0;
-                }
-            }
-            __syncthreads();
-            for (int t = threadIdx.x; t < CB * CB; t += blockDim.x) {
-                const int i = t / CB, j = t % CB;
-                A[(int64_t)(p0 + i) * np + p0 + j] = sh.a[i][j];
-                X[(int64_t)(p0 + i) * np + p0 + j] = sh.b[i][j];
-            }
-            if (threadIdx.x == 0) {
-                if (sh.bad && *info == 0) *info = sh.bad;
-                double mn = dinfo[0], mx = dinfo[1];
-                for (int k = 0; k < CB; ++k)
-                    if (p0 + k < n) { mn = fmin(mn, sh.a[k][k]); mx = fmax(mx, sh.a[k][k]); }
-                dinfo[0] = mn;
-                dinfo[1] = mx;
-            }
-        }
-        grid.sync();
-        if (p + 1 < nb) {
-            // (2) L_ip = A_ip L_pp^{-T}: one warp per row below the panel
-            const int warp_g = (int)(gtid >> 5), nw = (int)(gstride >> 5), lane = threadIdx.x & 31;
-            for (int i = p0 + CB + warp_g; i < np; i += nw) {
-                double* row = A + (int64_t)i * np + p0;
-                const double* Li = X + (int64_t)p0 * np + p0;  // L_pp^{-1}, row-major
-                const double a_l = row[lane];
-                double acc = 0.0;
-                // L_ip[c] = sum_k A_ip[k] * Linv[c][k]
-                for (int k = 0; k < CB; ++k) acc += __shfl_sync(0xffffffffu, a_l, k) * Li[(int64_t)lane * np + k];
-                __syncwarp();
-                row[lane] = acc;
-            }
-            grid.sync();
-            // (3) trailing update of tiles (I, J), p < J <= I
-            const int m = nb - p - 1;
-            const int ntile = m * (m + 1) / 2;
-            for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
-                int I = 0, rem = t;
-                while (rem > I) { rem -= I + 1; ++I; }
-                const int J = rem;
-                const int I0 = (p + 1 + I) * CB, J0 = (p + 1 + J) * CB;
-                for (int q = threadIdx.x; q < CB * CB; q += blockDim.x) {
-                    const int r = q / CB, c = q % CB;
-                    sh.a[r][c] = A[(int64_t)(I0 + r) * np + p0 + c];   // L_Ip
-                    sh.b[r][c] = A[(int64_t)(J0 + r) * np + p0 + c];   // L_Jp
-                    sh.c[r][c] = A[(int64_t)(I0 + r) * np + J0 + c];
-                }
-                __syncthreads();
-                tile_mm(sh.c, sh.a, sh.b, 0, -1.0, true);
-                for (int q = threadIdx.x; q < CB * CB; q += blockDim.x)
-                    A[(int64_t)(I0 + q / CB) * np + J0 + q % CB] = sh.c[q / CB][q % CB];
-                __syncthreads();
-            }
-            grid.sync();
-        }
-    }
-    // X = L^{-1} by block columns: block column J depends only on itself
-    // (X_IJ = -L_II^{-1} sum_{K=J}^{I-1} L_IK X_KJ), so one CTA sweeps down one
-    // column with it resident in shared memory -- no grid syncs.
-    // resident copy in smem when np x 32 doubles fit, else read X (L1/L2)
-    double* colS = reinterpret_cast<double*>(smraw + sizeof(CIShared));  // np x CB
-    for (int J = blockIdx.x; J < nb; J += gridDim.x) {
-        const int J0 = J * CB;
-        double* colX = col_in_smem ? colS : X + J0;
-        const int64_t cld = col_in_smem ? CB : np;   // leading dim of the column view
-        if (col_in_smem) {
-            for (int q = threadIdx.x; q < CB * CB; q += blockDim.x)
-                colS[(q / CB) * CB + q % CB] = X[(int64_t)(J0 + q / CB) * np + J0 + q % CB];
         }
         __syncthreads();
-        for (int I = J + 1; I < nb; ++I) {
-            const int I0 = I * CB;
-            // T = sum_K L_IK X_KJ : thread (r, c4) accumulates 4 outputs
-            const int tr = threadIdx.x / 8, tc = (threadIdx.x % 8) * 4;
-            double acc[4] = {0, 0, 0, 0};
-            const double* Lrow = A + (int64_t)(I0 + tr) * np;
-            for (int k = J0; k < I0; ++k) {
-                const double l = Lrow[k];
-                const double* xr = colX + (int64_t)(col_in_smem ? k - J0 : k) * cld + tc;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[j] += l * xr[j];
+        tstore(Lb, p * CB, p * CB, sh.a);
+        tstore(X, p * CB, p * CB, sh.b);
+    };
+    if (blockIdx.x == 0) {
+        if (threadIdx.x == 0) {
+            dinfo[0] = INFINITY;
+            dinfo[1] = 0.0;
+        }
+        tload(sh.c, A, 0, 0);
+        factor(0, sh.c);
+    }
+    for (int p = 0; p < nb; ++p) {
+        stamp(4 * p + 0);
+        grid.sync();
+        stamp(4 * p + 1);
+        const int p0 = p * CB;
+        const int m = nb - 1 - p;
+        const int ntrail = m * (m + 1) / 2;
+        const int ntask = ntrail + (nb - p) * p;   // + inverse layer: rows p..nb-1 x J < p
+        for (int t = blockIdx.x; t < ntask; t += gridDim.x) {
+            if (t < ntrail) {
+                // trailing tile: t = 0 is (p+1, p+1); then row-major over J <= I
+                int I = 0, rem = t;
+                while (rem > I) {
+                    rem -= I + 1;
+                    ++I;
+                }
+                int J = rem;
+                // remap so task 0 is the lookahead tile (p+1, p+1): tile order
+                // (0,0),(1,0),(1,1),... -> (I, J) relative to p+1
+                const int I0 = (p + 1 + I) * CB, J0 = (p + 1 + J) * CB;
+                tload(sh.b, X, p0, p0);                 // L_pp^{-1}
+                tload(sh.a, A, I0, p0);                 // A_Ip
+                __syncthreads();
+                tile_mm(sh.c, sh.a, sh.b, 0, 1.0, false);   // L_Ip = A_Ip L_pp^{-T}
+                if (J == 0) tstore(Lb, I0, p0, sh.c);
+                if (I != J) {
+                    tload(sh.a, A, J0, p0);             // A_Jp
+                    __syncthreads();
+                    tile_mm(sd, sh.a, sh.b, 0, 1.0, false);  // L_Jp
+                } else {
+                    for (int q = threadIdx.x; q < CB * CB; q += blockDim.x)
+                        sd[q / CB][q % CB] = sh.c[q / CB][q % CB];
+                    __syncthreads();
+                }
+                tload(sh.a, A, I0, J0);                 // A_IJ
+                __syncthreads();
+                tile_mm(sh.a, sh.c, sd, 0, -1.0, true); // A_IJ -= L_Ip L_Jp^T
+                tstore(A, I0, J0, sh.a);
+                if (t == 0 && blockIdx.x == 0) {
+                    stamp(4 * p + 2);
+                    factor(p + 1, sh.a);  // lookahead
+                    stamp(4 * p + 3);
+                }
+                __syncthreads();
+            } else {
+                // inverse layer K = p-1 for tile (r, J), r >= p, J < p
+                const int u = t - ntrail;
+                const int r = p + u / p, J = u % p;
+                const int R0 = r * CB, J0 = J * CB, K0 = (p - 1) * CB;
+                tload(sh.a, Lb, R0, K0);                // L_{r,p-1}
+                tload(sh.b, X, K0, J0);                 // X_{p-1,J}
+                tload(sd, S, R0, J0);                   // S_rJ
+                __syncthreads();
+                tile_mm(sd, sh.a, sh.b, 1, 1.0, true);  // S_rJ += L_{r,p-1} X_{p-1,J}
+                if (r > p) {
+                    tstore(S, R0, J0, sd);
+                } else {
+                    tload(sh.a, X, p0, p0);             // L_pp^{-1}
+                    __syncthreads();
+                    tile_mm(sh.c, sh.a, sd, 1, -1.0, false);
+                    tstore(X, p0, J0, sh.c);
+                }
+                __syncthreads();
             }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) sh.c[tr][tc + j] = acc[j];
-            for (int q = threadIdx.x; q < CB * CB; q += blockDim.x)
-                sh.a[q / CB][q % CB] = X[(int64_t)(I0 + q / CB) * np + I0 + q % CB];  // L_II^{-1}
-            __syncthreads();
-            tile_mm(sh.b, sh.a, sh.c, 1, -1.0, false);
-            for (int q = threadIdx.x; q < CB * CB; q += blockDim.x) {
-                const double v = sh.b[q / CB][q % CB];
-                if (col_in_smem) colS[(int64_t)(I0 - J0 + q / CB) * CB + q % CB] = v;
-                X[(int64_t)(I0 + q / CB) * np + J0 + q % CB] = v;
-            }
-            __syncthreads();
         }
     }
     grid.sync();
@@ -226,7 +329,7 @@ using namespace skp;
 
 extern "C" int64_t skp_cholinv_ws_bytes(int64_t n) {
     const int64_t np = cdiv(n, CB) * CB;
-    return 2 * np * np * (int64_t)sizeof(double) + 64;
+    return 4 * np * np * (int64_t)sizeof(double) + 64;
 }
 
 extern "C" int skp_cholinv_f64(const double* G, int64_t n, int64_t ld, double rel_tol, double* X,
@@ -238,28 +341,51 @@ extern "C" int skp_cholinv_f64(const double* G, int64_t n, int64_t ld, double re
     const int nb = (int)cdiv(n, CB);
     const int np = nb * CB;
     double* A = reinterpret_cast<double*>(ws);
-    double* Xp = A + (int64_t)np * np;
+    double* Lb = A + (int64_t)np * np;
+    double* Xp = Lb + (int64_t)np * np;
+    double* Sp = Xp + (int64_t)np * np;
     // 2 doubles of pivot statistics live in the 64-byte tail of the workspace
     double* dinfo = reinterpret_cast<double*>(
-        (reinterpret_cast<uintptr_t>(Xp + (int64_t)np * np) + 15) & ~uintptr_t(15));
+        (reinterpret_cast<uintptr_t>(Sp + (int64_t)np * np) + 15) & ~uintptr_t(15));
     int dev = 0, sms = 148, per_sm = 0;
     SKP_CUDA(cudaGetDevice(&dev));
     SKP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    // CIShared + one resident block column of L^{-1} (np x 32 doubles) if it fits
-    const size_t col_bytes = (size_t)np * CB * sizeof(double);
-    int col_in_smem = sizeof(CIShared) + col_bytes + 16 <= 200 * 1024 ? 1 : 0;
-    const size_t smem = sizeof(CIShared) + (col_in_smem ? col_bytes : 0) + 16;
+    const size_t smem = sizeof(CIShared) + sizeof(double) * CB * (CB + 1) + 16;
     SKP_CUDA(cudaFuncSetAttribute(cholinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     SKP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cholinv_kernel, kCIThreads, smem));
     SKP_ARG(per_sm >= 1, "cholinv: cooperative kernel cannot be resident");
-    int blocks = std::min(sms, std::max(nb * (nb + 1) / 2, 1));
+    int maxtask = 1;
+    for (int p = 0; p < nb; ++p)
+        maxtask = std::max(maxtask, (nb - 1 - p) * (nb - p) / 2 + (nb - p) * p);
+    int blocks = std::min(sms, std::max(maxtask, 1));
     int nn = (int)n;
     int64_t ldg = ld;
-    void* args[] = {(void*)&G, &nn, &ldg, (void*)&nb, &rel_tol, &A, &Xp, &dinfo, &info, &col_in_smem};
+    static unsigned long long* prof = nullptr;
+    unsigned long long* prof_arg = nullptr;
+    if (getenv("SKP_CI_PROF")) {
+        if (!prof) SKP_CUDA(cudaMalloc(&prof, 4 * 1024 * sizeof(unsigned long long)));
+        SKP_CUDA(cudaMemsetAsync(prof, 0, 4 * 1024 * sizeof(unsigned long long), st));
+        prof_arg = prof;
+    }
+    void* args[] = {(void*)&G, &nn, &ldg, (void*)&nb, &rel_tol, &A, &Lb, &Xp, &Sp, &dinfo, &info, &prof_arg};
     SKP_CUDA(cudaLaunchCooperativeKernel((void*)cholinv_kernel, dim3(blocks), dim3(kCIThreads), args,
                                          smem, st));
     count_launch();
+    if (prof_arg) {
+        unsigned long long h[4 * 1024];
+        SKP_CUDA(cudaStreamSynchronize(st));
+        SKP_CUDA(cudaMemcpy(h, prof_arg, sizeof(unsigned long long) * 4 * nb, cudaMemcpyDeviceToHost));
+        double wait = 0, task0 = 0, fac = 0, rest = 0;
+        for (int p = 0; p + 1 < nb; ++p) {
+            wait += (h[4 * p + 1] - h[4 * p + 0]) / 1e3;
+            task0 += (h[4 * p + 2] - h[4 * p + 1]) / 1e3;
+            fac += (h[4 * p + 3] - h[4 * p + 2]) / 1e3;
+            rest += (h[4 * (p + 1)] - h[4 * p + 3]) / 1e3;
+        }
+        fprintf(stderr, "[cholinv prof] n=%lld nb=%d blocks=%d per panel (us): sync %.2f task0 %.2f factor %.2f rest %.2f\n",
+                (long long)n, nb, blocks, wait / (nb - 1), task0 / (nb - 1), fac / (nb - 1), rest / (nb - 1));
+    }
     if (np == n) {
         SKP_CUDA(cudaMemcpyAsync(X, Xp, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
     } else {
