@@ -20,6 +20,7 @@
 // ~2 * n grid syncs in total vs ~13 * n for cyclic Jacobi.
 #include <cooperative_groups.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -46,25 +47,34 @@ __device__ double block_reduce_sum_all(double v, double* scratch) {
 
 // A: n x n symmetric (full storage, row-major, overwritten).  Outputs d[n],
 // e[n-1], tau[n-1], Hv (n x n; row i holds v_i on columns i+1.., v_i[i+1]=1).
+// Per column i, 2 grid syncs:
+//   every CTA stages column i (below the diagonal) in smem and builds the
+//   reflector v there (redundantly -- no sync); p = tau A' v, one warp per row
+//   (coalesced rows, v from smem); sync; every CTA forms w = p - K v in smem;
+//   the rank-2 update A' -= v w^T + w v^T by rows (row -> CTA, columns ->
+//   threads: no index division); sync.
+// smem: v[n], w[n] (dynamic).
 __global__ void __launch_bounds__(kTriThreads)
 sytrd_kernel(double* A, int n, double* d, double* e, double* tau, double* Hv, double* pbuf) {
+    extern __shared__ double tsm[];
+    double* vs = tsm;         // v over rows r0.. (index t = row - r0)
+    double* ws = tsm + n;     // w
     __shared__ double scratch[32];
     cg::grid_group grid = cg::this_grid();
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
     const int warp_g = (int)(gtid >> 5), lane = threadIdx.x & 31;
-    const int nwarps_g = (int)(gstride >> 5);
+    const int nwarps_g = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
     for (int i = 0; i + 2 < n; ++i) {
         const int r0 = i + 1, k = n - r0;
-        // (a) reflector from x = A[r0:, i] (column i below the diagonal is not
-        //     touched by this step's update, so every CTA can read it)
+        // (a) reflector from x = A[r0:, i] (untouched by this step's update)
         double ss = 0.0;
-        for (int t = 1 + threadIdx.x; t < k; t += blockDim.x) {
+        for (int t = threadIdx.x; t < k; t += blockDim.x) {
             const double x = A[(int64_t)(r0 + t) * n + i];
-            ss += x * x;
+            vs[t] = x;
+            if (t > 0) ss += x * x;
         }
-        const double xnorm2 = block_reduce_sum_all(ss, scratch);
-        const double alpha = A[(int64_t)r0 * n + i];
+        const double xnorm2 = block_reduce_sum_all(ss, scratch);   // (syncs the block)
+        const double alpha = vs[0];
         double t_, beta, scal;
         if (xnorm2 == 0.0) {
             t_ = 0.0;
@@ -75,16 +85,14 @@ sytrd_kernel(double* A, int n, double* d, double* e, double* tau, double* Hv, do
             t_ = (beta - alpha) / beta;
             scal = 1.0 / (alpha - beta);
         }
-        // v_c (c = r0 + t): t == 0 -> 1, else x_t * scal
-        auto vat = [&](int t) -> double {
-            return t == 0 ? 1.0 : A[(int64_t)(r0 + t) * n + i] * scal;
-        };
+        for (int t = threadIdx.x; t < k; t += blockDim.x) vs[t] = t == 0 ? 1.0 : vs[t] * scal;
+        __syncthreads();
         // (b) p = tau * A' v, one warp per row of A' = A[r0:, r0:]
         if (t_ != 0.0) {
             for (int rr = warp_g; rr < k; rr += nwarps_g) {
                 const double* row = A + (int64_t)(r0 + rr) * n + r0;
                 double acc = 0.0;
-                for (int t = lane; t < k; t += 32) acc += row[t] * vat(t);
+                for (int t = lane; t < k; t += 32) acc += row[t] * vs[t];
                 acc = warp_sum(acc);
                 if (lane == 0) pbuf[rr] = t_ * acc;
             }
@@ -94,22 +102,29 @@ sytrd_kernel(double* A, int n, double* d, double* e, double* tau, double* Hv, do
             e[i] = beta;
             tau[i] = t_;
         }
+        // store v_i for the back-transformation (row i of Hv)
+        for (int64_t t = gtid; t < k; t += (int64_t)gridDim.x * blockDim.x)
+            Hv[(int64_t)i * n + r0 + t] = vs[t];
         grid.sync();
         if (t_ != 0.0) {
-            // (c) K = tau/2 * p.v ; w = p - K v   (redundant per CTA)
+            // (c) K = tau/2 * p.v ; w = p - K v   (redundant per CTA, into smem)
             double pv = 0.0;
-            for (int t = threadIdx.x; t < k; t += blockDim.x) pv += pbuf[t] * vat(t);
+            for (int t = threadIdx.x; t < k; t += blockDim.x) {
+                const double pt = pbuf[t];
+                ws[t] = pt;
+                pv += pt * vs[t];
+            }
             const double K = 0.5 * t_ * block_reduce_sum_all(pv, scratch);
-            // (d) A' -= v w^T + w v^T
-            for (int64_t q = gtid; q < (int64_t)k * k; q += gstride) {
-                const int rr = (int)(q / k), cc = (int)(q % k);
-                const double vr = vat(rr), vc = vat(cc);
-                const double wr = pbuf[rr] - K * vr, wc = pbuf[cc] - K * vc;
-                A[(int64_t)(r0 + rr) * n + r0 + cc] -= vr * wc + wr * vc;
+            for (int t = threadIdx.x; t < k; t += blockDim.x) ws[t] -= K * vs[t];
+            __syncthreads();
+            // (d) A' -= v w^T + w v^T: rows over CTAs, columns over threads
+            for (int rr = blockIdx.x; rr < k; rr += gridDim.x) {
+                double* row = A + (int64_t)(r0 + rr) * n + r0;
+                const double vr = vs[rr], wr = ws[rr];
+                for (int cc = threadIdx.x; cc < k; cc += blockDim.x)
+                    row[cc] -= vr * ws[cc] + wr * vs[cc];
             }
         }
-        // store v_i for the back-transformation (row i of Hv)
-        for (int64_t t = gtid; t < k; t += gstride) Hv[(int64_t)i * n + r0 + t] = vat((int)t);
         grid.sync();
     }
     if (gtid == 0) {
@@ -120,6 +135,157 @@ sytrd_kernel(double* A, int n, double* d, double* e, double* tau, double* Hv, do
         }
         d[n - 1] = A[(int64_t)(n - 1) * n + n - 1];
     }
+}
+
+// ---- cluster tridiagonalisation: the whole matrix in distributed smem -------
+// A cluster of kCl CTAs (one per SM) holds A row-interleaved in shared memory
+// (row r -> CTA r % kCl, local row r / kCl); per column: the owners broadcast
+// column i and their norm partials by DSMEM stores, cluster barrier, every CTA
+// builds v and computes p for its rows, broadcasts p and p.v partials, cluster
+// barrier, every CTA forms w and updates its rows.  No global-memory round
+// trips and hardware cluster barriers instead of grid syncs.  Exchange buffers
+// alternate with the column parity (a CTA is never more than one phase ahead).
+constexpr int kCl = 16;
+constexpr int kClThreads = 512;
+
+__device__ __forceinline__ uint32_t cl_smem(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t cl_mapa(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cl_st(uint32_t a, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                     "memory");
+}
+
+__global__ void __launch_bounds__(kClThreads, 1)
+sytrd_cluster_kernel(const double* __restrict__ Ag, int n, int rpc, double* d, double* e,
+                     double* tau, double* Hv) {
+    extern __shared__ __align__(16) double csm[];
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    // layout: A rows [rpc][n] | xv[2][n] | pv[2][n] | ssp[2][kCl] | pvp[2][kCl] | vs[n] | ws[n]
+    double* Al = csm;
+    double* xv = Al + (size_t)rpc * n;
+    double* pvv = xv + 2 * (size_t)n;
+    double* ssp = pvv + 2 * (size_t)n;
+    double* pvp = ssp + 2 * kCl;
+    double* vs = pvp + 2 * kCl;
+    double* wsv = vs + n;
+    __shared__ double scratch[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    // load owned rows
+    for (int lr = 0; lr < rpc; ++lr) {
+        const int r = lr * kCl + (int)rank;
+        for (int c = tid; c < n; c += blockDim.x) Al[(size_t)lr * n + c] = r < n ? Ag[(int64_t)r * n + c] : 0.0;
+    }
+    cl_sync();
+    const uint32_t xv_a = cl_smem(xv), pv_a = cl_smem(pvv), ssp_a = cl_smem(ssp), pvp_a = cl_smem(pvp);
+    for (int i = 0; i + 2 < n; ++i) {
+        const int par = i & 1;
+        const int r0 = i + 1, k = n - r0;
+        // (1) broadcast column i of my rows r > i, and sum_{r > r0} x_r^2
+        double ss = 0.0;
+        for (int q = tid; q < rpc * kCl; q += blockDim.x) {
+            const int lr = q / kCl, dst = q % kCl;
+            const int r = lr * kCl + (int)rank;
+            if (r <= i || r >= n) continue;
+            const double x = Al[(size_t)lr * n + i];
+            if (dst == 0 && r > r0) ss += x * x;
+            cl_st(cl_mapa(xv_a + 8u * (uint32_t)(par * n + r), (uint32_t)dst), x);
+        }
+        ss = warp_sum(ss);
+        if (lane == 0) scratch[warp] = ss;
+        __syncthreads();
+        if (tid < kCl) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += scratch[w];
+            cl_st(cl_mapa(ssp_a + 8u * (uint32_t)(par * kCl + (int)rank), (uint32_t)tid), t);
+        }
+        cl_sync();
+        // (2) reflector (every CTA), p for my rows, broadcast p and p.v partials
+        double xnorm2 = 0.0;
+        for (int c = 0; c < kCl; ++c) xnorm2 += ssp[par * kCl + c];
+        const double* xcol = xv + (size_t)par * n;
+        const double alpha = xcol[r0];
+        double t_, beta, scal;
+        if (xnorm2 == 0.0) {
+            t_ = 0.0;
+            beta = alpha;
+            scal = 0.0;
+        } else {
+            beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
+            t_ = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        for (int c = r0 + tid; c < n; c += blockDim.x) vs[c] = c == r0 ? 1.0 : xcol[c] * scal;
+        if (rank == 0) {
+            if (tid == 0) {
+                e[i] = beta;
+                tau[i] = t_;
+            }
+            for (int c = r0 + tid; c < n; c += blockDim.x)
+                Hv[(int64_t)i * n + c] = c == r0 ? 1.0 : xcol[c] * scal;
+        }
+        if ((i % kCl) == (int)rank && tid == 0) d[i] = Al[(size_t)(i / kCl) * n + i];
+        __syncthreads();
+        double pvpart = 0.0;
+        for (int lr = warp; lr < rpc; lr += nw) {
+            const int r = lr * kCl + (int)rank;
+            if (r < r0 || r >= n) continue;
+            const double* row = Al + (size_t)lr * n;
+            double acc = 0.0;
+            for (int c = r0 + lane; c < n; c += 32) acc += row[c] * vs[c];
+            acc = warp_sum(acc) * t_;
+            if (lane < kCl) cl_st(cl_mapa(pv_a + 8u * (uint32_t)(par * n + r), (uint32_t)lane), acc);
+            pvpart += acc * vs[r];
+        }
+        if (lane == 0) scratch[warp] = pvpart;
+        __syncthreads();
+        if (tid < kCl) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += scratch[w];
+            cl_st(cl_mapa(pvp_a + 8u * (uint32_t)(par * kCl + (int)rank), (uint32_t)tid), t);
+        }
+        cl_sync();
+        // (3) w = p - K v ; update my rows  A[r][c] -= v_r w_c + w_r v_c  (r, c > i)
+        if (t_ != 0.0) {
+            double pv = 0.0;
+            for (int c = 0; c < kCl; ++c) pv += pvp[par * kCl + c];
+            const double K = 0.5 * t_ * pv;
+            const double* pcol = pvv + (size_t)par * n;
+            for (int c = r0 + tid; c < n; c += blockDim.x) wsv[c] = pcol[c] - K * vs[c];
+            __syncthreads();
+            for (int lr = warp; lr < rpc; lr += nw) {
+                const int r = lr * kCl + (int)rank;
+                if (r < r0 || r >= n) continue;
+                double* row = Al + (size_t)lr * n;
+                const double vr = vs[r], wr = wsv[r];
+                for (int c = r0 + lane; c < n; c += 32) row[c] -= vr * wsv[c] + wr * vs[c];
+            }
+        }
+        __syncthreads();
+    }
+    cl_sync();
+    if (n >= 2) {
+        if (((n - 2) % kCl) == (int)rank && tid == 0) {
+            d[n - 2] = Al[(size_t)((n - 2) / kCl) * n + n - 2];
+            tau[n - 2] = 0.0;
+        }
+        if (((n - 1) % kCl) == (int)rank && tid == 0) e[n - 2] = Al[(size_t)((n - 1) / kCl) * n + n - 2];
+    }
+    if (((n - 1) % kCl) == (int)rank && tid == 0) d[n - 1] = Al[(size_t)((n - 1) / kCl) * n + n - 1];
+}
+
+size_t sytrd_cluster_smem(int n) {
+    const int rpc = (n + kCl - 1) / kCl;
+    return sizeof(double) * ((size_t)rpc * n + 4 * (size_t)n + 4 * kCl + 2 * (size_t)n);
 }
 
 // #eigenvalues of T strictly less than x (Sturm sequence via LDL^T)
@@ -137,6 +303,9 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
     return cnt;
 }
 
+// One WARP per eigenvalue: 32 lanes evaluate Sturm counts at 32 interior
+// points of the bracket, which then shrinks 33x per round (~11 rounds to
+// machine precision instead of ~55 bisection steps).
 __global__ void bisect_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n,
                               double* __restrict__ W, double* __restrict__ tnorm_out) {
     extern __shared__ double sm[];
@@ -164,30 +333,46 @@ __global__ void bisect_kernel(const double* __restrict__ dg, const double* __res
     const double tn = fmax(fabs(lo_s), fabs(hi_s));
     const double pivmin = 1e-290;
     const double width = 4.0 * 2.220446049250313e-16 * tn + 1e-300;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += gridDim.x * wpb) {
         // (i+1)-th largest: the value x with count(x) <= n-1-i < count(x')
         const int target = n - 1 - i;  // number of eigenvalues below it
         double lo = lo_s, hi = hi_s;
-        for (int it = 0; it < 200; ++it) {
-            const double mid = 0.5 * (lo + hi);
-            if (mid == lo || mid == hi || hi - lo <= width) break;
-            if (sturm_count(d, e2, n, mid, pivmin) > target) hi = mid;
-            else lo = mid;
+        for (int it = 0; it < 64; ++it) {
+            if (hi - lo <= width) break;
+            const double step = (hi - lo) / 33.0;
+            const double x = lo + step * (lane + 1);
+            const bool above = x < hi && x > lo && sturm_count(d, e2, n, x, pivmin) > target;
+            // first lane whose point already has more than `target` below it
+            const unsigned mask = __ballot_sync(0xffffffffu, above);
+            const int k = mask ? __ffs(mask) - 1 : 32;   // points 0..k-1 are "not above"
+            const double nlo = k > 0 ? lo + step * k : lo;
+            const double nhi = k < 32 ? lo + step * (k + 1) : hi;
+            if (!(nlo > lo || nhi < hi)) break;          // no progress at this resolution
+            lo = nlo;
+            hi = nhi;
         }
-        W[i] = 0.5 * (lo + hi);
+        if (lane == 0) W[i] = 0.5 * (lo + hi);
     }
 }
 
 // Inverse iteration: thread j computes eigenvector j of T for lambda = W[j].
-// Scratch per thread (interleaved [row][j]): u1, u2, u3 (upper bands), mult,
-// piv (as double 0/1), x.  Z (n x n) receives column j.
-__global__ void inviter_kernel(const double* __restrict__ d, const double* __restrict__ e, int n,
-                               const double* __restrict__ W, const double* __restrict__ tnorm_p,
-                               double* __restrict__ scr, double* __restrict__ Z) {
+// Scratch per thread (interleaved [row][j], coalesced across a warp): 1/u1,
+// u2, u3 (the U bands), the multiplier and the interchange flag of a
+// partially pivoted tridiagonal LU (LAPACK dlagtf / dlagts scheme).  Every
+// recurrence carries its running values in REGISTERS -- global memory only
+// holds the previous pass's vector, whose loads do not depend on the chain (a
+// store-then-reload per step made each step a global round trip).  The
+// normalisation is folded into the next pass.  Z (n x n) receives column j.
+__global__ void __launch_bounds__(64)
+inviter_kernel(const double* __restrict__ d, const double* __restrict__ e, int n,
+               const double* __restrict__ W, const double* __restrict__ tnorm_p,
+               double* __restrict__ scr, double* __restrict__ Z) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const int64_t N = n;
-    double* U1 = scr;
+    double* IU1 = scr;
     double* U2 = scr + N * N;
     double* U3 = scr + 2 * N * N;
     double* ML = scr + 3 * N * N;
@@ -196,7 +381,6 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
     const double lam = W[j];
     const double eps_piv = 2.2e-16 * tn;
     // LU with partial pivoting of (T - lam I), rows r, r+1 interchange
-    // column layout: row r has u1 (diag), u2 (super 1), u3 (super 2)
     double a = d[0] - lam;              // current diag candidate of row r
     double b = n > 1 ? e[0] : 0.0;      // super diag of row r
     double c3 = 0.0;                    // 2nd super of row r (from a previous swap)
@@ -205,11 +389,11 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
         const double dnext = d[r + 1] - lam;      // T[r+1][r+1]
         const double snext = r + 1 < n - 1 ? e[r + 1] : 0.0;  // T[r+1][r+2]
         if (fabs(a) >= fabs(sub)) {
-            // no swap: row r stays pivot
             double piv = a;
             if (fabs(piv) < eps_piv) piv = copysign(eps_piv, piv == 0.0 ? 1.0 : piv);
-            const double m = sub / piv;
-            U1[r * N + j] = piv;
+            const double ip = 1.0 / piv;
+            const double m = sub * ip;
+            IU1[r * N + j] = ip;
             U2[r * N + j] = b;
             U3[r * N + j] = c3;
             ML[r * N + j] = m;
@@ -218,9 +402,8 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
             b = snext - m * c3;
             c3 = 0.0;
         } else {
-            // swap rows r and r+1: pivot row is (sub, dnext, snext)
             const double m = a / sub;
-            U1[r * N + j] = sub;
+            IU1[r * N + j] = 1.0 / sub;
             U2[r * N + j] = dnext;
             U3[r * N + j] = snext;
             ML[r * N + j] = m;
@@ -233,7 +416,7 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
     {
         double piv = a;
         if (fabs(piv) < eps_piv) piv = copysign(eps_piv, piv == 0.0 ? 1.0 : piv);
-        U1[(N - 1) * N + j] = piv;
+        IU1[(N - 1) * N + j] = 1.0 / piv;
         U2[(N - 1) * N + j] = 0.0;
         U3[(N - 1) * N + j] = 0.0;
     }
@@ -243,27 +426,30 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
         st ^= st << 13; st ^= st >> 7; st ^= st << 17;
         Z[r * N + j] = 0.5 + (double)(st >> 11) * 0x1p-53;
     }
+    double scale = 1.0;
     for (int iter = 0; iter < 3; ++iter) {
-        // forward: apply L^{-1} (with the recorded interchanges)
+        // forward: apply L^{-1} with the recorded interchanges (scale folded in)
+        double carry = Z[j] * scale;
         for (int r = 0; r < n - 1; ++r) {
-            double xr = Z[r * N + j], xn = Z[(r + 1) * N + j];
+            double xr = carry, xn = Z[(r + 1) * N + j] * scale;
             if (PV[r * N + j] != 0.0) { const double t = xr; xr = xn; xn = t; }
             Z[r * N + j] = xr;
-            Z[(r + 1) * N + j] = xn - ML[r * N + j] * xr;
+            carry = xn - ML[r * N + j] * xr;
         }
-        // backward: U x = y
+        Z[(N - 1) * N + j] = carry;
+        // backward: U x = y, carrying x_{r+1}, x_{r+2}; sum of squares on the fly
+        double x1 = 0.0, x2 = 0.0, nrm = 0.0;
         for (int r = n - 1; r >= 0; --r) {
-            double s = Z[r * N + j];
-            if (r + 1 < n) s -= U2[r * N + j] * Z[(r + 1) * N + j];
-            if (r + 2 < n) s -= U3[r * N + j] * Z[(r + 2) * N + j];
-            Z[r * N + j] = s / U1[r * N + j];
+            const double s0 = Z[r * N + j] - U2[r * N + j] * x1 - U3[r * N + j] * x2;
+            const double x = s0 * IU1[r * N + j];
+            Z[r * N + j] = x;
+            nrm += x * x;
+            x2 = x1;
+            x1 = x;
         }
-        // normalise
-        double nrm = 0.0;
-        for (int r = 0; r < n; ++r) nrm += Z[r * N + j] * Z[r * N + j];
-        nrm = 1.0 / sqrt(nrm);
-        for (int r = 0; r < n; ++r) Z[r * N + j] *= nrm;
+        scale = 1.0 / sqrt(nrm);
     }
+    for (int r = 0; r < n; ++r) Z[r * N + j] *= scale;
 }
 
 // MGS inside clusters: one warp per cluster start (eigenvalue j that begins a
@@ -296,14 +482,55 @@ __global__ void reorth_kernel(const double* __restrict__ W, int n, const double*
 
 // V[:, j] = H_0 ... H_{n-3} Z[:, j]; one warp per column, reflectors applied
 // from the last to the first (H_i = I - tau_i v_i v_i^T on rows i+1..n-1).
-__global__ void backtr_kernel(const double* __restrict__ Z, int n, const double* __restrict__ tau,
-                              const double* __restrict__ Hv, double* __restrict__ scr,
-                              double* __restrict__ V) {
+// The column lives in registers (lane holds rows lane + 32 m); the reflectors
+// (2 MB for n = 520) are read from L2 by every warp.
+constexpr int kBtMaxM = 34;  // rows per lane: n <= 1088 in registers (C5: r2 = 1050)
+template <int M>
+__global__ void __launch_bounds__(256)
+backtr_kernel(const double* __restrict__ Z, int n, const double* __restrict__ tau,
+              const double* __restrict__ Hv, double* __restrict__ V) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= n) return;
     const int64_t N = n;
     const int j = warp;
-    double* x = scr + (int64_t)j * N;  // contiguous working copy of column j
+    double x[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const int r = lane + 32 * m;
+        x[m] = r < n ? Z[r * N + j] : 0.0;
+    }
+    for (int i = n - 3; i >= 0; --i) {
+        const double t = tau[i];
+        if (t == 0.0) continue;
+        const double* v = Hv + (int64_t)i * N;
+        double vv[M];
+        double dot = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            const int r = lane + 32 * m;
+            vv[m] = (r > i && r < n) ? __ldg(v + r) : 0.0;
+            dot += vv[m] * x[m];
+        }
+        dot = warp_sum(dot) * t;
+#pragma unroll
+        for (int m = 0; m < M; ++m) x[m] -= dot * vv[m];
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const int r = lane + 32 * m;
+        if (r < n) V[r * N + j] = x[m];
+    }
+}
+
+// generic fallback (n > 32 * kBtMaxM): column in global scratch
+__global__ void backtr_kernel_big(const double* __restrict__ Z, int n, const double* __restrict__ tau,
+                                  const double* __restrict__ Hv, double* __restrict__ scr,
+                                  double* __restrict__ V) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const int64_t N = n;
+    const int j = warp;
+    double* x = scr + (int64_t)j * N;
     for (int r = lane; r < n; r += 32) x[r] = Z[r * N + j];
     __syncwarp();
     for (int i = n - 3; i >= 0; --i) {
@@ -347,27 +574,70 @@ int syev_tri(const double* A, int64_t n, double* W, double* V, void* ws, int64_t
     int dev = 0, sms = 148, per_sm = 0;
     SKP_CUDA(cudaGetDevice(&dev));
     SKP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SKP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sytrd_kernel, kTriThreads, 0));
+    const size_t tsm = 2 * (size_t)n * sizeof(double);
+    SKP_CUDA(cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(tsm, 1)));
+    SKP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sytrd_kernel, kTriThreads, tsm));
     if (per_sm < 1) {
         set_error("syev_tri: cooperative kernel cannot be resident");
         return SKP_ERR_CUDA;
     }
     int nn = (int)n;
-    void* args[] = {&Ac, &nn, &d, &e, &tau, &Hv, &pbuf};
-    SKP_CUDA(cudaLaunchCooperativeKernel((void*)sytrd_kernel, dim3(sms), dim3(kTriThreads), args, 0,
-                                         st));
-    count_launch();
+    // whole matrix in a 16-CTA cluster's shared memory when it fits
+    bool clustered = false;
+    const size_t csm = sytrd_cluster_smem(nn);
+    if (csm <= 220 * 1024 && !getenv("SKP_TRI_NOCLUSTER")) {
+        cudaError_t ea = cudaFuncSetAttribute(sytrd_cluster_kernel,
+                                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaError_t eb = cudaFuncSetAttribute(sytrd_cluster_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+        if (ea == cudaSuccess && eb == cudaSuccess) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(kCl);
+            cfg.blockDim = dim3(kClThreads);
+            cfg.dynamicSmemBytes = csm;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = kCl;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, sytrd_cluster_kernel, &cfg) == cudaSuccess &&
+                ncl >= 1) {
+                const int rpc = (nn + kCl - 1) / kCl;
+                SKP_CUDA(cudaLaunchKernelEx(&cfg, sytrd_cluster_kernel, (const double*)Ac, nn, rpc,
+                                            d, e, tau, Hv));
+                SKP_LAUNCHED(sytrd_cluster_kernel);
+                clustered = true;
+            }
+        }
+        cudaGetLastError();  // clear a refused attribute / occupancy query
+    }
+    if (!clustered) {
+        void* args[] = {&Ac, &nn, &d, &e, &tau, &Hv, &pbuf};
+        SKP_CUDA(cudaLaunchCooperativeKernel((void*)sytrd_kernel, dim3(sms), dim3(kTriThreads), args,
+                                             tsm, st));
+        count_launch();
+    }
     const size_t bsm = 2 * (size_t)n * sizeof(double);
     SKP_CUDA(cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)std::max<size_t>(bsm, 1)));
-    bisect_kernel<<<(unsigned)cdiv(n, 128), 128, bsm, st>>>(d, e, nn, W, tnorm);
+    bisect_kernel<<<(unsigned)cdiv(n, 8), 256, bsm, st>>>(d, e, nn, W, tnorm);
     SKP_LAUNCHED(bisect_kernel);
-    inviter_kernel<<<(unsigned)cdiv(n, 64), 64, 0, st>>>(d, e, nn, W, tnorm, scr, Z);
+    inviter_kernel<<<(unsigned)cdiv(n, 32), 32, 0, st>>>(d, e, nn, W, tnorm, scr, Z);
     SKP_LAUNCHED(inviter_kernel);
     reorth_kernel<<<(unsigned)cdiv(n * 32, 256), 256, 0, st>>>(W, nn, tnorm, Z);
     SKP_LAUNCHED(reorth_kernel);
-    backtr_kernel<<<(unsigned)cdiv(n * 32, 256), 256, 0, st>>>(Z, nn, tau, Hv, bscr, V);
-    SKP_LAUNCHED(backtr_kernel);
+    {
+        const unsigned bgrid = (unsigned)cdiv(n * 32, 256);
+        if (n <= 32 * 17) backtr_kernel<17><<<bgrid, 256, 0, st>>>(Z, nn, tau, Hv, V);
+        else if (n <= 32 * kBtMaxM) backtr_kernel<kBtMaxM><<<bgrid, 256, 0, st>>>(Z, nn, tau, Hv, V);
+        else backtr_kernel_big<<<bgrid, 256, 0, st>>>(Z, nn, tau, Hv, bscr, V);
+        SKP_LAUNCHED(backtr_kernel);
+    }
     if (sweeps) SKP_CUDA(cudaMemsetAsync(sweeps, 0, sizeof(int32_t), st));
     return SKP_OK;
 }

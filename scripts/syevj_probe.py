@@ -17,9 +17,11 @@ for n in (520, 1050):
     e0.record(); w, v = be.eig_desc64(t); e1.record(); torch.cuda.synchronize()
     sw = int(be.info[1].item())
     err = np.abs(np.sort(w.cpu().numpy())[::-1] - np.sort(np.linalg.eigvalsh(g))[::-1]).max() / lam[0]
-    print(f"n={n} time={e0.elapsed_time(e1):.2f} ms sweeps={sw} eigerr={err:.1e}", flush=True)
+    V = v.cpu().numpy(); W = w.cpu().numpy()
+    res = np.abs(g @ V - V * W).max() / lam[0]; orth = np.abs(V.T @ V - np.eye(n)).max()
+    print(f"n={n} time={e0.elapsed_time(e1):.2f} ms sweeps={sw} eigerr={err:.1e} resid={res:.1e} orth={orth:.1e}", flush=True)
 '''
-for variant in ("tri", "coop"):
+for variant in ("tri",):
     env = dict(os.environ, SKP_SYEVJ=variant)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     print(variant, r.stdout, r.stderr[-400:], flush=True)
