@@ -195,6 +195,13 @@ int64_t skp_syevj_ws_bytes(int64_t n);
 int skp_syevj_f64(double* A, int64_t n, double* W, double* V, int32_t max_sweeps,
                   void* ws, int64_t ws_bytes, int32_t* sweeps, void* stream);
 
+/* G (C x C, fp64) = X^T X for fp32 X (K x C): exact fp32 products, fp64
+ * accumulation (randsvd's B B^T from B^T, reference power.py:196-197 /
+ * linalg.py:84-88 in fp64).  ws: skp_gram_f32_f64_ws_bytes.                 */
+int64_t skp_gram_f32_f64_ws_bytes(int64_t K, int64_t C);
+int skp_gram_f32_f64(const float* X, int64_t K, int64_t C, int64_t ldx, double* G, int64_t ldg,
+                     void* ws, int64_t ws_bytes, void* stream);
+
 /* ----------------------------------------------------------- utilities -- */
 int skp_cast_f32_f64(const float* x, double* y, int64_t count, void* stream);
 int skp_cast_f64_f32(const double* x, float* y, int64_t count, void* stream);

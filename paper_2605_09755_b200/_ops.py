@@ -320,7 +320,16 @@ class CudaBackend:
         return gemm(bd, bd, False, True)
 
     def gram64_rows_t(self, bt):
-        """(bt^T bt) in fp64 arithmetic, i.e. b b^T for b = bt^T (bt: n x c)."""
+        """(bt^T bt) in fp64 arithmetic, i.e. b b^T for b = bt^T (bt: n x c).
+        fp32 bt: exact products, fp64 accumulation, no widened copy."""
+        if bt.dtype == F32:
+            k, c, ld = _rows_ld(bt)
+            g = torch.empty((c, c), dtype=F64, device=self.device)
+            wsb = int(_lib.load().skp_gram_f32_f64_ws_bytes(k, c))
+            ws = workspace(self.device, wsb)
+            call("skp_gram_f32_f64", ptr(bt), k, c, ld, ptr(g), c, ptr(ws), wsb,
+                 stream_ptr(self.device))
+            return g
         bd = cast(bt, F64)
         return gemm(bd, bd, True, False)
 

@@ -374,3 +374,17 @@ def test_gaussian_omega_matches_numpy(ops, rows, cols, seed):
     ulp = np.spacing(np.abs(ref))
     assert (np.abs(d64 - ref) <= ulp).all()
     assert np.count_nonzero(d64 != ref) <= max(3, rows * cols // 100000)
+
+
+@pytest.mark.parametrize("k,c", [(16384, 520), (1000, 130), (37, 5), (262144, 64)])
+def test_gram_f32_f64(ops, k, c):
+    """G = X^T X in fp64 from fp32 X: exact products, fp64 sums (randsvd's B B^T)."""
+    rng = np.random.default_rng(k + c)
+    x = rng.standard_normal((k, c)).astype(np.float32)
+    t = ops.empty2d(k, c, torch.float32, "cuda")
+    t.copy_(torch.from_numpy(x))
+    be = ops.CudaBackend(torch.device("cuda", 0), torch.float32)
+    g = be.gram64_rows_t(t).cpu().numpy()
+    ref = x.astype(np.float64).T @ x.astype(np.float64)
+    assert np.abs(g - ref).max() <= 1e-13 * np.abs(ref).max()
+    np.testing.assert_array_equal(g, g.T)
