@@ -88,9 +88,11 @@ int skp_sketch_right_f64(const double* A, int64_t lda, int64_t m, int64_t n,
 
 /* K2 v2 (fp32, range-finder path): the same product written with PERMUTED
  * output columns, out = (A . S) P, by a row gather with a register-resident,
- * bank-conflict-free schedule.  P sorts the columns of each 768-column slice
- * by entry count; its table is plan[0 .. slices*768) (int32 column of S, -1
- * past r).  Build the plan once per sketch (skp_sketch_gather_plan, from the
+ * bank-conflict-free schedule.  The r columns are cut into ceil(r/768)
+ * equal slices (one CTA each); P sorts the columns of each slice by entry
+ * count; its table is plan[0 .. r) (int32 column of S at each output
+ * position; -1 from r to slices*768).  Build the plan once per sketch
+ * (skp_sketch_gather_plan, from the
  * CSC view); it is usable iff the int32 at byte offset
  * skp_sketch_gather_plan_fail_offset(r) is 0 after the build -- or, without a
  * host check, run skp_sketch_gather_f32 anyway: with a failed plan it writes

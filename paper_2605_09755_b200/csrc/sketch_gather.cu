@@ -22,17 +22,23 @@
 // writes A~ P, and the range finder multiplies by P^T Omega instead of Omega
 // (Y = A~ Omega = (A~ P)(P^T Omega)); apply_right keeps K2 v1's column order.
 //
-// CTA = one slice of kGCols = 768 output columns (24 warps); the last warp to
-// finish a row refills its buffer (bulk copy of the row two ahead).  Grid = G row groups x P slices; CTAs of a row
-// group walk the same rows at the same time, so the P-fold reuse of each row
-// is served by L2 and A is read from HBM once.  Non-finite test: every column
-// of A feeds s >= 1 nonzero (+-1/sqrt(s)) entries, so A has a non-finite entry
-// iff A~ does -- each thread tests the value it stores (one instruction per
-// row; a fused fp64 ||A||^2 here cost 20% of the kernel).  ||A||_F^2, when
-// asked for, is a separate HBM-bound pass (skp_sumsq).
+// CTA = one slice of <= kGCols = 768 output columns (24 warps; the slices are
+// balanced to gather_width columns each); the last warp to finish a row
+// refills its buffer (bulk copy of the row two ahead).  Grid = G row groups x
+// P slices.  The CTAs of a row group read the same rows but drift apart, so
+// ~3x |A| comes from HBM (ncu, C3: 50 GB).  Pacing them to within L2 reach (a
+// group row counter, tested) cut that to 17.2 GB but cost 12-25% time: the
+// kernel is bound by its shared-memory gathers, not by HBM.
+//
+// Non-finite test: every column of A feeds s >= 1 nonzero (+-1/sqrt(s))
+// entries, so A has a non-finite entry iff A~ does -- each thread tests the
+// value it stores (one instruction per row; a fused fp64 ||A||^2 here cost 20%
+// of the kernel).  ||A||_F^2, when asked for, is a separate HBM-bound pass
+// (skp_sumsq).
 #include <cuda.h>
 
 #include <algorithm>
+#include <stdlib.h>
 #include <type_traits>
 
 #include "common.cuh"
@@ -99,23 +105,27 @@ __device__ __forceinline__ void g_bulk_load_e(uint32_t dst, const void* src, uin
 }
 
 // ---- plan 1: per-slice column order, sorted by entry count (descending) -----
-// perm[p*kGCols + v] = output column, or -1 past the end; one block per slice.
-__global__ void gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r,
-                                   int32_t* __restrict__ perm) {
+// Slice p owns output positions [p*width, p*width + nc_p) (width = the balanced
+// slice width, gather_width); perm[pos] = the column written at position pos
+// (compact: the first r entries), -1 for pos in [r, P*kGCols).  One block per slice.
+__global__ void gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r, int width,
+                                   int64_t slots, int32_t* __restrict__ perm) {
     __shared__ int key[kGCols];
-    const int64_t c0 = (int64_t)blockIdx.x * kGCols;
-    const int nc = (int)(r - c0 < kGCols ? r - c0 : kGCols);
+    const int64_t c0 = (int64_t)blockIdx.x * width;
+    const int nc = (int)(r - c0 < width ? r - c0 : width);
     for (int v = threadIdx.x; v < kGCols; v += blockDim.x)
         key[v] = v < nc ? colptr[c0 + v + 1] - colptr[c0 + v] : -1;
+    if (blockIdx.x == 0)
+        for (int64_t v = r + threadIdx.x; v < slots; v += blockDim.x) perm[v] = -1;
     __syncthreads();
-    for (int v = threadIdx.x; v < kGCols; v += blockDim.x) {
+    for (int v = threadIdx.x; v < nc; v += blockDim.x) {
         const int kv = key[v];
         int rank = 0;
-        for (int u = 0; u < kGCols; ++u) {
+        for (int u = 0; u < nc; ++u) {
             const int ku = key[u];
             rank += (ku > kv) || (ku == kv && u < v);
         }
-        perm[c0 + rank] = v < nc ? (int32_t)(c0 + v) : -1;
+        perm[c0 + rank] = (int32_t)(c0 + v);
     }
 }
 
@@ -131,14 +141,16 @@ __global__ void gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r
 // without an entry read a zero word in a distinct free bank.
 __global__ void __launch_bounds__(128)
 gather_sched_kernel(const int32_t* __restrict__ colptr, const int32_t* __restrict__ entries,
-                    const int32_t* __restrict__ perm, int nwarps, int64_t n,
-                    uint32_t* __restrict__ sched, int32_t* __restrict__ tw,
+                    const int32_t* __restrict__ perm, int nwarps, int64_t n, int64_t r,
+                    int width, uint32_t* __restrict__ sched, int32_t* __restrict__ tw,
                     int32_t* __restrict__ fail) {
     const int wg = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (wg >= nwarps) return;
     const uint32_t zero_word = (uint32_t)((n + 31) / 32 * 32);  // 32 zero words after the row
-    const int c = perm[wg * 32 + lane];
+    const int local = (wg % kGW) * 32 + lane;          // position inside the slice
+    const int64_t pos = (int64_t)(wg / kGW) * width + local;
+    const int c = (local < width && pos < r) ? perm[pos] : -1;
     const int beg = c >= 0 ? colptr[c] : 0;
     const int cnt = c >= 0 ? colptr[c + 1] - colptr[c] : 0;
     if (__any_sync(0xffffffffu, cnt > kGTMax)) {
@@ -234,10 +246,11 @@ gather_sched_kernel(const int32_t* __restrict__ colptr, const int32_t* __restric
 
 // ---- the gather ----------------------------------------------------------------
 __global__ void __maxnreg__(80)
-sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n, int P,
-                     const uint32_t* __restrict__ sched, const int32_t* __restrict__ tw,
-                     const int32_t* __restrict__ perm, const int32_t* __restrict__ plan_fail,
-                     float scale, float* __restrict__ out, int64_t ldo, int64_t* nonfinite) {
+sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n, int64_t r,
+                     int P, int width, const uint32_t* __restrict__ sched,
+                     const int32_t* __restrict__ tw, const int32_t* __restrict__ plan_fail,
+                     float scale, float* __restrict__ out, int64_t ldo,
+                     int64_t* nonfinite) {
     extern __shared__ __align__(128) unsigned char sm[];
     if (*plan_fail) {
         // the plan's schedule overflowed: report it through the non-finite
@@ -285,8 +298,8 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
         // (steps >= kGTReg, if any, are read per row below)
         e[t] = v + base;  // absolute smem address in buffer 0; bit 31 (sign) kept
     }
-    const int v_out = slice * kGCols + warp * 32 + lane;
-    const bool valid = perm[v_out] >= 0;
+    const int64_t v_out = (int64_t)slice * width + warp * 32 + lane;  // output position
+    const bool valid = warp * 32 + lane < width && v_out < r;
     bool bad = false;  // a non-finite output of this thread (iff a non-finite input)
 
     auto do_row = [&](int64_t i, int b, uint32_t ph, auto boff_c) {
@@ -365,6 +378,12 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
 // plan layout (bytes): perm int32[P*kGCols] | tw int32[P*kGW] | fail int32 |
 //                      pad to 16 | sched uint32[P*kGW*kGTMax*32]
 int gather_slices(int64_t r) { return (int)cdiv(r, (int64_t)kGCols); }
+// balanced slice width: the P slices share the r columns evenly (multiple of
+// 32), so no CTA carries a short last slice while its SM idles (C3: 6 x 672
+// instead of 5 x 768 + 160)
+int gather_width(int64_t r) {
+    return (int)(cdiv(cdiv(r, (int64_t)gather_slices(r)), 32) * 32);
+}
 int64_t gather_plan_bytes(int64_t r) {
     const int64_t P = gather_slices(r);
     const int64_t head = (P * kGCols + P * kGW + 1) * 4;
@@ -387,11 +406,12 @@ int gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n, int64_
     uint32_t* sched =
         reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(plan) + (head + 15) / 16 * 16);
     SKP_CUDA(cudaMemsetAsync(fail, 0, 4, st));
-    gather_sort_kernel<<<P, 256, 0, st>>>(colptr, r, perm);
+    const int width = gather_width(r);
+    gather_sort_kernel<<<P, 256, 0, st>>>(colptr, r, width, (int64_t)P * kGCols, perm);
     SKP_LAUNCHED(gather_sort_kernel);
     const int nw = P * kGW;
-    gather_sched_kernel<<<(unsigned)cdiv(nw, 4), 128, 0, st>>>(colptr, entries, perm, nw, n,
-                                                                sched, tw, fail);
+    gather_sched_kernel<<<(unsigned)cdiv(nw, 4), 128, 0, st>>>(colptr, entries, perm, nw, n, r,
+                                                                width, sched, tw, fail);
     SKP_LAUNCHED(gather_sched_kernel);
     return SKP_OK;
 }
@@ -412,16 +432,16 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int P = gather_slices(r);
     const int G = std::max(1, std::min<int>(sms / P, (int)std::min<int64_t>(m, 1 << 20)));
-    const int32_t* perm = reinterpret_cast<const int32_t*>(plan);
-    const int32_t* tw = perm + (int64_t)P * kGCols;
+    const int32_t* tw = reinterpret_cast<const int32_t*>(plan) + (int64_t)P * kGCols;
     const int32_t* pfail = tw + (int64_t)P * kGW;
     const int64_t head = ((int64_t)P * kGCols + P * kGW + 1) * 4;
     const uint32_t* sched = reinterpret_cast<const uint32_t*>(
         reinterpret_cast<const char*>(plan) + (head + 15) / 16 * 16);
     SKP_CUDA(cudaFuncSetAttribute(sketch_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kGSmem));
-    sketch_gather_kernel<<<G * P, kGThreads, kGSmem, st>>>(A, lda, m, n, P, sched, tw, perm, pfail,
-                                                           scale, out, ldo, nonfinite);
+    sketch_gather_kernel<<<G * P, kGThreads, kGSmem, st>>>(A, lda, m, n, r, P, gather_width(r),
+                                                           sched, tw, pfail, scale, out, ldo,
+                                                           nonfinite);
     SKP_LAUNCHED(sketch_gather_kernel);
     if (fro2) {  // ||A||_F^2: a separate HBM-bound pass (only when asked for)
         const int rc = skp_sumsq_f32(A, m, n, lda, fro2, nullptr, st);

@@ -13,7 +13,10 @@ def timeit(f, reps=5):
     e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
 
-for (m, n, l) in [(262144, 16384, 4000), (262144, 16384, 8000), (65536, 24576, 4096)]:
+SHAPES = [(262144, 16384, 4000), (262144, 16384, 8000), (65536, 24576, 4096)]
+if len(sys.argv) > 1:
+    SHAPES = SHAPES[:int(sys.argv[1])]
+for (m, n, l) in SHAPES:
     a = _ops.empty2d(m, n, torch.float32, "cuda"); a.normal_()
     op = make_sketch("countsketch", n, l, 7, s=8)
     out = _ops.empty2d(m, l, torch.float32, "cuda")

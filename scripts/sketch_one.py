@@ -1,13 +1,21 @@
-"""One C3-shape sketch apply (for ncu)."""
+"""One C3-shape sketch apply (for ncu): python scripts/sketch_one.py [v2|v1] [m n l]
+
+v2 = the row-gather kernel the range finder runs (permuted output columns),
+v1 = the rows-in-lanes ELL kernel (fallback)."""
 import sys
 import torch
 sys.path.insert(0, ".")
 from paper_2605_09755_b200.sketching import make_sketch
-m, n, l = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (262144, 16384, 4000)))
+mode = sys.argv[1] if len(sys.argv) > 1 else "v2"
+m, n, l = (int(x) for x in (sys.argv[2:5] if len(sys.argv) > 4 else (262144, 16384, 4000)))
 a = torch.randn(m, n, device="cuda")
 op = make_sketch("countsketch", n, l, 7, s=8)
 out = torch.empty(m, l, device="cuda")
+nonfinite = torch.zeros(1, dtype=torch.int64, device="cuda")
 for _ in range(2):
-    op.right(a, out=out)
+    if mode == "v2":
+        assert op.right_permuted(a, out=out, nonfinite=nonfinite) is not None
+    else:
+        op.right(a, out=out, nonfinite=nonfinite)
 torch.cuda.synchronize()
 print("ok")
