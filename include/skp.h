@@ -212,6 +212,26 @@ int skp_cast2d_f32_f64(const float* x, int64_t ldx, double* y, int64_t ldy, int6
                        int64_t cols, void* stream);
 int skp_cast2d_f64_f32(const double* x, int64_t ldx, float* y, int64_t ldy, int64_t rows,
                        int64_t cols, void* stream);
+/* ------------------------------------------------------------ 3xFP16 ----
+ * FP32 GEMM on the kind::f16 tensor cores from PRE-SPLIT operands (K4h,
+ * gemm_h3.cu) -- the power-iteration products of power.py:129-133.
+ * skp_split_h2_f32: X (rows x cols, ld) -> hi, lo (fp16 planes, ldh) with
+ * X 2^e ~= hi + lo, e = e_io[0] = 15 - ceil(log2 max|X|) (written on the
+ * device; e_io[1] is scratch); trans=1 writes X^T (cols x rows).
+ * skp_gemm_h3: C = alpha op(A) B^T + beta C, computed as 2^-(ea+eb) times
+ * the fp32-accumulated A_lo B_hi + A_hi B_lo + A_hi B_hi, with op(A) = A
+ * (M x K, transA=0) or A^T (A stored K x M, transA=1, lda % 64 == 0) and B
+ * stored N x K.  Planes 16-byte aligned, ld % 8 == 0.  Accuracy ~2^-22 per
+ * product (3xTF32: 2^-20).
+ * ws: skp_gemm_h3_ws_bytes (split-K partials; 0 = none needed).            */
+int skp_split_h2_f32(const float* X, int64_t rows, int64_t cols, int64_t ld, int32_t trans,
+                     void* hi, void* lo, int64_t ldh, int32_t* e_io, void* stream);
+int64_t skp_gemm_h3_ws_bytes(int transA, int64_t M, int64_t N, int64_t K);
+int skp_gemm_h3(int transA, int64_t M, int64_t N, int64_t K, float alpha, const void* A_hi,
+                const void* A_lo, int64_t lda, const int32_t* a_exp, const void* B_hi,
+                const void* B_lo, int64_t ldb, const int32_t* b_exp, float beta, float* C,
+                int64_t ldc, void* ws, int64_t ws_bytes, void* stream);
+
 /* Row gather y[v, :] = x[perm[v], :], v < rows (P^T Omega for the K2 v2
  * column permutation; perm = the first `rows` int32 of a gather plan).       */
 int skp_permute_rows_f32(const float* x, int64_t ldx, const int32_t* perm, float* y, int64_t ldy,

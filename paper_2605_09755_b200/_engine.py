@@ -92,7 +92,10 @@ def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: b
 def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_total=None,
                   lazy: bool = False):
     """power.py:113-134 on a row slab of A~: Y = A~ Omega, then q x
-    {orth(Y) if stabilized; Z = sum_p A~_p^T Y_p; Y = A~ Z}."""
+    {orth(Y) if stabilized; Z = sum_p A~_p^T Y_p; Y = A~ Z}.  A~ feeds all
+    1 + 2q products, so it is prepared once (be.prepare: the fp16 split of
+    the 3xFP16 GEMM on the CUDA backend)."""
+    atil = be.prepare(atil)
     y = be.mm(atil, omega)
     for _ in range(q):
         if stabilized:

@@ -7,6 +7,7 @@ or the CPU.  ``CudaBackend`` is the compute backend the algorithm engine
 """
 from __future__ import annotations
 
+import os
 import threading
 
 import numpy as np
@@ -255,6 +256,58 @@ def gemm(a, b, ta: bool = False, tb: bool = False, alpha: float = 1.0, beta: flo
     return out
 
 
+# ------------------------------------------------ 3xFP16 (pre-split) GEMM --
+
+H3_MIN_ELEMS = 1 << 22   # prepare() splits left operands of at least this many entries
+
+
+class SplitH2:
+    """fp16 two-term split of an fp32 matrix with one power-of-two scale:
+    x 2^e ~= hi + lo (skp_split_h2_f32).  ``t`` (rows x cols as stored in the
+    planes) is the source or, with trans=True, its transpose; planes have
+    128-byte rows (ld % 64 == 0) so either major-ness can be TMA-loaded."""
+    __slots__ = ("hi", "lo", "e", "rows", "cols", "ld")
+
+    def __init__(self, hi, lo, e, rows, cols, ld):
+        self.hi, self.lo, self.e, self.rows, self.cols, self.ld = hi, lo, e, rows, cols, ld
+
+
+def split_h2(x: torch.Tensor, trans: bool = False, out: "SplitH2 | None" = None) -> SplitH2:
+    r, c, ld = _rows_ld(x)
+    if x.dtype != F32:
+        raise ValueError("split_h2 needs float32")
+    rows, cols = (c, r) if trans else (r, c)
+    ldh = max(64, (cols + 63) // 64 * 64)
+    if out is None or out.rows != rows or out.cols != cols:
+        buf = torch.empty((2, rows, ldh), dtype=torch.float16, device=x.device)
+        out = SplitH2(buf[0], buf[1], torch.zeros(2, dtype=torch.int32, device=x.device),
+                      rows, cols, ldh)
+    call("skp_split_h2_f32", ptr(x), r, c, ld, int(trans), ptr(out.hi), ptr(out.lo), out.ld,
+         ptr(out.e), stream_ptr(x.device))
+    return out
+
+
+def gemm_h3(a: SplitH2, b: SplitH2, ta: bool = False, alpha: float = 1.0, beta: float = 0.0,
+            out=None) -> torch.Tensor:
+    """K4h: out = alpha op(a) b^T + beta out from pre-split operands: op(a) =
+    a (M x K) or a^T (a stored K x M, ta=True); b stored N x K."""
+    M, K = (a.cols, a.rows) if ta else (a.rows, a.cols)
+    N, Kb = b.rows, b.cols
+    if K != Kb:
+        raise ValueError(f"dimension mismatch: {M}x{K} @ {Kb}x{N}")
+    if out is None:
+        if beta != 0.0:
+            raise ValueError("beta != 0 needs out")
+        out = empty2d(M, N, F32, a.hi.device)
+    _, _, ldc = _rows_ld(out)
+    lib = _lib.load()
+    wsb = lib.skp_gemm_h3_ws_bytes(int(ta), M, N, K)
+    ws = workspace(a.hi.device, wsb) if wsb else None
+    call("skp_gemm_h3", int(ta), M, N, K, alpha, ptr(a.hi), ptr(a.lo), a.ld, ptr(a.e), ptr(b.hi),
+         ptr(b.lo), b.ld, ptr(b.e), beta, ptr(out), ldc, ptr(ws), wsb, stream_ptr(a.hi.device))
+    return out
+
+
 # ------------------------------------------------------------ utilities ----
 
 def cast(x: torch.Tensor, dtype) -> torch.Tensor:
@@ -305,10 +358,32 @@ class CudaBackend:
         self.gemm_mode = gemm_mode if dtype == F32 else "auto"
         self.info = torch.zeros(2, dtype=torch.int32, device=device)
         self.fail = torch.zeros(2, dtype=torch.int32, device=device)
+        self._bsplit = {}
 
     # dense products in the compute dtype
     def mm(self, a, b, ta=False, tb=False, out=None, alpha=1.0, beta=0.0):
+        if isinstance(a, SplitH2):
+            # pre-split left operand (prepare): 3xFP16; b split (transposed) per call
+            if tb:
+                raise ValueError("mm: a pre-split left operand takes a K x N right operand")
+            key = tuple(b.shape)
+            self._bsplit[key] = sb = split_h2(b, trans=True, out=self._bsplit.get(key))
+            return gemm_h3(a, sb, ta=ta, alpha=alpha, beta=beta, out=out)
         return gemm(a, b, ta, tb, alpha=alpha, beta=beta, out=out, mode=self.gemm_mode)
+
+    def prepare(self, x):
+        """A left operand reused by several products (the power iteration's
+        A~): split once into fp16 hi/lo planes for the 3xFP16 GEMM (twice the
+        3xTF32 rate at 22-bit operand accuracy).  Returns x itself where that
+        does not apply (fp64, explicit GEMM modes, small operands, no
+        tcgen05) or is switched off (SKP_NO_H3)."""
+        if isinstance(x, SplitH2) or self.dtype != F32 or self.gemm_mode != "auto":
+            return x
+        if x.dim() != 2 or x.shape[0] * x.shape[1] < H3_MIN_ELEMS or os.environ.get("SKP_NO_H3"):
+            return x
+        if not _lib.load().skp_has_tcgen05():
+            return x
+        return split_h2(x)
 
     def gram64(self, y):
         """y^T y as fp64 (computed in the compute dtype, then widened)."""

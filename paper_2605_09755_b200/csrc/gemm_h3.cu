@@ -1,0 +1,710 @@
+// K4h: FP32 GEMM from PRE-SPLIT fp16 operands on the sm_100a tensor cores
+// ("3xFP16"), tcgen05.mma.kind::f16 with fp32 accumulation in TMEM.
+//
+//   x * 2^e = x_hi + x_lo + O(2^-22 |x| 2^e),   x_hi = fp16(x 2^e),
+//   x_lo = fp16(x 2^e - x_hi),  e = 15 - ceil(log2 max|X|)  (one power of two
+//   per matrix, so max|x| 2^e lies in [2^14, 2^15): no fp16 overflow, and the
+//   bulk of the entries far above the fp16 subnormal range)
+//   a.b ~= 2^-(ea+eb) (a_lo b_hi + a_hi b_lo + a_hi b_hi)
+//
+// Why: 3xTF32 (gemm_tc.cu) already runs the TF32 tensor pipe at ~93% of its
+// peak; the only way past it is a faster pipe.  kind::f16 runs at twice the
+// TF32 rate, and an 11+11-bit fp16 pair carries the same 22 significant bits
+// as a TF32 hi/lo pair (fp16's narrow exponent range is what the per-matrix
+// power-of-two scale handles).  Per-product error 2^-22 vs 3xTF32's 2^-20.
+//
+// The operands are split ONCE per matrix in HBM (skp_split_h2_f32: hi and lo
+// planes of 2 bytes each = the fp32 footprint), not per tile: A~ (m x l) is
+// reused by all 1+2q power-iteration products, and with no split warps the
+// kernel is a plain TMA -> MMA -> epilogue pipeline whose shared-memory traffic
+// (TMA writes + operand reads) stays under the 128 B/clk the split version
+// would have exceeded at the f16 rate.
+//
+// One persistent CTA (or CTA pair) per SM, warp-specialised (6 warps):
+//   warp 0     TMA producer: A_hi, A_lo, B_hi, B_lo tiles -> smem ring
+//   warp 1     MMA issuer (leader CTA): 12 tcgen05.mma per stage (4 K-steps of
+//              16 x 3 products), both operands from shared memory
+//   warps 2-5  epilogue: tcgen05.ld -> 2^-(ea+eb) alpha (+ beta C) -> global
+// Operand layouts: A K-major (op(A) = A, M x K, K contiguous) or MN-major
+// (op(A) = A^T, A stored K x M) -- SWIZZLE_128B, 64 fp16 per 128-byte row;
+// B always K-major (stored N x K; the split kernel transposes small B's for
+// free).  CTA pair (cta_group::2, M = 256): each CTA loads its own 128 A rows
+// and half of the B tile, both CTAs' TMA signal the leader's full barrier.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <stdlib.h>
+#include <stdio.h>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace skp {
+namespace {
+
+constexpr int HM = 128;          // UMMA M per CTA
+constexpr int HK = 64;           // fp16 K per stage: one 128-byte swizzled row
+constexpr int kHKSteps = HK / 16;  // f16 UMMA K = 16
+constexpr int kHWarpTma = 0, kHWarpMma = 1, kHWarpEpi = 2, kHNumEpi = 4;
+constexpr int kHThreads = 32 * (kHWarpEpi + kHNumEpi);
+constexpr uint32_t kHTmemCols = 512;
+constexpr int kHMaxStages = 8;
+constexpr uint32_t kHChunkBytes = 64 * HK * 2;  // MN-major A: 64 M x HK K per TMA box chunk
+
+struct H3Params {
+    int M, N, K;
+    int bn, tiles_m, tiles_n, splits, kb_per_split, num_kb;
+    int a_kmajor;
+    float alpha, beta;
+    float* C;
+    long long ldc;
+    float* ws;
+    int stages;
+    uint32_t a_bytes, b_bytes, stage_bytes;
+    uint32_t idesc;
+    int acc_stride;
+    const int* a_e;
+    const int* b_e;
+};
+
+// TMA 2-D / 3-D loads signalling a barrier given by its shared::cluster
+// address (the leader CTA's barrier when paired: .cta_group::2 lets the peer's
+// copy complete_tx on it)
+template <bool kPair>
+__device__ __forceinline__ void h_tma_2d(const CUtensorMap* map, uint32_t bar_cl, uint32_t dst,
+                                         int c0, int c1) {
+    if (kPair)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+            "@p cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(c0), "r"(c1)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+            "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(c0), "r"(c1)
+            : "memory");
+}
+template <bool kPair>
+__device__ __forceinline__ void h_tma_3d(const CUtensorMap* map, uint32_t bar_cl, uint32_t dst,
+                                         int c0, int c1, int c2) {
+    if (kPair)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+            "@p cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4, %5}], [%2];\n\t}" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
+            "@p cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4, %5}], [%2];\n\t}" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2)
+            : "memory");
+}
+// D[tmem] (+)= A[smem desc] * B[smem desc], kind::f16 (fp16 in, fp32 accumulate)
+template <bool kPair>
+__device__ __forceinline__ void h_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                      uint32_t acc) {
+    if (kPair)
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t.reg .b32 r;\n\t"
+            "setp.ne.b32 q, %4, 0;\n\t"
+            "elect.sync r|p, 0xffffffff;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, q;\n\t}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t.reg .b32 r;\n\t"
+            "setp.ne.b32 q, %4, 0;\n\t"
+            "elect.sync r|p, 0xffffffff;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n\t}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+}
+
+struct HWork {
+    int tm, tn, ks, kb0, kb1;
+};
+__device__ __forceinline__ HWork h_unit(const H3Params& p, int u) {
+    // N-tiles of one M block are adjacent units: co-resident CTAs share the A
+    // row block through L2
+    HWork w;
+    w.tn = u % p.tiles_n;
+    const int r = u / p.tiles_n;
+    w.tm = r % p.tiles_m;
+    w.ks = r / p.tiles_m;
+    w.kb0 = w.ks * p.kb_per_split;
+    w.kb1 = min(w.kb0 + p.kb_per_split, p.num_kb);
+    return w;
+}
+
+template <bool kPair>
+__global__ void __launch_bounds__(kHThreads, 1)
+gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
+               const __grid_constant__ CUtensorMap map_bh, const __grid_constant__ CUtensorMap map_bl,
+               const H3Params p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = p.stages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + S;
+    uint64_t* tfull = bars + 2 * S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int units = p.tiles_m * p.tiles_n * p.splits;
+    const uint32_t rank = kPair ? cluster_rank() : 0u;
+    const bool leader = rank == 0;
+    const int ustart = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int ustride = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    constexpr int kRowsPerUnit = kPair ? 2 * HM : HM;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);  // the leader's expect_tx arrive (+ tx of both CTAs)
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], kPair ? 2 * kHNumEpi : kHNumEpi);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == kHWarpMma) {
+        if (kPair) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kHTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kHTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+    }
+    tc_fence_before();
+    if (kPair) cluster_sync_all();
+    else __syncthreads();
+    tc_fence_after();
+    const uint32_t full_cl0 = kPair ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
+    const uint32_t tempty_cl0 = kPair ? mapa_shared(smem_u32(tempty), 0) : 0u;
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t smem0 = smem_u32(smem);
+
+    if (warp == kHWarpTma) {
+        Ring r;
+        const int bcols = kPair ? p.bn / 2 : p.bn;
+        for (int u = ustart; u < units; u += ustride) {
+            const HWork w = h_unit(p, u);
+            const int m0 = w.tm * kRowsPerUnit + (int)rank * HM;
+            const int n0 = w.tn * p.bn + (int)rank * bcols;
+            for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
+                const int s = r.s;
+                mbar_wait(&empty[s], r.ph ^ 1);
+                if (leader) mbar_expect_tx_e(&full[s], (kPair ? 2u : 1u) * p.stage_bytes);
+                const uint32_t bar = full_cl0 + 8u * (uint32_t)s;
+                const uint32_t st = smem0 + (uint32_t)s * p.stage_bytes;
+                const int k0 = kb * HK;
+                if (p.a_kmajor) {
+                    h_tma_2d<kPair>(&map_ah, bar, st, k0, m0);
+                    h_tma_2d<kPair>(&map_al, bar, st + p.a_bytes, k0, m0);
+                } else {
+                    h_tma_3d<kPair>(&map_ah, bar, st, 0, k0, m0 / 64);
+                    h_tma_3d<kPair>(&map_al, bar, st + p.a_bytes, 0, k0, m0 / 64);
+                }
+                h_tma_2d<kPair>(&map_bh, bar, st + 2 * p.a_bytes, k0, n0);
+                h_tma_2d<kPair>(&map_bl, bar, st + 2 * p.a_bytes + p.b_bytes, k0, n0);
+            }
+        }
+    } else if (warp == kHWarpMma && leader) {
+        // descriptors of stage 0, K-step 0; per-stage / per-K-step / plane
+        // offsets in 16-byte units (start-address field never carries: < 228 KB)
+        const uint64_t a0 = p.a_kmajor ? make_desc(smem0, 16u, 1024u, kLayoutSW128)
+                                       : make_desc(smem0, kHChunkBytes, 1024u, kLayoutSW128);
+        const uint64_t b0 = make_desc(smem0 + 2 * p.a_bytes, 16u, 1024u, kLayoutSW128);
+        const uint64_t sstep = p.stage_bytes >> 4;
+        const uint64_t ajstep = p.a_kmajor ? (32u >> 4) : (2048u >> 4);  // 16 K: +32 B | +2 rows groups
+        const uint64_t bjstep = 32u >> 4;
+        const uint64_t alo = p.a_bytes >> 4, blo = p.b_bytes >> 4;
+        Ring r;
+        int ul = 0;
+        for (int u = ustart; u < units; u += ustride, ++ul) {
+            const HWork w = h_unit(p, u);
+            const int buf = ul & 1;
+            const uint32_t aph = (uint32_t)(ul >> 1) & 1u;
+            mbar_wait(&tempty[buf], aph ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
+            for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
+                const int s = r.s;
+                mbar_wait(&full[s], r.ph);
+                tc_fence_after();
+                const uint64_t as = a0 + (uint64_t)s * sstep, bs = b0 + (uint64_t)s * sstep;
+#pragma unroll
+                for (int j = 0; j < kHKSteps; ++j) {
+                    const uint32_t acc = (kb > w.kb0 || j > 0) ? 1u : 0u;
+                    const uint64_t ah = as + (uint64_t)j * ajstep, bh = bs + (uint64_t)j * bjstep;
+                    h_mma<kPair>(d, ah + alo, bh, p.idesc, acc);  // a_lo b_hi
+                    h_mma<kPair>(d, ah, bh + blo, p.idesc, 1u);   // a_hi b_lo
+                    h_mma<kPair>(d, ah, bh, p.idesc, 1u);         // a_hi b_hi
+                }
+                if (kPair) tc_commit_pair_e(&empty[s]);
+                else tc_commit_e(&empty[s]);
+            }
+            if (kPair) tc_commit_pair_e(&tfull[buf]);
+            else tc_commit_e(&tfull[buf]);
+        }
+    } else if (warp >= kHWarpEpi) {
+        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        // 2^-(ea+eb), applied as two exact power-of-two factors
+        const float sc = ldexpf(1.f, -__ldg(p.a_e)) * ldexpf(1.f, -__ldg(p.b_e));
+        const float alpha = p.alpha * sc;
+        int ul = 0;
+        for (int u = ustart; u < units; u += ustride, ++ul) {
+            const HWork w = h_unit(p, u);
+            const int buf = ul & 1;
+            const uint32_t aph = (uint32_t)(ul >> 1) & 1u;
+            mbar_wait(&tfull[buf], aph);
+            tc_fence_after();
+            const int row = w.tm * kRowsPerUnit + (int)rank * HM + q * 32 + lane;
+            const uint32_t tbase =
+                tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * p.acc_stride);
+            for (int c0 = 0; c0 < p.bn; c0 += 16) {
+                float v[16];
+                tmem_ld16(tbase + c0, v);
+                const int col0 = w.tn * p.bn + c0;
+                if (row >= p.M || col0 >= p.N) continue;
+                const int lim = min(16, p.N - col0);
+                if (p.splits > 1) {
+                    float* dst = p.ws + ((size_t)w.ks * p.M + row) * p.N + col0;
+                    for (int i = 0; i < lim; ++i) dst[i] = sc * v[i];
+                } else {
+                    float* dst = p.C + (size_t)row * p.ldc + col0;
+                    const bool vec = lim == 16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+                    if (vec) {
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4) {
+                            float4 o = make_float4(alpha * v[i], alpha * v[i + 1], alpha * v[i + 2],
+                                                   alpha * v[i + 3]);
+                            if (p.beta != 0.f) {
+                                const float4 c = *reinterpret_cast<float4*>(dst + i);
+                                o.x += p.beta * c.x; o.y += p.beta * c.y;
+                                o.z += p.beta * c.z; o.w += p.beta * c.w;
+                            }
+                            *reinterpret_cast<float4*>(dst + i) = o;
+                        }
+                    } else {
+                        for (int i = 0; i < lim; ++i)
+                            dst[i] = p.beta != 0.f ? alpha * v[i] + p.beta * dst[i] : alpha * v[i];
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (kPair) mbar_arrive_cluster_e(tempty_cl0 + 8u * (uint32_t)buf);
+            else mbar_arrive_e(&tempty[buf]);
+        }
+    }
+    tc_fence_before();
+    if (kPair) cluster_sync_all();
+    else __syncthreads();
+    if (warp == kHWarpMma) {
+        tc_fence_after();
+        if (kPair)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(kHTmemCols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(kHTmemCols));
+    }
+}
+
+__global__ void h3_splitk_reduce(const float* __restrict__ ws, int splits, int64_t M, int64_t N,
+                                 float alpha, float beta, float* __restrict__ C, int64_t ldc) {
+    const int64_t total = M * N;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        float s = 0.f;
+        for (int z = 0; z < splits; ++z) s += ws[(int64_t)z * total + t];
+        const int64_t i = t / N, j = t - i * N;
+        float* c = C + i * ldc + j;
+        *c = beta == 0.f ? alpha * s : alpha * s + beta * *c;
+    }
+}
+
+// ------------------------------------------------------------- the split --
+// e = 15 - E for max|X| = f 2^E (f in [0.5, 1)): max|X| 2^e in [2^14, 2^15).
+// All-zero or non-finite max: e = 0 (non-finite inputs are rejected upstream).
+__device__ __forceinline__ int h2_exponent(uint32_t amax_bits) {
+    const float a = __uint_as_float(amax_bits);
+    if (!(a > 0.f) || !isfinite(a)) return 0;
+    int E;
+    frexpf(a, &E);
+    return min(15 - E, 126);
+}
+__device__ __forceinline__ void h2_pair(float x, float s, __half& hi, __half& lo) {
+    const float xs = x * s;  // exact: a power of two
+    hi = __float2half_rn(xs);
+    lo = __float2half_rn(xs - __half2float(hi));  // the difference is exact in fp32
+}
+
+__global__ void absmax_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ld,
+                              uint32_t* __restrict__ amax) {
+    uint32_t m = 0;
+    const int64_t c4 = (cols + 3) / 4;
+    const bool vec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows * c4;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / c4, j = (t - i * c4) * 4;
+        const float* x = X + i * ld + j;
+        if (vec && j + 4 <= cols) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(x));
+            m = max(m, max(max(__float_as_uint(fabsf(v.x)), __float_as_uint(fabsf(v.y))),
+                           max(__float_as_uint(fabsf(v.z)), __float_as_uint(fabsf(v.w)))));
+        } else {
+            for (int64_t k = j; k < cols && k < j + 4; ++k)
+                m = max(m, __float_as_uint(fabsf(x[k - j])));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(amax, m);
+}
+
+// out (rows x cols, ldh) = split of X, 4 elements per thread
+__global__ void split_h2_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ld,
+                                const uint32_t* __restrict__ amax, __half* __restrict__ hi,
+                                __half* __restrict__ lo, int64_t ldh, int* __restrict__ e_out) {
+    const int e = h2_exponent(*amax);
+    const float s = ldexpf(1.f, e);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *e_out = e;
+    const int64_t c4 = (cols + 3) / 4;
+    const bool vec = (ld & 3) == 0 && (ldh & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(hi) & 7) == 0 &&
+                     (reinterpret_cast<uintptr_t>(lo) & 7) == 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows * c4;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / c4, j = (t - i * c4) * 4;
+        const float* x = X + i * ld + j;
+        if (vec && j + 4 <= cols) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(x));
+            __half h[4], l[4];
+            h2_pair(v.x, s, h[0], l[0]);
+            h2_pair(v.y, s, h[1], l[1]);
+            h2_pair(v.z, s, h[2], l[2]);
+            h2_pair(v.w, s, h[3], l[3]);
+            *reinterpret_cast<uint2*>(hi + i * ldh + j) = *reinterpret_cast<uint2*>(h);
+            *reinterpret_cast<uint2*>(lo + i * ldh + j) = *reinterpret_cast<uint2*>(l);
+        } else {
+            for (int64_t k = j; k < cols && k < j + 4; ++k)
+                h2_pair(x[k - j], s, hi[i * ldh + k], lo[i * ldh + k]);
+        }
+    }
+}
+
+// out (cols x rows, ldh) = split of X^T: 64 x 64 tiles through shared memory
+__global__ void __launch_bounds__(256)
+split_h2_t_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ld,
+                  const uint32_t* __restrict__ amax, __half* __restrict__ hi,
+                  __half* __restrict__ lo, int64_t ldh, int* __restrict__ e_out) {
+    __shared__ float tile[64][65];
+    const int e = h2_exponent(*amax);
+    const float s = ldexpf(1.f, e);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *e_out = e;
+    const int64_t r0 = (int64_t)blockIdx.y * 64, c0 = (int64_t)blockIdx.x * 64;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+    for (int k = ty; k < 64; k += 4) {
+        const int64_t i = r0 + k, j = c0 + tx;
+        tile[k][tx] = (i < rows && j < cols) ? __ldg(X + i * ld + j) : 0.f;
+    }
+    __syncthreads();
+    // output row c0 + k holds X[r0 .. r0+63, c0 + k]; a thread writes 2 elements
+    const int tx2 = threadIdx.x & 31, ty2 = threadIdx.x >> 5;  // 32 x 8
+    for (int k = ty2; k < 64; k += 8) {
+        const int64_t orow = c0 + k, oc = r0 + 2 * tx2;
+        if (orow >= cols || oc >= rows) continue;
+        __half h0, l0, h1, l1;
+        h2_pair(tile[2 * tx2][k], s, h0, l0);
+        h2_pair(tile[2 * tx2 + 1][k], s, h1, l1);
+        if (oc + 1 < rows && (ldh & 1) == 0) {
+            *reinterpret_cast<__half2*>(hi + orow * ldh + oc) = __halves2half2(h0, h1);
+            *reinterpret_cast<__half2*>(lo + orow * ldh + oc) = __halves2half2(l0, l1);
+        } else {
+            hi[orow * ldh + oc] = h0;
+            lo[orow * ldh + oc] = l0;
+            if (oc + 1 < rows) {
+                hi[orow * ldh + oc + 1] = h1;
+                lo[orow * ldh + oc + 1] = l1;
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------- host ----
+PFN_cuTensorMapEncodeTiled_v12000 h_encode = nullptr;
+int h_state = -1;
+int h_sms = 148;
+
+bool h_init() {
+    if (h_state >= 0) return h_state == 1;
+    h_state = 0;
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cudaDeviceGetAttribute(&h_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (major != 10 || minor != 0 || getenv("SKP_DISABLE_TCGEN05")) return false;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+        return false;
+    h_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    h_state = 1;
+    return true;
+}
+
+// K-major fp16 [rows x cols] (cols = K contiguous), box {64, box_rows}, SWIZZLE_128B
+bool h_encode_k(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t ld,
+                uint32_t box_rows) {
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld * 2};
+    cuuint32_t box[2] = {(cuuint32_t)HK, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return h_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// MN-major fp16 A stored [K x M] (M contiguous) as {64, K, M/64 chunks}: one
+// box {64, HK, 2} = the CTA's 128 M x HK K tile as [chunk][k][64], SWIZZLE_128B
+bool h_encode_mn(CUtensorMap* map, const void* base, uint64_t m, uint64_t k, uint64_t ld) {
+    cuuint64_t dims[3] = {64, k, (cuuint64_t)cdiv((int64_t)m, 64)};
+    cuuint64_t strides[2] = {ld * 2, 128};
+    cuuint32_t box[3] = {64, (cuuint32_t)HK, (cuuint32_t)(HM / 64)};
+    cuuint32_t es[3] = {1, 1, 1};
+    return h_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct HPlan {
+    int bn, tiles_m, tiles_n, splits, num_kb, kb_per_split, stages, acc_stride;
+    uint32_t a_bytes, b_bytes, stage_bytes;
+    size_t smem;
+};
+
+bool h_pair(int64_t M) {
+    if (getenv("SKP_H3_NO2CTA")) return false;
+    if (getenv("SKP_H3_FORCE2CTA")) return true;
+    return M > HM;
+}
+
+HPlan h_plan(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool pair) {
+    HPlan pl;
+    const int max_bn = pair ? 256 : 128;
+    pl.tiles_n = (int)cdiv(N, max_bn);
+    pl.bn = (int)(cdiv(cdiv(N, pl.tiles_n), 16) * 16);
+    pl.tiles_m = (int)cdiv(M, pair ? 2 * HM : HM);
+    pl.num_kb = (int)cdiv(K, HK);
+    const int slots_machine = pair ? h_sms / 2 : h_sms;
+    const int64_t base = (int64_t)pl.tiles_m * pl.tiles_n;
+    int splits = 1;
+    if (base < 4 * slots_machine) {
+        double best = 0;
+        const int maxs = (int)std::max<int64_t>(1, pl.num_kb / 4);
+        for (int s = 1; s <= std::min(64, maxs); ++s) {
+            const int64_t units = base * s;
+            if (s > 1 && (int64_t)s * M * N > ws_cap_elems) break;
+            const double waves = (double)cdiv(units, slots_machine);
+            const double eff = (double)units / (waves * slots_machine);
+            const double score = std::min(1.0, (double)units / slots_machine) * eff;
+            if (score > best + 0.02) { best = score; splits = s; }
+        }
+    }
+    pl.kb_per_split = (int)cdiv(pl.num_kb, splits);
+    pl.splits = (int)cdiv(pl.num_kb, pl.kb_per_split);
+    pl.a_bytes = HM * HK * 2;
+    const int bcols = pair ? pl.bn / 2 : pl.bn;
+    pl.b_bytes = (uint32_t)bcols * HK * 2;
+    pl.stage_bytes = 2 * pl.a_bytes + 2 * pl.b_bytes;
+    pl.acc_stride = (int)cdiv(pl.bn, 32) * 32;
+    const size_t budget = 227 * 1024;
+    const int st = (int)((budget - 1024 - 256) / pl.stage_bytes);
+    pl.stages = std::max(2, std::min(kHMaxStages, st));
+    if (getenv("SKP_H3_STAGES")) pl.stages = std::max(2, std::min(pl.stages, atoi(getenv("SKP_H3_STAGES"))));
+    pl.smem = 1024 + (size_t)pl.stages * pl.stage_bytes + (2 * pl.stages + 4) * 8 + 16;
+    return pl;
+}
+
+}  // namespace
+
+int64_t gemm_h3_ws_bytes(int ta, int64_t M, int64_t N, int64_t K) {
+    (void)ta;
+    if (!h_init()) return 0;
+    const HPlan pl = h_plan(M, N, K, INT64_MAX, h_pair(M));
+    return pl.splits > 1 ? (int64_t)pl.splits * M * N * 4 : 0;
+}
+
+int gemm_h3(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo,
+            int64_t lda, const int32_t* a_e, const void* Bhi, const void* Blo, int64_t ldb,
+            const int32_t* b_e, float beta, float* C, int64_t ldc, void* ws, int64_t ws_bytes,
+            cudaStream_t st) {
+    if (!h_init()) {
+        set_error("unsupported: the 3xFP16 tcgen05 GEMM needs an sm_100 device");
+        return SKP_ERR_UNSUPPORTED;
+    }
+    if (M == 0 || N == 0) return SKP_OK;
+    if (K == 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) {
+        set_error("unsupported: gemm_h3 sizes");
+        return SKP_ERR_UNSUPPORTED;
+    }
+    const uintptr_t al = reinterpret_cast<uintptr_t>(Ahi) | reinterpret_cast<uintptr_t>(Alo) |
+                         reinterpret_cast<uintptr_t>(Bhi) | reinterpret_cast<uintptr_t>(Blo);
+    if ((al & 15) || (lda & 7) || (ldb & 7) || (ta && (lda & 63))) {
+        set_error("unsupported: gemm_h3 needs 16-byte aligned planes, ld %% 8 == 0 (%% 64 for "
+                  "MN-major A): lda=%lld ldb=%lld", (long long)lda, (long long)ldb);
+        return SKP_ERR_UNSUPPORTED;
+    }
+    const bool pair = h_pair(M);
+    const int64_t cap = ws ? ws_bytes / 4 : 0;
+    HPlan pl = h_plan(M, N, K, cap, pair);
+    if (pl.splits > 1 && (!ws || (int64_t)pl.splits * M * N * 4 > ws_bytes))
+        pl = h_plan(M, N, K, 0, pair);
+    H3Params p;
+    p.M = (int)M; p.N = (int)N; p.K = (int)K;
+    p.bn = pl.bn; p.tiles_m = pl.tiles_m; p.tiles_n = pl.tiles_n; p.splits = pl.splits;
+    p.kb_per_split = pl.kb_per_split; p.num_kb = pl.num_kb;
+    p.a_kmajor = ta ? 0 : 1;
+    p.alpha = alpha; p.beta = beta; p.C = C; p.ldc = ldc;
+    p.ws = pl.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
+    p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
+    p.stage_bytes = pl.stage_bytes; p.acc_stride = pl.acc_stride;
+    p.a_e = a_e; p.b_e = b_e;
+    // kind::f16 instruction descriptor: D f32, A/B f16, A major from the layout,
+    // B K-major, N >> 3, M >> 4
+    p.idesc = (1u << 4) | ((uint32_t)(!p.a_kmajor) << 15) | ((uint32_t)(p.bn >> 3) << 17) |
+              ((uint32_t)((pair ? 2 * HM : HM) >> 4) << 24);
+    CUtensorMap mah, mal, mbh, mbl;
+    const int bcols = pair ? p.bn / 2 : p.bn;
+    bool ok;
+    if (p.a_kmajor)
+        ok = h_encode_k(&mah, Ahi, (uint64_t)K, (uint64_t)M, lda, HM) &&
+             h_encode_k(&mal, Alo, (uint64_t)K, (uint64_t)M, lda, HM);
+    else
+        ok = h_encode_mn(&mah, Ahi, (uint64_t)M, (uint64_t)K, lda) &&
+             h_encode_mn(&mal, Alo, (uint64_t)M, (uint64_t)K, lda);
+    ok = ok && h_encode_k(&mbh, Bhi, (uint64_t)K, (uint64_t)N, ldb, (uint32_t)bcols) &&
+         h_encode_k(&mbl, Blo, (uint64_t)K, (uint64_t)N, ldb, (uint32_t)bcols);
+    if (!ok) {
+        set_error("cuTensorMapEncodeTiled failed (gemm_h3)");
+        return SKP_ERR_UNSUPPORTED;
+    }
+    const int units = p.tiles_m * p.tiles_n * p.splits;
+    if (pair) {
+        SKP_CUDA(cudaFuncSetAttribute(gemm_h3_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(2 * std::min(units, h_sms / 2)));
+        cfg.blockDim = dim3(kHThreads);
+        cfg.dynamicSmemBytes = pl.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SKP_CUDA(cudaLaunchKernelEx(&cfg, gemm_h3_kernel<true>, mah, mal, mbh, mbl, p));
+        SKP_LAUNCHED(gemm_h3_kernel_pair);
+    } else {
+        SKP_CUDA(cudaFuncSetAttribute(gemm_h3_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        gemm_h3_kernel<false><<<std::min(units, h_sms), kHThreads, pl.smem, st>>>(mah, mal, mbh, mbl,
+                                                                                 p);
+        SKP_LAUNCHED(gemm_h3_kernel);
+    }
+    if (p.splits > 1) {
+        const int64_t blocks = std::min<int64_t>(cdiv(M * N, 256), (int64_t)h_sms * 8);
+        h3_splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(p.ws, p.splits, M, N, alpha, beta, C,
+                                                           ldc);
+        SKP_LAUNCHED(h3_splitk_reduce);
+    }
+    return SKP_OK;
+}
+
+int split_h2(const float* X, int64_t rows, int64_t cols, int64_t ld, int trans, void* hi, void* lo,
+             int64_t ldh, int32_t* e, cudaStream_t st) {
+    if (rows == 0 || cols == 0) {
+        SKP_CUDA(cudaMemsetAsync(e, 0, 4, st));
+        return SKP_OK;
+    }
+    uint32_t* amax = reinterpret_cast<uint32_t*>(e + 1);
+    SKP_CUDA(cudaMemsetAsync(amax, 0, 4, st));
+    const int64_t work = rows * cdiv(cols, 4);
+    const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(work, 256), (int64_t)h_sms * 16);
+    absmax_kernel<<<blocks, 256, 0, st>>>(X, rows, cols, ld, amax);
+    SKP_LAUNCHED(absmax_kernel);
+    if (!trans) {
+        split_h2_kernel<<<blocks, 256, 0, st>>>(X, rows, cols, ld, amax, (__half*)hi, (__half*)lo,
+                                                ldh, e);
+        SKP_LAUNCHED(split_h2_kernel);
+    } else {
+        SKP_ARG(cdiv(rows, 64) <= 65535, "split_h2: too many rows for the transposing split");
+        split_h2_t_kernel<<<dim3((unsigned)cdiv(cols, 64), (unsigned)cdiv(rows, 64)), 256, 0, st>>>(
+            X, rows, cols, ld, amax, (__half*)hi, (__half*)lo, ldh, e);
+        SKP_LAUNCHED(split_h2_t_kernel);
+    }
+    return SKP_OK;
+}
+
+}  // namespace skp
+
+using namespace skp;
+
+extern "C" int64_t skp_gemm_h3_ws_bytes(int transA, int64_t M, int64_t N, int64_t K) {
+    return gemm_h3_ws_bytes(transA, M, N, K);
+}
+
+extern "C" int skp_gemm_h3(int transA, int64_t M, int64_t N, int64_t K, float alpha,
+                           const void* A_hi, const void* A_lo, int64_t lda, const int32_t* a_exp,
+                           const void* B_hi, const void* B_lo, int64_t ldb, const int32_t* b_exp,
+                           float beta, float* C, int64_t ldc, void* ws, int64_t ws_bytes,
+                           void* stream) {
+    SKP_ARG(M >= 0 && N >= 0 && K >= 0, "gemm_h3: negative size");
+    SKP_ARG(transA == 0 || transA == 1, "gemm_h3: transA must be 0/1");
+    SKP_ARG(lda >= (transA ? M : K) && lda >= 1, "gemm_h3: lda too small");
+    SKP_ARG(ldb >= K && ldb >= 1, "gemm_h3: ldb too small");
+    SKP_ARG(ldc >= N && ldc >= 1, "gemm_h3: ldc too small");
+    SKP_ARG((M == 0 || N == 0 || K == 0 || (A_hi && A_lo && B_hi && B_lo && a_exp && b_exp)) &&
+                (M == 0 || N == 0 || C),
+            "gemm_h3: null pointer");
+    return gemm_h3(transA, M, N, K, alpha, A_hi, A_lo, lda, a_exp, B_hi, B_lo, ldb, b_exp, beta, C,
+                   ldc, ws, ws_bytes, SKP_STREAM(stream));
+}
+
+extern "C" int skp_split_h2_f32(const float* X, int64_t rows, int64_t cols, int64_t ld,
+                                int32_t trans, void* hi, void* lo, int64_t ldh, int32_t* e,
+                                void* stream) {
+    SKP_ARG(rows >= 0 && cols >= 0 && ld >= cols && ld >= 1, "split_h2: bad sizes");
+    SKP_ARG(trans == 0 || trans == 1, "split_h2: trans must be 0/1");
+    SKP_ARG(ldh >= (trans ? rows : cols), "split_h2: ldh too small");
+    SKP_ARG(e && (rows == 0 || cols == 0 || (X && hi && lo)), "split_h2: null pointer");
+    h_init();
+    return split_h2(X, rows, cols, ld, trans, hi, lo, ldh, e, SKP_STREAM(stream));
+}

@@ -161,7 +161,12 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
         atil, perm = got
     else:
         atil, perm = sk.right(a, fro2=fro2, nonfinite=nonfinite), None
+    del got
     ph.mark("apply_right")
+    # the power iteration's operand: A~ split once into fp16 hi/lo planes (the
+    # fp32 A~ is released here; the footprint stays m x l x 4 bytes)
+    atil = be.prepare(atil)
+    ph.mark("split")
 
     def omega_for(perm_dev, host: bool = False):
         if om_job is None and not host:

@@ -14,6 +14,9 @@ class NumpyBackend:
     def __init__(self, dtype=np.float64):
         self.dtype = np.dtype(dtype)
 
+    def prepare(self, x):
+        return x
+
     def mm(self, a, b, ta=False, tb=False, out=None, alpha=1.0, beta=0.0):
         r = (a.T if ta else a) @ (b.T if tb else b)
         return np.ascontiguousarray(r.astype(self.dtype, copy=False))

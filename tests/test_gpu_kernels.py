@@ -276,6 +276,61 @@ def test_gemm_modes_agree(ops):
         assert (c.double() - ref).abs().max().item() <= 1e-5 * ref.abs().max().item()
 
 
+# ------------------------------------------------ K4h (3xFP16, pre-split) --
+
+@pytest.mark.parametrize("scale", [1.0, 3e-19, 7e17])
+@pytest.mark.parametrize("trans", [False, True])
+def test_split_h2_roundtrip(ops, scale, trans):
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(300, 197, generator=g, device="cuda") * scale
+    x[3, 5] = 0.0
+    sp = ops.split_h2(x, trans=trans)
+    e = int(sp.e[0].item())
+    amax = x.abs().max().item()
+    assert 2.0 ** 14 <= amax * 2.0 ** e < 2.0 ** 15
+    rec = (sp.hi[:, :sp.cols].double() + sp.lo[:, :sp.cols].double()) * 2.0 ** -e
+    src = x.double().T if trans else x.double()
+    assert rec.shape == src.shape
+    # per element: |x - rec| <= 2^-22 |x| + the fp16 subnormal floor (2^-25 of 2^15)
+    err = (rec - src).abs()
+    assert (err <= 2.0 ** -22 * src.abs() + 2.0 ** (-25 - e)).all()
+
+
+def test_split_h2_zero(ops):
+    sp = ops.split_h2(torch.zeros(5, 9, device="cuda"))
+    assert int(sp.e[0].item()) == 0
+    assert sp.hi[:, :9].abs().max().item() == 0 and sp.lo[:, :9].abs().max().item() == 0
+
+
+@pytest.mark.parametrize("ta", [0, 1])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (67, 45, 131), (128, 16, 64), (300, 520, 4000),
+                                   (1000, 110, 2000), (4000, 520, 65536), (257, 176, 1000)])
+def test_gemm_h3_vs_torch(ops, ta, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    a = torch.randn((K, M) if ta else (M, K), generator=g, device="cuda") * 3.0
+    b = torch.randn(K, N, generator=g, device="cuda") * 1e-3
+    sa = ops.split_h2(a)
+    sb = ops.split_h2(b, trans=True)   # B^T (N x K, K-major)
+    ref = (a.double().T if ta else a.double()) @ b.double()
+    c0 = torch.randn(M, N, generator=g, device="cuda")
+    out = c0.clone()
+    ops.gemm_h3(sa, sb, ta=bool(ta), alpha=0.5, beta=2.0, out=out)
+    expect = 0.5 * ref + 2.0 * c0.double()
+    scale = (a.double().abs().max() * b.double().abs().max() * np.sqrt(K)).item()
+    # 2^-22 per product, fp32 accumulation: the same bound as the 3xTF32 test
+    assert (out.double() - expect).abs().max().item() <= 2e-6 * scale + 1e-6
+
+
+def test_gemm_h3_pair_forced_small(ops, monkeypatch):
+    monkeypatch.setenv("SKP_H3_FORCE2CTA", "1")
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.randn(100, 300, generator=g, device="cuda")
+    b = torch.randn(300, 48, generator=g, device="cuda")
+    out = ops.gemm_h3(ops.split_h2(a), ops.split_h2(b, trans=True))
+    ref = a.double() @ b.double()
+    assert (out.double() - ref).abs().max().item() <= 2e-6 * np.sqrt(300) * 25
+
+
 # ----------------------------------------------------------- K5 / K6 ------
 
 def _spd(n, cond=1e4, seed=0):
