@@ -100,6 +100,8 @@ int skp_sketch_right_f64(const double* A, int64_t lda, int64_t m, int64_t n,
  * Requires
  * n <= 24576 and 16-byte aligned rows padded to a multiple of 4 floats;
  * returns SKP_ERR_UNSUPPORTED otherwise (callers keep skp_sketch_right).
+ * amax (may be NULL): atomicMax of the bits of max |out| (for the 3xFP16
+ * split of the output, skp_split_h2_f32 with have_amax = 1).
  * nonfinite (may be NULL) += #non-finite outputs: > 0 iff A has a non-finite
  * entry (every column of A feeds nonzero entries), barring fp32 overflow of a
  * finite sum; fro2 (may be NULL) += ||A||_F^2 by a separate pass.
@@ -111,7 +113,7 @@ int skp_sketch_gather_plan(const int32_t* colptr, const int32_t* entries, int64_
                            void* plan, int64_t plan_bytes, void* stream);
 int skp_sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
                           const void* plan, float scale, float* out, int64_t ldo, double* fro2,
-                          int64_t* nonfinite, void* stream);
+                          int64_t* nonfinite, uint32_t* amax, void* stream);
 
 /* ----------------------------------------------------------- Omega ----
  * out (rows x cols) = Generator(PCG64 (state, inc)).standard_normal((rows,
@@ -217,7 +219,9 @@ int skp_cast2d_f64_f32(const double* x, int64_t ldx, float* y, int64_t ldy, int6
  * gemm_h3.cu) -- the power-iteration products of power.py:129-133.
  * skp_split_h2_f32: X (rows x cols, ld) -> hi, lo (fp16 planes, ldh) with
  * X 2^e ~= hi + lo, e = e_io[0] = 15 - ceil(log2 max|X|) (written on the
- * device; e_io[1] is scratch); trans=1 writes X^T (cols x rows).
+ * device; e_io[1] holds the bits of max|X|: computed here, or -- have_amax
+ * = 1 -- already accumulated by the caller, e.g. by skp_sketch_gather_f32's
+ * amax output); trans=1 writes X^T (cols x rows).
  * skp_gemm_h3: C = alpha op(A) B^T + beta C, computed as 2^-(ea+eb) times
  * the fp32-accumulated A_lo B_hi + A_hi B_lo + A_hi B_hi, with op(A) = A
  * (M x K, transA=0) or A^T (A stored K x M, transA=1, lda % 64 == 0) and B
@@ -225,7 +229,8 @@ int skp_cast2d_f64_f32(const double* x, int64_t ldx, float* y, int64_t ldy, int6
  * product (3xTF32: 2^-20).
  * ws: skp_gemm_h3_ws_bytes (split-K partials; 0 = none needed).            */
 int skp_split_h2_f32(const float* X, int64_t rows, int64_t cols, int64_t ld, int32_t trans,
-                     void* hi, void* lo, int64_t ldh, int32_t* e_io, void* stream);
+                     void* hi, void* lo, int64_t ldh, int32_t* e_io, int32_t have_amax,
+                     void* stream);
 int64_t skp_gemm_h3_ws_bytes(int transA, int64_t M, int64_t N, int64_t K);
 int skp_gemm_h3(int transA, int64_t M, int64_t N, int64_t K, float alpha, const void* A_hi,
                 const void* A_lo, int64_t lda, const int32_t* a_exp, const void* B_hi,

@@ -172,15 +172,16 @@ def gather_plan_checked(plan: torch.Tensor, r: int):
 
 
 def sketch_gather(a: torch.Tensor, plan: torch.Tensor, r: int, s: int, out=None, fro2=None,
-                  nonfinite=None):
+                  nonfinite=None, amax=None):
     """K2 v2: (a @ S) with the plan's column permutation, fused ||a||_F^2 and
-    non-finite test; fp32, a with 16-byte aligned rows (empty2d)."""
+    non-finite test; fp32, a with 16-byte aligned rows (empty2d).  amax (int32
+    view, 1 element, zeroed by the caller): atomicMax of max|out|'s bits."""
     m, n, lda = _rows_ld(a)
     if out is None:
         out = empty2d(m, r, a.dtype, a.device)
     _, _, ldo = _rows_ld(out)
     call("skp_sketch_gather_f32", ptr(a), lda, m, n, r, ptr(plan), 1.0 / float(np.sqrt(s)),
-         ptr(out), ldo, ptr(fro2), ptr(nonfinite), stream_ptr(a.device))
+         ptr(out), ldo, ptr(fro2), ptr(nonfinite), ptr(amax), stream_ptr(a.device))
     return out
 
 
@@ -272,7 +273,10 @@ class SplitH2:
         self.hi, self.lo, self.e, self.rows, self.cols, self.ld = hi, lo, e, rows, cols, ld
 
 
-def split_h2(x: torch.Tensor, trans: bool = False, out: "SplitH2 | None" = None) -> SplitH2:
+def split_h2(x: torch.Tensor, trans: bool = False, out: "SplitH2 | None" = None,
+             e_io: torch.Tensor | None = None) -> SplitH2:
+    """e_io (int32[2]): e_io[1] already holds max|x|'s bits (e.g. the sketch
+    kernel's amax output), so the max pass is skipped; e_io becomes out.e."""
     r, c, ld = _rows_ld(x)
     if x.dtype != F32:
         raise ValueError("split_h2 needs float32")
@@ -282,8 +286,10 @@ def split_h2(x: torch.Tensor, trans: bool = False, out: "SplitH2 | None" = None)
         buf = torch.empty((2, rows, ldh), dtype=torch.float16, device=x.device)
         out = SplitH2(buf[0], buf[1], torch.zeros(2, dtype=torch.int32, device=x.device),
                       rows, cols, ldh)
+    if e_io is not None:
+        out.e = e_io
     call("skp_split_h2_f32", ptr(x), r, c, ld, int(trans), ptr(out.hi), ptr(out.lo), out.ld,
-         ptr(out.e), stream_ptr(x.device))
+         ptr(out.e), int(e_io is not None), stream_ptr(x.device))
     return out
 
 
@@ -371,19 +377,19 @@ class CudaBackend:
             return gemm_h3(a, sb, ta=ta, alpha=alpha, beta=beta, out=out)
         return gemm(a, b, ta, tb, alpha=alpha, beta=beta, out=out, mode=self.gemm_mode)
 
-    def prepare(self, x):
+    def prepare(self, x, e_io=None):
         """A left operand reused by several products (the power iteration's
         A~): split once into fp16 hi/lo planes for the 3xFP16 GEMM (twice the
         3xTF32 rate at 22-bit operand accuracy).  Returns x itself where that
         does not apply (fp64, explicit GEMM modes, small operands, no
-        tcgen05) or is switched off (SKP_NO_H3)."""
+        tcgen05) or is switched off (SKP_NO_H3).  e_io: see split_h2."""
         if isinstance(x, SplitH2) or self.dtype != F32 or self.gemm_mode != "auto":
             return x
         if x.dim() != 2 or x.shape[0] * x.shape[1] < H3_MIN_ELEMS or os.environ.get("SKP_NO_H3"):
             return x
         if not _lib.load().skp_has_tcgen05():
             return x
-        return split_h2(x)
+        return split_h2(x, e_io=e_io)
 
     def gram64(self, y):
         """y^T y as fp64 (computed in the compute dtype, then widened)."""

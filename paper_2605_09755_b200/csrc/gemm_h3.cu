@@ -649,17 +649,19 @@ int gemm_h3(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ah
 }
 
 int split_h2(const float* X, int64_t rows, int64_t cols, int64_t ld, int trans, void* hi, void* lo,
-             int64_t ldh, int32_t* e, cudaStream_t st) {
+             int64_t ldh, int32_t* e, int have_amax, cudaStream_t st) {
     if (rows == 0 || cols == 0) {
         SKP_CUDA(cudaMemsetAsync(e, 0, 4, st));
         return SKP_OK;
     }
     uint32_t* amax = reinterpret_cast<uint32_t*>(e + 1);
-    SKP_CUDA(cudaMemsetAsync(amax, 0, 4, st));
     const int64_t work = rows * cdiv(cols, 4);
     const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(work, 256), (int64_t)h_sms * 16);
-    absmax_kernel<<<blocks, 256, 0, st>>>(X, rows, cols, ld, amax);
-    SKP_LAUNCHED(absmax_kernel);
+    if (!have_amax) {
+        SKP_CUDA(cudaMemsetAsync(amax, 0, 4, st));
+        absmax_kernel<<<blocks, 256, 0, st>>>(X, rows, cols, ld, amax);
+        SKP_LAUNCHED(absmax_kernel);
+    }
     if (!trans) {
         split_h2_kernel<<<blocks, 256, 0, st>>>(X, rows, cols, ld, amax, (__half*)hi, (__half*)lo,
                                                 ldh, e);
@@ -700,11 +702,11 @@ extern "C" int skp_gemm_h3(int transA, int64_t M, int64_t N, int64_t K, float al
 
 extern "C" int skp_split_h2_f32(const float* X, int64_t rows, int64_t cols, int64_t ld,
                                 int32_t trans, void* hi, void* lo, int64_t ldh, int32_t* e,
-                                void* stream) {
+                                int32_t have_amax, void* stream) {
     SKP_ARG(rows >= 0 && cols >= 0 && ld >= cols && ld >= 1, "split_h2: bad sizes");
     SKP_ARG(trans == 0 || trans == 1, "split_h2: trans must be 0/1");
     SKP_ARG(ldh >= (trans ? rows : cols), "split_h2: ldh too small");
     SKP_ARG(e && (rows == 0 || cols == 0 || (X && hi && lo)), "split_h2: null pointer");
     h_init();
-    return split_h2(X, rows, cols, ld, trans, hi, lo, ldh, e, SKP_STREAM(stream));
+    return split_h2(X, rows, cols, ld, trans, hi, lo, ldh, e, have_amax != 0, SKP_STREAM(stream));
 }

@@ -250,7 +250,7 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
                      int P, int width, const uint32_t* __restrict__ sched,
                      const int32_t* __restrict__ tw, const int32_t* __restrict__ plan_fail,
                      float scale, float* __restrict__ out, int64_t ldo,
-                     int64_t* nonfinite) {
+                     int64_t* nonfinite, uint32_t* __restrict__ amax) {
     extern __shared__ __align__(128) unsigned char sm[];
     if (*plan_fail) {
         // the plan's schedule overflowed: report it through the non-finite
@@ -301,6 +301,7 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
     const int64_t v_out = (int64_t)slice * width + warp * 32 + lane;  // output position
     const bool valid = warp * 32 + lane < width && v_out < r;
     bool bad = false;  // a non-finite output of this thread (iff a non-finite input)
+    uint32_t mx = 0;   // max |output| (bits; non-negative floats order as integers)
 
     auto do_row = [&](int64_t i, int b, uint32_t ph, auto boff_c) {
         constexpr uint32_t boff = decltype(boff_c)::value;
@@ -354,6 +355,7 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
         if (valid) {
             const float o = acc * scale;
             bad |= !isfinite(o);
+            mx = max(mx, __float_as_uint(fabsf(o)));
             out[i * ldo + v_out] = o;
         }
     };
@@ -366,6 +368,11 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
                    std::integral_constant<uint32_t, kGBufBytes>());
     }
 
+    if (amax) {  // max |A~| for the 3xFP16 split of A~ (skp_split_h2_f32, have_amax)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0 && mx) atomicMax(amax, mx);
+    }
     if (nonfinite) {
         const unsigned nb = __popc(__ballot_sync(0xffffffffu, bad));
         if (lane == 0 && nb)
@@ -418,7 +425,7 @@ int gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n, int64_
 
 int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
                       const void* plan, float scale, float* out, int64_t ldo, double* fro2,
-                      int64_t* nonfinite, cudaStream_t st) {
+                      int64_t* nonfinite, uint32_t* amax, cudaStream_t st) {
     SKP_ARG(m >= 0 && n >= 1 && r >= 1 && ldo >= r, "sketch_gather: bad sizes");
     if (n > kGBufWords - 32 || (reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3) ||
         lda < (n + 3) / 4 * 4) {
@@ -441,7 +448,7 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
                                   (int)kGSmem));
     sketch_gather_kernel<<<G * P, kGThreads, kGSmem, st>>>(A, lda, m, n, r, P, gather_width(r),
                                                            sched, tw, pfail, scale, out, ldo,
-                                                           nonfinite);
+                                                           nonfinite, amax);
     SKP_LAUNCHED(sketch_gather_kernel);
     if (fro2) {  // ||A||_F^2: a separate HBM-bound pass (only when asked for)
         const int rc = skp_sumsq_f32(A, m, n, lda, fro2, nullptr, st);
@@ -465,7 +472,8 @@ extern "C" int skp_sketch_gather_plan(const int32_t* colptr, const int32_t* entr
 }
 extern "C" int skp_sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
                                      const void* plan, float scale, float* out, int64_t ldo,
-                                     double* fro2, int64_t* nonfinite, void* stream) {
-    return sketch_gather_f32(A, lda, m, n, r, plan, scale, out, ldo, fro2, nonfinite,
+                                     double* fro2, int64_t* nonfinite, uint32_t* amax,
+                                     void* stream) {
+    return sketch_gather_f32(A, lda, m, n, r, plan, scale, out, ldo, fro2, nonfinite, amax,
                              (cudaStream_t)stream);
 }

@@ -156,16 +156,18 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     # the reference.  K2 v1 (natural column order) where v2 does not apply.
     # (deferred: no host sync for the plan check; a failed plan shows up as a
     # marker in the non-finite count checked at the end)
-    got = sk.right_permuted(a, fro2=fro2, nonfinite=nonfinite, deferred=True)
+    # (e_io[1]: max|A~|, accumulated by K2 v2 for the fp16 split below)
+    e_io = torch.zeros(2, dtype=torch.int32, device=dev)
+    got = sk.right_permuted(a, fro2=fro2, nonfinite=nonfinite, deferred=True, amax=e_io[1:])
     if got is not None:
         atil, perm = got
     else:
-        atil, perm = sk.right(a, fro2=fro2, nonfinite=nonfinite), None
+        atil, perm, e_io = sk.right(a, fro2=fro2, nonfinite=nonfinite), None, None
     del got
     ph.mark("apply_right")
     # the power iteration's operand: A~ split once into fp16 hi/lo planes (the
     # fp32 A~ is released here; the footprint stays m x l x 4 bytes)
-    atil = be.prepare(atil)
+    atil = be.prepare(atil, e_io)
     ph.mark("split")
 
     def omega_for(perm_dev, host: bool = False):

@@ -137,13 +137,14 @@ class SketchOperator:
         return self._gather
 
     def right_permuted(self, a: torch.Tensor, out=None, fro2=None, nonfinite=None,
-                       deferred: bool = False):
+                       deferred: bool = False, amax=None):
         """(a @ S P, perm) with perm[v] (int32, on the device) = the column of
         a @ S at position v, via the row-gather kernel (fp32, n <= 24576); None
         when it does not apply.  deferred=True skips the plan's host check: a
         failed schedule then adds _ops.GATHER_PLAN_FAIL_MARK to *nonfinite
         (required) and writes nothing -- the caller falls back to right().
-        Range-finder use: (a S P)(P^T Omega) == (a S) Omega."""
+        Range-finder use: (a S P)(P^T Omega) == (a S) Omega.  amax: see
+        _ops.sketch_gather."""
         if a.dtype != torch.float32 or (a.stride(0) * 4) % 16 or a.data_ptr() % 16:
             return None
         if deferred and nonfinite is None:
@@ -153,7 +154,7 @@ class SketchOperator:
             return None
         g = plan[0]
         perm_dev = g[:4 * self.r].view(torch.int32)   # the first r entries are the valid ones
-        return _ops.sketch_gather(a, g, self.r, self.s, out, fro2, nonfinite), perm_dev
+        return _ops.sketch_gather(a, g, self.r, self.s, out, fro2, nonfinite, amax), perm_dev
 
     def left_t(self, x: torch.Tensor, out=None) -> torch.Tensor:
         if self.kind == "countsketch":

@@ -159,8 +159,11 @@ def test_sketch_gather_permuted(skp, ops, m, n, r, s):
     t.copy_(torch.from_numpy(a))
     fro2 = torch.zeros(1, dtype=torch.float64, device="cuda")
     bad = torch.zeros(1, dtype=torch.int64, device="cuda")
-    out, perm2 = op.right_permuted(t, fro2=fro2, nonfinite=bad)
+    amax = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out, perm2 = op.right_permuted(t, fro2=fro2, nonfinite=bad, amax=amax)
     assert (perm2.cpu().numpy() == perm).all()
+    # the fused max|A S| (input of the 3xFP16 split) is exact
+    assert amax.view(torch.float32).item() == out.abs().max().item()
     ref = o.CountSketch("countsketch", n, r, 13, s=s).apply_right(a.astype(np.float64))
     got = out.cpu().numpy().astype(np.float64)
     scale = np.abs(ref).max()
