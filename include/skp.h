@@ -190,7 +190,9 @@ int skp_cholinv_f64(const double* G, int64_t n, int64_t ld, double rel_tol, doub
 int skp_trinv_lower_f64(const double* L, int64_t ldl, int64_t n, double* X, void* stream);
 
 /* ---------------------------------------------------------------- K6 ----
- * Symmetric eigensolver (parallel cyclic Jacobi, fp64) for the small cores:
+ * Symmetric eigensolver (fp64) for the small cores -- one-CTA cyclic Jacobi
+ * for n <= 112, tridiagonal reduction (cluster sytrd) + bisection + inverse
+ * iteration + back-transform above (eig_tri.cu):
  * the Gram B B^T of randsvd's B = Q^T A (replaces thin_svd / gesdd,
  * linalg.py:84-88) and the Nystrom W.  A (n x n) is destroyed.  On return
  * W[n] holds eigenvalues DESCENDING and V (n x n) the matching eigenvectors
