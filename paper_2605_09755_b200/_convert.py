@@ -54,6 +54,61 @@ def upload(a, name: str = "matrix", device=None, dtype=None, check_finite: bool 
     return op
 
 
+class Streamed:
+    """A host matrix bound for the device in row blocks: ``t`` is the device
+    destination (128-byte rows), allocated but not yet filled; ``blocks()``
+    issues the H2D copy of each block on a side stream and makes the current
+    stream wait for it, so a consumer can start on block b while blocks
+    b+1.. are still on the link (the range finder sketches behind the copy)."""
+
+    BLOCK_BYTES = 1 << 30
+
+    def __init__(self, src: torch.Tensor, dst: torch.Tensor):
+        self.src, self.t = src, dst
+        self.rows_per_block = max(1, self.BLOCK_BYTES // max(1, src.shape[1] * src.element_size()))
+        self.done = False
+
+    def blocks(self):
+        m = self.t.shape[0]
+        dev = self.t.device
+        side = torch.cuda.Stream(dev)
+        cur = torch.cuda.current_stream(dev)
+        side.wait_stream(cur)   # the destination's allocation is ordered on cur
+        for r0 in range(0, m, self.rows_per_block):
+            r1 = min(m, r0 + self.rows_per_block)
+            with torch.cuda.stream(side):
+                self.t[r0:r1].copy_(self.src[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            cur.wait_event(ev)
+            yield r0, r1
+        self.t.record_stream(side)
+        self.done = True
+
+
+def upload_streamed(a, name: str = "matrix", device=None):
+    """(Operand, Streamed | None): like upload(check_finite=False), except that
+    a host 2-D float32/float64 matrix is NOT copied yet -- the caller drives
+    the copy block by block through Streamed.blocks()."""
+    dev = _ops.require_cuda(device)
+    if isinstance(a, torch.Tensor) and (a.is_cuda or a.dim() != 2 or a.dtype not in (F32, F64)):
+        return upload(a, name, device, check_finite=False), None
+    if isinstance(a, torch.Tensor):
+        src, kind = a, "cpu"
+    else:
+        arr = np.asarray(a)
+        if arr.ndim != 2 or arr.size == 0:
+            return upload(a, name, device, check_finite=False), None
+        want = np.float32 if _torch_dtype_for(arr.dtype.type) == F32 else np.float64
+        src, kind = torch.from_numpy(np.ascontiguousarray(arr, dtype=want)), "numpy"
+    if src.numel() == 0:
+        raise ValueError(f"{name} must be non-empty")
+    if src.stride(1) != 1:
+        src = src.contiguous()
+    dst = _ops.empty2d(src.shape[0], src.shape[1], src.dtype, dev)
+    return Operand(dst, kind, name), Streamed(src, dst)
+
+
 def ensure_finite(op: Operand, nonfinite: torch.Tensor | None = None) -> None:
     """Raise ValueError on non-finite entries (one fused device reduction)."""
     if nonfinite is None:

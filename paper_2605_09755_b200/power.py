@@ -135,9 +135,12 @@ def power_iterate(atil, omega, q: int, stabilized: bool = True):
 
 def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL,
                       rows_total: int | None = None, phases: _Phases | None = None,
-                      fro2: torch.Tensor | None = None, name: str = "a"):
+                      fro2: torch.Tensor | None = None, name: str = "a",
+                      streamed: "_convert.Streamed | None" = None):
     """Alg. 1 on a device row slab; returns Q (rows x <= r2).  Raises on
-    non-finite entries of a (counted inside the sketch kernel)."""
+    non-finite entries of a (counted inside the sketch kernel).  streamed: a
+    still arrives from the host block by block -- each block is sketched as
+    soon as it lands, behind the copy of the next (A S is row-separable)."""
     ph = phases or _Phases(False)
     dev = a.device
     m_loc, n = a.shape
@@ -158,12 +161,28 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     # marker in the non-finite count checked at the end)
     # (e_io[1]: max|A~|, accumulated by K2 v2 for the fp16 split below)
     e_io = torch.zeros(2, dtype=torch.int32, device=dev)
-    got = sk.right_permuted(a, fro2=fro2, nonfinite=nonfinite, deferred=True, amax=e_io[1:])
-    if got is not None:
-        atil, perm = got
+    if streamed is None:
+        got = sk.right_permuted(a, fro2=fro2, nonfinite=nonfinite, deferred=True, amax=e_io[1:])
+        if got is not None:
+            atil, perm = got
+        else:
+            atil, perm, e_io = sk.right(a, fro2=fro2, nonfinite=nonfinite), None, None
+        del got
     else:
-        atil, perm, e_io = sk.right(a, fro2=fro2, nonfinite=nonfinite), None, None
-    del got
+        atil = _ops.empty2d(m_loc, spec.r1, a.dtype, dev)
+        v2, perm = None, None
+        for r0, r1 in streamed.blocks():
+            if v2 is not False:
+                got = sk.right_permuted(a[r0:r1], out=atil[r0:r1], fro2=fro2, nonfinite=nonfinite,
+                                        deferred=True, amax=e_io[1:])
+                if got is None and v2:   # v2 applies by dtype/layout: all blocks or none
+                    raise RuntimeError("internal: K2 v2 declined mid-stream")
+                v2 = got is not None
+                perm = got[1] if v2 else None
+                del got
+            if not v2:
+                sk.right(a[r0:r1], out=atil[r0:r1], fro2=fro2, nonfinite=nonfinite)
+                e_io = None
     ph.mark("apply_right")
     # the power iteration's operand: A~ split once into fp16 hi/lo planes (the
     # fp32 A~ is released here; the footprint stays m x l x 4 bytes)
@@ -198,6 +217,8 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
         # K2 v2's schedule overflowed (very uneven sketch columns): K2 v1 in
         # the natural column order, with Omega unpermuted
         nonfinite.zero_()
+        if fro2 is not None:
+            fro2.zero_()
         atil = sk.right(a, fro2=fro2, nonfinite=nonfinite)
         nbad = int(comm.allreduce_(nonfinite).item()) % _ops.GATHER_PLAN_FAIL_MARK
         perm = None
@@ -214,11 +235,11 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
 
 def range_finder_sketched(a, spec: RangeFinderSpec, *, timings: dict | None = None, device=None):
     """Orthonormal range finder from power iteration on the sketch A S (power.py:141-154)."""
-    op = _convert.upload(a, "a", device, check_finite=False)
+    op, streamed = _convert.upload_streamed(a, "a", device)
     m, n = op.t.shape
     spec.validate(m, n)
     ph = _Phases(timings is not None)
-    qb = _range_finder_dev(op.t, spec, phases=ph)
+    qb = _range_finder_dev(op.t, spec, phases=ph, streamed=streamed)
     ph.result(timings)
     return _convert.download(qb, op.kind)
 
@@ -261,12 +282,12 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
     Returns SvdResult, or (SvdResult, rel_err) with ``with_error`` where
     rel_err = ||a - QQ^T a||_F / ||a||_F from ||a||_F^2 - sum(sigma^2)
     (Pythagorean identity; ||a||_F^2 is fused into the sketch)."""
-    op = _convert.upload(a, "a", check_finite=False)
+    op, streamed = _convert.upload_streamed(a, "a")
     m, n = op.t.shape
     spec.validate(m, n)
     ph = _Phases(timings is not None)
     fro2 = torch.zeros(1, dtype=torch.float64, device=op.t.device) if with_error else None
-    qb = _range_finder_dev(op.t, spec, phases=ph, fro2=fro2)
+    qb = _range_finder_dev(op.t, spec, phases=ph, fro2=fro2, streamed=streamed)
     u, s, v = _randsvd_dev(op.t, qb, check=False)
     ph.mark("randsvd")
     res = SvdResult(_convert.download(u, op.kind), _convert.download(s, op.kind),
