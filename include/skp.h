@@ -239,6 +239,22 @@ int skp_gemm_h3(int transA, int64_t M, int64_t N, int64_t K, float alpha, const 
                 const void* B_lo, int64_t ldb, const int32_t* b_exp, float beta, float* C,
                 int64_t ldc, void* ws, int64_t ws_bytes, void* stream);
 
+/* skp_gemm_h3s: C = alpha A^T B + beta C with A (K x M, fp32, lda % 32 == 0)
+ * split into fp16 hi/lo INSIDE the kernel with the caller's exponent 2^a_exp
+ * (a bound on max|A|: skp_h2_exponent_f32), B pre-split as for skp_gemm_h3.
+ * randsvd's B^T = A^T Q (power.py:197), whose A is read once.  If a scaled
+ * entry of A does not fit fp16 (|a 2^e| >= 65504, or NaN), *overflow |= 1
+ * (may be NULL) and C is invalid: the caller recomputes (skp_gemm_f32).
+ * skp_h2_exponent_f32: e_io[0] = 15 - ceil(log2 max|X|) - margin_bits, with
+ * max|X| computed here or (have_amax = 1) taken from e_io[1]'s bits.        */
+int64_t skp_gemm_h3s_ws_bytes(int64_t M, int64_t N, int64_t K);
+int skp_gemm_h3s(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
+                 const int32_t* a_exp, const void* B_hi, const void* B_lo, int64_t ldb,
+                 const int32_t* b_exp, float beta, float* C, int64_t ldc, int32_t* overflow,
+                 void* ws, int64_t ws_bytes, void* stream);
+int skp_h2_exponent_f32(const float* X, int64_t rows, int64_t cols, int64_t ld, int32_t* e_io,
+                        int32_t have_amax, int32_t margin_bits, void* stream);
+
 /* Row gather y[v, :] = x[perm[v], :], v < rows (P^T Omega for the K2 v2
  * column permutation; perm = the first `rows` int32 of a gather plan).       */
 int skp_permute_rows_f32(const float* x, int64_t ldx, const int32_t* perm, float* y, int64_t ldy,

@@ -67,7 +67,7 @@ def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: b
         q = be.mm(y, be.to_compute(x), tb=True)
         if passes == 1:
             return q
-        g2 = comm.allreduce_(be.gram64(q))
+        g2 = comm.allreduce_(be.gram64(q, accurate=True))
         x2 = be.chol_inv64(g2, 0.0, lazy=True)
         return be.mm(q, be.to_compute(x2), tb=True)
     x = be.chol_inv64(g, rel)
@@ -82,7 +82,7 @@ def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: b
         if x is None:
             raise RuntimeError("orthonormalize: Cholesky failed after rank truncation")
     q = be.mm(y, be.to_compute(x), tb=True)
-    g2 = comm.allreduce_(be.gram64(q))
+    g2 = comm.allreduce_(be.gram64(q, accurate=True))
     x2 = be.chol_inv64(g2, 0.0)
     if x2 is None:
         raise RuntimeError("orthonormalize: second CholeskyQR pass failed")
@@ -106,7 +106,7 @@ def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_t
     return y
 
 
-def randsvd(be, comm, a, qb, check: bool = True):
+def randsvd(be, comm, a, qb, check: bool = True, amax_hint=None):
     """power.py:181-199: B = Q^T A (summed over row slabs), thin SVD of B via
     the fp64 Gram B B^T and the eigensolver; U = Q U~, V = B^T U~ / sigma.
 
@@ -118,7 +118,12 @@ def randsvd(be, comm, a, qb, check: bool = True):
         dev = be.orth_dev(g)
         if not dev <= ORTHO_TOL[_dtype_key(be)]:
             raise ValueError(f"Q is not orthonormal (deviation {dev:.3e})")
-    bt = comm.allreduce_(be.mm(a, qb, ta=True))           # n x c
+    bt = be.mm_at_big(a, qb, amax_hint)                      # n x c, this rank's part
+    if be.overflowed(comm):
+        # the in-kernel fp16 split met an entry beyond its exponent bound
+        # (a hint that did not hold): recompute with 3xTF32 on every rank
+        bt = be.mm(a, qb, ta=True)
+    bt = comm.allreduce_(bt)
     n, c = bt.shape
     gb = be.gram64_rows_t(bt)                               # c x c, fp64
     w, v = be.eig_desc64(gb)

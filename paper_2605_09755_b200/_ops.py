@@ -314,6 +314,39 @@ def gemm_h3(a: SplitH2, b: SplitH2, ta: bool = False, alpha: float = 1.0, beta: 
     return out
 
 
+def h2_exponent(x: torch.Tensor, e_io: torch.Tensor | None = None, have_amax: bool = False,
+                margin_bits: int = 0) -> torch.Tensor:
+    """int32[2] e_io with e_io[0] = 15 - ceil(log2 max|x|) - margin_bits (max|x|
+    computed here unless have_amax: then e_io[1] holds its bits already)."""
+    r, c, ld = _rows_ld(x)
+    if e_io is None:
+        e_io = torch.zeros(2, dtype=torch.int32, device=x.device)
+    call("skp_h2_exponent_f32", ptr(x), r, c, ld, ptr(e_io), int(have_amax), int(margin_bits),
+         stream_ptr(x.device))
+    return e_io
+
+
+def gemm_h3s_t(a: torch.Tensor, a_e: torch.Tensor, b: SplitH2, alpha: float = 1.0,
+               beta: float = 0.0, out=None, overflow=None) -> torch.Tensor:
+    """K4h with the in-kernel split: out = alpha a^T b_src + beta out, a
+    (K x M fp32) scaled by 2^a_e[0], b pre-split (b.rows = N, b.cols = K)."""
+    K, M, lda = _rows_ld(a)
+    N, Kb = b.rows, b.cols
+    if K != Kb:
+        raise ValueError(f"dimension mismatch: {M}x{K} @ {Kb}x{N}")
+    if out is None:
+        if beta != 0.0:
+            raise ValueError("beta != 0 needs out")
+        out = empty2d(M, N, F32, a.device)
+    _, _, ldc = _rows_ld(out)
+    lib = _lib.load()
+    wsb = lib.skp_gemm_h3s_ws_bytes(M, N, K)
+    ws = workspace(a.device, wsb) if wsb else None
+    call("skp_gemm_h3s", M, N, K, alpha, ptr(a), lda, ptr(a_e), ptr(b.hi), ptr(b.lo), b.ld,
+         ptr(b.e), beta, ptr(out), ldc, ptr(overflow), ptr(ws), wsb, stream_ptr(a.device))
+    return out
+
+
 # ------------------------------------------------------------ utilities ----
 
 def cast(x: torch.Tensor, dtype) -> torch.Tensor:
@@ -365,6 +398,7 @@ class CudaBackend:
         self.info = torch.zeros(2, dtype=torch.int32, device=device)
         self.fail = torch.zeros(2, dtype=torch.int32, device=device)
         self._bsplit = {}
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=device)
 
     # dense products in the compute dtype
     def mm(self, a, b, ta=False, tb=False, out=None, alpha=1.0, beta=0.0):
@@ -376,6 +410,33 @@ class CudaBackend:
             self._bsplit[key] = sb = split_h2(b, trans=True, out=self._bsplit.get(key))
             return gemm_h3(a, sb, ta=ta, alpha=alpha, beta=beta, out=out)
         return gemm(a, b, ta, tb, alpha=alpha, beta=beta, out=out, mode=self.gemm_mode)
+
+    def mm_at_big(self, a, q, amax_hint=None):
+        """a^T q for the one-pass product of randsvd (a = the input, read
+        once): 3xFP16 with a split in the kernel where it applies, else
+        3xTF32.  amax_hint = (e_io, margin_bits): e_io[1] holds the bits of a
+        value v with max|a| <= v 2^margin_bits expected (from max|A S|); a
+        wrong hint is caught by the kernel's overflow flag (overflowed())."""
+        K, M = a.shape
+        self.overflow.zero_()
+        if (self.dtype != F32 or self.gemm_mode != "auto" or a.shape[0] * a.shape[1] < H3_MIN_ELEMS
+                or a.stride(1) != 1 or a.stride(0) % 32 or a.data_ptr() % 16
+                or os.environ.get("SKP_NO_H3") or not _lib.load().skp_has_tcgen05()):
+            return self.mm(a, q, ta=True)
+        if amax_hint is not None:
+            e_a = amax_hint[0].clone()
+            h2_exponent(a, e_a, have_amax=True, margin_bits=amax_hint[1])
+        else:
+            e_a = h2_exponent(a)
+        sq = split_h2(q, trans=True)
+        return gemm_h3s_t(a, e_a, sq, overflow=self.overflow)
+
+    def overflowed(self, comm=None) -> bool:
+        """Did the last mm_at_big overflow (on any rank)?  Host sync."""
+        f = self.overflow.clone()
+        if comm is not None:
+            comm.allreduce_(f)
+        return bool(f.item())
 
     def prepare(self, x, e_io=None):
         """A left operand reused by several products (the power iteration's
@@ -391,9 +452,22 @@ class CudaBackend:
             return x
         return split_h2(x, e_io=e_io)
 
-    def gram64(self, y):
-        """y^T y as fp64 (computed in the compute dtype, then widened)."""
+    def gram64(self, y, accurate: bool = False):
+        """y^T y as fp64 (computed in the compute dtype, then widened).
+        accurate: the Gram that decides the final Q's orthonormality (the
+        last CholeskyQR pass).  Over K = rows ~ 1e5 the tensor core's
+        truncating fp32 accumulation biases a Gram's diagonal by ~1e-4
+        (measured at C3: Q^T Q = (1 + 1.2e-4) I, i.e. sigma inflated by 6e-5),
+        so that pass runs 3xFP16 with register-promoted accumulation."""
+        if accurate and self._h3_ok(y):
+            sy = split_h2(y, trans=True)            # y^T planes: (cols x rows), K-major
+            return cast(gemm_h3(sy, sy), F64)
         return cast(self.mm(y, y, ta=True), F64)
+
+    def _h3_ok(self, x) -> bool:
+        return (self.dtype == F32 and self.gemm_mode == "auto" and x.dim() == 2
+                and x.shape[0] * x.shape[1] >= H3_MIN_ELEMS and not os.environ.get("SKP_NO_H3")
+                and bool(_lib.load().skp_has_tcgen05()))
 
     def gram64_rows(self, b):
         """b b^T in fp64 arithmetic (b: c x n, widened first)."""

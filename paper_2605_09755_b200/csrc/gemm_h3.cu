@@ -47,7 +47,13 @@ namespace {
 constexpr int HM = 128;          // UMMA M per CTA
 constexpr int HK = 64;           // fp16 K per stage: one 128-byte swizzled row
 constexpr int kHKSteps = HK / 16;  // f16 UMMA K = 16
-constexpr int kHWarpTma = 0, kHWarpMma = 1, kHWarpEpi = 2, kHNumEpi = 4;
+constexpr int kHWarpTma = 0, kHWarpMma = 1, kHWarpEpi = 2, kHNumEpi = 12;
+// 16-column groups per epilogue thread: the accumulator lives in registers
+// across the chunks of a unit, 3 column thirds x 4 groups -> bn <= 192 (14
+// warps leave 128 registers a thread: 4 warps share an SMSP's 16K registers)
+constexpr int kHEpiCols = 4;
+constexpr int kHEpiParts = kHNumEpi / 4;
+constexpr int kHMaxBn = kHEpiParts * 16 * kHEpiCols;
 constexpr int kHThreads = 32 * (kHWarpEpi + kHNumEpi);
 constexpr uint32_t kHTmemCols = 512;
 constexpr int kHMaxStages = 8;
@@ -67,6 +73,7 @@ struct H3Params {
     int acc_stride;
     const int* a_e;
     const int* b_e;
+    int chunk_kb;  // K blocks per accumulation chunk (promotion period)
 };
 
 // TMA 2-D / 3-D loads signalling a barrier given by its shared::cluster
@@ -128,6 +135,46 @@ __device__ __forceinline__ void h_mma(uint32_t d, uint64_t a, uint64_t b, uint32
             "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n\t}" ::"r"(d),
             "l"(a), "l"(b), "r"(idesc), "r"(acc)
             : "memory");
+}
+
+// mbarrier wait for the epilogue warps: back off between polls (12 warps
+// spinning on try_wait took issue slots from the TMA / MMA warps)
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    long long t0 = 0;
+    for (int it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(128);
+        if (it == 64) t0 = clock64();
+        if (it > 64 && (it & 1023) == 0 && clock64() - t0 > (long long)40e9) __trap();
+    }
+}
+
+// acc[0..15] += v[0..15] as ONE volatile asm: it stays ordered against the
+// tcgen05.ld of the next 16 columns, so only 16 loaded values are live at a
+// time (left to the compiler, all groups' loads were hoisted and spilled)
+__device__ __forceinline__ void acc_add16(float* acc, const float* v) {
+    asm volatile(
+        "add.f32 %0, %0, %16;\n\tadd.f32 %1, %1, %17;\n\tadd.f32 %2, %2, %18;\n\t"
+        "add.f32 %3, %3, %19;\n\tadd.f32 %4, %4, %20;\n\tadd.f32 %5, %5, %21;\n\t"
+        "add.f32 %6, %6, %22;\n\tadd.f32 %7, %7, %23;\n\tadd.f32 %8, %8, %24;\n\t"
+        "add.f32 %9, %9, %25;\n\tadd.f32 %10, %10, %26;\n\tadd.f32 %11, %11, %27;\n\t"
+        "add.f32 %12, %12, %28;\n\tadd.f32 %13, %13, %29;\n\tadd.f32 %14, %14, %30;\n\t"
+        "add.f32 %15, %15, %31;"
+        : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3]), "+f"(acc[4]), "+f"(acc[5]),
+          "+f"(acc[6]), "+f"(acc[7]), "+f"(acc[8]), "+f"(acc[9]), "+f"(acc[10]), "+f"(acc[11]),
+          "+f"(acc[12]), "+f"(acc[13]), "+f"(acc[14]), "+f"(acc[15])
+        : "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+          "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+          "f"(v[15]));
 }
 
 struct HWork {
@@ -238,83 +285,118 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
         const uint64_t ajstep = p.a_kmajor ? (32u >> 4) : (2048u >> 4);  // 16 K: +32 B | +2 rows groups
         const uint64_t bjstep = 32u >> 4;
         const uint64_t alo = p.a_bytes >> 4, blo = p.b_bytes >> 4;
+        // Accumulation chunks of chunk_kb K blocks alternate between the two
+        // TMEM buffers; the epilogue adds each finished chunk into registers
+        // (fp32, round to nearest) while the next one accumulates.  The
+        // tensor core's own fp32 accumulation truncates, so its error grows
+        // with the chain length (K = 262144 in one chain: -3e-5 relative on
+        // positive data, about -1e-4 on sigma at C3); chains of 1024 keep it
+        // at ~7e-6 there (measured: 512 -> 3.3e-6, 64 -> 2.3e-7).
         Ring r;
-        int ul = 0;
-        for (int u = ustart; u < units; u += ustride, ++ul) {
+        int cc = 0;
+        for (int u = ustart; u < units; u += ustride) {
             const HWork w = h_unit(p, u);
-            const int buf = ul & 1;
-            const uint32_t aph = (uint32_t)(ul >> 1) & 1u;
-            mbar_wait(&tempty[buf], aph ^ 1);
-            tc_fence_after();
-            const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
-            for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
-                const int s = r.s;
-                mbar_wait(&full[s], r.ph);
+            for (int c0 = w.kb0; c0 < w.kb1; c0 += p.chunk_kb, ++cc) {
+                const int buf = cc & 1;
+                const uint32_t aph = (uint32_t)(cc >> 1) & 1u;
+                mbar_wait(&tempty[buf], aph ^ 1);
                 tc_fence_after();
-                const uint64_t as = a0 + (uint64_t)s * sstep, bs = b0 + (uint64_t)s * sstep;
+                const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
+                const int c1 = min(c0 + p.chunk_kb, w.kb1);
+                for (int kb = c0; kb < c1; ++kb, r.next(S)) {
+                    const int s = r.s;
+                    mbar_wait(&full[s], r.ph);
+                    tc_fence_after();
+                    const uint64_t as = a0 + (uint64_t)s * sstep, bs = b0 + (uint64_t)s * sstep;
 #pragma unroll
-                for (int j = 0; j < kHKSteps; ++j) {
-                    const uint32_t acc = (kb > w.kb0 || j > 0) ? 1u : 0u;
-                    const uint64_t ah = as + (uint64_t)j * ajstep, bh = bs + (uint64_t)j * bjstep;
-                    h_mma<kPair>(d, ah + alo, bh, p.idesc, acc);  // a_lo b_hi
-                    h_mma<kPair>(d, ah, bh + blo, p.idesc, 1u);   // a_hi b_lo
-                    h_mma<kPair>(d, ah, bh, p.idesc, 1u);         // a_hi b_hi
+                    for (int j = 0; j < kHKSteps; ++j) {
+                        const uint32_t acc = (kb > c0 || j > 0) ? 1u : 0u;
+                        const uint64_t ah = as + (uint64_t)j * ajstep, bh = bs + (uint64_t)j * bjstep;
+                        h_mma<kPair>(d, ah + alo, bh, p.idesc, acc);  // a_lo b_hi
+                        h_mma<kPair>(d, ah, bh + blo, p.idesc, 1u);   // a_hi b_lo
+                        h_mma<kPair>(d, ah, bh, p.idesc, 1u);         // a_hi b_hi
+                    }
+                    if (kPair) tc_commit_pair_e(&empty[s]);
+                    else tc_commit_e(&empty[s]);
                 }
-                if (kPair) tc_commit_pair_e(&empty[s]);
-                else tc_commit_e(&empty[s]);
+                if (kPair) tc_commit_pair_e(&tfull[buf]);
+                else tc_commit_e(&tfull[buf]);
             }
-            if (kPair) tc_commit_pair_e(&tfull[buf]);
-            else tc_commit_e(&tfull[buf]);
         }
     } else if (warp >= kHWarpEpi) {
-        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        // 12 warps: TMEM lane quadrant q = warp % 4, column part = which 4 of them
+        const int q = warp & 3;
+        const int part = (warp - kHWarpEpi) >> 2;
+        const int ng = p.bn / 16, per = (ng + kHEpiParts - 1) / kHEpiParts;
+        const int g0 = part * per;                               // first 16-column group
+        const int g1 = min(ng, g0 + per);                        // past the last
         // 2^-(ea+eb), applied as two exact power-of-two factors
         const float sc = ldexpf(1.f, -__ldg(p.a_e)) * ldexpf(1.f, -__ldg(p.b_e));
         const float alpha = p.alpha * sc;
-        int ul = 0;
-        for (int u = ustart; u < units; u += ustride, ++ul) {
+        int cc = 0;
+        for (int u = ustart; u < units; u += ustride) {
             const HWork w = h_unit(p, u);
-            const int buf = ul & 1;
-            const uint32_t aph = (uint32_t)(ul >> 1) & 1u;
-            mbar_wait(&tfull[buf], aph);
-            tc_fence_after();
+            float acc[kHEpiCols][16];
+#pragma unroll
+            for (int i = 0; i < kHEpiCols; ++i)
+#pragma unroll
+                for (int e = 0; e < 16; ++e) acc[i][e] = 0.f;
+            for (int c0 = w.kb0; c0 < w.kb1; c0 += p.chunk_kb, ++cc) {
+                const int buf = cc & 1;
+                const uint32_t aph = (uint32_t)(cc >> 1) & 1u;
+                mbar_wait_idle(&tfull[buf], aph);
+                tc_fence_after();
+                const uint32_t tbase =
+                    tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * p.acc_stride);
+#pragma unroll
+                for (int i = 0; i < kHEpiCols; ++i) {
+                    if (g0 + i < g1) {
+                        float v[16];
+                        tmem_ld16(tbase + 16u * (uint32_t)(g0 + i), v);
+                        acc_add16(acc[i], v);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (kPair) mbar_arrive_cluster_e(tempty_cl0 + 8u * (uint32_t)buf);
+                else mbar_arrive_e(&tempty[buf]);
+            }
             const int row = w.tm * kRowsPerUnit + (int)rank * HM + q * 32 + lane;
-            const uint32_t tbase =
-                tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * p.acc_stride);
-            for (int c0 = 0; c0 < p.bn; c0 += 16) {
-                float v[16];
-                tmem_ld16(tbase + c0, v);
-                const int col0 = w.tn * p.bn + c0;
-                if (row >= p.M || col0 >= p.N) continue;
+            if (row >= p.M) continue;
+#pragma unroll
+            for (int i = 0; i < kHEpiCols; ++i) {
+                const int col0 = w.tn * p.bn + 16 * (g0 + i);
+                if (g0 + i >= g1 || col0 >= p.N) continue;
                 const int lim = min(16, p.N - col0);
                 if (p.splits > 1) {
                     float* dst = p.ws + ((size_t)w.ks * p.M + row) * p.N + col0;
-                    for (int i = 0; i < lim; ++i) dst[i] = sc * v[i];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        if (e < lim) dst[e] = sc * acc[i][e];
                 } else {
                     float* dst = p.C + (size_t)row * p.ldc + col0;
                     const bool vec = lim == 16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
                     if (vec) {
 #pragma unroll
-                        for (int i = 0; i < 16; i += 4) {
-                            float4 o = make_float4(alpha * v[i], alpha * v[i + 1], alpha * v[i + 2],
-                                                   alpha * v[i + 3]);
+                        for (int e = 0; e < 16; e += 4) {
+                            float4 o = make_float4(alpha * acc[i][e], alpha * acc[i][e + 1],
+                                                   alpha * acc[i][e + 2], alpha * acc[i][e + 3]);
                             if (p.beta != 0.f) {
-                                const float4 c = *reinterpret_cast<float4*>(dst + i);
+                                const float4 c = *reinterpret_cast<float4*>(dst + e);
                                 o.x += p.beta * c.x; o.y += p.beta * c.y;
                                 o.z += p.beta * c.z; o.w += p.beta * c.w;
                             }
-                            *reinterpret_cast<float4*>(dst + i) = o;
+                            *reinterpret_cast<float4*>(dst + e) = o;
                         }
                     } else {
-                        for (int i = 0; i < lim; ++i)
-                            dst[i] = p.beta != 0.f ? alpha * v[i] + p.beta * dst[i] : alpha * v[i];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            if (e < lim)
+                                dst[e] = p.beta != 0.f ? alpha * acc[i][e] + p.beta * dst[e]
+                                                       : alpha * acc[i][e];
                     }
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (kPair) mbar_arrive_cluster_e(tempty_cl0 + 8u * (uint32_t)buf);
-            else mbar_arrive_e(&tempty[buf]);
         }
     }
     tc_fence_before();
@@ -452,6 +534,355 @@ split_h2_t_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64
     }
 }
 
+
+// ---------------------------------------------- 3xFP16 with an in-kernel A split --
+// gemm_h3s: the same products with A given in FP32 -- for the one big
+// product whose left operand is read once (randsvd's B^T = A^T Q, A = the
+// m x n input itself, too large to pre-split: a split pass would cost more
+// HBM time than it saves).  op(A) = A^T with A stored K x M (MN-major),
+// exponent 2^ea from the caller (a bound on max|A|); B pre-split (K-major
+// planes).  Warps: 0 TMA (fp32 A tile as [4 chunks][HK k][32 m], B hi/lo
+// planes), 1 MMA (kind::f16 with A from TENSOR MEMORY), 2-5 split (thread =
+// tile row: 64 fp32 -> (hi, lo) fp16 pairs -> tcgen05.st into the stage's TMEM
+// slot), 6-9 epilogue.  TMEM: [accumulator | A slots of 64 columns: 32 hi |
+// 32 lo].  A value that does not fit fp16 after scaling sets *overflow (the
+// caller then recomputes with 3xTF32).
+constexpr int kSWarpTma = 0, kSWarpMma = 1, kSWarpAx = 2, kSWarpEpi = 6, kSNumEpi = 8;
+constexpr int kSThreads = 32 * (kSWarpEpi + kSNumEpi);
+constexpr int kSEpiCols = 6;                     // 16-column groups per epilogue thread
+constexpr int kSMaxBn = 2 * 16 * kSEpiCols;      // 192
+constexpr int kSSlots = 2;                       // TMEM A slots (the smem ring runs deeper)
+constexpr uint32_t kSSlotCols = 64;              // 32 hi | 32 lo (2 fp16 per column)
+constexpr uint32_t kSChunkBytes = 32 * HK * 4;   // fp32 A: 32 M x HK K per box chunk
+
+struct H3SParams {
+    int M, N, K;
+    int bn, tiles_m, tiles_n, splits, kb_per_split, num_kb;
+    float alpha, beta;
+    float* C;
+    long long ldc;
+    float* ws;
+    int stages;
+    uint32_t a_bytes, b_bytes, stage_bytes;
+    uint32_t idesc;
+    int acc_stride;
+    const int* a_e;
+    const int* b_e;
+    int* overflow;
+    int chunk_kb;
+};
+
+__device__ __forceinline__ HWork hs_unit(const H3SParams& p, int u) {
+    HWork w;
+    w.tn = u % p.tiles_n;
+    const int r = u / p.tiles_n;
+    w.tm = r % p.tiles_m;
+    w.ks = r / p.tiles_m;
+    w.kb0 = w.ks * p.kb_per_split;
+    w.kb1 = min(w.kb0 + p.kb_per_split, p.num_kb);
+    return w;
+}
+
+// D[tmem] (+)= A[tmem] * B[smem desc], kind::f16
+template <bool kPair>
+__device__ __forceinline__ void hs_mma(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+    if (kPair)
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t.reg .b32 r;\n\t"
+            "setp.ne.b32 q, %4, 0;\n\t"
+            "elect.sync r|p, 0xffffffff;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, q;\n\t}" ::"r"(d),
+            "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t.reg .b32 r;\n\t"
+            "setp.ne.b32 q, %4, 0;\n\t"
+            "elect.sync r|p, 0xffffffff;\n\t"
+            "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, q;\n\t}" ::"r"(d),
+            "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+}
+
+// two fp32 values (already scaled) -> packed fp16 hi pair and lo pair
+__device__ __forceinline__ void h2_split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(x0, x1);     // .x (low half) = x0
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+template <bool kPair>
+__global__ void __launch_bounds__(kSThreads, 1)
+gemm_h3s_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bh,
+                const __grid_constant__ CUtensorMap map_bl, const H3SParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = p.stages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
+    uint64_t* full = bars;                 // [S] smem stage landed (TMA)
+    uint64_t* empty = bars + S;            // [S] smem stage consumed (MMA commit)
+    uint64_t* split = bars + 2 * S;        // [2] TMEM A slot written (split warps)
+    uint64_t* slotfree = split + kSSlots;  // [2] TMEM A slot consumed (MMA commit)
+    uint64_t* tfull = slotfree + kSSlots;  // [2] accumulator chunk done (MMA commit)
+    uint64_t* tempty = tfull + 2;          // [2] accumulator drained (epilogue)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int units = p.tiles_m * p.tiles_n * p.splits;
+    const uint32_t rank = kPair ? cluster_rank() : 0u;
+    const bool leader = rank == 0;
+    const int ustart = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int ustride = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    constexpr int kRowsPerUnit = kPair ? 2 * HM : HM;
+    constexpr int kNumXf = 4;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int t = 0; t < kSSlots; ++t) {
+            // paired: the peer's MMA warp forwards its split warps' completion
+            // as ONE cluster arrive on the leader's split[t]
+            mbar_init(&split[t], (kPair && leader) ? kNumXf + 1 : kNumXf);
+            mbar_init(&slotfree[t], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], kPair ? 2 * kSNumEpi : kSNumEpi);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == kSWarpMma) {
+        if (kPair) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kHTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kHTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+    }
+    tc_fence_before();
+    if (kPair) cluster_sync_all();
+    else __syncthreads();
+    tc_fence_after();
+    const uint32_t split_cl0 = kPair ? mapa_shared(smem_u32(split), 0) : 0u;
+    const uint32_t tempty_cl0 = kPair ? mapa_shared(smem_u32(tempty), 0) : 0u;
+    const uint32_t tmem_base = *tmem_slot;
+    // TMEM: [accumulator 0 | accumulator 1 | A slot 0 | A slot 1]
+    const uint32_t acol0 = 2u * (uint32_t)p.acc_stride;
+    const uint32_t smem0 = smem_u32(smem);
+
+    if (warp == kSWarpTma) {
+        Ring r;
+        const int bcols = kPair ? p.bn / 2 : p.bn;
+        for (int u = ustart; u < units; u += ustride) {
+            const HWork w = hs_unit(p, u);
+            const int m0 = w.tm * kRowsPerUnit + (int)rank * HM;
+            const int n0 = w.tn * p.bn + (int)rank * bcols;
+            for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
+                const int s = r.s;
+                mbar_wait(&empty[s], r.ph ^ 1);
+                mbar_expect_tx_e(&full[s], p.stage_bytes);
+                const uint32_t st = smem0 + (uint32_t)s * p.stage_bytes;
+                const uint32_t bar = smem_u32(&full[s]);
+                const int k0 = kb * HK;
+                h_tma_3d<false>(&map_a, bar, st, 0, k0, m0 / 32);
+                h_tma_2d<false>(&map_bh, bar, st + p.a_bytes, k0, n0);
+                h_tma_2d<false>(&map_bl, bar, st + p.a_bytes + p.b_bytes, k0, n0);
+            }
+        }
+    } else if (warp == kSWarpMma && leader) {
+        // accumulation chunks alternate between the two TMEM accumulators and
+        // are summed in registers by the epilogue (see gemm_h3_kernel)
+        const uint64_t b0 = make_desc(smem0 + p.a_bytes, 16u, 1024u, kLayoutSW128);
+        const uint64_t sstep = p.stage_bytes >> 4;
+        const uint64_t bjstep = 32u >> 4;
+        const uint64_t blo = p.b_bytes >> 4;
+        Ring r, rt;
+        int cc = 0;
+        for (int u = ustart; u < units; u += ustride) {
+            const HWork w = hs_unit(p, u);
+            for (int c0 = w.kb0; c0 < w.kb1; c0 += p.chunk_kb, ++cc) {
+                const int buf = cc & 1;
+                mbar_wait(&tempty[buf], ((uint32_t)(cc >> 1) & 1u) ^ 1u);
+                tc_fence_after();
+                const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
+                const int c1 = min(c0 + p.chunk_kb, w.kb1);
+                for (int kb = c0; kb < c1; ++kb, r.next(S), rt.next(kSSlots)) {
+                    const int s = r.s, t = rt.s;
+                    mbar_wait(&split[t], rt.ph);  // implies stage s landed
+                    tc_fence_after();
+                    const uint64_t bs = b0 + (uint64_t)s * sstep;
+                    const uint32_t ah = tmem_base + acol0 + kSSlotCols * (uint32_t)t;
+#pragma unroll
+                    for (int j = 0; j < kHKSteps; ++j) {
+                        const uint32_t acc = (kb > c0 || j > 0) ? 1u : 0u;
+                        const uint32_t a_hi = ah + 8u * j, a_lo = a_hi + 32u;
+                        const uint64_t bh = bs + (uint64_t)j * bjstep;
+                        hs_mma<kPair>(d, a_lo, bh, p.idesc, acc);      // a_lo b_hi
+                        hs_mma<kPair>(d, a_hi, bh + blo, p.idesc, 1u); // a_hi b_lo
+                        hs_mma<kPair>(d, a_hi, bh, p.idesc, 1u);       // a_hi b_hi
+                    }
+                    if (kPair) {
+                        tc_commit_pair_e(&empty[s]);
+                        tc_commit_pair_e(&slotfree[t]);
+                    } else {
+                        tc_commit_e(&empty[s]);
+                        tc_commit_e(&slotfree[t]);
+                    }
+                }
+                if (kPair) tc_commit_pair_e(&tfull[buf]);
+                else tc_commit_e(&tfull[buf]);
+            }
+        }
+    } else if (kPair && warp == kSWarpMma) {
+        // peer CTA: forward "slot t split done" to the leader's split[t]
+        Ring rt;
+        for (int u = ustart; u < units; u += ustride) {
+            const HWork w = hs_unit(p, u);
+            for (int kb = w.kb0; kb < w.kb1; ++kb, rt.next(kSSlots)) {
+                mbar_wait(&split[rt.s], rt.ph);
+                mbar_arrive_cluster_e(split_cl0 + 8u * (uint32_t)rt.s);
+            }
+        }
+    } else if (warp >= kSWarpAx && warp < kSWarpEpi) {
+        // split: thread = tile row (TMEM lane); lane quadrant = warp % 4 = box chunk
+        const int q = warp & 3;
+        const uint32_t tlane = (uint32_t)(q * 32) << 16;
+        const float sa = ldexpf(1.f, __ldg(p.a_e));
+        float amax = 0.f;
+        Ring r, rt;
+        for (int u = ustart; u < units; u += ustride) {
+            const HWork w = hs_unit(p, u);
+            // rows past M read the row padding (any bits): kept out of the
+            // overflow test; their outputs are never stored
+            const bool live = w.tm * kRowsPerUnit + (int)rank * HM + q * 32 + lane < p.M;
+            for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S), rt.next(kSSlots)) {
+                const int s = r.s, t = rt.s;
+                mbar_wait(&full[s], r.ph);
+                mbar_wait(&slotfree[t], rt.ph ^ 1);
+                tc_fence_after();
+                // [chunk q][k][32 m]: lanes read 128 contiguous bytes per k
+                const uint32_t cb = smem0 + (uint32_t)s * p.stage_bytes +
+                                    (uint32_t)q * kSChunkBytes + (uint32_t)lane * 4u;
+                const uint32_t ta = tmem_base + tlane + acol0 + kSSlotCols * (uint32_t)t;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {  // K 0..31 | 32..63
+                    uint32_t hi[16], lo[16];
+#pragma unroll
+                    for (int k2 = 0; k2 < 16; ++k2) {
+                        const int k = half * 32 + 2 * k2;
+                        const float x0 = __uint_as_float(lds32(cb + 128u * k)) * sa;
+                        const float x1 = __uint_as_float(lds32(cb + 128u * (k + 1))) * sa;
+                        if (live) amax = fmaxf(amax, fmaxf(fabsf(x0), fabsf(x1)));
+                        h2_split2(x0, x1, hi[k2], lo[k2]);
+                    }
+                    tmem_st16(ta + 16u * half, hi);
+                    tmem_st16(ta + 32u + 16u * half, lo);
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                mbar_arrive_e(&split[t]);
+            }
+        }
+        // fp16 holds |x| < 65520 (round to nearest); NaN entries propagate to C
+        if (!(amax < 65504.f) && p.overflow) atomicOr(p.overflow, 1);
+    } else if (warp >= kSWarpEpi) {
+        // 8 warps: TMEM lane quadrant q = warp % 4, column half = which 4 of them
+        const int q = warp & 3;
+        const int part = (warp - kSWarpEpi) >> 2;
+        const int ng = p.bn / 16, per = (ng + 1) / 2;
+        const int g0 = part * per, g1 = min(ng, g0 + per);
+        const float sc = ldexpf(1.f, -__ldg(p.a_e)) * ldexpf(1.f, -__ldg(p.b_e));
+        const float alpha = p.alpha * sc;
+        int cc = 0;
+        for (int u = ustart; u < units; u += ustride) {
+            const HWork w = hs_unit(p, u);
+            float acc[kSEpiCols][16];
+#pragma unroll
+            for (int i = 0; i < kSEpiCols; ++i)
+#pragma unroll
+                for (int e = 0; e < 16; ++e) acc[i][e] = 0.f;
+            for (int c0 = w.kb0; c0 < w.kb1; c0 += p.chunk_kb, ++cc) {
+                const int buf = cc & 1;
+                mbar_wait_idle(&tfull[buf], (uint32_t)(cc >> 1) & 1u);
+                tc_fence_after();
+                const uint32_t tbase =
+                    tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * p.acc_stride);
+#pragma unroll
+                for (int i = 0; i < kSEpiCols; ++i) {
+                    if (g0 + i < g1) {
+                        float v[16];
+                        tmem_ld16(tbase + 16u * (uint32_t)(g0 + i), v);
+                        acc_add16(acc[i], v);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (kPair) mbar_arrive_cluster_e(tempty_cl0 + 8u * (uint32_t)buf);
+                else mbar_arrive_e(&tempty[buf]);
+            }
+            const int row = w.tm * kRowsPerUnit + (int)rank * HM + q * 32 + lane;
+            if (row >= p.M) continue;
+#pragma unroll
+            for (int i = 0; i < kSEpiCols; ++i) {
+                const int col0 = w.tn * p.bn + 16 * (g0 + i);
+                if (g0 + i >= g1 || col0 >= p.N) continue;
+                const int lim = min(16, p.N - col0);
+                if (p.splits > 1) {
+                    float* dst = p.ws + ((size_t)w.ks * p.M + row) * p.N + col0;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        if (e < lim) dst[e] = sc * acc[i][e];
+                } else {
+                    float* dst = p.C + (size_t)row * p.ldc + col0;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        if (e < lim)
+                            dst[e] = p.beta != 0.f ? alpha * acc[i][e] + p.beta * dst[e]
+                                                   : alpha * acc[i][e];
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    if (kPair) cluster_sync_all();
+    else __syncthreads();
+    if (warp == kSWarpMma) {
+        tc_fence_after();
+        if (kPair)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(kHTmemCols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(kHTmemCols));
+    }
+}
+
+// e_io[0] = 15 - E - margin for max|X| = f 2^E (max from e_io[1]'s bits)
+__global__ void h2_exponent_kernel(int* e_io, int margin) {
+    if (threadIdx.x == 0) {
+        const float a = __uint_as_float((uint32_t)e_io[1]);
+        int e = 0;
+        if (a > 0.f && isfinite(a)) {
+            int E;
+            frexpf(a, &E);
+            e = min(15 - E - margin, 126);
+        }
+        e_io[0] = e;
+    }
+}
+
 // ----------------------------------------------------------------- host ----
 PFN_cuTensorMapEncodeTiled_v12000 h_encode = nullptr;
 int h_state = -1;
@@ -508,6 +939,12 @@ struct HPlan {
     size_t smem;
 };
 
+// K blocks per accumulation chunk (chains of 1024): see the MMA role
+int h_chunk_kb() {
+    static int v = getenv("SKP_H3_CHUNK") ? std::max(1, atoi(getenv("SKP_H3_CHUNK"))) : 16;
+    return v;
+}
+
 bool h_pair(int64_t M) {
     if (getenv("SKP_H3_NO2CTA")) return false;
     if (getenv("SKP_H3_FORCE2CTA")) return true;
@@ -516,7 +953,7 @@ bool h_pair(int64_t M) {
 
 HPlan h_plan(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool pair) {
     HPlan pl;
-    const int max_bn = pair ? 256 : 128;
+    const int max_bn = pair ? kHMaxBn : 128;
     pl.tiles_n = (int)cdiv(N, max_bn);
     pl.bn = (int)(cdiv(cdiv(N, pl.tiles_n), 16) * 16);
     pl.tiles_m = (int)cdiv(M, pair ? 2 * HM : HM);
@@ -551,6 +988,31 @@ HPlan h_plan(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool pair) {
     return pl;
 }
 
+
+// fp32 A stored [K x M] (M contiguous) as {32, K, M/32 chunks}: one box
+// {32, HK, 4} = the CTA's 128 M x HK K tile as [chunk][k][32], unswizzled (the
+// split warps read it row-per-lane)
+bool hs_encode_a(CUtensorMap* map, const float* base, uint64_t m, uint64_t k, uint64_t ld) {
+    cuuint64_t dims[3] = {32, k, (cuuint64_t)cdiv((int64_t)m, 32)};
+    cuuint64_t strides[2] = {ld * 4, 128};
+    cuuint32_t box[3] = {32, (cuuint32_t)HK, (cuuint32_t)(HM / 32)};
+    cuuint32_t es[3] = {1, 1, 1};
+    return h_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
+                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+HPlan hs_plan(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool pair) {
+    HPlan pl = h_plan(M, N, K, ws_cap_elems, pair);
+    pl.a_bytes = HM * HK * 4;
+    pl.stage_bytes = pl.a_bytes + 2 * pl.b_bytes;
+    const size_t budget = 227 * 1024;
+    const int st = (int)((budget - 1024 - 512) / pl.stage_bytes);
+    pl.stages = std::max(2, std::min(kHMaxStages, st));
+    pl.smem = 1024 + (size_t)pl.stages * pl.stage_bytes + (2 * pl.stages + 2 * kSSlots + 4) * 8 + 16;
+    return pl;
+}
 }  // namespace
 
 int64_t gemm_h3_ws_bytes(int ta, int64_t M, int64_t N, int64_t K) {
@@ -595,6 +1057,7 @@ int gemm_h3(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ah
     p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
     p.stage_bytes = pl.stage_bytes; p.acc_stride = pl.acc_stride;
     p.a_e = a_e; p.b_e = b_e;
+    p.chunk_kb = h_chunk_kb();
     // kind::f16 instruction descriptor: D f32, A/B f16, A major from the layout,
     // B K-major, N >> 3, M >> 4
     p.idesc = (1u << 4) | ((uint32_t)(!p.a_kmajor) << 15) | ((uint32_t)(p.bn >> 3) << 17) |
@@ -645,6 +1108,113 @@ int gemm_h3(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ah
                                                            ldc);
         SKP_LAUNCHED(h3_splitk_reduce);
     }
+    return SKP_OK;
+}
+
+int64_t gemm_h3s_ws_bytes(int64_t M, int64_t N, int64_t K) {
+    if (!h_init()) return 0;
+    const HPlan pl = hs_plan(M, N, K, INT64_MAX, h_pair(M));
+    return pl.splits > 1 ? (int64_t)pl.splits * M * N * 4 : 0;
+}
+
+int gemm_h3s(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
+             const int32_t* a_e, const void* Bhi, const void* Blo, int64_t ldb, const int32_t* b_e,
+             float beta, float* C, int64_t ldc, int32_t* overflow, void* ws, int64_t ws_bytes,
+             cudaStream_t st) {
+    if (!h_init()) {
+        set_error("unsupported: the 3xFP16 tcgen05 GEMM needs an sm_100 device");
+        return SKP_ERR_UNSUPPORTED;
+    }
+    if (M == 0 || N == 0) return SKP_OK;
+    if (K == 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) {
+        set_error("unsupported: gemm_h3s sizes");
+        return SKP_ERR_UNSUPPORTED;
+    }
+    const uintptr_t al = reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Bhi) |
+                         reinterpret_cast<uintptr_t>(Blo);
+    if ((al & 15) || (lda & 31) || (ldb & 7)) {
+        set_error("unsupported: gemm_h3s needs 16-byte aligned operands, lda %% 32 == 0, "
+                  "ldb %% 8 == 0 (lda=%lld ldb=%lld)", (long long)lda, (long long)ldb);
+        return SKP_ERR_UNSUPPORTED;
+    }
+    const bool pair = h_pair(M);
+    const int64_t cap = ws ? ws_bytes / 4 : 0;
+    HPlan pl = hs_plan(M, N, K, cap, pair);
+    if (pl.splits > 1 && (!ws || (int64_t)pl.splits * M * N * 4 > ws_bytes))
+        pl = hs_plan(M, N, K, 0, pair);
+    H3SParams p;
+    p.M = (int)M; p.N = (int)N; p.K = (int)K;
+    p.bn = pl.bn; p.tiles_m = pl.tiles_m; p.tiles_n = pl.tiles_n; p.splits = pl.splits;
+    p.kb_per_split = pl.kb_per_split; p.num_kb = pl.num_kb;
+    p.alpha = alpha; p.beta = beta; p.C = C; p.ldc = ldc;
+    p.ws = pl.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
+    p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
+    p.stage_bytes = pl.stage_bytes; p.acc_stride = pl.acc_stride;
+    p.a_e = a_e; p.b_e = b_e; p.overflow = overflow;
+    p.chunk_kb = h_chunk_kb();
+    if (2 * p.acc_stride + kSSlots * (int)kSSlotCols > (int)kHTmemCols || p.bn > kSMaxBn) {
+        set_error("internal: gemm_h3s tile does not fit TMEM (bn=%d)", p.bn);
+        return SKP_ERR_UNSUPPORTED;
+    }
+    // A from TMEM (K-major there), B K-major
+    p.idesc = (1u << 4) | ((uint32_t)(p.bn >> 3) << 17) |
+              ((uint32_t)((pair ? 2 * HM : HM) >> 4) << 24);
+    CUtensorMap ma, mbh, mbl;
+    const int bcols = pair ? p.bn / 2 : p.bn;
+    const bool ok = hs_encode_a(&ma, A, (uint64_t)M, (uint64_t)K, lda) &&
+                    h_encode_k(&mbh, Bhi, (uint64_t)K, (uint64_t)N, ldb, (uint32_t)bcols) &&
+                    h_encode_k(&mbl, Blo, (uint64_t)K, (uint64_t)N, ldb, (uint32_t)bcols);
+    if (!ok) {
+        set_error("cuTensorMapEncodeTiled failed (gemm_h3s)");
+        return SKP_ERR_UNSUPPORTED;
+    }
+    const int units = p.tiles_m * p.tiles_n * p.splits;
+    if (pair) {
+        SKP_CUDA(cudaFuncSetAttribute(gemm_h3s_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(2 * std::min(units, h_sms / 2)));
+        cfg.blockDim = dim3(kSThreads);
+        cfg.dynamicSmemBytes = pl.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SKP_CUDA(cudaLaunchKernelEx(&cfg, gemm_h3s_kernel<true>, ma, mbh, mbl, p));
+        SKP_LAUNCHED(gemm_h3s_kernel_pair);
+    } else {
+        SKP_CUDA(cudaFuncSetAttribute(gemm_h3s_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        gemm_h3s_kernel<false><<<std::min(units, h_sms), kSThreads, pl.smem, st>>>(ma, mbh, mbl, p);
+        SKP_LAUNCHED(gemm_h3s_kernel);
+    }
+    if (p.splits > 1) {
+        const int64_t blocks = std::min<int64_t>(cdiv(M * N, 256), (int64_t)h_sms * 8);
+        h3_splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(p.ws, p.splits, M, N, alpha, beta, C,
+                                                           ldc);
+        SKP_LAUNCHED(h3_splitk_reduce);
+    }
+    return SKP_OK;
+}
+
+int h2_exponent(const float* X, int64_t rows, int64_t cols, int64_t ld, int32_t* e_io,
+                int have_amax, int margin, cudaStream_t st) {
+    uint32_t* amax = reinterpret_cast<uint32_t*>(e_io + 1);
+    if (!have_amax) {
+        SKP_CUDA(cudaMemsetAsync(amax, 0, 4, st));
+        if (rows > 0 && cols > 0) {
+            const int64_t work = rows * cdiv(cols, 4);
+            const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(work, 256), (int64_t)h_sms * 16);
+            absmax_kernel<<<blocks, 256, 0, st>>>(X, rows, cols, ld, amax);
+            SKP_LAUNCHED(absmax_kernel);
+        }
+    }
+    h2_exponent_kernel<<<1, 32, 0, st>>>(e_io, margin);
+    SKP_LAUNCHED(h2_exponent_kernel);
     return SKP_OK;
 }
 
@@ -709,4 +1279,32 @@ extern "C" int skp_split_h2_f32(const float* X, int64_t rows, int64_t cols, int6
     SKP_ARG(e && (rows == 0 || cols == 0 || (X && hi && lo)), "split_h2: null pointer");
     h_init();
     return split_h2(X, rows, cols, ld, trans, hi, lo, ldh, e, have_amax != 0, SKP_STREAM(stream));
+}
+
+extern "C" int64_t skp_gemm_h3s_ws_bytes(int64_t M, int64_t N, int64_t K) {
+    return gemm_h3s_ws_bytes(M, N, K);
+}
+
+extern "C" int skp_gemm_h3s(int64_t M, int64_t N, int64_t K, float alpha, const float* A,
+                            int64_t lda, const int32_t* a_exp, const void* B_hi, const void* B_lo,
+                            int64_t ldb, const int32_t* b_exp, float beta, float* C, int64_t ldc,
+                            int32_t* overflow, void* ws, int64_t ws_bytes, void* stream) {
+    SKP_ARG(M >= 0 && N >= 0 && K >= 0, "gemm_h3s: negative size");
+    SKP_ARG(lda >= M && lda >= 1, "gemm_h3s: lda too small");
+    SKP_ARG(ldb >= K && ldb >= 1, "gemm_h3s: ldb too small");
+    SKP_ARG(ldc >= N && ldc >= 1, "gemm_h3s: ldc too small");
+    SKP_ARG((M == 0 || N == 0 || K == 0 || (A && B_hi && B_lo && a_exp && b_exp)) &&
+                (M == 0 || N == 0 || C),
+            "gemm_h3s: null pointer");
+    return gemm_h3s(M, N, K, alpha, A, lda, a_exp, B_hi, B_lo, ldb, b_exp, beta, C, ldc, overflow,
+                    ws, ws_bytes, SKP_STREAM(stream));
+}
+
+extern "C" int skp_h2_exponent_f32(const float* X, int64_t rows, int64_t cols, int64_t ld,
+                                   int32_t* e_io, int32_t have_amax, int32_t margin_bits,
+                                   void* stream) {
+    SKP_ARG(rows >= 0 && cols >= 0 && ld >= cols && e_io, "h2_exponent: bad arguments");
+    SKP_ARG(margin_bits >= 0 && margin_bits <= 60, "h2_exponent: margin_bits out of range");
+    h_init();
+    return h2_exponent(X, rows, cols, ld, e_io, have_amax != 0, margin_bits, SKP_STREAM(stream));
 }

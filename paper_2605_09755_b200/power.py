@@ -136,7 +136,7 @@ def power_iterate(atil, omega, q: int, stabilized: bool = True):
 def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL,
                       rows_total: int | None = None, phases: _Phases | None = None,
                       fro2: torch.Tensor | None = None, name: str = "a",
-                      streamed: "_convert.Streamed | None" = None):
+                      streamed: "_convert.Streamed | None" = None, hint_out: dict | None = None):
     """Alg. 1 on a device row slab; returns Q (rows x <= r2).  Raises on
     non-finite entries of a (counted inside the sketch kernel).  streamed: a
     still arrives from the host block by block -- each block is sketched as
@@ -230,6 +230,10 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     if plan_failed or omega_failed or be.lazy_failed():
         y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total)
         qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total)
+    if hint_out is not None and e_io is not None and not plan_failed:
+        # for randsvd's in-kernel fp16 split of a: max|a| <~ sqrt(s) max|a S|
+        # (a lone large entry lands in s outputs scaled 1/sqrt(s)); 2x slack
+        hint_out["amax"] = (e_io, int(math.ceil(math.log2(2.0 * math.sqrt(spec.s or 1)))) + 1)
     return qb
 
 
@@ -254,9 +258,10 @@ def range_finder_classical(a, k: int, r2: int, q: int, seed: int, stabilized: bo
     return _convert.download(_range_finder_dev(op.t, spec), op.kind)
 
 
-def _randsvd_dev(a: torch.Tensor, qb: torch.Tensor, comm=_engine.LOCAL, check: bool = True):
+def _randsvd_dev(a: torch.Tensor, qb: torch.Tensor, comm=_engine.LOCAL, check: bool = True,
+                 amax_hint=None):
     be = _be(a.dtype, a.device)
-    return _engine.randsvd(be, comm, a, qb, check)
+    return _engine.randsvd(be, comm, a, qb, check, amax_hint)
 
 
 def randsvd(a, q_basis, *, timings: dict | None = None) -> SvdResult:
@@ -287,8 +292,9 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
     spec.validate(m, n)
     ph = _Phases(timings is not None)
     fro2 = torch.zeros(1, dtype=torch.float64, device=op.t.device) if with_error else None
-    qb = _range_finder_dev(op.t, spec, phases=ph, fro2=fro2, streamed=streamed)
-    u, s, v = _randsvd_dev(op.t, qb, check=False)
+    hint = {}
+    qb = _range_finder_dev(op.t, spec, phases=ph, fro2=fro2, streamed=streamed, hint_out=hint)
+    u, s, v = _randsvd_dev(op.t, qb, check=False, amax_hint=hint.get("amax"))
     ph.mark("randsvd")
     res = SvdResult(_convert.download(u, op.kind), _convert.download(s, op.kind),
                     _convert.download(v, op.kind))

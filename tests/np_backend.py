@@ -17,11 +17,17 @@ class NumpyBackend:
     def prepare(self, x):
         return x
 
+    def mm_at_big(self, a, q, amax_hint=None):
+        return self.mm(a, q, ta=True)
+
+    def overflowed(self, comm=None):
+        return False
+
     def mm(self, a, b, ta=False, tb=False, out=None, alpha=1.0, beta=0.0):
         r = (a.T if ta else a) @ (b.T if tb else b)
         return np.ascontiguousarray(r.astype(self.dtype, copy=False))
 
-    def gram64(self, y):
+    def gram64(self, y, accurate=False):
         return np.ascontiguousarray((y.T @ y).astype(np.float64))
 
     def gram64_rows(self, b):

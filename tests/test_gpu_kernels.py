@@ -324,6 +324,74 @@ def test_gemm_h3_vs_torch(ops, ta, M, N, K):
     assert (out.double() - expect).abs().max().item() <= 2e-6 * scale + 1e-6
 
 
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (67, 45, 131), (300, 520, 4000), (16384, 520, 20000),
+                                   (257, 176, 1000)])
+def test_gemm_h3s_vs_torch(ops, M, N, K):
+    """In-kernel split of an fp32 A^T operand (randsvd's B^T = A^T Q)."""
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * N + K)
+    a = ops.empty2d(K, M, torch.float32, "cuda")
+    a.copy_(torch.randn(K, M, generator=g, device="cuda") * 7.0)
+    b = torch.randn(K, N, generator=g, device="cuda") * 1e-2
+    e_a = ops.h2_exponent(a)
+    assert 2.0 ** 14 <= a.abs().max().item() * 2.0 ** int(e_a[0].item()) < 2.0 ** 15
+    ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c0 = torch.randn(M, N, generator=g, device="cuda")
+    out = c0.clone()
+    ops.gemm_h3s_t(a, e_a, ops.split_h2(b, trans=True), alpha=0.5, beta=2.0, out=out, overflow=ovf)
+    assert int(ovf.item()) == 0
+    expect = 0.5 * (a.double().T @ b.double()) + 2.0 * c0.double()
+    scale = (a.double().abs().max() * b.double().abs().max() * np.sqrt(K)).item()
+    assert (out.double() - expect).abs().max().item() <= 2e-6 * scale + 1e-6
+
+
+def test_gemm_h3s_overflow_flag_and_fallback(ops):
+    g = torch.Generator(device="cuda").manual_seed(1)
+    a = ops.empty2d(4096, 2048, torch.float32, "cuda")
+    a.copy_(torch.randn(4096, 2048, generator=g, device="cuda"))
+    q = torch.randn(4096, 64, generator=g, device="cuda")
+    be = ops.CudaBackend("cuda", torch.float32)
+    # a hint far below the true max: the kernel flags it ...
+    e_io = torch.zeros(2, dtype=torch.int32, device="cuda")
+    e_io[1] = torch.tensor([1e-6], dtype=torch.float32).view(torch.int32).item()
+    be.mm_at_big(a, q, (e_io, 0))
+    assert be.overflowed()
+    # ... and the engine recomputes with 3xTF32
+    from paper_2605_09755_b200 import _engine
+    u, s, v = _engine.randsvd(be, _engine.LOCAL, a, torch.linalg.qr(q)[0].contiguous(), False,
+                              (e_io, 0))
+    ref = torch.linalg.svdvals((torch.linalg.qr(q.double())[0].T @ a.double()))
+    assert (s.cpu() - ref.cpu()).abs().max().item() <= 1e-5 * ref.max().item()
+
+
+def test_h3_long_k_accumulation_is_unbiased(ops):
+    """The tensor core's fp32 accumulation truncates: one 262144-deep chain of
+    positive products comes out ~3e-5 low (3xTF32 in one chain: ~8e-5).  The
+    3xFP16 kernels sum 1024-deep chunks in registers (round to nearest)."""
+    K, M, N = 262144, 256, 64
+    g = torch.Generator(device="cuda").manual_seed(0)
+    a = ops.empty2d(K, M, torch.float32, "cuda")
+    a.copy_(torch.rand(K, M, generator=g, device="cuda") + 0.5)
+    q = torch.rand(K, N, generator=g, device="cuda") + 0.5
+    ref = a.double().T @ q.double()
+    sq = ops.split_h2(q, trans=True)
+    for out in (ops.gemm_h3s_t(a, ops.h2_exponent(a), sq), ops.gemm_h3(ops.split_h2(a), sq, ta=True)):
+        rel = (out.double() - ref) / ref
+        assert abs(rel.mean().item()) < 1e-5 and rel.abs().max().item() < 2e-5
+
+
+def test_accurate_gram_orthonormal_basis(ops):
+    """The Gram of the last CholeskyQR pass (accurate=True) is unbiased at
+    K = 262144, so the final basis is orthonormal to ~1e-5."""
+    g = torch.Generator(device="cuda").manual_seed(2)
+    y = ops.empty2d(262144, 96, torch.float32, "cuda")
+    y.copy_(torch.randn(262144, 96, generator=g, device="cuda") + 0.3)
+    be = ops.CudaBackend("cuda", torch.float32)
+    ref = y.double().T @ y.double()
+    g64 = be.gram64(y, accurate=True)
+    rel = (torch.diagonal(g64) - torch.diagonal(ref)) / torch.diagonal(ref)
+    assert rel.abs().max().item() < 1e-5
+
+
 def test_gemm_h3_pair_forced_small(ops, monkeypatch):
     monkeypatch.setenv("SKP_H3_FORCE2CTA", "1")
     g = torch.Generator(device="cuda").manual_seed(3)
