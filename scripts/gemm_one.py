@@ -1,4 +1,5 @@
-"""One C3-shape GEMM (for ncu): python scripts/gemm_one.py nn|tn [3xtf32|h3] [reps]"""
+"""One C3-shape GEMM (for ncu): python scripts/gemm_one.py nn|tn|qta [3xtf32|h3|h3s] [reps]
+(qta: randsvd's B^T = A^T Q with A 262144 x 16384)"""
 import sys
 import torch
 sys.path.insert(0, ".")
@@ -10,7 +11,18 @@ m, l, r2 = 262144, 4000, 520
 torch.manual_seed(0)
 at = _ops.empty2d(m, l, torch.float32, "cuda")
 at.normal_()
-if kind == "nn":
+if kind == "qta":
+    del at
+    a = _ops.empty2d(m, 16384, torch.float32, "cuda")
+    a.normal_()
+    q = _ops.empty2d(m, r2, torch.float32, "cuda")
+    q.normal_()
+    if mode == "h3s":
+        e_a, sq = _ops.h2_exponent(a), _ops.split_h2(q, trans=True)
+        f = lambda: _ops.gemm_h3s_t(a, e_a, sq)
+    else:
+        f = lambda: _ops.gemm(a, q, True, False, mode=mode)
+elif kind == "nn":
     z = _ops.empty2d(l, r2, torch.float32, "cuda")
     z.normal_()
     if mode == "h3":
