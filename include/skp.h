@@ -239,6 +239,20 @@ int skp_gemm_h3(int transA, int64_t M, int64_t N, int64_t K, float alpha, const 
                 const void* B_lo, int64_t ldb, const int32_t* b_exp, float beta, float* C,
                 int64_t ldc, void* ws, int64_t ws_bytes, void* stream);
 
+/* skp_gemm_h3_emit_t: the product of skp_gemm_h3 (beta = 0), written not as
+ * fp32 C but as the fp16 split of C^T: Ct_hi, Ct_lo (N x M planes, ldct),
+ * C^T 2^e ~= hi + lo with e = e_fixed (fixed = 1; a caller-known bound, e.g.
+ * 14 for an orthonormal basis) or ea + eb - shift (fixed = 0; shift = 15 +
+ * ceil(log2 K) bounds every entry), stored to *e_out.  An entry that does
+ * not fit fp16 (or NaN) sets *overflow (may be NULL).  The epilogue's rows
+ * are consecutive in C^T, so the transposed planes are written coalesced:
+ * products feed the next product without an fp32 round trip or split pass. */
+int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, float alpha, const void* A_hi,
+                       const void* A_lo, int64_t lda, const int32_t* a_exp, const void* B_hi,
+                       const void* B_lo, int64_t ldb, const int32_t* b_exp, void* Ct_hi,
+                       void* Ct_lo, int64_t ldct, int32_t shift, int32_t fixed, int32_t e_fixed,
+                       int32_t* e_out, int32_t* overflow, void* stream);
+
 /* skp_gemm_h3s: C = alpha A^T B + beta C with A (K x M, fp32, lda % 32 == 0)
  * split into fp16 hi/lo INSIDE the kernel with the caller's exponent 2^a_exp
  * (a bound on max|A|: skp_h2_exponent_f32), B pre-split as for skp_gemm_h3.

@@ -58,6 +58,13 @@ def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: b
     ~eps * cond(Y)^2; used for the stabilisations inside the power iteration,
     whose only job is to keep the block well conditioned (the final Q always
     gets two passes)."""
+    if hasattr(be, "orth_planes") and not isinstance(y, np.ndarray) and hasattr(y, "hi"):
+        # y given as the fp16 planes of its transpose (the lazy planes path)
+        rows_total = y.cols if rows_total is None else rows_total
+        rel = pivot_tol(be, rows_total, y.rows, tol)
+        if lazy and passes == 2:
+            return be.orth_planes(comm, y, rel)
+        y = be.planes_to_compute(y)
     c = y.shape[1]
     rows_total = y.shape[0] if rows_total is None else rows_total
     rel = pivot_tol(be, rows_total, c, tol)
@@ -96,6 +103,10 @@ def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_t
     1 + 2q products, so it is prepared once (be.prepare: the fp16 split of
     the 3xFP16 GEMM on the CUDA backend)."""
     atil = be.prepare(atil)
+    if lazy and stabilized and q > 0 and hasattr(be, "planes_ok") and be.planes_ok(atil, omega):
+        def rel_of(yt):
+            return pivot_tol(be, yt.cols if rows_total is None else rows_total, yt.rows)
+        return be.power_lazy_planes(comm, atil, omega, q, rel_of)
     y = be.mm(atil, omega)
     for _ in range(q):
         if stabilized:

@@ -314,6 +314,30 @@ def gemm_h3(a: SplitH2, b: SplitH2, ta: bool = False, alpha: float = 1.0, beta: 
     return out
 
 
+def gemm_h3_emit_t(a: SplitH2, b: SplitH2, ta: bool = False, shift: int | None = None,
+                   e_fixed: int | None = None, out: SplitH2 | None = None, overflow=None,
+                   alpha: float = 1.0) -> SplitH2:
+    """K4h product written as the fp16 split of C^T (N x M planes): C =
+    alpha op(a) b^T.  Exponent e_fixed, or ea + eb - shift (default shift =
+    15 + ceil(log2 K): no entry can overflow)."""
+    M, K = (a.cols, a.rows) if ta else (a.rows, a.cols)
+    N, Kb = b.rows, b.cols
+    if K != Kb:
+        raise ValueError(f"dimension mismatch: {M}x{K} @ {Kb}x{N}")
+    if shift is None:
+        shift = 15 + max(0, (K - 1).bit_length())
+    ld = max(64, (M + 63) // 64 * 64)
+    if out is None or out.rows != N or out.cols != M:
+        buf = torch.empty((2, N, ld), dtype=torch.float16, device=a.hi.device)
+        out = SplitH2(buf[0], buf[1], torch.zeros(2, dtype=torch.int32, device=a.hi.device),
+                      N, M, ld)
+    call("skp_gemm_h3_emit_t", int(ta), M, N, K, alpha, ptr(a.hi), ptr(a.lo), a.ld, ptr(a.e),
+         ptr(b.hi), ptr(b.lo), b.ld, ptr(b.e), ptr(out.hi), ptr(out.lo), out.ld, int(shift),
+         int(e_fixed is not None), int(e_fixed or 0), ptr(out.e), ptr(overflow),
+         stream_ptr(a.hi.device))
+    return out
+
+
 def h2_exponent(x: torch.Tensor, e_io: torch.Tensor | None = None, have_amax: bool = False,
                 margin_bits: int = 0) -> torch.Tensor:
     """int32[2] e_io with e_io[0] = 15 - ceil(log2 max|x|) - margin_bits (max|x|
@@ -513,8 +537,55 @@ class CudaBackend:
     def lazy_reset(self):
         self.fail.zero_()
 
-    def lazy_failed(self) -> bool:
-        return int(self.fail[0].item()) != 0
+    def lazy_failed(self, comm=None) -> bool:
+        """Any lazy failure (Cholesky pivot: fail[0], identical on every rank;
+        an emitted fp16 split out of range: fail[1], per rank) -- all ranks
+        agree (host sync)."""
+        f = self.fail.clone()
+        if comm is not None:
+            comm.allreduce_(f)
+        return bool((f != 0).any().item())
+
+    # ---- lazy power iteration on fp16 planes (3xFP16 end to end) --------------
+    def planes_ok(self, atil, omega) -> bool:
+        return isinstance(atil, SplitH2) and isinstance(omega, torch.Tensor) \
+            and omega.dtype == F32 and omega.dim() == 2 and not os.environ.get("SKP_NO_PLANES")
+
+    def gram64_planes(self, yt: SplitH2):
+        """Y^T Y (fp64) from the split planes of Y^T: 3xFP16, promoted accumulation."""
+        return cast(gemm_h3(yt, yt), F64)
+
+    def power_lazy_planes(self, comm, atil: SplitH2, omega, q: int, rel_of):
+        """Stabilized power iteration (power.py:113-134) with every product on
+        K4h and every intermediate block kept as fp16 planes of its
+        TRANSPOSE, written by the producing product's epilogue:
+            Y^T = (A~ Omega)^T,  q x { G = Y^T Y;  X = chol_inv(G);
+                                       Q^T = (Y X^T)^T (|Q| <= 1: fixed exponent 14);
+                                       Z = A~^T Q;  Y^T = (A~ Z)^T }.
+        Lazy: a Cholesky failure or a Q entry out of fp16 range only sets
+        self.fail (the caller then reruns eagerly in fp32).  Returns Y^T planes."""
+        yt = gemm_h3_emit_t(atil, split_h2(omega, trans=True))
+        qt = None
+        for _ in range(q):
+            x = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), rel_of(yt), lazy=True)
+            qt = gemm_h3_emit_t(yt, split_h2(self.to_compute(x)), ta=True, e_fixed=14, out=qt,
+                                overflow=self.fail[1:])
+            z = comm.allreduce_(gemm_h3(atil, qt, ta=True))
+            yt = gemm_h3_emit_t(atil, split_h2(z, trans=True), out=yt)
+        return yt
+
+    def orth_planes(self, comm, yt: SplitH2, rel: float):
+        """Lazy CholeskyQR2 of Y given as Y^T planes; returns Q (fp32, rows x c)."""
+        x1 = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), rel, lazy=True)
+        q1t = gemm_h3_emit_t(yt, split_h2(self.to_compute(x1)), ta=True, e_fixed=14,
+                             overflow=self.fail[1:])
+        x2 = self.chol_inv64(comm.allreduce_(self.gram64_planes(q1t)), 0.0, lazy=True)
+        return gemm_h3(q1t, split_h2(self.to_compute(x2)), ta=True)
+
+    def planes_to_compute(self, yt: SplitH2):
+        """fp32 Y from Y^T planes (the eager fallback): Y = (Y^T)^T I."""
+        eye = torch.eye(yt.rows, dtype=F32, device=self.device)
+        return gemm_h3(yt, split_h2(eye), ta=True)
 
     def eig_desc64(self, g, max_sweeps=30):
         n = g.shape[0]

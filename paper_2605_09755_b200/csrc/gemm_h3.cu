@@ -74,6 +74,16 @@ struct H3Params {
     const int* a_e;
     const int* b_e;
     int chunk_kb;  // K blocks per accumulation chunk (promotion period)
+    // emit mode (emit_hi != null): instead of C, write the fp16 split of
+    // C^T (N x M planes, ld emit_ld) with exponent e_out = emit_fixed ?
+    // emit_e_fixed : ea + eb - emit_shift, stored to *emit_e; an entry that
+    // does not fit fp16 sets *overflow
+    __half* emit_hi;
+    __half* emit_lo;
+    long long emit_ld;
+    int emit_shift, emit_fixed, emit_e_fixed;
+    int* emit_e;
+    int* overflow;
 };
 
 // TMA 2-D / 3-D loads signalling a barrier given by its shared::cluster
@@ -331,8 +341,16 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
         const int g0 = part * per;                               // first 16-column group
         const int g1 = min(ng, g0 + per);                        // past the last
         // 2^-(ea+eb), applied as two exact power-of-two factors
-        const float sc = ldexpf(1.f, -__ldg(p.a_e)) * ldexpf(1.f, -__ldg(p.b_e));
+        const int ea = __ldg(p.a_e), eb = __ldg(p.b_e);
+        const float sc = ldexpf(1.f, -ea) * ldexpf(1.f, -eb);
         const float alpha = p.alpha * sc;
+        float emit_scale = 0.f;
+        bool emit_bad = false;
+        if (p.emit_hi) {
+            const int e_out = p.emit_fixed ? p.emit_e_fixed : ea + eb - p.emit_shift;
+            emit_scale = p.alpha * ldexpf(ldexpf(1.f, e_out - ea), -eb);
+            if (blockIdx.x == 0 && warp == kHWarpEpi && lane == 0) *p.emit_e = e_out;
+        }
         int cc = 0;
         for (int u = ustart; u < units; u += ustride) {
             const HWork w = h_unit(p, u);
@@ -363,6 +381,27 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
             }
             const int row = w.tm * kRowsPerUnit + (int)rank * HM + q * 32 + lane;
             if (row >= p.M) continue;
+            if (p.emit_hi) {
+                // C^T split: for each column, the warp's 32 rows are 64
+                // contiguous bytes of each plane
+#pragma unroll
+                for (int i = 0; i < kHEpiCols; ++i) {
+                    const int col0 = w.tn * p.bn + 16 * (g0 + i);
+                    if (g0 + i >= g1 || col0 >= p.N) continue;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        if (col0 + e < p.N) {
+                            const float v = emit_scale * acc[i][e];
+                            emit_bad |= !(fabsf(v) < 65504.f);  // (NaN included)
+                            const __half h = __float2half_rn(v);
+                            const size_t o = (size_t)(col0 + e) * p.emit_ld + row;
+                            p.emit_hi[o] = h;
+                            p.emit_lo[o] = __float2half_rn(v - __half2float(h));
+                        }
+                    }
+                }
+                continue;
+            }
 #pragma unroll
             for (int i = 0; i < kHEpiCols; ++i) {
                 const int col0 = w.tn * p.bn + 16 * (g0 + i);
@@ -398,6 +437,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
                 }
             }
         }
+        if (p.emit_hi && p.overflow && emit_bad) atomicOr(p.overflow, 1);
     }
     tc_fence_before();
     if (kPair) cluster_sync_all();
@@ -1022,10 +1062,19 @@ int64_t gemm_h3_ws_bytes(int ta, int64_t M, int64_t N, int64_t K) {
     return pl.splits > 1 ? (int64_t)pl.splits * M * N * 4 : 0;
 }
 
-int gemm_h3(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo,
-            int64_t lda, const int32_t* a_e, const void* Bhi, const void* Blo, int64_t ldb,
-            const int32_t* b_e, float beta, float* C, int64_t ldc, void* ws, int64_t ws_bytes,
-            cudaStream_t st) {
+struct H3Emit {
+    void* hi;
+    void* lo;
+    int64_t ld;
+    int shift, fixed, e_fixed;
+    int32_t* e_out;
+    int32_t* overflow;
+};
+
+int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ahi,
+                 const void* Alo, int64_t lda, const int32_t* a_e, const void* Bhi, const void* Blo,
+                 int64_t ldb, const int32_t* b_e, float beta, float* C, int64_t ldc, void* ws,
+                 int64_t ws_bytes, const H3Emit* emit, cudaStream_t st) {
     if (!h_init()) {
         set_error("unsupported: the 3xFP16 tcgen05 GEMM needs an sm_100 device");
         return SKP_ERR_UNSUPPORTED;
@@ -1043,9 +1092,9 @@ int gemm_h3(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ah
         return SKP_ERR_UNSUPPORTED;
     }
     const bool pair = h_pair(M);
-    const int64_t cap = ws ? ws_bytes / 4 : 0;
+    const int64_t cap = (ws && !emit) ? ws_bytes / 4 : 0;  // emit: no split-K partials
     HPlan pl = h_plan(M, N, K, cap, pair);
-    if (pl.splits > 1 && (!ws || (int64_t)pl.splits * M * N * 4 > ws_bytes))
+    if (pl.splits > 1 && (!ws || emit || (int64_t)pl.splits * M * N * 4 > ws_bytes))
         pl = h_plan(M, N, K, 0, pair);
     H3Params p;
     p.M = (int)M; p.N = (int)N; p.K = (int)K;
@@ -1058,6 +1107,14 @@ int gemm_h3(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ah
     p.stage_bytes = pl.stage_bytes; p.acc_stride = pl.acc_stride;
     p.a_e = a_e; p.b_e = b_e;
     p.chunk_kb = h_chunk_kb();
+    p.emit_hi = emit ? reinterpret_cast<__half*>(emit->hi) : nullptr;
+    p.emit_lo = emit ? reinterpret_cast<__half*>(emit->lo) : nullptr;
+    p.emit_ld = emit ? emit->ld : 0;
+    p.emit_shift = emit ? emit->shift : 0;
+    p.emit_fixed = emit ? emit->fixed : 0;
+    p.emit_e_fixed = emit ? emit->e_fixed : 0;
+    p.emit_e = emit ? emit->e_out : nullptr;
+    p.overflow = emit ? emit->overflow : nullptr;
     // kind::f16 instruction descriptor: D f32, A/B f16, A major from the layout,
     // B K-major, N >> 3, M >> 4
     p.idesc = (1u << 4) | ((uint32_t)(!p.a_kmajor) << 15) | ((uint32_t)(p.bn >> 3) << 17) |
@@ -1109,6 +1166,14 @@ int gemm_h3(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ah
         SKP_LAUNCHED(h3_splitk_reduce);
     }
     return SKP_OK;
+}
+
+int gemm_h3(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo,
+            int64_t lda, const int32_t* a_e, const void* Bhi, const void* Blo, int64_t ldb,
+            const int32_t* b_e, float beta, float* C, int64_t ldc, void* ws, int64_t ws_bytes,
+            cudaStream_t st) {
+    return gemm_h3_impl(ta, M, N, K, alpha, Ahi, Alo, lda, a_e, Bhi, Blo, ldb, b_e, beta, C, ldc,
+                        ws, ws_bytes, nullptr, st);
 }
 
 int64_t gemm_h3s_ws_bytes(int64_t M, int64_t N, int64_t K) {
@@ -1307,4 +1372,22 @@ extern "C" int skp_h2_exponent_f32(const float* X, int64_t rows, int64_t cols, i
     SKP_ARG(margin_bits >= 0 && margin_bits <= 60, "h2_exponent: margin_bits out of range");
     h_init();
     return h2_exponent(X, rows, cols, ld, e_io, have_amax != 0, margin_bits, SKP_STREAM(stream));
+}
+
+extern "C" int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, float alpha,
+                                  const void* A_hi, const void* A_lo, int64_t lda,
+                                  const int32_t* a_exp, const void* B_hi, const void* B_lo,
+                                  int64_t ldb, const int32_t* b_exp, void* Ct_hi, void* Ct_lo,
+                                  int64_t ldct, int32_t shift, int32_t fixed, int32_t e_fixed,
+                                  int32_t* e_out, int32_t* overflow, void* stream) {
+    SKP_ARG(M >= 0 && N >= 0 && K >= 0, "gemm_h3_emit_t: negative size");
+    SKP_ARG(transA == 0 || transA == 1, "gemm_h3_emit_t: transA must be 0/1");
+    SKP_ARG(lda >= (transA ? M : K) && lda >= 1, "gemm_h3_emit_t: lda too small");
+    SKP_ARG(ldb >= K && ldb >= 1, "gemm_h3_emit_t: ldb too small");
+    SKP_ARG(ldct >= M, "gemm_h3_emit_t: ldct too small");
+    SKP_ARG(Ct_hi && Ct_lo && e_out && A_hi && A_lo && B_hi && B_lo && a_exp && b_exp,
+            "gemm_h3_emit_t: null pointer");
+    H3Emit em{Ct_hi, Ct_lo, ldct, shift, fixed, e_fixed, e_out, overflow};
+    return gemm_h3_impl(transA, M, N, K, alpha, A_hi, A_lo, lda, a_exp, B_hi, B_lo, ldb, b_exp,
+                        0.f, nullptr, 0, nullptr, 0, &em, SKP_STREAM(stream));
 }

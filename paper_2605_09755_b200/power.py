@@ -227,7 +227,7 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     if plan_failed or omega_failed:
         # (a device Omega that could not complete is redrawn by numpy itself)
         omega = omega_for(perm, host=omega_failed)
-    if plan_failed or omega_failed or be.lazy_failed():
+    if plan_failed or omega_failed or be.lazy_failed(comm):
         y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total)
         qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total)
     if hint_out is not None and e_io is not None and not plan_failed:

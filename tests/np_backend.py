@@ -95,5 +95,5 @@ class NumpyBackend:
     def lazy_reset(self):
         self._fail = False
 
-    def lazy_failed(self):
+    def lazy_failed(self, comm=None):
         return getattr(self, "_fail", False)

@@ -151,3 +151,29 @@ def test_streamed_upload_matches_device_input(skp, monkeypatch, dtype):
     a[m - 3, n // 2] = np.inf
     with pytest.raises(ValueError, match="non-finite"):
         skp.rsvd(a, spec)
+
+
+def test_planes_power_iteration_matches_fp32_path(skp, monkeypatch):
+    """Large enough for the 3xFP16 planes path (A~ split, products emitting
+    fp16 planes of their transposes): same sigma / error as the fp32 3xTF32
+    path to 1e-5, orthonormal Q."""
+    import torch
+    from paper_2605_09755_b200 import _ops, power
+    g = torch.Generator(device="cuda").manual_seed(4)
+    m, n, k = 65536, 1024, 40
+    u = torch.linalg.qr(torch.randn(m, k, generator=g, device="cuda"))[0]
+    v = torch.linalg.qr(torch.randn(n, k, generator=g, device="cuda"))[0]
+    s = torch.logspace(0, -2, k, device="cuda")
+    a = _ops.empty2d(m, n, torch.float32, "cuda")
+    a.copy_((u * s) @ v.T + 1e-4 * torch.randn(m, n, generator=g, device="cuda"))
+    spec = skp.RangeFinderSpec(k=30, l=200, r1=200, r2=60, q=2, eps=0.5, s=8, seed=21)
+    assert m * spec.r1 >= _ops.H3_MIN_ELEMS
+    res, rel = skp.rsvd(a, spec, with_error=True)
+    q = power._range_finder_dev(a, spec)
+    qq = q.double().T @ q.double()
+    assert (qq - torch.eye(qq.shape[0], device="cuda", dtype=torch.float64)).abs().max().item() < 2e-5
+    monkeypatch.setenv("SKP_NO_H3", "1")
+    res32, rel32 = skp.rsvd(a, spec, with_error=True)
+    s_h, s_32 = res.sigma.double().cpu(), res32.sigma.double().cpu()
+    assert (s_h - s_32).abs().max().item() <= 1e-5 * s_32[0].item()
+    assert abs(rel - rel32) <= 1e-4 * rel32
