@@ -129,11 +129,16 @@ def randsvd(be, comm, a, qb, check: bool = True, amax_hint=None):
         dev = be.orth_dev(g)
         if not dev <= ORTHO_TOL[_dtype_key(be)]:
             raise ValueError(f"Q is not orthonormal (deviation {dev:.3e})")
-    bt = be.mm_at_big(a, qb, amax_hint)                      # n x c, this rank's part
+    out = _randsvd_core(be, comm, be.mm_at_big(a, qb, amax_hint), qb)   # B^T: this rank's part
     if be.overflowed(comm):
-        # the in-kernel fp16 split met an entry beyond its exponent bound
-        # (a hint that did not hold): recompute with 3xTF32 on every rank
-        bt = be.mm(a, qb, ta=True)
+        # the in-kernel fp16 split met an entry beyond its exponent bound (a
+        # hint that did not hold): recompute with 3xTF32 on every rank.  The
+        # flag is read once, after everything is queued (no mid-call sync).
+        out = _randsvd_core(be, comm, be.mm(a, qb, ta=True), qb)
+    return out
+
+
+def _randsvd_core(be, comm, bt, qb):
     bt = comm.allreduce_(bt)
     n, c = bt.shape
     gb = be.gram64_rows_t(bt)                               # c x c, fp64
