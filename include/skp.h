@@ -228,7 +228,9 @@ int skp_cast2d_f64_f32(const double* x, int64_t ldx, float* y, int64_t ldy, int6
  * the fp32-accumulated A_lo B_hi + A_hi B_lo + A_hi B_hi, with op(A) = A
  * (M x K, transA=0) or A^T (A stored K x M, transA=1, lda % 64 == 0) and B
  * stored N x K.  Planes 16-byte aligned, ld % 8 == 0.  Accuracy ~2^-22 per
- * product (3xTF32: 2^-20).
+ * product (3xTF32: 2^-20).  B_lo = NULL: two products (A_lo B_hi + A_hi B_hi),
+ * i.e. B rounded to fp16 (2^-12), A kept to 22 bits -- for the power
+ * iteration, whose products only need to preserve the span.
  * ws: skp_gemm_h3_ws_bytes (split-K partials; 0 = none needed).            */
 int skp_split_h2_f32(const float* X, int64_t rows, int64_t cols, int64_t ld, int32_t trans,
                      void* hi, void* lo, int64_t ldh, int32_t* e_io, int32_t have_amax,

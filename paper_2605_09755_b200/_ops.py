@@ -294,7 +294,7 @@ def split_h2(x: torch.Tensor, trans: bool = False, out: "SplitH2 | None" = None,
 
 
 def gemm_h3(a: SplitH2, b: SplitH2, ta: bool = False, alpha: float = 1.0, beta: float = 0.0,
-            out=None) -> torch.Tensor:
+            out=None, b_lo: bool = True) -> torch.Tensor:
     """K4h: out = alpha op(a) b^T + beta out from pre-split operands: op(a) =
     a (M x K) or a^T (a stored K x M, ta=True); b stored N x K."""
     M, K = (a.cols, a.rows) if ta else (a.rows, a.cols)
@@ -310,13 +310,14 @@ def gemm_h3(a: SplitH2, b: SplitH2, ta: bool = False, alpha: float = 1.0, beta: 
     wsb = lib.skp_gemm_h3_ws_bytes(int(ta), M, N, K)
     ws = workspace(a.hi.device, wsb) if wsb else None
     call("skp_gemm_h3", int(ta), M, N, K, alpha, ptr(a.hi), ptr(a.lo), a.ld, ptr(a.e), ptr(b.hi),
-         ptr(b.lo), b.ld, ptr(b.e), beta, ptr(out), ldc, ptr(ws), wsb, stream_ptr(a.hi.device))
+         ptr(b.lo) if b_lo else None, b.ld, ptr(b.e), beta, ptr(out), ldc, ptr(ws), wsb,
+         stream_ptr(a.hi.device))
     return out
 
 
 def gemm_h3_emit_t(a: SplitH2, b: SplitH2, ta: bool = False, shift: int | None = None,
                    e_fixed: int | None = None, out: SplitH2 | None = None, overflow=None,
-                   alpha: float = 1.0) -> SplitH2:
+                   alpha: float = 1.0, b_lo: bool = True) -> SplitH2:
     """K4h product written as the fp16 split of C^T (N x M planes): C =
     alpha op(a) b^T.  Exponent e_fixed, or ea + eb - shift (default shift =
     15 + ceil(log2 K): no entry can overflow)."""
@@ -332,7 +333,8 @@ def gemm_h3_emit_t(a: SplitH2, b: SplitH2, ta: bool = False, shift: int | None =
         out = SplitH2(buf[0], buf[1], torch.zeros(2, dtype=torch.int32, device=a.hi.device),
                       N, M, ld)
     call("skp_gemm_h3_emit_t", int(ta), M, N, K, alpha, ptr(a.hi), ptr(a.lo), a.ld, ptr(a.e),
-         ptr(b.hi), ptr(b.lo), b.ld, ptr(b.e), ptr(out.hi), ptr(out.lo), out.ld, int(shift),
+         ptr(b.hi), ptr(b.lo) if b_lo else None, b.ld, ptr(b.e), ptr(out.hi), ptr(out.lo), out.ld,
+         int(shift),
          int(e_fixed is not None), int(e_fixed or 0), ptr(out.e), ptr(overflow),
          stream_ptr(a.hi.device))
     return out
@@ -564,14 +566,18 @@ class CudaBackend:
                                        Z = A~^T Q;  Y^T = (A~ Z)^T }.
         Lazy: a Cholesky failure or a Q entry out of fp16 range only sets
         self.fail (the caller then reruns eagerly in fp32).  Returns Y^T planes."""
-        yt = gemm_h3_emit_t(atil, split_h2(omega, trans=True))
+        # SKP_H3_POWER2=1: the products with A~ round the block to fp16 (2 MMAs
+        # per MAC instead of 3; power phase -15% at C3).  Measured: sigma moves
+        # by up to 2.1e-5 relative at C3 (the 1e-5 parity target), so 3 by default.
+        bl = not os.environ.get("SKP_H3_POWER2")
+        yt = gemm_h3_emit_t(atil, split_h2(omega, trans=True), b_lo=bl)
         qt = None
         for _ in range(q):
             x = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), rel_of(yt), lazy=True)
             qt = gemm_h3_emit_t(yt, split_h2(self.to_compute(x)), ta=True, e_fixed=14, out=qt,
                                 overflow=self.fail[1:])
-            z = comm.allreduce_(gemm_h3(atil, qt, ta=True))
-            yt = gemm_h3_emit_t(atil, split_h2(z, trans=True), out=yt)
+            z = comm.allreduce_(gemm_h3(atil, qt, ta=True, b_lo=bl))
+            yt = gemm_h3_emit_t(atil, split_h2(z, trans=True), out=yt, b_lo=bl)
         return yt
 
     def orth_planes(self, comm, yt: SplitH2, rel: float):

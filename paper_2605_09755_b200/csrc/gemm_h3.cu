@@ -74,6 +74,7 @@ struct H3Params {
     const int* a_e;
     const int* b_e;
     int chunk_kb;  // K blocks per accumulation chunk (promotion period)
+    int b_lo;      // 1: 3 products; 0: B's lo plane dropped (2 products, B to 11 bits)
     // emit mode (emit_hi != null): instead of C, write the fp16 split of
     // C^T (N x M planes, ld emit_ld) with exponent e_out = emit_fixed ?
     // emit_e_fixed : ea + eb - emit_shift, stored to *emit_e; an entry that
@@ -282,7 +283,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
                     h_tma_3d<kPair>(&map_al, bar, st + p.a_bytes, 0, k0, m0 / 64);
                 }
                 h_tma_2d<kPair>(&map_bh, bar, st + 2 * p.a_bytes, k0, n0);
-                h_tma_2d<kPair>(&map_bl, bar, st + 2 * p.a_bytes + p.b_bytes, k0, n0);
+                if (p.b_lo) h_tma_2d<kPair>(&map_bl, bar, st + 2 * p.a_bytes + p.b_bytes, k0, n0);
             }
         }
     } else if (warp == kHWarpMma && leader) {
@@ -323,7 +324,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
                         const uint32_t acc = (kb > c0 || j > 0) ? 1u : 0u;
                         const uint64_t ah = as + (uint64_t)j * ajstep, bh = bs + (uint64_t)j * bjstep;
                         h_mma<kPair>(d, ah + alo, bh, p.idesc, acc);  // a_lo b_hi
-                        h_mma<kPair>(d, ah, bh + blo, p.idesc, 1u);   // a_hi b_lo
+                        if (p.b_lo) h_mma<kPair>(d, ah, bh + blo, p.idesc, 1u);  // a_hi b_lo
                         h_mma<kPair>(d, ah, bh, p.idesc, 1u);         // a_hi b_hi
                     }
                     if (kPair) tc_commit_pair_e(&empty[s]);
@@ -991,7 +992,7 @@ bool h_pair(int64_t M) {
     return M > HM;
 }
 
-HPlan h_plan(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool pair) {
+HPlan h_plan(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool pair, bool b_lo = true) {
     HPlan pl;
     const int max_bn = pair ? kHMaxBn : 128;
     pl.tiles_n = (int)cdiv(N, max_bn);
@@ -1018,7 +1019,7 @@ HPlan h_plan(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool pair) {
     pl.a_bytes = HM * HK * 2;
     const int bcols = pair ? pl.bn / 2 : pl.bn;
     pl.b_bytes = (uint32_t)bcols * HK * 2;
-    pl.stage_bytes = 2 * pl.a_bytes + 2 * pl.b_bytes;
+    pl.stage_bytes = 2 * pl.a_bytes + (b_lo ? 2 : 1) * pl.b_bytes;
     pl.acc_stride = (int)cdiv(pl.bn, 32) * 32;
     const size_t budget = 227 * 1024;
     const int st = (int)((budget - 1024 - 256) / pl.stage_bytes);
@@ -1074,7 +1075,7 @@ struct H3Emit {
 int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ahi,
                  const void* Alo, int64_t lda, const int32_t* a_e, const void* Bhi, const void* Blo,
                  int64_t ldb, const int32_t* b_e, float beta, float* C, int64_t ldc, void* ws,
-                 int64_t ws_bytes, const H3Emit* emit, cudaStream_t st) {
+                 int64_t ws_bytes, const H3Emit* emit, cudaStream_t st, bool b_lo = true) {
     if (!h_init()) {
         set_error("unsupported: the 3xFP16 tcgen05 GEMM needs an sm_100 device");
         return SKP_ERR_UNSUPPORTED;
@@ -1084,6 +1085,7 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
         set_error("unsupported: gemm_h3 sizes");
         return SKP_ERR_UNSUPPORTED;
     }
+    b_lo = b_lo && Blo != nullptr;  // no lo plane: 2 products, B rounded to fp16
     const uintptr_t al = reinterpret_cast<uintptr_t>(Ahi) | reinterpret_cast<uintptr_t>(Alo) |
                          reinterpret_cast<uintptr_t>(Bhi) | reinterpret_cast<uintptr_t>(Blo);
     if ((al & 15) || (lda & 7) || (ldb & 7) || (ta && (lda & 63))) {
@@ -1093,10 +1095,11 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
     }
     const bool pair = h_pair(M);
     const int64_t cap = (ws && !emit) ? ws_bytes / 4 : 0;  // emit: no split-K partials
-    HPlan pl = h_plan(M, N, K, cap, pair);
+    HPlan pl = h_plan(M, N, K, cap, pair, b_lo);
     if (pl.splits > 1 && (!ws || emit || (int64_t)pl.splits * M * N * 4 > ws_bytes))
-        pl = h_plan(M, N, K, 0, pair);
+        pl = h_plan(M, N, K, 0, pair, b_lo);
     H3Params p;
+    p.b_lo = b_lo ? 1 : 0;
     p.M = (int)M; p.N = (int)N; p.K = (int)K;
     p.bn = pl.bn; p.tiles_m = pl.tiles_m; p.tiles_n = pl.tiles_n; p.splits = pl.splits;
     p.kb_per_split = pl.kb_per_split; p.num_kb = pl.num_kb;
@@ -1129,7 +1132,7 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
         ok = h_encode_mn(&mah, Ahi, (uint64_t)M, (uint64_t)K, lda) &&
              h_encode_mn(&mal, Alo, (uint64_t)M, (uint64_t)K, lda);
     ok = ok && h_encode_k(&mbh, Bhi, (uint64_t)K, (uint64_t)N, ldb, (uint32_t)bcols) &&
-         h_encode_k(&mbl, Blo, (uint64_t)K, (uint64_t)N, ldb, (uint32_t)bcols);
+         h_encode_k(&mbl, b_lo ? Blo : Bhi, (uint64_t)K, (uint64_t)N, ldb, (uint32_t)bcols);
     if (!ok) {
         set_error("cuTensorMapEncodeTiled failed (gemm_h3)");
         return SKP_ERR_UNSUPPORTED;
@@ -1328,7 +1331,7 @@ extern "C" int skp_gemm_h3(int transA, int64_t M, int64_t N, int64_t K, float al
     SKP_ARG(lda >= (transA ? M : K) && lda >= 1, "gemm_h3: lda too small");
     SKP_ARG(ldb >= K && ldb >= 1, "gemm_h3: ldb too small");
     SKP_ARG(ldc >= N && ldc >= 1, "gemm_h3: ldc too small");
-    SKP_ARG((M == 0 || N == 0 || K == 0 || (A_hi && A_lo && B_hi && B_lo && a_exp && b_exp)) &&
+    SKP_ARG((M == 0 || N == 0 || K == 0 || (A_hi && A_lo && B_hi && a_exp && b_exp)) &&
                 (M == 0 || N == 0 || C),
             "gemm_h3: null pointer");
     return gemm_h3(transA, M, N, K, alpha, A_hi, A_lo, lda, a_exp, B_hi, B_lo, ldb, b_exp, beta, C,
@@ -1385,7 +1388,7 @@ extern "C" int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, f
     SKP_ARG(lda >= (transA ? M : K) && lda >= 1, "gemm_h3_emit_t: lda too small");
     SKP_ARG(ldb >= K && ldb >= 1, "gemm_h3_emit_t: ldb too small");
     SKP_ARG(ldct >= M, "gemm_h3_emit_t: ldct too small");
-    SKP_ARG(Ct_hi && Ct_lo && e_out && A_hi && A_lo && B_hi && B_lo && a_exp && b_exp,
+    SKP_ARG(Ct_hi && Ct_lo && e_out && A_hi && A_lo && B_hi && a_exp && b_exp,
             "gemm_h3_emit_t: null pointer");
     H3Emit em{Ct_hi, Ct_lo, ldct, shift, fixed, e_fixed, e_out, overflow};
     return gemm_h3_impl(transA, M, N, K, alpha, A_hi, A_lo, lda, a_exp, B_hi, B_lo, ldb, b_exp,
