@@ -48,7 +48,7 @@ def pivot_tol(be, rows: int, cols: int, tol=None) -> float:
 
 
 def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: bool = False,
-                   passes: int = 2):
+                   passes: int = 2, planes_out: bool = False):
     """Orthonormal basis of range(y) (linalg.py:57-81) by CholeskyQR2.
 
     ``lazy``: no host synchronisation; a Cholesky failure (rank deficiency)
@@ -63,7 +63,7 @@ def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: b
         rows_total = y.cols if rows_total is None else rows_total
         rel = pivot_tol(be, rows_total, y.rows, tol)
         if lazy and passes == 2:
-            return be.orth_planes(comm, y, rel)
+            return be.orth_planes(comm, y, rel, planes_out)
         y = be.planes_to_compute(y)
     c = y.shape[1]
     rows_total = y.shape[0] if rows_total is None else rows_total
@@ -125,7 +125,7 @@ def randsvd(be, comm, a, qb, check: bool = True, amax_hint=None):
     sits on the GEMM's M side (full 256-row CTA-pair tiles) instead of the
     short c, and B B^T = (B^T)^T B^T, V = B^T U~ read it directly."""
     if check:
-        g = comm.allreduce_(be.gram64(qb))
+        g = comm.allreduce_(be.gram64(be.dense(qb) if hasattr(be, "dense") else qb))
         dev = be.orth_dev(g)
         if not dev <= ORTHO_TOL[_dtype_key(be)]:
             raise ValueError(f"Q is not orthonormal (deviation {dev:.3e})")
@@ -134,7 +134,7 @@ def randsvd(be, comm, a, qb, check: bool = True, amax_hint=None):
         # the in-kernel fp16 split met an entry beyond its exponent bound (a
         # hint that did not hold): recompute with 3xTF32 on every rank.  The
         # flag is read once, after everything is queued (no mid-call sync).
-        out = _randsvd_core(be, comm, be.mm(a, qb, ta=True), qb)
+        out = _randsvd_core(be, comm, be.mm(a, be.dense(qb), ta=True), qb)
     return out
 
 
@@ -146,7 +146,8 @@ def _randsvd_core(be, comm, bt, qb):
     p = min(c, n)
     sig, inv = be.sqrt_eigs(w)
     vc = be.to_compute(be.cols(v, p))
-    u = be.mm(qb, vc)
+    planes = hasattr(qb, "hi")          # Q given as the fp16 planes of Q^T
+    u = be.mm(qb, vc, ta=planes)
     vv = be.mm(bt, vc)
     be.scale_cols_(vv, inv[:p])
     return u, sig[:p], vv

@@ -448,14 +448,19 @@ class CudaBackend:
         if (self.dtype != F32 or self.gemm_mode != "auto" or a.shape[0] * a.shape[1] < H3_MIN_ELEMS
                 or a.stride(1) != 1 or a.stride(0) % 32 or a.data_ptr() % 16
                 or os.environ.get("SKP_NO_H3") or not _lib.load().skp_has_tcgen05()):
-            return self.mm(a, q, ta=True)
+            return self.mm(a, self.dense(q), ta=True)
         if amax_hint is not None:
             e_a = amax_hint[0].clone()
             h2_exponent(a, e_a, have_amax=True, margin_bits=amax_hint[1])
         else:
             e_a = h2_exponent(a)
-        sq = split_h2(q, trans=True)
+        # q: fp32 (rows x c), or already the planes of q^T (the planes path)
+        sq = q if isinstance(q, SplitH2) else split_h2(q, trans=True)
         return gemm_h3s_t(a, e_a, sq, overflow=self.overflow)
+
+    def dense(self, q):
+        """fp32 matrix of q (q itself, or Q from the planes of Q^T)."""
+        return self.planes_to_compute(q) if isinstance(q, SplitH2) else q
 
     def overflowed(self, comm=None) -> bool:
         """Did the last mm_at_big overflow (on any rank)?  Host sync."""
@@ -580,12 +585,16 @@ class CudaBackend:
             yt = gemm_h3_emit_t(atil, split_h2(z, trans=True), out=yt, b_lo=bl)
         return yt
 
-    def orth_planes(self, comm, yt: SplitH2, rel: float):
-        """Lazy CholeskyQR2 of Y given as Y^T planes; returns Q (fp32, rows x c)."""
+    def orth_planes(self, comm, yt: SplitH2, rel: float, planes_out: bool = False):
+        """Lazy CholeskyQR2 of Y given as Y^T planes; returns Q (fp32, rows x
+        c), or with planes_out the planes of Q^T (what randsvd consumes)."""
         x1 = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), rel, lazy=True)
         q1t = gemm_h3_emit_t(yt, split_h2(self.to_compute(x1)), ta=True, e_fixed=14,
                              overflow=self.fail[1:])
         x2 = self.chol_inv64(comm.allreduce_(self.gram64_planes(q1t)), 0.0, lazy=True)
+        if planes_out:
+            return gemm_h3_emit_t(q1t, split_h2(self.to_compute(x2)), ta=True, e_fixed=14,
+                                  overflow=self.fail[1:])
         return gemm_h3(q1t, split_h2(self.to_compute(x2)), ta=True)
 
     def planes_to_compute(self, yt: SplitH2):

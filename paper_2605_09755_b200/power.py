@@ -136,7 +136,8 @@ def power_iterate(atil, omega, q: int, stabilized: bool = True):
 def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL,
                       rows_total: int | None = None, phases: _Phases | None = None,
                       fro2: torch.Tensor | None = None, name: str = "a",
-                      streamed: "_convert.Streamed | None" = None, hint_out: dict | None = None):
+                      streamed: "_convert.Streamed | None" = None, hint_out: dict | None = None,
+                      planes_out: bool = False):
     """Alg. 1 on a device row slab; returns Q (rows x <= r2).  Raises on
     non-finite entries of a (counted inside the sketch kernel).  streamed: a
     still arrives from the host block by block -- each block is sketched as
@@ -207,7 +208,8 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total,
                               lazy=True)
     ph.mark("power")
-    qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total, lazy=True)
+    qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total, lazy=True,
+                                planes_out=planes_out)
     ph.mark("orth")
     nbad = int(bad.item())
     omega_failed = nbad >= _ops.OMEGA_FAIL_MARK
@@ -293,7 +295,8 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
     ph = _Phases(timings is not None)
     fro2 = torch.zeros(1, dtype=torch.float64, device=op.t.device) if with_error else None
     hint = {}
-    qb = _range_finder_dev(op.t, spec, phases=ph, fro2=fro2, streamed=streamed, hint_out=hint)
+    qb = _range_finder_dev(op.t, spec, phases=ph, fro2=fro2, streamed=streamed, hint_out=hint,
+                           planes_out=True)
     u, s, v = _randsvd_dev(op.t, qb, check=False, amax_hint=hint.get("amax"))
     ph.mark("randsvd")
     res = SvdResult(_convert.download(u, op.kind), _convert.download(s, op.kind),

@@ -17,6 +17,9 @@ class NumpyBackend:
     def prepare(self, x):
         return x
 
+    def dense(self, q):
+        return q
+
     def mm_at_big(self, a, q, amax_hint=None):
         return self.mm(a, q, ta=True)
 
