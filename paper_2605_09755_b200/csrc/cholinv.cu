@@ -38,6 +38,7 @@ struct CIShared {
     double a[CB][CB + 1];
     double b[CB][CB + 1];
     double c[CB][CB + 1];
+    double e[CB][CB + 1];
     double invd[CB];
     int bad;
 };
@@ -78,54 +79,75 @@ __device__ __forceinline__ double rsqrt64(double d) {   // d > 0, finite, normal
 
 // 32x32 SPD tile T (smem, lower part) -> L into T (lower, upper zeroed) and
 // L^{-1} into Li, by the whole block (block-uniform; 256 threads):
-//   Cholesky, right-looking: per step k thread 0 takes the pivot (rsqrt64),
-//   the column below is scaled, the trailing triangle (<= 496 entries) is
-//   updated ~2 entries per thread -- 3 block barriers per step;
+//   Cholesky, right-looking on the UNSCALED columns: step k reads the pivot
+//   d_k = T[k][k] and updates T[i][j] -= T[i][k] T[j][k] / d_k for
+//   k < j <= i -- column k is never written again, so one block barrier per
+//   step suffices; each thread owns <= 3 fixed (i, j) entries of the lower
+//   triangle (no per-step index arithmetic).  Afterwards L_ij = T_ij / sqrt(d_j)
+//   in one pass.  (Scaling the column in place took 3 barriers per step and a
+//   triangular index decode per entry: 18.8 us per tile.)
 //   inverse by recursive doubling: with the diagonal 1/L_ii, level b = 1..16
 //   fills every off-diagonal block of the inverse at once,
 //   X21 = -X22 (L21 X11), one output entry per thread, 2 barriers per level.
-// (A one-warp version serialised on the 32-step dependency chains and its
-// register rows were demoted to local memory.)  Returns the first bad pivot
-// (1-based in the tile, 0 if none) and the pivot range via *mn / *mx.
+// Returns the first bad pivot (1-based in the tile, 0 if none) and the pivot
+// range via *mn / *mx.
 __device__ __forceinline__ int tile_chol_inv(double (*T)[CB + 1], double (*Li)[CB + 1],
                                              double (*W)[CB + 1], double* invd, double* mn,
                                              double* mx) {
     __shared__ int s_bad;
     __shared__ double s_mn, s_mx;
+    __shared__ double s_d[CB];
     const int tid = threadIdx.x;
-    if (tid == 0) {
-        s_bad = 0;
-        s_mn = INFINITY;
-        s_mx = 0.0;
+    // owned lower-triangle entries (i >= j), linear index t = i (i + 1) / 2 + j
+    int oi[3], oj[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+        const int t = tid + u * 256;
+        int r = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+        while (r * (r + 1) / 2 > t) --r;
+        while ((r + 1) * (r + 2) / 2 <= t) ++r;
+        oi[u] = t < CB * (CB + 1) / 2 ? r : -1;
+        oj[u] = t - r * (r + 1) / 2;
     }
+    if (tid == 0) s_bad = 0;
     for (int k = 0; k < CB; ++k) {
+        __syncthreads();  // step k-1's updates (and the pivot T[k][k]) are visible
+        double d = T[k][k];
+        const bool ok = d > 1e-300 && isfinite(d);
+        if (!ok) d = 1.0;  // keep going; the caller discards the result
         if (tid == 0) {
-            double d = T[k][k];
-            if (!(d > 1e-300) || !isfinite(d)) {
-                if (!s_bad) s_bad = k + 1;
-                d = 1.0;  // keep going; the caller discards the result
-            }
-            const double inv = rsqrt64(d);
-            const double l = d * inv;
-            T[k][k] = l;
-            invd[k] = inv;
-            s_mn = fmin(s_mn, l);
-            s_mx = fmax(s_mx, l);
+            if (!ok && !s_bad) s_bad = k + 1;
+            s_d[k] = d;
         }
-        __syncthreads();
-        if (tid > k && tid < CB) T[tid][k] *= invd[k];   // L_ik
-        __syncthreads();
-        const int m = CB - 1 - k;                        // trailing triangle k < j <= i
-        for (int t = tid; t < m * (m + 1) / 2; t += blockDim.x) {
-            int r = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-            while (r * (r + 1) / 2 > t) --r;
-            while ((r + 1) * (r + 2) / 2 <= t) ++r;
-            const int c = t - r * (r + 1) / 2;
-            const int i = k + 1 + r, j = k + 1 + c;
-            T[i][j] -= T[i][k] * T[j][k];
+        const double rd = 1.0 / d;
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+            const int i = oi[u], j = oj[u];
+            if (i >= 0 && j > k) T[i][j] -= (T[i][k] * rd) * T[j][k];
         }
-        __syncthreads();
     }
+    __syncthreads();
+    if (tid < CB) {
+        const double is = rsqrt64(s_d[tid]);
+        invd[tid] = is;  // 1 / L_jj
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+        const int i = oi[u], j = oj[u];
+        if (i >= 0) T[i][j] = (i == j) ? s_d[j] * invd[j] : T[i][j] * invd[j];
+    }
+    if (tid == 0) {
+        double lo = INFINITY, hi = 0.0;
+        for (int k = 0; k < CB; ++k) {
+            const double l = s_d[k] * invd[k];
+            lo = fmin(lo, l);
+            hi = fmax(hi, l);
+        }
+        s_mn = lo;
+        s_mx = hi;
+    }
+    __syncthreads();
     for (int q = tid; q < CB * CB; q += blockDim.x) {
         const int i = q / CB, j = q % CB;
         if (j > i) T[i][j] = 0.0;
@@ -266,27 +288,20 @@ cholinv_kernel(const double* __restrict__ G, int n, int64_t ldg, int nb, double 
                 // remap so task 0 is the lookahead tile (p+1, p+1): tile order
                 // (0,0),(1,0),(1,1),... -> (I, J) relative to p+1
                 const int I0 = (p + 1 + I) * CB, J0 = (p + 1 + J) * CB;
+                // all operand tiles in flight at once (one global round trip)
                 tload(sh.b, X, p0, p0);                 // L_pp^{-1}
                 tload(sh.a, A, I0, p0);                 // A_Ip
+                if (I != J) tload(sd, A, J0, p0);       // A_Jp
+                tload(sh.e, A, I0, J0);                 // A_IJ
                 __syncthreads();
                 tile_mm(sh.c, sh.a, sh.b, 0, 1.0, false);   // L_Ip = A_Ip L_pp^{-T}
                 if (J == 0) tstore(Lb, I0, p0, sh.c);
-                if (I != J) {
-                    tload(sh.a, A, J0, p0);             // A_Jp
-                    __syncthreads();
-                    tile_mm(sd, sh.a, sh.b, 0, 1.0, false);  // L_Jp
-                } else {
-                    for (int q = threadIdx.x; q < CB * CB; q += blockDim.x)
-                        sd[q / CB][q % CB] = sh.c[q / CB][q % CB];
-                    __syncthreads();
-                }
-                tload(sh.a, A, I0, J0);                 // A_IJ
-                __syncthreads();
-                tile_mm(sh.a, sh.c, sd, 0, -1.0, true); // A_IJ -= L_Ip L_Jp^T
-                tstore(A, I0, J0, sh.a);
+                if (I != J) tile_mm(sh.a, sd, sh.b, 0, 1.0, false);  // L_Jp
+                tile_mm(sh.e, sh.c, I != J ? sh.a : sh.c, 0, -1.0, true);  // A_IJ -= L_Ip L_Jp^T
+                tstore(A, I0, J0, sh.e);
                 if (t == 0 && blockIdx.x == 0) {
                     stamp(4 * p + 2);
-                    factor(p + 1, sh.a);  // lookahead
+                    factor(p + 1, sh.e);  // lookahead
                     stamp(4 * p + 3);
                 }
                 __syncthreads();
