@@ -379,8 +379,10 @@ def run_benchmark(cfg: BenchConfig, csv_path: str | None = None, a=None,
     if a is None:
         a = synthetic(cfg.dataset)
         if a is None:
-            raise ValueError(f"unsupported dataset {cfg.dataset!r}: pass the matrix as `a` "
-                             "(file ingestion is not on the device path)")
+            # files go straight to the device (io.py: .skpw streamed, MatrixMarket parsed)
+            from . import io as skio
+            a = (skio.read_skpw(cfg.dataset) if cfg.dataset.endswith(".skpw")
+                 else skio.read_matrix_market(cfg.dataset))
     label = cfg.label or cfg.dataset
     dt = F64 if cfg.dtype == "float64" else F32
     dev = _ops.require_cuda()
