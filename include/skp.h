@@ -271,6 +271,21 @@ int skp_gemm_h3s(int64_t M, int64_t N, int64_t K, float alpha, const float* A, i
 int skp_h2_exponent_f32(const float* X, int64_t rows, int64_t cols, int64_t ld, int32_t* e_io,
                         int32_t have_amax, int32_t margin_bits, void* stream);
 
+/* ---------------------------------------------------------------- K7 ----
+ * SRHT (sketching.py:125-130, :167-171, :185-189): for each of `fibres`
+ * input fibres f (element j at X[f*x_fs + j*x_es], j < n),
+ *   out[f*o_fs + c*o_es] = scale * (H D pad(x_f))[subset[c]],  c < r,
+ * with D = diag(signs) (int8 +-1, n_pad entries), H the unnormalised
+ * Sylvester Hadamard matrix of order n_pad (a power of two), scale normally
+ * 1/sqrt(r).  A S: fibres = rows of A (x_fs = lda, x_es = 1); S^T X: fibres
+ * = columns of X (x_fs = 1, x_es = ldx).  n_pad * sizeof(T) <= 200 KB.      */
+int skp_srht_apply_f32(const float* X, int64_t fibres, int64_t n, int64_t x_fs, int64_t x_es,
+                       const int8_t* signs, int64_t n_pad, const int32_t* subset, int64_t r,
+                       double scale, float* out, int64_t o_fs, int64_t o_es, void* stream);
+int skp_srht_apply_f64(const double* X, int64_t fibres, int64_t n, int64_t x_fs, int64_t x_es,
+                       const int8_t* signs, int64_t n_pad, const int32_t* subset, int64_t r,
+                       double scale, double* out, int64_t o_fs, int64_t o_es, void* stream);
+
 /* Row gather y[v, :] = x[perm[v], :], v < rows (P^T Omega for the K2 v2
  * column permutation; perm = the first `rows` int32 of a gather plan).       */
 int skp_permute_rows_f32(const float* x, int64_t ldx, const int32_t* perm, float* y, int64_t ldy,

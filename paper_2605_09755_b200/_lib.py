@@ -73,6 +73,10 @@ SIGNATURES = {
     "skp_gemm_h3s": (_int, [_i64, _i64, _i64, _f32, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _f32, _vp,
                             _i64, _vp, _vp, _i64, _vp]),
     "skp_h2_exponent_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _i32, _i32, _vp]),
+    "skp_srht_apply_f32": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _f64, _vp,
+                                  _i64, _i64, _vp]),
+    "skp_srht_apply_f64": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _f64, _vp,
+                                  _i64, _i64, _vp]),
     "skp_gram_f32_f64_ws_bytes": (_i64, [_i64, _i64]),
     "skp_gram_f32_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "skp_permute_rows_f32": (_int, [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp]),

@@ -257,6 +257,28 @@ def gemm(a, b, ta: bool = False, tb: bool = False, alpha: float = 1.0, beta: flo
     return out
 
 
+def srht(x: torch.Tensor, signs: torch.Tensor, n_pad: int, subset: torch.Tensor, r: int,
+         left_t: bool, out=None) -> torch.Tensor:
+    """K7: x S (left_t=False; x is m x n, fibres = rows) or S^T x (left_t=True;
+    x is n x c, fibres = columns) for the SRHT S (sketching.py:167-171, :185-189)."""
+    rows, cols, ld = _rows_ld(x)
+    if left_t:
+        fibres, n, x_fs, x_es = cols, rows, 1, ld
+        if out is None:
+            out = empty2d(r, cols, x.dtype, x.device)
+        _, _, ldo = _rows_ld(out)
+        o_fs, o_es = 1, ldo
+    else:
+        fibres, n, x_fs, x_es = rows, cols, ld, 1
+        if out is None:
+            out = empty2d(rows, r, x.dtype, x.device)
+        _, _, ldo = _rows_ld(out)
+        o_fs, o_es = ldo, 1
+    call(f"skp_srht_apply_{_SFX[x.dtype]}", ptr(x), fibres, n, x_fs, x_es, ptr(signs), n_pad,
+         ptr(subset), r, 1.0 / float(np.sqrt(r)), ptr(out), o_fs, o_es, stream_ptr(x.device))
+    return out
+
+
 # ------------------------------------------------ 3xFP16 (pre-split) GEMM --
 
 H3_MIN_ELEMS = 1 << 22   # prepare() splits left operands of at least this many entries

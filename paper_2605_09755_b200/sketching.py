@@ -10,8 +10,11 @@ Mirrors /root/reference/pkg/src/skpower/sketching.py: ``SketchOperator``
 * ``identity``    -- the classical (unsketched) hook (sketching.py:137-139).
 * ``gaussian`` / ``sign`` -- dense S drawn on the host with the reference's
   numpy stream (bit-identical), applied with the device GEMM.
-* ``srht``        -- not on the accelerated path: raises
-  ValueError("unsupported ...").  No CPU fallback exists.
+* ``srht``        -- the signs and the sorted coordinate subset are numpy's
+  draw (bit-identical, sketching.py:125-130); apply_right /
+  apply_left_transpose are the K7 kernel (sign, zero-pad, fast
+  Walsh-Hadamard transform in shared memory, subset gather), densify is K7
+  applied to the identity.  No CPU fallback exists.
 """
 from __future__ import annotations
 
@@ -25,7 +28,7 @@ from . import _convert, _ops
 from ._ops import F32, F64
 
 SKETCH_KINDS = ("gaussian", "sign", "countsketch", "srht", "identity")
-DEVICE_KINDS = ("gaussian", "sign", "countsketch", "identity")
+DEVICE_KINDS = ("gaussian", "sign", "countsketch", "srht", "identity")
 
 _DENSIFY_CAP = 10**7
 _MASK64 = (1 << 64) - 1
@@ -71,10 +74,17 @@ class SketchOperator:
         self.s = None
         self._dense_host = None
         self._dense_dev = {}
-        if kind == "srht":
-            raise ValueError("unsupported on the B200 path: the srht sketch is out of scope "
-                             "(countsketch, identity, gaussian and sign are supported)")
         self.device = _ops.require_cuda(device)
+        if kind == "srht":  # (handled first; the chain below covers the other kinds)
+            n_pad = 1 << (int(n) - 1).bit_length()
+            if r > n_pad:
+                raise ValueError(f"srht needs r <= padded dimension {n_pad}, got r={r}")
+            rng = _host_rng(self.seed)
+            self._n_pad = n_pad
+            self._srht_signs = rng.integers(0, 2, size=n_pad).astype(np.float64) * 2.0 - 1.0
+            self._subset = np.sort(rng.choice(n_pad, size=r, replace=False))
+            self.d_srht_signs = torch.from_numpy(self._srht_signs.astype(np.int8)).to(self.device)
+            self.d_subset = torch.from_numpy(self._subset.astype(np.int32)).to(self.device)
         if kind == "countsketch":
             s = 1 if s is None else int(s)
             if not 1 <= s <= r:
@@ -88,7 +98,7 @@ class SketchOperator:
         elif kind == "sign":
             d = _host_rng(self.seed).integers(0, 2, size=(n, r)).astype(np.float64) * 2.0 - 1.0
             self._dense_host = d / math.sqrt(r)
-        else:  # identity
+        elif kind == "identity":
             if r != n:
                 raise ValueError(f"identity sketch needs r == n, got n={n}, r={r}")
 
@@ -103,6 +113,8 @@ class SketchOperator:
 
     @property
     def _signs(self) -> np.ndarray:
+        if self.kind == "srht":
+            return self._srht_signs
         return self.d_signs.cpu().numpy().astype(np.float64)
 
     def _dense(self, dtype) -> torch.Tensor:
@@ -121,6 +133,8 @@ class SketchOperator:
             _ops.sumsq(a, fro2, nonfinite)
         if self.kind == "identity":
             return a.clone() if out is None else out.copy_(a)
+        if self.kind == "srht":
+            return _ops.srht(a, self.d_srht_signs, self._n_pad, self.d_subset, self.r, False, out)
         return _ops.gemm(a, self._dense(a.dtype), out=out)
 
     def gather_plan(self, check: bool = True):
@@ -161,6 +175,8 @@ class SketchOperator:
             return _ops.sketch_left_t(x, self.colptr, self.entries, self.s, self.r, out)
         if self.kind == "identity":
             return x.clone() if out is None else out.copy_(x)
+        if self.kind == "srht":
+            return _ops.srht(x, self.d_srht_signs, self._n_pad, self.d_subset, self.r, True, out)
         return _ops.gemm(self._dense(x.dtype), x, ta=True, out=out)
 
     # -- reference API --------------------------------------------------------
@@ -189,6 +205,9 @@ class SketchOperator:
             return out
         if self.kind == "identity":
             return np.eye(self.n)
+        if self.kind == "srht":   # S = (S^T I)^T, K7 on the identity
+            eye = torch.eye(self.n, dtype=F64, device=self.device)
+            return self.left_t(_ops.aligned2d(eye)).T.cpu().numpy().copy()
         return self._dense_host.copy()
 
 

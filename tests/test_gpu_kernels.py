@@ -89,8 +89,33 @@ def test_countsketch_bad_arguments(skp):
         skp.make_sketch("nope", 10, 4, seed=0)
     with pytest.raises(ValueError):
         skp.make_sketch("identity", 10, 4, seed=0)
-    with pytest.raises(ValueError, match="unsupported"):
-        skp.make_sketch("srht", 16, 4, seed=0)
+    with pytest.raises(ValueError, match="padded dimension"):
+        skp.make_sketch("srht", 16, 17, seed=0)
+
+
+# ------------------------------------------------------------------- K7 ---
+
+@pytest.mark.parametrize("case", ["50_12_9", "64_64_3", "1000_37_21", "3000_300_77"])
+@pytest.mark.parametrize("dtype,tol", [(np.float64, 1e-12), (np.float32, 3e-6)])
+def test_srht_matches_live_reference(skp, case, dtype, tol):
+    """Signs / subset bit-exact (numpy draw); A S, S^T X and densify vs the
+    reference's own outputs (tests/golden/make_srht_golden.py)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "srht_golden.npz"))
+    n, r, seed = (int(v) for v in case.split("_"))
+    op = skp.make_sketch("srht", n, r, seed=seed)
+    assert np.array_equal(op._signs, g[f"signs_{case}"])
+    assert np.array_equal(op._subset, g[f"subset_{case}"])
+    a, x = g[f"a_{case}"].astype(dtype), g[f"x_{case}"].astype(dtype)
+    ra, rx = g[f"right_{case}"], g[f"left_{case}"]
+    got_a, got_x = op.apply_right(a), op.apply_left_transpose(x)
+    assert got_a.dtype == dtype and got_x.dtype == dtype
+    scale_a = np.abs(a).max() * np.sqrt(n) + 1e-300
+    scale_x = np.abs(x).max() * np.sqrt(n) + 1e-300
+    assert np.abs(got_a - ra).max() <= tol * scale_a
+    assert np.abs(got_x - rx).max() <= tol * scale_x
+    if f"dense_{case}" in g.files:
+        assert np.abs(op.densify() - g[f"dense_{case}"]).max() <= 1e-12
 
 
 # ---------------------------------------------------------------- K2/K3 ---
@@ -514,3 +539,17 @@ def test_gram_f32_f64(ops, k, c):
     ref = x.astype(np.float64).T @ x.astype(np.float64)
     assert np.abs(g - ref).max() <= 1e-13 * np.abs(ref).max()
     np.testing.assert_array_equal(g, g.T)
+
+
+def test_srht_range_finder_exact_rank(skp):
+    """The SRHT sketch inside the range finder: an exactly rank-8 matrix is
+    recovered (sigma to 1e-10 in fp64), as with the other sketch kinds."""
+    rng = np.random.default_rng(3)
+    u = np.linalg.qr(rng.standard_normal((300, 8)))[0]
+    v = np.linalg.qr(rng.standard_normal((200, 8)))[0]
+    s = np.linspace(3.0, 1.0, 8)
+    a = (u * s) @ v.T
+    spec = skp.RangeFinderSpec(k=8, l=40, r1=40, r2=12, q=1, eps=0.5, sketch_kind="srht", seed=4)
+    q = skp.range_finder_sketched(a, spec)
+    res = skp.randsvd(a, q)
+    np.testing.assert_allclose(np.asarray(res.sigma)[:8], s, rtol=0, atol=1e-10)
