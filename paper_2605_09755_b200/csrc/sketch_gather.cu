@@ -104,28 +104,129 @@ __device__ __forceinline__ void g_bulk_load_e(uint32_t dst, const void* src, uin
         : "memory");
 }
 
-// ---- plan 1: per-slice column order, sorted by entry count (descending) -----
+// ---- plan 1: per-slice lane table ---------------------------------------------
 // Slice p owns output positions [p*width, p*width + nc_p) (width = the balanced
-// slice width, gather_width); perm[pos] = the column written at position pos
-// (compact: the first r entries), -1 for pos in [r, P*kGCols).  One block per slice.
-__global__ void gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r, int width,
-                                   int64_t slots, int32_t* __restrict__ perm) {
-    __shared__ int key[kGCols];
+// slice width, gather_width).  A warp's schedule is as long as its heaviest
+// lane, and columns sorted by entry count leave the heavy warps ~1.5x longer
+// than the mean (C3: 52-56 steps vs 35 -- warps idle a third of the time).
+// So columns with more than `cap` entries are split into two half-columns on
+// an adjacent lane pair (2k, 2k+1) whose sums the kernel combines with one
+// shuffle; cap is the smallest value >= the mean count for which the lanes
+// still fit the CTA's 32*kGW.  Lane units (1 or 2 lanes) are sorted by
+// per-lane count, descending, and placed in order (a pair never straddles an
+// even lane boundary; the hole it skips is filled by the next single).
+// Per lane: seg_beg / seg_cnt (its range of the column's CSC entries) and
+// lanepos = output position | kGPrimary (add lane+1's sum), or -1 (no write).
+// perm[pos] = the column written at position pos (compact: the first r
+// entries), -1 for pos in [r, P*kGCols).  One block per slice.
+constexpr int kGPrimary = 1 << 30;
+__global__ void __launch_bounds__(256)
+gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r, int width, int64_t slots,
+                   int32_t* __restrict__ perm, int32_t* __restrict__ seg_beg,
+                   int32_t* __restrict__ seg_cnt, int32_t* __restrict__ lanepos) {
+    __shared__ int key[kGCols];        // column entry counts
+    __shared__ int ucnt[kGCols];       // per-lane count of the column's unit
+    __shared__ int order[kGCols];      // units in placement order (column index)
+    __shared__ int lane_col[kGCols];   // lane -> column (-1 empty)
+    __shared__ int lane_part[kGCols];  // 0 single, 1 first half (primary), 2 second half
+    __shared__ int hist[kGTMax + 2];
+    __shared__ int s_cap;
     const int64_t c0 = (int64_t)blockIdx.x * width;
     const int nc = (int)(r - c0 < width ? r - c0 : width);
-    for (int v = threadIdx.x; v < kGCols; v += blockDim.x)
+    const int lanes = kGCols;
+    for (int v = threadIdx.x; v < kGCols; v += blockDim.x) {
         key[v] = v < nc ? colptr[c0 + v + 1] - colptr[c0 + v] : -1;
+        lane_col[v] = -1;
+        lane_part[v] = 0;
+    }
+    for (int v = threadIdx.x; v < kGTMax + 2; v += blockDim.x) hist[v] = 0;
     if (blockIdx.x == 0)
         for (int64_t v = r + threadIdx.x; v < slots; v += blockDim.x) perm[v] = -1;
     __syncthreads();
+    for (int v = threadIdx.x; v < nc; v += blockDim.x) atomicAdd(&hist[min(key[v], kGTMax + 1)], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long tot = 0;
+        for (int c = 0; c <= kGTMax + 1; ++c) tot += (long long)c * hist[c];
+        const int mean = nc ? (int)((tot + nc - 1) / nc) : 0;
+        // columns above cap become 2 lanes (+ at most one hole each)
+        int above = 0, cap = kGTMax + 1;
+        for (int c = kGTMax + 1; c >= mean; --c) {
+            if (nc + 2 * (above + hist[c]) > lanes) break;
+            above += hist[c];
+            cap = c - 1;
+        }
+        s_cap = max(cap, mean);
+    }
+    __syncthreads();
+    const int cap = s_cap;
+    for (int v = threadIdx.x; v < kGCols; v += blockDim.x)
+        ucnt[v] = v < nc ? (key[v] > cap ? (key[v] + 1) / 2 : key[v]) : -1;
+    __syncthreads();
     for (int v = threadIdx.x; v < nc; v += blockDim.x) {
-        const int kv = key[v];
+        const int kv = ucnt[v];
         int rank = 0;
         for (int u = 0; u < nc; ++u) {
-            const int ku = key[u];
+            const int ku = ucnt[u];
             rank += (ku > kv) || (ku == kv && u < v);
         }
-        perm[c0 + rank] = (int32_t)(c0 + v);
+        order[rank] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int pos = 0, hole = -1;
+        for (int k = 0; k < nc; ++k) {
+            const int v = order[k];
+            if (key[v] > cap) {
+                if (pos & 1) {  // keep the pair on (2k, 2k+1): skip a lane
+                    if (hole < 0) hole = pos;
+                    ++pos;
+                }
+                lane_col[pos] = v;
+                lane_part[pos] = 1;
+                lane_col[pos + 1] = v;
+                lane_part[pos + 1] = 2;
+                pos += 2;
+            } else if (hole >= 0) {
+                lane_col[hole] = v;
+                hole = -1;
+            } else {
+                lane_col[pos++] = v;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // output positions in lane order
+        int k = 0;
+        for (int l = 0; l < lanes; ++l) {
+            const int v = lane_col[l];
+            const int64_t g = (int64_t)blockIdx.x * kGCols + l;
+            if (v < 0) {
+                seg_beg[g] = 0;
+                seg_cnt[g] = 0;
+                lanepos[g] = -1;
+                continue;
+            }
+            const int beg = colptr[c0 + v], cnt = key[v];
+            const int half = (cnt + 1) / 2;
+            if (lane_part[l] == 0) {
+                seg_beg[g] = beg;
+                seg_cnt[g] = cnt;
+            } else if (lane_part[l] == 1) {
+                seg_beg[g] = beg;
+                seg_cnt[g] = half;
+            } else {
+                seg_beg[g] = beg + half;
+                seg_cnt[g] = cnt - half;
+            }
+            if (lane_part[l] == 2) {
+                lanepos[g] = -1;
+            } else {
+                perm[c0 + k] = (int32_t)(c0 + v);
+                lanepos[g] = (int32_t)(c0 + k) | (lane_part[l] == 1 ? kGPrimary : 0);
+                ++k;
+            }
+        }
     }
 }
 
@@ -140,19 +241,16 @@ __global__ void gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r
 // taken (a 2-way conflict rather than a longer schedule), and lanes left
 // without an entry read a zero word in a distinct free bank.
 __global__ void __launch_bounds__(128)
-gather_sched_kernel(const int32_t* __restrict__ colptr, const int32_t* __restrict__ entries,
-                    const int32_t* __restrict__ perm, int nwarps, int64_t n, int64_t r,
-                    int width, uint32_t* __restrict__ sched, int32_t* __restrict__ tw,
+gather_sched_kernel(const int32_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_cnt,
+                    const int32_t* __restrict__ entries, int nwarps, int64_t n,
+                    uint32_t* __restrict__ sched, int32_t* __restrict__ tw,
                     int32_t* __restrict__ fail) {
     const int wg = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (wg >= nwarps) return;
     const uint32_t zero_word = (uint32_t)((n + 31) / 32 * 32);  // 32 zero words after the row
-    const int local = (wg % kGW) * 32 + lane;          // position inside the slice
-    const int64_t pos = (int64_t)(wg / kGW) * width + local;
-    const int c = (local < width && pos < r) ? perm[pos] : -1;
-    const int beg = c >= 0 ? colptr[c] : 0;
-    const int cnt = c >= 0 ? colptr[c + 1] - colptr[c] : 0;
+    const int beg = seg_beg[(int64_t)wg * 32 + lane];   // this lane's (half-)column
+    const int cnt = seg_cnt[(int64_t)wg * 32 + lane];
     if (__any_sync(0xffffffffu, cnt > kGTMax)) {
         if (lane == 0) {
             atomicOr(fail, 1);
@@ -246,8 +344,8 @@ gather_sched_kernel(const int32_t* __restrict__ colptr, const int32_t* __restric
 
 // ---- the gather ----------------------------------------------------------------
 __global__ void __maxnreg__(80)
-sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n, int64_t r,
-                     int P, int width, const uint32_t* __restrict__ sched,
+sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                     const int32_t* __restrict__ lanepos, int P, const uint32_t* __restrict__ sched,
                      const int32_t* __restrict__ tw, const int32_t* __restrict__ plan_fail,
                      float scale, float* __restrict__ out, int64_t ldo,
                      int64_t* nonfinite, uint32_t* __restrict__ amax) {
@@ -298,8 +396,10 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
         // (steps >= kGTReg, if any, are read per row below)
         e[t] = v + base;  // absolute smem address in buffer 0; bit 31 (sign) kept
     }
-    const int64_t v_out = (int64_t)slice * width + warp * 32 + lane;  // output position
-    const bool valid = warp * 32 + lane < width && v_out < r;
+    const int lp = lanepos[(int64_t)wg * 32 + lane];
+    const int64_t v_out = lp & (kGPrimary - 1);  // output position
+    const bool valid = lp >= 0;                  // (second halves of split columns: no write)
+    const bool primary = lp >= 0 && (lp & kGPrimary);
     bool bad = false;  // a non-finite output of this thread (iff a non-finite input)
     uint32_t mx = 0;   // max |output| (bits; non-negative floats order as integers)
 
@@ -352,6 +452,9 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
                 }
             }
         }
+        // a split column's second half sits on the next lane
+        const float part = __shfl_down_sync(0xffffffffu, acc, 1);
+        if (primary) acc += part;
         if (valid) {
             const float o = acc * scale;
             bad |= !isfinite(o);
@@ -383,7 +486,8 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
 }  // namespace
 
 // plan layout (bytes): perm int32[P*kGCols] | tw int32[P*kGW] | fail int32 |
-//                      pad to 16 | sched uint32[P*kGW*kGTMax*32]
+//                      pad to 16 | sched uint32[P*kGW*kGTMax*32] |
+//                      seg_beg, seg_cnt, lanepos int32[P*kGCols] each
 int gather_slices(int64_t r) { return (int)cdiv(r, (int64_t)kGCols); }
 // balanced slice width: the P slices share the r columns evenly (multiple of
 // 32), so no CTA carries a short last slice while its SM idles (C3: 6 x 672
@@ -394,7 +498,14 @@ int gather_width(int64_t r) {
 int64_t gather_plan_bytes(int64_t r) {
     const int64_t P = gather_slices(r);
     const int64_t head = (P * kGCols + P * kGW + 1) * 4;
-    return (head + 15) / 16 * 16 + P * kGW * kGTMax * 32 * 4;
+    return (head + 15) / 16 * 16 + P * kGW * kGTMax * 32 * 4 + 3 * P * kGCols * 4;
+}
+// the lane tables after the schedule: seg_beg | seg_cnt | lanepos (P*kGCols each)
+int32_t* gather_lane_tables(void* plan, int64_t r) {
+    const int64_t P = gather_slices(r);
+    const int64_t head = (P * kGCols + P * kGW + 1) * 4;
+    return reinterpret_cast<int32_t*>(reinterpret_cast<char*>(plan) + (head + 15) / 16 * 16 +
+                                      P * kGW * kGTMax * 32 * 4);
 }
 
 int gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n, int64_t r, void* plan,
@@ -414,11 +525,16 @@ int gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n, int64_
         reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(plan) + (head + 15) / 16 * 16);
     SKP_CUDA(cudaMemsetAsync(fail, 0, 4, st));
     const int width = gather_width(r);
-    gather_sort_kernel<<<P, 256, 0, st>>>(colptr, r, width, (int64_t)P * kGCols, perm);
+    int32_t* lt = gather_lane_tables(plan, r);
+    int32_t* seg_beg = lt;
+    int32_t* seg_cnt = lt + (int64_t)P * kGCols;
+    int32_t* lanepos = lt + 2 * (int64_t)P * kGCols;
+    gather_sort_kernel<<<P, 256, 0, st>>>(colptr, r, width, (int64_t)P * kGCols, perm, seg_beg,
+                                          seg_cnt, lanepos);
     SKP_LAUNCHED(gather_sort_kernel);
     const int nw = P * kGW;
-    gather_sched_kernel<<<(unsigned)cdiv(nw, 4), 128, 0, st>>>(colptr, entries, perm, nw, n, r,
-                                                                width, sched, tw, fail);
+    gather_sched_kernel<<<(unsigned)cdiv(nw, 4), 128, 0, st>>>(seg_beg, seg_cnt, entries, nw, n,
+                                                                sched, tw, fail);
     SKP_LAUNCHED(gather_sched_kernel);
     return SKP_OK;
 }
@@ -446,9 +562,11 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
         reinterpret_cast<const char*>(plan) + (head + 15) / 16 * 16);
     SKP_CUDA(cudaFuncSetAttribute(sketch_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kGSmem));
-    sketch_gather_kernel<<<G * P, kGThreads, kGSmem, st>>>(A, lda, m, n, r, P, gather_width(r),
-                                                           sched, tw, pfail, scale, out, ldo,
-                                                           nonfinite, amax);
+    const int32_t* lanepos =
+        gather_lane_tables(const_cast<void*>(plan), r) + 2 * (int64_t)P * kGCols;
+    sketch_gather_kernel<<<G * P, kGThreads, kGSmem, st>>>(A, lda, m, n, lanepos, P, sched, tw,
+                                                           pfail, scale, out, ldo, nonfinite,
+                                                           amax);
     SKP_LAUNCHED(sketch_gather_kernel);
     if (fro2) {  // ||A||_F^2: a separate HBM-bound pass (only when asked for)
         const int rc = skp_sumsq_f32(A, m, n, lda, fro2, nullptr, st);
