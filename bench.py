@@ -282,18 +282,39 @@ def run_ours(args, cfg, rank, world, local_rank):
     tf32_peak = bf16 if h3 else bf16 / 2.0
     power_tflops = (power_f / world) / (phases.get("power", float("nan")) * 1e-3) / 1e12
     dominant = "power" if phases.get("power", 0) >= phases.get("apply_right", 0) else "sketch"
+    # DRAM bytes per launch of the dominant kernel from the committed ncu
+    # --set full capture (profiles/traffic.json, scripts/summarize_ncu.py traffic)
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                               "traffic.json")) as fh:
+            _tr = json.load(fh)
+    except (OSError, ValueError):
+        _tr = {}
+    def traffic_of(key):
+        t = _tr.get(key)
+        return None if t is None else t["bytes_per_launch"]
+
+    def traffic_src(key):
+        t = _tr.get(key)
+        return None if t is None else "profiles/traffic.json <- " + t["source"]
     if dominant == "power":
         roof = {"kernel": "gemm_nn A~.Z (power iteration)" + (
                     " tcgen05 3xFP16 (pre-split A~)" if h3 else " tcgen05 3xTF32" if tc else " SIMT"),
                 "bound": "tensor", "achieved": round(pipe_tflops, 2), "peak": round(tf32_peak, 1),
-                "unit": "TFLOP/s", "frac": round(pipe_tflops / tf32_peak, 4), "traffic": None,
+                "unit": "TFLOP/s", "frac": round(pipe_tflops / tf32_peak, 4),
+                "traffic": traffic_of("gemm_h3_nn" if h3 else "gemm_tc_nn"),
+                "traffic_unit": "DRAM bytes per launch (ncu --set full)",
+                "traffic_source": traffic_src("gemm_h3_nn" if h3 else "gemm_tc_nn"),
                 "useful_tflops": round(gemm_tflops, 2), "ms_per_launch": round(gemm_ms, 4),
                 "peak_note": (f"f16 dense = {peak_src} bf16 {bf16} TFLOP/s" if h3 else
                               f"TF32 dense = bf16/2 of {peak_src} bf16 {bf16} TFLOP/s"),
                 "algorithmic_flop_per_launch": gemm_flop}
     else:
         roof = {"kernel": "sketch_gather (K2 v2)" if v2 else "sketch_right (K2 v1)", "bound": "hbm", "achieved": round(sketch_gbs, 1),
-                "peak": hbm, "unit": "GB/s", "frac": round(sketch_gbs / hbm, 4), "traffic": None,
+                "peak": hbm, "unit": "GB/s", "frac": round(sketch_gbs / hbm, 4),
+                "traffic": traffic_of("sketch_gather" if v2 else "sketch_rows"),
+                "traffic_unit": "DRAM bytes per launch (ncu --set full)",
+                "traffic_source": traffic_src("sketch_gather" if v2 else "sketch_rows"),
                 "ms_per_launch": round(sketch_ms, 4), "algorithmic_bytes_per_launch": sketch_bytes}
     extra = {
         "sketch": {"kernel": "sketch_gather (K2 v2)" if v2 else "sketch_right (K2 v1)",

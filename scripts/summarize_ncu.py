@@ -72,5 +72,32 @@ def full(path, out):
                     f.write(f"{k:85s} {units[hdr.index(k)]:8s} {d[k]}\n")
 
 
+def traffic(out, *reps):
+    """profiles/traffic.json: DRAM bytes (read + write) per launch of each
+    captured kernel, for bench.py's roofline "traffic" field.
+        python scripts/summarize_ncu.py traffic profiles/traffic.json key=report.ncu-rep ..."""
+    import json
+    res = {}
+    for kv in reps:
+        key, path = kv.split("=", 1)
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
+        rows = list(csv.reader(raw.splitlines()))
+        hdr, units, vals = rows[0], rows[1], rows[2]
+        d = dict(zip(hdr, vals))
+        u = dict(zip(hdr, units))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(d[k]) * scale[u[k]]
+        res[key] = {"bytes_per_launch": tot, "source": path.split("/")[-1],
+                    "kernel": d.get("Kernel Name", "?")[:80]}
+    with open(out, "w") as f:
+        json.dump(res, f, indent=1)
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    if sys.argv[1] == "traffic":
+        traffic(sys.argv[2], *sys.argv[3:])
+    else:
+        {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
