@@ -235,6 +235,12 @@ int skp_cast2d_f64_f32(const double* x, int64_t ldx, float* y, int64_t ldy, int6
 int skp_split_h2_f32(const float* X, int64_t rows, int64_t cols, int64_t ld, int32_t trans,
                      void* hi, void* lo, int64_t ldh, int32_t* e_io, int32_t have_amax,
                      void* stream);
+/* In place: row i of X (fp32, ld) becomes the fp16 planes [hi | lo]: hi at
+ * (half*)X + i*2ld, lo at (half*)X + ld + i*2ld -- planes with leading
+ * dimension 2 ld -- so a buffer that is no longer needed in fp32 (A~) is split
+ * without a second allocation.  ld % 8 == 0, rows <= 50K columns.           */
+int skp_split_h2_inplace_f32(float* X, int64_t rows, int64_t cols, int64_t ld, int32_t* e_io,
+                             int32_t have_amax, void* stream);
 int64_t skp_gemm_h3_ws_bytes(int transA, int64_t M, int64_t N, int64_t K);
 int skp_gemm_h3(int transA, int64_t M, int64_t N, int64_t K, float alpha, const void* A_hi,
                 const void* A_lo, int64_t lda, const int32_t* a_exp, const void* B_hi,

@@ -64,6 +64,7 @@ SIGNATURES = {
     "skp_cast_f32_f64": (_int, [_vp, _vp, _i64, _vp]),
     "skp_cast_f64_f32": (_int, [_vp, _vp, _i64, _vp]),
     "skp_split_h2_f32": (_int, [_vp, _i64, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _i32, _vp]),
+    "skp_split_h2_inplace_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _i32, _vp]),
     "skp_gemm_h3_ws_bytes": (_i64, [_int, _i64, _i64, _i64]),
     "skp_gemm_h3": (_int, [_int, _i64, _i64, _i64, _f32, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
                            _f32, _vp, _i64, _vp, _i64, _vp]),

@@ -537,6 +537,40 @@ __global__ void split_h2_kernel(const float* __restrict__ X, int64_t rows, int64
     }
 }
 
+// In place: row i of X (ld fp32 = 4 ld bytes) becomes [hi (cols halves) ... |
+// lo at half offset ld ...]: the planes' leading dimension is 2 ld halves.
+// One CTA per row at a time: the row is staged in shared memory first.
+__global__ void __launch_bounds__(256)
+split_h2_inplace_kernel(float* __restrict__ X, int64_t rows, int64_t cols, int64_t ld,
+                        const uint32_t* __restrict__ amax, int* __restrict__ e_out) {
+    extern __shared__ __align__(16) float srow[];
+    const int e = h2_exponent(*amax);
+    const float s = ldexpf(1.f, e);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *e_out = e;
+    const int64_t c4 = cols / 4;
+    for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
+        float* x = X + i * ld;
+        for (int64_t j = threadIdx.x; j < c4; j += blockDim.x)
+            reinterpret_cast<float4*>(srow)[j] = reinterpret_cast<const float4*>(x)[j];
+        for (int64_t j = c4 * 4 + threadIdx.x; j < cols; j += blockDim.x) srow[j] = x[j];
+        __syncthreads();
+        __half* hi = reinterpret_cast<__half*>(x);
+        __half* lo = hi + ld;
+        for (int64_t j = threadIdx.x; j < (cols + 3) / 4; j += blockDim.x) {
+            const int64_t k = 4 * j;
+            __half h[4], l[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (k + u < cols) h2_pair(srow[k + u], s, h[u], l[u]);
+                else h[u] = l[u] = __float2half_rn(0.f);
+            }
+            reinterpret_cast<uint2*>(hi)[j] = *reinterpret_cast<uint2*>(h);  // 8-byte stores
+            reinterpret_cast<uint2*>(lo)[j] = *reinterpret_cast<uint2*>(l);
+        }
+        __syncthreads();
+    }
+}
+
 // out (cols x rows, ldh) = split of X^T: 64 x 64 tiles through shared memory
 __global__ void __launch_bounds__(256)
 split_h2_t_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ld,
@@ -1286,6 +1320,32 @@ int h2_exponent(const float* X, int64_t rows, int64_t cols, int64_t ld, int32_t*
     return SKP_OK;
 }
 
+int split_h2_inplace(float* X, int64_t rows, int64_t cols, int64_t ld, int32_t* e,
+                     int have_amax, cudaStream_t st) {
+    if (rows == 0 || cols == 0) {
+        SKP_CUDA(cudaMemsetAsync(e, 0, 4, st));
+        return SKP_OK;
+    }
+    SKP_ARG((ld & 7) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && cols <= ld,
+            "split_h2_inplace: needs 16-byte aligned rows with ld %% 8 == 0");
+    SKP_ARG(cols * 4 <= 200 * 1024, "split_h2_inplace: row too long for shared memory");
+    uint32_t* amax = reinterpret_cast<uint32_t*>(e + 1);
+    if (!have_amax) {
+        SKP_CUDA(cudaMemsetAsync(amax, 0, 4, st));
+        const int64_t work = rows * cdiv(cols, 4);
+        const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(work, 256), (int64_t)h_sms * 16);
+        absmax_kernel<<<blocks, 256, 0, st>>>(X, rows, cols, ld, amax);
+        SKP_LAUNCHED(absmax_kernel);
+    }
+    const size_t smem = (size_t)cols * 4;
+    SKP_CUDA(cudaFuncSetAttribute(split_h2_inplace_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned blocks = (unsigned)std::min<int64_t>(rows, (int64_t)h_sms * 16);
+    split_h2_inplace_kernel<<<blocks, 256, smem, st>>>(X, rows, cols, ld, amax, e);
+    SKP_LAUNCHED(split_h2_inplace_kernel);
+    return SKP_OK;
+}
+
 int split_h2(const float* X, int64_t rows, int64_t cols, int64_t ld, int trans, void* hi, void* lo,
              int64_t ldh, int32_t* e, int have_amax, cudaStream_t st) {
     if (rows == 0 || cols == 0) {
@@ -1393,4 +1453,12 @@ extern "C" int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, f
     H3Emit em{Ct_hi, Ct_lo, ldct, shift, fixed, e_fixed, e_out, overflow};
     return gemm_h3_impl(transA, M, N, K, alpha, A_hi, A_lo, lda, a_exp, B_hi, B_lo, ldb, b_exp,
                         0.f, nullptr, 0, nullptr, 0, &em, SKP_STREAM(stream));
+}
+
+extern "C" int skp_split_h2_inplace_f32(float* X, int64_t rows, int64_t cols, int64_t ld,
+                                        int32_t* e, int32_t have_amax, void* stream) {
+    SKP_ARG(rows >= 0 && cols >= 0 && ld >= cols && ld >= 1 && e && (rows == 0 || cols == 0 || X),
+            "split_h2_inplace: bad arguments");
+    h_init();
+    return split_h2_inplace(X, rows, cols, ld, e, have_amax != 0, SKP_STREAM(stream));
 }

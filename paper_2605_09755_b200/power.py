@@ -187,7 +187,7 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     ph.mark("apply_right")
     # the power iteration's operand: A~ split once into fp16 hi/lo planes (the
     # fp32 A~ is released here; the footprint stays m x l x 4 bytes)
-    atil = be.prepare(atil, e_io)
+    atil = be.prepare(atil, e_io, inplace=True)
     ph.mark("split")
 
     def omega_for(perm_dev, host: bool = False):

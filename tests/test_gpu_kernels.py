@@ -324,6 +324,17 @@ def test_split_h2_roundtrip(ops, scale, trans):
     assert (err <= 2.0 ** -22 * src.abs() + 2.0 ** (-25 - e)).all()
 
 
+def test_split_h2_inplace_matches(ops):
+    g = torch.Generator(device="cuda").manual_seed(12)
+    x = ops.empty2d(301, 133, torch.float32, "cuda")
+    x.copy_(torch.randn(301, 133, generator=g, device="cuda") * 5e3)
+    ref = ops.split_h2(x)
+    sp = ops.split_h2_inplace(x)
+    assert int(sp.e[0].item()) == int(ref.e[0].item())
+    assert torch.equal(sp.hi, ref.hi[:, :133]) and torch.equal(sp.lo, ref.lo[:, :133])
+    assert sp.hi.data_ptr() == x.data_ptr() and sp.ld == 2 * x.stride(0)
+
+
 def test_split_h2_zero(ops):
     sp = ops.split_h2(torch.zeros(5, 9, device="cuda"))
     assert int(sp.e[0].item()) == 0
