@@ -257,7 +257,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     y = _ops.empty2d(rows, cfg["r2"], a.dtype, device)
     # the kernel the power iteration runs: 3xFP16 on the pre-split A~ where
     # the backend prepares it (fp32, tcgen05), else 3xTF32 / SIMT
-    pa = _ops.CudaBackend(device, a.dtype).prepare(atil)
+    pa = _ops.CudaBackend(device, a.dtype).prepare(atil, inplace=True)  # (A~ is not reused)
     h3 = isinstance(pa, _ops.SplitH2)
     if h3:
         sz = _ops.split_h2(z, trans=True)

@@ -426,29 +426,67 @@ inviter_kernel(const double* __restrict__ d, const double* __restrict__ e, int n
         st ^= st << 13; st ^= st >> 7; st ^= st << 17;
         Z[r * N + j] = 0.5 + (double)(st >> 11) * 0x1p-53;
     }
+    // The recurrences below are sequential in r, but their operands are not:
+    // each group of kIvG rows is loaded up front (independent loads in
+    // flight together) and then consumed -- one L2 round trip per group
+    // instead of per row (1.1 ms -> ~0.1 ms at n = 520).
+    constexpr int kIvG = 16;
     double scale = 1.0;
     for (int iter = 0; iter < 3; ++iter) {
         // forward: apply L^{-1} with the recorded interchanges (scale folded in)
         double carry = Z[j] * scale;
-        for (int r = 0; r < n - 1; ++r) {
-            double xr = carry, xn = Z[(r + 1) * N + j] * scale;
-            if (PV[r * N + j] != 0.0) { const double t = xr; xr = xn; xn = t; }
-            Z[r * N + j] = xr;
-            carry = xn - ML[r * N + j] * xr;
+        for (int r0 = 0; r0 < n - 1; r0 += kIvG) {
+            double zn[kIvG], pv[kIvG], ml[kIvG];
+#pragma unroll
+            for (int u = 0; u < kIvG; ++u) {
+                const int r = r0 + u;
+                if (r < n - 1) {
+                    zn[u] = Z[(r + 1) * N + j];
+                    pv[u] = PV[r * N + j];
+                    ml[u] = ML[r * N + j];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kIvG; ++u) {
+                const int r = r0 + u;
+                if (r < n - 1) {
+                    double xr = carry, xn = zn[u] * scale;
+                    if (pv[u] != 0.0) { const double t = xr; xr = xn; xn = t; }
+                    Z[r * N + j] = xr;
+                    carry = xn - ml[u] * xr;
+                }
+            }
         }
         Z[(N - 1) * N + j] = carry;
         // backward: U x = y, carrying x_{r+1}, x_{r+2}; sum of squares on the fly
         double x1 = 0.0, x2 = 0.0, nrm = 0.0;
-        for (int r = n - 1; r >= 0; --r) {
-            const double s0 = Z[r * N + j] - U2[r * N + j] * x1 - U3[r * N + j] * x2;
-            const double x = s0 * IU1[r * N + j];
-            Z[r * N + j] = x;
-            nrm += x * x;
-            x2 = x1;
-            x1 = x;
+        for (int r1 = n - 1; r1 >= 0; r1 -= kIvG) {
+            double zr[kIvG], u2[kIvG], u3[kIvG], iu[kIvG];
+#pragma unroll
+            for (int u = 0; u < kIvG; ++u) {
+                const int r = r1 - u;
+                if (r >= 0) {
+                    zr[u] = Z[r * N + j];
+                    u2[u] = U2[r * N + j];
+                    u3[u] = U3[r * N + j];
+                    iu[u] = IU1[r * N + j];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kIvG; ++u) {
+                const int r = r1 - u;
+                if (r >= 0) {
+                    const double x = (zr[u] - u2[u] * x1 - u3[u] * x2) * iu[u];
+                    Z[r * N + j] = x;
+                    nrm += x * x;
+                    x2 = x1;
+                    x1 = x;
+                }
+            }
         }
         scale = 1.0 / sqrt(nrm);
     }
+#pragma unroll 8
     for (int r = 0; r < n; ++r) Z[r * N + j] *= scale;
 }
 
