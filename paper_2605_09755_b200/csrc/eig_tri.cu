@@ -537,19 +537,34 @@ backtr_kernel(const double* __restrict__ Z, int n, const double* __restrict__ ta
         const int r = lane + 32 * m;
         x[m] = r < n ? Z[r * N + j] : 0.0;
     }
-    for (int i = n - 3; i >= 0; --i) {
-        const double t = tau[i];
-        if (t == 0.0) continue;
+    // software-pipelined: reflector i-1 is loaded while reflector i is applied
+    // (each load was an exposed L2 round trip per reflector: 455 us at n = 520)
+    double vn[M];
+    double tn = 0.0;
+    auto load = [&](int i) {
         const double* v = Hv + (int64_t)i * N;
-        double vv[M];
-        double dot = 0.0;
+        tn = __ldg(tau + i);
 #pragma unroll
         for (int m = 0; m < M; ++m) {
             const int r = lane + 32 * m;
-            vv[m] = (r > i && r < n) ? __ldg(v + r) : 0.0;
-            dot += vv[m] * x[m];
+            vn[m] = (r > i && r < n) ? __ldg(v + r) : 0.0;
         }
-        dot = warp_sum(dot) * t;
+    };
+    if (n >= 3) load(n - 3);
+    for (int i = n - 3; i >= 0; --i) {
+        double vv[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) vv[m] = vn[m];
+        const double t = tn;
+        if (i > 0) load(i - 1);
+        if (t == 0.0) continue;
+        double d0 = 0.0, d1 = 0.0;  // two chains: the fp64 FMA latency, not the rate
+#pragma unroll
+        for (int m = 0; m < M; m += 2) {
+            d0 += vv[m] * x[m];
+            if (m + 1 < M) d1 += vv[m + 1] * x[m + 1];
+        }
+        const double dot = warp_sum(d0 + d1) * t;
 #pragma unroll
         for (int m = 0; m < M; ++m) x[m] -= dot * vv[m];
     }
@@ -663,17 +678,18 @@ int syev_tri(const double* A, int64_t n, double* W, double* V, void* ws, int64_t
     const size_t bsm = 2 * (size_t)n * sizeof(double);
     SKP_CUDA(cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)std::max<size_t>(bsm, 1)));
-    bisect_kernel<<<(unsigned)cdiv(n, 8), 256, bsm, st>>>(d, e, nn, W, tnorm);
+    // 2 warps (eigenvalues) per block: the launch spreads over all SMs
+    bisect_kernel<<<(unsigned)cdiv(n, 2), 64, bsm, st>>>(d, e, nn, W, tnorm);
     SKP_LAUNCHED(bisect_kernel);
     inviter_kernel<<<(unsigned)cdiv(n, 32), 32, 0, st>>>(d, e, nn, W, tnorm, scr, Z);
     SKP_LAUNCHED(inviter_kernel);
     reorth_kernel<<<(unsigned)cdiv(n * 32, 256), 256, 0, st>>>(W, nn, tnorm, Z);
     SKP_LAUNCHED(reorth_kernel);
     {
-        const unsigned bgrid = (unsigned)cdiv(n * 32, 256);
-        if (n <= 32 * 17) backtr_kernel<17><<<bgrid, 256, 0, st>>>(Z, nn, tau, Hv, V);
-        else if (n <= 32 * kBtMaxM) backtr_kernel<kBtMaxM><<<bgrid, 256, 0, st>>>(Z, nn, tau, Hv, V);
-        else backtr_kernel_big<<<bgrid, 256, 0, st>>>(Z, nn, tau, Hv, bscr, V);
+        const unsigned bgrid = (unsigned)cdiv(n * 32, 64);  // 2 columns per block: all SMs
+        if (n <= 32 * 17) backtr_kernel<17><<<bgrid, 64, 0, st>>>(Z, nn, tau, Hv, V);
+        else if (n <= 32 * kBtMaxM) backtr_kernel<kBtMaxM><<<bgrid, 64, 0, st>>>(Z, nn, tau, Hv, V);
+        else backtr_kernel_big<<<bgrid, 64, 0, st>>>(Z, nn, tau, Hv, bscr, V);
         SKP_LAUNCHED(backtr_kernel);
     }
     if (sweeps) SKP_CUDA(cudaMemsetAsync(sweeps, 0, sizeof(int32_t), st));
