@@ -244,3 +244,55 @@ def test_lowrank_factorize(skp):
     assert abs(err - err_o) <= 1e-10 * err_o
     np.testing.assert_allclose(res.Y @ res.X, y_o @ x_o, atol=1e-9 * np.abs(a).max())
     assert set(res.elapsed) >= {"sketch", "power", "regression"}
+
+
+# test_power.py:47-64 -- choose_q (host arithmetic; same formula and messages)
+def test_choose_q(skp):
+    import math
+    for eps, m_hat in [(0.5, 1), (0.5, 1000), (0.1, 50), (0.25, 10**6)]:
+        assert skp.choose_q(eps, m_hat) == math.ceil(math.log(2 * m_hat) / (2 * eps))
+    qs = [skp.choose_q(e, 500) for e in (0.05, 0.1, 0.2, 0.5)]
+    assert qs == sorted(qs, reverse=True)
+    with pytest.raises(ValueError, match="eps"):
+        skp.choose_q(0.0, 10)
+    with pytest.raises(ValueError, match="m_hat"):
+        skp.choose_q(0.5, 0)
+
+
+# test_power.py:101-106 with the sketch kind that is new on the device path
+def test_exact_rank_capture_srht(skp):
+    a = random_lowrank(120, 90, 6, seed=21)
+    spec = skp.RangeFinderSpec(k=6, l=24, r1=24, r2=10, q=1, eps=0.5, sketch_kind="srht", seed=4)
+    qb = skp.range_finder_sketched(a, spec)
+    assert spectral_residual(a, qb) <= 1e-10 * np.linalg.norm(a, 2)
+
+
+# test_power.py:150-154 -- classical range finder on a diagonal matrix
+def test_classical_full_capture_diagonal(skp):
+    a = np.diag(np.arange(10.0, 0.0, -1.0))
+    qb = skp.range_finder_classical(a, k=10, r2=10, q=1, seed=3)
+    assert spectral_residual(a, qb) <= 1e-10
+
+
+# test_power.py:231-235 -- exact-rank recovery by the generalized Nystrom factorization
+@pytest.mark.parametrize("kind,s", [("countsketch", 2), ("gaussian", None), ("srht", None)])
+def test_lowrank_exact_rank_recovery(skp, kind, s):
+    a = random_lowrank(80, 60, 5, seed=8)
+    spec = skp.RangeFinderSpec(k=5, l=12, r1=12, r2=8, q=1, eps=0.5, sketch_kind=kind, seed=2,
+                               s=s)
+    res = skp.lowrank_factorize(a, spec)
+    assert np.linalg.norm(a - res.Y @ res.X) <= 1e-9 * np.linalg.norm(a)
+
+
+# test_power.py:259-266 and :294-300 -- exact-rank psd recovery, symmetric psd core
+def test_nystrom_exact_rank_and_core(skp):
+    v = datagen.haar_columns(70, 4, 9)
+    a = (v * np.array([4.0, 3.0, 2.0, 1.0])) @ v.T
+    a = (a + a.T) / 2
+    spec = skp.RangeFinderSpec(k=4, l=10, r1=10, r2=6, q=1, eps=0.5, seed=5, s=2)
+    res = skp.nystrom_psd(a, spec)
+    approx = res.C @ skp.pinv(res.W) @ res.C.T
+    assert np.linalg.norm(a - approx, 2) <= 1e-6 * np.linalg.norm(a, 2)
+    w_norm = np.linalg.norm(res.W, 2)
+    assert np.abs(res.W - res.W.T).max() <= 1e-8 * w_norm
+    assert np.linalg.eigvalsh(res.W).min() >= -1e-8 * w_norm
