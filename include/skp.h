@@ -97,8 +97,9 @@ int skp_sketch_right_f64(const double* A, int64_t lda, int64_t m, int64_t n,
  * skp_sketch_gather_plan_fail_offset(r) is 0 after the build -- or, without a
  * host check, run skp_sketch_gather_f32 anyway: with a failed plan it writes
  * nothing and adds 2^40 to *nonfinite (the caller then uses skp_sketch_right).
- * Requires
- * n <= 24576 and 16-byte aligned rows padded to a multiple of 4 floats;
+ * Requires n <= 98304 (rows wider than one 24576-column shared-memory buffer
+ * run as up to 4 column passes, each adding to the previous) and 16-byte
+ * aligned rows padded to a multiple of 4 floats;
  * returns SKP_ERR_UNSUPPORTED otherwise (callers keep skp_sketch_right).
  * amax (may be NULL): atomicMax of the bits of max |out| (for the 3xFP16
  * split of the output, skp_split_h2_f32 with have_amax = 1).
@@ -107,7 +108,7 @@ int skp_sketch_right_f64(const double* A, int64_t lda, int64_t m, int64_t n,
  * finite sum; fro2 (may be NULL) += ||A||_F^2 by a separate pass.
  * Replaces the same `a @ self._sparse` (sketching.py:158-164) inside
  * range_finder_sketched (power.py:141-154): Y = (A S) Omega = (A S P)(P^T Omega). */
-int64_t skp_sketch_gather_plan_bytes(int64_t r);
+int64_t skp_sketch_gather_plan_bytes(int64_t n, int64_t r);
 int64_t skp_sketch_gather_plan_fail_offset(int64_t r);
 int skp_sketch_gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n, int64_t r,
                            void* plan, int64_t plan_bytes, void* stream);

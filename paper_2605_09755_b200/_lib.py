@@ -41,7 +41,7 @@ SIGNATURES = {
                                 _i64, _vp]),
     "skp_gaussian_f64": (_int, [_u64, _u64, _u64, _u64, _i64, _i64, _f64, _vp, _i64, _vp, _vp,
                                 _i64, _vp]),
-    "skp_sketch_gather_plan_bytes": (_i64, [_i64]),
+    "skp_sketch_gather_plan_bytes": (_i64, [_i64, _i64]),
     "skp_sketch_gather_plan_fail_offset": (_i64, [_i64]),
     "skp_sketch_gather_plan": (_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "skp_sketch_gather_f32": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, ctypes.c_float, _vp, _i64,

@@ -143,13 +143,13 @@ GATHER_PLAN_FAIL_MARK = 1 << 40   # added to the non-finite counter by a failed 
 def gather_plan(colptr, entries, n: int, r: int, device, check: bool = True):
     """K2 v2 plan (once per sketch): (plan bytes on the device, perm or None).
 
-    None when the shape is outside the kernel (n > 24576).  With check=True the
+    None when the shape is outside the kernel (n > 98304).  With check=True the
     schedule is verified on the host (one sync; None if a column / warp needs
     more than 128 steps) and perm[v] (numpy) = the column written at position v.
     With check=False nothing is read back: a failed schedule surfaces as
     GATHER_PLAN_FAIL_MARK in the non-finite counter of sketch_gather."""
     lib = _lib.load()
-    nb = int(lib.skp_sketch_gather_plan_bytes(r))
+    nb = int(lib.skp_sketch_gather_plan_bytes(n, r))
     plan = torch.empty(nb, dtype=torch.uint8, device=device)
     rc = lib.skp_sketch_gather_plan(ptr(colptr), ptr(entries), n, r, ptr(plan), nb,
                                     stream_ptr(device))

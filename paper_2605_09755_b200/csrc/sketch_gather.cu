@@ -120,10 +120,18 @@ __device__ __forceinline__ void g_bulk_load_e(uint32_t dst, const void* src, uin
 // perm[pos] = the column written at position pos (compact: the first r
 // entries), -1 for pos in [r, P*kGCols).  One block per slice.
 constexpr int kGPrimary = 1 << 30;
+constexpr int kGMaxPass = 4;  // column passes: n <= 4 x 24576
+struct GSched {
+    int H;
+    uint32_t* sched[kGMaxPass];
+    int32_t* tw[kGMaxPass];
+};
 __global__ void __launch_bounds__(256)
-gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r, int width, int64_t slots,
+gather_sort_kernel(const int32_t* __restrict__ colptr, const int32_t* __restrict__ entries,
+                   int64_t r, int width, int64_t slots, int H, int npass,
                    int32_t* __restrict__ perm, int32_t* __restrict__ seg_beg,
-                   int32_t* __restrict__ seg_cnt, int32_t* __restrict__ lanepos) {
+                   int32_t* __restrict__ seg_cnt, int32_t* __restrict__ lanepos,
+                   int32_t* __restrict__ fail) {
     __shared__ int key[kGCols];        // column entry counts
     __shared__ int ucnt[kGCols];       // per-lane count of the column's unit
     __shared__ int order[kGCols];      // units in placement order (column index)
@@ -131,6 +139,9 @@ gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r, int width, int
     __shared__ int lane_part[kGCols];  // 0 single, 1 first half (primary), 2 second half
     __shared__ int hist[kGTMax + 2];
     __shared__ int s_cap;
+    // column passes (n > one row buffer): bnd[v][h] = first entry of column v
+    // with j >= h * npass (entries are ascending in j)
+    __shared__ int bnd[kGCols][kGMaxPass + 1];
     const int64_t c0 = (int64_t)blockIdx.x * width;
     const int nc = (int)(r - c0 < width ? r - c0 : width);
     const int lanes = kGCols;
@@ -143,7 +154,22 @@ gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r, int width, int
     if (blockIdx.x == 0)
         for (int64_t v = r + threadIdx.x; v < slots; v += blockDim.x) perm[v] = -1;
     __syncthreads();
-    for (int v = threadIdx.x; v < nc; v += blockDim.x) atomicAdd(&hist[min(key[v], kGTMax + 1)], 1);
+    for (int v = threadIdx.x; v < nc; v += blockDim.x) {
+        atomicAdd(&hist[min(key[v], kGTMax + 1)], 1);
+        const int b0 = colptr[c0 + v], b1 = colptr[c0 + v + 1];
+        bnd[v][0] = b0;
+        bnd[v][H] = b1;
+        for (int h = 1; h < H; ++h) {
+            const int jt = h * npass;
+            int lo = b0, hi = b1;  // first index with (entry & 0x7fffffff) >= jt
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if ((entries[mid] & 0x7fffffff) < jt) lo = mid + 1;
+                else hi = mid;
+            }
+            bnd[v][h] = lo;
+        }
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         long long tot = 0;
@@ -177,7 +203,12 @@ gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r, int width, int
         int pos = 0, hole = -1;
         for (int k = 0; k < nc; ++k) {
             const int v = order[k];
-            if (key[v] > cap) {
+            const bool pair = key[v] > cap;
+            if (pair ? pos + 2 + (pos & 1) > lanes : (hole < 0 && pos >= lanes)) {
+                atomicOr(fail, 1);  // lanes exhausted (mean count near kGTMax): no plan
+                break;
+            }
+            if (pair) {
                 if (pos & 1) {  // keep the pair on (2k, 2k+1): skip a lane
                     if (hole < 0) hole = pos;
                     ++pos;
@@ -201,23 +232,24 @@ gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r, int width, int
         for (int l = 0; l < lanes; ++l) {
             const int v = lane_col[l];
             const int64_t g = (int64_t)blockIdx.x * kGCols + l;
+            const int64_t pstride = slots;  // per-pass table stride (P * kGCols)
             if (v < 0) {
-                seg_beg[g] = 0;
-                seg_cnt[g] = 0;
+                for (int h = 0; h < H; ++h) {
+                    seg_beg[h * pstride + g] = 0;
+                    seg_cnt[h * pstride + g] = 0;
+                }
                 lanepos[g] = -1;
                 continue;
             }
             const int beg = colptr[c0 + v], cnt = key[v];
             const int half = (cnt + 1) / 2;
-            if (lane_part[l] == 0) {
-                seg_beg[g] = beg;
-                seg_cnt[g] = cnt;
-            } else if (lane_part[l] == 1) {
-                seg_beg[g] = beg;
-                seg_cnt[g] = half;
-            } else {
-                seg_beg[g] = beg + half;
-                seg_cnt[g] = cnt - half;
+            // this lane's part of the column, intersected with each pass's j range
+            const int pb = lane_part[l] == 2 ? beg + half : beg;
+            const int pe = lane_part[l] == 1 ? beg + half : beg + cnt;
+            for (int h = 0; h < H; ++h) {
+                const int sb = max(pb, bnd[v][h]), se = min(pe, bnd[v][h + 1]);
+                seg_beg[h * pstride + g] = sb;
+                seg_cnt[h * pstride + g] = max(0, se - sb);
             }
             if (lane_part[l] == 2) {
                 lanepos[g] = -1;
@@ -242,15 +274,20 @@ gather_sort_kernel(const int32_t* __restrict__ colptr, int64_t r, int width, int
 // without an entry read a zero word in a distinct free bank.
 __global__ void __launch_bounds__(128)
 gather_sched_kernel(const int32_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_cnt,
-                    const int32_t* __restrict__ entries, int nwarps, int64_t n,
-                    uint32_t* __restrict__ sched, int32_t* __restrict__ tw,
-                    int32_t* __restrict__ fail) {
-    const int wg = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+                    const int32_t* __restrict__ entries, int nwarps, int64_t n, int npass,
+                    GSched ps, int32_t* __restrict__ fail) {
+    const int wg_all = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
-    if (wg >= nwarps) return;
-    const uint32_t zero_word = (uint32_t)((n + 31) / 32 * 32);  // 32 zero words after the row
-    const int beg = seg_beg[(int64_t)wg * 32 + lane];   // this lane's (half-)column
-    const int cnt = seg_cnt[(int64_t)wg * 32 + lane];
+    if (wg_all >= nwarps * ps.H) return;
+    const int h = wg_all / nwarps, wg = wg_all % nwarps;      // column pass, warp
+    const uint32_t j0 = (uint32_t)(h * npass);
+    const int64_t nh = std::min<int64_t>(npass, n - j0);
+    uint32_t* sched = ps.sched[h];
+    int32_t* tw = ps.tw[h];
+    const uint32_t zero_word = (uint32_t)((nh + 31) / 32 * 32);  // 32 zero words after the row
+    const int64_t ti = (int64_t)h * nwarps * 32 + (int64_t)wg * 32 + lane;
+    const int beg = seg_beg[ti];   // this lane's (half-)column, this pass's j range
+    const int cnt = seg_cnt[ti];
     if (__any_sync(0xffffffffu, cnt > kGTMax)) {
         if (lane == 0) {
             atomicOr(fail, 1);
@@ -285,7 +322,7 @@ gather_sched_kernel(const int32_t* __restrict__ seg_beg, const int32_t* __restri
         const uint32_t v = ent[bptr[bk]++];
         if (bptr[bk] == bstart[bk + 1]) avail &= ~(1u << bk);
         --rem;
-        return ((v & 0x7fffffffu) * 4u) | (v & 0x80000000u);
+        return (((v & 0x7fffffffu) - j0) * 4u) | (v & 0x80000000u);
     };
     int t = 0;
     while (__any_sync(0xffffffffu, rem > 0) || (t & 3)) {
@@ -348,12 +385,13 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
                      const int32_t* __restrict__ lanepos, int P, const uint32_t* __restrict__ sched,
                      const int32_t* __restrict__ tw, const int32_t* __restrict__ plan_fail,
                      float scale, float* __restrict__ out, int64_t ldo,
-                     int64_t* nonfinite, uint32_t* __restrict__ amax) {
+                     int64_t* nonfinite, uint32_t* __restrict__ amax, int accumulate,
+                     int mark_fail) {
     extern __shared__ __align__(128) unsigned char sm[];
     if (*plan_fail) {
         // the plan's schedule overflowed: report it through the non-finite
         // counter (the caller re-runs with K2 v1; no host sync at plan time)
-        if (blockIdx.x == 0 && threadIdx.x == 0 && nonfinite)
+        if (blockIdx.x == 0 && threadIdx.x == 0 && nonfinite && mark_fail)
             atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), kGPlanFailMark);
         return;
     }
@@ -456,7 +494,8 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
         const float part = __shfl_down_sync(0xffffffffu, acc, 1);
         if (primary) acc += part;
         if (valid) {
-            const float o = acc * scale;
+            // column passes after the first add to what the earlier ones wrote
+            const float o = accumulate ? fmaf(acc, scale, out[i * ldo + v_out]) : acc * scale;
             bad |= !isfinite(o);
             mx = max(mx, __float_as_uint(fabsf(o)));
             out[i * ldo + v_out] = o;
@@ -485,9 +524,10 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
 
 }  // namespace
 
-// plan layout (bytes): perm int32[P*kGCols] | tw int32[P*kGW] | fail int32 |
-//                      pad to 16 | sched uint32[P*kGW*kGTMax*32] |
-//                      seg_beg, seg_cnt, lanepos int32[P*kGCols] each
+// plan layout (bytes): perm int32[P*kGCols] | fail int32 | pad to 16 |
+//   per column pass h < H: tw int32[P*kGW] (padded to 16) | sched uint32[P*kGW*kGTMax*32]
+//   | seg_beg int32[H][P*kGCols] | seg_cnt int32[H][P*kGCols] | lanepos int32[P*kGCols]
+// H = ceil(n / 24576) column passes of npass (a multiple of 32) columns each.
 int gather_slices(int64_t r) { return (int)cdiv(r, (int64_t)kGCols); }
 // balanced slice width: the P slices share the r columns evenly (multiple of
 // 32), so no CTA carries a short last slice while its SM idles (C3: 6 x 672
@@ -495,46 +535,70 @@ int gather_slices(int64_t r) { return (int)cdiv(r, (int64_t)kGCols); }
 int gather_width(int64_t r) {
     return (int)(cdiv(cdiv(r, (int64_t)gather_slices(r)), 32) * 32);
 }
-int64_t gather_plan_bytes(int64_t r) {
-    const int64_t P = gather_slices(r);
-    const int64_t head = (P * kGCols + P * kGW + 1) * 4;
-    return (head + 15) / 16 * 16 + P * kGW * kGTMax * 32 * 4 + 3 * P * kGCols * 4;
+int gather_passes(int64_t n) { return (int)cdiv(n, (int64_t)(kGBufWords - 32)); }
+int gather_npass(int64_t n) {
+    return (int)(cdiv(cdiv(n, (int64_t)gather_passes(n)), 32) * 32);
 }
-// the lane tables after the schedule: seg_beg | seg_cnt | lanepos (P*kGCols each)
-int32_t* gather_lane_tables(void* plan, int64_t r) {
-    const int64_t P = gather_slices(r);
-    const int64_t head = (P * kGCols + P * kGW + 1) * 4;
-    return reinterpret_cast<int32_t*>(reinterpret_cast<char*>(plan) + (head + 15) / 16 * 16 +
-                                      P * kGW * kGTMax * 32 * 4);
+
+struct GLayout {
+    int P, H, npass;
+    int32_t* perm;
+    int32_t* fail;
+    GSched ps;
+    int32_t* seg_beg;
+    int32_t* seg_cnt;
+    int32_t* lanepos;
+    int64_t bytes;
+};
+GLayout gather_layout(void* plan, int64_t n, int64_t r) {
+    GLayout L;
+    L.P = gather_slices(r);
+    L.H = gather_passes(n);
+    L.npass = gather_npass(n);
+    char* b = reinterpret_cast<char*>(plan);
+    int64_t off = 0;
+    auto take = [&](int64_t bytes) {
+        char* p = b ? b + off : nullptr;
+        off += (bytes + 15) / 16 * 16;
+        return p;
+    };
+    L.perm = reinterpret_cast<int32_t*>(take((int64_t)L.P * kGCols * 4));
+    L.fail = reinterpret_cast<int32_t*>(take(4));
+    L.ps.H = L.H;
+    for (int h = 0; h < kGMaxPass; ++h) {
+        L.ps.tw[h] = nullptr;
+        L.ps.sched[h] = nullptr;
+    }
+    for (int h = 0; h < L.H && h < kGMaxPass; ++h) {
+        L.ps.tw[h] = reinterpret_cast<int32_t*>(take((int64_t)L.P * kGW * 4));
+        L.ps.sched[h] = reinterpret_cast<uint32_t*>(take((int64_t)L.P * kGW * kGTMax * 32 * 4));
+    }
+    L.seg_beg = reinterpret_cast<int32_t*>(take((int64_t)L.H * L.P * kGCols * 4));
+    L.seg_cnt = reinterpret_cast<int32_t*>(take((int64_t)L.H * L.P * kGCols * 4));
+    L.lanepos = reinterpret_cast<int32_t*>(take((int64_t)L.P * kGCols * 4));
+    L.bytes = off;
+    return L;
 }
+int64_t gather_plan_bytes(int64_t n, int64_t r) { return gather_layout(nullptr, n, r).bytes; }
 
 int gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n, int64_t r, void* plan,
                 int64_t plan_bytes, cudaStream_t st) {
     SKP_ARG(n >= 1 && r >= 1 && plan, "sketch_gather_plan: bad sizes");
-    SKP_ARG(plan_bytes >= gather_plan_bytes(r), "sketch_gather_plan: plan buffer too small");
-    if (n > kGBufWords - 32) {
-        set_error("unsupported: sketch_gather needs n <= %d", kGBufWords - 32);
+    if (gather_passes(n) > kGMaxPass) {
+        set_error("unsupported: sketch_gather needs n <= %d", kGMaxPass * (kGBufWords - 32));
         return SKP_ERR_UNSUPPORTED;
     }
-    const int P = gather_slices(r);
-    int32_t* perm = reinterpret_cast<int32_t*>(plan);
-    int32_t* tw = perm + (int64_t)P * kGCols;
-    int32_t* fail = tw + (int64_t)P * kGW;
-    const int64_t head = ((int64_t)P * kGCols + P * kGW + 1) * 4;
-    uint32_t* sched =
-        reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(plan) + (head + 15) / 16 * 16);
-    SKP_CUDA(cudaMemsetAsync(fail, 0, 4, st));
+    SKP_ARG(plan_bytes >= gather_plan_bytes(n, r), "sketch_gather_plan: plan buffer too small");
+    const GLayout L = gather_layout(plan, n, r);
+    SKP_CUDA(cudaMemsetAsync(L.fail, 0, 4, st));
     const int width = gather_width(r);
-    int32_t* lt = gather_lane_tables(plan, r);
-    int32_t* seg_beg = lt;
-    int32_t* seg_cnt = lt + (int64_t)P * kGCols;
-    int32_t* lanepos = lt + 2 * (int64_t)P * kGCols;
-    gather_sort_kernel<<<P, 256, 0, st>>>(colptr, r, width, (int64_t)P * kGCols, perm, seg_beg,
-                                          seg_cnt, lanepos);
+    gather_sort_kernel<<<L.P, 256, 0, st>>>(colptr, entries, r, width, (int64_t)L.P * kGCols, L.H,
+                                            L.npass, L.perm, L.seg_beg, L.seg_cnt, L.lanepos,
+                                            L.fail);
     SKP_LAUNCHED(gather_sort_kernel);
-    const int nw = P * kGW;
-    gather_sched_kernel<<<(unsigned)cdiv(nw, 4), 128, 0, st>>>(seg_beg, seg_cnt, entries, nw, n,
-                                                                sched, tw, fail);
+    const int nw = L.P * kGW;
+    gather_sched_kernel<<<(unsigned)cdiv((int64_t)nw * L.H, 4), 128, 0, st>>>(
+        L.seg_beg, L.seg_cnt, entries, nw, n, L.npass, L.ps, L.fail);
     SKP_LAUNCHED(gather_sched_kernel);
     return SKP_OK;
 }
@@ -543,31 +607,32 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
                       const void* plan, float scale, float* out, int64_t ldo, double* fro2,
                       int64_t* nonfinite, uint32_t* amax, cudaStream_t st) {
     SKP_ARG(m >= 0 && n >= 1 && r >= 1 && ldo >= r, "sketch_gather: bad sizes");
-    if (n > kGBufWords - 32 || (reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3) ||
+    if (gather_passes(n) > kGMaxPass || (reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3) ||
         lda < (n + 3) / 4 * 4) {
         set_error("unsupported: sketch_gather needs n <= %d and 16-byte aligned, padded rows",
-                  kGBufWords - 32);
+                  kGMaxPass * (kGBufWords - 32));
         return SKP_ERR_UNSUPPORTED;
     }
     if (m == 0) return SKP_OK;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int P = gather_slices(r);
+    const GLayout L = gather_layout(const_cast<void*>(plan), n, r);
+    const int P = L.P;
     const int G = std::max(1, std::min<int>(sms / P, (int)std::min<int64_t>(m, 1 << 20)));
-    const int32_t* tw = reinterpret_cast<const int32_t*>(plan) + (int64_t)P * kGCols;
-    const int32_t* pfail = tw + (int64_t)P * kGW;
-    const int64_t head = ((int64_t)P * kGCols + P * kGW + 1) * 4;
-    const uint32_t* sched = reinterpret_cast<const uint32_t*>(
-        reinterpret_cast<const char*>(plan) + (head + 15) / 16 * 16);
     SKP_CUDA(cudaFuncSetAttribute(sketch_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kGSmem));
-    const int32_t* lanepos =
-        gather_lane_tables(const_cast<void*>(plan), r) + 2 * (int64_t)P * kGCols;
-    sketch_gather_kernel<<<G * P, kGThreads, kGSmem, st>>>(A, lda, m, n, lanepos, P, sched, tw,
-                                                           pfail, scale, out, ldo, nonfinite,
-                                                           amax);
-    SKP_LAUNCHED(sketch_gather_kernel);
+    // one launch per column pass: pass h gathers A[:, h*npass ...] and adds
+    // to what the earlier passes wrote; the checks ride on the last pass
+    for (int h = 0; h < L.H; ++h) {
+        const int64_t j0 = (int64_t)h * L.npass, nh = std::min<int64_t>(L.npass, n - j0);
+        const bool last = h + 1 == L.H;
+        sketch_gather_kernel<<<G * P, kGThreads, kGSmem, st>>>(
+            A + j0, lda, m, nh, L.lanepos, P, L.ps.sched[h], L.ps.tw[h], L.fail, scale, out, ldo,
+            last ? nonfinite : (h == 0 ? nonfinite : nullptr), last ? amax : nullptr, h > 0,
+            h == 0);
+        SKP_LAUNCHED(sketch_gather_kernel);
+    }
     if (fro2) {  // ||A||_F^2: a separate HBM-bound pass (only when asked for)
         const int rc = skp_sumsq_f32(A, m, n, lda, fro2, nullptr, st);
         if (rc != SKP_OK) return rc;
@@ -579,10 +644,11 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
 
 using namespace skp;
 
-extern "C" int64_t skp_sketch_gather_plan_bytes(int64_t r) { return gather_plan_bytes(r); }
+extern "C" int64_t skp_sketch_gather_plan_bytes(int64_t n, int64_t r) {
+    return gather_plan_bytes(n, r);
+}
 extern "C" int64_t skp_sketch_gather_plan_fail_offset(int64_t r) {
-    const int64_t P = gather_slices(r);
-    return (P * kGCols + P * kGW) * 4;
+    return (int64_t)gather_slices(r) * kGCols * 4;
 }
 extern "C" int skp_sketch_gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n,
                                       int64_t r, void* plan, int64_t plan_bytes, void* stream) {

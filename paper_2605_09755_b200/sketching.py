@@ -153,7 +153,7 @@ class SketchOperator:
     def right_permuted(self, a: torch.Tensor, out=None, fro2=None, nonfinite=None,
                        deferred: bool = False, amax=None):
         """(a @ S P, perm) with perm[v] (int32, on the device) = the column of
-        a @ S at position v, via the row-gather kernel (fp32, n <= 24576); None
+        a @ S at position v, via the row-gather kernel (fp32, n <= 98304); None
         when it does not apply.  deferred=True skips the plan's host check: a
         failed schedule then adds _ops.GATHER_PLAN_FAIL_MARK to *nonfinite
         (required) and writes nothing -- the caller falls back to right().

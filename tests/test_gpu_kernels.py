@@ -169,7 +169,8 @@ def test_sketch_fused_norm_and_nonfinite(skp, ops):
 
 
 @pytest.mark.parametrize("m,n,r,s", [(67, 16384, 4000, 8), (5, 1000, 300, 8), (130, 513, 64, 1),
-                                     (40, 2050, 1600, 3), (1, 24576, 4000, 8)])
+                                     (40, 2050, 1600, 3), (1, 24576, 4000, 8),
+                                     (9, 32768, 4000, 8), (3, 70001, 6000, 4)])
 def test_sketch_gather_permuted(skp, ops, m, n, r, s):
     """K2 v2: (A S) P from the row-gather kernel == the oracle's A S with its
     columns taken in plan order; fused fp64 ||A||_F^2 and the non-finite test."""
@@ -207,7 +208,7 @@ def test_sketch_gather_permuted(skp, ops, m, n, r, s):
 def test_sketch_gather_declines_outside_its_envelope(skp, ops):
     """No plan (and right_permuted -> None, the caller keeps K2 v1) when rows do
     not fit the smem row buffer or a column needs more than 128 steps."""
-    assert skp.make_sketch("countsketch", 24577, 4000, seed=1, s=8).gather_plan() is None
+    assert skp.make_sketch("countsketch", 98305, 4000, seed=1, s=8).gather_plan() is None
     op = skp.make_sketch("countsketch", 4096, 64, seed=1, s=8)     # ~512 entries per column
     assert op.gather_plan() is None
     t = ops.empty2d(3, 4096, torch.float32, "cuda").zero_()
