@@ -39,6 +39,9 @@ struct CIShared {
     double b[CB][CB + 1];
     double c[CB][CB + 1];
     double e[CB][CB + 1];
+    double xpp[CB][CB + 1];  // CTA 0: L_pp^{-1} of its last factorisation (no reload)
+    double dmn, dmx;         // CTA 0: running pivot range (written to dinfo at the end)
+    int info0;               // CTA 0: first failing pivot
     double invd[CB];
     int bad;
 };
@@ -237,33 +240,35 @@ cholinv_kernel(const double* __restrict__ G, int n, int64_t ldg, int nb, double 
             __syncthreads();
             const int bad = tile_chol_inv(sh.a, sh.b, sh.c, sh.invd, &mn, &mx);
             if (threadIdx.x == 0) {
+                // (pivot bookkeeping in shared memory: a global read here was a
+                // round trip on the per-panel critical path)
                 const int p0 = p * CB;
-                if (bad && *info == 0) *info = p0 + bad;
+                if (bad && sh.info0 == 0) sh.info0 = p0 + bad;
                 // pivots of the identity padding are 1: count only real rows
-                double dmn = dinfo[0], dmx = dinfo[1];
                 if (p0 < n) {
                     if (p0 + CB <= n) {
-                        dmn = fmin(dmn, mn);
-                        dmx = fmax(dmx, mx);
+                        sh.dmn = fmin(sh.dmn, mn);
+                        sh.dmx = fmax(sh.dmx, mx);
                     } else {
                         for (int k = 0; p0 + k < n; ++k) {
-                            dmn = fmin(dmn, sh.a[k][k]);
-                            dmx = fmax(dmx, sh.a[k][k]);
+                            sh.dmn = fmin(sh.dmn, sh.a[k][k]);
+                            sh.dmx = fmax(sh.dmx, sh.a[k][k]);
                         }
                     }
                 }
-                dinfo[0] = dmn;
-                dinfo[1] = dmx;
             }
         }
         __syncthreads();
+        for (int q = threadIdx.x; q < CB * CB; q += blockDim.x)
+            sh.xpp[q / CB][q % CB] = sh.b[q / CB][q % CB];
         tstore(Lb, p * CB, p * CB, sh.a);
         tstore(X, p * CB, p * CB, sh.b);
     };
     if (blockIdx.x == 0) {
         if (threadIdx.x == 0) {
-            dinfo[0] = INFINITY;
-            dinfo[1] = 0.0;
+            sh.dmn = INFINITY;
+            sh.dmx = 0.0;
+            sh.info0 = 0;
         }
         tload(sh.c, A, 0, 0);
         factor(0, sh.c);
@@ -288,8 +293,15 @@ cholinv_kernel(const double* __restrict__ G, int n, int64_t ldg, int nb, double 
                 // remap so task 0 is the lookahead tile (p+1, p+1): tile order
                 // (0,0),(1,0),(1,1),... -> (I, J) relative to p+1
                 const int I0 = (p + 1 + I) * CB, J0 = (p + 1 + J) * CB;
-                // all operand tiles in flight at once (one global round trip)
-                tload(sh.b, X, p0, p0);                 // L_pp^{-1}
+                // all operand tiles in flight at once (one global round trip);
+                // CTA 0 factored L_pp itself and still holds its inverse (its
+                // later tasks of this panel run after factor(p+1) replaced it)
+                if (t == 0) {
+                    for (int q = threadIdx.x; q < CB * CB; q += blockDim.x)
+                        sh.b[q / CB][q % CB] = sh.xpp[q / CB][q % CB];
+                } else {
+                    tload(sh.b, X, p0, p0);             // L_pp^{-1}
+                }
                 tload(sh.a, A, I0, p0);                 // A_Ip
                 if (I != J) tload(sd, A, J0, p0);       // A_Jp
                 tload(sh.e, A, I0, J0);                 // A_IJ
@@ -328,7 +340,12 @@ cholinv_kernel(const double* __restrict__ G, int n, int64_t ldg, int nb, double 
         }
     }
     grid.sync();
-    if (gtid == 0 && *info == 0 && dinfo[0] < rel_tol * dinfo[1]) *info = -1;
+    if (gtid == 0) {
+        dinfo[0] = sh.dmn;
+        dinfo[1] = sh.dmx;
+        if (sh.info0 != 0 && *info == 0) *info = sh.info0;
+        else if (*info == 0 && sh.dmn < rel_tol * sh.dmx) *info = -1;
+    }
 }
 
 __global__ void unpad_kernel(const double* __restrict__ Xp, int np, int n, double* __restrict__ X) {

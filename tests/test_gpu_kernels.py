@@ -448,7 +448,7 @@ def _spd(n, cond=1e4, seed=0):
     return (q * w) @ q.T
 
 
-@pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 130, 520])
+@pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 130, 520, 1050])
 def test_cholesky_and_trinv(n):
     from paper_2605_09755_b200 import _lib
     from paper_2605_09755_b200._ops import ptr
