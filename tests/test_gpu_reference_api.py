@@ -158,6 +158,29 @@ def test_seed_determinism(skp):
     np.testing.assert_array_equal(q1, q2)
 
 
+# SPEC.md:103-104 / bench.py:397-403: pure functions, safe to call from
+# ThreadPoolExecutor workers at once; results identical to sequential calls
+def test_concurrent_calls_match_sequential(skp):
+    from concurrent.futures import ThreadPoolExecutor
+    cases = []
+    for i in range(6):
+        a = gen_polydecay(300 + 40 * i, 120, seed=30 + i).astype(np.float32 if i % 2 else np.float64)
+        spec = skp.RangeFinderSpec(k=8, l=40, r1=60, r2=16, q=2, eps=0.5, seed=7 + i, s=3)
+        cases.append((a, spec))
+
+    def run(case):
+        a, spec = case
+        qb = skp.range_finder_sketched(a, spec)
+        return qb, skp.randsvd(a, qb).sigma
+
+    seq = [run(c) for c in cases]
+    with ThreadPoolExecutor(max_workers=6) as pool:
+        par = list(pool.map(run, cases * 2))
+    for i, (qb, sig) in enumerate(par):
+        np.testing.assert_array_equal(qb, seq[i % len(cases)][0])
+        np.testing.assert_array_equal(sig, seq[i % len(cases)][1])
+
+
 def test_classical_equals_identity_sketch(skp):
     a = gen_polydecay(70, 40, seed=9)
     q1 = skp.range_finder_classical(a, k=5, r2=10, q=2, seed=3)
