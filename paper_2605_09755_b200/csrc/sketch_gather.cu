@@ -12,13 +12,13 @@
 //
 // Bank conflicts: the 32 lanes of a warp load 32 data-dependent words of the
 // row; the order of each lane's entries is scheduled offline (per sketch, on
-// the device) so that at every step the warp touches 32 distinct banks -- a
-// greedy edge colouring of the lane x bank multigraph, lanes with the most
-// remaining entries served first (a lane that would otherwise lengthen the
-// schedule accepts a conflict).  Lanes without an entry at a step read a zero
-// word in a free bank.  Columns are sorted by entry count inside each slice,
-// so the 32 lanes of a warp need about the same number of steps (C3: ~34
-// steps for ~33 entries).  The sort permutes the OUTPUT COLUMNS: the kernel
+// the device) so that at every step the warp touches 32 distinct banks -- an
+// edge colouring of the lane x bank multigraph (plan 2) in as many steps as
+// the busiest lane has entries; a bank with more entries than that meets
+// itself in a few steps (2-way conflicts).  Lanes without an entry at a step
+// read a zero word in a free bank.  Columns are sorted by entry count inside
+// each slice, so the 32 lanes of a warp carry about the same number of
+// entries.  The sort permutes the OUTPUT COLUMNS: the kernel
 // writes A~ P, and the range finder multiplies by P^T Omega instead of Omega
 // (Y = A~ Omega = (A~ P)(P^T Omega)); apply_right keeps K2 v1's column order.
 //
@@ -262,121 +262,161 @@ gather_sort_kernel(const int32_t* __restrict__ colptr, const int32_t* __restrict
     }
 }
 
-// ---- plan 2: greedy bank-conflict-free step schedule, one WARP per warp ------
+// ---- plan 2: step schedule, one block per warp schedule ----------------------
 // sched[(wg*kGTMax + t)*32 + lane] = byte offset into the row buffer (bit 31:
-// negate); tw[wg] = steps (a multiple of 4); fail |= 1 when a column or a
-// warp needs more than kGTMax steps (the caller then keeps K2 v1).
-// Per step: rounds in which every unserved lane proposes the bank of its first
-// unscheduled entry whose bank is still free; per bank the lane with the most
-// remaining entries wins (ties: lower lane).  Then critical lanes (as many
-// remaining entries as the warp maximum) take an entry even if its bank is
-// taken (a 2-way conflict rather than a longer schedule), and lanes left
-// without an entry read a zero word in a distinct free bank.
-__global__ void __launch_bounds__(128)
+// negate); tw[wg] = steps (a multiple of 4); fail |= 1 when a warp needs more
+// than kGTMax steps (the caller then keeps K2 v1).
+// The warp's entries are the edges of a bipartite multigraph lanes x banks
+// (bank = column index mod 32); a step is a set of edges with each lane at most
+// once, and its shared-memory wavefronts are the most lanes on one bank.  The
+// warp must take L = (most entries on one lane) steps; a bank with more than L
+// entries is split into virtual banks of <= L entries each, and the graph
+// lanes x virtual banks is coloured with exactly L colours (Koenig's theorem):
+// L steps, and a 2-way conflict only where both halves of an overloaded bank
+// meet in one step (C3: ~1.1 wavefronts per LDS; a greedy colouring measured
+// 2.47, and a conflict-free colouring needs max(L, bank degree) steps -- 30%
+// more, and slower).
+// Colouring (one thread; ~1000 edges per warp): an edge takes a colour free at
+// both ends; otherwise, with a free at its lane and b free at its bank, the
+// a/b alternating path from the bank is swapped first (it cannot reach the
+// lane: bipartite), which frees a at the bank.  Lanes idle at a step read a
+// zero word in a distinct unused bank.
+constexpr int kGCW = kGTMax / 32;  // colour mask words
+constexpr int kGVB = 4;            // virtual banks per bank
+__device__ __forceinline__ int g_first_free(const uint32_t* m0, const uint32_t* m1, int lim) {
+#pragma unroll
+    for (int w = 0; w < kGCW; ++w) {
+        const uint32_t f = ~(m0[w] | (m1 ? m1[w] : 0u));
+        if (f) {
+            const int c = w * 32 + __ffs(f) - 1;
+            return c < lim ? c : -1;
+        }
+    }
+    return -1;
+}
+__global__ void __launch_bounds__(32)
 gather_sched_kernel(const int32_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_cnt,
                     const int32_t* __restrict__ entries, int nwarps, int64_t n, int npass,
                     GSched ps, int32_t* __restrict__ fail) {
-    const int wg_all = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (wg_all >= nwarps * ps.H) return;
-    const int h = wg_all / nwarps, wg = wg_all % nwarps;      // column pass, warp
+    __shared__ uint8_t lane_bank[32][kGTMax];        // virtual bank of lane at colour c (0xff: none)
+    __shared__ uint8_t bank_lane[32 * kGVB][kGTMax];  // lane on virtual bank at colour c
+    __shared__ uint32_t val[32][kGTMax];              // the entry at (lane, colour)
+    __shared__ uint32_t lmask[32][kGCW], bmask[32 * kGVB][kGCW];  // colours in use
+    __shared__ int bdeg[32], bfill[32], sbeg[32], scnt[32];
+    const int lane = threadIdx.x;
+    const int h = blockIdx.x / nwarps, wg = blockIdx.x % nwarps;  // column pass, warp
     const uint32_t j0 = (uint32_t)(h * npass);
     const int64_t nh = std::min<int64_t>(npass, n - j0);
     uint32_t* sched = ps.sched[h];
     int32_t* tw = ps.tw[h];
     const uint32_t zero_word = (uint32_t)((nh + 31) / 32 * 32);  // 32 zero words after the row
     const int64_t ti = (int64_t)h * nwarps * 32 + (int64_t)wg * 32 + lane;
-    const int beg = seg_beg[ti];   // this lane's (half-)column, this pass's j range
+    const int beg = seg_beg[ti];  // this lane's (half-)column, this pass's j range
     const int cnt = seg_cnt[ti];
-    if (__any_sync(0xffffffffu, cnt > kGTMax)) {
+    sbeg[lane] = beg;
+    scnt[lane] = cnt;
+    bdeg[lane] = bfill[lane] = 0;
+    for (int c = 0; c < kGTMax; ++c) {
+        lane_bank[lane][c] = 0xff;
+#pragma unroll
+        for (int k = 0; k < kGVB; ++k) bank_lane[lane + 32 * k][c] = 0xff;
+    }
+#pragma unroll
+    for (int w = 0; w < kGCW; ++w) {
+        lmask[lane][w] = 0u;
+#pragma unroll
+        for (int k = 0; k < kGVB; ++k) bmask[lane + 32 * k][w] = 0u;
+    }
+    __syncwarp();
+    for (int k = 0; k < cnt; ++k) atomicAdd(&bdeg[(uint32_t)entries[beg + k] & 31u], 1);
+    __syncwarp();
+    int L = cnt, B = bdeg[lane];
+    for (int o = 16; o; o >>= 1) {
+        L = max(L, __shfl_xor_sync(0xffffffffu, L, o));
+        B = max(B, __shfl_xor_sync(0xffffffffu, B, o));
+    }
+    const int T = (L + 3) & ~3;
+    if (T > kGTMax || B > kGVB * L) {
         if (lane == 0) {
             atomicOr(fail, 1);
             tw[wg] = 0;
         }
         return;
     }
-    // this lane's entries bucketed by bank (counting sort, local memory)
-    uint32_t ent[kGTMax];
-    uint8_t bstart[33], bptr[32];
-    {
-        uint8_t bc[32];
-        for (int b = 0; b < 32; ++b) bc[b] = 0;
-        for (int k = 0; k < cnt; ++k) ++bc[(uint32_t)entries[beg + k] & 31u];
-        int acc = 0;
-        for (int b = 0; b < 32; ++b) {
-            bstart[b] = (uint8_t)acc;
-            bptr[b] = (uint8_t)acc;
-            acc += bc[b];
+    if (lane == 0) {
+        auto put = [&](int l, int b, int c, uint32_t v) {
+            lane_bank[l][c] = (uint8_t)b;
+            bank_lane[b][c] = (uint8_t)l;
+            val[l][c] = v;
+            lmask[l][c >> 5] |= 1u << (c & 31);
+            bmask[b][c >> 5] |= 1u << (c & 31);
+        };
+        auto drop = [&](int l, int b, int c) {
+            lane_bank[l][c] = 0xff;
+            bank_lane[b][c] = 0xff;
+            lmask[l][c >> 5] &= ~(1u << (c & 31));
+            bmask[b][c >> 5] &= ~(1u << (c & 31));
+        };
+        // (lane, vbank, colour) of the alternating path: each lane at most once
+        uint32_t path[2 * 32], pv[2 * 32];
+        // the overflow edges of overloaded banks first: they take the lowest
+        // colours, so their 2-way conflicts gather in few steps
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int q = 0; q < 32; ++q) bfill[q] = 0;
+          for (int u = 0; u < 32; ++u) {
+            for (int k = 0; k < scnt[u]; ++k) {
+                const uint32_t v = (uint32_t)entries[sbeg[u] + k];
+                const int rb = (int)(v & 31u);
+                const int vi = bfill[rb]++;  // this edge's index on its bank
+                if ((vi >= L) != (pass == 0)) continue;
+                const int b = rb + 32 * (vi / L);  // virtual bank (<= L entries each)
+                int c = g_first_free(lmask[u], bmask[b], L);
+                if (c < 0) {
+                    const int ca = g_first_free(lmask[u], nullptr, L);  // free at the lane
+                    const int cb = g_first_free(bmask[b], nullptr, L);  // free at the bank
+                    // swap colours ca <-> cb on the path bank b -ca- lane -cb- bank ...
+                    int np = 0, x = b;
+                    for (;;) {
+                        const int l = bank_lane[x][ca];
+                        if (l == 0xff) break;
+                        path[np++] = (uint32_t)l | ((uint32_t)x << 8) | ((uint32_t)ca << 16);
+                        const int y = lane_bank[l][cb];
+                        if (y == 0xff) break;
+                        path[np++] = (uint32_t)l | ((uint32_t)y << 8) | ((uint32_t)cb << 16);
+                        x = y;
+                    }
+                    for (int q = 0; q < np; ++q) {
+                        const int l = path[q] & 0xff, bb = (path[q] >> 8) & 0xff, cc = path[q] >> 16;
+                        pv[q] = val[l][cc];
+                        drop(l, bb, cc);
+                    }
+                    for (int q = 0; q < np; ++q) {
+                        const int l = path[q] & 0xff, bb = (path[q] >> 8) & 0xff, cc = path[q] >> 16;
+                        put(l, bb, cc == ca ? cb : ca, pv[q]);
+                    }
+                    c = ca;
+                }
+                put(u, b, c, (((v & 0x7fffffffu) - j0) * 4u) | (v & 0x80000000u));
+            }
+          }
         }
-        bstart[32] = (uint8_t)acc;
-        for (int k = 0; k < cnt; ++k) {
-            const uint32_t v = (uint32_t)entries[beg + k];
-            ent[bptr[v & 31u]++] = v;
-        }
-        for (int b = 0; b < 32; ++b) bptr[b] = bstart[b];
     }
-    uint32_t avail = 0;  // banks with an unscheduled entry
-    for (int b = 0; b < 32; ++b) avail |= (bstart[b + 1] > bstart[b] ? 1u : 0u) << b;
-    int rem = cnt;
-    auto take = [&](int bk) -> uint32_t {
-        const uint32_t v = ent[bptr[bk]++];
-        if (bptr[bk] == bstart[bk + 1]) avail &= ~(1u << bk);
-        --rem;
-        return (((v & 0x7fffffffu) - j0) * 4u) | (v & 0x80000000u);
-    };
-    int t = 0;
-    while (__any_sync(0xffffffffu, rem > 0) || (t & 3)) {
-        if (t >= kGTMax) {
-            if (lane == 0) {
-                atomicOr(fail, 1);
-                tw[wg] = 0;
-            }
-            return;
-        }
-        uint32_t taken = 0;
-        bool served = false;
-        uint32_t val = 0;
-        int maxrem = rem;
-        for (int o = 16; o; o >>= 1) maxrem = max(maxrem, __shfl_xor_sync(0xffffffffu, maxrem, o));
-        for (int round = 0; round < 32; ++round) {
-            const uint32_t cand = served ? 0u : (avail & ~taken);
-            const int bank = cand ? __ffs(cand) - 1 : -1;
-            const unsigned grp = __match_any_sync(0xffffffffu, bank);
-            const unsigned key = bank >= 0 ? ((unsigned)rem << 5) | (31u - (unsigned)lane) : 0u;
-            const unsigned best = __reduce_max_sync(grp, key);
-            const bool win = bank >= 0 && key == best;
-            if (win) {
-                val = take(bank);
-                served = true;
-            }
-            const unsigned won = __reduce_or_sync(0xffffffffu, win ? 1u << bank : 0u);
-            if (!won) break;
-            taken |= won;
-        }
-        // critical lanes accept a conflict rather than lengthen the schedule
-        if (!served && rem > 0 && rem >= maxrem) {
-            const int bk = __ffs(avail) - 1;
-            val = take(bk);
-            served = true;
-            taken |= 1u << bk;
-        }
-        for (int o = 16; o; o >>= 1) taken |= __shfl_xor_sync(0xffffffffu, taken, o);
-        // unserved lanes: distinct free banks for their zero-word reads
-        const unsigned idle = __ballot_sync(0xffffffffu, !served);
-        if (!served) {
+    __syncwarp();
+    for (int t = 0; t < T; ++t) {
+        const int b = t < L ? lane_bank[lane][t] : 0xff;
+        const bool has = b != 0xff;
+        const uint32_t used = __reduce_or_sync(0xffffffffu, has ? 1u << (b & 31) : 0u);
+        const unsigned idle = __ballot_sync(0xffffffffu, !has);
+        uint32_t w;
+        if (has) {
+            w = val[lane][t];
+        } else {  // a zero word in the rank-th unused bank
             const int rank = __popc(idle & ((1u << lane) - 1u));
-            uint32_t freeb = ~taken;
-            int bk = 0;
-            for (int q = 0; q <= rank && freeb; ++q) {
-                bk = __ffs(freeb) - 1;
-                freeb &= freeb - 1;
-            }
-            val = (zero_word + (uint32_t)bk) * 4u;
+            w = (zero_word + (uint32_t)__fns(~used, 0, rank + 1)) * 4u;
         }
-        sched[((int64_t)wg * kGTMax + t) * 32 + lane] = val;
-        ++t;
+        sched[((int64_t)wg * kGTMax + t) * 32 + lane] = w;
     }
-    if (lane == 0) tw[wg] = t;
+    if (lane == 0) tw[wg] = T;
 }
 
 // ---- the gather ----------------------------------------------------------------
@@ -597,7 +637,7 @@ int gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n, int64_
                                             L.fail);
     SKP_LAUNCHED(gather_sort_kernel);
     const int nw = L.P * kGW;
-    gather_sched_kernel<<<(unsigned)cdiv((int64_t)nw * L.H, 4), 128, 0, st>>>(
+    gather_sched_kernel<<<(unsigned)(nw * L.H), 32, 0, st>>>(
         L.seg_beg, L.seg_cnt, entries, nw, n, L.npass, L.ps, L.fail);
     SKP_LAUNCHED(gather_sched_kernel);
     return SKP_OK;
