@@ -56,12 +56,21 @@ constexpr int kGCols = kGW * 32;          // output columns per slice
 // split allows (a 25th warp puts 7 warps on one SMSP: 17920 > 16384); the last
 // warp to finish a row issues the bulk copy of the row two ahead instead
 constexpr int kGThreads = 32 * kGW;
-constexpr int kGTReg = 56;                // schedule steps held in registers
+constexpr int kGTReg = 52;                // schedule steps held in registers
 constexpr int kGTMax = 128;               // schedule steps per warp (the rest: L1/global)
 constexpr unsigned long long kGPlanFailMark = 1ull << 40;  // added to *nonfinite
 constexpr int kGBufWords = 24608;         // row buffer: n <= 24576 floats + 32 zero words
 constexpr uint32_t kGBufBytes = kGBufWords * 4;  // 98432, a multiple of 128
-constexpr size_t kGSmem = 2 * (size_t)kGBufBytes + 32;
+// three row buffers when a row fits 75 KB (n <= 18880, e.g. C3): warps of a
+// CTA may then drift two rows apart before the slowest gates a refill, and a
+// refill has two rows' time to land
+constexpr uint32_t kGBufBytes3 = 75776;  // 18944 words, a multiple of 128
+constexpr int kGN3 = kGBufBytes3 / 4 - 64;
+template <int NB>
+struct GBuf {
+    static constexpr uint32_t bytes = NB == 2 ? kGBufBytes : kGBufBytes3;
+    static constexpr size_t smem = NB * (size_t)bytes + 64;
+};
 
 __device__ __forceinline__ uint32_t g_smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -400,6 +409,63 @@ gather_sched_kernel(const int32_t* __restrict__ seg_beg, const int32_t* __restri
             }
           }
         }
+        // Concentrate the conflicts.  A step is a 2-way conflict iff it holds
+        // an overflow vbank (b + 32k, k >= 1) edge, so the wavefronts are L +
+        // |colours used by overflow vbanks|; the lower bound is L + K, K = the
+        // largest overflow vbank (= the busiest bank's degree).  The Kempe
+        // swaps above scatter those colours over all L steps (C3: 72% of the
+        // steps conflicted, 1.72 wavefronts per LDS), so move every overflow
+        // vbank's colours into [0, K): for its edge of colour x >= K pick a
+        // y < K it lacks and swap x <-> y along the x/y path from it.  The
+        // path enters vbanks by y and leaves by x, so it ends at any vbank
+        // without x: a y whose path would end at an already aligned overflow
+        // vbank is skipped (C3: 1.72 -> 1.60 wavefronts per LDS; the lower
+        // bound, the busiest bank's degree / L, is ~1.35 -- reaching it needs
+        // the conflict edges chosen first, a degree-bounded flow; not done).
+        int K = 0;
+        for (int vb = 32; vb < 32 * kGVB; ++vb) {
+            int c = 0;
+#pragma unroll
+            for (int w = 0; w < kGCW; ++w) c += __popc(bmask[vb][w]);
+            K = max(K, c);
+        }
+        uint32_t aligned[kGVB] = {};  // bit vb & 31 of word vb / 32
+        auto has = [&](const uint32_t* msk, int c) { return (msk[c >> 5] >> (c & 31)) & 1u; };
+        for (int vb = 32; K > 0 && K < L && vb < 32 * kGVB; ++vb) {
+            for (int x = K; x < L; ++x) {
+                if (!has(bmask[vb], x)) continue;
+                for (int y = 0; y < K; ++y) {
+                    if (has(bmask[vb], y)) continue;
+                    int np = 0, xv = vb;
+                    bool bad = false;
+                    for (;;) {
+                        const int l = bank_lane[xv][x];
+                        if (l == 0xff) break;
+                        path[np++] = (uint32_t)l | ((uint32_t)xv << 8) | ((uint32_t)x << 16);
+                        const int v2 = lane_bank[l][y];
+                        if (v2 == 0xff) break;
+                        path[np++] = (uint32_t)l | ((uint32_t)v2 << 8) | ((uint32_t)y << 16);
+                        if ((aligned[v2 >> 5] >> (v2 & 31)) & 1u) {
+                            bad = true;  // would push an aligned vbank out of [0, K)
+                            break;
+                        }
+                        xv = v2;
+                    }
+                    if (bad) continue;
+                    for (int q = 0; q < np; ++q) {
+                        const int l = path[q] & 0xff, bb = (path[q] >> 8) & 0xff, cc = path[q] >> 16;
+                        pv[q] = val[l][cc];
+                        drop(l, bb, cc);
+                    }
+                    for (int q = 0; q < np; ++q) {
+                        const int l = path[q] & 0xff, bb = (path[q] >> 8) & 0xff, cc = path[q] >> 16;
+                        put(l, bb, cc == x ? y : x, pv[q]);
+                    }
+                    break;
+                }
+            }
+            aligned[vb >> 5] |= 1u << (vb & 31);
+        }
     }
     __syncwarp();
     for (int t = 0; t < T; ++t) {
@@ -420,6 +486,7 @@ gather_sched_kernel(const int32_t* __restrict__ seg_beg, const int32_t* __restri
 }
 
 // ---- the gather ----------------------------------------------------------------
+template <int NB>
 __global__ void __maxnreg__(80)
 sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                      const int32_t* __restrict__ lanepos, int P, const uint32_t* __restrict__ sched,
@@ -435,8 +502,9 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
             atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), kGPlanFailMark);
         return;
     }
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * (size_t)kGBufBytes);
-    uint32_t* done = reinterpret_cast<uint32_t*>(full + 2);  // warps finished with a buffer
+    constexpr uint32_t kB = GBuf<NB>::bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + NB * (size_t)kB);
+    uint32_t* done = reinterpret_cast<uint32_t*>(full + NB);  // warps finished with a buffer
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slice = blockIdx.x % P;
@@ -446,21 +514,21 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
     const uint32_t row_bytes = (uint32_t)((n + 3) / 4 * 16);
 
     if (threadIdx.x == 0) {
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NB; ++b) {
             g_mbar_init(&full[b], 1);
             done[b] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (threadIdx.x < 64) {  // zero words (targets of idle lanes) of both buffers
-        float* z = reinterpret_cast<float*>(sm + (threadIdx.x >> 5) * (size_t)kGBufBytes);
+    if (threadIdx.x < 32 * NB) {  // zero words (targets of idle lanes) of every buffer
+        float* z = reinterpret_cast<float*>(sm + (threadIdx.x >> 5) * (size_t)kB);
         z[zero_word + (threadIdx.x & 31)] = 0.f;
     }
     __syncthreads();
-    if (warp == 0) {  // first two rows of this group
-        if (g < m) g_bulk_load_e(base, A + (int64_t)g * lda, row_bytes, &full[0]);
-        if (g + G < m)
-            g_bulk_load_e(base + kGBufBytes, A + (int64_t)(g + G) * lda, row_bytes, &full[1]);
+    if (warp == 0) {  // first NB rows of this group
+        for (int b = 0; b < NB; ++b)
+            if (g + b * (int64_t)G < m)
+                g_bulk_load_e(base + b * kB, A + (g + b * (int64_t)G) * lda, row_bytes, &full[b]);
     }
 
     // compute warps: this warp's schedule -> registers (absolute smem addresses)
@@ -511,10 +579,10 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
         }
         __syncwarp();
         if (lane == 0) {
-            // the last warp done with this buffer refills it with row i + 2G
+            // the last warp done with this buffer refills it with row i + NB*G
             if (atomicAdd(&done[b], 1u) == kGW - 1) {
                 done[b] = 0;
-                const int64_t nx = i + 2 * (int64_t)G;
+                const int64_t nx = i + NB * (int64_t)G;
                 if (nx < m) {
                     asm volatile(
                         "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
@@ -523,7 +591,7 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
                         : "memory");
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
-                        "[%1], %2, [%3];" ::"r"(base + (uint32_t)b * kGBufBytes),
+                        "[%1], %2, [%3];" ::"r"(base + (uint32_t)b * kB),
                         "l"(reinterpret_cast<uint64_t>(A + nx * lda)), "r"(row_bytes),
                         "r"(g_smem_u32(&full[b]))
                         : "memory");
@@ -542,12 +610,14 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
         }
     };
 
-    int it = 0;
-    for (int64_t i = g; i < m; i += 2 * G, it += 2) {
-        do_row(i, 0, (uint32_t)((it >> 1) & 1), std::integral_constant<uint32_t, 0>());
-        if (i + G < m)
-            do_row(i + G, 1, (uint32_t)((it >> 1) & 1),
-                   std::integral_constant<uint32_t, kGBufBytes>());
+    // one row body per buffer: the buffer offset is the LDS immediate
+    uint32_t ph = 0;  // the k-th use of a buffer waits for parity k & 1
+    for (int64_t i = g; i < m; i += NB * (int64_t)G, ph ^= 1u) {
+        do_row(i, 0, ph, std::integral_constant<uint32_t, 0>());
+        if (i + G < m) do_row(i + G, 1, ph, std::integral_constant<uint32_t, kB>());
+        if constexpr (NB > 2)
+            if (i + 2 * (int64_t)G < m)
+                do_row(i + 2 * G, 2, ph, std::integral_constant<uint32_t, 2 * kB>());
     }
 
     if (amax) {  // max |A~| for the 3xFP16 split of A~ (skp_split_h2_f32, have_amax)
@@ -660,14 +730,17 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
     const GLayout L = gather_layout(const_cast<void*>(plan), n, r);
     const int P = L.P;
     const int G = std::max(1, std::min<int>(sms / P, (int)std::min<int64_t>(m, 1 << 20)));
-    SKP_CUDA(cudaFuncSetAttribute(sketch_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kGSmem));
+    static const int nb_env = getenv("SKP_GATHER_NB") ? atoi(getenv("SKP_GATHER_NB")) : 3;
+    const bool nb3 = L.H == 1 && n <= kGN3 && nb_env != 2;
+    auto kern = nb3 ? sketch_gather_kernel<3> : sketch_gather_kernel<2>;
+    const size_t smem = nb3 ? GBuf<3>::smem : GBuf<2>::smem;
+    SKP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // one launch per column pass: pass h gathers A[:, h*npass ...] and adds
     // to what the earlier passes wrote; the checks ride on the last pass
     for (int h = 0; h < L.H; ++h) {
         const int64_t j0 = (int64_t)h * L.npass, nh = std::min<int64_t>(L.npass, n - j0);
         const bool last = h + 1 == L.H;
-        sketch_gather_kernel<<<G * P, kGThreads, kGSmem, st>>>(
+        kern<<<G * P, kGThreads, smem, st>>>(
             A + j0, lda, m, nh, L.lanepos, P, L.ps.sched[h], L.ps.tw[h], L.fail, scale, out, ldo,
             last ? nonfinite : (h == 0 ? nonfinite : nullptr), last ? amax : nullptr, h > 0,
             h == 0);
