@@ -170,7 +170,9 @@ def test_sketch_fused_norm_and_nonfinite(skp, ops):
 
 @pytest.mark.parametrize("m,n,r,s", [(67, 16384, 4000, 8), (5, 1000, 300, 8), (130, 513, 64, 1),
                                      (40, 2050, 1600, 3), (1, 24576, 4000, 8),
-                                     (9, 32768, 4000, 8), (3, 70001, 6000, 4)])
+                                     (9, 32768, 4000, 8), (3, 70001, 6000, 4),
+                                     # the three-buffer ring wrapping several times
+                                     (300, 4096, 2000, 8), (1000, 8192, 768, 8)])
 def test_sketch_gather_permuted(skp, ops, m, n, r, s):
     """K2 v2: (A S) P from the row-gather kernel == the oracle's A S with its
     columns taken in plan order; fused fp64 ||A||_F^2 and the non-finite test."""
