@@ -159,6 +159,33 @@ __device__ __forceinline__ uint32_t cl_mapa(uint32_t a, uint32_t rank) {
 __device__ __forceinline__ void cl_st(uint32_t a, double v) {
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
+// remote store that completes `8 bytes` on the destination's mbarrier
+__device__ __forceinline__ void cl_st_async(uint32_t a, double v, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(a),
+                 "d"(v), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void cl_arm(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cl_wait(uint32_t bar, uint32_t parity) {
+    long long t0 = 0;
+    for (int it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (ok) return;
+        // watchdog: a protocol bug becomes a trap (error), never a hung GPU
+        if (it == 64) t0 = clock64();
+        if (it > 64 && (it & 1023) == 0 && clock64() - t0 > (long long)40e9) __trap();
+    }
+}
 __device__ __forceinline__ void cl_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
                      "memory");
@@ -179,16 +206,37 @@ sytrd_cluster_kernel(const double* __restrict__ Ag, int n, int rpc, double* d, d
     double* vs = pvp + 2 * kCl;
     double* wsv = vs + n;
     __shared__ double scratch[32];
+    // exchange completion: xbar[par] (column i's entries + norm partials),
+    // pbar[par] (p and p.v partials); each CTA arms its own for the bytes it
+    // will receive and the senders' st.async complete them -- no cluster
+    // barrier per exchange.  A sender is never more than one column ahead of a
+    // receiver's reads of a buffer: to send column i + 2 it needs every CTA's
+    // p of column i + 1, sent after that CTA finished column i.
+    __shared__ __align__(8) uint64_t xbar[2], pbar[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    auto xbytes = [&](int i) { return (uint32_t)(8 * ((n - 1 - i) + kCl)); };
+    if (tid == 0) {
+        for (int b = 0; b < 2; ++b) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cl_smem(&xbar[b])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cl_smem(&pbar[b])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < 2 && i + 2 < n; ++i) {  // columns 0 and 1
+            cl_arm(cl_smem(&xbar[i]), xbytes(i));
+            cl_arm(cl_smem(&pbar[i]), xbytes(i));
+        }
+    }
     // load owned rows
     for (int lr = 0; lr < rpc; ++lr) {
         const int r = lr * kCl + (int)rank;
         for (int c = tid; c < n; c += blockDim.x) Al[(size_t)lr * n + c] = r < n ? Ag[(int64_t)r * n + c] : 0.0;
     }
-    cl_sync();
+    cl_sync();  // every CTA's rows loaded and barriers armed
     const uint32_t xv_a = cl_smem(xv), pv_a = cl_smem(pvv), ssp_a = cl_smem(ssp), pvp_a = cl_smem(pvp);
+    const uint32_t xb_a = cl_smem(&xbar[0]), pb_a = cl_smem(&pbar[0]);
     for (int i = 0; i + 2 < n; ++i) {
         const int par = i & 1;
+        const uint32_t ph = (uint32_t)((i >> 1) & 1);  // use i / 2 of each barrier
         const int r0 = i + 1, k = n - r0;
         // (1) broadcast column i of my rows r > i, and sum_{r > r0} x_r^2
         double ss = 0.0;
@@ -198,7 +246,8 @@ sytrd_cluster_kernel(const double* __restrict__ Ag, int n, int rpc, double* d, d
             if (r <= i || r >= n) continue;
             const double x = Al[(size_t)lr * n + i];
             if (dst == 0 && r > r0) ss += x * x;
-            cl_st(cl_mapa(xv_a + 8u * (uint32_t)(par * n + r), (uint32_t)dst), x);
+            cl_st_async(cl_mapa(xv_a + 8u * (uint32_t)(par * n + r), (uint32_t)dst), x,
+                        cl_mapa(xb_a + 8u * par, (uint32_t)dst));
         }
         ss = warp_sum(ss);
         if (lane == 0) scratch[warp] = ss;
@@ -206,9 +255,11 @@ sytrd_cluster_kernel(const double* __restrict__ Ag, int n, int rpc, double* d, d
         if (tid < kCl) {
             double t = 0.0;
             for (int w = 0; w < nw; ++w) t += scratch[w];
-            cl_st(cl_mapa(ssp_a + 8u * (uint32_t)(par * kCl + (int)rank), (uint32_t)tid), t);
+            cl_st_async(cl_mapa(ssp_a + 8u * (uint32_t)(par * kCl + (int)rank), (uint32_t)tid), t,
+                        cl_mapa(xb_a + 8u * par, (uint32_t)tid));
         }
-        cl_sync();
+        cl_wait(xb_a + 8u * par, ph);
+        if (tid == 0 && i + 4 < n) cl_arm(xb_a + 8u * par, xbytes(i + 2));  // column i + 2
         // (2) reflector (every CTA), p for my rows, broadcast p and p.v partials
         double xnorm2 = 0.0;
         for (int c = 0; c < kCl; ++c) xnorm2 += ssp[par * kCl + c];
@@ -243,7 +294,9 @@ sytrd_cluster_kernel(const double* __restrict__ Ag, int n, int rpc, double* d, d
             double acc = 0.0;
             for (int c = r0 + lane; c < n; c += 32) acc += row[c] * vs[c];
             acc = warp_sum(acc) * t_;
-            if (lane < kCl) cl_st(cl_mapa(pv_a + 8u * (uint32_t)(par * n + r), (uint32_t)lane), acc);
+            if (lane < kCl)
+                cl_st_async(cl_mapa(pv_a + 8u * (uint32_t)(par * n + r), (uint32_t)lane), acc,
+                            cl_mapa(pb_a + 8u * par, (uint32_t)lane));
             pvpart += acc * vs[r];
         }
         if (lane == 0) scratch[warp] = pvpart;
@@ -251,9 +304,11 @@ sytrd_cluster_kernel(const double* __restrict__ Ag, int n, int rpc, double* d, d
         if (tid < kCl) {
             double t = 0.0;
             for (int w = 0; w < nw; ++w) t += scratch[w];
-            cl_st(cl_mapa(pvp_a + 8u * (uint32_t)(par * kCl + (int)rank), (uint32_t)tid), t);
+            cl_st_async(cl_mapa(pvp_a + 8u * (uint32_t)(par * kCl + (int)rank), (uint32_t)tid), t,
+                        cl_mapa(pb_a + 8u * par, (uint32_t)tid));
         }
-        cl_sync();
+        cl_wait(pb_a + 8u * par, ph);
+        if (tid == 0 && i + 4 < n) cl_arm(pb_a + 8u * par, xbytes(i + 2));
         // (3) w = p - K v ; update my rows  A[r][c] -= v_r w_c + w_r v_c  (r, c > i)
         if (t_ != 0.0) {
             double pv = 0.0;
