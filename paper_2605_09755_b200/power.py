@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import math
 import os
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -133,6 +134,39 @@ def power_iterate(atil, omega, q: int, stabilized: bool = True):
     return _convert.download(y, oa.kind)
 
 
+class _SideStreams(threading.local):
+    """One side stream per (thread, device): concurrent callers never share."""
+
+    def __init__(self):
+        self.s = {}
+
+    def get(self, dev) -> torch.cuda.Stream:
+        if dev.index not in self.s:
+            self.s[dev.index] = torch.cuda.Stream(dev)
+        return self.s[dev.index]
+
+
+_SIDE = _SideStreams()
+
+
+def _omega_side(spec, seed, dtype, dev, fail_counter):
+    """(Omega, ready event): the device Gaussian draw (numpy's ziggurat, draw
+    for draw) queued on a side stream after everything already on the
+    caller's stream (fail_counter's zeroing included)."""
+    if spec.omega_kind != "gaussian":
+        return None
+    main = torch.cuda.current_stream(dev)
+    side = _SIDE.get(dev)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        om = omega_device("gaussian", spec.r1, spec.r2, seed, dtype, dev, None, fail_counter)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    om.record_stream(main)        # freed by the caller's stream, not the side one
+    fail_counter.record_stream(side)
+    return om, ev
+
+
 def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL,
                       rows_total: int | None = None, phases: _Phases | None = None,
                       fro2: torch.Tensor | None = None, name: str = "a",
@@ -152,9 +186,13 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     om_seed = substream(spec.seed, 1)
     om_job = None if spec.omega_kind == "gaussian" else \
         OmegaDraw(spec.omega_kind, spec.r1, spec.r2, om_seed, a.dtype)
-    sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
-    ph.mark("make_sketch")
     nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
+    sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
+    # the Gaussian Omega is drawn on a side stream, concurrently with the K2
+    # plan (one warp per SM; K1 before it fills the GPU) and K2's first rows;
+    # only P^T waits for the plan
+    om_side = _omega_side(spec, om_seed, a.dtype, dev, nonfinite) if om_job is None else None
+    ph.mark("make_sketch")
     # K2 v2 writes A~ with its columns permuted (A S P); the power iteration
     # then uses P^T Omega, so Y = (A S P)(P^T Omega) = A S Omega exactly as in
     # the reference.  K2 v1 (natural column order) where v2 does not apply.
@@ -191,6 +229,9 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     ph.mark("split")
 
     def omega_for(perm_dev, host: bool = False):
+        if om_side is not None and not host:
+            torch.cuda.current_stream(dev).wait_event(om_side[1])
+            return _ops.permute_rows(om_side[0], perm_dev) if perm_dev is not None else om_side[0]
         if om_job is None and not host:
             return omega_device(spec.omega_kind, spec.r1, spec.r2, om_seed, a.dtype, dev,
                                 perm_dev, nonfinite)
