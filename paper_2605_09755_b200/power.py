@@ -190,8 +190,10 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
     # the Gaussian Omega is drawn on a side stream, concurrently with the K2
     # plan (one warp per SM; K1 before it fills the GPU) and K2's first rows;
-    # only P^T waits for the plan
-    om_side = _omega_side(spec, om_seed, a.dtype, dev, nonfinite) if om_job is None else None
+    # only P^T waits for the plan (SKP_OMEGA_SIDE=0: in line; alternating A/B
+    # at C3, scripts/ab_omega.sh: 63.1 vs 63.5 ms per step)
+    om_side = _omega_side(spec, om_seed, a.dtype, dev, nonfinite) \
+        if om_job is None and os.environ.get("SKP_OMEGA_SIDE", "1") != "0" else None
     ph.mark("make_sketch")
     # K2 v2 writes A~ with its columns permuted (A S P); the power iteration
     # then uses P^T Omega, so Y = (A S P)(P^T Omega) = A S Omega exactly as in
