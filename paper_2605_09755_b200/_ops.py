@@ -147,7 +147,7 @@ def sketch_right(a: torch.Tensor, colptr, entries, s: int, r: int, out=None, fro
     return out
 
 
-GATHER_COLS = 768  # output columns per slice of the K2 v2 plan (sketch_gather.cu)
+GATHER_COLS = 896  # output columns per slice of the K2 v2 plan (sketch_gather.cu)
 
 
 GATHER_PLAN_FAIL_MARK = 1 << 40   # added to the non-finite counter by a failed plan

@@ -22,7 +22,7 @@
 // writes A~ P, and the range finder multiplies by P^T Omega instead of Omega
 // (Y = A~ Omega = (A~ P)(P^T Omega)); apply_right keeps K2 v1's column order.
 //
-// CTA = one slice of <= kGCols = 768 output columns (24 warps; the slices are
+// CTA = one slice of <= kGCols = 896 output columns (28 warps; the slices are
 // balanced to gather_width columns each); the last warp to finish a row
 // refills its buffer (bulk copy of the row two ahead).  Grid = G row groups x
 // P slices.  The CTAs of a row group read the same rows but drift apart, so
@@ -50,13 +50,16 @@ namespace skp {
 
 namespace {
 
-constexpr int kGW = 24;                   // compute warps per CTA
+constexpr int kGW = 28;                   // compute warps per CTA
 constexpr int kGCols = kGW * 32;          // output columns per slice
-// no producer warp: 24 warps x 80 registers is the most a 4-way register file
-// split allows (a 25th warp puts 7 warps on one SMSP: 17920 > 16384); the last
-// warp to finish a row issues the bulk copy of the row two ahead instead
+// no producer warp; 28 warps x 72 registers (7 warps per SMSP: 16128 <=
+// 16384 registers) so that C3's l = 4000 takes 5 slices of 800 columns instead
+// of 6 of 672 -- each row is bulk-copied into one CTA fewer -- with 96 spare
+// lanes per slice for splitting the heavy columns.  44 register-resident
+// steps cover C3's heaviest warp (44); the last warp to finish a row issues
+// the bulk copy of the row NB ahead
 constexpr int kGThreads = 32 * kGW;
-constexpr int kGTReg = 52;                // schedule steps held in registers
+constexpr int kGTReg = 44;                // schedule steps held in registers
 constexpr int kGTMax = 128;               // schedule steps per warp (the rest: L1/global)
 constexpr unsigned long long kGPlanFailMark = 1ull << 40;  // added to *nonfinite
 constexpr int kGBufWords = 24608;         // row buffer: n <= 24576 floats + 32 zero words
@@ -487,7 +490,7 @@ gather_sched_kernel(const int32_t* __restrict__ seg_beg, const int32_t* __restri
 
 // ---- the gather ----------------------------------------------------------------
 template <int NB>
-__global__ void __maxnreg__(80)
+__global__ void __maxnreg__(72)
 sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                      const int32_t* __restrict__ lanepos, int P, const uint32_t* __restrict__ sched,
                      const int32_t* __restrict__ tw, const int32_t* __restrict__ plan_fail,

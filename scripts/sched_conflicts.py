@@ -11,15 +11,17 @@ from paper_2605_09755_b200.sketching import make_sketch
 n, l = 16384, 4000
 op = make_sketch("countsketch", n, l, 7, s=8)
 plan, perm = op.gather_plan()
-P = -(-l // 768)
+from paper_2605_09755_b200._ops import GATHER_COLS
+W = GATHER_COLS // 32
+P = -(-l // GATHER_COLS)
 g = plan.cpu().numpy().view(np.uint32)
-o = P * 768 + 4
-tw = g[o:o + P * 24].astype(np.int64)
-o += P * 24
-sched = g[o:o + P * 24 * 128 * 32].reshape(P * 24, 128, 32)
+o = P * GATHER_COLS + 4
+tw = g[o:o + P * W].astype(np.int64)
+o += (P * W + 3) // 4 * 4
+sched = g[o:o + P * W * 128 * 32].reshape(P * W, 128, 32)
 tot_w = tot_i = 0
 hist = np.zeros(40, np.int64)
-for w in range(P * 24):
+for w in range(P * W):
     for t in range(tw[w]):
         words = (sched[w, t] & 0x7fffffff) >> 2
         banks = words & 31
