@@ -64,9 +64,11 @@ constexpr int kGTMax = 128;               // schedule steps per warp (the rest: 
 constexpr unsigned long long kGPlanFailMark = 1ull << 40;  // added to *nonfinite
 constexpr int kGBufWords = 24608;         // row buffer: n <= 24576 floats + 32 zero words
 constexpr uint32_t kGBufBytes = kGBufWords * 4;  // 98432, a multiple of 128
-// three row buffers when a row fits 75 KB (n <= 18880, e.g. C3): warps of a
-// CTA may then drift two rows apart before the slowest gates a refill, and a
-// refill has two rows' time to land
+// three row buffers (SKP_GATHER_NB=3, rows <= 75 KB): warps of a CTA may
+// drift two rows apart before the slowest gates a refill.  Measured at C3:
+// 11.54 -> 11.46 ms with 6 slices of 24 warps, but 9.86 (two) vs 10.01 ms
+// (three) with 5 slices of 28 warps, and ~20% more DRAM re-reads -- so two
+// buffers are the default
 constexpr uint32_t kGBufBytes3 = 75776;  // 18944 words, a multiple of 128
 constexpr int kGN3 = kGBufBytes3 / 4 - 64;
 template <int NB>
@@ -733,7 +735,7 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
     const GLayout L = gather_layout(const_cast<void*>(plan), n, r);
     const int P = L.P;
     const int G = std::max(1, std::min<int>(sms / P, (int)std::min<int64_t>(m, 1 << 20)));
-    static const int nb_env = getenv("SKP_GATHER_NB") ? atoi(getenv("SKP_GATHER_NB")) : 3;
+    static const int nb_env = getenv("SKP_GATHER_NB") ? atoi(getenv("SKP_GATHER_NB")) : 2;
     const bool nb3 = L.H == 1 && n <= kGN3 && nb_env != 2;
     auto kern = nb3 ? sketch_gather_kernel<3> : sketch_gather_kernel<2>;
     const size_t smem = nb3 ? GBuf<3>::smem : GBuf<2>::smem;
