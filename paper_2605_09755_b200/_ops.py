@@ -147,7 +147,8 @@ def sketch_right(a: torch.Tensor, colptr, entries, s: int, r: int, out=None, fro
     return out
 
 
-GATHER_COLS = 896  # output columns per slice of the K2 v2 plan (sketch_gather.cu)
+GATHER_COLS = 896  # lanes per slice of the K2 v2 plan (sketch_gather.cu kGCols)
+GATHER_SPARE = 96  # slices hold at most GATHER_COLS - GATHER_SPARE columns (kGSpare)
 
 
 GATHER_PLAN_FAIL_MARK = 1 << 40   # added to the non-finite counter by a failed plan
@@ -179,7 +180,7 @@ def gather_plan_checked(plan: torch.Tensor, r: int):
     off = int(_lib.load().skp_sketch_gather_plan_fail_offset(r))
     if int(plan[off:off + 4].view(torch.int32).item()) != 0:
         return None
-    nslice = -(-r // GATHER_COLS)
+    nslice = -(-r // (GATHER_COLS - GATHER_SPARE))
     perm = plan[:nslice * GATHER_COLS * 4].view(torch.int32).cpu().numpy()
     return plan, perm[perm >= 0].astype(np.int64)
 

@@ -643,7 +643,11 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
 //   per column pass h < H: tw int32[P*kGW] (padded to 16) | sched uint32[P*kGW*kGTMax*32]
 //   | seg_beg int32[H][P*kGCols] | seg_cnt int32[H][P*kGCols] | lanepos int32[P*kGCols]
 // H = ceil(n / 24576) column passes of npass (a multiple of 32) columns each.
-int gather_slices(int64_t r) { return (int)cdiv(r, (int64_t)kGCols); }
+// slices of at most kGCols - 96 columns: the spare lanes split heavy columns
+// (with none, C3-like sketches put 56 steps on the heaviest warps, past the 44
+// register-resident ones); C3's 4000 columns -> 5 x 800
+constexpr int kGSpare = 96;
+int gather_slices(int64_t r) { return (int)cdiv(r, (int64_t)(kGCols - kGSpare)); }
 // balanced slice width: the P slices share the r columns evenly (multiple of
 // 32), so no CTA carries a short last slice while its SM idles (C3: 6 x 672
 // instead of 5 x 768 + 160)

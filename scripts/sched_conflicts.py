@@ -13,7 +13,7 @@ op = make_sketch("countsketch", n, l, 7, s=8)
 plan, perm = op.gather_plan()
 from paper_2605_09755_b200._ops import GATHER_COLS
 W = GATHER_COLS // 32
-P = -(-l // GATHER_COLS)
+P = -(-l // (GATHER_COLS - 96))
 g = plan.cpu().numpy().view(np.uint32)
 o = P * GATHER_COLS + 4
 tw = g[o:o + P * W].astype(np.int64)
