@@ -180,13 +180,16 @@ int skp_cholesky_f64(double* G, int64_t n, int64_t ld, int32_t* info, void* stre
  * orthonormalize's column dropping, linalg.py:75-81).                       */
 int skp_chol_pivot_check_f64(const double* L, int64_t n, int64_t ld, double rel_tol,
                              int32_t* info, void* stream);
-/* Fused K5: G = L L^T, rank check and X = L^{-1} in one cooperative kernel
- * (32-wide panels).  X dense n x n (strict upper zero).  *info (device) is
- * only written on failure: k+1 first non-positive pivot, -1 if min L_ii <
- * rel_tol * max L_ii; callers zero it (failures accumulate across calls).   */
+/* Fused K5: G + shift = L L^T, rank check and X = L^{-1} in one cooperative
+ * kernel (32-wide panels), shift = shift_rel * max_i G_ii * I (0: plain
+ * Cholesky; > 0: the first pass of shifted CholeskyQR3, which replaces the
+ * pivoted QR of orthonormalize, linalg.py:57-81, without losing columns to
+ * the Gram's rounding floor).  X dense n x n (strict upper zero).  *info
+ * (device) is only written on failure: k+1 first non-positive pivot, -1 if
+ * min L_ii < rel_tol * max L_ii; callers zero it (failures accumulate).     */
 int64_t skp_cholinv_ws_bytes(int64_t n);
-int skp_cholinv_f64(const double* G, int64_t n, int64_t ld, double rel_tol, double* X,
-                    int32_t* info, void* ws, int64_t ws_bytes, void* stream);
+int skp_cholinv_f64(const double* G, int64_t n, int64_t ld, double rel_tol, double shift_rel,
+                    double* X, int32_t* info, void* ws, int64_t ws_bytes, void* stream);
 /* X (n x n, dense, row-major) = L^{-1} (lower; strict upper zeroed). */
 int skp_trinv_lower_f64(const double* L, int64_t ldl, int64_t n, double* X, void* stream);
 

@@ -7,6 +7,7 @@ arithmetic step runs in hand-written sm_100a kernels in ``libskp.so``
 (include/skp.h) behind a ctypes binding; there is no CPU fallback.  Row-
 sharded multi-GPU drivers live in ``paper_2605_09755_b200.distributed``.
 """
+from ._convert import DeviceMatrix, device_matrix
 from .linalg import (
     SvdResult,
     as_matrix,
@@ -41,7 +42,7 @@ from .sketching import (
     substream,
 )
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
 
 
 def library_path() -> str:

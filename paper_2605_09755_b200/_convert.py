@@ -29,6 +29,14 @@ def _torch_dtype_for(dt) -> torch.dtype:
 
 def upload(a, name: str = "matrix", device=None, dtype=None, check_finite: bool = True) -> Operand:
     dev = _ops.require_cuda(device)
+    if isinstance(a, DeviceMatrix):
+        op = a.resident()
+        if dtype is not None and op.t.dtype != dtype:
+            op = Operand(_ops.cast(op.t, dtype), op.kind, name)
+        if check_finite and not a.finite:
+            ensure_finite(op)
+            a.finite = True
+        return op
     if isinstance(a, torch.Tensor):
         kind = "cuda" if a.is_cuda else "cpu"
         want = dtype or (a.dtype if a.dtype in (F32, F64) else F64)
@@ -90,6 +98,8 @@ def upload_streamed(a, name: str = "matrix", device=None):
     """(Operand, Streamed | None): like upload(check_finite=False), except that
     a host 2-D float32/float64 matrix is NOT copied yet -- the caller drives
     the copy block by block through Streamed.blocks()."""
+    if isinstance(a, DeviceMatrix):
+        return a.take()
     dev = _ops.require_cuda(device)
     if isinstance(a, torch.Tensor) and (a.is_cuda or a.dim() != 2 or a.dtype not in (F32, F64)):
         return upload(a, name, device, check_finite=False), None
@@ -136,3 +146,54 @@ def download(t: torch.Tensor, kind: str):
     host.copy_(t, non_blocking=True)
     torch.cuda.current_stream(t.device).synchronize()
     return host if kind == "cpu" else host.numpy()
+
+
+class DeviceMatrix:
+    """A host matrix uploaded ONCE for a sequence of reference calls, e.g. the
+    drop-in pair ``range_finder_sketched(A, spec)`` then ``randsvd(A, Q)``
+    (power.py:141, :181), each of which would otherwise copy ``a`` to the
+    device again.  Nothing is copied at construction: the first call that
+    takes the matrix streams it in row blocks behind its own sketch (as
+    ``rsvd`` does); later calls use the resident copy.  Results keep the
+    caller's kind (numpy in, numpy out).  The caller must not modify ``a``
+    while the handle is in use (the device copy would not follow)."""
+
+    def __init__(self, a, device=None):
+        self.op, self._streamed = upload_streamed(a, "a", device)
+        self.finite = False      # set by the first call that tested every entry
+        self._taken = False
+
+    @property
+    def shape(self):
+        return tuple(self.op.t.shape)
+
+    @property
+    def dtype(self):
+        return self.op.t.dtype
+
+    def take(self):
+        """(Operand, Streamed | None) for the first consumer; (Operand, None) after."""
+        if self._streamed is not None and not self._taken:
+            self._taken = True
+            return self.op, self._streamed
+        return self.resident(), None
+
+    def resident(self) -> Operand:
+        """The operand with every row on the device."""
+        st = self._streamed
+        if st is not None and not st.done:
+            if self._taken:      # a consumer stopped part way: copy it all again
+                self.op.t.copy_(st.src, non_blocking=True)
+                st.done = True
+            else:
+                self._taken = True
+                for _ in st.blocks():
+                    pass
+        return self.op
+
+
+def device_matrix(a, device=None) -> DeviceMatrix:
+    """Upload handle for reusing one device copy of ``a`` across calls."""
+    if isinstance(a, DeviceMatrix):
+        return a
+    return DeviceMatrix(a, device)

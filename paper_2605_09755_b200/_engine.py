@@ -10,10 +10,11 @@ linalg.py:57-88) written once against two small interfaces:
   product A~^T Y, the r2 x r2 Gram matrices and the r2 x n matrix Q^T A are
   summed.
 
-Orthonormalisation is CholeskyQR2 (two passes of Gram -> Cholesky -> L^{-1}
--> Y L^{-T}).  Where the reference's pivoted QR would drop columns
-(linalg.py:75-81) the Cholesky pivot check fails and an eigen-based
-truncating pass (Y V_k Lambda_k^{-1/2}) runs first.
+Orthonormalisation is shifted CholeskyQR3 (three passes of Gram ->
+Cholesky -> L^{-1} -> Y L^{-T}, the first on a shifted Gram).  Where the
+reference's pivoted QR would drop columns (linalg.py:75-81) the second
+pass's pivot check fails and an eigen-based truncating step
+(Q V_k Lambda_k^{-1/2}) runs before the last pass.
 """
 from __future__ import annotations
 
@@ -30,11 +31,19 @@ class LocalComm:
 
 LOCAL = LocalComm()
 
-# Relative pivot floor for the Gram-based rank test: CholeskyQR resolves
-# sigma_i / sigma_1 down to ~sqrt(eps) of the Gram's precision, so the
-# reference tolerance max(m, c) * eps (linalg.py:51-54) is raised to these
-# floors (documented deviation).
-PIVOT_FLOOR = {"float64": 1e-6, "float32": 5e-4}
+# Orthonormalisation is shifted CholeskyQR3 (Fukaya et al., SIAM J. Sci.
+# Comput. 2020): pass 1 factors G + SHIFT_REL * max_i G_ii * I, which never
+# fails on a numerically full-rank Y and leaves range(Y) intact (directions
+# below the shift come out damped, not dropped); passes 2 and 3 are plain
+# CholeskyQR on the now well-conditioned block.  The rank test (the
+# reference's |R_ii| >= tol * max|R_ii|, linalg.py:75-81) runs on pass 2's
+# Gram, where a direction with sigma_i(Y)/sigma_1(Y) = rho < sqrt(shift)
+# has pivot rho / sqrt(shift): its smallest resolvable pivot ratio is
+# RESOLVE (set by the Gram's own rounding), so the smallest resolvable rho
+# is RESOLVE * sqrt(SHIFT_REL) -- 2.8e-6 in fp32 and 3.2e-13 in fp64, where
+# the reference keeps max(m, c) * eps (5.8e-11 at C3).
+SHIFT_REL = {"float64": 1e-13, "float32": 2.0 ** -17}
+RESOLVE = {"float64": 1e-6, "float32": 1e-3}
 ORTHO_TOL = {"float64": 1e-6, "float32": 1e-4}
 
 
@@ -42,58 +51,81 @@ def _dtype_key(be) -> str:
     return "float32" if "32" in str(be.dtype) else "float64"
 
 
-def pivot_tol(be, rows: int, cols: int, tol=None) -> float:
+def rank_floor(be, rows: int, cols: int, tol=None) -> float:
+    """Smallest kept sigma_i(Y) / sigma_1(Y): the reference's tolerance
+    (linalg.py:51-54, or the caller's ``tol``), raised to what the compute
+    precision resolves."""
+    key = _dtype_key(be)
     ref = (max(rows, cols) * np.finfo(np.float64).eps) if tol is None else float(tol)
-    return max(ref, PIVOT_FLOOR[_dtype_key(be)])
+    return max(ref, RESOLVE[key] * SHIFT_REL[key] ** 0.5)
+
+
+def _pass2_floor(be, f: float) -> float:
+    """Pivot-ratio floor of pass 2 equivalent to the floor f on sigma(Y)."""
+    return min(1.0, f / SHIFT_REL[_dtype_key(be)] ** 0.5)
 
 
 def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: bool = False,
-                   passes: int = 2, planes_out: bool = False):
-    """Orthonormal basis of range(y) (linalg.py:57-81) by CholeskyQR2.
+                   passes: int = 3, planes_out: bool = False):
+    """Orthonormal basis of range(y), numerically rank-truncated (linalg.py:57-81),
+    by shifted CholeskyQR3 (see SHIFT_REL).
 
-    ``lazy``: no host synchronisation; a Cholesky failure (rank deficiency)
-    is only flagged on the device (``be.lazy_failed()``) and the caller must
-    redo the computation eagerly, where the truncating eigen path runs.
-    ``passes=1`` (lazy only): one CholeskyQR pass -- same span, orthogonality
-    ~eps * cond(Y)^2; used for the stabilisations inside the power iteration,
-    whose only job is to keep the block well conditioned (the final Q always
-    gets two passes)."""
+    ``lazy``: no host synchronisation; a rank-deficiency flag (pass 2's pivot
+    test) or a failed factorisation is only recorded on the device
+    (``be.lazy_failed()``) and the caller must redo the computation eagerly,
+    where the truncating eigen path runs.  ``passes=1`` (lazy only): the
+    shifted pass alone -- same span, no rank test; used for the
+    stabilisations inside the power iteration, whose only job is to keep the
+    block well conditioned (the final Q always gets all three passes)."""
     if hasattr(be, "orth_planes") and not isinstance(y, np.ndarray) and hasattr(y, "hi"):
         # y given as the fp16 planes of its transpose (the lazy planes path)
         rows_total = y.cols if rows_total is None else rows_total
-        rel = pivot_tol(be, rows_total, y.rows, tol)
-        if lazy and passes == 2:
-            return be.orth_planes(comm, y, rel, planes_out)
+        t2 = _pass2_floor(be, rank_floor(be, rows_total, y.rows, tol))
+        if lazy and passes == 3:
+            return be.orth_planes(comm, y, t2, SHIFT_REL[_dtype_key(be)], planes_out)
         y = be.planes_to_compute(y)
     c = y.shape[1]
     rows_total = y.shape[0] if rows_total is None else rows_total
-    rel = pivot_tol(be, rows_total, c, tol)
+    key = _dtype_key(be)
+    f = rank_floor(be, rows_total, c, tol)
+    t2 = _pass2_floor(be, f)
     g = comm.allreduce_(be.gram64(y))
-    if lazy:
-        x = be.chol_inv64(g, rel, lazy=True)
-        q = be.mm(y, be.to_compute(x), tb=True)
-        if passes == 1:
-            return q
-        g2 = comm.allreduce_(be.gram64(q, accurate=True))
-        x2 = be.chol_inv64(g2, 0.0, lazy=True)
-        return be.mm(q, be.to_compute(x2), tb=True)
-    x = be.chol_inv64(g, rel)
-    if x is None:
+    x1 = be.chol_inv64(g, 0.0, lazy=lazy, shift=SHIFT_REL[key])
+    if x1 is None:
+        # G is indefinite beyond the shift (all-zero or degenerate input):
+        # truncate on G's own spectrum, dropping what lies under the shift
         w, v = be.eig_desc64(g)
-        t, k = be.eig_orth64(w, v, rel * rel)
+        t, k = be.eig_orth64(w, v, max(f * f, SHIFT_REL[key]))
         if k == 0:
             raise ValueError("cannot orthonormalize an all-zero matrix")
         y = be.mm(y, be.to_compute(be.cols(t, k)))
-        g = comm.allreduce_(be.gram64(y))
-        x = be.chol_inv64(g, 0.0)
-        if x is None:
+        g = comm.allreduce_(be.gram64(y, accurate=True))
+        x1 = be.chol_inv64(g, 0.0, shift=SHIFT_REL[key])
+        if x1 is None:
             raise RuntimeError("orthonormalize: Cholesky failed after rank truncation")
-    q = be.mm(y, be.to_compute(x), tb=True)
+    q = be.mm(y, be.to_compute(x1), tb=True)
+    if lazy and passes == 1:
+        return q
     g2 = comm.allreduce_(be.gram64(q, accurate=True))
-    x2 = be.chol_inv64(g2, 0.0)
+    x2 = be.chol_inv64(g2, t2, lazy=lazy)
     if x2 is None:
-        raise RuntimeError("orthonormalize: second CholeskyQR pass failed")
-    return be.mm(q, be.to_compute(x2), tb=True)
+        # rank deficient: keep the directions of q whose pass-2 pivots clear
+        # t2 (sigma_i(Y) >= f sigma_1(Y)), as the pivoted QR keeps |R_ii|
+        w, v = be.eig_desc64(g2)
+        t, k = be.eig_orth64(w, v, t2 * t2)
+        if k == 0:
+            raise ValueError("cannot orthonormalize an all-zero matrix")
+        q = be.mm(q, be.to_compute(be.cols(t, k)))
+        g2 = comm.allreduce_(be.gram64(q, accurate=True))
+        x2 = be.chol_inv64(g2, 0.0)
+        if x2 is None:
+            raise RuntimeError("orthonormalize: Cholesky failed after rank truncation")
+    q = be.mm(q, be.to_compute(x2), tb=True)
+    g3 = comm.allreduce_(be.gram64(q, accurate=True))
+    x3 = be.chol_inv64(g3, 0.0, lazy=lazy)
+    if x3 is None:
+        raise RuntimeError("orthonormalize: third CholeskyQR pass failed")
+    return be.mm(q, be.to_compute(x3), tb=True)
 
 
 def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_total=None,
@@ -104,14 +136,12 @@ def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_t
     the 3xFP16 GEMM on the CUDA backend)."""
     atil = be.prepare(atil)
     if lazy and stabilized and q > 0 and hasattr(be, "planes_ok") and be.planes_ok(atil, omega):
-        def rel_of(yt):
-            return pivot_tol(be, yt.cols if rows_total is None else rows_total, yt.rows)
-        return be.power_lazy_planes(comm, atil, omega, q, rel_of)
+        return be.power_lazy_planes(comm, atil, omega, q, SHIFT_REL[_dtype_key(be)])
     y = be.mm(atil, omega)
     for _ in range(q):
         if stabilized:
             y = orthonormalize(be, comm, y, rows_total=rows_total, lazy=lazy,
-                               passes=1 if lazy else 2)
+                               passes=1 if lazy else 3)
         z = comm.allreduce_(be.mm(atil, y, ta=True))
         y = be.mm(atil, z)
     return y
@@ -123,19 +153,33 @@ def randsvd(be, comm, a, qb, check: bool = True, amax_hint=None):
 
     B is formed transposed, B^T = A^T Q (n x c): the long dimension n then
     sits on the GEMM's M side (full 256-row CTA-pair tiles) instead of the
-    short c, and B B^T = (B^T)^T B^T, V = B^T U~ read it directly."""
+    short c, and B B^T = (B^T)^T B^T, V = B^T U~ read it directly.
+
+    ``check``: the reference's ||Q^T Q - I||_max test (power.py:194-196).  On
+    backends with a device-side deviation (``orth_dev_t``) it is queued with
+    the rest and read once at the end, with the overflow flag -- no host
+    synchronisation between the check and the products."""
+    dev = None
     if check:
-        g = comm.allreduce_(be.gram64(be.dense(qb) if hasattr(be, "dense") else qb))
-        dev = be.orth_dev(g)
-        if not dev <= ORTHO_TOL[_dtype_key(be)]:
-            raise ValueError(f"Q is not orthonormal (deviation {dev:.3e})")
+        if hasattr(be, "orth_dev_t"):
+            dev = be.orth_dev_t(comm.allreduce_(be.gram64_q(qb)))
+        else:
+            g = comm.allreduce_(be.gram64(be.dense(qb) if hasattr(be, "dense") else qb))
+            _raise_if_not_orthonormal(be, be.orth_dev(g))
     out = _randsvd_core(be, comm, be.mm_at_big(a, qb, amax_hint), qb)   # B^T: this rank's part
+    if dev is not None:
+        _raise_if_not_orthonormal(be, be.scalar(dev))
     if be.overflowed(comm):
         # the in-kernel fp16 split met an entry beyond its exponent bound (a
         # hint that did not hold): recompute with 3xTF32 on every rank.  The
         # flag is read once, after everything is queued (no mid-call sync).
         out = _randsvd_core(be, comm, be.mm(a, be.dense(qb), ta=True), qb)
     return out
+
+
+def _raise_if_not_orthonormal(be, dev: float):
+    if not dev <= ORTHO_TOL[_dtype_key(be)]:
+        raise ValueError(f"Q is not orthonormal (deviation {dev:.3e})")
 
 
 def _randsvd_core(be, comm, bt, qb):

@@ -58,7 +58,7 @@ SIGNATURES = {
     "skp_cholesky_f64": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "skp_trinv_lower_f64": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "skp_cholinv_ws_bytes": (_i64, [_i64]),
-    "skp_cholinv_f64": (_int, [_vp, _i64, _i64, _f64, _vp, _vp, _vp, _i64, _vp]),
+    "skp_cholinv_f64": (_int, [_vp, _i64, _i64, _f64, _f64, _vp, _vp, _vp, _i64, _vp]),
     "skp_syevj_ws_bytes": (_i64, [_i64]),
     "skp_syevj_f64": (_int, [_vp, _i64, _vp, _vp, _i32, _vp, _i64, _vp, _vp]),
     "skp_cast_f32_f64": (_int, [_vp, _vp, _i64, _vp]),

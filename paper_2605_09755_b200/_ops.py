@@ -462,6 +462,10 @@ def scale_cols_(x: torch.Tensor, scale64: torch.Tensor):
     return x
 
 
+SIMT_MIN_K = 128          # shorter chains: the tensor core's truncation is below 1e-6
+SIMT_MAX_MACS = 1 << 33   # ~1 ms of SIMT fp32
+
+
 class CudaBackend:
     """Compute backend for the engine: every op is a libskp kernel launch."""
 
@@ -485,7 +489,22 @@ class CudaBackend:
             key = tuple(b.shape)
             self._bsplit[key] = sb = split_h2(b, trans=True, out=self._bsplit.get(key))
             return gemm_h3(a, sb, ta=ta, alpha=alpha, beta=beta, out=out)
-        return gemm(a, b, ta, tb, alpha=alpha, beta=beta, out=out, mode=self.gemm_mode)
+        M = a.shape[1] if ta else a.shape[0]
+        K = a.shape[0] if ta else a.shape[1]
+        N = b.shape[0] if tb else b.shape[1]
+        return gemm(a, b, ta, tb, alpha=alpha, beta=beta, out=out, mode=self._mode_for(M, N, K))
+
+    def _mode_for(self, M: int, N: int, K: int) -> str:
+        """fp32 products below the 3xFP16 sizes: the tcgen05 3xTF32 kernel
+        accumulates in the tensor core, which truncates once per MMA (measured
+        r02: a K = 4000 Gram of unit columns came out 7.4e-5 low, so
+        Q^T Q = (1 - 7e-5) I and sigma moved past the 1e-5 parity bar); long
+        chains that small run on the SIMT kernel instead (round-to-nearest
+        FMA, 2.6e-7 on the same Gram, sub-millisecond at these sizes)."""
+        if (self.dtype == F32 and self.gemm_mode == "auto" and K >= SIMT_MIN_K
+                and M * N * K <= SIMT_MAX_MACS):
+            return "fp32"
+        return self.gemm_mode
 
     def mm_at_big(self, a, q, amax_hint=None):
         """a^T q for the one-pass product of randsvd (a = the input, read
@@ -581,8 +600,8 @@ class CudaBackend:
         bd = cast(bt, F64)
         return gemm(bd, bd, True, False)
 
-    def chol_inv64(self, g, rel_tol, lazy: bool = False):
-        """L^{-1} of G = L L^T (fused cooperative kernel).
+    def chol_inv64(self, g, rel_tol, lazy: bool = False, shift: float = 0.0):
+        """L^{-1} of G + shift max_i G_ii I = L L^T (fused cooperative kernel).
 
         Eager: zeroes the status, then one 4-byte device->host read; returns
         None when G is not numerically full rank.  Lazy: no host sync; a failure
@@ -596,7 +615,8 @@ class CudaBackend:
         flag = self.fail if lazy else self.info
         if not lazy:
             self.info.zero_()
-        call("skp_cholinv_f64", ptr(g), n, g.stride(0), rel_tol, ptr(x), ptr(flag), ptr(ws), wsb, st)
+        call("skp_cholinv_f64", ptr(g), n, g.stride(0), rel_tol, shift, ptr(x), ptr(flag), ptr(ws),
+             wsb, st)
         if lazy:
             return x
         if int(self.info[0].item()) != 0:
@@ -624,40 +644,44 @@ class CudaBackend:
         """Y^T Y (fp64) from the split planes of Y^T: 3xFP16, promoted accumulation."""
         return cast(gemm_h3(yt, yt), F64)
 
-    def power_lazy_planes(self, comm, atil: SplitH2, omega, q: int, rel_of):
+    def power_lazy_planes(self, comm, atil: SplitH2, omega, q: int, shift: float):
         """Stabilized power iteration (power.py:113-134) with every product on
         K4h and every intermediate block kept as fp16 planes of its
         TRANSPOSE, written by the producing product's epilogue:
-            Y^T = (A~ Omega)^T,  q x { G = Y^T Y;  X = chol_inv(G);
+            Y^T = (A~ Omega)^T,  q x { G = Y^T Y;  X = chol_inv(G + shift);
                                        Q^T = (Y X^T)^T (|Q| <= 1: fixed exponent 14);
                                        Z = A~^T Q;  Y^T = (A~ Z)^T }.
-        Lazy: a Cholesky failure or a Q entry out of fp16 range only sets
-        self.fail (the caller then reruns eagerly in fp32).  Returns Y^T planes."""
-        # SKP_H3_POWER2=1: the products with A~ round the block to fp16 (2 MMAs
-        # per MAC instead of 3; power phase -15% at C3).  Measured: sigma moves
-        # by up to 2.1e-5 relative at C3 (the 1e-5 parity target), so 3 by default.
-        bl = not os.environ.get("SKP_H3_POWER2")
-        yt = gemm_h3_emit_t(atil, split_h2(omega, trans=True), b_lo=bl)
+        The stabilisation is the shifted CholeskyQR pass alone (range kept,
+        no rank test; _engine.SHIFT_REL).  Lazy: a failed factorisation or a
+        Q entry out of fp16 range only sets self.fail (the caller then reruns
+        eagerly in fp32).  Returns Y^T planes."""
+        yt = gemm_h3_emit_t(atil, split_h2(omega, trans=True))
         qt = None
         for _ in range(q):
-            x = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), rel_of(yt), lazy=True)
+            x = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), 0.0, lazy=True,
+                                shift=shift)
             qt = gemm_h3_emit_t(yt, split_h2(self.to_compute(x)), ta=True, e_fixed=14, out=qt,
                                 overflow=self.fail[1:])
-            z = comm.allreduce_(gemm_h3(atil, qt, ta=True, b_lo=bl))
-            yt = gemm_h3_emit_t(atil, split_h2(z, trans=True), out=yt, b_lo=bl)
+            z = comm.allreduce_(gemm_h3(atil, qt, ta=True))
+            yt = gemm_h3_emit_t(atil, split_h2(z, trans=True), out=yt)
         return yt
 
-    def orth_planes(self, comm, yt: SplitH2, rel: float, planes_out: bool = False):
-        """Lazy CholeskyQR2 of Y given as Y^T planes; returns Q (fp32, rows x
-        c), or with planes_out the planes of Q^T (what randsvd consumes)."""
-        x1 = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), rel, lazy=True)
+    def orth_planes(self, comm, yt: SplitH2, t2: float, shift: float, planes_out: bool = False):
+        """Lazy shifted CholeskyQR3 of Y given as Y^T planes (_engine.orthonormalize):
+        pass 1 on G + shift, pass 2 with the rank test t2 on its pivots, pass 3.
+        Returns Q (fp32, rows x c), or with planes_out the planes of Q^T (what
+        randsvd consumes)."""
+        x1 = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), 0.0, lazy=True, shift=shift)
         q1t = gemm_h3_emit_t(yt, split_h2(self.to_compute(x1)), ta=True, e_fixed=14,
                              overflow=self.fail[1:])
-        x2 = self.chol_inv64(comm.allreduce_(self.gram64_planes(q1t)), 0.0, lazy=True)
+        x2 = self.chol_inv64(comm.allreduce_(self.gram64_planes(q1t)), t2, lazy=True)
+        q2t = gemm_h3_emit_t(q1t, split_h2(self.to_compute(x2)), ta=True, e_fixed=14,
+                             overflow=self.fail[1:])
+        x3 = self.chol_inv64(comm.allreduce_(self.gram64_planes(q2t)), 0.0, lazy=True)
         if planes_out:
-            return gemm_h3_emit_t(q1t, split_h2(self.to_compute(x2)), ta=True, e_fixed=14,
-                                  overflow=self.fail[1:])
-        return gemm_h3(q1t, split_h2(self.to_compute(x2)), ta=True)
+            return gemm_h3_emit_t(q2t, split_h2(self.to_compute(x3)), ta=True, e_fixed=14,
+                                  out=q1t, overflow=self.fail[1:])
+        return gemm_h3(q2t, split_h2(self.to_compute(x3)), ta=True)
 
     def planes_to_compute(self, yt: SplitH2):
         """fp32 Y from Y^T planes (the eager fallback): Y = (Y^T)^T I."""
@@ -688,11 +712,22 @@ class CudaBackend:
         call("skp_sqrt_eigs_f64", ptr(w), w.shape[0], ptr(sig), ptr(inv), stream_ptr(self.device))
         return sig, inv
 
-    def orth_dev(self, g64) -> float:
+    def orth_dev_t(self, g64) -> torch.Tensor:
+        """max |G - I| as a device scalar (no host synchronisation)."""
         out = torch.empty(1, dtype=F64, device=self.device)
         call("skp_orth_dev_f64", ptr(g64), g64.shape[0], g64.stride(0), ptr(out),
              stream_ptr(self.device))
-        return float(out.item())
+        return out
+
+    def orth_dev(self, g64) -> float:
+        return float(self.orth_dev_t(g64).item())
+
+    def gram64_q(self, q):
+        """Q^T Q (fp64) for randsvd's orthonormality check: from the planes of
+        Q^T directly on the planes path, else the accurate Gram."""
+        if isinstance(q, SplitH2):
+            return self.gram64_planes(q)
+        return self.gram64(q, accurate=True)
 
     def to_compute(self, x64):
         return cast(x64, self.dtype)

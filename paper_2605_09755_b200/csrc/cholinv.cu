@@ -13,6 +13,9 @@
 //                X_IJ = -L_II^{-1} sum_{K=J}^{I-1} L_IK X_KJ,
 //   independent of the other columns (no grid syncs).
 // ~3 nb grid syncs in total instead of ~30 launches + a serial inverse.
+// shift_rel > 0: factor G + shift_rel * max_i G_ii * I instead (shifted
+// CholeskyQR: a Gram whose noise floor would give a non-positive pivot still
+// factors, and range(Y L^{-T}) = range(Y) is kept; see _engine.orthonormalize).
 // info: left untouched on success; set to k+1 if pivot k is not
 // positive/finite, -1 if min L_ii < rel_tol * max L_ii (numerically rank
 // deficient -> eigen-based path).  Callers zero it; failures accumulate, so one
@@ -198,7 +201,7 @@ __device__ __forceinline__ int tile_chol_inv(double (*T)[CB + 1], double (*Li)[C
 //   CTA 0 takes task (p+1, p+1) first and factors the result right away.
 __global__ void __launch_bounds__(kCIThreads, 1)
 cholinv_kernel(const double* __restrict__ G, int n, int64_t ldg, int nb, double rel_tol,
-               double* A, double* Lb, double* X, double* S, double* dinfo, int32_t* info,
+               double shift_rel, double* A, double* Lb, double* X, double* S, double* dinfo, int32_t* info,
                unsigned long long* prof) {
     auto stamp = [&](int slot) {
         if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -214,10 +217,24 @@ cholinv_kernel(const double* __restrict__ G, int n, int64_t ldg, int nb, double 
     const int np = nb * CB;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-    // padded copy: [[G, 0], [0, I]]; X = 0
+    // diagonal shift: every CTA reduces max_i G_ii itself (n loads, no sync)
+    double shift = 0.0;
+    if (shift_rel > 0.0) {
+        __shared__ double s_red[kCIThreads / 32];
+        double mx = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) mx = fmax(mx, G[(int64_t)i * ldg + i]);
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        mx = 0.0;
+        for (int w = 0; w < kCIThreads / 32; ++w) mx = fmax(mx, s_red[w]);
+        shift = shift_rel * mx;
+    }
+    // padded copy: [[G + shift I, 0], [0, I]]; X = 0
     for (int64_t t = gtid; t < (int64_t)np * np; t += gstride) {
         const int i = (int)(t / np), j = (int)(t % np);
-        A[t] = (i < n && j < n) ? G[(int64_t)i * ldg + j] : (i == j ? 1.0 : 0.0);
+        A[t] = (i < n && j < n) ? G[(int64_t)i * ldg + j] + (i == j ? shift : 0.0)
+                                : (i == j ? 1.0 : 0.0);
         X[t] = 0.0;
         S[t] = 0.0;
     }
@@ -364,9 +381,10 @@ extern "C" int64_t skp_cholinv_ws_bytes(int64_t n) {
     return 4 * np * np * (int64_t)sizeof(double) + 64;
 }
 
-extern "C" int skp_cholinv_f64(const double* G, int64_t n, int64_t ld, double rel_tol, double* X,
-                               int32_t* info, void* ws, int64_t ws_bytes, void* stream) {
-    SKP_ARG(n >= 1 && n <= 16384 && ld >= n && G && X && info, "cholinv: bad arguments");
+extern "C" int skp_cholinv_f64(const double* G, int64_t n, int64_t ld, double rel_tol,
+                               double shift_rel, double* X, int32_t* info, void* ws, int64_t ws_bytes, void* stream) {
+    SKP_ARG(n >= 1 && n <= 16384 && ld >= n && G && X && info && shift_rel >= 0.0,
+            "cholinv: bad arguments");
     SKP_ARG(ws && ws_bytes >= skp_cholinv_ws_bytes(n), "cholinv needs %lld bytes of workspace",
             (long long)skp_cholinv_ws_bytes(n));
     cudaStream_t st = SKP_STREAM(stream);
@@ -400,7 +418,7 @@ extern "C" int skp_cholinv_f64(const double* G, int64_t n, int64_t ld, double re
         SKP_CUDA(cudaMemsetAsync(prof, 0, 4 * 1024 * sizeof(unsigned long long), st));
         prof_arg = prof;
     }
-    void* args[] = {(void*)&G, &nn, &ldg, (void*)&nb, &rel_tol, &A, &Lb, &Xp, &Sp, &dinfo, &info, &prof_arg};
+    void* args[] = {(void*)&G, &nn, &ldg, (void*)&nb, &rel_tol, &shift_rel, &A, &Lb, &Xp, &Sp, &dinfo, &info, &prof_arg};
     SKP_CUDA(cudaLaunchCooperativeKernel((void*)cholinv_kernel, dim3(blocks), dim3(kCIThreads), args,
                                          smem, st));
     count_launch();

@@ -289,6 +289,8 @@ def range_finder_sketched(a, spec: RangeFinderSpec, *, timings: dict | None = No
     spec.validate(m, n)
     ph = _Phases(timings is not None)
     qb = _range_finder_dev(op.t, spec, phases=ph, streamed=streamed)
+    if isinstance(a, _convert.DeviceMatrix):
+        a.finite = True           # K2 counted every entry (none non-finite)
     ph.result(timings)
     return _convert.download(qb, op.kind)
 
@@ -340,7 +342,9 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
     hint = {}
     qb = _range_finder_dev(op.t, spec, phases=ph, fro2=fro2, streamed=streamed, hint_out=hint,
                            planes_out=True)
-    u, s, v = _randsvd_dev(op.t, qb, check=False, amax_hint=hint.get("amax"))
+    if isinstance(a, _convert.DeviceMatrix):
+        a.finite = True
+    u, s, v = _randsvd_dev(op.t, qb, check=True, amax_hint=hint.get("amax"))
     ph.mark("randsvd")
     res = SvdResult(_convert.download(u, op.kind), _convert.download(s, op.kind),
                     _convert.download(v, op.kind))

@@ -9,5 +9,5 @@ t = torch.from_numpy(g).cuda(); x = torch.empty_like(t)
 info = torch.zeros(1, dtype=torch.int32, device="cuda")
 wsb = _lib.load().skp_cholinv_ws_bytes(n); ws = _ops.workspace(t.device, wsb)
 for _ in range(3):
-    _lib.call("skp_cholinv_f64", _ops.ptr(t), n, n, 1e-9, _ops.ptr(x), _ops.ptr(info), _ops.ptr(ws), wsb, torch.cuda.current_stream().cuda_stream)
+    _lib.call("skp_cholinv_f64", _ops.ptr(t), n, n, 1e-9, 0.0, _ops.ptr(x), _ops.ptr(info), _ops.ptr(ws), wsb, torch.cuda.current_stream().cuda_stream)
 torch.cuda.synchronize(); print("ok", int(info.item()))

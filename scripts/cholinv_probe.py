@@ -14,7 +14,7 @@ for n in (1, 7, 32, 33, 100, 520, 544, 1050):
     wsb = _lib.load().skp_cholinv_ws_bytes(n)
     ws = _ops.workspace(t.device, wsb)
     st = torch.cuda.current_stream().cuda_stream
-    f = lambda: _lib.call("skp_cholinv_f64", _ops.ptr(t), n, n, 1e-9, _ops.ptr(x), _ops.ptr(info), _ops.ptr(ws), wsb, st)
+    f = lambda: _lib.call("skp_cholinv_f64", _ops.ptr(t), n, n, 1e-9, 0.0, _ops.ptr(x), _ops.ptr(info), _ops.ptr(ws), wsb, st)
     f(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()

@@ -41,9 +41,9 @@ class NumpyBackend:
         bt = bt.astype(np.float64)
         return bt.T @ bt
 
-    def chol_inv64(self, g, rel_tol, lazy=False):
+    def chol_inv64(self, g, rel_tol, lazy=False, shift=0.0):
         try:
-            lmat = np.linalg.cholesky(g)
+            lmat = np.linalg.cholesky(g + shift * max(float(np.diag(g).max()), 0.0) * np.eye(len(g)))
             d = np.abs(np.diag(lmat))
             ok = d.min() >= rel_tol * d.max()
         except np.linalg.LinAlgError:

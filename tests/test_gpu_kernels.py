@@ -503,18 +503,24 @@ def test_fused_cholinv(n):
     info = torch.zeros(1, dtype=torch.int32, device="cuda")
     wsb = _lib.load().skp_cholinv_ws_bytes(n)
     ws = workspace(t.device, wsb)
-    _lib.call("skp_cholinv_f64", ptr(t), n, n, 1e-9, ptr(x), ptr(info), ptr(ws), wsb,
+    _lib.call("skp_cholinv_f64", ptr(t), n, n, 1e-9, 0.0, ptr(x), ptr(info), ptr(ws), wsb,
               torch.cuda.current_stream().cuda_stream)
     assert int(info.item()) == 0
     xi = x.cpu().numpy()
     lmat = np.linalg.cholesky(g)
     np.testing.assert_allclose(xi @ lmat, np.eye(n), atol=1e-7)
     assert np.all(np.triu(xi, 1) == 0)
+    # shifted factorisation (first pass of shifted CholeskyQR3): G + 1e-3 max G_ii I
+    _lib.call("skp_cholinv_f64", ptr(t), n, n, 0.0, 1e-3, ptr(x), ptr(info), ptr(ws), wsb,
+              torch.cuda.current_stream().cuda_stream)
+    assert int(info.item()) == 0
+    ls = np.linalg.cholesky(g + 1e-3 * np.diag(g).max() * np.eye(n))
+    np.testing.assert_allclose(x.cpu().numpy() @ ls, np.eye(n), atol=1e-9)
     # rank check and indefinite detection
     g2 = g.copy()
     g2[n // 2, n // 2] = -1.0 if n > 1 else -1.0
     t2 = torch.from_numpy(g2).cuda()
-    _lib.call("skp_cholinv_f64", ptr(t2), n, n, 1e-9, ptr(x), ptr(info), ptr(ws), wsb,
+    _lib.call("skp_cholinv_f64", ptr(t2), n, n, 1e-9, 0.0, ptr(x), ptr(info), ptr(ws), wsb,
               torch.cuda.current_stream().cuda_stream)
     assert int(info.item()) != 0
 
