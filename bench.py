@@ -1,13 +1,15 @@
 #!/usr/bin/env python
 """Benchmark: row-sharded sketched rSVD on 1..8 B200s (one process per GPU).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 A "step" is one full pass of the hot path over the resident input: CountSketch
-draw (K1) -> A~ = A S (K2, fused ||A||_F^2 + finiteness) -> Y = A~ Omega ->
-q x {CholeskyQR2(Y); Z = sum_p A~_p^T Y_p (NCCL); Y = A~ Z} -> CholeskyQR2 ->
-B = sum_p Q_p^T A_p (NCCL) -> Gram + Jacobi -> U, sigma, V.
+draw (K1) -> A~ = A S (K2, fused finiteness test) -> Y = A~ Omega ->
+q x {shifted CholeskyQR(Y); Z = sum_p A~_p^T Y_p (NCCL); Y = A~ Z} ->
+shifted CholeskyQR3 -> ||Q^T Q - I|| check -> B = sum_p Q_p^T A_p (NCCL) ->
+fp64 Gram + eigensolver -> U, sigma, V.  Default workload: C5 (BASELINE
+configs[4], m = 2^20, n = 2^15, l = 8000, q = 4; A = 128 GiB resident).
 
 value      = device time of one rSVD (ms, max over ranks), inputs resident in HBM.
 e2e        = the same through the public API ``paper_2605_09755_b200.rsvd`` with
@@ -15,10 +17,11 @@ e2e        = the same through the public API ``paper_2605_09755_b200.rsvd`` with
              U, sigma, V copied back (D2H inside).
 roofline   = the dominant kernel of the step, measured live with CUDA events.
 cpu_baseline / --impl reference = the oracle port (oracle/skp_oracle.py, the
-             reference's algorithm on numpy/scipy) on a bounded row slab,
-             extrapolated per phase to the full workload.
-Inputs (A = 17 GB at C3) are far larger than the 126 MB L2, so no flush is
-needed between steps.
+             reference's algorithm on numpy/scipy) on the workload's first
+             rows, extrapolated per phase to the full workload; slab_parity
+             compares the GPU path with it on that slab.
+Inputs (A = 128 GiB at C5, 17 GB at C3) are far larger than the 126 MB L2,
+so no flush is needed between steps.
 """
 from __future__ import annotations
 
@@ -44,7 +47,9 @@ CONFIGS = {
     "C1": dict(m=2000, n=1000, l=200, s=8, k=20, r2=30, q=2, dtype="f64", gen="c1"),
     "C2": dict(m=20000, n=10000, l=2000, s=8, k=100, r2=110, q=3, dtype="f32", gen="c2"),
     "C3": dict(m=262144, n=16384, l=4000, s=8, k=500, r2=520, q=3, dtype="f32", gen="c3"),
-    "C5": dict(m=1048576, n=32768, l=8000, s=8, k=1000, r2=1050, q=4, dtype="f32", gen="c5"),
+    # the headline: the largest config that fits one B200 (BASELINE configs[4], l = 8000, q = 4)
+    "C5": dict(m=1048576, n=32768, l=8000, s=8, k=1000, r2=1050, q=4, dtype="f32", gen="c5",
+               seed=5),
 }
 
 
@@ -130,19 +135,30 @@ def flops_of(cfg):
 
 
 # ---------------------------------------------------------- CPU baseline ----
-def cpu_baseline(cfg, sample_rows: int, reps: int = 1):
-    """Oracle port on a row slab; phases extrapolated linearly in m (except
-    those independent of m).  Returns (ms for the full workload, details)."""
+def workload_slab(cfg, rows: int):
+    """The first ``rows`` rows of the workload's own matrix (same generator,
+    spectrum and noise as the timed run), as float32/float64 numpy."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t = make_input(cfg, 0, min(rows, cfg["m"]), dev)
+    out = t.cpu().numpy()
+    del t
+    torch.cuda.empty_cache()
+    return out
+
+
+def cpu_baseline(cfg, sample_rows: int, reps: int = 1, slab=None):
+    """Oracle port on a row slab of the workload; phases extrapolated linearly
+    in m (except those independent of m: the sketch draw, Omega, the SVD of
+    the r2 x n matrix B).  Returns (ms for the full workload, details, Q)."""
     from oracle import skp_oracle as o
     m, n = cfg["m"], cfg["n"]
-    rows = min(sample_rows, m)
-    rng = np.random.default_rng(0)
-    # same structure as the workload: low rank + noise (values only shape the flops)
-    r = min(256, n)
-    a = ((rng.standard_normal((rows, r)) @ rng.standard_normal((r, n))) / math.sqrt(r * n)).astype(
-        np.float32 if cfg["dtype"] == "f32" else np.float64)
-    spec = o.Spec(k=cfg["k"], l=cfg["l"], r1=cfg["l"], r2=cfg["r2"], q=cfg["q"], seed=3, s=cfg["s"])
+    a = workload_slab(cfg, sample_rows) if slab is None else slab
+    rows = a.shape[0]
+    spec = o.Spec(k=cfg["k"], l=cfg["l"], r1=cfg["l"], r2=cfg["r2"], q=cfg["q"],
+                  seed=cfg.get("seed", 3), s=cfg["s"])
     best = None
+    qb = None
     for _ in range(reps):
         t = {}
         qb = o.range_finder_sketched(a, spec, timings=t)
@@ -157,7 +173,30 @@ def cpu_baseline(cfg, sample_rows: int, reps: int = 1):
     linear = ("cast", "apply_right", "power", "orth", "qta")
     full = sum(v * (scale if k in linear else 1.0) for k, v in best.items())
     return full * 1e3, {"phases_s_sample": {k: round(v, 4) for k, v in best.items()},
-                        "rows_sampled": rows, "extrapolated_to_m": m}
+                        "rows_sampled": rows, "extrapolated_to_m": m,
+                        "q_columns_kept": int(qb.shape[1])}, (a, qb, spec)
+
+
+def slab_parity(cfg, a, qb, spec_o):
+    """The GPU path (rsvd, as timed) against the oracle on the same slab:
+    max relative sigma difference over the top k, and both rel_err values."""
+    import torch
+    import paper_2605_09755_b200 as skp
+    from oracle import skp_oracle as o
+    _, so, _ = o.randsvd(a, qb)
+    eo = o.proj_rel_error(a, qb)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    spec = spec_of(cfg, spec_o.seed)
+    res, rel = skp.rsvd(torch.from_numpy(a).to(dev), spec, with_error=True)
+    k = cfg["k"]
+    sg = res.sigma.double().cpu().numpy()
+    return {"rows": int(a.shape[0]), "k": k,
+            "sigma_max_rel_diff": float(np.max(np.abs(sg[:k] - so[:k]) / so[:k])),
+            "sigma_1": [float(sg[0]), float(so[0])],
+            "sigma_k": [float(sg[k - 1]), float(so[k - 1])],
+            "rel_err": [float(rel), float(eo)],
+            "rel_err_rel_diff": float(abs(rel - eo) / eo) if eo > 0 else 0.0,
+            "tolerance": {"sigma": 1e-5, "rel_err": 1e-3}}
 
 
 def host_threads():
@@ -168,16 +207,44 @@ def host_threads():
 
 
 # --------------------------------------------------------------- the arm ----
+def _traffic(config: str, key: str):
+    """DRAM bytes per launch of a kernel at a config, from the committed ncu
+    --set full capture (profiles/traffic.json, scripts/summarize_ncu.py)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh)
+    except (OSError, ValueError):
+        return None, None
+    t = tr.get(config, {}).get(key)
+    if t is None:
+        return None, None
+    return t["bytes_per_launch"], "profiles/traffic.json <- " + t["source"]
+
+
+def _time_launches(fn, reps: int = 5) -> float:
+    """Average ms per call of fn on the current stream (CUDA events, warm)."""
+    import torch
+    for _ in range(2):
+        fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def run_ours(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     import paper_2605_09755_b200 as skp
-    from paper_2605_09755_b200 import _lib, distributed as D
+    from paper_2605_09755_b200 import _lib, _ops, distributed as D
     from paper_2605_09755_b200.sketching import make_sketch, substream
 
     device = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(device)
-    comm = D.TorchComm() if world > 1 else None
+    comm = D.TorchComm() if world > 1 else _LocalComm()
     m, n = cfg["m"], cfg["n"]
     row0, rows = D.shard_rows(m, world, rank)
     a = make_input(cfg, row0, rows, device)
@@ -189,11 +256,11 @@ def run_ours(args, cfg, rank, world, local_rank):
             dist.barrier()
 
     def step(timings=None, with_error=False):
-        # the timed step is the rSVD (range finder + randsvd) as the reference
-        # times it; the quality number ||A - QQ^T A|| / ||A|| is evaluated once
-        # after the timed loop (it needs an extra pass for ||A||_F)
-        return D.rsvd_sharded(a, spec, m, comm if world > 1 else _LocalComm(), timings,
-                              with_error=with_error)
+        # the timed step is the rSVD (range finder + randsvd, with the
+        # reference's orthonormality check) as the reference times it; the
+        # quality number ||A - QQ^T A|| / ||A|| is evaluated once after the
+        # timed loop (it needs ||A||_F, fused into the sketch)
+        return D.rsvd_sharded(a, spec, m, comm, timings, with_error=with_error)
 
     for _ in range(args.warmup):
         step()
@@ -224,10 +291,9 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     # ---- dominant-kernel measurements (live, CUDA events on this stream) ----
     hbm, bf16, bf16_sus, peak_src = load_peaks()
-    from paper_2605_09755_b200 import _ops
-    sk = make_sketch("countsketch", n, cfg["l"], substream(spec.seed, 0), s=cfg["s"], device=device)
-    atil = _ops.empty2d(rows, cfg["l"], a.dtype, device)
-    fro2 = torch.zeros(1, dtype=torch.float64, device=device)
+    l, r2, s_ = cfg["l"], cfg["r2"], cfg["s"]
+    sk = make_sketch("countsketch", n, l, substream(spec.seed, 0), s=s_, device=device)
+    atil = _ops.empty2d(rows, l, a.dtype, device)
     nonfinite = torch.zeros(1, dtype=torch.int64, device=device)
     # the kernel the range finder runs: K2 v2 (row gather) when it applies, else v1
     v2 = sk.right_permuted(a, out=atil, nonfinite=nonfinite) is not None
@@ -237,24 +303,15 @@ def run_ours(args, cfg, rank, world, local_rank):
             sk.right_permuted(a, out=atil, nonfinite=nonfinite)
         else:
             sk.right(a, out=atil, nonfinite=nonfinite)
-    for _ in range(2):
-        run_sketch()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 5
-    e0.record()
-    for _ in range(reps):
-        run_sketch()
-    e1.record()
-    torch.cuda.synchronize()
-    sketch_ms = e0.elapsed_time(e1) / reps
+    sketch_ms = _time_launches(run_sketch)
     esz = a.element_size()
-    sketch_bytes = rows * n * esz + rows * cfg["l"] * esz + n * cfg["s"] * 5 + (cfg["l"] + 1) * 4
+    sketch_bytes = rows * n * esz + rows * l * esz + n * s_ * 5 + (l + 1) * 4
     sketch_gbs = sketch_bytes / (sketch_ms * 1e-3) / 1e9
     # power-iteration GEMM: Y = A~ Z  (rows x l) . (l x r2), operands laid out
     # as in the pipeline (128-byte padded rows)
-    z = _ops.empty2d(cfg["l"], cfg["r2"], a.dtype, device)
+    z = _ops.empty2d(l, r2, a.dtype, device)
     z.normal_()
-    y = _ops.empty2d(rows, cfg["r2"], a.dtype, device)
+    y = _ops.empty2d(rows, r2, a.dtype, device)
     # the kernel the power iteration runs: 3xFP16 on the pre-split A~ where
     # the backend prepares it (fp32, tcgen05), else 3xTF32 / SIMT
     pa = _ops.CudaBackend(device, a.dtype).prepare(atil, inplace=True)  # (A~ is not reused)
@@ -264,109 +321,67 @@ def run_ours(args, cfg, rank, world, local_rank):
         run_gemm = lambda: _ops.gemm_h3(pa, sz, out=y)
     else:
         run_gemm = lambda: _ops.gemm(atil, z, out=y)
-    for _ in range(2):
-        run_gemm()
-    e0.record()
-    for _ in range(reps):
-        run_gemm()
-    e1.record()
-    torch.cuda.synchronize()
-    gemm_ms = e0.elapsed_time(e1) / reps
-    gemm_flop = 2.0 * rows * cfg["l"] * cfg["r2"]
+    gemm_ms = _time_launches(run_gemm)
+    del pa, atil, y, z, run_gemm
+    gemm_flop = 2.0 * rows * l * r2
     gemm_tflops = gemm_flop / (gemm_ms * 1e-3) / 1e12
     power_f, orth_f, qta_f = flops_of(cfg)
     tc = bool(_lib.load().skp_has_tcgen05())
     # tensor-pipe view: 3 MMAs per useful MAC -- kind::f16 (3xFP16) at the
     # measured dense bf16/fp16 rate, or kind::tf32 (3xTF32) at bf16 / 2
     pipe_tflops = gemm_tflops * 3 if (tc and cfg["dtype"] == "f32") else gemm_tflops
-    tf32_peak = bf16 if h3 else bf16 / 2.0
+    pipe_peak = bf16 if h3 else bf16 / 2.0
     power_tflops = (power_f / world) / (phases.get("power", float("nan")) * 1e-3) / 1e12
-    dominant = "power" if phases.get("power", 0) >= phases.get("apply_right", 0) else "sketch"
-    # DRAM bytes per launch of the dominant kernel from the committed ncu
-    # --set full capture (profiles/traffic.json, scripts/summarize_ncu.py traffic)
-    try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                               "traffic.json")) as fh:
-            _tr = json.load(fh)
-    except (OSError, ValueError):
-        _tr = {}
-    def traffic_of(key):
-        t = _tr.get(key)
-        return None if t is None else t["bytes_per_launch"]
-
-    def traffic_src(key):
-        t = _tr.get(key)
-        return None if t is None else "profiles/traffic.json <- " + t["source"]
-    if dominant == "power":
-        roof = {"kernel": "gemm_nn A~.Z (power iteration)" + (
-                    " tcgen05 3xFP16 (pre-split A~)" if h3 else " tcgen05 3xTF32" if tc else " SIMT"),
-                # achieved = ALGORITHMIC flop (2 m l r2) per launch / launch time,
-                # peak = the measured dense bf16 figure as is; the fp32-accurate
-                # product costs 3 f16 MMAs (3xTF32: 3 at half rate) per MAC, so
-                # the tensor pipe itself runs at "pipe_frac" of that peak
-                "bound": "tensor", "achieved": round(gemm_tflops, 2), "peak": round(bf16, 1),
-                "unit": "TFLOP/s", "frac": round(gemm_tflops / bf16, 4),
-                "emulation": {"mma_per_mac": 3 if (tc and cfg["dtype"] == "f32") else 1,
-                              "pipe_tflops": round(pipe_tflops, 2),
-                              "pipe_peak": round(tf32_peak, 1),
-                              "pipe_frac": round(pipe_tflops / tf32_peak, 4)},
-                "traffic": traffic_of("gemm_h3_nn" if h3 else "gemm_tc_nn"),
-                "traffic_unit": "DRAM bytes per launch (ncu --set full)",
-                "traffic_source": traffic_src("gemm_h3_nn" if h3 else "gemm_tc_nn"),
-                "ms_per_launch": round(gemm_ms, 4),
-                "peak_note": (f"{peak_src} dense bf16 {bf16} TFLOP/s; pipe peak = the same for "
-                              "kind::f16 (3xFP16)" if h3 else
-                              f"{peak_src} dense bf16 {bf16} TFLOP/s; pipe peak = bf16/2 for kind::tf32"),
-                "algorithmic_flop_per_launch": gemm_flop}
-    else:
-        roof = {"kernel": "sketch_gather (K2 v2)" if v2 else "sketch_right (K2 v1)", "bound": "hbm", "achieved": round(sketch_gbs, 1),
-                "peak": hbm, "unit": "GB/s", "frac": round(sketch_gbs / hbm, 4),
-                "traffic": traffic_of("sketch_gather" if v2 else "sketch_rows"),
-                "traffic_unit": "DRAM bytes per launch (ncu --set full)",
-                "traffic_source": traffic_src("sketch_gather" if v2 else "sketch_rows"),
-                "ms_per_launch": round(sketch_ms, 4), "algorithmic_bytes_per_launch": sketch_bytes}
+    gkey = "gemm_h3_nn" if h3 else "gemm_tc_nn"
+    skey = "sketch_gather" if v2 else "sketch_rows"
+    g_tr, g_src = _traffic(args.config, gkey)
+    s_tr, s_src = _traffic(args.config, skey)
+    roof = {"kernel": "gemm_nn A~.Z (power iteration)" + (
+                " tcgen05 3xFP16 (pre-split A~)" if h3 else " tcgen05 3xTF32" if tc else " SIMT"),
+            # achieved = ALGORITHMIC flop (2 m l r2) per launch / launch time,
+            # peak = the measured dense bf16 figure as is; the fp32-accurate
+            # product costs 3 f16 MMAs (3xTF32: 3 at half rate) per MAC, so
+            # the tensor pipe itself runs at "pipe_frac" of that peak
+            "bound": "tensor", "achieved": round(gemm_tflops, 2), "peak": round(bf16, 1),
+            "unit": "TFLOP/s", "frac": round(gemm_tflops / bf16, 4),
+            "emulation": {"mma_per_mac": 3 if (tc and cfg["dtype"] == "f32") else 1,
+                          "pipe_tflops": round(pipe_tflops, 2),
+                          "pipe_peak": round(pipe_peak, 1),
+                          "pipe_frac": round(pipe_tflops / pipe_peak, 4),
+                          "pipe_peak_sustained": round(bf16_sus if h3 else bf16_sus / 2, 1),
+                          "pipe_frac_sustained": round(pipe_tflops / (bf16_sus if h3 else bf16_sus / 2), 4)},
+            "traffic": g_tr, "traffic_unit": "DRAM bytes per launch (ncu --set full)",
+            "traffic_source": g_src, "ms_per_launch": round(gemm_ms, 4),
+            "peak_note": (f"{peak_src} dense bf16 {bf16} TFLOP/s (burst; sustained "
+                          f"{bf16_sus}); pipe peak = the same for kind::f16 (3xFP16)" if h3 else
+                          f"{peak_src} dense bf16 {bf16} TFLOP/s; pipe peak = bf16/2 for kind::tf32"),
+            "algorithmic_flop_per_launch": gemm_flop,
+            "share_of_step": round(gemm_ms * (1 + 2 * cfg["q"]) / ms, 3)}
     extra = {
         "sketch": {"kernel": "sketch_gather (K2 v2)" if v2 else "sketch_right (K2 v1)",
-                   "ms": round(sketch_ms, 4), "GB/s": round(sketch_gbs, 1),
-                   "frac_hbm": round(sketch_gbs / hbm, 4), "bytes": sketch_bytes},
+                   "bound": "hbm", "ms": round(sketch_ms, 4), "GB/s": round(sketch_gbs, 1),
+                   "peak": hbm, "frac_hbm": round(sketch_gbs / hbm, 4), "bytes": sketch_bytes,
+                   "traffic": s_tr, "traffic_source": s_src,
+                   "share_of_step": round(sketch_ms / ms, 3)},
         "power_gemm": {"ms": round(gemm_ms, 4), "useful_TFLOP/s": round(gemm_tflops, 2),
-                       "pipe_frac": round(pipe_tflops / tf32_peak, 4)},
+                       "pipe_frac": round(pipe_tflops / pipe_peak, 4)},
         "power_phase_TFLOP/s": round(power_tflops, 2),
     }
+    # slab of the workload for the CPU baseline / oracle parity (rank 0)
+    slab = a[:min(args.cpu_rows, rows)].cpu().numpy() if rank == 0 else None
 
     # ---- end to end through the public API from pinned host memory ----------
     e2e = None
+    e2e_note = None
+    holder = [a]
+    del a                     # (also unbinds the closures' cell: _e2e can free it)
     if not args.no_e2e:
-        host = a.cpu().pin_memory()
-        torch.cuda.synchronize()
-        for _ in range(max(1, min(args.warmup, 2))):
-            skp.rsvd(host, spec) if world == 1 else _e2e_sharded(host, spec, m, comm, device, D)
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        k2 = max(1, min(args.steps, 3))
-        res = None
-        for _ in range(k2):
-            if world == 1:
-                res = None   # the caller is done with the previous result
-                res = skp.rsvd(host, spec)
-                out_b = res.U.numel() * res.U.element_size() + res.V.numel() * res.V.element_size() \
-                    + res.sigma.numel() * res.sigma.element_size()
-            else:
-                out_b = _e2e_sharded(host, spec, m, comm, device, D)
-        torch.cuda.synchronize()
-        barrier()
-        e2e_ms = (time.perf_counter() - t0) * 1e3 / k2
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        e2e = {"value": round(e2e_ms, 3), "unit": "ms",
-               "h2d_bytes_per_step": int(host.numel() * host.element_size()),
-               "d2h_bytes_per_step": int(out_b), "steps": k2}
+        e2e, e2e_note = _e2e(args, holder, spec, m, comm, device, world, barrier, D, skp)
+    holder.clear()
+    torch.cuda.empty_cache()
 
     if rank != 0:
-        return None
+        return None, None
     line = {
         "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
@@ -374,8 +389,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "dtype": cfg["dtype"] + ("(power: 3xFP16, other GEMMs: 3xTF32, tcgen05)" if h3 else
                                  "(3xTF32 tcgen05)" if tc and cfg["dtype"] == "f32" else ""),
         "data": "synthetic (seeded, BASELINE config recipe; random-init factors, no dataset)",
-        "config": {"workload": args.config, "m": m, "n": n, "l": cfg["l"], "s": cfg["s"],
-                   "k": cfg["k"], "r2": cfg["r2"], "q": cfg["q"],
+        "config": {"workload": args.config, "m": m, "n": n, "l": l, "s": s_,
+                   "k": cfg["k"], "r2": r2, "q": cfg["q"],
                    "parallelism": f"rows sharded x{world} (NCCL allreduce of l x r2 / r2 x r2 / r2 x n)",
                    "l2": "no flush: A is far larger than the 126 MB L2"},
         "phases_ms": {k: round(v, 3) for k, v in phases.items()},
@@ -385,7 +400,81 @@ def run_ours(args, cfg, rank, world, local_rank):
         "clocks": clocks,
         "e2e": e2e,
     }
-    return line
+    if e2e_note:
+        line["e2e_note"] = e2e_note
+    return line, slab
+
+
+def _e2e(args, holder, spec, m, comm, device, world, barrier, D, skp):
+    """e2e through the public API: the input in pinned host memory, H2D inside
+    the timed region (streamed behind the sketch) and U, sigma, V copied back.
+    Also times the reference's own two-call sequence on one device_matrix
+    handle (range_finder_sketched + randsvd, one upload)."""
+    import torch
+    import torch.distributed as dist
+    a = holder[0]
+    nbytes = a.numel() * a.element_size()
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = None
+    if avail is not None and avail < nbytes + (24 << 30):
+        return None, f"host RAM {avail >> 30} GiB < input {nbytes >> 30} GiB + 24 GiB margin"
+    host = torch.empty(tuple(a.shape), dtype=a.dtype, pin_memory=True)
+    host.copy_(a)
+    torch.cuda.synchronize()
+    # the device copy of A is released first: the public call allocates its own
+    del a
+    holder.clear()
+    torch.cuda.empty_cache()
+
+    def one():
+        if world == 1:
+            res = skp.rsvd(host, spec)
+            return (res.U.numel() * res.U.element_size() + res.V.numel() * res.V.element_size()
+                    + res.sigma.numel() * res.sigma.element_size())
+        return _e2e_sharded(host, spec, m, comm, device, D)
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        one()
+    barrier()
+    torch.cuda.synchronize()
+    k2 = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    out_b = 0
+    for _ in range(k2):
+        out_b = one()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / k2
+    pair_ms = None
+    if world == 1:
+        # the drop-in pair: device_matrix(host) -> range_finder_sketched -> randsvd
+        def pair():
+            h = skp.device_matrix(host)
+            qb = skp.range_finder_sketched(h, spec)
+            return skp.randsvd(h, qb)
+        pair()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pair()
+        torch.cuda.synchronize()
+        pair_ms = (time.perf_counter() - t0) * 1e3
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": round(e2e_ms, 3), "unit": "ms",
+           "h2d_bytes_per_step": int(nbytes), "d2h_bytes_per_step": int(out_b), "steps": k2,
+           "api": "paper_2605_09755_b200.rsvd(pinned host tensor)" if world == 1 else
+                  "distributed.rsvd_sharded on the rank's pinned slab"}
+    if pair_ms is not None:
+        e2e["drop_in_pair_ms"] = round(pair_ms, 3)
+        e2e["drop_in_pair_api"] = ("device_matrix(host) -> range_finder_sketched -> randsvd "
+                                   "(one upload; Q returned to and re-read from the host)")
+    del host
+    return e2e, None
 
 
 class _LocalComm:
@@ -403,28 +492,42 @@ def _e2e_sharded(host, spec, m, comm, device, D):
     return u_h.numel() * 4 + s_h.numel() * 8 + v_h.numel() * 4
 
 
+REF_MAX_STEPS, REF_MAX_WARMUP = 5, 1
+
+
 def run_reference(args, cfg):
+    """The reference's CPU path (the oracle port) on the workload's first
+    rows.  One sample is a full range finder + randsvd on the slab (C5: ~20 s
+    on 16 cores, most of it m-independent: the sketch draw and the SVD of the
+    r2 x n matrix B), so at most REF_MAX_STEPS samples (+ REF_MAX_WARMUP) are
+    timed and the JSON line states the counts actually run."""
     ncores = host_threads()
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ.setdefault(var, str(ncores))
-    sample = args.cpu_rows
+    slab = workload_slab(cfg, args.cpu_rows)
+    steps = max(1, min(args.steps, REF_MAX_STEPS))
+    warm = min(args.warmup, REF_MAX_WARMUP)
     vals = []
     det = None
-    for i in range(args.warmup + args.steps):
-        v, det = cpu_baseline(cfg, sample)
-        if i >= args.warmup:
+    for i in range(warm + steps):
+        v, det, _ = cpu_baseline(cfg, args.cpu_rows, slab=slab)
+        if i >= warm:
             vals.append(v)
     val = statistics.median(vals)
     return {
         "metric": METRIC, "impl": "reference", "value": round(val, 1), "unit": "ms",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
         "ms_per_step": round(val, 1), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64 (numpy/scipy, as the reference computes)",
-        "data": "synthetic", "config": {"workload": args.config, **{k: cfg[k] for k in
-                                                                    ("m", "n", "l", "s", "k", "r2", "q")}},
+        "data": "synthetic (the workload's own first rows: same generator, spectrum, noise)",
+        "config": {"workload": args.config, **{k: cfg[k] for k in
+                                               ("m", "n", "l", "s", "k", "r2", "q")}},
         "cpu_baseline": {"value": round(val, 1), "unit": "ms", "cores": ncores, "kind": "port",
-                         "sample": f"{det['rows_sampled']} of {cfg['m']} rows, phases extrapolated "
-                                   f"linearly in m (sketch/SVD-of-B phases not scaled)",
+                         "sample": f"rows 0..{det['rows_sampled']} of the {cfg['m']}-row workload, "
+                                   f"m-linear phases extrapolated x{cfg['m'] / det['rows_sampled']:g}"
+                                   " (sketch draw, Omega, SVD of B not scaled); median of "
+                                   f"{steps} samples",
                          **det},
         "e2e": {"value": round(val, 1), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -436,11 +539,13 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--q", type=int, default=None)
     ap.add_argument("--l", type=int, default=None)
-    ap.add_argument("--cpu-rows", type=int, default=4096)
+    ap.add_argument("--cpu-rows", type=int, default=None,
+                    help="CPU slab rows (default: 4096, or l rounded up to 1024 when l > 4096 "
+                         "-- the reference's spec.validate needs l <= rows)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -451,6 +556,8 @@ def main():
         cfg["q"] = args.q
     if args.l is not None:
         cfg["l"] = args.l
+    if args.cpu_rows is None:
+        args.cpu_rows = max(4096, -(-cfg["l"] // 1024) * 1024)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
@@ -469,14 +576,16 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group("gloo")
-    line = run_ours(args, cfg, rank, world, local_rank)
+    line, slab = run_ours(args, cfg, rank, world, local_rank)
     if line is not None:
         if world == 1 and not args.no_cpu:
-            v, det = cpu_baseline(cfg, args.cpu_rows)
-            line["cpu_baseline"] = {"value": round(v, 1), "unit": "ms", "cores": host_threads(),
-                                    "kind": "port",
-                                    "sample": f"{det['rows_sampled']} of {cfg['m']} rows, "
-                                              f"extrapolated linearly in m", **det}
+            v, det, (a_s, qb_s, spec_o) = cpu_baseline(cfg, args.cpu_rows, slab=slab)
+            line["cpu_baseline"] = {
+                "value": round(v, 1), "unit": "ms", "cores": host_threads(), "kind": "port",
+                "sample": f"rows 0..{det['rows_sampled']} of the {cfg['m']}-row workload, "
+                          f"m-linear phases extrapolated x{cfg['m'] / det['rows_sampled']:g} "
+                          "(sketch draw, Omega, SVD of B not scaled)", **det}
+            line["slab_parity"] = slab_parity(cfg, a_s, qb_s, spec_o)
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

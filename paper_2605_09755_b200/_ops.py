@@ -670,12 +670,13 @@ class CudaBackend:
         """Lazy shifted CholeskyQR3 of Y given as Y^T planes (_engine.orthonormalize):
         pass 1 on G + shift, pass 2 with the rank test t2 on its pivots, pass 3.
         Returns Q (fp32, rows x c), or with planes_out the planes of Q^T (what
-        randsvd consumes)."""
+        randsvd consumes).  yt is consumed (its buffers are reused)."""
         x1 = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), 0.0, lazy=True, shift=shift)
         q1t = gemm_h3_emit_t(yt, split_h2(self.to_compute(x1)), ta=True, e_fixed=14,
                              overflow=self.fail[1:])
         x2 = self.chol_inv64(comm.allreduce_(self.gram64_planes(q1t)), t2, lazy=True)
-        q2t = gemm_h3_emit_t(q1t, split_h2(self.to_compute(x2)), ta=True, e_fixed=14,
+        # (Q2 goes into Y's planes: two plane buffers in flight, not three)
+        q2t = gemm_h3_emit_t(q1t, split_h2(self.to_compute(x2)), ta=True, e_fixed=14, out=yt,
                              overflow=self.fail[1:])
         x3 = self.chol_inv64(comm.allreduce_(self.gram64_planes(q2t)), 0.0, lazy=True)
         if planes_out:

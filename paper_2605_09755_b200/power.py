@@ -250,9 +250,14 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     be.lazy_reset()
     y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total,
                               lazy=True)
+    # A~ is released before the final orthonormalisation (C5 on one GPU: A
+    # 128 GiB + A~ 31 GiB leave no room for Q); the rare eager rerun below
+    # sketches again
+    atil = None
     ph.mark("power")
     qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total, lazy=True,
                                 planes_out=planes_out)
+    del y
     ph.mark("orth")
     nbad = int(bad.item())
     omega_failed = nbad >= _ops.OMEGA_FAIL_MARK
@@ -273,6 +278,11 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
         # (a device Omega that could not complete is redrawn by numpy itself)
         omega = omega_for(perm, host=omega_failed)
     if plan_failed or omega_failed or be.lazy_failed(comm):
+        if atil is None:
+            qb = None
+            scratch = torch.zeros(1, dtype=torch.int64, device=dev)
+            got = sk.right_permuted(a, nonfinite=scratch) if perm is not None else None
+            atil = got[0] if got is not None else sk.right(a, nonfinite=scratch)
         y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total)
         qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total)
     if hint_out is not None and e_io is not None and not plan_failed:
