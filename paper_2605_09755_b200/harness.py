@@ -29,7 +29,6 @@ from __future__ import annotations
 
 import argparse
 import csv
-import re
 from dataclasses import dataclass, field, fields
 
 import numpy as np
@@ -132,19 +131,44 @@ def _rotate_spectrum(m: int, n: int, spectrum: np.ndarray, seed: int) -> np.ndar
     return datagen.rotate_spectrum(m, n, spectrum, seed)
 
 
+_RECIPES = ("polydecay", "expdecay", "lowrank")
+
+
+def _leading_digits(s: str, i: int) -> int:
+    """End of the run of decimal digits starting at s[i]."""
+    while i < len(s) and s[i].isdecimal():
+        i += 1
+    return i
+
+
+def _recipe(text: str):
+    """(name, m, n, options) of a synthetic dataset spec, or None.
+
+    Grammar (the reference's pattern, bench.py:88-107): NAME ":" DIGITS "x"
+    DIGITS REST, where REST is ``:key=value`` fields and holds no newline
+    (one trailing newline on the whole text is tolerated)."""
+    body = text[:-1] if text.endswith("\n") else text
+    name, colon, tail = body.partition(":")
+    if not colon or name not in _RECIPES or "\n" in tail:
+        return None
+    i = _leading_digits(tail, 0)
+    if i == 0 or tail[i:i + 1] != "x":
+        return None
+    j = _leading_digits(tail, i + 1)
+    if j == i + 1:
+        return None
+    fields = (f.partition("=") for f in tail[j:].split(":") if f)
+    return name, int(tail[:i]), int(tail[i + 1:j]), {k: v for k, _, v in fields}
+
+
 def synthetic(text: str) -> np.ndarray | None:
     """The reference's synthetic recipes (bench.py:88-107, data_io.py:49-81):
     ``polydecay:MxN:seed=S``, ``expdecay:MxN:rate=R:seed=S``,
     ``lowrank:MxN:rank=R:noise=E:seed=S``; None for anything else."""
-    match = re.match(r"^(polydecay|expdecay|lowrank):(\d+)x(\d+)(.*)$", text)
-    if not match:
+    parsed = _recipe(text)
+    if parsed is None:
         return None
-    name, m, n = match.group(1), int(match.group(2)), int(match.group(3))
-    opts = {}
-    for part in match.group(4).split(":"):
-        if part:
-            key, _, value = part.partition("=")
-            opts[key] = value
+    name, m, n, opts = parsed
     seed = int(opts.get("seed", 0))
     p = min(m, n)
     if name == "polydecay":

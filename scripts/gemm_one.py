@@ -1,5 +1,6 @@
-"""One C3-shape GEMM (for ncu): python scripts/gemm_one.py nn|tn|qta [3xtf32|h3|h3s] [reps]
-(qta: randsvd's B^T = A^T Q with A 262144 x 16384)"""
+"""One config-shape GEMM (for ncu):
+    python scripts/gemm_one.py nn|tn|qta [3xtf32|h3|h3s] [reps] [C3|C5]
+(qta: randsvd's B^T = A^T Q with A m x n)"""
 import sys
 import torch
 sys.path.insert(0, ".")
@@ -7,13 +8,14 @@ from paper_2605_09755_b200 import _ops
 kind = sys.argv[1] if len(sys.argv) > 1 else "nn"
 mode = sys.argv[2] if len(sys.argv) > 2 else "3xtf32"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-m, l, r2 = 262144, 4000, 520
+cfg = sys.argv[4] if len(sys.argv) > 4 else "C3"
+m, n, l, r2 = {"C3": (262144, 16384, 4000, 520), "C5": (1048576, 32768, 8000, 1050)}[cfg]
 torch.manual_seed(0)
 at = _ops.empty2d(m, l, torch.float32, "cuda")
 at.normal_()
 if kind == "qta":
     del at
-    a = _ops.empty2d(m, 16384, torch.float32, "cuda")
+    a = _ops.empty2d(m, n, torch.float32, "cuda")
     a.normal_()
     q = _ops.empty2d(m, r2, torch.float32, "cuda")
     q.normal_()

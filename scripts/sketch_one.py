@@ -8,7 +8,8 @@ sys.path.insert(0, ".")
 from paper_2605_09755_b200.sketching import make_sketch
 mode = sys.argv[1] if len(sys.argv) > 1 else "v2"
 m, n, l = (int(x) for x in (sys.argv[2:5] if len(sys.argv) > 4 else (262144, 16384, 4000)))
-a = torch.randn(m, n, device="cuda")
+a = torch.empty(m, n, device="cuda")
+a.normal_()
 op = make_sketch("countsketch", n, l, 7, s=8)
 out = torch.empty(m, l, device="cuda")
 nonfinite = torch.zeros(1, dtype=torch.int64, device="cuda")

@@ -75,3 +75,28 @@ def test_read_matrix_market_errors(tmp_path, text, msg):
     with pytest.raises(ValueError) as ei:
         skio.read_matrix_market(p)
     assert msg in str(ei.value)
+
+
+def test_matrix_market_host_parser_matches_reference_fuzz(tmp_path):
+    """600 seeded well-formed and malformed files with the LIVE reference's
+    outcome (tests/golden/make_mm_fuzz.py): same matrix, or the same
+    ValueError message and line number.  Host parsing only (no GPU); the
+    non-finite test the reference does in as_matrix runs on the device in
+    read_matrix_market, so those cases must parse to a non-finite matrix."""
+    import json
+    cases = json.load(open(os.path.join(GOLD, "mm_fuzz.json")))
+    p = tmp_path / "f.mtx"
+    for c in cases:
+        p.write_text(c["text"])
+        try:
+            got = skio.read_matrix_market_host(p).numpy()
+            err = None
+        except ValueError as e:
+            got, err = None, str(e).split(str(p), 1)[1]
+        if c["ok"]:
+            assert err is None, (c["text"], err)
+            assert np.array_equal(got, np.asarray(c["matrix"])), c["text"]
+        elif "non-finite" in c["error"]:
+            assert err is None and not np.isfinite(got).all(), c["text"]
+        else:
+            assert err == c["error"], (c["text"], err, c["error"])
