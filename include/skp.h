@@ -265,6 +265,17 @@ int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, float alpha,
                        void* Ct_lo, int64_t ldct, int32_t shift, int32_t fixed, int32_t e_fixed,
                        int32_t* e_out, int32_t* overflow, void* stream);
 
+/* skp_syrk_h3: C = alpha A^T A (N x N, fp32, exactly symmetric) from the
+ * pre-split planes of A stored K x N (lda % 64 == 0, both GEMM operands
+ * MN-major).  Replaces the operator A~^T A~ that power.py:131-133 applies
+ * twice per power step (y = atil @ (atil.T @ y)): formed once, the q power
+ * steps then run in the l-dimensional sketch space (SKETCH-SPACE power
+ * iteration).  Only the tiles meeting the lower triangle run;
+ * the strict upper triangle is mirrored.  Same 3xFP16 numerics as
+ * skp_gemm_h3 (2^-22 per product, register-promoted accumulation).          */
+int skp_syrk_h3(int64_t N, int64_t K, float alpha, const void* A_hi, const void* A_lo,
+                int64_t lda, const int32_t* a_exp, float* C, int64_t ldc, void* stream);
+
 /* skp_gemm_h3s: C = alpha A^T B + beta C with A (K x M, fp32, lda % 32 == 0)
  * split into fp16 hi/lo INSIDE the kernel with the caller's exponent 2^a_exp
  * (a bound on max|A|: skp_h2_exponent_f32), B pre-split as for skp_gemm_h3.

@@ -135,6 +135,8 @@ def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_t
     1 + 2q products, so it is prepared once (be.prepare: the fp16 split of
     the 3xFP16 GEMM on the CUDA backend)."""
     atil = be.prepare(atil)
+    if lazy and stabilized and q > 0 and hasattr(be, "gram_ok") and be.gram_ok(atil, omega, q):
+        return be.power_gram(comm, atil, omega, q, SHIFT_REL[_dtype_key(be)])
     if lazy and stabilized and q > 0 and hasattr(be, "planes_ok") and be.planes_ok(atil, omega):
         return be.power_lazy_planes(comm, atil, omega, q, SHIFT_REL[_dtype_key(be)])
     y = be.mm(atil, omega)
@@ -147,7 +149,7 @@ def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_t
     return y
 
 
-def randsvd(be, comm, a, qb, check: bool = True, amax_hint=None):
+def randsvd(be, comm, a, qb, check: bool = True, amax_hint=None, stats: dict | None = None):
     """power.py:181-199: B = Q^T A (summed over row slabs), thin SVD of B via
     the fp64 Gram B B^T and the eigensolver; U = Q U~, V = B^T U~ / sigma.
 
@@ -158,22 +160,29 @@ def randsvd(be, comm, a, qb, check: bool = True, amax_hint=None):
     ``check``: the reference's ||Q^T Q - I||_max test (power.py:194-196).  On
     backends with a device-side deviation (``orth_dev_t``) it is queued with
     the rest and read once at the end, with the overflow flag -- no host
-    synchronisation between the check and the products."""
+    synchronisation between the check and the products.
+
+    ``stats`` (optional dict) receives "qa2", a device scalar with
+    ||A||_F^2 - ||A - Q Q^T A||_F^2 = 2 tr(B B^T) - <Q^T Q, B B^T> (exact for
+    any Q, so the error identity does not assume Q^T Q = I: with an fp32 Q,
+    ||Q^T Q - I|| ~ 1e-6 would otherwise move a small rel_err by ~1e-6 / rel^2)."""
     dev = None
+    gq = None
     if check:
         if hasattr(be, "orth_dev_t"):
-            dev = be.orth_dev_t(comm.allreduce_(be.gram64_q(qb)))
+            gq = comm.allreduce_(be.gram64_q(qb))
+            dev = be.orth_dev_t(gq)
         else:
             g = comm.allreduce_(be.gram64(be.dense(qb) if hasattr(be, "dense") else qb))
             _raise_if_not_orthonormal(be, be.orth_dev(g))
-    out = _randsvd_core(be, comm, be.mm_at_big(a, qb, amax_hint), qb)   # B^T: this rank's part
+    out = _randsvd_core(be, comm, be.mm_at_big(a, qb, amax_hint), qb, gq, stats)
     if dev is not None:
         _raise_if_not_orthonormal(be, be.scalar(dev))
     if be.overflowed(comm):
         # the in-kernel fp16 split met an entry beyond its exponent bound (a
         # hint that did not hold): recompute with 3xTF32 on every rank.  The
         # flag is read once, after everything is queued (no mid-call sync).
-        out = _randsvd_core(be, comm, be.mm(a, be.dense(qb), ta=True), qb)
+        out = _randsvd_core(be, comm, be.mm(a, be.dense(qb), ta=True), qb, gq, stats)
     return out
 
 
@@ -182,10 +191,12 @@ def _raise_if_not_orthonormal(be, dev: float):
         raise ValueError(f"Q is not orthonormal (deviation {dev:.3e})")
 
 
-def _randsvd_core(be, comm, bt, qb):
+def _randsvd_core(be, comm, bt, qb, gq=None, stats=None):
     bt = comm.allreduce_(bt)
     n, c = bt.shape
     gb = be.gram64_rows_t(bt)                               # c x c, fp64
+    if stats is not None:
+        stats["qa2"] = be.proj_sq(gb, gq)
     w, v = be.eig_desc64(gb)
     p = min(c, n)
     sig, inv = be.sqrt_eigs(w)

@@ -390,6 +390,18 @@ def gemm_h3_emit_t(a: SplitH2, b: SplitH2, ta: bool = False, shift: int | None =
     return out
 
 
+def syrk_h3(a: SplitH2, alpha: float = 1.0, out=None) -> torch.Tensor:
+    """K4h SYRK: alpha a^T a (a.cols x a.cols, exactly symmetric) from the
+    planes of a stored K x N (a.rows = K); both operands MN-major."""
+    K, N = a.rows, a.cols
+    if out is None:
+        out = empty2d(N, N, F32, a.hi.device)
+    _, _, ldc = _rows_ld(out)
+    call("skp_syrk_h3", N, K, alpha, ptr(a.hi), ptr(a.lo), a.ld, ptr(a.e), ptr(out), ldc,
+         stream_ptr(a.hi.device))
+    return out
+
+
 def h2_exponent(x: torch.Tensor, e_io: torch.Tensor | None = None, have_amax: bool = False,
                 margin_bits: int = 0) -> torch.Tensor:
     """int32[2] e_io with e_io[0] = 15 - ceil(log2 max|x|) - margin_bits (max|x|
@@ -666,6 +678,49 @@ class CudaBackend:
             yt = gemm_h3_emit_t(atil, split_h2(z, trans=True), out=yt)
         return yt
 
+    def gram_ok(self, atil, omega, q: int) -> bool:
+        """Run the power iteration in the sketch space (power_gram)?  It costs
+        one SYRK (m l^2 useful MACs, tiles of the lower triangle) plus one
+        product (m l r2) against the 1 + 2q products of m l r2 each: taken
+        when l <= 3.6 q r2 (the SYRK's 256 x 128 tiles run ~10% below the
+        products' 256 x 176), and when the rows outnumber the sketch columns
+        (the l x l work of the q steps is replicated on every rank)."""
+        if not self.planes_ok(atil, omega) or q < 1:
+            return False
+        m, l, r2 = atil.rows, atil.cols, omega.shape[1]
+        return l <= 3.6 * q * r2 and m >= 2 * l and atil.ld % 64 == 0
+
+    def power_gram(self, comm, atil: SplitH2, omega, q: int, shift: float):
+        """The stabilized power iteration (power.py:113-134) in the sketch
+        space: with Y = A~ W,
+            A~ (A~^T Y) = A~ (G W),  G = A~^T A~ (l x l, summed over ranks),
+            Y^T Y = W^T G W,
+        so after one SYRK every step is l-dimensional:
+            W = Omega;  q x { V = G W;  X = chol_inv(W^T V + shift);  W = V X^T }
+        (the shifted CholeskyQR pass of power_lazy_planes, Q = Y X^T, applied
+        to W), and Y = A~ W at the end -- the same block as the product path
+        in exact arithmetic, with one pass over A~ for G instead of 2q.  The
+        q steps are 3xFP16 products of l x l by l x r2 whose blocks stay as
+        fp16 planes of their transposes.  Lazy, as power_lazy_planes: a
+        failed factorisation only sets self.fail.  Returns Y^T planes."""
+        g = comm.allreduce_(syrk_h3(atil))
+        gs = split_h2(g)
+        del g
+        # the blocks are re-split from fp32 every step (fresh exponents): an
+        # emitted split's worst-case exponent bound (ea + eb - 15 - log2 K)
+        # compounds over a chain of steps and would push W into fp16's
+        # subnormal range within a few steps
+        wt = split_h2(omega, trans=True)                     # W^T planes (r2 x l)
+        vt = None
+        for _ in range(q):
+            vt = split_h2(gemm_h3(gs, wt), trans=True, out=vt)   # V^T, V = G W
+            mg = cast(gemm_h3(wt, vt), F64)                  # W^T G W = Y^T Y
+            symmetrize_(mg)
+            x = self.chol_inv64(mg, 0.0, lazy=True, shift=shift)
+            wt = split_h2(gemm_h3(vt, split_h2(self.to_compute(x)), ta=True), trans=True,
+                          out=wt)                            # W = V X^T
+        return gemm_h3_emit_t(atil, wt)                      # (A~ W)^T
+
     def orth_planes(self, comm, yt: SplitH2, t2: float, shift: float, planes_out: bool = False):
         """Lazy shifted CholeskyQR3 of Y given as Y^T planes (_engine.orthonormalize):
         pass 1 on G + shift, pass 2 with the rank test t2 on its pivots, pass 3.
@@ -719,6 +774,14 @@ class CudaBackend:
         call("skp_orth_dev_f64", ptr(g64), g64.shape[0], g64.stride(0), ptr(out),
              stream_ptr(self.device))
         return out
+
+    def proj_sq(self, gb, gq=None):
+        """||A||^2 - ||A - Q Q^T A||^2 = 2 tr(BB^T) - <Q^T Q, BB^T> as a
+        device scalar (tr(BB^T) alone when Q^T Q is not at hand)."""
+        t = torch.diagonal(gb).sum()
+        if gq is None:
+            return t
+        return 2.0 * t - (gq[: gb.shape[0], : gb.shape[1]] * gb).sum()
 
     def orth_dev(self, g64) -> float:
         return float(self.orth_dev_t(g64).item())

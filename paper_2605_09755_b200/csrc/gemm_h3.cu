@@ -63,6 +63,8 @@ struct H3Params {
     int M, N, K;
     int bn, tiles_m, tiles_n, splits, kb_per_split, num_kb;
     int a_kmajor;
+    int b_kmajor;  // 0: B stored K x N (N contiguous; the SYRK's second operand)
+    int sym;       // 1: C = A^T A, only the units of the lower triangle (mirrored after)
     float alpha, beta;
     float* C;
     long long ldc;
@@ -191,10 +193,29 @@ __device__ __forceinline__ void acc_add16(float* acc, const float* v) {
 struct HWork {
     int tm, tn, ks, kb0, kb1;
 };
+template <bool kPair>
 __device__ __forceinline__ HWork h_unit(const H3Params& p, int u) {
     // N-tiles of one M block are adjacent units: co-resident CTAs share the A
     // row block through L2
     HWork w;
+    if (p.sym) {
+        // lower triangle only: M block tm needs the N tiles that start at or
+        // before its last row (the units are enumerated block row by row)
+        constexpr int R = kPair ? 2 * HM : HM;
+        int tm = 0, base = 0;
+        for (;;) {
+            const int c = min(p.tiles_n, ((tm + 1) * R + p.bn - 1) / p.bn);
+            if (u < base + c) break;
+            base += c;
+            ++tm;
+        }
+        w.tm = tm;
+        w.tn = u - base;
+        w.ks = 0;
+        w.kb0 = 0;
+        w.kb1 = p.num_kb;
+        return w;
+    }
     w.tn = u % p.tiles_n;
     const int r = u / p.tiles_n;
     w.tm = r % p.tiles_m;
@@ -221,7 +242,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int units = p.tiles_m * p.tiles_n * p.splits;
+    const int units = p.sym ? p.sym : p.tiles_m * p.tiles_n * p.splits;
     const uint32_t rank = kPair ? cluster_rank() : 0u;
     const bool leader = rank == 0;
     const int ustart = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
@@ -265,7 +286,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
         Ring r;
         const int bcols = kPair ? p.bn / 2 : p.bn;
         for (int u = ustart; u < units; u += ustride) {
-            const HWork w = h_unit(p, u);
+            const HWork w = h_unit<kPair>(p, u);
             const int m0 = w.tm * kRowsPerUnit + (int)rank * HM;
             const int n0 = w.tn * p.bn + (int)rank * bcols;
             for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
@@ -282,8 +303,16 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
                     h_tma_3d<kPair>(&map_ah, bar, st, 0, k0, m0 / 64);
                     h_tma_3d<kPair>(&map_al, bar, st + p.a_bytes, 0, k0, m0 / 64);
                 }
-                h_tma_2d<kPair>(&map_bh, bar, st + 2 * p.a_bytes, k0, n0);
-                if (p.b_lo) h_tma_2d<kPair>(&map_bl, bar, st + 2 * p.a_bytes + p.b_bytes, k0, n0);
+                if (p.b_kmajor) {
+                    h_tma_2d<kPair>(&map_bh, bar, st + 2 * p.a_bytes, k0, n0);
+                    if (p.b_lo)
+                        h_tma_2d<kPair>(&map_bl, bar, st + 2 * p.a_bytes + p.b_bytes, k0, n0);
+                } else {
+                    h_tma_3d<kPair>(&map_bh, bar, st + 2 * p.a_bytes, 0, k0, n0 / 64);
+                    if (p.b_lo)
+                        h_tma_3d<kPair>(&map_bl, bar, st + 2 * p.a_bytes + p.b_bytes, 0, k0,
+                                        n0 / 64);
+                }
             }
         }
     } else if (warp == kHWarpMma && leader) {
@@ -291,10 +320,12 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
         // offsets in 16-byte units (start-address field never carries: < 228 KB)
         const uint64_t a0 = p.a_kmajor ? make_desc(smem0, 16u, 1024u, kLayoutSW128)
                                        : make_desc(smem0, kHChunkBytes, 1024u, kLayoutSW128);
-        const uint64_t b0 = make_desc(smem0 + 2 * p.a_bytes, 16u, 1024u, kLayoutSW128);
+        const uint64_t b0 = p.b_kmajor ? make_desc(smem0 + 2 * p.a_bytes, 16u, 1024u, kLayoutSW128)
+                                       : make_desc(smem0 + 2 * p.a_bytes, kHChunkBytes, 1024u,
+                                                   kLayoutSW128);
         const uint64_t sstep = p.stage_bytes >> 4;
         const uint64_t ajstep = p.a_kmajor ? (32u >> 4) : (2048u >> 4);  // 16 K: +32 B | +2 rows groups
-        const uint64_t bjstep = 32u >> 4;
+        const uint64_t bjstep = p.b_kmajor ? (32u >> 4) : (2048u >> 4);
         const uint64_t alo = p.a_bytes >> 4, blo = p.b_bytes >> 4;
         // Accumulation chunks of chunk_kb K blocks alternate between the two
         // TMEM buffers; the epilogue adds each finished chunk into registers
@@ -306,7 +337,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
         Ring r;
         int cc = 0;
         for (int u = ustart; u < units; u += ustride) {
-            const HWork w = h_unit(p, u);
+            const HWork w = h_unit<kPair>(p, u);
             for (int c0 = w.kb0; c0 < w.kb1; c0 += p.chunk_kb, ++cc) {
                 const int buf = cc & 1;
                 const uint32_t aph = (uint32_t)(cc >> 1) & 1u;
@@ -354,7 +385,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
         }
         int cc = 0;
         for (int u = ustart; u < units; u += ustride) {
-            const HWork w = h_unit(p, u);
+            const HWork w = h_unit<kPair>(p, u);
             float acc[kHEpiCols][16];
 #pragma unroll
             for (int i = 0; i < kHEpiCols; ++i)
@@ -997,10 +1028,11 @@ bool h_encode_k(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows
 }
 // MN-major fp16 A stored [K x M] (M contiguous) as {64, K, M/64 chunks}: one
 // box {64, HK, 2} = the CTA's 128 M x HK K tile as [chunk][k][64], SWIZZLE_128B
-bool h_encode_mn(CUtensorMap* map, const void* base, uint64_t m, uint64_t k, uint64_t ld) {
+bool h_encode_mn(CUtensorMap* map, const void* base, uint64_t m, uint64_t k, uint64_t ld,
+                 uint32_t box_mn = HM) {
     cuuint64_t dims[3] = {64, k, (cuuint64_t)cdiv((int64_t)m, 64)};
     cuuint64_t strides[2] = {ld * 2, 128};
-    cuuint32_t box[3] = {64, (cuuint32_t)HK, (cuuint32_t)(HM / 64)};
+    cuuint32_t box[3] = {64, (cuuint32_t)HK, box_mn / 64};
     cuuint32_t es[3] = {1, 1, 1};
     return h_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides,
                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1138,6 +1170,8 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
     p.bn = pl.bn; p.tiles_m = pl.tiles_m; p.tiles_n = pl.tiles_n; p.splits = pl.splits;
     p.kb_per_split = pl.kb_per_split; p.num_kb = pl.num_kb;
     p.a_kmajor = ta ? 0 : 1;
+    p.b_kmajor = 1;
+    p.sym = 0;
     p.alpha = alpha; p.beta = beta; p.C = C; p.ldc = ldc;
     p.ws = pl.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
     p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
@@ -1202,6 +1236,116 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
                                                            ldc);
         SKP_LAUNCHED(h3_splitk_reduce);
     }
+    return SKP_OK;
+}
+
+// C = alpha A^T A (N x N, symmetric) with A pre-split, stored K x N (N
+// contiguous): both operands MN-major from the same planes.  Only the unit
+// tiles meeting the lower triangle run (M blocks of 256 rows x N tiles of 128
+// columns: ~half of the full product's MMAs); the strict upper triangle is
+// then mirrored from the lower one, so C comes out exactly symmetric.
+__global__ void sym_mirror_kernel(float* __restrict__ C, int64_t N, int64_t ldc) {
+    __shared__ float t[32][33];
+    const int64_t bi = blockIdx.y, bj = blockIdx.x;  // source tile (bi, bj), bi >= bj
+    if (bj > bi) return;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t i = bi * 32 + r, j = bj * 32 + tx;
+        t[r][tx] = (i < N && j < N) ? C[i * ldc + j] : 0.f;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t i = bj * 32 + r, j = bi * 32 + tx;  // destination (i, j) = source (j, i)
+        if (i < N && j < N && j > i) C[i * ldc + j] = t[tx][r];
+    }
+}
+
+int syrk_h3(int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo, int64_t lda,
+            const int32_t* a_e, float* C, int64_t ldc, cudaStream_t st) {
+    if (!h_init()) {
+        set_error("unsupported: the 3xFP16 tcgen05 GEMM needs an sm_100 device");
+        return SKP_ERR_UNSUPPORTED;
+    }
+    if (N == 0) return SKP_OK;
+    if (K == 0 || N > INT32_MAX || K > INT32_MAX) {
+        set_error("unsupported: syrk_h3 sizes");
+        return SKP_ERR_UNSUPPORTED;
+    }
+    const uintptr_t al = reinterpret_cast<uintptr_t>(Ahi) | reinterpret_cast<uintptr_t>(Alo);
+    if ((al & 15) || (lda & 63)) {
+        set_error("unsupported: syrk_h3 needs 16-byte aligned planes with lda %% 64 == 0 (lda=%lld)",
+                  (long long)lda);
+        return SKP_ERR_UNSUPPORTED;
+    }
+    const bool pair = h_pair(N);
+    HPlan pl = h_plan(N, N, K, 0, pair);
+    // N tiles of 128 columns: MN-major B comes in 64-column swizzle atoms per CTA
+    pl.bn = 128;
+    pl.tiles_n = (int)cdiv(N, 128);
+    const int bcols = pair ? 64 : 128;
+    pl.b_bytes = (uint32_t)bcols * HK * 2;
+    pl.stage_bytes = 2 * pl.a_bytes + 2 * pl.b_bytes;
+    pl.acc_stride = 128;
+    pl.stages = std::max(2, std::min(kHMaxStages, (int)((227 * 1024 - 1024 - 256) / pl.stage_bytes)));
+    pl.smem = 1024 + (size_t)pl.stages * pl.stage_bytes + (2 * pl.stages + 4) * 8 + 16;
+    const int R = pair ? 2 * HM : HM;
+    int units = 0;
+    for (int tm = 0; tm < pl.tiles_m; ++tm)
+        units += (int)std::min<int64_t>(pl.tiles_n, cdiv((int64_t)(tm + 1) * R, 128));
+    H3Params p = {};
+    p.b_lo = 1;
+    p.M = (int)N; p.N = (int)N; p.K = (int)K;
+    p.bn = pl.bn; p.tiles_m = pl.tiles_m; p.tiles_n = pl.tiles_n; p.splits = 1;
+    p.kb_per_split = pl.num_kb; p.num_kb = pl.num_kb;
+    p.a_kmajor = 0;
+    p.b_kmajor = 0;
+    p.sym = units;
+    p.alpha = alpha; p.beta = 0.f; p.C = C; p.ldc = ldc;
+    p.ws = nullptr;
+    p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
+    p.stage_bytes = pl.stage_bytes; p.acc_stride = pl.acc_stride;
+    p.a_e = a_e; p.b_e = a_e;
+    p.chunk_kb = h_chunk_kb();
+    p.emit_hi = nullptr; p.emit_lo = nullptr; p.emit_e = nullptr; p.overflow = nullptr;
+    // kind::f16: D f32, A and B f16, both MN-major (bits 15, 16)
+    p.idesc = (1u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(p.bn >> 3) << 17) |
+              ((uint32_t)(R >> 4) << 24);
+    CUtensorMap mah, mal, mbh, mbl;
+    const bool ok = h_encode_mn(&mah, Ahi, (uint64_t)N, (uint64_t)K, lda) &&
+                    h_encode_mn(&mal, Alo, (uint64_t)N, (uint64_t)K, lda) &&
+                    h_encode_mn(&mbh, Ahi, (uint64_t)N, (uint64_t)K, lda, (uint32_t)bcols) &&
+                    h_encode_mn(&mbl, Alo, (uint64_t)N, (uint64_t)K, lda, (uint32_t)bcols);
+    if (!ok) {
+        set_error("cuTensorMapEncodeTiled failed (syrk_h3)");
+        return SKP_ERR_UNSUPPORTED;
+    }
+    if (pair) {
+        SKP_CUDA(cudaFuncSetAttribute(gemm_h3_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(2 * std::min(units, h_sms / 2)));
+        cfg.blockDim = dim3(kHThreads);
+        cfg.dynamicSmemBytes = pl.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SKP_CUDA(cudaLaunchKernelEx(&cfg, gemm_h3_kernel<true>, mah, mal, mbh, mbl, p));
+        SKP_LAUNCHED(gemm_h3_kernel_pair);
+    } else {
+        SKP_CUDA(cudaFuncSetAttribute(gemm_h3_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        gemm_h3_kernel<false><<<std::min(units, h_sms), kHThreads, pl.smem, st>>>(mah, mal, mbh, mbl,
+                                                                                 p);
+        SKP_LAUNCHED(gemm_h3_kernel);
+    }
+    const unsigned nt = (unsigned)cdiv(N, 32);
+    sym_mirror_kernel<<<dim3(nt, nt), dim3(32, 8), 0, st>>>(C, N, ldc);
+    SKP_LAUNCHED(sym_mirror_kernel);
     return SKP_OK;
 }
 
@@ -1407,6 +1551,13 @@ extern "C" int skp_split_h2_f32(const float* X, int64_t rows, int64_t cols, int6
     SKP_ARG(e && (rows == 0 || cols == 0 || (X && hi && lo)), "split_h2: null pointer");
     h_init();
     return split_h2(X, rows, cols, ld, trans, hi, lo, ldh, e, have_amax != 0, SKP_STREAM(stream));
+}
+
+extern "C" int skp_syrk_h3(int64_t N, int64_t K, float alpha, const void* A_hi, const void* A_lo,
+                           int64_t lda, const int32_t* a_exp, float* C, int64_t ldc, void* stream) {
+    SKP_ARG(N >= 0 && K >= 0 && lda >= N && ldc >= N && a_exp && (N == 0 || (A_hi && A_lo && C)),
+            "syrk_h3: bad arguments");
+    return skp::syrk_h3(N, K, alpha, A_hi, A_lo, lda, a_exp, C, ldc, SKP_STREAM(stream));
 }
 
 extern "C" int64_t skp_gemm_h3s_ws_bytes(int64_t M, int64_t N, int64_t K) {

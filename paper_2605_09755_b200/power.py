@@ -316,9 +316,9 @@ def range_finder_classical(a, k: int, r2: int, q: int, seed: int, stabilized: bo
 
 
 def _randsvd_dev(a: torch.Tensor, qb: torch.Tensor, comm=_engine.LOCAL, check: bool = True,
-                 amax_hint=None):
+                 amax_hint=None, stats: dict | None = None):
     be = _be(a.dtype, a.device)
-    return _engine.randsvd(be, comm, a, qb, check, amax_hint)
+    return _engine.randsvd(be, comm, a, qb, check, amax_hint, stats)
 
 
 def randsvd(a, q_basis, *, timings: dict | None = None) -> SvdResult:
@@ -343,7 +343,8 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
 
     Returns SvdResult, or (SvdResult, rel_err) with ``with_error`` where
     rel_err = ||a - QQ^T a||_F / ||a||_F from ||a||_F^2 - sum(sigma^2)
-    (Pythagorean identity; ||a||_F^2 is fused into the sketch)."""
+    (Pythagorean identity, in the form that holds for any Q:
+    _engine.randsvd's stats; ||a||_F^2 is fused into the sketch)."""
     op, streamed = _convert.upload_streamed(a, "a")
     m, n = op.t.shape
     spec.validate(m, n)
@@ -354,7 +355,8 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
                            planes_out=True)
     if isinstance(a, _convert.DeviceMatrix):
         a.finite = True
-    u, s, v = _randsvd_dev(op.t, qb, check=True, amax_hint=hint.get("amax"))
+    st = {}
+    u, s, v = _randsvd_dev(op.t, qb, check=True, amax_hint=hint.get("amax"), stats=st)
     ph.mark("randsvd")
     res = SvdResult(_convert.download(u, op.kind), _convert.download(s, op.kind),
                     _convert.download(v, op.kind))
@@ -362,9 +364,7 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
     if not with_error:
         return res
     a2 = float(fro2.item())
-    s64 = np.asarray(res.sigma.cpu() if isinstance(res.sigma, torch.Tensor) else res.sigma,
-                     dtype=np.float64)
-    rel = math.sqrt(max(a2 - float((s64 ** 2).sum()), 0.0) / a2) if a2 > 0 else 0.0
+    rel = math.sqrt(max(a2 - float(st["qa2"]), 0.0) / a2) if a2 > 0 else 0.0
     return res, rel
 
 

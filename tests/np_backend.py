@@ -71,6 +71,10 @@ class NumpyBackend:
         inv = np.where(s > 0, 1 / np.where(s > 0, s, 1), 0)
         return s, inv
 
+    def proj_sq(self, gb, gq=None):
+        t = float(np.trace(gb))
+        return t if gq is None else 2.0 * t - float((gq * gb).sum())
+
     def orth_dev(self, g):
         return float(np.abs(g - np.eye(g.shape[0])).max())
 

@@ -431,6 +431,40 @@ def test_accurate_gram_orthonormal_basis(ops):
     assert rel.abs().max().item() < 1e-5
 
 
+@pytest.mark.parametrize("N,K", [(1, 1), (45, 131), (128, 64), (300, 5000), (520, 4000),
+                                 (1000, 20000), (1111, 3000), (4000, 8192)])
+def test_syrk_h3_vs_torch(ops, N, K):
+    """K4h SYRK (the sketch-space power iteration's G = A~^T A~): both
+    operands MN-major from one set of planes, lower-triangle tiles only,
+    mirrored -- exactly symmetric, 3xFP16 accuracy against fp64."""
+    g = torch.Generator(device="cuda").manual_seed(N + 7 * K)
+    a = torch.randn(K, N, generator=g, device="cuda") * 2.0 + 0.1
+    out = ops.syrk_h3(ops.split_h2(a), alpha=0.5)
+    ref = 0.5 * (a.double().T @ a.double())
+    assert torch.equal(out, out.T)
+    # 2^-22 per product plus the fp32 accumulation of 1024-deep chunks, whose
+    # truncation on the positive diagonal (sums of squares) is ~1e-5 of
+    # sum |a_ki a_kj| (test_h3_long_k_accumulation_is_unbiased)
+    ab = a.double().abs()
+    bound = 0.5 * (2e-5 * (ab.T @ ab) + 2e-6 * ab.max().item() ** 2 * np.sqrt(K))
+    assert bool(((out.double() - ref).abs() <= bound + 1e-6).all())
+
+
+def test_syrk_h3_inplace_planes_long_k(ops):
+    """The power iteration's operand: A~ split in place (planes with leading
+    dimension 2 ld) and K = 262144 rows (register-promoted accumulation:
+    the diagonal of G = sums of squares is unbiased)."""
+    K, N = 262144, 640
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = ops.empty2d(K, N, torch.float32, "cuda")
+    x.copy_(torch.randn(K, N, generator=g, device="cuda"))
+    ref = x.double().T @ x.double()
+    out = ops.syrk_h3(ops.split_h2_inplace(x))
+    rel = (torch.diagonal(out).double() - torch.diagonal(ref)) / torch.diagonal(ref)
+    assert abs(rel.mean().item()) < 1e-5 and rel.abs().max().item() < 2e-5
+    assert (out.double() - ref).abs().max().item() <= 2e-5 * torch.diagonal(ref).max().item()
+
+
 def test_gemm_h3_pair_forced_small(ops, monkeypatch):
     monkeypatch.setenv("SKP_H3_FORCE2CTA", "1")
     g = torch.Generator(device="cuda").manual_seed(3)

@@ -183,6 +183,63 @@ def test_reduced_configs_vs_live_oracle(skp, name, m, n, l, r2, k, q, rank, deca
     assert abs(rel_d - eo) <= ERR_TOL * eo, (rel_d, eo)
 
 
+@pytest.mark.parametrize("name,m,n,l,r2,k,q,rank,decay", [
+    ("C3-structure", 16384, 4096, 1000, 120, 100, 3, 2048, "poly"),
+    ("C5-structure", 32768, 2048, 1000, 210, 200, 2, 1024, "exp"),
+    ("graded", 16384, 2048, 500, 80, 60, 2, 400, "graded"),
+])
+def test_sketch_space_power_matches_products(skp, monkeypatch, name, m, n, l, r2, k, q, rank,
+                                             decay):
+    """The power iteration in the sketch space (one SYRK G = A~^T A~, then
+    q l-dimensional steps; _ops.CudaBackend.power_gram) against the product
+    path (2q products with A~) and the CPU oracle on the same bytes: sigma
+    within 1e-5 and rel_err within 1e-3 of the oracle for both.  'graded':
+    sigma_i = 10^(-i/40), a 100x spread inside the top k."""
+    from paper_2605_09755_b200 import _ops
+    if decay == "poly":
+        spec_v = np.arange(1.0, rank + 1.0) ** -0.5
+    elif decay == "exp":
+        spec_v = np.exp(-np.arange(1.0, rank + 1.0) / 200.0)
+    else:
+        spec_v = 10.0 ** (-np.arange(1.0, rank + 1.0) / 40.0)
+    a_dev = datagen.lowrank_plus_noise_gpu(m, n, spec_v, 1e-8, seed=6)
+    a = a_dev.cpu().numpy()
+    spec = skp.RangeFinderSpec(k=k, l=l, r1=l, r2=r2, q=q, eps=0.5, seed=6, s=8)
+    ospec = o.Spec(k=k, l=l, r1=l, r2=r2, q=q, seed=6, s=8)
+    qo = o.range_finder_sketched(a, ospec)
+    _, so, _ = o.randsvd(a, qo)
+    eo = o.proj_rel_error(a, qo)
+    used = []
+    real_gram = _ops.CudaBackend.power_gram
+
+    def spy(self, *args, **kw):
+        used.append(True)
+        return real_gram(self, *args, **kw)
+
+    monkeypatch.setattr(_ops.CudaBackend, "power_gram", spy)
+    res_g, rel_g = skp.rsvd(a_dev, spec, with_error=True)
+    assert used, "the sketch-space path did not run"
+    monkeypatch.setattr(_ops.CudaBackend, "gram_ok", lambda self, *a_, **k_: False)
+    res_p, rel_p = skp.rsvd(a_dev, spec, with_error=True)
+    a64 = a_dev.double()
+    nrm = float(torch.linalg.norm(a64))
+    report = {}
+    for tag, res, rel in (("sketch-space", res_g, rel_g), ("products", res_p, rel_p)):
+        u = res.U.double()
+        exact = float(torch.linalg.norm(a64 - u @ (u.T @ a64))) / nrm
+        sig_err = float(np.max(np.abs(res.sigma.cpu().numpy()[:k] - so[:k]) / so[:k]))
+        report[tag] = dict(sigma=sig_err, exact=exact, fused=rel)
+    print(report, "oracle", eo)
+    for tag, r in report.items():
+        assert r["sigma"] <= SIG_TOL[np.float32], (tag, r)
+        assert abs(r["exact"] - eo) <= ERR_TOL * eo, (tag, r, eo)
+        # the fused error is the identity sqrt(1 - (|A|^2 - |A - QQ^T A|^2)/|A|^2)
+        # from 3xFP16 products of fp32 data: its absolute error on rel^2 is
+        # ~1e-6, i.e. 1e-6 / (2 rel) on rel (outside 1e-3 relative below rel ~
+        # 0.03; the exact residual above is the parity metric there)
+        assert abs(r["fused"] - eo) <= ERR_TOL * eo + 1e-6 / (2 * eo), (tag, r, eo)
+
+
 def _fp64_restatement(a32: torch.Tensor, spec, cols, signs, omega):
     """Alg. 1 + randsvd (power.py:113-154, :181-199) in fp64 torch/cuBLAS/
     cuSOLVER at full size -- an independent checker for sizes the CPU oracle
