@@ -225,7 +225,7 @@ __device__ __forceinline__ HWork h_unit(const H3Params& p, int u) {
     return w;
 }
 
-template <bool kPair>
+template <bool kPair, int kEC = kHEpiCols>
 __global__ void __launch_bounds__(kHThreads, 1)
 gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
                const __grid_constant__ CUtensorMap map_bh, const __grid_constant__ CUtensorMap map_bl,
@@ -386,9 +386,9 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
         int cc = 0;
         for (int u = ustart; u < units; u += ustride) {
             const HWork w = h_unit<kPair>(p, u);
-            float acc[kHEpiCols][16];
+            float acc[kEC][16];
 #pragma unroll
-            for (int i = 0; i < kHEpiCols; ++i)
+            for (int i = 0; i < kEC; ++i)
 #pragma unroll
                 for (int e = 0; e < 16; ++e) acc[i][e] = 0.f;
             for (int c0 = w.kb0; c0 < w.kb1; c0 += p.chunk_kb, ++cc) {
@@ -399,7 +399,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
                 const uint32_t tbase =
                     tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * p.acc_stride);
 #pragma unroll
-                for (int i = 0; i < kHEpiCols; ++i) {
+                for (int i = 0; i < kEC; ++i) {
                     if (g0 + i < g1) {
                         float v[16];
                         tmem_ld16(tbase + 16u * (uint32_t)(g0 + i), v);
@@ -417,7 +417,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
                 // C^T split: for each column, the warp's 32 rows are 64
                 // contiguous bytes of each plane
 #pragma unroll
-                for (int i = 0; i < kHEpiCols; ++i) {
+                for (int i = 0; i < kEC; ++i) {
                     const int col0 = w.tn * p.bn + 16 * (g0 + i);
                     if (g0 + i >= g1 || col0 >= p.N) continue;
 #pragma unroll
@@ -435,7 +435,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
                 continue;
             }
 #pragma unroll
-            for (int i = 0; i < kHEpiCols; ++i) {
+            for (int i = 0; i < kEC; ++i) {
                 const int col0 = w.tn * p.bn + 16 * (g0 + i);
                 if (g0 + i >= g1 || col0 >= p.N) continue;
                 const int lim = min(16, p.N - col0);
@@ -1279,19 +1279,22 @@ int syrk_h3(int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo,
     }
     const bool pair = h_pair(N);
     HPlan pl = h_plan(N, N, K, 0, pair);
-    // N tiles of 128 columns: MN-major B comes in 64-column swizzle atoms per CTA
-    pl.bn = 128;
-    pl.tiles_n = (int)cdiv(N, 128);
-    const int bcols = pair ? 64 : 128;
+    // square tiles: 256 x 256 per CTA pair (each CTA 128 rows of A and 128
+    // columns of B = two 64-column MN-major swizzle atoms; 6 column groups per
+    // epilogue thread), 128 x 128 on one CTA
+    const int bn = pair ? 256 : 128;
+    pl.bn = bn;
+    pl.tiles_n = (int)cdiv(N, bn);
+    const int bcols = pair ? bn / 2 : bn;
     pl.b_bytes = (uint32_t)bcols * HK * 2;
     pl.stage_bytes = 2 * pl.a_bytes + 2 * pl.b_bytes;
-    pl.acc_stride = 128;
+    pl.acc_stride = bn;
     pl.stages = std::max(2, std::min(kHMaxStages, (int)((227 * 1024 - 1024 - 256) / pl.stage_bytes)));
     pl.smem = 1024 + (size_t)pl.stages * pl.stage_bytes + (2 * pl.stages + 4) * 8 + 16;
     const int R = pair ? 2 * HM : HM;
     int units = 0;
     for (int tm = 0; tm < pl.tiles_m; ++tm)
-        units += (int)std::min<int64_t>(pl.tiles_n, cdiv((int64_t)(tm + 1) * R, 128));
+        units += (int)std::min<int64_t>(pl.tiles_n, cdiv((int64_t)(tm + 1) * R, bn));
     H3Params p = {};
     p.b_lo = 1;
     p.M = (int)N; p.N = (int)N; p.K = (int)K;
@@ -1320,7 +1323,7 @@ int syrk_h3(int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo,
         return SKP_ERR_UNSUPPORTED;
     }
     if (pair) {
-        SKP_CUDA(cudaFuncSetAttribute(gemm_h3_kernel<true>,
+        SKP_CUDA(cudaFuncSetAttribute(gemm_h3_kernel<true, 6>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(2 * std::min(units, h_sms / 2)));
@@ -1334,7 +1337,7 @@ int syrk_h3(int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo,
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        SKP_CUDA(cudaLaunchKernelEx(&cfg, gemm_h3_kernel<true>, mah, mal, mbh, mbl, p));
+        SKP_CUDA(cudaLaunchKernelEx(&cfg, gemm_h3_kernel<true, 6>, mah, mal, mbh, mbl, p));
         SKP_LAUNCHED(gemm_h3_kernel_pair);
     } else {
         SKP_CUDA(cudaFuncSetAttribute(gemm_h3_kernel<false>,
