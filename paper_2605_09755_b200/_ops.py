@@ -7,7 +7,6 @@ or the CPU.  ``CudaBackend`` is the compute backend the algorithm engine
 """
 from __future__ import annotations
 
-import os
 import threading
 
 import numpy as np
@@ -147,10 +146,6 @@ def sketch_right(a: torch.Tensor, colptr, entries, s: int, r: int, out=None, fro
     return out
 
 
-GATHER_COLS = 896  # lanes per slice of the K2 v2 plan (sketch_gather.cu kGCols)
-GATHER_SPARE = 96  # slices hold at most GATHER_COLS - GATHER_SPARE columns (kGSpare)
-
-
 GATHER_PLAN_FAIL_MARK = 1 << 40   # added to the non-finite counter by a failed plan
 
 
@@ -180,8 +175,9 @@ def gather_plan_checked(plan: torch.Tensor, r: int):
     off = int(_lib.load().skp_sketch_gather_plan_fail_offset(r))
     if int(plan[off:off + 4].view(torch.int32).item()) != 0:
         return None
-    nslice = -(-r // (GATHER_COLS - GATHER_SPARE))
-    perm = plan[:nslice * GATHER_COLS * 4].view(torch.int32).cpu().numpy()
+    # the plan starts with the perm table (P slices x kGCols int32), which
+    # ends where the fail word begins
+    perm = plan[:off].view(torch.int32).cpu().numpy()
     return plan, perm[perm >= 0].astype(np.int64)
 
 
@@ -528,7 +524,7 @@ class CudaBackend:
         self.overflow.zero_()
         if (self.dtype != F32 or self.gemm_mode != "auto" or a.shape[0] * a.shape[1] < H3_MIN_ELEMS
                 or a.stride(1) != 1 or a.stride(0) % 32 or a.data_ptr() % 16
-                or os.environ.get("SKP_NO_H3") or not _lib.load().skp_has_tcgen05()):
+                or not _lib.load().skp_has_tcgen05()):
             return self.mm(a, self.dense(q), ta=True)
         if amax_hint is not None:
             e_a = amax_hint[0].clone()
@@ -555,12 +551,12 @@ class CudaBackend:
         A~): split once into fp16 hi/lo planes for the 3xFP16 GEMM (twice the
         3xTF32 rate at 22-bit operand accuracy).  Returns x itself where that
         does not apply (fp64, explicit GEMM modes, small operands, no
-        tcgen05) or is switched off (SKP_NO_H3).  e_io: see split_h2.
+        tcgen05).  e_io: see split_h2.
         inplace: the caller gives x up (the range finder's A~), so the planes
         are written over it."""
         if isinstance(x, SplitH2) or self.dtype != F32 or self.gemm_mode != "auto":
             return x
-        if x.dim() != 2 or x.shape[0] * x.shape[1] < H3_MIN_ELEMS or os.environ.get("SKP_NO_H3"):
+        if x.dim() != 2 or x.shape[0] * x.shape[1] < H3_MIN_ELEMS:
             return x
         if not _lib.load().skp_has_tcgen05():
             return x
@@ -572,7 +568,7 @@ class CudaBackend:
             # driver query, cudaMemGetInfo, waits for the device -- a host
             # stall here left the GPU idle for up to 19 ms per step)
             free = _device_total(x.device) - torch.cuda.memory_allocated(x.device)
-            if free < 4 * x.shape[0] * x.stride(0) * 4 or os.environ.get("SKP_SPLIT_INPLACE"):
+            if free < 4 * x.shape[0] * x.stride(0) * 4:
                 return split_h2_inplace(x, e_io)
         return split_h2(x, e_io=e_io)
 
@@ -590,7 +586,7 @@ class CudaBackend:
 
     def _h3_ok(self, x) -> bool:
         return (self.dtype == F32 and self.gemm_mode == "auto" and x.dim() == 2
-                and x.shape[0] * x.shape[1] >= H3_MIN_ELEMS and not os.environ.get("SKP_NO_H3")
+                and x.shape[0] * x.shape[1] >= H3_MIN_ELEMS
                 and bool(_lib.load().skp_has_tcgen05()))
 
     def gram64_rows(self, b):
@@ -650,7 +646,7 @@ class CudaBackend:
     # ---- lazy power iteration on fp16 planes (3xFP16 end to end) --------------
     def planes_ok(self, atil, omega) -> bool:
         return isinstance(atil, SplitH2) and isinstance(omega, torch.Tensor) \
-            and omega.dtype == F32 and omega.dim() == 2 and not os.environ.get("SKP_NO_PLANES")
+            and omega.dtype == F32 and omega.dim() == 2
 
     def gram64_planes(self, yt: SplitH2):
         """Y^T Y (fp64) from the split planes of Y^T: 3xFP16, promoted accumulation."""

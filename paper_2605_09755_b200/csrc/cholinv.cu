@@ -411,31 +411,11 @@ extern "C" int skp_cholinv_f64(const double* G, int64_t n, int64_t ld, double re
     int blocks = std::min(sms, std::max(maxtask, 1));
     int nn = (int)n;
     int64_t ldg = ld;
-    static unsigned long long* prof = nullptr;
-    unsigned long long* prof_arg = nullptr;
-    if (getenv("SKP_CI_PROF")) {
-        if (!prof) SKP_CUDA(cudaMalloc(&prof, 4 * 1024 * sizeof(unsigned long long)));
-        SKP_CUDA(cudaMemsetAsync(prof, 0, 4 * 1024 * sizeof(unsigned long long), st));
-        prof_arg = prof;
-    }
+    unsigned long long* prof_arg = nullptr;  // (per-panel timestamps: unused)
     void* args[] = {(void*)&G, &nn, &ldg, (void*)&nb, &rel_tol, &shift_rel, &A, &Lb, &Xp, &Sp, &dinfo, &info, &prof_arg};
     SKP_CUDA(cudaLaunchCooperativeKernel((void*)cholinv_kernel, dim3(blocks), dim3(kCIThreads), args,
                                          smem, st));
     count_launch();
-    if (prof_arg) {
-        unsigned long long h[4 * 1024];
-        SKP_CUDA(cudaStreamSynchronize(st));
-        SKP_CUDA(cudaMemcpy(h, prof_arg, sizeof(unsigned long long) * 4 * nb, cudaMemcpyDeviceToHost));
-        double wait = 0, task0 = 0, fac = 0, rest = 0;
-        for (int p = 0; p + 1 < nb; ++p) {
-            wait += (h[4 * p + 1] - h[4 * p + 0]) / 1e3;
-            task0 += (h[4 * p + 2] - h[4 * p + 1]) / 1e3;
-            fac += (h[4 * p + 3] - h[4 * p + 2]) / 1e3;
-            rest += (h[4 * (p + 1)] - h[4 * p + 3]) / 1e3;
-        }
-        fprintf(stderr, "[cholinv prof] n=%lld nb=%d blocks=%d per panel (us): sync %.2f task0 %.2f factor %.2f rest %.2f\n",
-                (long long)n, nb, blocks, wait / (nb - 1), task0 / (nb - 1), fac / (nb - 1), rest / (nb - 1));
-    }
     if (np == n) {
         SKP_CUDA(cudaMemcpyAsync(X, Xp, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
     } else {

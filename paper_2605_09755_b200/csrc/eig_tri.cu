@@ -694,7 +694,7 @@ int syev_tri(const double* A, int64_t n, double* W, double* V, void* ws, int64_t
     // whole matrix in a 16-CTA cluster's shared memory when it fits
     bool clustered = false;
     const size_t csm = sytrd_cluster_smem(nn);
-    if (csm <= 220 * 1024 && !getenv("SKP_TRI_NOCLUSTER")) {
+    if (csm <= 220 * 1024) {
         cudaError_t ea = cudaFuncSetAttribute(sytrd_cluster_kernel,
                                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaError_t eb = cudaFuncSetAttribute(sytrd_cluster_kernel,

@@ -1002,7 +1002,7 @@ bool h_init() {
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
     cudaDeviceGetAttribute(&h_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (major != 10 || minor != 0 || getenv("SKP_DISABLE_TCGEN05")) return false;
+    if (major != 10 || minor != 0) return false;
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
@@ -1048,13 +1048,10 @@ struct HPlan {
 
 // K blocks per accumulation chunk (chains of 1024): see the MMA role
 int h_chunk_kb() {
-    static int v = getenv("SKP_H3_CHUNK") ? std::max(1, atoi(getenv("SKP_H3_CHUNK"))) : 16;
-    return v;
+    return 16;
 }
 
 bool h_pair(int64_t M) {
-    if (getenv("SKP_H3_NO2CTA")) return false;
-    if (getenv("SKP_H3_FORCE2CTA")) return true;
     return M > HM;
 }
 
@@ -1090,7 +1087,6 @@ HPlan h_plan(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool pair, b
     const size_t budget = 227 * 1024;
     const int st = (int)((budget - 1024 - 256) / pl.stage_bytes);
     pl.stages = std::max(2, std::min(kHMaxStages, st));
-    if (getenv("SKP_H3_STAGES")) pl.stages = std::max(2, std::min(pl.stages, atoi(getenv("SKP_H3_STAGES"))));
     pl.smem = 1024 + (size_t)pl.stages * pl.stage_bytes + (2 * pl.stages + 4) * 8 + 16;
     return pl;
 }

@@ -71,9 +71,6 @@ struct TcParams {
     int a_mn3d, b_mn3d;  // MN-major operand loaded by ONE 3-D box per stage
     int acc_stride;      // TMEM columns per accumulator buffer
     int nacc;            // accumulator buffers (2: epilogue overlaps the next tile)
-    unsigned long long* prof;  // debug (SKP_TC_PROF): per-role cycle counters, summed over CTAs
-    int dbg;      // debug: bit0 A / bit1 B re-read a 4-block k window (L2-resident)
-    int xf_mode;  // 0: 3xTF32 (split in smem); 1: debug -- raw operands, one product
 };
 
 constexpr uint32_t kMnChunkBytes = 32 * BK * 4;  // one TMA box: 32 MN x BK K
@@ -172,18 +169,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const uint32_t smem0 = smem_u32(smem);
     auto stage_a = [&](int s) { return smem + (size_t)s * p.stage_bytes; };
     auto stage_b = [&](int s) { return stage_a(s) + p.a_bytes; };
-    long long pw0 = 0, pw1 = 0;
-    const long long role_t0 = p.prof ? clock64() : 0;
-#define SKP_TIMED_WAIT(acc, call)                 \
-    do {                                          \
-        if (p.prof) {                             \
-            const long long t_ = clock64();       \
-            call;                                 \
-            acc += clock64() - t_;                \
-        } else {                                  \
-            call;                                 \
-        }                                         \
-    } while (0)
 
     if (warp == kWarpTma) {
         Ring r;
@@ -193,10 +178,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const int n0 = w.tn * p.bn + (kPair ? (int)rank * (p.bn / 2) : 0);
             for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
                 const int s = r.s;
-                SKP_TIMED_WAIT(pw0, mbar_wait_k<kPair>(&empty[s], r.ph ^ 1, (p.dbg & 128) != 0));
+                mbar_wait_k<kPair>(&empty[s], r.ph ^ 1);
                 mbar_expect_tx_e(&full[s], p.a_bytes + p.b_bytes);
-                const int k0 = ((p.dbg & 1) ? (kb & 3) : kb) * BK;
-                const int k0b = ((p.dbg & 2) ? (kb & 3) : kb) * BK;
+                const int k0 = kb * BK;
+                const int k0b = k0;
                 if (p.a_kmajor) {
                     tma_load_2d_e(&map_a, &full[s], stage_a(s), k0, m0);
                 } else if (p.a_mn3d) {
@@ -226,19 +211,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const uint64_t sstep = p.stage_bytes >> 4;
         const uint64_t jstep = p.b_kmajor ? (32u >> 4) : (1024u >> 4);
         const uint64_t lostep = p.b_bytes >> 4;
-        const bool raw = p.xf_mode == 1;
         Ring r;
         int ul = 0;
         for (int u = ustart; u < units; u += ustride, ++ul) {
             Work w = unit_of(p, u);
             const int buf = p.nacc == 2 ? (ul & 1) : 0;
             const uint32_t aph = (uint32_t)(p.nacc == 2 ? (ul >> 1) : ul) & 1u;
-            SKP_TIMED_WAIT(pw1, mbar_wait_k<kPair>(&tempty[buf], aph ^ 1, (p.dbg & 128) != 0));
+            mbar_wait_k<kPair>(&tempty[buf], aph ^ 1);
             tc_fence_after();
             const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
             for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
                 const int s = r.s;
-                SKP_TIMED_WAIT(pw0, mbar_wait_k<kPair>(&split[s], r.ph, (p.dbg & 128) != 0));
+                mbar_wait_k<kPair>(&split[s], r.ph);
                 tc_fence_after();
                 const uint64_t bh = bdesc0 + (uint64_t)s * sstep;
                 // A slot: hi at +0..BK-1, lo at +BK..2BK-1
@@ -252,13 +236,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     const uint32_t acc = (kb > w.kb0 || j > 0) ? 1u : 0u;
                     const uint32_t a_hi = ah + 8u * j, a_lo = a_hi + BK;
                     const uint64_t b_hi = bh + (uint64_t)j * jstep;
-                    if (raw) {
-                        mma(a_hi, b_hi, acc);
-                    } else {
-                        mma(a_lo, b_hi, acc);          // a_lo b_hi
-                        mma(a_hi, b_hi + lostep, 1u);  // a_hi b_lo
-                        mma(a_hi, b_hi, 1u);           // a_hi b_hi
-                    }
+                    mma(a_lo, b_hi, acc);          // a_lo b_hi
+                    mma(a_hi, b_hi + lostep, 1u);  // a_hi b_lo
+                    mma(a_hi, b_hi, 1u);           // a_hi b_hi
                 }
                 // frees the smem stage and the TMEM A slot (in both CTAs)
                 if (kPair) tc_commit_pair_e(&empty[s]);
@@ -273,7 +253,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         for (int u = ustart; u < units; u += ustride) {
             Work w = unit_of(p, u);
             for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
-                SKP_TIMED_WAIT(pw0, mbar_wait(&split[r.s], r.ph));
+                mbar_wait(&split[r.s], r.ph);
                 mbar_arrive_cluster_e(split_cl0 + 8u * (uint32_t)r.s);
             }
         }
@@ -282,13 +262,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const int q = warp & 3;
         const int row = q * 32 + lane;
         const uint32_t tlane = (uint32_t)(q * 32) << 16;
-        const bool raw = p.xf_mode == 1;
         Ring r;
         for (int u = ustart; u < units; u += ustride) {
             Work w = unit_of(p, u);
             for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
                 const int s = r.s;
-                SKP_TIMED_WAIT(pw0, mbar_wait(&full[s], r.ph));
+                mbar_wait(&full[s], r.ph);
                 const uint32_t a0 = smem0 + (uint32_t)s * p.stage_bytes;
                 uint32_t hi[BK], lo[BK];
                 if (p.a_kmajor) {
@@ -311,12 +290,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const uint32_t ta = tmem_base + tlane + acol0 + kASlotCols * (uint32_t)s;
                 tmem_st16(ta, hi);
                 tmem_st16(ta + 16, hi + 16);
-                if (!raw) {
 #pragma unroll
-                    for (int k = 0; k < BK; ++k) lo[k] = tf32_lo(hi[k]);
-                    tmem_st16(ta + BK, lo);
-                    tmem_st16(ta + BK + 16, lo + 16);
-                }
+                for (int k = 0; k < BK; ++k) lo[k] = tf32_lo(hi[k]);
+                tmem_st16(ta + BK, lo);
+                tmem_st16(ta + BK + 16, lo + 16);
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
@@ -327,35 +304,32 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         // B split: b_lo beside the raw B tile
         const int t = threadIdx.x - kWarpBx * 32;
         const uint32_t nB = p.b_bytes / 16;
-        const bool raw = p.xf_mode == 1;
         Ring r;
         for (int u = ustart; u < units; u += ustride) {
             Work w = unit_of(p, u);
             for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
                 const int s = r.s;
-                SKP_TIMED_WAIT(pw0, mbar_wait(&full[s], r.ph));
-                if (!raw) {
-                    const uint32_t b0 = smem0 + (uint32_t)s * p.stage_bytes + p.a_bytes;
-                    // 4 loads in flight before the stores (the asm loads/stores
-                    // are not reordered by the compiler)
-                    for (uint32_t i0 = t; i0 < nB; i0 += 4 * 128) {
-                        uint4 v[4];
+                mbar_wait(&full[s], r.ph);
+                const uint32_t b0 = smem0 + (uint32_t)s * p.stage_bytes + p.a_bytes;
+                // 4 loads in flight before the stores (the asm loads/stores
+                // are not reordered by the compiler)
+                for (uint32_t i0 = t; i0 < nB; i0 += 4 * 128) {
+                    uint4 v[4];
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const uint32_t i = i0 + 128u * k;
-                            if (i < nB) v[k] = lds128(b0 + 16u * i);
-                        }
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const uint32_t i = i0 + 128u * k;
-                            if (i < nB)
-                                sts128(b0 + p.b_bytes + 16u * i,
-                                       make_uint4(tf32_lo(v[k].x), tf32_lo(v[k].y), tf32_lo(v[k].z),
-                                                  tf32_lo(v[k].w)));
-                        }
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t i = i0 + 128u * k;
+                        if (i < nB) v[k] = lds128(b0 + 16u * i);
                     }
-                    fence_proxy_async();
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t i = i0 + 128u * k;
+                        if (i < nB)
+                            sts128(b0 + p.b_bytes + 16u * i,
+                                   make_uint4(tf32_lo(v[k].x), tf32_lo(v[k].y), tf32_lo(v[k].z),
+                                              tf32_lo(v[k].w)));
+                    }
                 }
+                fence_proxy_async();
                 __syncwarp();
                 mbar_arrive_e(&split[s]);
             }
@@ -367,7 +341,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             Work w = unit_of(p, u);
             const int buf = p.nacc == 2 ? (ul & 1) : 0;
             const uint32_t aph = (uint32_t)(p.nacc == 2 ? (ul >> 1) : ul) & 1u;
-            SKP_TIMED_WAIT(pw0, mbar_wait_k<kPair>(&tfull[buf], aph, (p.dbg & 128) != 0));
+            mbar_wait_k<kPair>(&tfull[buf], aph);
             tc_fence_after();
             const int row = w.tm * kRowsPerUnit + (int)rank * BM + q * 32 + lane;
             const uint32_t tbase =
@@ -414,19 +388,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             else mbar_arrive_e(&tempty[buf]);
         }
     }
-#undef SKP_TIMED_WAIT
-    if (p.prof && lane == 0) {
-        // slots: role*4 + {0 total, 1 wait0, 2 wait1}; roles 0 tma, 1 mma, 2 a-split, 3 b-split, 4 epi
-        const int role = warp == kWarpTma ? 0 : warp == kWarpMma ? (leader ? 1 : 5) : warp < kWarpBx ? 2
-                       : warp < kWarpEpi ? 3 : 4;
-        const bool first = warp == kWarpTma || warp == kWarpMma || warp == kWarpAx ||
-                           warp == kWarpBx || warp == kWarpEpi;
-        if (first) {
-            atomicAdd(&p.prof[role * 4 + 0], (unsigned long long)(clock64() - role_t0));
-            atomicAdd(&p.prof[role * 4 + 1], (unsigned long long)pw0);
-            atomicAdd(&p.prof[role * 4 + 2], (unsigned long long)pw1);
-        }
-    }
     tc_fence_before();
     if (kPair) cluster_sync_all();
     else __syncthreads();
@@ -468,7 +429,6 @@ bool init_tc() {
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     if (major != 10 || minor != 0) return false;
-    if (getenv("SKP_DISABLE_TCGEN05")) return false;
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
@@ -567,20 +527,16 @@ Plan plan_for(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool b_mn, 
     // double-buffer the accumulator (epilogue overlaps the next tile) only when
     // that still leaves room for 4 A slots
     pl.nacc = ((int)kTmemCols - 2 * pl.acc_stride) / (int)kASlotCols >= 4 ? 2 : 1;
-    if (getenv("SKP_TC_NACC")) pl.nacc = std::max(1, std::min(2, atoi(getenv("SKP_TC_NACC"))));
     const int slots = ((int)kTmemCols - pl.nacc * pl.acc_stride) / (int)kASlotCols;
     const size_t budget = 220 * 1024;
     int st = (int)((budget - 1024 - 256) / pl.stage_bytes);
     pl.stages = std::max(2, std::min({kMaxStages, st, slots}));
-    if (getenv("SKP_TC_STAGES")) pl.stages = std::max(2, std::min(pl.stages, atoi(getenv("SKP_TC_STAGES"))));
     pl.smem = 1024 + (size_t)pl.stages * pl.stage_bytes + (3 * pl.stages + 4) * 8 + 16;
     return pl;
 }
 
 // CTA pairs pay off once there are enough 256-row units to fill the machine
 bool use_pair(int64_t M) {
-    if (getenv("SKP_TC_NO2CTA")) return false;
-    if (getenv("SKP_TC_FORCE2CTA")) return true;  // test hook: pairs at any M
     return M > BM;
 }
 
@@ -611,9 +567,8 @@ int gemm_tc_3xtf32(int ta, int tb, int64_t M, int64_t N, int64_t K, float alpha,
     }
     const int64_t cap = ws ? ws_bytes / 4 : 0;
     // one 3-D box per MN-major operand per stage when rows are 128-byte padded
-    const bool no3d = getenv("SKP_TC_NO3D") != nullptr;
-    const bool a_mn3d = ta && (lda % 32 == 0) && !no3d;
-    const bool b_mn3d = !tb && (ldb % 32 == 0) && !no3d;
+    const bool a_mn3d = ta && (lda % 32 == 0);
+    const bool b_mn3d = !tb && (ldb % 32 == 0);
     const bool pair = use_pair(M);
     Plan pl = plan_for(M, N, K, cap, tb == 0, b_mn3d, pair);
     if (pl.splits > 1 && (!ws || (int64_t)pl.splits * M * N * 4 > ws_bytes)) {
@@ -631,15 +586,6 @@ int gemm_tc_3xtf32(int ta, int tb, int64_t M, int64_t N, int64_t K, float alpha,
     p.stage_bytes = pl.stage_bytes;
     p.acc_stride = pl.acc_stride;
     p.nacc = pl.nacc;
-    p.xf_mode = getenv("SKP_TC_RAW1") ? 1 : 0;
-    p.dbg = getenv("SKP_TC_DBG") ? atoi(getenv("SKP_TC_DBG")) : 0;
-    static unsigned long long* prof_buf = nullptr;
-    p.prof = nullptr;
-    if (getenv("SKP_TC_PROF")) {
-        if (!prof_buf) SKP_CUDA(cudaMalloc(&prof_buf, 24 * sizeof(unsigned long long)));
-        SKP_CUDA(cudaMemsetAsync(prof_buf, 0, 24 * sizeof(unsigned long long), st));
-        p.prof = prof_buf;
-    }
     // A comes from TMEM (always K-major there); B's major-ness from its layout
     p.idesc = (1u << 4) | (2u << 7) | (2u << 10) |
               ((uint32_t)(!p.b_kmajor) << 16) | ((uint32_t)(p.bn >> 3) << 17) |
@@ -690,19 +636,6 @@ int gemm_tc_3xtf32(int ta, int tb, int64_t M, int64_t N, int64_t K, float alpha,
         grid = std::min(units, g_sms);
         gemm_tc_kernel<false><<<grid, kThreads, pl.smem, st>>>(ma, mb, p);
         SKP_LAUNCHED(gemm_tc_kernel);
-    }
-    if (p.prof) {
-        unsigned long long h[24];
-        SKP_CUDA(cudaStreamSynchronize(st));
-        SKP_CUDA(cudaMemcpy(h, p.prof, sizeof(h), cudaMemcpyDeviceToHost));
-        const char* names[6] = {"tma", "mma", "asp", "bsp", "epi", "fwd"};
-        fprintf(stderr, "[gemm_tc prof] M=%lld N=%lld K=%lld bn=%d stages=%d units=%d grid=%d pair=%d\n",
-                (long long)M, (long long)N, (long long)K, p.bn, p.stages, units, grid, (int)pair);
-        for (int r = 0; r < (pair ? 6 : 5); ++r) {
-            const double n = (pair && (r == 1 || r == 5)) ? grid / 2 : grid;  // leader / peer only
-            fprintf(stderr, "  %-4s total %10.0f  wait0 %10.0f  wait1 %10.0f  (cycles per CTA)\n", names[r],
-                    (double)h[r * 4] / n, (double)h[r * 4 + 1] / n, (double)h[r * 4 + 2] / n);
-        }
     }
     if (p.splits > 1) {
         int64_t blocks = std::min<int64_t>(cdiv(M * N, 256), (int64_t)g_sms * 8);

@@ -176,7 +176,7 @@ int sketch_right(const T* A, int64_t lda, int64_t m, int64_t n, const int32_t* c
     SKP_ARG(m >= 1 && n >= 1 && r >= 1 && s >= 1, "sketch_right: bad sizes");
     SKP_ARG(lda >= n && ldo >= r, "sketch_right: bad leading dimension");
     cudaStream_t st = SKP_STREAM(stream);
-    if (ws && !getenv("SKP_SKETCH_SLAB")) {
+    if (ws) {
         int rc = sketch_right_rows<T>(A, lda, m, n, colptr, entries, s, r, out, ldo, fro2,
                                       nonfinite, ws, ws_bytes, st);
         if (rc != SKP_ERR_UNSUPPORTED) return rc;

@@ -64,7 +64,7 @@ constexpr int kGTMax = 128;               // schedule steps per warp (the rest: 
 constexpr unsigned long long kGPlanFailMark = 1ull << 40;  // added to *nonfinite
 constexpr int kGBufWords = 24608;         // row buffer: n <= 24576 floats + 32 zero words
 constexpr uint32_t kGBufBytes = kGBufWords * 4;  // 98432, a multiple of 128
-// three row buffers (SKP_GATHER_NB=3, rows <= 75 KB): warps of a CTA may
+// three row buffers (NB = 3, rows <= 75 KB; tested, not launched): warps of a CTA may
 // drift two rows apart before the slowest gates a refill.  Measured at C3:
 // 11.54 -> 11.46 ms with 6 slices of 24 warps, but 9.86 (two) vs 10.01 ms
 // (three) with 5 slices of 28 warps, and ~20% more DRAM re-reads -- so two
@@ -582,6 +582,10 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
             asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(x) : "r"(ev & 0x7fffffffu), "n"(boff));
             acc += __int_as_float(__float_as_int(x) ^ (int)(ev & 0x80000000u));
         }
+        // every load of this row (the non-volatile register-resident ones
+        // included: acc depends on all of them) completes before this warp
+        // reports the buffer done -- the last warp's refill overwrites it
+        asm volatile("" : "+f"(acc)::"memory");
         __syncwarp();
         if (lane == 0) {
             // the last warp done with this buffer refills it with row i + NB*G
@@ -739,10 +743,8 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
     const GLayout L = gather_layout(const_cast<void*>(plan), n, r);
     const int P = L.P;
     const int G = std::max(1, std::min<int>(sms / P, (int)std::min<int64_t>(m, 1 << 20)));
-    static const int nb_env = getenv("SKP_GATHER_NB") ? atoi(getenv("SKP_GATHER_NB")) : 2;
-    const bool nb3 = L.H == 1 && n <= kGN3 && nb_env != 2;
-    auto kern = nb3 ? sketch_gather_kernel<3> : sketch_gather_kernel<2>;
-    const size_t smem = nb3 ? GBuf<3>::smem : GBuf<2>::smem;
+    auto kern = sketch_gather_kernel<2>;
+    const size_t smem = GBuf<2>::smem;
     SKP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // one launch per column pass: pass h gathers A[:, h*npass ...] and adds
     // to what the earlier passes wrote; the checks ride on the last pass

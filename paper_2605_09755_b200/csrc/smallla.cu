@@ -329,265 +329,6 @@ __device__ void jacobi_apply_db(const double* Ain, double* Aout, int n, int np, 
     }
 }
 
-// Cooperative: A ping-pongs between A and A2 (both global), V in workspace;
-// one grid.sync per round.  The final matrix is copied back into A.
-__global__ void syevj_coop_kernel(double* A, double* A2, int64_t n, double* V, int max_sweeps,
-                                  int32_t* counters, int32_t* sweeps) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    cg::grid_group grid = cg::this_grid();
-    const int nn = (int)n, np = nn + (nn & 1);
-    JacobiShared sh;
-    jacobi_shared_carve(sh, sm, np);
-    __shared__ int cnt;
-    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = gtid; t < (int64_t)nn * nn; t += gstride)
-        V[t] = (t / nn == t % nn) ? 1.0 : 0.0;
-    const double tol_abs = 0x1p-47 * diag_absmax(A, nn, nn);
-    grid.sync();
-    double* cur = A;
-    double* nxt = A2;
-    int sw = 0;
-    for (; sw < max_sweeps; ++sw) {
-        for (int k = 0; k < np - 1; ++k) {
-            int c = jacobi_rotations(cur, nn, nn, np, k, sh, &cnt, tol_abs);
-            if (blockIdx.x == 0 && threadIdx.x == 0 && c) atomicAdd(&counters[sw], c);
-            jacobi_apply_db(cur, nxt, nn, np, sh, V, gtid, gstride);
-            grid.sync();
-            double* t = cur; cur = nxt; nxt = t;
-        }
-        int total = *((volatile int32_t*)&counters[sw]);
-        if (total == 0) break;
-    }
-    if (cur != A) {
-        for (int64_t t = gtid; t < (int64_t)nn * nn; t += gstride) A[t] = cur[t];
-    }
-    if (gtid == 0) *sweeps = sw + 1;
-}
-
-// ----------------------------------------------------------- block Jacobi ---
-// n > 112: indices are cut into 32-wide blocks (zero-padded to an even count),
-// blocks are paired round-robin; per round every pair's 64x64 subproblem
-// S = G[P u Q, P u Q] gets ONE in-shared-memory cyclic 2x2 Jacobi sweep whose
-// rotations accumulate into a 64x64 orthogonal U; then G <- J^T G J and
-// V <- V J (J = the pairs' U's) as 64x64 block products.  Two grid syncs per
-// round and ~nb rounds per sweep (vs ~n for the 2x2 scheme).
-constexpr int kBJ = 32, kBJ2 = 64, kBJThreads = 256;
-
-struct BJShared {
-    double S[kBJ2][kBJ2 + 1];
-    double U[kBJ2][kBJ2 + 1];
-    double c[kBJ2 / 2], s[kBJ2 / 2];
-    int p[kBJ2 / 2], q[kBJ2 / 2];
-    int cnt;
-};
-
-// block index of slot t in round k (round-robin over nb slots, slot 0 fixed)
-__device__ __forceinline__ int bj_slot(int t, int k, int nb) {
-    return t == 0 ? 0 : ((t - 1 + k) % (nb - 1)) + 1;
-}
-__device__ __forceinline__ void bj_pair(int u, int k, int nb, int& a, int& b) {
-    a = bj_slot(u, k, nb);
-    b = bj_slot(nb - 1 - u, k, nb);
-}
-// global row index of local index i (0..63) of pair (a, b)
-__device__ __forceinline__ int bj_idx(int i, int a, int b) {
-    return i < kBJ ? a * kBJ + i : b * kBJ + (i - kBJ);
-}
-
-// one cyclic sweep over the 64x64 S in smem, accumulating rotations into U
-__device__ int bj_inner_sweep(BJShared& sh, double tol_abs) {
-    int total = 0;
-    for (int k = 0; k < kBJ2 - 1; ++k) {
-        if (threadIdx.x == 0) sh.cnt = 0;
-        __syncthreads();
-        if (threadIdx.x < kBJ2 / 2) {
-            const int i = threadIdx.x;
-            int a = rr_slot(i, k, kBJ2), b = rr_slot(kBJ2 - 1 - i, k, kBJ2);
-            int p = a < b ? a : b, q = a < b ? b : a;
-            double c = 1.0, sn = 0.0;
-            const double apq = sh.S[p][q], app = sh.S[p][p], aqq = sh.S[q][q];
-            if (jacobi_rotate(apq, app, aqq, tol_abs)) {
-                const double theta = (aqq - app) / (2.0 * apq);
-                double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-                if (!isfinite(theta)) t = 0.5 / theta;
-                c = 1.0 / sqrt(1.0 + t * t);
-                sn = t * c;
-                atomicAdd(&sh.cnt, 1);
-            }
-            sh.c[i] = c; sh.s[i] = sn; sh.p[i] = p; sh.q[i] = q;
-        }
-        __syncthreads();
-        total += sh.cnt;
-        // S <- J^T S J on 2x2 blocks (independent, in place); U <- U J
-        for (int t = threadIdx.x; t < (kBJ2 / 2) * (kBJ2 / 2); t += blockDim.x) {
-            const int u = t / (kBJ2 / 2), v = t % (kBJ2 / 2);
-            const double cu = sh.c[u], su = sh.s[u], cv = sh.c[v], sv = sh.s[v];
-            if (su == 0.0 && sv == 0.0) continue;
-            const int pu = sh.p[u], qu = sh.q[u], pv = sh.p[v], qv = sh.q[v];
-            const double a00 = sh.S[pu][pv], a01 = sh.S[pu][qv], a10 = sh.S[qu][pv], a11 = sh.S[qu][qv];
-            const double r00 = cu * a00 - su * a10, r01 = cu * a01 - su * a11;
-            const double r10 = su * a00 + cu * a10, r11 = su * a01 + cu * a11;
-            double b00 = r00 * cv - r01 * sv, b01 = r00 * sv + r01 * cv;
-            double b10 = r10 * cv - r11 * sv, b11 = r10 * sv + r11 * cv;
-            if (u == v) { b01 = 0.0; b10 = 0.0; }
-            sh.S[pu][pv] = b00; sh.S[pu][qv] = b01; sh.S[qu][pv] = b10; sh.S[qu][qv] = b11;
-        }
-        for (int t = threadIdx.x; t < kBJ2 * (kBJ2 / 2); t += blockDim.x) {
-            const int row = t / (kBJ2 / 2), u = t % (kBJ2 / 2);
-            const double su = sh.s[u];
-            if (su == 0.0) continue;
-            const double cu = sh.c[u];
-            const double up = sh.U[row][sh.p[u]], uq = sh.U[row][sh.q[u]];
-            sh.U[row][sh.p[u]] = cu * up - su * uq;
-            sh.U[row][sh.q[u]] = su * up + cu * uq;
-        }
-        __syncthreads();
-    }
-    return total;
-}
-
-// C (64x64, smem) = op(X) * Y with X, Y 64x64 in smem; opX: 0 = X, 1 = X^T
-__device__ void bj_mm64(double (*C)[kBJ2 + 1], double (*X)[kBJ2 + 1], double (*Y)[kBJ2 + 1],
-                        int opx) {
-    // each thread: 16 outputs (4x4 of a 16x16 thread grid)
-    const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
-    double acc[4][4] = {};
-    for (int k = 0; k < kBJ2; ++k) {
-        double x[4], y[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) x[i] = opx ? X[k][tr * 4 + i] : X[tr * 4 + i][k];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) y[j] = Y[k][tc * 4 + j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) C[tr * 4 + i][tc * 4 + j] = acc[i][j];
-    __syncthreads();
-}
-
-__global__ void __launch_bounds__(kBJThreads)
-syevj_block_kernel(const double* __restrict__ Ain, int64_t n, int nb, double* G0, double* G1,
-                   double* V, double* Us, int max_sweeps, int32_t* counters, int32_t* sweeps,
-                   double* Aout) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    BJShared& sh = *reinterpret_cast<BJShared*>(smraw);
-    cg::grid_group grid = cg::this_grid();
-    const int np = nb * kBJ;            // padded order
-    const int npairs = nb / 2;
-    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = gtid; t < (int64_t)np * np; t += gstride) {
-        const int64_t i = t / np, j = t % np;
-        G0[t] = (i < n && j < n) ? Ain[i * n + j] : 0.0;
-        V[t] = i == j ? 1.0 : 0.0;
-    }
-    const double tol_abs = 0x1p-47 * diag_absmax(Ain, n, n);
-    grid.sync();
-    double* cur = G0;
-    double* nxt = G1;
-    int sw = 0;
-    for (; sw < max_sweeps; ++sw) {
-        for (int k = 0; k < nb - 1; ++k) {
-            // phase 1: subproblem sweeps, one CTA per pair
-            for (int u = blockIdx.x; u < npairs; u += gridDim.x) {
-                int a, b;
-                bj_pair(u, k, nb, a, b);
-                for (int t = threadIdx.x; t < kBJ2 * kBJ2; t += blockDim.x) {
-                    const int i = t / kBJ2, j = t % kBJ2;
-                    sh.S[i][j] = cur[(int64_t)bj_idx(i, a, b) * np + bj_idx(j, a, b)];
-                    sh.U[i][j] = i == j ? 1.0 : 0.0;
-                }
-                __syncthreads();
-                const int c = bj_inner_sweep(sh, tol_abs);
-                if (threadIdx.x == 0 && c) atomicAdd(&counters[sw], c);
-                double* Uo = Us + (int64_t)u * kBJ2 * kBJ2;
-                for (int t = threadIdx.x; t < kBJ2 * kBJ2; t += blockDim.x)
-                    Uo[t] = sh.U[t / kBJ2][t % kBJ2];
-                __syncthreads();
-            }
-            grid.sync();
-            // phase 2: G' = J^T G J (64x64 tiles), V' = V J (64-row strips)
-            const int ntiles = npairs * npairs, nvstrips = npairs * (np / kBJ2);
-            for (int job = blockIdx.x; job < ntiles + nvstrips; job += gridDim.x) {
-                if (job < ntiles) {
-                    const int u = job / npairs, v = job % npairs;
-                    int au, bu, av, bv;
-                    bj_pair(u, k, nb, au, bu);
-                    bj_pair(v, k, nb, av, bv);
-                    for (int t = threadIdx.x; t < kBJ2 * kBJ2; t += blockDim.x) {
-                        const int i = t / kBJ2, j = t % kBJ2;
-                        sh.S[i][j] = cur[(int64_t)bj_idx(i, au, bu) * np + bj_idx(j, av, bv)];
-                        sh.U[i][j] = Us[(int64_t)u * kBJ2 * kBJ2 + t];
-                    }
-                    __syncthreads();
-                    // T = U_u^T S  (into S via the shared scratch)
-                    bj_mm64(sh.S, sh.U, sh.S, 1);
-                    for (int t = threadIdx.x; t < kBJ2 * kBJ2; t += blockDim.x)
-                        sh.U[t / kBJ2][t % kBJ2] = Us[(int64_t)v * kBJ2 * kBJ2 + t];
-                    __syncthreads();
-                    bj_mm64(sh.S, sh.S, sh.U, 0);  // T U_v
-                    for (int t = threadIdx.x; t < kBJ2 * kBJ2; t += blockDim.x) {
-                        const int i = t / kBJ2, j = t % kBJ2;
-                        nxt[(int64_t)bj_idx(i, au, bu) * np + bj_idx(j, av, bv)] = sh.S[i][j];
-                    }
-                    __syncthreads();
-                } else {
-                    const int jv = job - ntiles;
-                    const int u = jv % npairs, rs = jv / npairs;  // rows [rs*64, rs*64+64)
-                    int au, bu;
-                    bj_pair(u, k, nb, au, bu);
-                    for (int t = threadIdx.x; t < kBJ2 * kBJ2; t += blockDim.x) {
-                        const int i = t / kBJ2, j = t % kBJ2;
-                        sh.S[i][j] = V[(int64_t)(rs * kBJ2 + i) * np + bj_idx(j, au, bu)];
-                        sh.U[i][j] = Us[(int64_t)u * kBJ2 * kBJ2 + t];
-                    }
-                    __syncthreads();
-                    bj_mm64(sh.S, sh.S, sh.U, 0);
-                    for (int t = threadIdx.x; t < kBJ2 * kBJ2; t += blockDim.x) {
-                        const int i = t / kBJ2, j = t % kBJ2;
-                        V[(int64_t)(rs * kBJ2 + i) * np + bj_idx(j, au, bu)] = sh.S[i][j];
-                    }
-                    __syncthreads();
-                }
-            }
-            grid.sync();
-            double* t = cur; cur = nxt; nxt = t;
-        }
-        const int total = *((volatile int32_t*)&counters[sw]);
-        if (total == 0) break;
-    }
-    // final diagonal matrix (n x n part) for the sort kernel; V stays padded
-    for (int64_t t = gtid; t < n * n; t += gstride) {
-        const int64_t i = t / n, j = t % n;
-        Aout[t] = cur[i * np + j];
-    }
-    if (gtid == 0) *sweeps = sw + 1;
-}
-
-// sort for the padded V (leading dimension np)
-__global__ void eig_sort_padded_kernel(const double* __restrict__ A, int64_t n,
-                                       const double* __restrict__ V, int64_t ldv,
-                                       double* __restrict__ W, double* __restrict__ Vout) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        double li = A[i * n + i];
-        int64_t rank = 0;
-        for (int64_t j = 0; j < n; ++j) {
-            double lj = A[j * n + j];
-            rank += (lj > li) || (lj == li && j < i);
-        }
-        W[rank] = li;
-        for (int64_t r = 0; r < n; ++r) Vout[r * n + rank] = V[r * ldv + i];
-    }
-}
-
 // eigenvalues = diag(A) sorted descending (ties by index); permute V columns.
 __global__ void eig_sort_kernel(const double* __restrict__ A, int64_t n,
                                 const double* __restrict__ V, double* __restrict__ W,
@@ -790,10 +531,8 @@ extern "C" int skp_trinv_lower_f64(const double* L, int64_t ldl, int64_t n, doub
 }
 
 extern "C" int64_t skp_syevj_ws_bytes(int64_t n) {
-    const int64_t nb0 = cdiv(n, 32), nb = nb0 + (nb0 & 1), np = nb * 32;
-    const int64_t blk = (3 * np * np + (nb / 2) * 64 * 64 + n * n) * (int64_t)sizeof(double);
     const int64_t small = 2 * n * n * (int64_t)sizeof(double);
-    int64_t b = blk > small ? blk : small;
+    int64_t b = small;
     const int64_t tri = syev_tri_ws_bytes(n);
     b = b > tri ? b : tri;
     return b + 64 * sizeof(int32_t) + 256;
@@ -808,7 +547,6 @@ extern "C" int skp_syevj_f64(double* A, int64_t n, double* W, double* V, int32_t
     cudaStream_t st = SKP_STREAM(stream);
     double* Vws = reinterpret_cast<double*>(ws);
     double* Aws = Vws + n * n;
-    int32_t* counters = reinterpret_cast<int32_t*>(Aws + n * n);
     const int np = (int)(n + (n & 1));
     const size_t rot_bytes = (size_t)(np / 2) * (2 * sizeof(double) + 2 * sizeof(int));
     if (n <= 112) {
@@ -821,65 +559,8 @@ extern "C" int skp_syevj_f64(double* A, int64_t n, double* W, double* V, int32_t
         SKP_LAUNCHED(eig_sort_kernel);
         return SKP_OK;
     }
-    // n > 112: tridiagonal reduction + bisection + inverse iteration (default);
-    // SKP_SYEVJ=coop|block selects the Jacobi variants (2x2 cooperative rounds /
-    // 64x64 block rotations) kept for cross-checking.
-    const char* force = getenv("SKP_SYEVJ");
-    if (!force || force[0] == 't') return syev_tri(A, n, W, V, ws, ws_bytes, sweeps, st);
-    const bool use_coop = force[0] == 'c';
-    {
-        if (use_coop) {
-            SKP_CUDA(cudaMemsetAsync(counters, 0, 64 * sizeof(int32_t), st));
-            int dev = 0, sms = 148, per_sm = 0;
-            SKP_CUDA(cudaGetDevice(&dev));
-            SKP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            SKP_CUDA(cudaFuncSetAttribute(syevj_coop_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)rot_bytes));
-            SKP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, syevj_coop_kernel, 256,
-                                                                   rot_bytes));
-            int mx = max_sweeps;
-            void* args[] = {&A, &Aws, &n, &Vws, &mx, &counters, &sweeps};
-            SKP_CUDA(cudaLaunchCooperativeKernel((void*)syevj_coop_kernel, dim3(sms), dim3(256),
-                                                 args, rot_bytes, st));
-            count_launch();
-            eig_sort_kernel<<<grid_for(n), 256, 0, st>>>(A, n, Vws, W, V);
-            SKP_LAUNCHED(eig_sort_kernel);
-            return SKP_OK;
-        }
-    }
-    // block Jacobi (n > 112)
-    const int nb0 = (int)cdiv(n, kBJ), nb = nb0 + (nb0 & 1);
-    const int64_t npad = (int64_t)nb * kBJ;
-    double* G0 = reinterpret_cast<double*>(ws);
-    double* G1 = G0 + npad * npad;
-    double* Vp = G1 + npad * npad;
-    double* Us = Vp + npad * npad;
-    double* Aout = Us + (int64_t)(nb / 2) * kBJ2 * kBJ2;
-    int32_t* cnts = reinterpret_cast<int32_t*>(Aout + n * n);
-    SKP_CUDA(cudaMemsetAsync(cnts, 0, 64 * sizeof(int32_t), st));
-    int dev = 0, sms = 148, per_sm = 0;
-    SKP_CUDA(cudaGetDevice(&dev));
-    SKP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const size_t smem = sizeof(BJShared);
-    SKP_CUDA(cudaFuncSetAttribute(syevj_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    SKP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, syevj_block_kernel,
-                                                           kBJThreads, smem));
-    SKP_ARG(per_sm >= 1, "syevj: cooperative kernel cannot be resident");
-    const int npairs = nb / 2;
-    const int jobs = npairs * npairs + npairs * (int)(npad / kBJ2);
-    int blocks = std::min(sms * per_sm, std::max(jobs, npairs));
-    const double* Ain = A;
-    int mx = max_sweeps;
-    int64_t nn = n;
-    void* args[] = {(void*)&Ain, &nn, (void*)&nb, &G0, &G1, &Vp, &Us, &mx, &cnts, &sweeps, &Aout};
-    SKP_CUDA(cudaLaunchCooperativeKernel((void*)syevj_block_kernel, dim3(blocks),
-                                         dim3(kBJThreads), args, smem, st));
-    count_launch();
-    eig_sort_padded_kernel<<<grid_for(n), 256, 0, st>>>(Aout, n, Vp, npad, W, V);
-    SKP_LAUNCHED(eig_sort_padded_kernel);
-    return SKP_OK;
+    // n > 112: tridiagonal reduction + bisection + inverse iteration (eig_tri.cu)
+    return syev_tri(A, n, W, V, ws, ws_bytes, sweeps, st);
 }
 
 extern "C" int skp_cast_f32_f64(const float* x, double* y, int64_t count, void* stream) {

@@ -17,12 +17,9 @@ events on the launching stream).
 from __future__ import annotations
 
 import math
-import os
 import threading
-import time
 from dataclasses import dataclass, field
 
-import numpy as np
 import torch
 
 from . import _convert, _engine, _ops
@@ -91,19 +88,31 @@ class NystromResult:
 
 
 class _Phases:
-    """CUDA-event phase timer on the current stream (no-op when disabled)."""
+    """CUDA-event phase timer on the current stream (events only when
+    enabled) and NVTX ranges (always: skp.<phase> in nsys / ncu --nvtx).
+    mark(name, nxt) ends phase ``name`` and begins phase ``nxt``."""
 
     def __init__(self, enabled: bool):
         self.enabled = enabled
         self.ev = []
-        self.host = []
+        self.open = False
 
-    def mark(self, name: str):
+    def begin(self, nxt: str):
+        if self.open:
+            torch.cuda.nvtx.range_pop()
+        torch.cuda.nvtx.range_push("skp." + nxt)
+        self.open = True
+
+    def mark(self, name: str, nxt: str | None = None):
         if self.enabled:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
             self.ev.append((name, e))
-            self.host.append(time.perf_counter())
+        if nxt is not None:
+            self.begin(nxt)
+        elif self.open:
+            torch.cuda.nvtx.range_pop()
+            self.open = False
 
     def result(self, out: dict | None, scale: float = 1.0):
         if not self.enabled or out is None:
@@ -111,9 +120,6 @@ class _Phases:
         self.ev[-1][1].synchronize()
         for (_, a), (name, b) in zip(self.ev, self.ev[1:]):
             out[name] = out.get(name, 0.0) + a.elapsed_time(b) * scale
-        if os.environ.get("SKP_HOST_TRACE"):   # debug: host-side time per phase
-            for (name, _), h0, h1 in zip(self.ev[1:], self.host, self.host[1:]):
-                out["host_" + name] = out.get("host_" + name, 0.0) + (h1 - h0) * 1e3 * scale
 
 
 def _be(dtype, device):
@@ -180,7 +186,7 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     dev = a.device
     m_loc, n = a.shape
     be = _be(a.dtype, dev)
-    ph.mark("start")
+    ph.mark("start", "make_sketch")
     # Omega: the Gaussian kind is drawn on the device (omega_device, queued
     # after K2); the other kinds on a host thread while the device runs K1 + K2
     om_seed = substream(spec.seed, 1)
@@ -190,11 +196,10 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
     # the Gaussian Omega is drawn on a side stream, concurrently with the K2
     # plan (one warp per SM; K1 before it fills the GPU) and K2's first rows;
-    # only P^T waits for the plan (SKP_OMEGA_SIDE=0: in line; alternating A/B
-    # at C3, scripts/ab_omega.sh: 63.1 vs 63.5 ms per step)
-    om_side = _omega_side(spec, om_seed, a.dtype, dev, nonfinite) \
-        if om_job is None and os.environ.get("SKP_OMEGA_SIDE", "1") != "0" else None
-    ph.mark("make_sketch")
+    # only P^T waits for the plan (in line instead, alternating A/B at C3,
+    # scripts/ab_omega.sh: 63.5 vs 63.1 ms per step)
+    om_side = _omega_side(spec, om_seed, a.dtype, dev, nonfinite) if om_job is None else None
+    ph.mark("make_sketch", "apply_right")
     # K2 v2 writes A~ with its columns permuted (A S P); the power iteration
     # then uses P^T Omega, so Y = (A S P)(P^T Omega) = A S Omega exactly as in
     # the reference.  K2 v1 (natural column order) where v2 does not apply.
@@ -224,11 +229,11 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
             if not v2:
                 sk.right(a[r0:r1], out=atil[r0:r1], fro2=fro2, nonfinite=nonfinite)
                 e_io = None
-    ph.mark("apply_right")
+    ph.mark("apply_right", "split")
     # the power iteration's operand: A~ split once into fp16 hi/lo planes (the
     # fp32 A~ is released here; the footprint stays m x l x 4 bytes)
     atil = be.prepare(atil, e_io, inplace=True)
-    ph.mark("split")
+    ph.mark("split", "omega")
 
     def omega_for(perm_dev, host: bool = False):
         if om_side is not None and not host:
@@ -241,7 +246,7 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
         return job.to_device(dev, perm_dev)
 
     omega = omega_for(perm)
-    ph.mark("omega")
+    ph.mark("omega", "power")
     bad = comm.allreduce_(nonfinite)
     # Fast path: no host synchronisation until the end -- CholeskyQR failures
     # (numerical rank deficiency) are flagged on the device and checked once,
@@ -254,7 +259,7 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     # 128 GiB + A~ 31 GiB leave no room for Q); the rare eager rerun below
     # sketches again
     atil = None
-    ph.mark("power")
+    ph.mark("power", "orth")
     qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total, lazy=True,
                                 planes_out=planes_out)
     del y
@@ -329,7 +334,7 @@ def randsvd(a, q_basis, *, timings: dict | None = None) -> SvdResult:
         raise ValueError(f"dimension mismatch: Q has {oq.t.shape[0]} rows, a has {oa.t.shape[0]}")
     dt = _convert.common_dtype(oa, oq)
     ph = _Phases(timings is not None)
-    ph.mark("start")
+    ph.mark("start", "randsvd")
     u, s, v = _randsvd_dev(_convert.as_dtype(oa, dt), _convert.as_dtype(oq, dt))
     ph.mark("randsvd")
     ph.result(timings)
@@ -356,6 +361,7 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
     if isinstance(a, _convert.DeviceMatrix):
         a.finite = True
     st = {}
+    ph.begin("randsvd")
     u, s, v = _randsvd_dev(op.t, qb, check=True, amax_hint=hint.get("amax"), stats=st)
     ph.mark("randsvd")
     res = SvdResult(_convert.download(u, op.kind), _convert.download(s, op.kind),
@@ -379,16 +385,16 @@ def lowrank_factorize(a, spec: RangeFinderSpec) -> FactorizationResult:
     dev = t.device
     be = _be(t.dtype, dev)
     ph = _Phases(True)
-    ph.mark("t0")
+    ph.mark("t0", "sketch")
     s1 = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
     nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
     atil = s1.right(t, nonfinite=nonfinite)
-    ph.mark("sketch")
+    ph.mark("sketch", "power")
     if int(nonfinite.item()):
         raise ValueError("a contains non-finite entries")
     omega = omega_tensor(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), t.dtype, dev)
     y = _engine.power_iterate(be, _engine.LOCAL, atil, omega, spec.q, spec.stabilized)
-    ph.mark("power")
+    ph.mark("power", "regression")
     s2 = make_sketch(s2_kind, m, s2_r, substream(spec.seed, 2), s=spec.s, device=dev)
     s2y = s2.left_t(y)
     if float(_ops.sumsq(s2y).item()) == 0.0:
@@ -436,7 +442,7 @@ def _nystrom_dev(t: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL, row
     be = _be(t.dtype, dev)
     if stabilized is None:
         stabilized = t.dtype == F32 and spec.stabilized
-    ph.mark("t0")
+    ph.mark("t0", "sketch")
     sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
     nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
     ctil = sk.right(t, nonfinite=nonfinite)
@@ -450,7 +456,7 @@ def _nystrom_dev(t: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL, row
         wtil = shard.left_t(ctil)
     wtil = comm.allreduce_(wtil)
     be.symmetrize_(wtil)
-    ph.mark("sketch")
+    ph.mark("sketch", "contract")
     omega = omega_tensor(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), t.dtype, dev)
     cmat, w = _engine.nystrom(be, comm, ctil, wtil, omega, spec.q, stabilized)
     ph.mark("contract")

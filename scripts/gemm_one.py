@@ -1,5 +1,5 @@
 """One config-shape GEMM (for ncu):
-    python scripts/gemm_one.py nn|tn|qta [3xtf32|h3|h3s] [reps] [C3|C5]
+    python scripts/gemm_one.py nn|tn|qta|syrk [3xtf32|h3|h3s] [reps] [C3|C5]
 (qta: randsvd's B^T = A^T Q with A m x n)"""
 import sys
 import torch
@@ -24,6 +24,9 @@ if kind == "qta":
         f = lambda: _ops.gemm_h3s_t(a, e_a, sq)
     else:
         f = lambda: _ops.gemm(a, q, True, False, mode=mode)
+elif kind == "syrk":
+    sa = _ops.split_h2_inplace(at)
+    f = lambda: _ops.syrk_h3(sa)
 elif kind == "nn":
     z = _ops.empty2d(l, r2, torch.float32, "cuda")
     z.normal_()
@@ -40,7 +43,12 @@ else:
         f = lambda: _ops.gemm_h3(sa, sy, ta=True)
     else:
         f = lambda: _ops.gemm(at, y, True, False, mode=mode)
+f()
+torch.cuda.synchronize()
+t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+t0.record()
 for _ in range(reps):
     f()
+t1.record()
 torch.cuda.synchronize()
-print("ok")
+print("ok", kind, mode, cfg, "ms per call %.3f" % (t0.elapsed_time(t1) / reps))

@@ -11,7 +11,7 @@ from paper_2605_09755_b200.sketching import make_sketch
 n, l = 16384, 4000
 op = make_sketch("countsketch", n, l, 7, s=8)
 plan, perm = op.gather_plan()
-from paper_2605_09755_b200._ops import GATHER_COLS
+GATHER_COLS = 896  # sketch_gather.cu kGCols
 W = GATHER_COLS // 32
 P = -(-l // (GATHER_COLS - 96))
 g = plan.cpu().numpy().view(np.uint32)

@@ -465,16 +465,6 @@ def test_syrk_h3_inplace_planes_long_k(ops):
     assert (out.double() - ref).abs().max().item() <= 2e-5 * torch.diagonal(ref).max().item()
 
 
-def test_gemm_h3_pair_forced_small(ops, monkeypatch):
-    monkeypatch.setenv("SKP_H3_FORCE2CTA", "1")
-    g = torch.Generator(device="cuda").manual_seed(3)
-    a = torch.randn(100, 300, generator=g, device="cuda")
-    b = torch.randn(300, 48, generator=g, device="cuda")
-    out = ops.gemm_h3(ops.split_h2(a), ops.split_h2(b, trans=True))
-    ref = a.double() @ b.double()
-    assert (out.double() - ref).abs().max().item() <= 2e-6 * np.sqrt(300) * 25
-
-
 # ----------------------------------------------------------- K5 / K6 ------
 
 def _spd(n, cond=1e4, seed=0):

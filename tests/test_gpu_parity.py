@@ -395,7 +395,7 @@ def test_planes_power_iteration_matches_fp32_path(skp, monkeypatch):
     q = power._range_finder_dev(a, spec)
     qq = q.double().T @ q.double()
     assert (qq - torch.eye(qq.shape[0], device="cuda", dtype=torch.float64)).abs().max().item() < 2e-5
-    monkeypatch.setenv("SKP_NO_H3", "1")
+    monkeypatch.setattr(_ops, "H3_MIN_ELEMS", 1 << 62)     # every product on 3xTF32
     res32, rel32 = skp.rsvd(a, spec, with_error=True)
     s_h, s_32 = res.sigma.double().cpu(), res32.sigma.double().cpu()
     assert (s_h - s_32).abs().max().item() <= 1e-5 * s_32[0].item()
