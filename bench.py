@@ -47,6 +47,9 @@ CONFIGS = {
     "C1": dict(m=2000, n=1000, l=200, s=8, k=20, r2=30, q=2, dtype="f64", gen="c1"),
     "C2": dict(m=20000, n=10000, l=2000, s=8, k=100, r2=110, q=3, dtype="f32", gen="c2"),
     "C3": dict(m=262144, n=16384, l=4000, s=8, k=500, r2=520, q=3, dtype="f32", gen="c3"),
+    # psd Nystrom of the RBF kernel (BASELINE configs[3]; n x n fp32 = 17.2 GB, r2 = k assumed)
+    "C4": dict(m=65536, n=65536, l=4096, s=8, k=256, r2=256, q=2, dtype="f32", gen="c4", seed=4,
+               nystrom=True),
     # the headline: the largest config that fits one B200 (BASELINE configs[4], l = 8000, q = 4)
     "C5": dict(m=1048576, n=32768, l=8000, s=8, k=1000, r2=1050, q=4, dtype="f32", gen="c5",
                seed=5),
@@ -494,6 +497,198 @@ def _e2e_sharded(host, spec, m, comm, device, D):
 
 REF_MAX_STEPS, REF_MAX_WARMUP = 5, 1
 
+# ------------------------------------------------------------- C4: Nystrom ----
+NYS_SUB = 8192     # CPU baseline / slab parity: the leading principal n' x n' submatrix
+
+
+def c4_points(cfg):
+    from paper_2605_09755_b200 import datagen
+    x = datagen.rbf_points(cfg["n"], 16, seed=cfg["seed"])
+    return x, datagen.rbf_bandwidth(x, 4096, seed=cfg["seed"])
+
+
+def nystrom_spec(cfg):
+    from paper_2605_09755_b200 import RangeFinderSpec
+    return RangeFinderSpec(k=cfg["k"], l=cfg["l"], r1=cfg["l"], r2=cfg["r2"], q=cfg["q"], eps=0.5,
+                           seed=cfg["seed"], s=cfg["s"])
+
+
+def nystrom_rel_err_dev(kmat, c, w):
+    """||K - C W^+ C^T||_F / ||K||_F on the device (fp64, row blocks)."""
+    import torch
+    wp = torch.linalg.pinv(w.double(), hermitian=True)
+    right = wp @ c.double().T                       # r2 x n
+    num = den = 0.0
+    for r0 in range(0, kmat.shape[0], 4096):
+        kb = kmat[r0:r0 + 4096].double()
+        num += float(((kb - c[r0:r0 + 4096].double() @ right) ** 2).sum())
+        den += float((kb ** 2).sum())
+    return (num / den) ** 0.5
+
+
+def cpu_baseline_nystrom(cfg, sub=NYS_SUB):
+    """The oracle's literal nystrom_core (fp64, as the reference computes) on
+    the leading sub x sub principal block of the workload's own K; phases
+    extrapolated to n (K S ~ n^2, S^T C~ and C~ Y ~ n, the l-dimensional core
+    not scaled).  The reference's O(n^3) psd eigen-check is not timed (ours
+    skips it above n = 1024 too)."""
+    from paper_2605_09755_b200 import datagen
+    from oracle import skp_oracle as o
+    x, h = c4_points(cfg)
+    xs = x[:sub]
+    sq = (xs * xs).sum(1)
+    kmat = np.exp(-np.maximum(sq[:, None] + sq[None, :] - 2.0 * xs @ xs.T, 0.0) / (2 * h * h))
+    kmat = np.minimum(kmat, kmat.T).astype(np.float32)
+    spec = o.Spec(k=cfg["k"], l=cfg["l"], r1=cfg["l"], r2=cfg["r2"], q=cfg["q"],
+                  seed=cfg["seed"], s=cfg["s"])
+    t = {}
+    c, w = o.nystrom_core(kmat, spec, stabilized=False, timings=t)
+    f = cfg["n"] / sub
+    full = t["apply_right"] * f * f + (t["left_t"] + t["contract"]) * f + t["core"]
+    det = {"phases_s_sample": {k: round(v, 4) for k, v in t.items()},
+           "sample": f"leading {sub} x {sub} principal block of the {cfg['n']}-point RBF kernel; "
+                     f"K S extrapolated x{f * f:g} (n^2), S^T C~ and C~ Y x{f:g} (n), the "
+                     "l-dimensional core not scaled; the reference's O(n^3) psd check not timed"}
+    del xs
+    return full * 1e3, det, (kmat, spec, c, w)
+
+
+def nystrom_slab_parity(cfg, kmat, spec_o):
+    """nystrom_psd (fp32 sketch, fp64 literal core) on the CPU baseline's
+    principal block against the oracle's literal core on the same bytes."""
+    import torch
+    import paper_2605_09755_b200 as skp
+    from oracle import skp_oracle as o
+    co, wo = o.nystrom_core(kmat, spec_o, stabilized=False)
+    eo = o.nystrom_rel_error(kmat, co, wo)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    kd = torch.from_numpy(kmat).to(dev)
+    res = skp.nystrom_psd(kd, nystrom_spec(cfg))
+    e = nystrom_rel_err_dev(kd, res.C, res.W)
+    # literal on both sides: the same Y up to rounding, so W's leading
+    # eigenvalues are comparable
+    wg = np.sort(np.linalg.eigvalsh(res.W.double().cpu().numpy()))[::-1]
+    wr = np.sort(np.linalg.eigvalsh(wo))[::-1]
+    # |d lambda_i| / (1e-5 |lambda_i| + 1e-7 |lambda_1|): <= 1 passes
+    dev_w = np.abs(wg - wr) / (1e-5 * np.abs(wr) + 1e-7 * np.abs(wr[0]))
+    return {"n": int(kmat.shape[0]), "rel_err": [e, eo], "rel_err_rel_diff": abs(e - eo) / eo,
+            "W_eig_max_dev_over_tol": float(dev_w.max()),
+            "tolerance": {"rel_err": 1e-3,
+                          "W_eig": "|d lambda_i| <= 1e-5 lambda_i + 1e-7 lambda_1 (fp32 sketch)"}}
+
+
+def run_nystrom(args, cfg, rank, world, local_rank):
+    """C4: psd Nystrom (power.py:258-298) of the 65536-point RBF kernel.  A
+    step = the device symmetry check (N = 1; the transposed tiles live on
+    other ranks at N > 1) + sketch K S (K2 v2) + W~ = S^T C~ (all-reduced) +
+    the l-dimensional core + C = C~ Y, with K resident in HBM."""
+    import torch
+    import torch.distributed as dist
+    import paper_2605_09755_b200 as skp
+    from paper_2605_09755_b200 import _lib, _ops, datagen, distributed as D, power
+    from paper_2605_09755_b200.sketching import make_sketch, substream
+    device = torch.device("cuda", local_rank % torch.cuda.device_count())
+    torch.cuda.set_device(device)
+    comm = D.TorchComm() if world > 1 else _LocalComm()
+    n, l, s_ = cfg["n"], cfg["l"], cfg["s"]
+    x, h = c4_points(cfg)
+    row0, rows = D.shard_rows(n, world, rank)
+    kmat = datagen.rbf_kernel_gpu(x, h, device=device, row0=row0, rows=rows)
+    spec = nystrom_spec(cfg)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        if world == 1:
+            power._check_psd_dev(kmat)
+        return D.nystrom_sharded(kmat, spec, row0, n, comm)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = _lib.load().skp_launch_count()
+    clk = ClockSampler(device.index)
+    clk.start()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        c, w = step()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    launches = _lib.load().skp_launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    rel = nystrom_rel_err_dev(kmat, c, w) if world == 1 else None
+    hbm, _, _, _ = load_peaks()
+    # the dominant kernel: K2 v2 on the rank's rows of K
+    sk = make_sketch("countsketch", n, l, substream(spec.seed, 0), s=s_, device=device)
+    ctil = _ops.empty2d(rows, l, kmat.dtype, device)
+    nonfinite = torch.zeros(1, dtype=torch.int64, device=device)
+    v2 = sk.right_permuted(kmat, out=ctil, nonfinite=nonfinite) is not None
+    run_sketch = (lambda: sk.right_permuted(kmat, out=ctil, nonfinite=nonfinite)) if v2 else \
+        (lambda: sk.right(kmat, out=ctil, nonfinite=nonfinite))
+    sk_ms = _time_launches(run_sketch)
+    sk_bytes = rows * n * 4 + rows * l * 4 + n * s_ * 5
+    sym_ms = _time_launches(lambda: _ops.sym_check(kmat)) if world == 1 else None
+    del ctil
+    sk_gbs = sk_bytes / (sk_ms * 1e-3) / 1e9
+    roof = {"kernel": "sketch_gather (K2 v2) C~ = K S" if v2 else "sketch_right (K2 v1)",
+            "bound": "hbm", "achieved": round(sk_gbs, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(sk_gbs / hbm, 4), "traffic": None,
+            "traffic_unit": "DRAM bytes per launch (ncu --set full)",
+            "ms_per_launch": round(sk_ms, 4), "algorithmic_bytes_per_launch": sk_bytes,
+            "share_of_step": round(sk_ms / ms, 3)}
+    extra = {}
+    if sym_ms is not None:
+        sb = n * n * 4
+        extra["sym_check"] = {"ms": round(sym_ms, 4), "GB/s": round(sb / (sym_ms * 1e-3) / 1e9, 1),
+                              "frac_hbm": round(sb / (sym_ms * 1e-3) / 1e9 / hbm, 4),
+                              "bytes": sb, "share_of_step": round(sym_ms / ms, 3)}
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        host = torch.empty(tuple(kmat.shape), dtype=kmat.dtype, pin_memory=True)
+        host.copy_(kmat)
+        del kmat
+        torch.cuda.empty_cache()
+        skp.nystrom_psd(host, spec)
+        torch.cuda.synchronize()
+        k2 = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(k2):
+            res = skp.nystrom_psd(host, spec)
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / k2
+        e2e = {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": n * n * 4,
+               "d2h_bytes_per_step": int(res.C.numel() * 4 + res.W.numel() * 4), "steps": k2,
+               "api": "paper_2605_09755_b200.nystrom_psd(pinned host tensor)"}
+        del host
+    if rank != 0:
+        return None, None
+    line = {
+        "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 (l-dimensional core: 3xTF32 / SIMT fp32 products, fp64 small factorisations)",
+        "data": "synthetic (seeded RBF points, BASELINE config recipe)",
+        "config": {"workload": args.config, "n": n, "l": l, "s": s_, "k": cfg["k"],
+                   "r2": cfg["r2"], "q": cfg["q"], "bandwidth_h": round(h, 6),
+                   "parallelism": f"rows of K sharded x{world} (NCCL allreduce of the l x l W~)",
+                   "l2": "no flush: K (17.2 GB) is far larger than the 126 MB L2"},
+        "nystrom_rel_err": rel, "roofline": roof, "sketch": dict(roof), **extra,
+        "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e,
+    }
+    return line, None
+
+
 
 def run_reference(args, cfg):
     """The reference's CPU path (the oracle port) on the workload's first
@@ -504,6 +699,8 @@ def run_reference(args, cfg):
     ncores = host_threads()
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ.setdefault(var, str(ncores))
+    if cfg.get("nystrom"):
+        return run_reference_nystrom(args, cfg, ncores)
     slab = workload_slab(cfg, args.cpu_rows)
     steps = max(1, min(args.steps, REF_MAX_STEPS))
     warm = min(args.warmup, REF_MAX_WARMUP)
@@ -528,6 +725,30 @@ def run_reference(args, cfg):
                                    f"m-linear phases extrapolated x{cfg['m'] / det['rows_sampled']:g}"
                                    " (sketch draw, Omega, SVD of B not scaled); median of "
                                    f"{steps} samples",
+                         **det},
+        "e2e": {"value": round(val, 1), "unit": "ms", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def run_reference_nystrom(args, cfg, ncores):
+    steps = max(1, min(args.steps, REF_MAX_STEPS))
+    warm = min(args.warmup, REF_MAX_WARMUP)
+    vals, det = [], None
+    for i in range(warm + steps):
+        v, det, _ = cpu_baseline_nystrom(cfg)
+        if i >= warm:
+            vals.append(v)
+    val = statistics.median(vals)
+    return {
+        "metric": METRIC, "impl": "reference", "value": round(val, 1), "unit": "ms",
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "ms_per_step": round(val, 1), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64 (numpy/scipy, as the reference computes)",
+        "data": "synthetic (seeded RBF points, BASELINE config recipe)",
+        "config": {"workload": args.config, **{k: cfg[k] for k in ("n", "l", "s", "k", "r2", "q")}},
+        "cpu_baseline": {"value": round(val, 1), "unit": "ms", "cores": ncores, "kind": "port",
                          **det},
         "e2e": {"value": round(val, 1), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -576,6 +797,20 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group("gloo")
+    if cfg.get("nystrom"):
+        line, _ = run_nystrom(args, cfg, rank, world, local_rank)
+        if line is not None and world == 1 and not args.no_cpu:
+            v, det, (kmat, spec_o, _, _) = cpu_baseline_nystrom(cfg)
+            line["cpu_baseline"] = {"value": round(v, 1), "unit": "ms", "cores": host_threads(),
+                                    "kind": "port", **det}
+            line["slab_parity"] = nystrom_slab_parity(cfg, kmat, spec_o)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     line, slab = run_ours(args, cfg, rank, world, local_rank)
     if line is not None:
         if world == 1 and not args.no_cpu:

@@ -218,6 +218,11 @@ int skp_cast_f64_f32(const double* x, float* y, int64_t count, void* stream);
 /* 2-D strided casts: y[i*ldy + j] = x[i*ldx + j] for i < rows, j < cols */
 int skp_cast2d_f32_f64(const float* x, int64_t ldx, double* y, int64_t ldy, int64_t rows,
                        int64_t cols, void* stream);
+/* skp_sym_check_{f32,f64}: out[0] = max_ij |A_ij - A_ji|, out[1] = max |A_ij|
+ * (n x n, leading dimension ld; fp64 outputs), reading A once -- the
+ * symmetry test of _check_psd (power.py:242-255) at any size.              */
+int skp_sym_check_f32(const float* A, int64_t n, int64_t ld, double* out, void* stream);
+int skp_sym_check_f64(const double* A, int64_t n, int64_t ld, double* out, void* stream);
 int skp_cast2d_f64_f32(const double* x, int64_t ldx, float* y, int64_t ldy, int64_t rows,
                        int64_t cols, void* stream);
 /* ------------------------------------------------------------ 3xFP16 ----

@@ -270,27 +270,37 @@ def lowrank_factorize(a, spec: Spec):
     return y, pinv(s2.apply_left_transpose(y)) @ s2.apply_left_transpose(a)
 
 
-def nystrom_core(a, spec: Spec, stabilized: bool = False):
+def nystrom_core(a, spec: Spec, stabilized: bool = False, timings: dict | None = None):
     """power.py:272-287 without _check_psd (O(n^3), infeasible at C4).
 
     ``stabilized=False`` is the literal reference (Y = W~^q Omega).
     ``stabilized=True`` orthonormalises between W~ products -- same span in
     exact arithmetic; the parity reference for FP32.
+    ``timings`` (optional): seconds per phase (apply_right = K S, left_t =
+    S^T C~, core = the l-dimensional power + W, contract = C~ Y).
     Returns (C, W).
     """
+    import time
+    t = {} if timings is None else timings
+    t0 = time.perf_counter()
     a = as_matrix(a)
     n = a.shape[0]
     sk = CountSketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s)
     ctil = sk.apply_right(a)
+    t1 = time.perf_counter()
     wtil = sk.apply_left_transpose(ctil)
     wtil = (wtil + wtil.T) / 2.0
+    t2 = time.perf_counter()
     y = draw_omega(spec.r1, spec.r2, substream(spec.seed, 1))
     for _ in range(spec.q):
         if stabilized:
             y = orthonormalize(y)
         y = wtil @ y
-    c = ctil @ y
     w = y.T @ (wtil @ y)
+    t3 = time.perf_counter()
+    c = ctil @ y
+    t4 = time.perf_counter()
+    t.update(apply_right=t1 - t0, left_t=t2 - t1, core=t3 - t2, contract=t4 - t3)
     return c, (w + w.T) / 2.0
 
 

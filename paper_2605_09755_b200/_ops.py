@@ -214,6 +214,15 @@ def gaussian(st: int, inc: int, rows: int, cols: int, divisor: float, dtype, dev
     return out
 
 
+def sym_check(x: torch.Tensor) -> torch.Tensor:
+    """(max |x - x^T|, max |x|) as a float64 device tensor of 2, reading the
+    square matrix x once (skp_sym_check)."""
+    n, _, ld = _rows_ld(x)
+    out = torch.empty(2, dtype=F64, device=x.device)
+    call(f"skp_sym_check_{_SFX[x.dtype]}", ptr(x), n, ld, ptr(out), stream_ptr(x.device))
+    return out
+
+
 def permute_rows(x: torch.Tensor, perm_dev: torch.Tensor, out=None) -> torch.Tensor:
     """out[v, :] = x[perm_dev[v], :] for v < x.shape[0] (perm_dev: int32 on the device)."""
     rows, cols, ldx = _rows_ld(x)

@@ -151,7 +151,10 @@ gather_sort_kernel(const int32_t* __restrict__ colptr, const int32_t* __restrict
     __shared__ int order[kGCols];      // units in placement order (column index)
     __shared__ int lane_col[kGCols];   // lane -> column (-1 empty)
     __shared__ int lane_part[kGCols];  // 0 single, 1 first half (primary), 2 second half
-    __shared__ int hist[kGTMax + 2];
+    // entry counts over all column passes: a lane's per-pass count is ~1/H
+    // of it, so totals up to H * kGTMax are schedulable
+    constexpr int kHist = kGTMax * kGMaxPass + 2;
+    __shared__ int hist[kHist];
     __shared__ int s_cap;
     // column passes (n > one row buffer): bnd[v][h] = first entry of column v
     // with j >= h * npass (entries are ascending in j)
@@ -164,12 +167,13 @@ gather_sort_kernel(const int32_t* __restrict__ colptr, const int32_t* __restrict
         lane_col[v] = -1;
         lane_part[v] = 0;
     }
-    for (int v = threadIdx.x; v < kGTMax + 2; v += blockDim.x) hist[v] = 0;
+    for (int v = threadIdx.x; v < kHist; v += blockDim.x) hist[v] = 0;
+    const int cmax = H * kGTMax + 1;  // histogram clamp
     if (blockIdx.x == 0)
         for (int64_t v = r + threadIdx.x; v < slots; v += blockDim.x) perm[v] = -1;
     __syncthreads();
     for (int v = threadIdx.x; v < nc; v += blockDim.x) {
-        atomicAdd(&hist[min(key[v], kGTMax + 1)], 1);
+        atomicAdd(&hist[min(key[v], cmax)], 1);
         const int b0 = colptr[c0 + v], b1 = colptr[c0 + v + 1];
         bnd[v][0] = b0;
         bnd[v][H] = b1;
@@ -187,11 +191,11 @@ gather_sort_kernel(const int32_t* __restrict__ colptr, const int32_t* __restrict
     __syncthreads();
     if (threadIdx.x == 0) {
         long long tot = 0;
-        for (int c = 0; c <= kGTMax + 1; ++c) tot += (long long)c * hist[c];
+        for (int c = 0; c <= cmax; ++c) tot += (long long)c * hist[c];
         const int mean = nc ? (int)((tot + nc - 1) / nc) : 0;
         // columns above cap become 2 lanes (+ at most one hole each)
-        int above = 0, cap = kGTMax + 1;
-        for (int c = kGTMax + 1; c >= mean; --c) {
+        int above = 0, cap = cmax;
+        for (int c = cmax; c >= mean; --c) {
             if (nc + 2 * (above + hist[c]) > lanes) break;
             above += hist[c];
             cap = c - 1;

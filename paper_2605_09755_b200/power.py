@@ -416,10 +416,9 @@ def _check_psd_dev(t: torch.Tensor, tol: float = 1e-8) -> None:
     n = t.shape[0]
     if t.shape[0] != t.shape[1]:
         raise ValueError(f"psd input must be square, got {tuple(t.shape)}")
-    scale = float(t.abs().max().item())
+    asym, scale = _ops.sym_check(t).tolist()      # one tiled pass over t, one sync
     if scale == 0.0:
         return
-    asym = float((t - t.T).abs().max().item())
     if asym > tol * scale:
         raise ValueError("matrix is not symmetric within tolerance")
     if n <= PSD_EIG_MAX:
@@ -435,19 +434,41 @@ def _check_psd_dev(t: torch.Tensor, tol: float = 1e-8) -> None:
 def _nystrom_dev(t: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL, row0: int = 0,
                  n_total: int | None = None, stabilized: bool | None = None,
                  phases: _Phases | None = None):
-    """Alg. 3 on a row slab t = K[row0:row0+rows, :] (power.py:272-287)."""
+    """Alg. 3 on a row slab t = K[row0:row0+rows, :] (power.py:272-287).
+
+    The sketch C~ = K S runs in the input's precision (K2); everything after
+    it -- W~ = S^T C~, the power on W~, C = C~ Y and W = Y^T W~ Y -- runs in
+    fp64, as in the reference (as_matrix casts to float64): the core W is
+    ill-conditioned (C4: the Nystrom error came out 4x the reference's with
+    an fp32 core), and C, W are returned as float64 like the reference's.
+    FP64 follows the reference literally (Y = W~^q Omega) unless
+    ``stabilized`` asks for the orthonormalised power (same span)."""
     ph = phases or _Phases(False)
     dev = t.device
     n = t.shape[1] if n_total is None else n_total
-    be = _be(t.dtype, dev)
+    be = _be(F64, dev)
     if stabilized is None:
-        stabilized = t.dtype == F32 and spec.stabilized
+        stabilized = False
     ph.mark("t0", "sketch")
     sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
     nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
-    ctil = sk.right(t, nonfinite=nonfinite)
-    if int(comm.allreduce_(nonfinite).item()):
+    # K2 v2 (row gather) writes C~ P -- columns permuted by the plan; the
+    # whole core then runs in permuted sketch coordinates: W~_P = P^T W~ P
+    # (rows of S^T C~ P permuted), Omega_P = P^T Omega, so C = (C~ P)(P^T Y)
+    # and W = Y^T W~ Y are the reference's (power.py:276-287).  K2 v1
+    # (natural order) where v2 does not apply or its plan fails.
+    got = sk.right_permuted(t, nonfinite=nonfinite, deferred=True)
+    ctil, perm = got if got is not None else (None, None)
+    bad = int(comm.allreduce_(nonfinite).item())
+    if bad >= _ops.GATHER_PLAN_FAIL_MARK:
+        nonfinite.zero_()
+        ctil, perm = None, None
+    if ctil is None:
+        ctil = sk.right(t, nonfinite=nonfinite)
+        bad = int(comm.allreduce_(nonfinite).item())
+    if bad % _ops.GATHER_PLAN_FAIL_MARK:
         raise ValueError("a contains non-finite entries")
+    ctil = _ops.cast(ctil, F64)          # exact widening; the core is fp64
     rows = t.shape[0]
     if rows == n:
         wtil = sk.left_t(ctil)
@@ -455,9 +476,13 @@ def _nystrom_dev(t: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL, row
         shard = _shard_sketch(sk, row0, rows)
         wtil = shard.left_t(ctil)
     wtil = comm.allreduce_(wtil)
+    if perm is not None:
+        wtil = _ops.permute_rows(wtil, perm)
     be.symmetrize_(wtil)
     ph.mark("sketch", "contract")
-    omega = omega_tensor(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), t.dtype, dev)
+    omega = omega_tensor(spec.omega_kind, spec.r1, spec.r2, substream(spec.seed, 1), F64, dev)
+    if perm is not None:
+        omega = _ops.permute_rows(omega, perm)
     cmat, w = _engine.nystrom(be, comm, ctil, wtil, omega, spec.q, stabilized)
     ph.mark("contract")
     return cmat, w
@@ -492,10 +517,10 @@ def _shard_sketch(sk, row0, rows):
 def nystrom_psd(a, spec: RangeFinderSpec, *, stabilized: bool | None = None) -> NystromResult:
     """Psd Nystrom a ~= C pinv(W) C^T (power.py:258-298).
 
-    FP64 input follows the reference literally (Y = W~^q Omega).  FP32 input
-    orthonormalises between the W~ products (same span)
-    unless ``spec.stabilized`` is False or ``stabilized=False`` is passed:
-    the literal fp32 power collapses the block (SURVEY.md §7 hard part 5)."""
+    The sketch C~ = a S runs in a's precision (fp32: K2 v2); the core after
+    it in fp64, literally as the reference (Y = W~^q Omega; ``stabilized=True``
+    orthonormalises between the W~ products instead -- same span).
+    C and W are float64, as the reference returns them."""
     op = _convert.upload(a, "a", check_finite=False)
     t = op.t
     n = t.shape[0]
