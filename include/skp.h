@@ -218,6 +218,19 @@ int skp_cast_f64_f32(const double* x, float* y, int64_t count, void* stream);
 /* 2-D strided casts: y[i*ldy + j] = x[i*ldx + j] for i < rows, j < cols */
 int skp_cast2d_f32_f64(const float* x, int64_t ldx, double* y, int64_t ldy, int64_t rows,
                        int64_t cols, void* stream);
+/* skp_gesvj_{f64,f32}: thin SVD A = U diag(S) V^T of A (m x n, m >= n,
+ * row-major, lda) by one-sided Jacobi in fp64 (replaces LAPACK gesdd behind
+ * thin_svd / pinv, reference linalg.py:84-106): every sigma_i to an absolute
+ * ~eps sigma_1, so ill-conditioned inputs keep their small singular values.
+ * S descending (n), U (m x n, ldu), V (n x n, ldv), fp64; *sweeps = sweeps
+ * run (<= max_sweeps).  ws: skp_gesvj_ws_bytes(m, n).                      */
+int64_t skp_gesvj_ws_bytes(int64_t m, int64_t n);
+int skp_gesvj_f64(const double* A, int64_t m, int64_t n, int64_t lda, double* S, double* U,
+                  int64_t ldu, double* V, int64_t ldv, int32_t max_sweeps, void* ws,
+                  int64_t ws_bytes, int32_t* sweeps, void* stream);
+int skp_gesvj_f32(const float* A, int64_t m, int64_t n, int64_t lda, double* S, double* U,
+                  int64_t ldu, double* V, int64_t ldv, int32_t max_sweeps, void* ws,
+                  int64_t ws_bytes, int32_t* sweeps, void* stream);
 /* skp_sym_check_{f32,f64}: out[0] = max_ij |A_ij - A_ji|, out[1] = max |A_ij|
  * (n x n, leading dimension ld; fp64 outputs), reading A once -- the
  * symmetry test of _check_psd (power.py:242-255) at any size.              */

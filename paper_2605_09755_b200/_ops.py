@@ -214,6 +214,22 @@ def gaussian(st: int, inc: int, rows: int, cols: int, divisor: float, dtype, dev
     return out
 
 
+def gesvj(a: torch.Tensor, max_sweeps: int = 40):
+    """One-sided Jacobi thin SVD of a (m x n, m >= n; fp32 or fp64): fp64
+    (U m x n, S n descending, V n x n) -- skp_gesvj."""
+    m, n, lda = _rows_ld(a)
+    dev = a.device
+    s = torch.empty(n, dtype=F64, device=dev)
+    u = empty2d(m, n, F64, dev)
+    v = empty2d(n, n, F64, dev)
+    sweeps = torch.zeros(1, dtype=torch.int32, device=dev)
+    wsb = int(_lib.load().skp_gesvj_ws_bytes(m, n))
+    ws = workspace(dev, wsb)
+    call(f"skp_gesvj_{_SFX[a.dtype]}", ptr(a), m, n, lda, ptr(s), ptr(u), u.stride(0), ptr(v),
+         v.stride(0), max_sweeps, ptr(ws), wsb, ptr(sweeps), stream_ptr(dev))
+    return u, s, v
+
+
 def sym_check(x: torch.Tensor) -> torch.Tensor:
     """(max |x - x^T|, max |x|) as a float64 device tensor of 2, reading the
     square matrix x once (skp_sym_check)."""

@@ -1,10 +1,13 @@
 """Dense linalg on the B200 (drop-in for skpower.linalg, reference linalg.py).
 
 ``orthonormalize`` is CholeskyQR2 with a rank-revealing eigen pass
-(replaces the pivoted QR of linalg.py:57-81); ``thin_svd`` / ``pinv`` go
-through the fp64 Gram matrix and the device Jacobi eigensolver (replace
-LAPACK gesdd, linalg.py:84-106).  Results follow the operand kind (numpy in
--> numpy out, CUDA tensor in -> CUDA tensor out).
+(replaces the pivoted QR of linalg.py:57-81); ``thin_svd`` / ``pinv`` run
+the one-sided Jacobi SVD in fp64 on the matrix itself (replace LAPACK
+gesdd, linalg.py:84-106): no Gram matrix, so cond 1e12 inputs keep their
+small singular values.  (randsvd's r2 x n core keeps the Gram route, whose
+eigen-decomposition of B B^T resolves sigma_i >~ 1e-8 sigma_1 -- DESIGN.md.)
+Results follow the operand kind (numpy in -> numpy out, CUDA tensor in ->
+CUDA tensor out).
 """
 from __future__ import annotations
 
@@ -64,22 +67,14 @@ def orthonormalize(y, tol: float | None = None):
 
 
 def _thin_svd_dev(be, a: torch.Tensor):
+    """(U, sigma, V) of a (p x q) by one-sided Jacobi on a (p >= q) or a^T;
+    fp64 results, cast to the compute dtype for U and V."""
     p, q = a.shape
-    if p <= q:
-        g = be.gram64_rows(a)                      # a a^T
-        w, v = be.eig_desc64(g)
-        sig, inv = be.sqrt_eigs(w)
-        u = be.to_compute(v)
-        vv = be.mm(a, u, ta=True)
-        be.scale_cols_(vv, inv)
-        return u, sig, vv
-    g = be.gram64_rows(a.T.contiguous())           # a^T a
-    w, v = be.eig_desc64(g)
-    sig, inv = be.sqrt_eigs(w)
-    vv = be.to_compute(v)
-    u = be.mm(a, vv)
-    be.scale_cols_(u, inv)
-    return u, sig, vv
+    if p >= q:
+        u, s, v = _ops.gesvj(a)
+    else:
+        v, s, u = _ops.gesvj(a.T.contiguous())
+    return be.to_compute(u), s, be.to_compute(v)
 
 
 def thin_svd(a) -> SvdResult:
