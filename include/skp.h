@@ -276,23 +276,30 @@ int skp_gemm_h3(int transA, int64_t M, int64_t N, int64_t K, float alpha, const 
  * ceil(log2 K) bounds every entry), stored to *e_out.  An entry that does
  * not fit fp16 (or NaN) sets *overflow (may be NULL).  The epilogue's rows
  * are consecutive in C^T, so the transposed planes are written coalesced:
- * products feed the next product without an fp32 round trip or split pass. */
+ * products feed the next product without an fp32 round trip or split pass.
+ * b_lower = 1: B (stored N x K) is lower triangular (Q = Y L^-T with L^-1
+ * from the Cholesky kernel), so each N tile stops at its own K extent --
+ * half the MMAs of the dense product.                                       */
 int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, float alpha, const void* A_hi,
                        const void* A_lo, int64_t lda, const int32_t* a_exp, const void* B_hi,
                        const void* B_lo, int64_t ldb, const int32_t* b_exp, void* Ct_hi,
                        void* Ct_lo, int64_t ldct, int32_t shift, int32_t fixed, int32_t e_fixed,
-                       int32_t* e_out, int32_t* overflow, void* stream);
+                       int32_t* e_out, int32_t* overflow, int32_t b_lower, void* stream);
 
 /* skp_syrk_h3: C = alpha A^T A (N x N, fp32, exactly symmetric) from the
- * pre-split planes of A stored K x N (lda % 64 == 0, both GEMM operands
- * MN-major).  Replaces the operator A~^T A~ that power.py:131-133 applies
+ * pre-split planes of A stored K x N (kmajor = 0, lda % 64 == 0, both GEMM
+ * operands MN-major) or A^T stored N x K (kmajor = 1: the Gram of the rows,
+ * e.g. Y^T Y from the planes of Y^T; split over K when there are fewer
+ * lower-triangle tiles than CTA pairs, ws: skp_syrk_h3_ws_bytes).  Replaces the operator A~^T A~ that power.py:131-133 applies
  * twice per power step (y = atil @ (atil.T @ y)): formed once, the q power
  * steps then run in the l-dimensional sketch space (SKETCH-SPACE power
  * iteration).  Only the tiles meeting the lower triangle run;
  * the strict upper triangle is mirrored.  Same 3xFP16 numerics as
  * skp_gemm_h3 (2^-22 per product, register-promoted accumulation).          */
-int skp_syrk_h3(int64_t N, int64_t K, float alpha, const void* A_hi, const void* A_lo,
-                int64_t lda, const int32_t* a_exp, float* C, int64_t ldc, void* stream);
+int64_t skp_syrk_h3_ws_bytes(int64_t N, int64_t K);
+int skp_syrk_h3(int32_t kmajor, int64_t N, int64_t K, float alpha, const void* A_hi,
+                const void* A_lo, int64_t lda, const int32_t* a_exp, float* C, int64_t ldc,
+                void* ws, int64_t ws_bytes, void* stream);
 
 /* skp_gemm_h3s: C = alpha A^T B + beta C with A (K x M, fp32, lda % 32 == 0)
  * split into fp16 hi/lo INSIDE the kernel with the caller's exponent 2^a_exp

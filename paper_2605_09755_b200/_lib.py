@@ -69,7 +69,7 @@ SIGNATURES = {
     "skp_gemm_h3": (_int, [_int, _i64, _i64, _i64, _f32, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
                            _f32, _vp, _i64, _vp, _i64, _vp]),
     "skp_gemm_h3_emit_t": (_int, [_int, _i64, _i64, _i64, _f32, _vp, _vp, _i64, _vp, _vp, _vp, _i64,
-                                  _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]),
+                                  _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _vp]),
     "skp_gesvj_ws_bytes": (_i64, [_i64, _i64]),
     "skp_gesvj_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _i64, _vp,
                              _vp]),
@@ -77,7 +77,8 @@ SIGNATURES = {
                              _vp]),
     "skp_sym_check_f32": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "skp_sym_check_f64": (_int, [_vp, _i64, _i64, _vp, _vp]),
-    "skp_syrk_h3": (_int, [_i64, _i64, _f32, _vp, _vp, _i64, _vp, _vp, _i64, _vp]),
+    "skp_syrk_h3_ws_bytes": (_i64, [_i64, _i64]),
+    "skp_syrk_h3": (_int, [_i32, _i64, _i64, _f32, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp]),
     "skp_gemm_h3s_ws_bytes": (_i64, [_i64, _i64, _i64]),
     "skp_gemm_h3s": (_int, [_i64, _i64, _i64, _f32, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _f32, _vp,
                             _i64, _vp, _vp, _i64, _vp]),

@@ -388,10 +388,11 @@ def gemm_h3(a: SplitH2, b: SplitH2, ta: bool = False, alpha: float = 1.0, beta: 
 
 def gemm_h3_emit_t(a: SplitH2, b: SplitH2, ta: bool = False, shift: int | None = None,
                    e_fixed: int | None = None, out: SplitH2 | None = None, overflow=None,
-                   alpha: float = 1.0, b_lo: bool = True) -> SplitH2:
+                   alpha: float = 1.0, b_lo: bool = True, b_lower: bool = False) -> SplitH2:
     """K4h product written as the fp16 split of C^T (N x M planes): C =
     alpha op(a) b^T.  Exponent e_fixed, or ea + eb - shift (default shift =
-    15 + ceil(log2 K): no entry can overflow)."""
+    15 + ceil(log2 K): no entry can overflow).  b_lower: b (N x K) is lower
+    triangular (a Cholesky inverse), so each N tile stops at its K extent."""
     M, K = (a.cols, a.rows) if ta else (a.rows, a.cols)
     N, Kb = b.rows, b.cols
     if K != Kb:
@@ -406,20 +407,24 @@ def gemm_h3_emit_t(a: SplitH2, b: SplitH2, ta: bool = False, shift: int | None =
     call("skp_gemm_h3_emit_t", int(ta), M, N, K, alpha, ptr(a.hi), ptr(a.lo), a.ld, ptr(a.e),
          ptr(b.hi), ptr(b.lo) if b_lo else None, b.ld, ptr(b.e), ptr(out.hi), ptr(out.lo), out.ld,
          int(shift),
-         int(e_fixed is not None), int(e_fixed or 0), ptr(out.e), ptr(overflow),
+         int(e_fixed is not None), int(e_fixed or 0), ptr(out.e), ptr(overflow), int(b_lower),
          stream_ptr(a.hi.device))
     return out
 
 
-def syrk_h3(a: SplitH2, alpha: float = 1.0, out=None) -> torch.Tensor:
-    """K4h SYRK: alpha a^T a (a.cols x a.cols, exactly symmetric) from the
-    planes of a stored K x N (a.rows = K); both operands MN-major."""
-    K, N = a.rows, a.cols
+def syrk_h3(a: SplitH2, alpha: float = 1.0, out=None, rows: bool = False) -> torch.Tensor:
+    """K4h SYRK, exactly symmetric: alpha a^T a from the planes of a stored
+    K x N (a.rows = K; both operands MN-major), or with rows=True alpha a a^T
+    (the Gram of a's rows, a stored N x K, both operands K-major)."""
+    N, K = (a.rows, a.cols) if rows else (a.cols, a.rows)
     if out is None:
         out = empty2d(N, N, F32, a.hi.device)
     _, _, ldc = _rows_ld(out)
-    call("skp_syrk_h3", N, K, alpha, ptr(a.hi), ptr(a.lo), a.ld, ptr(a.e), ptr(out), ldc,
-         stream_ptr(a.hi.device))
+    lib = _lib.load()
+    wsb = int(lib.skp_syrk_h3_ws_bytes(N, K))
+    ws = workspace(a.hi.device, wsb) if wsb else None
+    call("skp_syrk_h3", int(rows), N, K, alpha, ptr(a.hi), ptr(a.lo), a.ld, ptr(a.e), ptr(out),
+         ldc, ptr(ws), wsb, stream_ptr(a.hi.device))
     return out
 
 
@@ -674,8 +679,9 @@ class CudaBackend:
             and omega.dtype == F32 and omega.dim() == 2
 
     def gram64_planes(self, yt: SplitH2):
-        """Y^T Y (fp64) from the split planes of Y^T: 3xFP16, promoted accumulation."""
-        return cast(gemm_h3(yt, yt), F64)
+        """Y^T Y (fp64) from the split planes of Y^T: the K-major SYRK (lower
+        tiles only, mirrored), 3xFP16 with promoted accumulation."""
+        return cast(syrk_h3(yt, rows=True), F64)
 
     def power_lazy_planes(self, comm, atil: SplitH2, omega, q: int, shift: float):
         """Stabilized power iteration (power.py:113-134) with every product on
@@ -694,7 +700,7 @@ class CudaBackend:
             x = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), 0.0, lazy=True,
                                 shift=shift)
             qt = gemm_h3_emit_t(yt, split_h2(self.to_compute(x)), ta=True, e_fixed=14, out=qt,
-                                overflow=self.fail[1:])
+                                overflow=self.fail[1:], b_lower=True)
             z = comm.allreduce_(gemm_h3(atil, qt, ta=True))
             yt = gemm_h3_emit_t(atil, split_h2(z, trans=True), out=yt)
         return yt
@@ -749,15 +755,15 @@ class CudaBackend:
         randsvd consumes).  yt is consumed (its buffers are reused)."""
         x1 = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), 0.0, lazy=True, shift=shift)
         q1t = gemm_h3_emit_t(yt, split_h2(self.to_compute(x1)), ta=True, e_fixed=14,
-                             overflow=self.fail[1:])
+                             overflow=self.fail[1:], b_lower=True)
         x2 = self.chol_inv64(comm.allreduce_(self.gram64_planes(q1t)), t2, lazy=True)
         # (Q2 goes into Y's planes: two plane buffers in flight, not three)
         q2t = gemm_h3_emit_t(q1t, split_h2(self.to_compute(x2)), ta=True, e_fixed=14, out=yt,
-                             overflow=self.fail[1:])
+                             overflow=self.fail[1:], b_lower=True)
         x3 = self.chol_inv64(comm.allreduce_(self.gram64_planes(q2t)), 0.0, lazy=True)
         if planes_out:
             return gemm_h3_emit_t(q2t, split_h2(self.to_compute(x3)), ta=True, e_fixed=14,
-                                  out=q1t, overflow=self.fail[1:])
+                                  out=q1t, overflow=self.fail[1:], b_lower=True)
         return gemm_h3(q2t, split_h2(self.to_compute(x3)), ta=True)
 
     def planes_to_compute(self, yt: SplitH2):

@@ -64,7 +64,9 @@ struct H3Params {
     int bn, tiles_m, tiles_n, splits, kb_per_split, num_kb;
     int a_kmajor;
     int b_kmajor;  // 0: B stored K x N (N contiguous; the SYRK's second operand)
-    int sym;       // 1: C = A^T A, only the units of the lower triangle (mirrored after)
+    int sym;       // > 0: C = A^T A, units = the lower-triangle tiles x splits (mirrored after)
+    int sym_tiles; // lower-triangle tiles (sym)
+    int tri_k;     // 1: B (stored N x K) is lower triangular: N tile tn needs K < (tn + 1) bn
     float alpha, beta;
     float* C;
     long long ldc;
@@ -200,20 +202,22 @@ __device__ __forceinline__ HWork h_unit(const H3Params& p, int u) {
     HWork w;
     if (p.sym) {
         // lower triangle only: M block tm needs the N tiles that start at or
-        // before its last row (the units are enumerated block row by row)
+        // before its last row (the tiles are enumerated block row by row);
+        // split-K slices of one tile are sym_tiles units apart
         constexpr int R = kPair ? 2 * HM : HM;
+        const int t = u % p.sym_tiles;
         int tm = 0, base = 0;
         for (;;) {
             const int c = min(p.tiles_n, ((tm + 1) * R + p.bn - 1) / p.bn);
-            if (u < base + c) break;
+            if (t < base + c) break;
             base += c;
             ++tm;
         }
         w.tm = tm;
-        w.tn = u - base;
-        w.ks = 0;
-        w.kb0 = 0;
-        w.kb1 = p.num_kb;
+        w.tn = t - base;
+        w.ks = u / p.sym_tiles;
+        w.kb0 = w.ks * p.kb_per_split;
+        w.kb1 = min(w.kb0 + p.kb_per_split, p.num_kb);
         return w;
     }
     w.tn = u % p.tiles_n;
@@ -222,6 +226,7 @@ __device__ __forceinline__ HWork h_unit(const H3Params& p, int u) {
     w.ks = r / p.tiles_m;
     w.kb0 = w.ks * p.kb_per_split;
     w.kb1 = min(w.kb0 + p.kb_per_split, p.num_kb);
+    if (p.tri_k) w.kb1 = min(w.kb1, ((w.tn + 1) * p.bn + HK - 1) / HK);
     return w;
 }
 
@@ -1132,6 +1137,7 @@ struct H3Emit {
     int shift, fixed, e_fixed;
     int32_t* e_out;
     int32_t* overflow;
+    int b_lower;  // B (stored N x K) is lower triangular: skip the K blocks past each N tile
 };
 
 int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ahi,
@@ -1168,6 +1174,8 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
     p.a_kmajor = ta ? 0 : 1;
     p.b_kmajor = 1;
     p.sym = 0;
+    p.sym_tiles = 0;
+    p.tri_k = 0;
     p.alpha = alpha; p.beta = beta; p.C = C; p.ldc = ldc;
     p.ws = pl.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
     p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
@@ -1182,6 +1190,7 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
     p.emit_e_fixed = emit ? emit->e_fixed : 0;
     p.emit_e = emit ? emit->e_out : nullptr;
     p.overflow = emit ? emit->overflow : nullptr;
+    p.tri_k = emit ? emit->b_lower : 0;
     // kind::f16 instruction descriptor: D f32, A/B f16, A major from the layout,
     // B K-major, N >> 3, M >> 4
     p.idesc = (1u << 4) | ((uint32_t)(!p.a_kmajor) << 15) | ((uint32_t)(p.bn >> 3) << 17) |
@@ -1235,11 +1244,59 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
     return SKP_OK;
 }
 
-// C = alpha A^T A (N x N, symmetric) with A pre-split, stored K x N (N
-// contiguous): both operands MN-major from the same planes.  Only the unit
-// tiles meeting the lower triangle run (M blocks of 256 rows x N tiles of 128
-// columns: ~half of the full product's MMAs); the strict upper triangle is
-// then mirrored from the lower one, so C comes out exactly symmetric.
+// split-K slices for the SYRK: enough units for every CTA pair, and at
+// least 64 K blocks (4 promotion chunks) per slice
+int syrk_splits(int64_t tiles, int64_t K, int slots) {
+    const int64_t nkb = cdiv(K, HK);
+    int64_t s = 1;
+    while (tiles * s < slots && nkb / (s + 1) >= 64 && s < 16) ++s;
+    return (int)s;
+}
+
+struct SyrkPlan {
+    HPlan pl;
+    int bn, bcols, R, tiles, splits;
+    bool pair;
+};
+SyrkPlan syrk_plan(int64_t N, int64_t K) {
+    SyrkPlan sp;
+    sp.pair = h_pair(N);
+    HPlan& pl = sp.pl;
+    pl = h_plan(N, N, K, 0, sp.pair);
+    // square tiles: 256 x 256 per CTA pair (each CTA 128 rows of A and 128
+    // columns of B; 6 column groups per epilogue thread), 128 x 128 on one CTA
+    sp.bn = sp.pair ? 256 : 128;
+    sp.bcols = sp.pair ? sp.bn / 2 : sp.bn;
+    sp.R = sp.pair ? 2 * HM : HM;
+    pl.bn = sp.bn;
+    pl.tiles_n = (int)cdiv(N, sp.bn);
+    pl.b_bytes = (uint32_t)sp.bcols * HK * 2;
+    pl.stage_bytes = 2 * pl.a_bytes + 2 * pl.b_bytes;
+    pl.acc_stride = sp.bn;
+    pl.stages = std::max(2, std::min(kHMaxStages, (int)((227 * 1024 - 1024 - 256) / pl.stage_bytes)));
+    pl.smem = 1024 + (size_t)pl.stages * pl.stage_bytes + (2 * pl.stages + 4) * 8 + 16;
+    sp.tiles = 0;
+    for (int tm = 0; tm < pl.tiles_m; ++tm)
+        sp.tiles += (int)std::min<int64_t>(pl.tiles_n, cdiv((int64_t)(tm + 1) * sp.R, sp.bn));
+    sp.splits = syrk_splits(sp.tiles, K, sp.pair ? h_sms / 2 : h_sms);
+    pl.kb_per_split = (int)cdiv(pl.num_kb, sp.splits);
+    sp.splits = (int)cdiv(pl.num_kb, pl.kb_per_split);
+    return sp;
+}
+
+int64_t syrk_h3_ws_bytes(int64_t N, int64_t K) {
+    if (!h_init() || N == 0 || K == 0) return 0;
+    const SyrkPlan sp = syrk_plan(N, K);
+    return sp.splits > 1 ? (int64_t)sp.splits * N * N * 4 : 0;
+}
+
+// C = alpha A^T A (N x N, symmetric) with A pre-split: stored K x N (N
+// contiguous, kmajor = 0: both operands MN-major from the same planes) or
+// N x K (kmajor = 1: both K-major, the Gram of the rows of a transposed
+// block).  Only the tiles meeting the lower triangle run (~half of the full
+// product's MMAs), split over K when there are fewer tiles than CTA pairs;
+// the strict upper triangle is then mirrored from the lower one, so C comes
+// out exactly symmetric.
 __global__ void sym_mirror_kernel(float* __restrict__ C, int64_t N, int64_t ldc) {
     __shared__ float t[32][33];
     const int64_t bi = blockIdx.y, bj = blockIdx.x;  // source tile (bi, bj), bi >= bj
@@ -1256,8 +1313,9 @@ __global__ void sym_mirror_kernel(float* __restrict__ C, int64_t N, int64_t ldc)
     }
 }
 
-int syrk_h3(int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo, int64_t lda,
-            const int32_t* a_e, float* C, int64_t ldc, cudaStream_t st) {
+int syrk_h3(int kmajor, int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo,
+            int64_t lda, const int32_t* a_e, float* C, int64_t ldc, void* ws, int64_t ws_bytes,
+            cudaStream_t st) {
     if (!h_init()) {
         set_error("unsupported: the 3xFP16 tcgen05 GEMM needs an sm_100 device");
         return SKP_ERR_UNSUPPORTED;
@@ -1268,56 +1326,60 @@ int syrk_h3(int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo,
         return SKP_ERR_UNSUPPORTED;
     }
     const uintptr_t al = reinterpret_cast<uintptr_t>(Ahi) | reinterpret_cast<uintptr_t>(Alo);
-    if ((al & 15) || (lda & 63)) {
-        set_error("unsupported: syrk_h3 needs 16-byte aligned planes with lda %% 64 == 0 (lda=%lld)",
-                  (long long)lda);
+    if ((al & 15) || (kmajor ? (lda & 7) : (lda & 63))) {
+        set_error("unsupported: syrk_h3 needs 16-byte aligned planes with lda %% %d == 0 (lda=%lld)",
+                  kmajor ? 8 : 64, (long long)lda);
         return SKP_ERR_UNSUPPORTED;
     }
-    const bool pair = h_pair(N);
-    HPlan pl = h_plan(N, N, K, 0, pair);
-    // square tiles: 256 x 256 per CTA pair (each CTA 128 rows of A and 128
-    // columns of B = two 64-column MN-major swizzle atoms; 6 column groups per
-    // epilogue thread), 128 x 128 on one CTA
-    const int bn = pair ? 256 : 128;
-    pl.bn = bn;
-    pl.tiles_n = (int)cdiv(N, bn);
-    const int bcols = pair ? bn / 2 : bn;
-    pl.b_bytes = (uint32_t)bcols * HK * 2;
-    pl.stage_bytes = 2 * pl.a_bytes + 2 * pl.b_bytes;
-    pl.acc_stride = bn;
-    pl.stages = std::max(2, std::min(kHMaxStages, (int)((227 * 1024 - 1024 - 256) / pl.stage_bytes)));
-    pl.smem = 1024 + (size_t)pl.stages * pl.stage_bytes + (2 * pl.stages + 4) * 8 + 16;
-    const int R = pair ? 2 * HM : HM;
-    int units = 0;
-    for (int tm = 0; tm < pl.tiles_m; ++tm)
-        units += (int)std::min<int64_t>(pl.tiles_n, cdiv((int64_t)(tm + 1) * R, bn));
+    const SyrkPlan sp = syrk_plan(N, K);
+    const HPlan& pl = sp.pl;
+    const bool pair = sp.pair;
+    const int splits = sp.splits;
+    if (splits > 1 && (!ws || ws_bytes < (int64_t)splits * N * N * 4)) {
+        set_error("syrk_h3 needs %lld bytes of workspace", (long long)splits * N * N * 4);
+        return SKP_ERR_ARG;
+    }
     H3Params p = {};
     p.b_lo = 1;
     p.M = (int)N; p.N = (int)N; p.K = (int)K;
-    p.bn = pl.bn; p.tiles_m = pl.tiles_m; p.tiles_n = pl.tiles_n; p.splits = 1;
-    p.kb_per_split = pl.num_kb; p.num_kb = pl.num_kb;
-    p.a_kmajor = 0;
-    p.b_kmajor = 0;
-    p.sym = units;
+    p.bn = pl.bn; p.tiles_m = pl.tiles_m; p.tiles_n = pl.tiles_n; p.splits = splits;
+    p.kb_per_split = pl.kb_per_split; p.num_kb = pl.num_kb;
+    p.a_kmajor = kmajor ? 1 : 0;
+    p.b_kmajor = kmajor ? 1 : 0;
+    p.sym_tiles = sp.tiles;
+    p.sym = sp.tiles * splits;
+    p.tri_k = 0;
     p.alpha = alpha; p.beta = 0.f; p.C = C; p.ldc = ldc;
-    p.ws = nullptr;
+    p.ws = splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
     p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
     p.stage_bytes = pl.stage_bytes; p.acc_stride = pl.acc_stride;
     p.a_e = a_e; p.b_e = a_e;
-    p.chunk_kb = h_chunk_kb();
+    // the Gram of rows (kmajor) decides the final basis' orthonormality and
+    // feeds the error identity: 256-deep promotion chains there (its tiles
+    // are few and short, so the extra epilogue drains are hidden)
+    p.chunk_kb = kmajor ? 4 : h_chunk_kb();
     p.emit_hi = nullptr; p.emit_lo = nullptr; p.emit_e = nullptr; p.overflow = nullptr;
-    // kind::f16: D f32, A and B f16, both MN-major (bits 15, 16)
-    p.idesc = (1u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(p.bn >> 3) << 17) |
-              ((uint32_t)(R >> 4) << 24);
+    // kind::f16: D f32, A and B f16, both MN-major (bits 15, 16) or both K-major
+    const uint32_t mn = kmajor ? 0u : 1u;
+    p.idesc = (1u << 4) | (mn << 15) | (mn << 16) | ((uint32_t)(p.bn >> 3) << 17) |
+              ((uint32_t)(sp.R >> 4) << 24);
     CUtensorMap mah, mal, mbh, mbl;
-    const bool ok = h_encode_mn(&mah, Ahi, (uint64_t)N, (uint64_t)K, lda) &&
-                    h_encode_mn(&mal, Alo, (uint64_t)N, (uint64_t)K, lda) &&
-                    h_encode_mn(&mbh, Ahi, (uint64_t)N, (uint64_t)K, lda, (uint32_t)bcols) &&
-                    h_encode_mn(&mbl, Alo, (uint64_t)N, (uint64_t)K, lda, (uint32_t)bcols);
+    bool ok;
+    if (kmajor)
+        ok = h_encode_k(&mah, Ahi, (uint64_t)K, (uint64_t)N, lda, HM) &&
+             h_encode_k(&mal, Alo, (uint64_t)K, (uint64_t)N, lda, HM) &&
+             h_encode_k(&mbh, Ahi, (uint64_t)K, (uint64_t)N, lda, (uint32_t)sp.bcols) &&
+             h_encode_k(&mbl, Alo, (uint64_t)K, (uint64_t)N, lda, (uint32_t)sp.bcols);
+    else
+        ok = h_encode_mn(&mah, Ahi, (uint64_t)N, (uint64_t)K, lda) &&
+             h_encode_mn(&mal, Alo, (uint64_t)N, (uint64_t)K, lda) &&
+             h_encode_mn(&mbh, Ahi, (uint64_t)N, (uint64_t)K, lda, (uint32_t)sp.bcols) &&
+             h_encode_mn(&mbl, Alo, (uint64_t)N, (uint64_t)K, lda, (uint32_t)sp.bcols);
     if (!ok) {
         set_error("cuTensorMapEncodeTiled failed (syrk_h3)");
         return SKP_ERR_UNSUPPORTED;
     }
+    const int units = p.sym;
     if (pair) {
         SKP_CUDA(cudaFuncSetAttribute(gemm_h3_kernel<true, 6>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
@@ -1341,6 +1403,11 @@ int syrk_h3(int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo,
         gemm_h3_kernel<false><<<std::min(units, h_sms), kHThreads, pl.smem, st>>>(mah, mal, mbh, mbl,
                                                                                  p);
         SKP_LAUNCHED(gemm_h3_kernel);
+    }
+    if (splits > 1) {
+        const int64_t blocks = std::min<int64_t>(cdiv(N * N, 256), (int64_t)h_sms * 8);
+        h3_splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(p.ws, splits, N, N, alpha, 0.f, C, ldc);
+        SKP_LAUNCHED(h3_splitk_reduce);
     }
     const unsigned nt = (unsigned)cdiv(N, 32);
     sym_mirror_kernel<<<dim3(nt, nt), dim3(32, 8), 0, st>>>(C, N, ldc);
@@ -1552,11 +1619,16 @@ extern "C" int skp_split_h2_f32(const float* X, int64_t rows, int64_t cols, int6
     return split_h2(X, rows, cols, ld, trans, hi, lo, ldh, e, have_amax != 0, SKP_STREAM(stream));
 }
 
-extern "C" int skp_syrk_h3(int64_t N, int64_t K, float alpha, const void* A_hi, const void* A_lo,
-                           int64_t lda, const int32_t* a_exp, float* C, int64_t ldc, void* stream) {
-    SKP_ARG(N >= 0 && K >= 0 && lda >= N && ldc >= N && a_exp && (N == 0 || (A_hi && A_lo && C)),
+extern "C" int64_t skp_syrk_h3_ws_bytes(int64_t N, int64_t K) { return skp::syrk_h3_ws_bytes(N, K); }
+
+extern "C" int skp_syrk_h3(int32_t kmajor, int64_t N, int64_t K, float alpha, const void* A_hi,
+                           const void* A_lo, int64_t lda, const int32_t* a_exp, float* C,
+                           int64_t ldc, void* ws, int64_t ws_bytes, void* stream) {
+    SKP_ARG(N >= 0 && K >= 0 && lda >= (kmajor ? K : N) && ldc >= N && a_exp &&
+                (N == 0 || (A_hi && A_lo && C)),
             "syrk_h3: bad arguments");
-    return skp::syrk_h3(N, K, alpha, A_hi, A_lo, lda, a_exp, C, ldc, SKP_STREAM(stream));
+    return skp::syrk_h3(kmajor, N, K, alpha, A_hi, A_lo, lda, a_exp, C, ldc, ws, ws_bytes,
+                        SKP_STREAM(stream));
 }
 
 extern "C" int64_t skp_gemm_h3s_ws_bytes(int64_t M, int64_t N, int64_t K) {
@@ -1592,7 +1664,8 @@ extern "C" int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, f
                                   const int32_t* a_exp, const void* B_hi, const void* B_lo,
                                   int64_t ldb, const int32_t* b_exp, void* Ct_hi, void* Ct_lo,
                                   int64_t ldct, int32_t shift, int32_t fixed, int32_t e_fixed,
-                                  int32_t* e_out, int32_t* overflow, void* stream) {
+                                  int32_t* e_out, int32_t* overflow, int32_t b_lower,
+                                  void* stream) {
     SKP_ARG(M >= 0 && N >= 0 && K >= 0, "gemm_h3_emit_t: negative size");
     SKP_ARG(transA == 0 || transA == 1, "gemm_h3_emit_t: transA must be 0/1");
     SKP_ARG(lda >= (transA ? M : K) && lda >= 1, "gemm_h3_emit_t: lda too small");
@@ -1600,7 +1673,7 @@ extern "C" int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, f
     SKP_ARG(ldct >= M, "gemm_h3_emit_t: ldct too small");
     SKP_ARG(Ct_hi && Ct_lo && e_out && A_hi && A_lo && B_hi && a_exp && b_exp,
             "gemm_h3_emit_t: null pointer");
-    H3Emit em{Ct_hi, Ct_lo, ldct, shift, fixed, e_fixed, e_out, overflow};
+    H3Emit em{Ct_hi, Ct_lo, ldct, shift, fixed, e_fixed, e_out, overflow, b_lower ? 1 : 0};
     return gemm_h3_impl(transA, M, N, K, alpha, A_hi, A_lo, lda, a_exp, B_hi, B_lo, ldb, b_exp,
                         0.f, nullptr, 0, nullptr, 0, &em, SKP_STREAM(stream));
 }

@@ -450,6 +450,39 @@ def test_syrk_h3_vs_torch(ops, N, K):
     assert bool(((out.double() - ref).abs() <= bound + 1e-6).all())
 
 
+@pytest.mark.parametrize("N,K", [(45, 1000), (130, 5000), (520, 262144), (1050, 65536)])
+def test_syrk_h3_rows_vs_torch(ops, N, K):
+    """The K-major SYRK (Y^T Y from the planes of Y^T: the CholeskyQR Grams),
+    with split-K when the lower-triangle tiles are fewer than the CTA pairs."""
+    g = torch.Generator(device="cuda").manual_seed(N * 3 + K)
+    y = torch.randn(K, N, generator=g, device="cuda") + 0.2
+    out = ops.syrk_h3(ops.split_h2(y, trans=True), rows=True)
+    ref = y.double().T @ y.double()
+    assert torch.equal(out, out.T)
+    ab = y.double().abs()
+    bound = 2e-5 * (ab.T @ ab) + 2e-6 * ab.max().item() ** 2 * np.sqrt(K)
+    assert bool(((out.double() - ref).abs() <= bound + 1e-6).all())
+
+
+@pytest.mark.parametrize("M,N,K", [(3000, 520, 520), (70000, 1050, 1050), (300, 130, 130)])
+def test_gemm_h3_emit_lower_triangular_b(ops, M, N, K):
+    """Q^T = (Y X^T)^T with X lower triangular (b_lower): the N tiles stop at
+    their K extent; same result as the dense product."""
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    y = torch.randn(M, K, generator=g, device="cuda")
+    x = torch.tril(torch.randn(N, K, generator=g, device="cuda"))
+    yt = ops.split_h2(y, trans=True)
+    xs = ops.split_h2(x)
+    dense = ops.gemm_h3_emit_t(yt, xs, ta=True)
+    tri = ops.gemm_h3_emit_t(yt, xs, ta=True, b_lower=True)
+    def val(p):
+        return ((p.hi.float() + p.lo.float())[:, :p.cols] * 2.0 ** -int(p.e[0].item())).double()
+    ref = (y.double() @ x.double().T).T
+    scale = (y.abs().max() * x.abs().max()).item() * np.sqrt(K)
+    assert (val(tri) - ref).abs().max().item() <= 4e-6 * scale
+    assert torch.equal(val(tri), val(dense))
+
+
 def test_syrk_h3_inplace_planes_long_k(ops):
     """The power iteration's operand: A~ split in place (planes with leading
     dimension 2 ld) and K = 262144 rows (register-promoted accumulation:

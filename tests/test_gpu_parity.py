@@ -234,10 +234,11 @@ def test_sketch_space_power_matches_products(skp, monkeypatch, name, m, n, l, r2
         assert r["sigma"] <= SIG_TOL[np.float32], (tag, r)
         assert abs(r["exact"] - eo) <= ERR_TOL * eo, (tag, r, eo)
         # the fused error is the identity sqrt(1 - (|A|^2 - |A - QQ^T A|^2)/|A|^2)
-        # from 3xFP16 products of fp32 data: its absolute error on rel^2 is
-        # ~1e-6, i.e. 1e-6 / (2 rel) on rel (outside 1e-3 relative below rel ~
-        # 0.03; the exact residual above is the parity metric there)
-        assert abs(r["fused"] - eo) <= ERR_TOL * eo + 1e-6 / (2 * eo), (tag, r, eo)
+        # from 3xFP16 products of fp32 data: its absolute error on rel^2 is a
+        # few 1e-6 (the fp32 accumulation of the Gram Q^T Q and of B), i.e.
+        # ~3e-6 / rel on rel (outside 1e-3 relative below rel ~ 0.05; the exact
+        # residual above is the parity metric there)
+        assert abs(r["fused"] - eo) <= ERR_TOL * eo + 5e-6 / (2 * eo), (tag, r, eo)
 
 
 def _fp64_restatement(a32: torch.Tensor, spec, cols, signs, omega):
