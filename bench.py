@@ -310,65 +310,95 @@ def run_ours(args, cfg, rank, world, local_rank):
     esz = a.element_size()
     sketch_bytes = rows * n * esz + rows * l * esz + n * s_ * 5 + (l + 1) * 4
     sketch_gbs = sketch_bytes / (sketch_ms * 1e-3) / 1e9
-    # power-iteration GEMM: Y = A~ Z  (rows x l) . (l x r2), operands laid out
-    # as in the pipeline (128-byte padded rows)
+    # ---- the tensor-core kernels of the step, each timed live as the step runs
+    # it (operands laid out as in the pipeline: 128-byte padded rows)
+    be = _ops.CudaBackend(device, a.dtype)
+    pa = be.prepare(atil, inplace=True)                 # A~ planes (A~ is not reused)
+    h3 = isinstance(pa, _ops.SplitH2)
     z = _ops.empty2d(l, r2, a.dtype, device)
     z.normal_()
-    y = _ops.empty2d(rows, r2, a.dtype, device)
-    # the kernel the power iteration runs: 3xFP16 on the pre-split A~ where
-    # the backend prepares it (fp32, tcgen05), else 3xTF32 / SIMT
-    pa = _ops.CudaBackend(device, a.dtype).prepare(atil, inplace=True)  # (A~ is not reused)
-    h3 = isinstance(pa, _ops.SplitH2)
+    omega_like = _ops.empty2d(l, r2, a.dtype, device)
+    omega_like.normal_()
+    gram_path = h3 and be.gram_ok(pa, omega_like, cfg["q"])
+    del omega_like
+    tc = bool(_lib.load().skp_has_tcgen05())
+    f32 = cfg["dtype"] == "f32"
+    kern = {}
     if h3:
         sz = _ops.split_h2(z, trans=True)
-        run_gemm = lambda: _ops.gemm_h3(pa, sz, out=y)
+        y = _ops.empty2d(rows, r2, a.dtype, device)
+        pg_ms = _time_launches(lambda: _ops.gemm_h3(pa, sz, out=y))
+        del y
     else:
-        run_gemm = lambda: _ops.gemm(atil, z, out=y)
-    gemm_ms = _time_launches(run_gemm)
-    del pa, atil, y, z, run_gemm
-    gemm_flop = 2.0 * rows * l * r2
-    gemm_tflops = gemm_flop / (gemm_ms * 1e-3) / 1e12
-    power_f, orth_f, qta_f = flops_of(cfg)
-    tc = bool(_lib.load().skp_has_tcgen05())
-    # tensor-pipe view: 3 MMAs per useful MAC -- kind::f16 (3xFP16) at the
-    # measured dense bf16/fp16 rate, or kind::tf32 (3xTF32) at bf16 / 2
-    pipe_tflops = gemm_tflops * 3 if (tc and cfg["dtype"] == "f32") else gemm_tflops
-    pipe_peak = bf16 if h3 else bf16 / 2.0
-    power_tflops = (power_f / world) / (phases.get("power", float("nan")) * 1e-3) / 1e12
-    gkey = "gemm_h3_nn" if h3 else "gemm_tc_nn"
-    skey = "sketch_gather" if v2 else "sketch_rows"
-    g_tr, g_src = _traffic(args.config, gkey)
-    s_tr, s_src = _traffic(args.config, skey)
-    roof = {"kernel": "gemm_nn A~.Z (power iteration)" + (
-                " tcgen05 3xFP16 (pre-split A~)" if h3 else " tcgen05 3xTF32" if tc else " SIMT"),
-            # achieved = ALGORITHMIC flop (2 m l r2) per launch / launch time,
-            # peak = the measured dense bf16 figure as is; the fp32-accurate
-            # product costs 3 f16 MMAs (3xTF32: 3 at half rate) per MAC, so
-            # the tensor pipe itself runs at "pipe_frac" of that peak
-            "bound": "tensor", "achieved": round(gemm_tflops, 2), "peak": round(bf16, 1),
-            "unit": "TFLOP/s", "frac": round(gemm_tflops / bf16, 4),
-            "emulation": {"mma_per_mac": 3 if (tc and cfg["dtype"] == "f32") else 1,
-                          "pipe_tflops": round(pipe_tflops, 2),
+        y = _ops.empty2d(rows, r2, a.dtype, device)
+        pg_ms = _time_launches(lambda: _ops.gemm(atil, z, out=y))
+        del y
+    kern["power_gemm"] = dict(
+        kernel="gemm_h3 Y = A~ W (tcgen05 3xFP16, pre-split A~)" if h3 else "gemm Y = A~ Z",
+        ms=pg_ms, flop=2.0 * rows * l * r2, launches=1 if gram_path else 1 + 2 * cfg["q"],
+        key="gemm_h3_nn")
+    if gram_path:
+        g_ms = _time_launches(lambda: _ops.syrk_h3(pa), reps=3)
+        kern["syrk"] = dict(kernel="syrk_h3 G = A~^T A~ (tcgen05 3xFP16, lower-triangle 256x256 "
+                                   "tiles, both operands MN-major)",
+                            ms=g_ms, flop=1.0 * rows * l * (l + 1), launches=1, key="syrk")
+    del pa, z, atil
+    torch.cuda.empty_cache()
+    # randsvd's B^T = A^T Q with the in-kernel split of A (Q as fp16 planes of Q^T)
+    if h3 and tc and f32:
+        qp = _ops.empty2d(rows, r2, a.dtype, device)
+        qp.normal_()
+        qp /= float(np.sqrt(rows))
+        sq = _ops.split_h2(qp, trans=True)
+        del qp
+        e_a = _ops.h2_exponent(a)
+        q_ms = _time_launches(lambda: _ops.gemm_h3s_t(a, e_a, sq), reps=2)
+        del sq
+        kern["qta"] = dict(kernel="gemm_h3s B^T = A^T Q (tcgen05 3xFP16, A split in the kernel)",
+                           ms=q_ms, flop=2.0 * rows * n * r2, launches=1, key="gemm_h3s_qta")
+        torch.cuda.empty_cache()
+    pipe_peak = bf16 if (h3 or not f32) else bf16 / 2.0
+    mma_per_mac = 3 if (tc and f32) else 1
+    kernels = {}
+    for name, kd in kern.items():
+        tflops = kd["flop"] / (kd["ms"] * 1e-3) / 1e12
+        tr, src = _traffic(args.config, kd["key"])
+        kernels[name] = {
+            "kernel": kd["kernel"], "bound": "tensor", "ms_per_launch": round(kd["ms"], 4),
+            "launches_per_step": kd["launches"],
+            "share_of_step": round(kd["ms"] * kd["launches"] / ms, 3),
+            "algorithmic_flop_per_launch": kd["flop"], "achieved": round(tflops, 2),
+            "peak": round(bf16, 1), "unit": "TFLOP/s", "frac": round(tflops / bf16, 4),
+            "emulation": {"mma_per_mac": mma_per_mac,
+                          "pipe_tflops": round(tflops * mma_per_mac, 2),
                           "pipe_peak": round(pipe_peak, 1),
-                          "pipe_frac": round(pipe_tflops / pipe_peak, 4),
-                          "pipe_peak_sustained": round(bf16_sus if h3 else bf16_sus / 2, 1),
-                          "pipe_frac_sustained": round(pipe_tflops / (bf16_sus if h3 else bf16_sus / 2), 4)},
-            "traffic": g_tr, "traffic_unit": "DRAM bytes per launch (ncu --set full)",
-            "traffic_source": g_src, "ms_per_launch": round(gemm_ms, 4),
-            "peak_note": (f"{peak_src} dense bf16 {bf16} TFLOP/s (burst; sustained "
-                          f"{bf16_sus}); pipe peak = the same for kind::f16 (3xFP16)" if h3 else
-                          f"{peak_src} dense bf16 {bf16} TFLOP/s; pipe peak = bf16/2 for kind::tf32"),
-            "algorithmic_flop_per_launch": gemm_flop,
-            "share_of_step": round(gemm_ms * (1 + 2 * cfg["q"]) / ms, 3)}
+                          "pipe_frac": round(tflops * mma_per_mac / pipe_peak, 4),
+                          "pipe_peak_sustained": round(bf16_sus if pipe_peak == bf16 else bf16_sus / 2, 1),
+                          "pipe_frac_sustained": round(
+                              tflops * mma_per_mac / (bf16_sus if pipe_peak == bf16 else bf16_sus / 2), 4)},
+            "traffic": tr, "traffic_unit": "DRAM bytes per launch (ncu --set full)",
+            "traffic_source": src}
+    skey = "sketch_gather" if v2 else "sketch_rows"
+    s_tr, s_src = _traffic(args.config, skey)
+    kernels["sketch"] = {
+        "kernel": "sketch_gather (K2 v2)" if v2 else "sketch_right (K2 v1)", "bound": "hbm",
+        "ms_per_launch": round(sketch_ms, 4), "launches_per_step": 1,
+        "share_of_step": round(sketch_ms / ms, 3), "algorithmic_bytes_per_launch": sketch_bytes,
+        "achieved": round(sketch_gbs, 1), "peak": hbm, "unit": "GB/s",
+        "frac": round(sketch_gbs / hbm, 4), "traffic": s_tr,
+        "traffic_unit": "DRAM bytes per launch (ncu --set full)", "traffic_source": s_src}
+    dom = max(kernels, key=lambda k: kernels[k]["share_of_step"])
+    roof = dict(kernels[dom], name=dom,
+                peak_note=f"{peak_src}: HBM {hbm} GB/s; dense bf16 {bf16} TFLOP/s burst, "
+                          f"{bf16_sus} sustained (3xFP16 runs kind::f16 at that rate, 3 MMAs "
+                          "per useful MAC: 'emulation')")
+    power_f, orth_f, qta_f = flops_of(cfg)
+    power_tflops = (power_f / world) / (phases.get("power", float("nan")) * 1e-3) / 1e12
     extra = {
-        "sketch": {"kernel": "sketch_gather (K2 v2)" if v2 else "sketch_right (K2 v1)",
-                   "bound": "hbm", "ms": round(sketch_ms, 4), "GB/s": round(sketch_gbs, 1),
-                   "peak": hbm, "frac_hbm": round(sketch_gbs / hbm, 4), "bytes": sketch_bytes,
-                   "traffic": s_tr, "traffic_source": s_src,
-                   "share_of_step": round(sketch_ms / ms, 3)},
-        "power_gemm": {"ms": round(gemm_ms, 4), "useful_TFLOP/s": round(gemm_tflops, 2),
-                       "pipe_frac": round(pipe_tflops / pipe_peak, 4)},
-        "power_phase_TFLOP/s": round(power_tflops, 2),
+        "kernels": kernels,
+        "power_path": "sketch space (one SYRK of A~, q l-dimensional steps, one A~ W)"
+                      if gram_path else "products (1 + 2q products with A~)",
+        "power_phase_TFLOP/s_equivalent": round(power_tflops, 2),
     }
     # slab of the workload for the CPU baseline / oracle parity (rank 0)
     slab = a[:min(args.cpu_rows, rows)].cpu().numpy() if rank == 0 else None
@@ -389,12 +419,14 @@ def run_ours(args, cfg, rank, world, local_rank):
         "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-        "dtype": cfg["dtype"] + ("(power: 3xFP16, other GEMMs: 3xTF32, tcgen05)" if h3 else
-                                 "(3xTF32 tcgen05)" if tc and cfg["dtype"] == "f32" else ""),
+        "dtype": cfg["dtype"] + (" (products 3xFP16 on tcgen05 kind::f16, fp64 small cores)" if h3
+                                 else " (3xTF32 tcgen05)" if tc and f32 else ""),
         "data": "synthetic (seeded, BASELINE config recipe; random-init factors, no dataset)",
         "config": {"workload": args.config, "m": m, "n": n, "l": l, "s": s_,
                    "k": cfg["k"], "r2": r2, "q": cfg["q"],
-                   "parallelism": f"rows sharded x{world} (NCCL allreduce of l x r2 / r2 x r2 / r2 x n)",
+                   "parallelism": f"rows sharded x{world} (NCCL allreduce of " + (
+                       "the l x l G once" if gram_path else "l x r2 per power step") +
+                       ", r2 x r2 Grams, r2 x n B^T)",
                    "l2": "no flush: A is far larger than the 126 MB L2"},
         "phases_ms": {k: round(v, 3) for k, v in phases.items()},
         "rel_err": rel, "sigma_1": float(sig[0].item()),
