@@ -67,6 +67,8 @@ struct H3Params {
     int sym;       // > 0: C = A^T A, units = the lower-triangle tiles x splits (mirrored after)
     int sym_tiles; // lower-triangle tiles (sym)
     int tri_k;     // 1: B (stored N x K) is lower triangular: N tile tn needs K < (tn + 1) bn
+    unsigned* prog;  // pacing slots (one per CTA; see h_pace), or null
+    int pace;        // > 0: a producer stays within pace K blocks of the slowest CTA of its wave
     float alpha, beta;
     float* C;
     long long ldc;
@@ -195,6 +197,48 @@ __device__ __forceinline__ void acc_add16(float* acc, const float* v) {
 struct HWork {
     int tm, tn, ks, kb0, kb1;
 };
+
+// Wave pacing for the long-K products (SYRK G = A~^T A~, B^T = A^T Q): the
+// CTAs working on the same wave of units read the same K slice of the shared
+// operand (A~ / A) at the same time only while they stay in step -- left
+// alone they drift apart by more than the 126 MB L2 holds, and ncu measured
+// A read 8x (K4s at C5: 1.06 TB for a 128 GB A).  Each TMA producer publishes
+// (wave << 20 | k block) in its slot and, every 4 K blocks, waits while it is
+// more than `pace` K blocks ahead of the slowest CTA of its own wave (other
+// waves are ignored, so the slowest CTA never waits: no deadlock).
+__device__ __forceinline__ unsigned h_ld_slot(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void h_st_slot(unsigned* p, unsigned v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void h_pace(unsigned* prog, int pace, unsigned wave, int kb_rel,
+                                       int& lo_cache) {
+    const int lane = threadIdx.x & 31;
+    const unsigned me = (wave << 20) | (unsigned)kb_rel;
+    if (lane == 0) h_st_slot(prog + blockIdx.x, me);
+    if (kb_rel == 0) lo_cache = 0;
+    // the slots are read only when this CTA may be getting ahead: the ring
+    // must not drain while the producer polls
+    if (kb_rel - lo_cache <= pace / 2) return;
+    for (int it = 0;; ++it) {
+        int lo = kb_rel;
+        for (int i = lane; i < (int)gridDim.x; i += 32) {
+            const unsigned v = h_ld_slot(prog + i);
+            if ((v >> 20) == wave) lo = min(lo, (int)(v & 0xFFFFFu));
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        lo_cache = lo;
+        if (kb_rel - lo <= pace || it > (1 << 22)) return;
+        __nanosleep(200);
+    }
+}
+__device__ __forceinline__ void h_pace_done(unsigned* prog) {
+    if ((threadIdx.x & 31) == 0) h_st_slot(prog + blockIdx.x, 0xFFFFFFFFu);
+}
 template <bool kPair>
 __device__ __forceinline__ HWork h_unit(const H3Params& p, int u) {
     // N-tiles of one M block are adjacent units: co-resident CTAs share the A
@@ -290,12 +334,16 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
     if (warp == kHWarpTma) {
         Ring r;
         const int bcols = kPair ? p.bn / 2 : p.bn;
-        for (int u = ustart; u < units; u += ustride) {
+        unsigned wave = 0;
+        int lo_cache = 0;
+        for (int u = ustart; u < units; u += ustride, ++wave) {
             const HWork w = h_unit<kPair>(p, u);
             const int m0 = w.tm * kRowsPerUnit + (int)rank * HM;
             const int n0 = w.tn * p.bn + (int)rank * bcols;
             for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
                 const int s = r.s;
+                if (p.pace && ((kb - w.kb0) & 3) == 0)
+                    h_pace(p.prog, p.pace, wave, kb - w.kb0, lo_cache);
                 mbar_wait(&empty[s], r.ph ^ 1);
                 if (leader) mbar_expect_tx_e(&full[s], (kPair ? 2u : 1u) * p.stage_bytes);
                 const uint32_t bar = full_cl0 + 8u * (uint32_t)s;
@@ -320,6 +368,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant
                 }
             }
         }
+        if (p.pace) h_pace_done(p.prog);
     } else if (warp == kHWarpMma && leader) {
         // descriptors of stage 0, K-step 0; per-stage / per-K-step / plane
         // offsets in 16-byte units (start-address field never carries: < 228 KB)
@@ -681,6 +730,8 @@ struct H3SParams {
     const int* b_e;
     int* overflow;
     int chunk_kb;
+    unsigned* prog;  // pacing slots (see h_pace), or null
+    int pace;
 };
 
 __device__ __forceinline__ HWork hs_unit(const H3SParams& p, int u) {
@@ -795,12 +846,16 @@ gemm_h3s_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     if (warp == kSWarpTma) {
         Ring r;
         const int bcols = kPair ? p.bn / 2 : p.bn;
-        for (int u = ustart; u < units; u += ustride) {
+        unsigned wave = 0;
+        int lo_cache = 0;
+        for (int u = ustart; u < units; u += ustride, ++wave) {
             const HWork w = hs_unit(p, u);
             const int m0 = w.tm * kRowsPerUnit + (int)rank * HM;
             const int n0 = w.tn * p.bn + (int)rank * bcols;
             for (int kb = w.kb0; kb < w.kb1; ++kb, r.next(S)) {
                 const int s = r.s;
+                if (p.pace && ((kb - w.kb0) & 3) == 0)
+                    h_pace(p.prog, p.pace, wave, kb - w.kb0, lo_cache);
                 mbar_wait(&empty[s], r.ph ^ 1);
                 mbar_expect_tx_e(&full[s], p.stage_bytes);
                 const uint32_t st = smem0 + (uint32_t)s * p.stage_bytes;
@@ -811,6 +866,7 @@ gemm_h3s_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 h_tma_2d<false>(&map_bl, bar, st + p.a_bytes + p.b_bytes, k0, n0);
             }
         }
+        if (p.pace) h_pace_done(p.prog);
     } else if (warp == kSWarpMma && leader) {
         // accumulation chunks alternate between the two TMEM accumulators and
         // are summed in registers by the epilogue (see gemm_h3_kernel)
@@ -1176,6 +1232,8 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
     p.sym = 0;
     p.sym_tiles = 0;
     p.tri_k = 0;
+    p.prog = nullptr;
+    p.pace = 0;
     p.alpha = alpha; p.beta = beta; p.C = C; p.ldc = ldc;
     p.ws = pl.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
     p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
@@ -1244,6 +1302,11 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
     return SKP_OK;
 }
 
+constexpr int64_t kPaceBytes = 1024;  // pacing slots (<= 256 CTAs) at the head of ws
+constexpr int kPaceKb = 32;            // K blocks a producer may lead its wave by (SYRK;
+constexpr int kPaceKbS = 64;           // K4s, whose wave reads ~1 MB per K block, 64)
+constexpr int kPaceMinKb = 512;        // units shorter than this are not paced
+
 // split-K slices for the SYRK: enough units for every CTA pair, and at
 // least 64 K blocks (4 promotion chunks) per slice
 int syrk_splits(int64_t tiles, int64_t K, int slots) {
@@ -1287,7 +1350,7 @@ SyrkPlan syrk_plan(int64_t N, int64_t K) {
 int64_t syrk_h3_ws_bytes(int64_t N, int64_t K) {
     if (!h_init() || N == 0 || K == 0) return 0;
     const SyrkPlan sp = syrk_plan(N, K);
-    return sp.splits > 1 ? (int64_t)sp.splits * N * N * 4 : 0;
+    return kPaceBytes + (sp.splits > 1 ? (int64_t)sp.splits * N * N * 4 : 0);
 }
 
 // C = alpha A^T A (N x N, symmetric) with A pre-split: stored K x N (N
@@ -1335,10 +1398,12 @@ int syrk_h3(int kmajor, int64_t N, int64_t K, float alpha, const void* Ahi, cons
     const HPlan& pl = sp.pl;
     const bool pair = sp.pair;
     const int splits = sp.splits;
-    if (splits > 1 && (!ws || ws_bytes < (int64_t)splits * N * N * 4)) {
-        set_error("syrk_h3 needs %lld bytes of workspace", (long long)splits * N * N * 4);
+    if (!ws || ws_bytes < syrk_h3_ws_bytes(N, K)) {
+        set_error("syrk_h3 needs %lld bytes of workspace", (long long)syrk_h3_ws_bytes(N, K));
         return SKP_ERR_ARG;
     }
+    unsigned* prog = reinterpret_cast<unsigned*>(ws);
+    void* wsp = reinterpret_cast<char*>(ws) + kPaceBytes;
     H3Params p = {};
     p.b_lo = 1;
     p.M = (int)N; p.N = (int)N; p.K = (int)K;
@@ -1350,10 +1415,13 @@ int syrk_h3(int kmajor, int64_t N, int64_t K, float alpha, const void* Ahi, cons
     p.sym = sp.tiles * splits;
     p.tri_k = 0;
     p.alpha = alpha; p.beta = 0.f; p.C = C; p.ldc = ldc;
-    p.ws = splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
+    p.ws = splits > 1 ? reinterpret_cast<float*>(wsp) : nullptr;
     p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
     p.stage_bytes = pl.stage_bytes; p.acc_stride = pl.acc_stride;
     p.a_e = a_e; p.b_e = a_e;
+    p.prog = prog;
+    p.pace = pl.kb_per_split >= kPaceMinKb ? kPaceKb : 0;
+    if (p.pace) SKP_CUDA(cudaMemsetAsync(prog, 0, kPaceBytes, st));
     // the Gram of rows (kmajor) decides the final basis' orthonormality and
     // feeds the error identity: 256-deep promotion chains there (its tiles
     // are few and short, so the extra epilogue drains are hidden)
@@ -1426,7 +1494,7 @@ int gemm_h3(int ta, int64_t M, int64_t N, int64_t K, float alpha, const void* Ah
 int64_t gemm_h3s_ws_bytes(int64_t M, int64_t N, int64_t K) {
     if (!h_init()) return 0;
     const HPlan pl = hs_plan(M, N, K, INT64_MAX, h_pair(M));
-    return pl.splits > 1 ? (int64_t)pl.splits * M * N * 4 : 0;
+    return kPaceBytes + (pl.splits > 1 ? (int64_t)pl.splits * M * N * 4 : 0);
 }
 
 int gemm_h3s(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
@@ -1450,19 +1518,26 @@ int gemm_h3s(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64
         return SKP_ERR_UNSUPPORTED;
     }
     const bool pair = h_pair(M);
-    const int64_t cap = ws ? ws_bytes / 4 : 0;
+    // ws: [pacing slots | split-K partials]
+    unsigned* prog = (ws && ws_bytes >= kPaceBytes) ? reinterpret_cast<unsigned*>(ws) : nullptr;
+    void* wsp = prog ? reinterpret_cast<char*>(ws) + kPaceBytes : ws;
+    const int64_t wsp_bytes = prog ? ws_bytes - kPaceBytes : ws_bytes;
+    const int64_t cap = wsp ? wsp_bytes / 4 : 0;
     HPlan pl = hs_plan(M, N, K, cap, pair);
-    if (pl.splits > 1 && (!ws || (int64_t)pl.splits * M * N * 4 > ws_bytes))
+    if (pl.splits > 1 && (!wsp || (int64_t)pl.splits * M * N * 4 > wsp_bytes))
         pl = hs_plan(M, N, K, 0, pair);
     H3SParams p;
     p.M = (int)M; p.N = (int)N; p.K = (int)K;
     p.bn = pl.bn; p.tiles_m = pl.tiles_m; p.tiles_n = pl.tiles_n; p.splits = pl.splits;
     p.kb_per_split = pl.kb_per_split; p.num_kb = pl.num_kb;
     p.alpha = alpha; p.beta = beta; p.C = C; p.ldc = ldc;
-    p.ws = pl.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
+    p.ws = pl.splits > 1 ? reinterpret_cast<float*>(wsp) : nullptr;
     p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
     p.stage_bytes = pl.stage_bytes; p.acc_stride = pl.acc_stride;
     p.a_e = a_e; p.b_e = b_e; p.overflow = overflow;
+    p.prog = prog;
+    p.pace = (prog && pl.kb_per_split >= kPaceMinKb) ? kPaceKbS : 0;
+    if (p.pace) SKP_CUDA(cudaMemsetAsync(prog, 0, kPaceBytes, st));
     p.chunk_kb = h_chunk_kb();
     if (2 * p.acc_stride + kSSlots * (int)kSSlotCols > (int)kHTmemCols || p.bn > kSMaxBn) {
         set_error("internal: gemm_h3s tile does not fit TMEM (bn=%d)", p.bn);
