@@ -56,6 +56,9 @@ CONFIGS = {
 }
 
 
+_SM_MAX_MHZ = 1965.0
+
+
 def load_peaks():
     p = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -380,8 +383,21 @@ def run_ours(args, cfg, rank, world, local_rank):
             "traffic_source": src}
     skey = "sketch_gather" if v2 else "sketch_rows"
     s_tr, s_src = _traffic(args.config, skey)
+    # K2's real bound is on chip: shared-memory wavefronts (profiles/
+    # r02_smem_gather_ceiling.txt: 0.957 per clock per SM, 8.8e12 gathered
+    # entries/s at 1.95 GHz).  Work = the m n s gathered entries plus the row
+    # ingest into each of the P slice CTAs (P n words per row), in entry units
+    P_sl = -(-l // (896 - 96))
+    onchip_work = rows * (n * s_ + P_sl * n)
+    onchip_ceiling = 148 * 32 * 0.957 * _SM_MAX_MHZ * 1e6
+    onchip = {"work_entries": onchip_work, "slices": P_sl,
+              "achieved_entries_per_s": round(onchip_work / (sketch_ms * 1e-3), 1),
+              "ceiling_entries_per_s": round(onchip_ceiling, 1),
+              "frac_onchip": round(onchip_work / (sketch_ms * 1e-3) / onchip_ceiling, 4),
+              "ceiling_source": "profiles/r02_smem_gather_ceiling.txt (scripts/micro/smem_gather.cu)"}
     kernels["sketch"] = {
         "kernel": "sketch_gather (K2 v2)" if v2 else "sketch_right (K2 v1)", "bound": "hbm",
+        "onchip": onchip,
         "ms_per_launch": round(sketch_ms, 4), "launches_per_step": 1,
         "share_of_step": round(sketch_ms / ms, 3), "algorithmic_bytes_per_launch": sketch_bytes,
         "achieved": round(sketch_gbs, 1), "peak": hbm, "unit": "GB/s",
