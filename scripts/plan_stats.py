@@ -9,21 +9,26 @@ from paper_2605_09755_b200.sketching import make_sketch, substream
 n, l = int(sys.argv[1]), int(sys.argv[2])
 op = make_sketch("countsketch", n, l, substream(3, 0), s=8, device="cuda")
 plan, _ = op.gather_plan()
-COLS, W, TMAX, SPARE = 896, 28, 128, 96
-P = -(-l // (COLS - SPARE))
 H = -(-n // (24608 - 32))
+npass = -(-(-(-n // H)) // 32) * 32
+V = 1                                           # sketch_gather.cu: one column per lane
+W = 20 if V == 2 else 28
+COLS, TMAX = 32 * W * V, 128
+SPARE = COLS * 3 // 28
+P = -(-l // (COLS - SPARE))
 g = plan.cpu().numpy().view(np.uint32)
 o = (P * COLS * 4 + 15) // 16 * 16 // 4 + 4   # perm, fail (16 B)
 entries = n * 8
 tot_steps = tot_wf = 0
 for h in range(H):
-    tw = g[o:o + P * W].astype(np.int64)
-    o += (P * W * 4 + 15) // 16 * 16 // 4
-    sched = g[o:o + P * W * TMAX * 32].reshape(P * W, TMAX, 32)
-    o += P * W * TMAX * 32
+    VW = W * V
+    tw = g[o:o + P * VW].astype(np.int64)
+    o += (P * VW * 4 + 15) // 16 * 16 // 4
+    sched = g[o:o + P * VW * TMAX * 32].reshape(P * VW, TMAX, 32)
+    o += P * VW * TMAX * 32
     steps = int(tw.sum())
     wf = 0
-    for w in range(P * W):
+    for w in range(P * VW):
         t = tw[w]
         if t == 0:
             continue
@@ -37,7 +42,7 @@ for h in range(H):
             wf += cnt.max()
     tot_steps += steps
     tot_wf += wf
-    print(f"pass {h}: warps {P * W} steps {steps} (mean T {steps / max(1, (tw > 0).sum()):.1f}, max {tw.max()}) wavefronts {wf} ({wf / steps:.3f} per LDS)")
+    print(f"pass {h}: V={V} virtual warps {P * VW} steps {steps} (mean T {steps / max(1, (tw > 0).sum()):.1f}, max {tw.max()}) wavefronts {wf} ({wf / steps:.3f} per LDS)")
 ideal = entries / 32
 print(f"total: steps {tot_steps} wavefronts {tot_wf}; ideal {ideal:.0f} -> padding x{tot_steps / ideal:.3f}, "
       f"conflicts x{tot_wf / tot_steps:.3f}, overall x{tot_wf / ideal:.3f}; P={P} slices, H={H} passes; "

@@ -13,10 +13,21 @@ a.normal_()
 op = make_sketch("countsketch", n, l, 7, s=8)
 out = torch.empty(m, l, device="cuda")
 nonfinite = torch.zeros(1, dtype=torch.int64, device="cuda")
-for _ in range(2):
+def run():
     if mode == "v2":
         assert op.right_permuted(a, out=out, nonfinite=nonfinite) is not None
     else:
         op.right(a, out=out, nonfinite=nonfinite)
+
+
+for _ in range(2):
+    run()
 torch.cuda.synchronize()
-print("ok")
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    run()
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 5
+print("ok", mode, m, n, l, "%.3f ms  %.1f GB/s" % (ms, (m * n * 4 + m * l * 4) / ms / 1e6))
