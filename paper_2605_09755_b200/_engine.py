@@ -194,7 +194,17 @@ def _raise_if_not_orthonormal(be, dev: float):
 def _randsvd_core(be, comm, bt, qb, gq=None, stats=None):
     bt = comm.allreduce_(bt)
     n, c = bt.shape
-    gb = be.gram64_rows_t(bt)                               # c x c, fp64
+    world = getattr(comm, "world", 1)
+    if world > 1:
+        # B B^T = sum over the n rows of B^T: each rank forms the Gram of its
+        # 1/world of them and the c x c partial Grams are summed -- the O(n c^2)
+        # fp64 Gram is not replicated on every rank (C5 at 8 ranks: 6.3 ->
+        # 0.8 ms per rank, SURVEY.md §8(e) strong-scaling limiters)
+        r0 = n * comm.rank // world
+        r1 = n * (comm.rank + 1) // world
+        gb = comm.allreduce_(be.gram64_rows_t(bt[r0:r1]))
+    else:
+        gb = be.gram64_rows_t(bt)                           # c x c, fp64
     if stats is not None:
         stats["qa2"] = be.proj_sq(gb, gq)
     w, v = be.eig_desc64(gb)
