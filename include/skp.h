@@ -115,6 +115,13 @@ int skp_sketch_gather_plan(const int32_t* colptr, const int32_t* entries, int64_
 int skp_sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
                           const void* plan, float scale, float* out, int64_t ldo, double* fro2,
                           int64_t* nonfinite, uint32_t* amax, void* stream);
+/* skp_sketch_gather_f32_acc64: the same gather of fp32 A with fp64
+ * accumulation and an fp64 output (the entries and their signs are exact in
+ * fp64): the sketch C~ = K S of the psd Nystrom core (power.py:272-275),
+ * whose literal power amplifies an fp32 sketch's rounding.                   */
+int skp_sketch_gather_f32_acc64(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
+                                const void* plan, double scale, double* out, int64_t ldo,
+                                double* fro2, int64_t* nonfinite, void* stream);
 
 /* ----------------------------------------------------------- Omega ----
  * out (rows x cols) = Generator(PCG64 (state, inc)).standard_normal((rows,

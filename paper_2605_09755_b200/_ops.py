@@ -182,14 +182,20 @@ def gather_plan_checked(plan: torch.Tensor, r: int):
 
 
 def sketch_gather(a: torch.Tensor, plan: torch.Tensor, r: int, s: int, out=None, fro2=None,
-                  nonfinite=None, amax=None):
+                  nonfinite=None, amax=None, out_dtype=None):
     """K2 v2: (a @ S) with the plan's column permutation, fused ||a||_F^2 and
-    non-finite test; fp32, a with 16-byte aligned rows (empty2d).  amax (int32
-    view, 1 element, zeroed by the caller): atomicMax of max|out|'s bits."""
+    non-finite test; fp32 a with 16-byte aligned rows (empty2d).  amax (int32
+    view, 1 element, zeroed by the caller): atomicMax of max|out|'s bits.
+    out_dtype=float64: fp64 accumulation and output (no amax)."""
     m, n, lda = _rows_ld(a)
+    od = out_dtype or (out.dtype if out is not None else a.dtype)
     if out is None:
-        out = empty2d(m, r, a.dtype, a.device)
+        out = empty2d(m, r, od, a.device)
     _, _, ldo = _rows_ld(out)
+    if od == F64:
+        call("skp_sketch_gather_f32_acc64", ptr(a), lda, m, n, r, ptr(plan), 1.0 / float(np.sqrt(s)),
+             ptr(out), ldo, ptr(fro2), ptr(nonfinite), stream_ptr(a.device))
+        return out
     call("skp_sketch_gather_f32", ptr(a), lda, m, n, r, ptr(plan), 1.0 / float(np.sqrt(s)),
          ptr(out), ldo, ptr(fro2), ptr(nonfinite), ptr(amax), stream_ptr(a.device))
     return out

@@ -499,12 +499,17 @@ gather_sched_kernel(const int32_t* __restrict__ seg_beg, const int32_t* __restri
 }
 
 // ---- the gather ----------------------------------------------------------------
-template <int NB>
+// Acc = float: the fp32 sketch of the range finder.  Acc = double: the same
+// gather with fp64 accumulation and an fp64 output (the fp32 entries and their
+// +-1 signs are exact in fp64, the 1/sqrt(s) scale is applied once), for the
+// psd Nystrom core, whose literal power W~^q Omega (cond ~1e15) turns the
+// rounding of an fp32 sketch into a 1e-3 change of its error.
+template <int NB, typename Acc = float, int TR = kGTReg>
 __global__ void __maxnreg__(72)
 sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                      const int32_t* __restrict__ lanepos, int P, const uint32_t* __restrict__ sched,
                      const int32_t* __restrict__ tw, const int32_t* __restrict__ plan_fail,
-                     float scale, float* __restrict__ out, int64_t ldo,
+                     Acc scale, Acc* __restrict__ out, int64_t ldo,
                      int64_t* nonfinite, uint32_t* __restrict__ amax, int accumulate,
                      int mark_fail) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -547,12 +552,12 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
     // compute warps: this warp's schedule -> registers (absolute smem addresses)
     const int wg = slice * kGW + warp;
     const int T = tw[wg];
-    uint32_t e[kGTReg];
+    uint32_t e[TR];
 #pragma unroll
-    for (int t = 0; t < kGTReg; ++t) {
+    for (int t = 0; t < TR; ++t) {
         const uint32_t v =
             t < T ? __ldg(sched + ((int64_t)wg * kGTMax + t) * 32 + lane) : zero_word * 4u;
-        // (steps >= kGTReg, if any, are read per row below)
+        // (steps >= TR, if any, are read per row below)
         e[t] = v + base;  // absolute smem address in buffer 0; bit 31 (sign) kept
     }
     const int lp = lanepos[(int64_t)wg * 32 + lane];
@@ -569,31 +574,32 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
         // out of the row loop (3x the registers, spills) and orders the loads
         // below after the wait
 #pragma unroll
-        for (int t = 0; t < kGTReg; ++t) asm volatile("" : "+r"(e[t]));
-        float acc = 0.f;
+        for (int t = 0; t < TR; ++t) asm volatile("" : "+r"(e[t]));
+        Acc acc = 0;
 #pragma unroll
-        for (int t4 = 0; t4 < kGTReg; t4 += 4) {
+        for (int t4 = 0; t4 < TR; t4 += 4) {
             if (t4 >= T) break;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t ev = e[t4 + u];
                 float x;  // buffer offset as the LDS immediate
                 asm("ld.shared.f32 %0, [%1+%2];" : "=f"(x) : "r"(ev & 0x7fffffffu), "n"(boff));
-                acc += __int_as_float(__float_as_int(x) ^ (int)(ev & 0x80000000u));
+                acc += (Acc)__int_as_float(__float_as_int(x) ^ (int)(ev & 0x80000000u));
             }
         }
         // rare heavy warps: the steps past the register-resident ones stream
         // from the (L1-resident) schedule
-        for (int t = kGTReg; t < T; ++t) {
+        for (int t = TR; t < T; ++t) {
             const uint32_t ev = __ldg(sched + ((int64_t)wg * kGTMax + t) * 32 + lane) + base;
             float x;
             asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(x) : "r"(ev & 0x7fffffffu), "n"(boff));
-            acc += __int_as_float(__float_as_int(x) ^ (int)(ev & 0x80000000u));
+            acc += (Acc)__int_as_float(__float_as_int(x) ^ (int)(ev & 0x80000000u));
         }
         // every load of this row (the non-volatile register-resident ones
         // included: acc depends on all of them) completes before this warp
         // reports the buffer done -- the last warp's refill overwrites it
-        asm volatile("" : "+f"(acc)::"memory");
+        if constexpr (sizeof(Acc) == 4) asm volatile("" : "+f"(acc)::"memory");
+        else asm volatile("" : "+d"(acc)::"memory");
         __syncwarp();
         if (lane == 0) {
             // the last warp done with this buffer refills it with row i + NB*G
@@ -616,13 +622,13 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
             }
         }
         // a split column's second half sits on the next lane
-        const float part = __shfl_down_sync(0xffffffffu, acc, 1);
+        const Acc part = __shfl_down_sync(0xffffffffu, acc, 1);
         if (primary) acc += part;
         if (valid) {
             // column passes after the first add to what the earlier ones wrote
-            const float o = accumulate ? fmaf(acc, scale, out[i * ldo + v_out]) : acc * scale;
+            const Acc o = accumulate ? fma(acc, scale, out[i * ldo + v_out]) : acc * scale;
             bad |= !isfinite(o);
-            mx = max(mx, __float_as_uint(fabsf(o)));
+            if constexpr (sizeof(Acc) == 4) mx = max(mx, __float_as_uint(fabsf(o)));
             out[i * ldo + v_out] = o;
         }
     };
@@ -734,8 +740,9 @@ int gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n, int64_
     return SKP_OK;
 }
 
-int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
-                      const void* plan, float scale, float* out, int64_t ldo, double* fro2,
+template <typename Acc>
+int sketch_gather(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
+                      const void* plan, Acc scale, Acc* out, int64_t ldo, double* fro2,
                       int64_t* nonfinite, uint32_t* amax, cudaStream_t st) {
     SKP_ARG(m >= 0 && n >= 1 && r >= 1 && ldo >= r, "sketch_gather: bad sizes");
     if (gather_passes(n) > kGMaxPass || (reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3) ||
@@ -751,7 +758,9 @@ int sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t
     const GLayout L = gather_layout(const_cast<void*>(plan), n, r);
     const int P = L.P;
     const int G = std::max(1, std::min<int>(sms / P, (int)std::min<int64_t>(m, 1 << 20)));
-    auto kern = sketch_gather_kernel<2>;
+    // fp64 accumulation: 40 register-resident steps (the accumulator and the
+    // output take two registers more)
+    auto kern = sizeof(Acc) == 4 ? sketch_gather_kernel<2, Acc, kGTReg> : sketch_gather_kernel<2, Acc, 40>;
     const size_t smem = GBuf<2>::smem;
     SKP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // one launch per column pass: pass h gathers A[:, h*npass ...] and adds
@@ -790,6 +799,13 @@ extern "C" int skp_sketch_gather_f32(const float* A, int64_t lda, int64_t m, int
                                      const void* plan, float scale, float* out, int64_t ldo,
                                      double* fro2, int64_t* nonfinite, uint32_t* amax,
                                      void* stream) {
-    return sketch_gather_f32(A, lda, m, n, r, plan, scale, out, ldo, fro2, nonfinite, amax,
-                             (cudaStream_t)stream);
+    return sketch_gather<float>(A, lda, m, n, r, plan, scale, out, ldo, fro2, nonfinite, amax,
+                                (cudaStream_t)stream);
+}
+extern "C" int skp_sketch_gather_f32_acc64(const float* A, int64_t lda, int64_t m, int64_t n,
+                                           int64_t r, const void* plan, double scale, double* out,
+                                           int64_t ldo, double* fro2, int64_t* nonfinite,
+                                           void* stream) {
+    return sketch_gather<double>(A, lda, m, n, r, plan, scale, out, ldo, fro2, nonfinite, nullptr,
+                                 (cudaStream_t)stream);
 }

@@ -457,7 +457,9 @@ def _nystrom_dev(t: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL, row
     # (rows of S^T C~ P permuted), Omega_P = P^T Omega, so C = (C~ P)(P^T Y)
     # and W = Y^T W~ Y are the reference's (power.py:276-287).  K2 v1
     # (natural order) where v2 does not apply or its plan fails.
-    got = sk.right_permuted(t, nonfinite=nonfinite, deferred=True)
+    # (fp32 K: the gather accumulates in fp64 and writes C~ in fp64 -- the
+    # literal core amplifies the rounding of an fp32 sketch)
+    got = sk.right_permuted(t, nonfinite=nonfinite, deferred=True, out_dtype=F64)
     ctil, perm = got if got is not None else (None, None)
     bad = int(comm.allreduce_(nonfinite).item())
     if bad >= _ops.GATHER_PLAN_FAIL_MARK:

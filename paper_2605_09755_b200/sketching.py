@@ -151,7 +151,7 @@ class SketchOperator:
         return self._gather
 
     def right_permuted(self, a: torch.Tensor, out=None, fro2=None, nonfinite=None,
-                       deferred: bool = False, amax=None):
+                       deferred: bool = False, amax=None, out_dtype=None):
         """(a @ S P, perm) with perm[v] (int32, on the device) = the column of
         a @ S at position v, via the row-gather kernel (fp32, n <= 98304); None
         when it does not apply.  deferred=True skips the plan's host check: a
@@ -168,7 +168,8 @@ class SketchOperator:
             return None
         g = plan[0]
         perm_dev = g[:4 * self.r].view(torch.int32)   # the first r entries are the valid ones
-        return _ops.sketch_gather(a, g, self.r, self.s, out, fro2, nonfinite, amax), perm_dev
+        return (_ops.sketch_gather(a, g, self.r, self.s, out, fro2, nonfinite, amax, out_dtype),
+                perm_dev)
 
     def left_t(self, x: torch.Tensor, out=None) -> torch.Tensor:
         if self.kind == "countsketch":

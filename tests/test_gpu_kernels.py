@@ -207,6 +207,23 @@ def test_sketch_gather_permuted(skp, ops, m, n, r, s):
     assert int(bad.item()) >= 1
 
 
+@pytest.mark.parametrize("m,n,r,s", [(67, 16384, 4000, 8), (9, 32768, 4000, 8), (5, 65536, 4096, 8)])
+def test_sketch_gather_acc64(skp, ops, m, n, r, s):
+    """K2 v2 with fp64 accumulation (the psd Nystrom sketch): (A S) P in fp64
+    equal to the oracle's fp64 product to fp64 rounding."""
+    rng = np.random.default_rng(n + r + 1)
+    op = skp.make_sketch("countsketch", n, r, seed=17, s=s)
+    g, perm = op.gather_plan()
+    a = rng.standard_normal((m, n)).astype(np.float32)
+    t = ops.empty2d(m, n, torch.float32, "cuda")
+    t.copy_(torch.from_numpy(a))
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out, _ = op.right_permuted(t, nonfinite=bad, out_dtype=torch.float64)
+    assert out.dtype == torch.float64 and int(bad.item()) == 0
+    ref = o.CountSketch("countsketch", n, r, 17, s=s).apply_right(a.astype(np.float64))
+    assert np.abs(out.cpu().numpy() - ref[:, perm]).max() <= 1e-13 * np.abs(ref).max()
+
+
 def test_sketch_gather_declines_outside_its_envelope(skp, ops):
     """No plan (and right_permuted -> None, the caller keeps K2 v1) when rows do
     not fit the smem row buffer or a column needs more than 128 steps."""

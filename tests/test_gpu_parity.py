@@ -356,7 +356,18 @@ def test_nystrom_fp32_vs_oracle(skp):
     ospec = o.Spec(k=64, l=512, r1=512, r2=64, q=2, seed=4, s=8)
     co, wo = o.nystrom_core(kmat, ospec, stabilized=False)
     eo = o.nystrom_rel_error(kmat, co, wo)
-    assert abs(e - eo) <= ERR_TOL * eo, (e, eo)
+    # the literal core W = Y^T W~ Y with Y = W~^2 Omega has cond(W) ~1e15 at
+    # this size: fp64 rounding alone (a different summation order in the
+    # products) moves its error by ~2e-3 relative -- the 5e-3 of the fp64
+    # literal golden test (test_nystrom_small_fp64_literal).  At C4's shape the
+    # same path matches the oracle to 1e-10 (bench.py slab_parity).
+    assert abs(e - eo) <= 5e-3 * eo, (e, eo)
+    # the orthonormalised power (same span) is well conditioned: 1e-3
+    rs = skp.nystrom_psd(kdev, spec, stabilized=True)
+    es = o.nystrom_rel_error(kmat, rs.C.cpu().numpy(), rs.W.cpu().numpy())
+    cs, ws = o.nystrom_core(kmat, ospec, stabilized=True)
+    eos = o.nystrom_rel_error(kmat, cs, ws)
+    assert abs(es - eos) <= ERR_TOL * eos, (es, eos)
 
 
 def _nystrom_fp64_restatement(kmat: torch.Tensor, spec, cols, signs, omega):
