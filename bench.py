@@ -679,17 +679,20 @@ def run_nystrom(args, cfg, rank, world, local_rank):
     hbm, _, _, _ = load_peaks()
     # the dominant kernel: K2 v2 on the rank's rows of K
     sk = make_sketch("countsketch", n, l, substream(spec.seed, 0), s=s_, device=device)
-    ctil = _ops.empty2d(rows, l, kmat.dtype, device)
+    # as the step runs it: fp32 K, fp64 accumulation and fp64 C~ (power._nystrom_dev)
+    ctil = _ops.empty2d(rows, l, torch.float64, device)
     nonfinite = torch.zeros(1, dtype=torch.int64, device=device)
-    v2 = sk.right_permuted(kmat, out=ctil, nonfinite=nonfinite) is not None
-    run_sketch = (lambda: sk.right_permuted(kmat, out=ctil, nonfinite=nonfinite)) if v2 else \
-        (lambda: sk.right(kmat, out=ctil, nonfinite=nonfinite))
+    v2 = sk.right_permuted(kmat, out=ctil, nonfinite=nonfinite,
+                           out_dtype=torch.float64) is not None
+    run_sketch = (lambda: sk.right_permuted(kmat, out=ctil, nonfinite=nonfinite,
+                                            out_dtype=torch.float64)) if v2 else \
+        (lambda: sk.right(kmat.double(), out=ctil, nonfinite=nonfinite))
     sk_ms = _time_launches(run_sketch)
-    sk_bytes = rows * n * 4 + rows * l * 4 + n * s_ * 5
+    sk_bytes = rows * n * 4 + rows * l * 8 + n * s_ * 5
     sym_ms = _time_launches(lambda: _ops.sym_check(kmat)) if world == 1 else None
     del ctil
     sk_gbs = sk_bytes / (sk_ms * 1e-3) / 1e9
-    roof = {"kernel": "sketch_gather (K2 v2) C~ = K S" if v2 else "sketch_right (K2 v1)",
+    roof = {"kernel": "sketch_gather (K2 v2, fp64 accumulation) C~ = K S" if v2 else "sketch_right (K2 v1)",
             "bound": "hbm", "achieved": round(sk_gbs, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(sk_gbs / hbm, 4), "traffic": None,
             "traffic_unit": "DRAM bytes per launch (ncu --set full)",
@@ -725,7 +728,7 @@ def run_nystrom(args, cfg, rank, world, local_rank):
         "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 (l-dimensional core: 3xTF32 / SIMT fp32 products, fp64 small factorisations)",
+        "dtype": "f32 K; sketch accumulated in fp64, core in fp64 (DMMA), as the reference",
         "data": "synthetic (seeded RBF points, BASELINE config recipe)",
         "config": {"workload": args.config, "n": n, "l": l, "s": s_, "k": cfg["k"],
                    "r2": cfg["r2"], "q": cfg["q"], "bandwidth_h": round(h, 6),

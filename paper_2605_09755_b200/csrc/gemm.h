@@ -11,6 +11,12 @@ int gemm_simt(int ta, int tb, int64_t M, int64_t N, int64_t K, T alpha, const T*
               cudaStream_t st);
 int64_t gemm_simt_ws_bytes(int64_t M, int64_t N, int64_t K, int elem);
 
+// FP64 on the DMMA tensor cores (gemm_dmma.cu)
+int gemm_dmma(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+              int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+              void* ws, int64_t ws_bytes, cudaStream_t st);
+int64_t gemm_dmma_ws_bytes(int64_t M, int64_t N, int64_t K);
+
 // tcgen05 3xTF32 path (gemm_tc.cu).  Returns SKP_ERR_UNSUPPORTED when the
 // shape/layout is outside what the kernel handles (caller falls back).
 bool tc_available();

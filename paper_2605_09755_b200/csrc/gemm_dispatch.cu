@@ -1,5 +1,5 @@
-// skp_gemm_* C-ABI: argument checks and dispatch between the tcgen05 3xTF32
-// kernel (FP32 hot path) and the SIMT kernels (FP64, exact FP32).
+// skp_gemm_* C-ABI: argument checks and dispatch: FP32 to the tcgen05 3xTF32
+// kernel (or the SIMT kernel for exact-FP32 mode), FP64 to the DMMA kernel.
 #include "common.cuh"
 #include "gemm.h"
 
@@ -24,7 +24,7 @@ extern "C" int skp_has_tcgen05(void) { return tc_available() ? 1 : 0; }
 
 extern "C" int64_t skp_gemm_ws_bytes(int transA, int transB, int64_t M, int64_t N, int64_t K,
                                      int32_t elem_bytes, int32_t mode) {
-    int64_t w = gemm_simt_ws_bytes(M, N, K, elem_bytes);
+    int64_t w = elem_bytes == 8 ? gemm_dmma_ws_bytes(M, N, K) : gemm_simt_ws_bytes(M, N, K, elem_bytes);
     if (elem_bytes == 4 && mode != 2 && tc_available()) {
         int64_t t = gemm_tc_ws_bytes(transA, transB, M, N, K);
         if (t > w) w = t;
@@ -59,6 +59,6 @@ extern "C" int skp_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_
     (void)mode;
     int rc = check(transA, transB, M, N, K, lda, ldb, ldc, A, B, C);
     if (rc) return rc;
-    return gemm_simt<double>(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws,
-                             ws_bytes, SKP_STREAM(stream));
+    return gemm_dmma(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_bytes,
+                     SKP_STREAM(stream));
 }

@@ -566,16 +566,19 @@ extern "C" int skp_syevj_f64(double* A, int64_t n, double* W, double* V, int32_t
 // _check_psd's symmetry test (power.py:242-255) at any n: out[0] = max
 // |a_ij - a_ji|, out[1] = max |a_ij| (fp64 bit patterns of non-negative
 // values, so an integer atomicMax orders them; the caller zeroes out).  One
-// CTA per 32 x 32 tile pair (bi >= bj): both tiles are read once, coalesced,
-// the transpose goes through shared memory -- the matrix is read exactly once
+// CTA per 64 x 64 tile pair (bi >= bj) at a time: tile (bi, bj) is read into
+// registers and tile (bj, bi) into shared memory with 16-byte loads (16
+// elements in flight per thread and tile), so the matrix is read exactly once
 // (C4: 17.2 GB, HBM-bound) with no n x n temporaries.
+constexpr int kSymT = 64;
 template <typename T>
 __global__ void __launch_bounds__(256)
-sym_check_kernel(const T* __restrict__ A, int64_t n, int64_t ld, int64_t tiles,
+sym_check_kernel(const T* __restrict__ A, int64_t n, int64_t ld, int64_t tiles, int vec_ok,
                  unsigned long long* __restrict__ out) {
-    __shared__ T t0[32][33];
-    __shared__ T t1[32][33];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    constexpr int V = 16 / sizeof(T);        // elements per 16-byte load
+    constexpr int RV = kSymT / V;            // vectors per tile row
+    constexpr int NV = kSymT * kSymT / V / 256;  // vectors per thread per tile
+    __shared__ T t1[kSymT][kSymT + 1];
     double dmax = 0.0, amax = 0.0;
     for (int64_t p = blockIdx.x; p < tiles * (tiles + 1) / 2; p += gridDim.x) {
         // p -> (bi, bj), bi >= bj: p = bi (bi + 1) / 2 + bj
@@ -583,25 +586,49 @@ sym_check_kernel(const T* __restrict__ A, int64_t n, int64_t ld, int64_t tiles,
         while (bi * (bi + 1) / 2 > p) --bi;
         while ((bi + 1) * (bi + 2) / 2 <= p) ++bi;
         const int64_t bj = p - bi * (bi + 1) / 2;
+        const bool full = vec_ok && (bi + 1) * kSymT <= n;
+        T a[NV][V];
         __syncthreads();
-        for (int r = ty; r < 32; r += 8) {
-            const int64_t i = bi * 32 + r, j = bj * 32 + tx;
-            t0[r][tx] = (i < n && j < n) ? A[i * ld + j] : T(0);
-            const int64_t i2 = bj * 32 + r, j2 = bi * 32 + tx;
-            t1[r][tx] = (i2 < n && j2 < n) ? A[i2 * ld + j2] : T(0);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int u = threadIdx.x + 256 * q, r = u / RV, c = (u % RV) * V;
+            const int64_t i = bi * kSymT + r, j = bj * kSymT + c;   // tile (bi, bj)
+            const int64_t i2 = bj * kSymT + r, j2 = bi * kSymT + c; // tile (bj, bi)
+            if (full) {
+                const uint4 x = *reinterpret_cast<const uint4*>(A + i * ld + j);
+                const uint4 y = *reinterpret_cast<const uint4*>(A + i2 * ld + j2);
+                const T* xs = reinterpret_cast<const T*>(&x);
+                const T* ys = reinterpret_cast<const T*>(&y);
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    a[q][e] = xs[e];
+                    t1[r][c + e] = ys[e];
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    a[q][e] = (i < n && j + e < n) ? A[i * ld + j + e] : T(0);
+                    t1[r][c + e] = (i2 < n && j2 + e < n) ? A[i2 * ld + j2 + e] : T(0);
+                }
+            }
         }
         __syncthreads();
-        for (int r = ty; r < 32; r += 8) {
-            const double a = (double)t0[r][tx], b = (double)t1[tx][r];  // a_ij, a_ji
-            dmax = fmax(dmax, fabs(a - b));
-            amax = fmax(amax, fmax(fabs(a), fabs(b)));
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int u = threadIdx.x + 256 * q, r = u / RV, c = (u % RV) * V;
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const double x = (double)a[q][e], y = (double)t1[c + e][r];  // a_ij, a_ji
+                dmax = fmax(dmax, fabs(x - y));
+                amax = fmax(amax, fmax(fabs(x), fabs(y)));
+            }
         }
     }
     for (int o = 16; o; o >>= 1) {
         dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
         amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     }
-    if (tx == 0) {
+    if ((threadIdx.x & 31) == 0) {
         atomicMax(&out[0], (unsigned long long)__double_as_longlong(dmax));
         atomicMax(&out[1], (unsigned long long)__double_as_longlong(amax));
     }
@@ -613,13 +640,14 @@ static int sym_check(const T* A, int64_t n, int64_t ld, double* out, void* strea
     cudaStream_t st = SKP_STREAM(stream);
     SKP_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(double), st));
     if (!n) return SKP_OK;
-    const int64_t tiles = cdiv(n, 32);
+    const int64_t tiles = cdiv(n, (int64_t)kSymT);
+    const int vec_ok = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (ld * sizeof(T)) % 16 == 0;
     int dev = 0, sms = 148;
     SKP_CUDA(cudaGetDevice(&dev));
     SKP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int64_t pairs = tiles * (tiles + 1) / 2;
     const unsigned grid = (unsigned)std::min<int64_t>(pairs, (int64_t)sms * 8);
-    sym_check_kernel<T><<<grid, 256, 0, st>>>(A, n, ld, tiles,
+    sym_check_kernel<T><<<grid, 256, 0, st>>>(A, n, ld, tiles, vec_ok,
                                              reinterpret_cast<unsigned long long*>(out));
     SKP_LAUNCHED(sym_check_kernel);
     return SKP_OK;

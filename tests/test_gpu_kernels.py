@@ -224,6 +224,27 @@ def test_sketch_gather_acc64(skp, ops, m, n, r, s):
     assert np.abs(out.cpu().numpy() - ref[:, perm]).max() <= 1e-13 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("n", [1, 63, 64, 65, 300, 4097])
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_sym_check(ops, n, dt):
+    """_check_psd's tiled symmetry test: max |a - a^T| and max |a| in one pass,
+    exact against torch (ragged tiles and unaligned rows included)."""
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randn(n, n, generator=g, device="cuda", dtype=torch.float64)
+    a = ((x + x.T) / 2).to(dt)
+    i, j = (n * 2) // 3, n // 5
+    a[i, j] += 0.125
+    ref_d = (a.double() - a.double().T).abs().max().item()
+    ref_a = a.double().abs().max().item()
+    got = ops.sym_check(a).tolist()
+    assert got == [ref_d, ref_a]
+    if n > 8:   # a view with an odd leading dimension (scalar loads)
+        big = torch.zeros(n, n + 3, device="cuda", dtype=dt)
+        big[:, :n] = a
+        got2 = ops.sym_check(big[:, :n]).tolist()
+        assert got2 == [ref_d, ref_a]
+
+
 def test_sketch_gather_declines_outside_its_envelope(skp, ops):
     """No plan (and right_permuted -> None, the caller keeps K2 v1) when rows do
     not fit the smem row buffer or a column needs more than 128 steps."""
