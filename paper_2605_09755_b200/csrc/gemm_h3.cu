@@ -1310,10 +1310,20 @@ constexpr int kPaceMinKb = 512;        // units shorter than this are not paced
 // split-K slices for the SYRK: enough units for every CTA pair, and at
 // least 64 K blocks (4 promotion chunks) per slice
 int syrk_splits(int64_t tiles, int64_t K, int slots) {
+    // time ~ waves(tiles s) / s: the smallest, at >= 64 K blocks per slice
+    // (C5's Grams: 15 tiles over 74 CTA pairs -> 4 slices in one wave, where
+    // 5 slices made 75 units and a second wave for one of them)
     const int64_t nkb = cdiv(K, HK);
-    int64_t s = 1;
-    while (tiles * s < slots && nkb / (s + 1) >= 64 && s < 16) ++s;
-    return (int)s;
+    int best = 1;
+    double best_t = 1e30;
+    for (int s = 1; s <= 16 && (s == 1 || nkb / s >= 64); ++s) {
+        const double t = (double)cdiv(tiles * s, (int64_t)slots) / s;
+        if (t < best_t - 1e-9) {
+            best_t = t;
+            best = s;
+        }
+    }
+    return best;
 }
 
 struct SyrkPlan {
