@@ -297,7 +297,9 @@ int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, float alpha,
  * pre-split planes of A stored K x N (kmajor = 0, lda % 64 == 0, both GEMM
  * operands MN-major) or A^T stored N x K (kmajor = 1: the Gram of the rows,
  * e.g. Y^T Y from the planes of Y^T; split over K when there are fewer
- * lower-triangle tiles than CTA pairs, ws: skp_syrk_h3_ws_bytes).  Replaces the operator A~^T A~ that power.py:131-133 applies
+ * lower-triangle tiles than CTA pairs, ws: skp_syrk_h3_ws_bytes).  beta:
+ * C = alpha A^T A + beta C (block-wise accumulation of G behind a streamed
+ * upload).  Replaces the operator A~^T A~ that power.py:131-133 applies
  * twice per power step (y = atil @ (atil.T @ y)): formed once, the q power
  * steps then run in the l-dimensional sketch space (SKETCH-SPACE power
  * iteration).  Only the tiles meeting the lower triangle run;
@@ -305,8 +307,8 @@ int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, float alpha,
  * skp_gemm_h3 (2^-22 per product, register-promoted accumulation).          */
 int64_t skp_syrk_h3_ws_bytes(int64_t N, int64_t K);
 int skp_syrk_h3(int32_t kmajor, int64_t N, int64_t K, float alpha, const void* A_hi,
-                const void* A_lo, int64_t lda, const int32_t* a_exp, float* C, int64_t ldc,
-                void* ws, int64_t ws_bytes, void* stream);
+                const void* A_lo, int64_t lda, const int32_t* a_exp, float beta, float* C,
+                int64_t ldc, void* ws, int64_t ws_bytes, void* stream);
 
 /* skp_gemm_h3s: C = alpha A^T B + beta C with A (K x M, fp32, lda % 32 == 0)
  * split into fp16 hi/lo INSIDE the kernel with the caller's exponent 2^a_exp

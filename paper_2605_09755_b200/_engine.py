@@ -129,14 +129,15 @@ def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: b
 
 
 def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_total=None,
-                  lazy: bool = False):
+                  lazy: bool = False, gram=None):
     """power.py:113-134 on a row slab of A~: Y = A~ Omega, then q x
     {orth(Y) if stabilized; Z = sum_p A~_p^T Y_p; Y = A~ Z}.  A~ feeds all
     1 + 2q products, so it is prepared once (be.prepare: the fp16 split of
-    the 3xFP16 GEMM on the CUDA backend)."""
+    the 3xFP16 GEMM on the CUDA backend).  gram: G = A~^T A~ already formed
+    for the sketch-space path (streamed uploads accumulate it per block)."""
     atil = be.prepare(atil)
     if lazy and stabilized and q > 0 and hasattr(be, "gram_ok") and be.gram_ok(atil, omega, q):
-        return be.power_gram(comm, atil, omega, q, SHIFT_REL[_dtype_key(be)])
+        return be.power_gram(comm, atil, omega, q, SHIFT_REL[_dtype_key(be)], g=gram)
     if lazy and stabilized and q > 0 and hasattr(be, "planes_ok") and be.planes_ok(atil, omega):
         return be.power_lazy_planes(comm, atil, omega, q, SHIFT_REL[_dtype_key(be)])
     y = be.mm(atil, omega)

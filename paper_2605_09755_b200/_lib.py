@@ -80,7 +80,8 @@ SIGNATURES = {
     "skp_sym_check_f32": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "skp_sym_check_f64": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "skp_syrk_h3_ws_bytes": (_i64, [_i64, _i64]),
-    "skp_syrk_h3": (_int, [_i32, _i64, _i64, _f32, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp]),
+    "skp_syrk_h3": (_int, [_i32, _i64, _i64, _f32, _vp, _vp, _i64, _vp, _f32, _vp, _i64, _vp, _i64,
+                           _vp]),
     "skp_gemm_h3s_ws_bytes": (_i64, [_i64, _i64, _i64]),
     "skp_gemm_h3s": (_int, [_i64, _i64, _i64, _f32, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _f32, _vp,
                             _i64, _vp, _vp, _i64, _vp]),

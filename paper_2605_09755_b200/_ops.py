@@ -418,19 +418,22 @@ def gemm_h3_emit_t(a: SplitH2, b: SplitH2, ta: bool = False, shift: int | None =
     return out
 
 
-def syrk_h3(a: SplitH2, alpha: float = 1.0, out=None, rows: bool = False) -> torch.Tensor:
-    """K4h SYRK, exactly symmetric: alpha a^T a from the planes of a stored
-    K x N (a.rows = K; both operands MN-major), or with rows=True alpha a a^T
-    (the Gram of a's rows, a stored N x K, both operands K-major)."""
+def syrk_h3(a: SplitH2, alpha: float = 1.0, out=None, rows: bool = False,
+            beta: float = 0.0) -> torch.Tensor:
+    """K4h SYRK, exactly symmetric: alpha a^T a (+ beta out) from the planes
+    of a stored K x N (a.rows = K; both operands MN-major), or with rows=True
+    alpha a a^T (the Gram of a's rows, a stored N x K, both operands K-major)."""
     N, K = (a.rows, a.cols) if rows else (a.cols, a.rows)
     if out is None:
+        if beta != 0.0:
+            raise ValueError("beta != 0 needs out")
         out = empty2d(N, N, F32, a.hi.device)
     _, _, ldc = _rows_ld(out)
     lib = _lib.load()
     wsb = int(lib.skp_syrk_h3_ws_bytes(N, K))
     ws = workspace(a.hi.device, wsb) if wsb else None
-    call("skp_syrk_h3", int(rows), N, K, alpha, ptr(a.hi), ptr(a.lo), a.ld, ptr(a.e), ptr(out),
-         ldc, ptr(ws), wsb, stream_ptr(a.hi.device))
+    call("skp_syrk_h3", int(rows), N, K, alpha, ptr(a.hi), ptr(a.lo), a.ld, ptr(a.e), beta,
+         ptr(out), ldc, ptr(ws), wsb, stream_ptr(a.hi.device))
     return out
 
 
@@ -711,6 +714,13 @@ class CudaBackend:
             yt = gemm_h3_emit_t(atil, split_h2(z, trans=True), out=yt)
         return yt
 
+    def gram_wanted(self, rows: int, l: int, r2: int, q: int) -> bool:
+        """gram_ok's decision from the shapes alone (before A~ exists: the
+        streamed upload accumulates G block by block behind the copy)."""
+        return (self.dtype == F32 and self.gemm_mode == "auto" and q >= 1
+                and rows * l >= H3_MIN_ELEMS and l <= 3.6 * q * r2 and rows >= 2 * l
+                and bool(_lib.load().skp_has_tcgen05()))
+
     def gram_ok(self, atil, omega, q: int) -> bool:
         """Run the power iteration in the sketch space (power_gram)?  It costs
         one SYRK (m l^2 useful MACs, tiles of the lower triangle) plus one
@@ -723,7 +733,7 @@ class CudaBackend:
         m, l, r2 = atil.rows, atil.cols, omega.shape[1]
         return l <= 3.6 * q * r2 and m >= 2 * l and atil.ld % 64 == 0
 
-    def power_gram(self, comm, atil: SplitH2, omega, q: int, shift: float):
+    def power_gram(self, comm, atil: SplitH2, omega, q: int, shift: float, g=None):
         """The stabilized power iteration (power.py:113-134) in the sketch
         space: with Y = A~ W,
             A~ (A~^T Y) = A~ (G W),  G = A~^T A~ (l x l, summed over ranks),
@@ -735,8 +745,10 @@ class CudaBackend:
         in exact arithmetic, with one pass over A~ for G instead of 2q.  The
         q steps are 3xFP16 products of l x l by l x r2 whose blocks stay as
         fp16 planes of their transposes.  Lazy, as power_lazy_planes: a
-        failed factorisation only sets self.fail.  Returns Y^T planes."""
-        g = comm.allreduce_(syrk_h3(atil))
+        failed factorisation only sets self.fail.  Returns Y^T planes.
+        g: this rank's G already formed (block by block behind a streamed
+        upload), else one SYRK of atil here."""
+        g = comm.allreduce_(g if g is not None else syrk_h3(atil))
         gs = split_h2(g)
         del g
         # the blocks are re-split from fp32 every step (fresh exponents): an

@@ -1387,8 +1387,8 @@ __global__ void sym_mirror_kernel(float* __restrict__ C, int64_t N, int64_t ldc)
 }
 
 int syrk_h3(int kmajor, int64_t N, int64_t K, float alpha, const void* Ahi, const void* Alo,
-            int64_t lda, const int32_t* a_e, float* C, int64_t ldc, void* ws, int64_t ws_bytes,
-            cudaStream_t st) {
+            int64_t lda, const int32_t* a_e, float beta, float* C, int64_t ldc, void* ws,
+            int64_t ws_bytes, cudaStream_t st) {
     if (!h_init()) {
         set_error("unsupported: the 3xFP16 tcgen05 GEMM needs an sm_100 device");
         return SKP_ERR_UNSUPPORTED;
@@ -1424,7 +1424,7 @@ int syrk_h3(int kmajor, int64_t N, int64_t K, float alpha, const void* Ahi, cons
     p.sym_tiles = sp.tiles;
     p.sym = sp.tiles * splits;
     p.tri_k = 0;
-    p.alpha = alpha; p.beta = 0.f; p.C = C; p.ldc = ldc;
+    p.alpha = alpha; p.beta = beta; p.C = C; p.ldc = ldc;
     p.ws = splits > 1 ? reinterpret_cast<float*>(wsp) : nullptr;
     p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
     p.stage_bytes = pl.stage_bytes; p.acc_stride = pl.acc_stride;
@@ -1484,7 +1484,7 @@ int syrk_h3(int kmajor, int64_t N, int64_t K, float alpha, const void* Ahi, cons
     }
     if (splits > 1) {
         const int64_t blocks = std::min<int64_t>(cdiv(N * N, 256), (int64_t)h_sms * 8);
-        h3_splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(p.ws, splits, N, N, alpha, 0.f, C, ldc);
+        h3_splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(p.ws, splits, N, N, alpha, beta, C, ldc);
         SKP_LAUNCHED(h3_splitk_reduce);
     }
     const unsigned nt = (unsigned)cdiv(N, 32);
@@ -1707,12 +1707,12 @@ extern "C" int skp_split_h2_f32(const float* X, int64_t rows, int64_t cols, int6
 extern "C" int64_t skp_syrk_h3_ws_bytes(int64_t N, int64_t K) { return skp::syrk_h3_ws_bytes(N, K); }
 
 extern "C" int skp_syrk_h3(int32_t kmajor, int64_t N, int64_t K, float alpha, const void* A_hi,
-                           const void* A_lo, int64_t lda, const int32_t* a_exp, float* C,
-                           int64_t ldc, void* ws, int64_t ws_bytes, void* stream) {
+                           const void* A_lo, int64_t lda, const int32_t* a_exp, float beta,
+                           float* C, int64_t ldc, void* ws, int64_t ws_bytes, void* stream) {
     SKP_ARG(N >= 0 && K >= 0 && lda >= (kmajor ? K : N) && ldc >= N && a_exp &&
                 (N == 0 || (A_hi && A_lo && C)),
             "syrk_h3: bad arguments");
-    return skp::syrk_h3(kmajor, N, K, alpha, A_hi, A_lo, lda, a_exp, C, ldc, ws, ws_bytes,
+    return skp::syrk_h3(kmajor, N, K, alpha, A_hi, A_lo, lda, a_exp, beta, C, ldc, ws, ws_bytes,
                         SKP_STREAM(stream));
 }
 

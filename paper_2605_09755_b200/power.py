@@ -217,6 +217,12 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     else:
         atil = _ops.empty2d(m_loc, spec.r1, a.dtype, dev)
         v2, perm = None, None
+        # the sketch-space power iteration needs G = A~^T A~: formed here block
+        # by block (each block's own fp16 split, the SYRK accumulating into G)
+        # while the next blocks are still on the PCIe link
+        gram = None
+        if spec.stabilized and be.gram_wanted(m_loc, spec.r1, spec.r2, spec.q):
+            gram = _ops.empty2d(spec.r1, spec.r1, a.dtype, dev)
         for r0, r1 in streamed.blocks():
             if v2 is not False:
                 got = sk.right_permuted(a[r0:r1], out=atil[r0:r1], fro2=fro2, nonfinite=nonfinite,
@@ -229,6 +235,9 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
             if not v2:
                 sk.right(a[r0:r1], out=atil[r0:r1], fro2=fro2, nonfinite=nonfinite)
                 e_io = None
+                gram = None
+            if gram is not None:
+                _ops.syrk_h3(_ops.split_h2(atil[r0:r1]), out=gram, beta=0.0 if r0 == 0 else 1.0)
     ph.mark("apply_right", "split")
     # the power iteration's operand: A~ split once into fp16 hi/lo planes (the
     # fp32 A~ is released here; the footprint stays m x l x 4 bytes)
@@ -254,7 +263,7 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     # rank-truncating path run.
     be.lazy_reset()
     y = _engine.power_iterate(be, comm, atil, omega, spec.q, spec.stabilized, rows_total,
-                              lazy=True)
+                              lazy=True, gram=gram if streamed is not None else None)
     # A~ is released before the final orthonormalisation (C5 on one GPU: A
     # 128 GiB + A~ 31 GiB leave no room for Q); the rare eager rerun below
     # sketches again

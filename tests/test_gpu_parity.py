@@ -477,6 +477,37 @@ def test_streamed_upload_matches_device_input(skp, monkeypatch, dtype):
         skp.rsvd(a, spec)
 
 
+def test_streamed_upload_forms_gram_behind_the_copy(skp, monkeypatch):
+    """Host input on the sketch-space path: G = A~^T A~ is accumulated block by
+    block behind the H2D copy (each block its own fp16 split); same sigma /
+    error as the device-resident call (G summed in a different order: 1e-5)."""
+    from paper_2605_09755_b200 import _convert, _ops
+    monkeypatch.setattr(_convert.Streamed, "BLOCK_BYTES", 1 << 22)   # 128 blocks
+    calls = []
+    real = _ops.syrk_h3
+
+    def spy(*a, **k):
+        if not k.get("rows", False):       # G = A~^T A~ (not the CholeskyQR Grams)
+            calls.append(k.get("beta", 0.0))
+        return real(*a, **k)
+
+    monkeypatch.setattr(_ops, "syrk_h3", spy)
+    m, n = 65536, 2048
+    spec_v = np.exp(-np.arange(1.0, 801.0) / 150.0)
+    a_dev = datagen.lowrank_plus_noise_gpu(m, n, spec_v, 1e-6, seed=8)
+    host = a_dev.cpu().pin_memory()
+    spec = skp.RangeFinderSpec(k=80, l=600, r1=600, r2=100, q=2, eps=0.5, seed=8, s=8)
+    res_h, rel_h = skp.rsvd(host, spec, with_error=True)
+    assert len(calls) == 128 and calls.count(1.0) == 127               # one per block
+    calls.clear()
+    res_d, rel_d = skp.rsvd(a_dev, spec, with_error=True)
+    assert len(calls) == 1                                              # one SYRK of A~
+    s_h = np.asarray(res_h.sigma)[:80]
+    s_d = res_d.sigma.cpu().numpy()[:80]
+    np.testing.assert_allclose(s_h, s_d, rtol=1e-5)
+    assert abs(rel_h - rel_d) <= 1e-4 * rel_d
+
+
 def test_planes_power_iteration_matches_fp32_path(skp, monkeypatch):
     """Large enough for the 3xFP16 planes path (A~ split, products emitting
     fp16 planes of their transposes): same sigma / error as the fp32 3xTF32
