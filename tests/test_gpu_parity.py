@@ -477,6 +477,36 @@ def test_streamed_upload_matches_device_input(skp, monkeypatch, dtype):
         skp.rsvd(a, spec)
 
 
+@pytest.mark.parametrize("path", ["sketch-space", "products"])
+def test_wide_dynamic_range_on_the_planes_path(skp, monkeypatch, path):
+    """the 3xFP16 planes carry one power-of-two exponent
+    per matrix, so entries below ~2^-18 max|X| lose bits.  Rows scaled over 6
+    decades and columns over 3 (entries spanning ~9 decades) through the
+    benchmarked rsvd() on both power paths: sigma within 1e-5 and the exact
+    residual within 1e-3 of the oracle on the same bytes."""
+    from paper_2605_09755_b200 import _ops
+    if path == "products":
+        monkeypatch.setattr(_ops.CudaBackend, "gram_ok", lambda self, *a_, **k_: False)
+    m, n = 16384, 2048
+    base = datagen.lowrank_plus_noise_gpu(m, n, np.exp(-np.arange(1.0, 401.0) / 80.0), 1e-6,
+                                          seed=9)
+    rs = torch.logspace(0, -6, m, device="cuda", dtype=torch.float64)
+    cs = torch.logspace(0, -3, n, device="cuda", dtype=torch.float64)
+    a_dev = (base.double() * rs[:, None] * cs[None, :]).float().contiguous()
+    a = a_dev.cpu().numpy()
+    spec = skp.RangeFinderSpec(k=60, l=600, r1=600, r2=100, q=2, eps=0.5, seed=9, s=8)
+    ospec = o.Spec(k=60, l=600, r1=600, r2=100, q=2, seed=9, s=8)
+    qo = o.range_finder_sketched(a, ospec)
+    _, so, _ = o.randsvd(a, qo)
+    eo = o.proj_rel_error(a, qo)
+    res, _ = skp.rsvd(a_dev, spec, with_error=True)
+    np.testing.assert_allclose(res.sigma.cpu().numpy()[:60], so[:60], rtol=SIG_TOL[np.float32])
+    u = res.U.double()
+    a64 = a_dev.double()
+    exact = float(torch.linalg.norm(a64 - u @ (u.T @ a64)) / torch.linalg.norm(a64))
+    assert abs(exact - eo) <= ERR_TOL * eo, (exact, eo)
+
+
 def test_streamed_upload_forms_gram_behind_the_copy(skp, monkeypatch):
     """Host input on the sketch-space path: G = A~^T A~ is accumulated block by
     block behind the H2D copy (each block its own fp16 split); same sigma /
