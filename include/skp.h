@@ -260,7 +260,7 @@ int skp_cast2d_f64_f32(const double* x, int64_t ldx, float* y, int64_t ldy, int6
  * product (3xTF32: 2^-20).  B_lo = NULL: two products (A_lo B_hi + A_hi B_hi),
  * i.e. B rounded to fp16 (2^-12), A kept to 22 bits -- for the power
  * iteration, whose products only need to preserve the span.
- * ws: skp_gemm_h3_ws_bytes (split-K partials; 0 = none needed).            */
+ * ws: skp_gemm_h3_ws_bytes (wave-pacing slots, then split-K partials).     */
 int skp_split_h2_f32(const float* X, int64_t rows, int64_t cols, int64_t ld, int32_t trans,
                      void* hi, void* lo, int64_t ldh, int32_t* e_io, int32_t have_amax,
                      void* stream);
@@ -286,12 +286,15 @@ int skp_gemm_h3(int transA, int64_t M, int64_t N, int64_t K, float alpha, const 
  * products feed the next product without an fp32 round trip or split pass.
  * b_lower = 1: B (stored N x K) is lower triangular (Q = Y L^-T with L^-1
  * from the Cholesky kernel), so each N tile stops at its own K extent --
- * half the MMAs of the dense product.                                       */
+ * half the MMAs of the dense product.  ws (may be NULL): skp_gemm_h3_ws_bytes
+ * -- its head holds the wave-pacing slots (the N tiles of an M block stay in
+ * step so A is read ~once per wave).                                        */
 int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, float alpha, const void* A_hi,
                        const void* A_lo, int64_t lda, const int32_t* a_exp, const void* B_hi,
                        const void* B_lo, int64_t ldb, const int32_t* b_exp, void* Ct_hi,
                        void* Ct_lo, int64_t ldct, int32_t shift, int32_t fixed, int32_t e_fixed,
-                       int32_t* e_out, int32_t* overflow, int32_t b_lower, void* stream);
+                       int32_t* e_out, int32_t* overflow, int32_t b_lower, void* ws,
+                       int64_t ws_bytes, void* stream);
 
 /* skp_syrk_h3: C = alpha A^T A (N x N, fp32, exactly symmetric) from the
  * pre-split planes of A stored K x N (kmajor = 0, lda % 64 == 0, both GEMM

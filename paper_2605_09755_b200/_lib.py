@@ -71,7 +71,8 @@ SIGNATURES = {
     "skp_gemm_h3": (_int, [_int, _i64, _i64, _i64, _f32, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
                            _f32, _vp, _i64, _vp, _i64, _vp]),
     "skp_gemm_h3_emit_t": (_int, [_int, _i64, _i64, _i64, _f32, _vp, _vp, _i64, _vp, _vp, _vp, _i64,
-                                  _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _vp]),
+                                  _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _i64,
+                                  _vp]),
     "skp_gesvj_ws_bytes": (_i64, [_i64, _i64]),
     "skp_gesvj_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _i64, _vp,
                              _vp]),

@@ -410,11 +410,13 @@ def gemm_h3_emit_t(a: SplitH2, b: SplitH2, ta: bool = False, shift: int | None =
         buf = torch.empty((2, N, ld), dtype=torch.float16, device=a.hi.device)
         out = SplitH2(buf[0], buf[1], torch.zeros(2, dtype=torch.int32, device=a.hi.device),
                       N, M, ld)
+    wsb = int(_lib.load().skp_gemm_h3_ws_bytes(int(ta), M, N, K))
+    ws = workspace(a.hi.device, wsb) if wsb else None
     call("skp_gemm_h3_emit_t", int(ta), M, N, K, alpha, ptr(a.hi), ptr(a.lo), a.ld, ptr(a.e),
          ptr(b.hi), ptr(b.lo) if b_lo else None, b.ld, ptr(b.e), ptr(out.hi), ptr(out.lo), out.ld,
          int(shift),
          int(e_fixed is not None), int(e_fixed or 0), ptr(out.e), ptr(overflow), int(b_lower),
-         stream_ptr(a.hi.device))
+         ptr(ws), wsb, stream_ptr(a.hi.device))
     return out
 
 

@@ -1179,11 +1179,18 @@ HPlan hs_plan(int64_t M, int64_t N, int64_t K, int64_t ws_cap_elems, bool pair) 
 }
 }  // namespace
 
+constexpr int64_t kPaceBytes = 1024;  // pacing slots (<= 256 CTAs) at the head of ws
+constexpr int kPaceKb = 32;            // K blocks a producer may lead its wave by (SYRK;
+constexpr int kPaceKbS = 64;           // K4s, whose wave reads ~1 MB per K block, 64)
+constexpr int kPaceMinKb = 512;        // units shorter than this are not paced
+constexpr int kPaceKbProd = 16;        // the products' units (K = l ~ 125 K blocks)
+constexpr int kPaceMinKbProd = 32;
+
 int64_t gemm_h3_ws_bytes(int ta, int64_t M, int64_t N, int64_t K) {
     (void)ta;
     if (!h_init()) return 0;
     const HPlan pl = h_plan(M, N, K, INT64_MAX, h_pair(M));
-    return pl.splits > 1 ? (int64_t)pl.splits * M * N * 4 : 0;
+    return kPaceBytes + (pl.splits > 1 ? (int64_t)pl.splits * M * N * 4 : 0);
 }
 
 struct H3Emit {
@@ -1218,9 +1225,13 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
         return SKP_ERR_UNSUPPORTED;
     }
     const bool pair = h_pair(M);
-    const int64_t cap = (ws && !emit) ? ws_bytes / 4 : 0;  // emit: no split-K partials
+    // ws: [pacing slots | split-K partials]
+    unsigned* prog = (ws && ws_bytes >= kPaceBytes) ? reinterpret_cast<unsigned*>(ws) : nullptr;
+    void* wsp = prog ? reinterpret_cast<char*>(ws) + kPaceBytes : ws;
+    const int64_t wsp_bytes = prog ? ws_bytes - kPaceBytes : ws_bytes;
+    const int64_t cap = (wsp && !emit) ? wsp_bytes / 4 : 0;  // emit: no split-K partials
     HPlan pl = h_plan(M, N, K, cap, pair, b_lo);
-    if (pl.splits > 1 && (!ws || emit || (int64_t)pl.splits * M * N * 4 > ws_bytes))
+    if (pl.splits > 1 && (!wsp || emit || (int64_t)pl.splits * M * N * 4 > wsp_bytes))
         pl = h_plan(M, N, K, 0, pair, b_lo);
     H3Params p;
     p.b_lo = b_lo ? 1 : 0;
@@ -1232,10 +1243,14 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
     p.sym = 0;
     p.sym_tiles = 0;
     p.tri_k = 0;
-    p.prog = nullptr;
-    p.pace = 0;
+    // pacing: the N tiles of one M block read the same A rows; many waves of
+    // units each holding ~100 MB of A in flight (C5's Y = A~ W: 12 M blocks x
+    // 8 MB per wave) thrash the L2 (ncu: A~ read 4.7x) unless they move in step
+    p.prog = prog;
+    p.pace = (prog && pl.kb_per_split >= kPaceMinKbProd) ? kPaceKbProd : 0;
+    if (p.pace) SKP_CUDA(cudaMemsetAsync(prog, 0, kPaceBytes, st));
     p.alpha = alpha; p.beta = beta; p.C = C; p.ldc = ldc;
-    p.ws = pl.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
+    p.ws = pl.splits > 1 ? reinterpret_cast<float*>(wsp) : nullptr;
     p.stages = pl.stages; p.a_bytes = pl.a_bytes; p.b_bytes = pl.b_bytes;
     p.stage_bytes = pl.stage_bytes; p.acc_stride = pl.acc_stride;
     p.a_e = a_e; p.b_e = b_e;
@@ -1302,10 +1317,6 @@ int gemm_h3_impl(int ta, int64_t M, int64_t N, int64_t K, float alpha, const voi
     return SKP_OK;
 }
 
-constexpr int64_t kPaceBytes = 1024;  // pacing slots (<= 256 CTAs) at the head of ws
-constexpr int kPaceKb = 32;            // K blocks a producer may lead its wave by (SYRK;
-constexpr int kPaceKbS = 64;           // K4s, whose wave reads ~1 MB per K block, 64)
-constexpr int kPaceMinKb = 512;        // units shorter than this are not paced
 
 // split-K slices for the SYRK: enough units for every CTA pair, and at
 // least 64 K blocks (4 promotion chunks) per slice
@@ -1749,8 +1760,8 @@ extern "C" int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, f
                                   const int32_t* a_exp, const void* B_hi, const void* B_lo,
                                   int64_t ldb, const int32_t* b_exp, void* Ct_hi, void* Ct_lo,
                                   int64_t ldct, int32_t shift, int32_t fixed, int32_t e_fixed,
-                                  int32_t* e_out, int32_t* overflow, int32_t b_lower,
-                                  void* stream) {
+                                  int32_t* e_out, int32_t* overflow, int32_t b_lower, void* ws,
+                                  int64_t ws_bytes, void* stream) {
     SKP_ARG(M >= 0 && N >= 0 && K >= 0, "gemm_h3_emit_t: negative size");
     SKP_ARG(transA == 0 || transA == 1, "gemm_h3_emit_t: transA must be 0/1");
     SKP_ARG(lda >= (transA ? M : K) && lda >= 1, "gemm_h3_emit_t: lda too small");
@@ -1760,7 +1771,7 @@ extern "C" int skp_gemm_h3_emit_t(int transA, int64_t M, int64_t N, int64_t K, f
             "gemm_h3_emit_t: null pointer");
     H3Emit em{Ct_hi, Ct_lo, ldct, shift, fixed, e_fixed, e_out, overflow, b_lower ? 1 : 0};
     return gemm_h3_impl(transA, M, N, K, alpha, A_hi, A_lo, lda, a_exp, B_hi, B_lo, ldb, b_exp,
-                        0.f, nullptr, 0, nullptr, 0, &em, SKP_STREAM(stream));
+                        0.f, nullptr, 0, ws, ws_bytes, &em, SKP_STREAM(stream));
 }
 
 extern "C" int skp_split_h2_inplace_f32(float* X, int64_t rows, int64_t cols, int64_t ld,
