@@ -16,6 +16,9 @@ int gemm_dmma(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, con
               int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
               void* ws, int64_t ws_bytes, cudaStream_t st);
 int64_t gemm_dmma_ws_bytes(int64_t M, int64_t N, int64_t K);
+int gram_dmma_f32(const float* X, int64_t K, int64_t C, int64_t ldx, double* G, int64_t ldg,
+                  void* ws, int64_t ws_bytes, cudaStream_t st);
+int64_t gram_dmma_ws_bytes(int64_t K, int64_t C);
 
 // tcgen05 3xTF32 path (gemm_tc.cu).  Returns SKP_ERR_UNSUPPORTED when the
 // shape/layout is outside what the kernel handles (caller falls back).

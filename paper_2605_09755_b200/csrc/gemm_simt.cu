@@ -163,111 +163,17 @@ template int gemm_simt<double>(int, int, int64_t, int64_t, int64_t, double, cons
 
 // ---- G = X^T X in fp64 from fp32 X (randsvd's B B^T via B^T) ----------------
 // fp32 x fp32 products are exact in fp64, so the fp64 Gram of fp32 data needs
-// no widened copy: X is read as fp32 (half the bytes) and converted in
-// registers.  128x128 output tiles, 8x8 per thread, lower-triangular tiles
-// only (the upper ones are mirrored), split-K partials reduced in a fixed
-// order (deterministic).
-namespace skp {
-namespace {
-
-constexpr int GT = 128, GBK = 16, GTHREADS = 256;
-
-__global__ void __launch_bounds__(GTHREADS)
-gram_f32_f64_kernel(const float* __restrict__ X, int64_t K, int64_t C, int64_t ldx,
-                    int64_t kchunk, int ntile, double* __restrict__ part) {
-    __shared__ float As[GBK][GT + 4];
-    __shared__ float Bs[GBK][GT + 4];
-    // lower-triangular tile (I, J), I >= J
-    int t = blockIdx.x, I = 0;
-    while (t > I) { t -= I + 1; ++I; }
-    const int J = t;
-    const int64_t i0 = (int64_t)I * GT, j0 = (int64_t)J * GT;
-    const int64_t kb = (int64_t)blockIdx.y * kchunk;
-    const int64_t ke = kb + kchunk < K ? kb + kchunk : K;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[8][8];
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
-    for (int64_t k0 = kb; k0 < ke; k0 += GBK) {
-        // 16 x 128 of each column block: 2048 floats, 8 per thread
-#pragma unroll
-        for (int q = 0; q < (GBK * GT) / GTHREADS; ++q) {
-            const int idx = threadIdx.x + q * GTHREADS;
-            const int kk = idx / GT, cc = idx % GT;
-            const int64_t gk = k0 + kk;
-            As[kk][cc] = (gk < ke && i0 + cc < C) ? X[gk * ldx + i0 + cc] : 0.f;
-            Bs[kk][cc] = (gk < ke && j0 + cc < C) ? X[gk * ldx + j0 + cc] : 0.f;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < GBK; ++kk) {
-            double a[8], b[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) a[u] = (double)As[kk][ty + 16 * u];
-#pragma unroll
-            for (int v = 0; v < 8; ++v) b[v] = (double)Bs[kk][tx + 16 * v];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-#pragma unroll
-                for (int v = 0; v < 8; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
-        }
-        __syncthreads();
-    }
-    double* P = part + ((int64_t)blockIdx.y * ntile + blockIdx.x) * GT * GT;
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int v = 0; v < 8; ++v) P[(ty + 16 * u) * GT + tx + 16 * v] = acc[u][v];
-}
-
-__global__ void gram_reduce_kernel(const double* __restrict__ part, int splits, int ntile,
-                                   int64_t C, double* __restrict__ G, int64_t ldg) {
-    const int tile = blockIdx.x;
-    int t = tile, I = 0;
-    while (t > I) { t -= I + 1; ++I; }
-    const int J = t;
-    for (int e = threadIdx.x; e < GT * GT; e += blockDim.x) {
-        const int r = e / GT, c = e % GT;
-        const int64_t gi = (int64_t)I * GT + r, gj = (int64_t)J * GT + c;
-        if (gi >= C || gj >= C) continue;
-        double s = 0.0;
-        for (int z = 0; z < splits; ++z) s += part[((int64_t)z * ntile + tile) * GT * GT + e];
-        G[gi * ldg + gj] = s;
-        if (I != J) G[gj * ldg + gi] = s;   // mirror
-    }
-}
-
-}  // namespace
-}  // namespace skp
-
+// no widened copy: gemm_dmma.cu widens X as it stages the tiles and
+// accumulates on the DMMA tensor cores (lower tiles only, mirrored; split-K
+// partials reduced in a fixed order).
 using namespace skp;
-
-static int gram_splits(int64_t K, int64_t C) {
-    const int nb = (int)cdiv(C, (int64_t)GT);
-    const int ntile = nb * (nb + 1) / 2;
-    int s = (int)std::max<int64_t>(1, std::min<int64_t>(64, (2 * 148 + ntile - 1) / ntile));
-    while (s > 1 && cdiv(K, (int64_t)s) < 4 * GBK) --s;
-    return s;
-}
 extern "C" int64_t skp_gram_f32_f64_ws_bytes(int64_t K, int64_t C) {
-    const int nb = (int)cdiv(C, (int64_t)GT);
-    return (int64_t)gram_splits(K, C) * nb * (nb + 1) / 2 * GT * GT * (int64_t)sizeof(double);
+    return skp::gram_dmma_ws_bytes(K, C);
 }
 extern "C" int skp_gram_f32_f64(const float* X, int64_t K, int64_t C, int64_t ldx, double* G,
                                 int64_t ldg, void* ws, int64_t ws_bytes, void* stream) {
     SKP_ARG(K >= 1 && C >= 1 && ldx >= C && ldg >= C, "gram_f32_f64: bad sizes");
-    SKP_ARG(ws && ws_bytes >= skp_gram_f32_f64_ws_bytes(K, C), "gram_f32_f64: workspace too small");
-    cudaStream_t st = SKP_STREAM(stream);
-    const int nb = (int)cdiv(C, (int64_t)GT);
-    const int ntile = nb * (nb + 1) / 2;
-    const int splits = gram_splits(K, C);
-    const int64_t kchunk = cdiv(cdiv(K, (int64_t)splits), (int64_t)GBK) * GBK;
-    double* part = reinterpret_cast<double*>(ws);
-    gram_f32_f64_kernel<<<dim3(ntile, splits), GTHREADS, 0, st>>>(X, K, C, ldx, kchunk, ntile, part);
-    SKP_LAUNCHED(gram_f32_f64_kernel);
-    gram_reduce_kernel<<<ntile, 256, 0, st>>>(part, splits, ntile, C, G, ldg);
-    SKP_LAUNCHED(gram_reduce_kernel);
-    return SKP_OK;
+    SKP_ARG(ws_bytes >= skp_gram_f32_f64_ws_bytes(K, C) && (ws || ws_bytes == 0),
+            "gram_f32_f64: workspace too small");
+    return skp::gram_dmma_f32(X, K, C, ldx, G, ldg, ws, ws_bytes, SKP_STREAM(stream));
 }
