@@ -1184,7 +1184,7 @@ constexpr int kPaceKb = 32;            // K blocks a producer may lead its wave 
 constexpr int kPaceKbS = 64;           // K4s, whose wave reads ~1 MB per K block, 64)
 constexpr int kPaceMinKb = 512;        // units shorter than this are not paced
 constexpr int kPaceKbProd = 16;        // the products' units (K = l ~ 125 K blocks)
-constexpr int kPaceMinKbProd = 32;
+constexpr int kPaceMinKbProd = 64;
 
 int64_t gemm_h3_ws_bytes(int ta, int64_t M, int64_t N, int64_t K) {
     (void)ta;
