@@ -213,9 +213,15 @@ def host_threads():
 
 
 # --------------------------------------------------------------- the arm ----
+_TRAFFIC_WORLD = [1]
+
+
 def _traffic(config: str, key: str):
     """DRAM bytes per launch of a kernel at a config, from the committed ncu
-    --set full capture (profiles/traffic.json, scripts/summarize_ncu.py)."""
+    --set full capture (profiles/traffic.json, scripts/summarize_ncu.py) --
+    single-GPU captures, so only for 1-rank runs."""
+    if _TRAFFIC_WORLD[0] != 1:
+        return None, None
     try:
         with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
             tr = json.load(fh)
@@ -251,6 +257,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     device = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(device)
     comm = D.TorchComm() if world > 1 else _LocalComm()
+    _TRAFFIC_WORLD[0] = world
     m, n = cfg["m"], cfg["n"]
     row0, rows = D.shard_rows(m, world, rank)
     a = make_input(cfg, row0, rows, device)
