@@ -707,7 +707,11 @@ split_h2_t_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64
 // slot), 6-9 epilogue.  TMEM: [accumulator | A slots of 64 columns: 32 hi |
 // 32 lo].  A value that does not fit fp16 after scaling sets *overflow (the
 // caller then recomputes with 3xTF32).
-constexpr int kSWarpTma = 0, kSWarpMma = 1, kSWarpAx = 2, kSWarpEpi = 6, kSNumEpi = 8;
+// 8 split warps: two per TMEM lane quadrant, each converting half of the
+// stage's 64 K rows (with 4, the split of stage s+1 did not finish within
+// stage s's MMAs: tensor pipe 77% active at C5)
+constexpr int kSWarpTma = 0, kSWarpMma = 1, kSWarpAx = 2, kSNumXf = 8,
+              kSWarpEpi = kSWarpAx + kSNumXf, kSNumEpi = 8;
 constexpr int kSThreads = 32 * (kSWarpEpi + kSNumEpi);
 constexpr int kSEpiCols = 6;                     // 16-column groups per epilogue thread
 constexpr int kSMaxBn = 2 * 16 * kSEpiCols;      // 192
@@ -800,7 +804,7 @@ gemm_h3s_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     const int ustart = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     const int ustride = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     constexpr int kRowsPerUnit = kPair ? 2 * HM : HM;
-    constexpr int kNumXf = 4;
+    constexpr int kNumXf = kSNumXf;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -922,8 +926,10 @@ gemm_h3s_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             }
         }
     } else if (warp >= kSWarpAx && warp < kSWarpEpi) {
-        // split: thread = tile row (TMEM lane); lane quadrant = warp % 4 = box chunk
+        // split: thread = tile row (TMEM lane); lane quadrant = warp % 4 = box
+        // chunk; the two warps of a quadrant take K rows 0..31 and 32..63
         const int q = warp & 3;
+        const int half = (warp - kSWarpAx) >> 2;
         const uint32_t tlane = (uint32_t)(q * 32) << 16;
         const float sa = ldexpf(1.f, __ldg(p.a_e));
         float amax = 0.f;
@@ -942,8 +948,7 @@ gemm_h3s_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                 const uint32_t cb = smem0 + (uint32_t)s * p.stage_bytes +
                                     (uint32_t)q * kSChunkBytes + (uint32_t)lane * 4u;
                 const uint32_t ta = tmem_base + tlane + acol0 + kSSlotCols * (uint32_t)t;
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {  // K 0..31 | 32..63
+                {
                     uint32_t hi[16], lo[16];
 #pragma unroll
                     for (int k2 = 0; k2 < 16; ++k2) {
