@@ -344,6 +344,14 @@ int skp_srht_apply_f64(const double* X, int64_t fibres, int64_t n, int64_t x_fs,
                        const int8_t* signs, int64_t n_pad, const int32_t* subset, int64_t r,
                        double scale, double* out, int64_t o_fs, int64_t o_es, void* stream);
 
+/* In-place column un-permutation X[i, perm[v]] = X[i, v] (v < cols): the
+ * K2 v2 output A S P back in the reference's column order, so that
+ * apply_right (sketching.py:158-174) runs on the row gather.  cols <= 25600
+ * (fp32) / 17066 (fp64); perm = the first `cols` int32 of a gather plan.      */
+int skp_unpermute_cols_f32(float* X, int64_t rows, int64_t cols, int64_t ldx, const int32_t* perm,
+                           void* stream);
+int skp_unpermute_cols_f64(double* X, int64_t rows, int64_t cols, int64_t ldx,
+                           const int32_t* perm, void* stream);
 /* Row gather y[v, :] = x[perm[v], :], v < rows (P^T Omega for the K2 v2
  * column permutation; perm = the first `rows` int32 of a gather plan).       */
 int skp_permute_rows_f32(const float* x, int64_t ldx, const int32_t* perm, float* y, int64_t ldy,

@@ -93,6 +93,8 @@ SIGNATURES = {
                                   _i64, _i64, _vp]),
     "skp_gram_f32_f64_ws_bytes": (_i64, [_i64, _i64]),
     "skp_gram_f32_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "skp_unpermute_cols_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
+    "skp_unpermute_cols_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
     "skp_permute_rows_f32": (_int, [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp]),
     "skp_permute_rows_f64": (_int, [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp]),
     "skp_cast2d_f32_f64": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),

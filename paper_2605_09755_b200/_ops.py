@@ -245,6 +245,18 @@ def sym_check(x: torch.Tensor) -> torch.Tensor:
     return out
 
 
+UNPERMUTE_MAX_COLS = 25600   # skp_unpermute_cols_f32's shared-memory row
+
+
+def unpermute_cols(x: torch.Tensor, perm_dev: torch.Tensor) -> torch.Tensor:
+    """In place: x[:, perm_dev[v]] = x[:, v] (the K2 v2 output back in the
+    natural column order).  Returns x."""
+    rows, cols, ldx = _rows_ld(x)
+    call(f"skp_unpermute_cols_{_SFX[x.dtype]}", ptr(x), rows, cols, ldx, ptr(perm_dev),
+         stream_ptr(x.device))
+    return x
+
+
 def permute_rows(x: torch.Tensor, perm_dev: torch.Tensor, out=None) -> torch.Tensor:
     """out[v, :] = x[perm_dev[v], :] for v < x.shape[0] (perm_dev: int32 on the device)."""
     rows, cols, ldx = _rows_ld(x)

@@ -655,6 +655,27 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
     }
 }
 
+// apply_right in the reference's column order: X[i, perm[v]] = X[i, v] in
+// place (X = the permuted A S P written by the gather).  One CTA holds the
+// inverse permutation and one row in shared memory: coalesced row read,
+// coalesced permuted write.  HBM-bound (2 x rows x cols words).
+template <typename T>
+__global__ void __launch_bounds__(512)
+unpermute_cols_kernel(T* __restrict__ X, int64_t rows, int cols, int64_t ldx,
+                      const int32_t* __restrict__ perm) {
+    extern __shared__ __align__(16) unsigned char usm[];
+    int32_t* inv = reinterpret_cast<int32_t*>(usm);
+    T* row = reinterpret_cast<T*>(usm + ((size_t)cols * 4 + 15) / 16 * 16);
+    for (int v = threadIdx.x; v < cols; v += blockDim.x) inv[perm[v]] = v;
+    for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
+        __syncthreads();  // inv built / the previous row written out
+        T* x = X + i * ldx;
+        for (int v = threadIdx.x; v < cols; v += blockDim.x) row[v] = x[v];
+        __syncthreads();
+        for (int c = threadIdx.x; c < cols; c += blockDim.x) x[c] = row[inv[c]];
+    }
+}
+
 }  // namespace
 
 // plan layout (bytes): perm int32[P*kGCols] | fail int32 | pad to 16 |
@@ -781,6 +802,28 @@ int sketch_gather(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
     return SKP_OK;
 }
 
+template <typename T>
+int unpermute_cols(T* X, int64_t rows, int64_t cols, int64_t ldx, const int32_t* perm,
+                   cudaStream_t st) {
+    SKP_ARG(rows >= 0 && cols >= 0 && ldx >= cols && (cols == 0 || perm), "unpermute_cols: bad sizes");
+    const size_t smem = ((size_t)cols * 4 + 15) / 16 * 16 + (size_t)cols * sizeof(T);
+    if (smem > 200 * 1024) {
+        set_error("unsupported: unpermute_cols needs cols <= %d", (int)(200 * 1024 / (4 + sizeof(T))));
+        return SKP_ERR_UNSUPPORTED;
+    }
+    if (!rows || !cols) return SKP_OK;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    SKP_CUDA(cudaFuncSetAttribute(unpermute_cols_kernel<T>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int per_sm = std::max(1, std::min(4, (int)(220 * 1024 / smem)));
+    const int64_t grid = std::min<int64_t>(rows, (int64_t)sms * per_sm);
+    unpermute_cols_kernel<T><<<(unsigned)grid, 512, smem, st>>>(X, rows, (int)cols, ldx, perm);
+    SKP_LAUNCHED(unpermute_cols_kernel);
+    return SKP_OK;
+}
+
 }  // namespace skp
 
 using namespace skp;
@@ -808,4 +851,12 @@ extern "C" int skp_sketch_gather_f32_acc64(const float* A, int64_t lda, int64_t 
                                            void* stream) {
     return sketch_gather<double>(A, lda, m, n, r, plan, scale, out, ldo, fro2, nonfinite, nullptr,
                                  (cudaStream_t)stream);
+}
+extern "C" int skp_unpermute_cols_f32(float* X, int64_t rows, int64_t cols, int64_t ldx,
+                                      const int32_t* perm, void* stream) {
+    return unpermute_cols<float>(X, rows, cols, ldx, perm, (cudaStream_t)stream);
+}
+extern "C" int skp_unpermute_cols_f64(double* X, int64_t rows, int64_t cols, int64_t ldx,
+                                      const int32_t* perm, void* stream) {
+    return unpermute_cols<double>(X, rows, cols, ldx, perm, (cudaStream_t)stream);
 }

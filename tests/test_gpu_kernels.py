@@ -158,6 +158,11 @@ def test_sketch_fused_norm_and_nonfinite(skp, ops):
         fro2 = torch.zeros(1, dtype=torch.float64, device="cuda")
         bad = torch.zeros(1, dtype=torch.int64, device="cuda")
         op.right(t, fro2=fro2, nonfinite=bad)
+        # K2 v1 counts the 2 non-finite inputs, the row gather (fp32, aligned
+        # rows) the s outputs each of them reaches: a counter read as a flag
+        assert int(bad.item()) >= 2
+        bad.zero_()
+        ops.sketch_right(t, op.colptr, op.entries, op.s, op.r, nonfinite=bad)
         assert int(bad.item()) == 2
         with pytest.raises(ValueError, match="non-finite"):
             op.apply_right(a)
@@ -205,6 +210,33 @@ def test_sketch_gather_permuted(skp, ops, m, n, r, s):
     bad.zero_()
     op.right_permuted(t, nonfinite=bad)
     assert int(bad.item()) >= 1
+
+
+@pytest.mark.parametrize("m,n,r,s", [(67, 16384, 4000, 8), (9, 32768, 4000, 8), (3, 70001, 6000, 4),
+                                     (130, 512, 64, 1), (1000, 8192, 768, 8)])
+def test_right_natural_order_on_the_gather(skp, ops, m, n, r, s):
+    """SketchOperator.right (apply_right's device op) in the reference's column
+    order through K2 v2 + the in-place column un-permutation -- fused checks
+    kept, a caller-provided out honoured -- against the oracle."""
+    rng = np.random.default_rng(m * 7 + n)
+    op = skp.make_sketch("countsketch", n, r, seed=23, s=s)
+    a = rng.standard_normal((m, n)).astype(np.float32)
+    t = ops.empty2d(m, n, torch.float32, "cuda")
+    t.copy_(torch.from_numpy(a))
+    fro2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = ops.empty2d(m, r, torch.float32, "cuda")
+    got = op.right(t, out=out, fro2=fro2, nonfinite=bad)
+    assert got.data_ptr() == out.data_ptr()
+    assert op.gather_plan() is not None          # the row gather ran (v1 has no plan)
+    ref = o.CountSketch("countsketch", n, r, 23, s=s).apply_right(a.astype(np.float64))
+    scale = np.abs(ref).max()
+    assert np.abs(got.cpu().numpy() - ref).max() <= 4e-7 * np.sqrt(n * s / r) * scale + 1e-30
+    assert int(bad.item()) == 0
+    want = float((a.astype(np.float64) ** 2).sum())
+    assert abs(fro2.item() - want) <= 1e-12 * want
+    # the reference API on top of it
+    assert np.abs(op.apply_right(a) - ref).max() <= 4e-7 * np.sqrt(n * s / r) * scale + 1e-30
 
 
 @pytest.mark.parametrize("m,n,r,s", [(67, 16384, 4000, 8), (9, 32768, 4000, 8), (5, 65536, 4096, 8)])
