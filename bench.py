@@ -445,12 +445,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "dtype": cfg["dtype"] + (" (products 3xFP16 on tcgen05 kind::f16, fp64 small cores)" if h3
                                  else " (3xTF32 tcgen05)" if tc and f32 else ""),
         "data": "synthetic (seeded, BASELINE config recipe; random-init factors, no dataset)",
-        "config": {"workload": args.config, "m": m, "n": n, "l": l, "s": s_,
-                   "k": cfg["k"], "r2": r2, "q": cfg["q"],
-                   "parallelism": f"rows sharded x{world} (NCCL allreduce of " + (
-                       "the l x l G once" if gram_path else "l x r2 per power step") +
-                       ", r2 x r2 Grams, r2 x n B^T)",
-                   "l2": "no flush: A is far larger than the 126 MB L2"},
+        "config": workload_config(args.config, cfg, world),
         "phases_ms": {k: round(v, 3) for k, v in phases.items()},
         "rel_err": rel, "sigma_1": float(sig[0].item()),
         "roofline": roof, **extra,
@@ -737,15 +732,25 @@ def run_nystrom(args, cfg, rank, world, local_rank):
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32 K; sketch accumulated in fp64, core in fp64 (DMMA), as the reference",
         "data": "synthetic (seeded RBF points, BASELINE config recipe)",
-        "config": {"workload": args.config, "n": n, "l": l, "s": s_, "k": cfg["k"],
-                   "r2": cfg["r2"], "q": cfg["q"], "bandwidth_h": round(h, 6),
-                   "parallelism": f"rows of K sharded x{world} (NCCL allreduce of the l x l W~)",
-                   "l2": "no flush: K (17.2 GB) is far larger than the 126 MB L2"},
+        "config": workload_config(args.config, cfg, world), "rbf_bandwidth_h": round(h, 6),
         "nystrom_rel_err": rel, "roofline": roof, "sketch": dict(roof), **extra,
         "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e,
     }
     return line, None
 
+
+
+def workload_config(name: str, cfg: dict, world: int) -> dict:
+    """The `config` object of both arms (ours and --impl reference): the
+    workload's shape and the descriptive keys, identical for the two."""
+    if cfg.get("nystrom"):
+        return {"workload": name, **{k: cfg[k] for k in ("n", "l", "s", "k", "r2", "q")},
+                "parallelism": f"rows of K sharded x{world} (NCCL allreduce of the l x l W~)",
+                "l2": "no flush: K (17.2 GB) is far larger than the 126 MB L2"}
+    return {"workload": name, **{k: cfg[k] for k in ("m", "n", "l", "s", "k", "r2", "q")},
+            "parallelism": f"rows sharded x{world} (NCCL allreduces: the l x l G once or "
+                           "l x r2 per power step, r2 x r2 Grams, r2 x n B^T)",
+            "l2": "no flush: A is far larger than the 126 MB L2"}
 
 
 def run_reference(args, cfg):
@@ -776,8 +781,7 @@ def run_reference(args, cfg):
         "ms_per_step": round(val, 1), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64 (numpy/scipy, as the reference computes)",
         "data": "synthetic (the workload's own first rows: same generator, spectrum, noise)",
-        "config": {"workload": args.config, **{k: cfg[k] for k in
-                                               ("m", "n", "l", "s", "k", "r2", "q")}},
+        "config": workload_config(args.config, cfg, args.gpus),
         "cpu_baseline": {"value": round(val, 1), "unit": "ms", "cores": ncores, "kind": "port",
                          "sample": f"rows 0..{det['rows_sampled']} of the {cfg['m']}-row workload, "
                                    f"m-linear phases extrapolated x{cfg['m'] / det['rows_sampled']:g}"
@@ -805,7 +809,7 @@ def run_reference_nystrom(args, cfg, ncores):
         "ms_per_step": round(val, 1), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64 (numpy/scipy, as the reference computes)",
         "data": "synthetic (seeded RBF points, BASELINE config recipe)",
-        "config": {"workload": args.config, **{k: cfg[k] for k in ("n", "l", "s", "k", "r2", "q")}},
+        "config": workload_config(args.config, cfg, args.gpus),
         "cpu_baseline": {"value": round(val, 1), "unit": "ms", "cores": ncores, "kind": "port",
                          **det},
         "e2e": {"value": round(val, 1), "unit": "ms", "h2d_bytes_per_step": 0,
