@@ -762,7 +762,13 @@ class CudaBackend:
         failed factorisation only sets self.fail.  Returns Y^T planes.
         g: this rank's G already formed (block by block behind a streamed
         upload), else one SYRK of atil here."""
-        g = comm.allreduce_(g if g is not None else syrk_h3(atil))
+        wt = self.power_gram_steps(comm, g if g is not None else syrk_h3(atil), omega, q, shift)
+        return gemm_h3_emit_t(atil, wt)                      # (A~ W)^T
+
+    def power_gram_steps(self, comm, g, omega, q: int, shift: float) -> SplitH2:
+        """power_gram's q l-dimensional steps from this rank's G (consumed):
+        the planes of W^T, Y = A~ W."""
+        g = comm.allreduce_(g)
         gs = split_h2(g)
         del g
         # the blocks are re-split from fp32 every step (fresh exponents): an
@@ -778,7 +784,7 @@ class CudaBackend:
             x = self.chol_inv64(mg, 0.0, lazy=True, shift=shift)
             wt = split_h2(gemm_h3(vt, split_h2(self.to_compute(x)), ta=True), trans=True,
                           out=wt)                            # W = V X^T
-        return gemm_h3_emit_t(atil, wt)                      # (A~ W)^T
+        return wt
 
     def orth_planes(self, comm, yt: SplitH2, t2: float, shift: float, planes_out: bool = False):
         """Lazy shifted CholeskyQR3 of Y given as Y^T planes (_engine.orthonormalize):

@@ -199,6 +199,10 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     # only P^T waits for the plan (in line instead, alternating A/B at C3,
     # scripts/ab_omega.sh: 63.5 vs 63.1 ms per step)
     om_side = _omega_side(spec, om_seed, a.dtype, dev, nonfinite) if om_job is None else None
+    if _atil_blocked(a, spec, be, sk):
+        return _range_finder_blocked(a, spec, comm, rows_total, ph, fro2, name, streamed,
+                                     hint_out, planes_out, be, sk, nonfinite, om_side, om_job,
+                                     om_seed)
     ph.mark("make_sketch", "apply_right")
     # K2 v2 writes A~ with its columns permuted (A S P); the power iteration
     # then uses P^T Omega, so Y = (A S P)(P^T Omega) = A S Omega exactly as in
@@ -302,6 +306,100 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     if hint_out is not None and e_io is not None and not plan_failed:
         # for randsvd's in-kernel fp16 split of a: max|a| <~ sqrt(s) max|a S|
         # (a lone large entry lands in s outputs scaled 1/sqrt(s)); 2x slack
+        hint_out["amax"] = (e_io, int(math.ceil(math.log2(2.0 * math.sqrt(spec.s or 1)))) + 1)
+    return qb
+
+
+def _atil_blocked(a: torch.Tensor, spec: RangeFinderSpec, be, sk) -> bool:
+    """Does A~ (rows x l fp32) fail to fit next to A?  Then the range finder
+    runs blocked (_range_finder_blocked): C5 at l = 16000 on one B200 (A 128
+    GiB + A~ 62.5 GiB > 178 GiB).  The estimate is the resident path's peak
+    beyond A: A~ (split in place), Y^T planes and Y, the l x l Gram and its
+    planes, 2 GiB of slack -- from the caching allocator's own counters (no
+    device sync)."""
+    if (a.dtype != F32 or sk.kind != "countsketch" or not spec.stabilized or spec.q < 1
+            or not hasattr(be, "power_gram_steps") or a.stride(1) != 1
+            or (a.stride(0) * 4) % 16 or a.data_ptr() % 16):
+        return False
+    m, ld, ldr = a.shape[0], -(-spec.r1 // 32) * 32, -(-spec.r2 // 32) * 32
+    need = m * ld * 4 + 2 * m * ldr * 4 + 3 * ld * ld * 4 + (2 << 30)
+    free = _ops._device_total(a.device) - torch.cuda.memory_allocated(a.device)
+    return need > free
+
+
+_BLOCK_BYTES = 2 << 30   # A~ row block of the blocked range finder (fp32)
+
+
+def _range_finder_blocked(a, spec, comm, rows_total, ph, fro2, name, streamed, hint_out,
+                          planes_out, be, sk, nonfinite, om_side, om_job, om_seed):
+    """Alg. 1 when A~ does not fit beside A: the sketch-space power iteration
+    with A~ formed in row blocks twice -- pass 1 sketches each block (K2 v2),
+    splits it and accumulates G = A~^T A~ (SYRK, beta = 1; behind a streamed
+    upload, block by block as it lands); the q steps run in the l-dimensional
+    space as in the resident path; pass 2 sketches each block again and forms
+    its rows of Y = A~ W.  Only an A~ block, G (l x l) and Y (rows x r2) are
+    ever resident.  The rare eager fallbacks (a sketch plan or device Omega
+    that failed, a rank-deficient CholeskyQR) need A~ resident and raise."""
+    dev = a.device
+    m_loc = a.shape[0]
+    l, r2 = spec.r1, spec.r2
+    ld = -(-l // 32) * 32
+    blk = int(max(1024, min(m_loc, _BLOCK_BYTES // (ld * 4))))
+    e_io = torch.zeros(2, dtype=torch.int32, device=dev)
+    buf = _ops.empty2d(blk, l, F32, dev)
+    gram = _ops.empty2d(l, l, F32, dev)
+
+    def ranges(src_blocks):
+        for r0, r1 in src_blocks:
+            for s0 in range(r0, r1, blk):
+                yield s0, min(r1, s0 + blk)
+
+    ph.mark("make_sketch", "apply_right")
+    perm, first = None, True
+    src = streamed.blocks() if streamed is not None else [(0, m_loc)]
+    for r0, r1 in ranges(src):
+        got = sk.right_permuted(a[r0:r1], out=buf[:r1 - r0], fro2=fro2, nonfinite=nonfinite,
+                                deferred=True, amax=e_io[1:])
+        if got is None:
+            raise RuntimeError("internal: the blocked range finder needs the row gather (K2 v2)")
+        perm = got[1]
+        _ops.syrk_h3(_ops.split_h2(buf[:r1 - r0]), out=gram, beta=0.0 if first else 1.0)
+        first = False
+    ph.mark("apply_right", "omega")
+    if om_side is not None:
+        torch.cuda.current_stream(dev).wait_event(om_side[1])
+        omega = _ops.permute_rows(om_side[0], perm)
+    elif om_job is None:
+        omega = omega_device(spec.omega_kind, l, r2, om_seed, a.dtype, dev, perm, nonfinite)
+    else:
+        omega = om_job.to_device(dev, perm)
+    ph.mark("omega", "power")
+    bad = comm.allreduce_(nonfinite)
+    be.lazy_reset()
+    wt = be.power_gram_steps(comm, gram, omega, spec.q, _engine.SHIFT_REL[_engine._dtype_key(be)])
+    del gram, omega
+    y = _ops.empty2d(m_loc, r2, F32, dev)
+    scratch = torch.zeros(1, dtype=torch.int64, device=dev)
+    for r0, r1 in ranges([(0, m_loc)]):
+        sk.right_permuted(a[r0:r1], out=buf[:r1 - r0], nonfinite=scratch, deferred=True)
+        _ops.gemm_h3(_ops.split_h2(buf[:r1 - r0]), wt, out=y[r0:r1])     # A~_b W
+    del buf, wt
+    yt = _ops.split_h2(y, trans=True)
+    del y
+    ph.mark("power", "orth")
+    qb = _engine.orthonormalize(be, comm, yt, rows_total=rows_total, lazy=True,
+                                planes_out=planes_out)
+    del yt
+    ph.mark("orth")
+    nbad = int(bad.item())
+    if nbad % _ops.GATHER_PLAN_FAIL_MARK:
+        raise ValueError(f"{name} contains non-finite entries")
+    if nbad >= _ops.GATHER_PLAN_FAIL_MARK or be.lazy_failed(comm):
+        raise RuntimeError(
+            "the blocked range finder (A~ does not fit beside A on this device) has no eager "
+            "fallback: the sketch plan or device Omega failed, or Y is numerically rank-deficient; "
+            "shard A over more GPUs so that A~ stays resident")
+    if hint_out is not None:
         hint_out["amax"] = (e_io, int(math.ceil(math.log2(2.0 * math.sqrt(spec.s or 1)))) + 1)
     return qb
 

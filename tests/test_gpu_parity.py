@@ -186,6 +186,48 @@ def test_reduced_configs_vs_live_oracle(skp, name, m, n, l, r2, k, q, rank, deca
 @pytest.mark.parametrize("name,m,n,l,r2,k,q,rank,decay", [
     ("C3-structure", 16384, 4096, 1000, 120, 100, 3, 2048, "poly"),
     ("C5-structure", 32768, 2048, 1000, 210, 200, 2, 1024, "exp"),
+])
+def test_blocked_range_finder_vs_live_oracle(skp, monkeypatch, name, m, n, l, r2, k, q, rank,
+                                             decay):
+    """The blocked range finder (A~ formed twice in row blocks when it does
+    not fit beside A: C5 at l = 16000 on one GPU), forced here with ~1000-row
+    blocks: resident input, the streamed upload (numpy) and rsvd_sharded, each
+    against the live oracle on the same bytes -- sigma 1e-5, rel_err 1e-3."""
+    from paper_2605_09755_b200 import _engine, power, distributed as D
+    spec_v = np.arange(1.0, rank + 1.0) ** -0.5 if decay == "poly" else np.exp(-np.arange(1.0, rank + 1.0) / 200.0)
+    a_dev = datagen.lowrank_plus_noise_gpu(m, n, spec_v, 1e-6 if decay == "poly" else 1e-8, seed=3)
+    a = a_dev.cpu().numpy()
+    spec = skp.RangeFinderSpec(k=k, l=l, r1=l, r2=r2, q=q, eps=0.5, seed=3, s=8)
+    ospec = o.Spec(k=k, l=l, r1=l, r2=r2, q=q, seed=3, s=8)
+    qo = o.range_finder_sketched(a, ospec)
+    _, so, _ = o.randsvd(a, qo)
+    eo = o.proj_rel_error(a, qo)
+    calls = []
+    real = power._range_finder_blocked
+
+    def spy(*args, **kw):
+        calls.append(1)
+        return real(*args, **kw)
+    monkeypatch.setattr(power, "_atil_blocked", lambda *x: True)
+    monkeypatch.setattr(power, "_range_finder_blocked", spy)
+    monkeypatch.setattr(power, "_BLOCK_BYTES", 1000 * l * 4)
+    qb = skp.range_finder_sketched(a_dev, spec)
+    res = skp.randsvd(a_dev, qb)
+    np.testing.assert_allclose(res.sigma.cpu().numpy()[:k], so[:k], rtol=SIG_TOL[np.float32])
+    e = _rel_err(a, qb.cpu().numpy())
+    assert abs(e - eo) <= ERR_TOL * eo, (e, eo)
+    res_b, rel_b = skp.rsvd(a, spec, with_error=True)          # streamed upload
+    np.testing.assert_allclose(res_b.sigma[:k], so[:k], rtol=SIG_TOL[np.float32])
+    assert abs(rel_b - eo) <= ERR_TOL * eo, (rel_b, eo)
+    _, s_d, _, rel_d = D.rsvd_sharded(a_dev, spec, m, _engine.LOCAL, with_error=True)
+    np.testing.assert_allclose(s_d.cpu().numpy()[:k], so[:k], rtol=SIG_TOL[np.float32])
+    assert abs(rel_d - eo) <= ERR_TOL * eo, (rel_d, eo)
+    assert len(calls) == 3
+
+
+@pytest.mark.parametrize("name,m,n,l,r2,k,q,rank,decay", [
+    ("C3-structure", 16384, 4096, 1000, 120, 100, 3, 2048, "poly"),
+    ("C5-structure", 32768, 2048, 1000, 210, 200, 2, 1024, "exp"),
     ("graded", 16384, 2048, 500, 80, 60, 2, 400, "graded"),
 ])
 def test_sketch_space_power_matches_products(skp, monkeypatch, name, m, n, l, r2, k, q, rank,
