@@ -348,6 +348,11 @@ class SplitH2:
         self.hi, self.lo, self.e, self.rows, self.cols, self.ld = hi, lo, e, rows, cols, ld
 
 
+def gram_pays(l: int, r2: int, q: int) -> bool:
+    """The sketch-space power iteration's cost rule (CudaBackend.gram_ok)."""
+    return l <= q * r2 * (4.4 + 1.5 * r2 / l)
+
+
 def split_h2(x: torch.Tensor, trans: bool = False, out: "SplitH2 | None" = None,
              e_io: torch.Tensor | None = None) -> SplitH2:
     """e_io (int32[2]): e_io[1] already holds max|x|'s bits (e.g. the sketch
@@ -732,20 +737,24 @@ class CudaBackend:
         """gram_ok's decision from the shapes alone (before A~ exists: the
         streamed upload accumulates G block by block behind the copy)."""
         return (self.dtype == F32 and self.gemm_mode == "auto" and q >= 1
-                and rows * l >= H3_MIN_ELEMS and l <= 3.6 * q * r2 and rows >= 2 * l
+                and rows * l >= H3_MIN_ELEMS and gram_pays(l, r2, q) and rows >= 2 * l
                 and bool(_lib.load().skp_has_tcgen05()))
 
     def gram_ok(self, atil, omega, q: int) -> bool:
         """Run the power iteration in the sketch space (power_gram)?  It costs
         one SYRK (m l^2 useful MACs, tiles of the lower triangle) plus one
-        product (m l r2) against the 1 + 2q products of m l r2 each: taken
-        when l <= 3.6 q r2 (the SYRK's 256 x 128 tiles run ~10% below the
-        products' 256 x 176), and when the rows outnumber the sketch columns
-        (the l x l work of the q steps is replicated on every rank)."""
+        product (m l r2) against the 1 + 2q products of m l r2 each and the q
+        CholeskyQR passes between them (~1.5 m r2^2 each): taken when
+        l <= q r2 (4.4 + 1.5 r2 / l) -- the SYRK's flops run ~10% faster than
+        the products' (C5: 0.79 vs 0.72 of the pipe; the measured l x q sweep,
+        profiles/r02w_c5_sweep.txt: l = 8000, q = 2 took 262 ms on the products
+        against ~215 in the sketch space) -- and when the rows outnumber the
+        sketch columns (the l x l work of the q steps is replicated on every
+        rank)."""
         if not self.planes_ok(atil, omega) or q < 1:
             return False
         m, l, r2 = atil.rows, atil.cols, omega.shape[1]
-        return l <= 3.6 * q * r2 and m >= 2 * l and atil.ld % 64 == 0
+        return gram_pays(l, r2, q) and m >= 2 * l and atil.ld % 64 == 0
 
     def power_gram(self, comm, atil: SplitH2, omega, q: int, shift: float, g=None):
         """The stabilized power iteration (power.py:113-134) in the sketch

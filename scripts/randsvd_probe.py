@@ -1,4 +1,4 @@
-"""Where randsvd's time goes at C3: CUDA events around each backend call of
+"""Where the step's time goes (python scripts/randsvd_probe.py [C3|C5]): CUDA events around each backend call of
 _engine.randsvd / _randsvd_core (one GPU, resident input)."""
 import sys
 import time
@@ -34,10 +34,11 @@ def wrap(name):
 
 for nm in ("mm_at_big", "gram64_rows_t", "eig_desc64", "sqrt_eigs", "mm", "scale_cols_",
            "to_compute", "cols", "overflowed", "chol_inv64", "gram64", "orth_planes",
-           "power_lazy_planes", "prepare", "gram64_planes"):
+           "power_lazy_planes", "prepare", "gram64_planes", "gram64_q", "orth_dev_t",
+           "power_gram", "power_gram_steps", "eig_orth64", "planes_to_compute", "dense"):
     if hasattr(_ops.CudaBackend, nm):
         wrap(nm)
-cfg = dict(bench.CONFIGS["C3"])
+cfg = dict(bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C3"])
 spec = bench.spec_of(cfg, 3)
 a = bench.make_input(cfg, 0, cfg["m"], torch.device("cuda", 0))
 for _ in range(3):
