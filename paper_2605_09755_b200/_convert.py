@@ -52,14 +52,36 @@ def upload(a, name: str = "matrix", device=None, dtype=None, check_finite: bool 
         raise ValueError(f"{name} must be 2-D, got ndim={t.dim()}")
     if t.numel() == 0:
         raise ValueError(f"{name} must be non-empty")
-    if t.device != dev or t.dtype != want:
-        t = t.to(device=dev, dtype=want, non_blocking=True)
-    if t.stride(1) != 1 or t.stride(0) < t.shape[1]:
-        t = t.contiguous()
+    if not t.is_cuda:
+        # host operands land in 128-byte rows (_ops.empty2d): the TMA / tcgen05
+        # paths (K2 v2's row copies, randsvd's in-kernel split of A) need them,
+        # and an unaligned n would otherwise fall back to slower kernels
+        if t.dtype != want:
+            t = t.to(dtype=want)
+        dst = _ops.empty2d(t.shape[0], t.shape[1], want, dev)
+        dst.copy_(t, non_blocking=t.is_pinned())
+        t = dst
+    else:
+        if t.device != dev or t.dtype != want:
+            t = t.to(device=dev, dtype=want, non_blocking=True)
+        per = 128 // t.element_size()
+        if t.stride(1) != 1 or t.stride(0) < t.shape[1] or (
+                t.stride(0) % per and _aligned_copy_fits(t)):
+            # a device operand with unaligned rows: one padded copy (when it
+            # fits) instead of the fallback kernels for every product
+            dst = _ops.empty2d(t.shape[0], t.shape[1], t.dtype, dev)
+            dst.copy_(t)
+            t = dst
     op = Operand(t, kind, name)
     if check_finite:
         ensure_finite(op)
     return op
+
+
+def _aligned_copy_fits(t: torch.Tensor) -> bool:
+    """Room for a padded copy of t (allocator counters, no device sync)."""
+    need = 2 * t.shape[0] * (t.shape[1] + 32) * t.element_size() + (1 << 30)
+    return _ops._device_total(t.device) - torch.cuda.memory_allocated(t.device) >= need
 
 
 class Streamed:

@@ -581,9 +581,14 @@ class CudaBackend:
         K, M = a.shape
         self.overflow.zero_()
         if (self.dtype != F32 or self.gemm_mode != "auto" or a.shape[0] * a.shape[1] < H3_MIN_ELEMS
-                or a.stride(1) != 1 or a.stride(0) % 32 or a.data_ptr() % 16
                 or not _lib.load().skp_has_tcgen05()):
             return self.mm(a, self.dense(q), ta=True)
+        if a.stride(1) != 1 or a.stride(0) % 32 or a.data_ptr() % 16:
+            # a device operand with unaligned rows that had no room for a padded
+            # copy (_convert.upload): the round-to-nearest SIMT kernel -- the
+            # 3xTF32 tensor-core chain over K = rows truncates (sigma 2.3e-5
+            # low at K = 65536, scripts/unaligned_probe.py)
+            return gemm(a, self.dense(q), ta=True, mode="fp32")
         if amax_hint is not None:
             e_a = amax_hint[0].clone()
             h2_exponent(a, e_a, have_amax=True, margin_bits=amax_hint[1])

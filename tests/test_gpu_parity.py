@@ -134,6 +134,26 @@ def test_c2_drop_in_pair_reuses_device_copy(skp, c2_ref, c2):
     np.testing.assert_array_equal(qb, qb2)
 
 
+@pytest.mark.parametrize("n", [4001, 4004])
+def test_unaligned_width_host_input_vs_live_oracle(skp, n):
+    """A numpy input whose rows are not 128-byte multiples through the
+    reference's own two calls.  The upload pads the rows, so randsvd's Q^T A
+    runs the 3xFP16 kernel with promoted accumulation.  Before: n = 4004
+    (16-byte rows) took the 3xTF32 tensor-core fallback, whose long-K chain
+    truncates (sigma 2.3e-5 off at m = 65536, past the 1e-5 bar), and n = 4001
+    the SIMT kernel at half the speed (scripts/unaligned_probe.py)."""
+    m, l, r2, k = 65536, 600, 80, 60
+    spec_v = np.exp(-np.arange(1.0, 513.0) / 60.0)
+    a = datagen.lowrank_plus_noise_gpu(m, n, spec_v, 1e-8, seed=9).cpu().numpy()
+    spec = skp.RangeFinderSpec(k=k, l=l, r1=l, r2=r2, q=2, eps=0.5, seed=9, s=8)
+    qb = skp.range_finder_sketched(a, spec)
+    res = skp.randsvd(a, qb)
+    ospec = o.Spec(k=k, l=l, r1=l, r2=r2, q=2, seed=9, s=8)
+    qo = o.range_finder_sketched(a, ospec)
+    _, so, _ = o.randsvd(a, qo)
+    np.testing.assert_allclose(res.sigma[:k], so[:k], rtol=SIG_TOL[np.float32])
+
+
 def test_rank_kept_on_polydecay_fp32(skp):
     """the fp32 range finder must keep the directions the
     reference's pivoted QR keeps (gen_polydecay spectrum max(m,n)/i,
