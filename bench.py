@@ -180,7 +180,7 @@ def cpu_baseline(cfg, sample_rows: int, reps: int = 1, slab=None):
     full = sum(v * (scale if k in linear else 1.0) for k, v in best.items())
     return full * 1e3, {"phases_s_sample": {k: round(v, 4) for k, v in best.items()},
                         "rows_sampled": rows, "extrapolated_to_m": m,
-                        "q_columns_kept": int(qb.shape[1])}, (a, qb, spec)
+                        "q_columns_kept": int(qb.shape[1]), "host": host_info()}, (a, qb, spec)
 
 
 def slab_parity(cfg, a, qb, spec_o):
@@ -210,6 +210,31 @@ def host_threads():
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count()
+
+
+def host_info() -> dict:
+    """The CPU baseline's host: cores, model and the
+    numpy / scipy / BLAS the oracle port runs on."""
+    import platform
+    import scipy
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg.get("Build Dependencies", {}).get("blas", {})
+        blas = f"{b.get('name')} {b.get('version')}".strip()
+    except Exception:
+        pass
+    return {"cpu_count": os.cpu_count(), "affinity": host_threads(), "cpu_model": model,
+            "numpy": np.__version__, "scipy": scipy.__version__, "blas": blas}
 
 
 # --------------------------------------------------------------- the arm ----
@@ -612,7 +637,8 @@ def cpu_baseline_nystrom(cfg, sub=NYS_SUB):
     det = {"phases_s_sample": {k: round(v, 4) for k, v in t.items()},
            "sample": f"leading {sub} x {sub} principal block of the {cfg['n']}-point RBF kernel; "
                      f"K S extrapolated x{f * f:g} (n^2), S^T C~ and C~ Y x{f:g} (n), the "
-                     "l-dimensional core not scaled; the reference's O(n^3) psd check not timed"}
+                     "l-dimensional core not scaled; the reference's O(n^3) psd check not timed",
+           "host": host_info()}
     del xs
     return full * 1e3, det, (kmat, spec, c, w)
 
