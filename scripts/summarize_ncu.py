@@ -45,7 +45,11 @@ def launches(path, out):
     for k, v in ks:
         agg[k][0] += 1
         agg[k][1] += v
-    ours = {k: v for k, v in agg.items() if "skp::" in k}
+    # (with --kernel-name-base demangled ncu prints "void unnamed>::..." for
+    # the kernels of libskp's anonymous namespace)
+    def mine(k):
+        return "skp::" in k or k.startswith("void unnamed>::") or k.startswith("unnamed>::")
+    ours = {k: v for k, v in agg.items() if mine(k)}
     tot = sum(v[1] for v in ours.values())
     with open(out, "w") as f:
         f.write(f"# launch list summary of {path}\n# (cold-cache, serialised: compare SHARES)\n")
@@ -53,7 +57,7 @@ def launches(path, out):
         f.write(f"{'ms':>10} {'share':>6} {'n':>5}  kernel\n")
         for k, v in sorted(ours.items(), key=lambda kv: -kv[1][1]):
             f.write(f"{v[1]/1e3:10.3f} {v[1]/tot*100:5.1f}% {v[0]:5d}  {k}\n")
-        other = {k: v for k, v in agg.items() if "skp::" not in k}
+        other = {k: v for k, v in agg.items() if not mine(k)}
         f.write("# non-libskp kernels (input generation by torch, not in the timed region)\n")
         for k, v in sorted(other.items(), key=lambda kv: -kv[1][1])[:10]:
             f.write(f"{v[1]/1e3:10.3f}        {v[0]:5d}  {k[:100]}\n")
