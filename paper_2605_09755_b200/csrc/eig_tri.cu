@@ -55,7 +55,8 @@ __device__ double block_reduce_sum_all(double v, double* scratch) {
 //   threads: no index division); sync.
 // smem: v[n], w[n] (dynamic).
 __global__ void __launch_bounds__(kTriThreads)
-sytrd_kernel(double* A, int n, double* d, double* e, double* tau, double* Hv, double* pbuf) {
+sytrd_kernel(double* A, int n, int i_end, double* d, double* e, double* tau, double* Hv,
+             double* pbuf) {
     extern __shared__ double tsm[];
     double* vs = tsm;         // v over rows r0.. (index t = row - r0)
     double* ws = tsm + n;     // w
@@ -64,7 +65,7 @@ sytrd_kernel(double* A, int n, double* d, double* e, double* tau, double* Hv, do
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int warp_g = (int)(gtid >> 5), lane = threadIdx.x & 31;
     const int nwarps_g = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-    for (int i = 0; i + 2 < n; ++i) {
+    for (int i = 0; i < i_end && i + 2 < n; ++i) {
         const int r0 = i + 1, k = n - r0;
         // (a) reflector from x = A[r0:, i] (untouched by this step's update)
         double ss = 0.0;
@@ -127,7 +128,7 @@ sytrd_kernel(double* A, int n, double* d, double* e, double* tau, double* Hv, do
         }
         grid.sync();
     }
-    if (gtid == 0) {
+    if (gtid == 0 && i_end >= n - 2) {  // (else the cluster kernel finishes the trailing block)
         if (n >= 2) {
             d[n - 2] = A[(int64_t)(n - 2) * n + n - 2];
             e[n - 2] = A[(int64_t)(n - 1) * n + n - 2];
@@ -192,8 +193,8 @@ __device__ __forceinline__ void cl_sync() {
 }
 
 __global__ void __launch_bounds__(kClThreads, 1)
-sytrd_cluster_kernel(const double* __restrict__ Ag, int n, int rpc, double* d, double* e,
-                     double* tau, double* Hv) {
+sytrd_cluster_kernel(const double* __restrict__ Ag, int lda, int n, int rpc, double* d,
+                     double* e, double* tau, double* Hv, int ldh) {
     extern __shared__ __align__(16) double csm[];
     uint32_t rank;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
@@ -229,7 +230,7 @@ sytrd_cluster_kernel(const double* __restrict__ Ag, int n, int rpc, double* d, d
     // load owned rows
     for (int lr = 0; lr < rpc; ++lr) {
         const int r = lr * kCl + (int)rank;
-        for (int c = tid; c < n; c += blockDim.x) Al[(size_t)lr * n + c] = r < n ? Ag[(int64_t)r * n + c] : 0.0;
+        for (int c = tid; c < n; c += blockDim.x) Al[(size_t)lr * n + c] = r < n ? Ag[(int64_t)r * lda + c] : 0.0;
     }
     cl_sync();  // every CTA's rows loaded and barriers armed
     const uint32_t xv_a = cl_smem(xv), pv_a = cl_smem(pvv), ssp_a = cl_smem(ssp), pvp_a = cl_smem(pvp);
@@ -282,7 +283,7 @@ sytrd_cluster_kernel(const double* __restrict__ Ag, int n, int rpc, double* d, d
                 tau[i] = t_;
             }
             for (int c = r0 + tid; c < n; c += blockDim.x)
-                Hv[(int64_t)i * n + c] = c == r0 ? 1.0 : xcol[c] * scal;
+                Hv[(int64_t)i * ldh + c] = c == r0 ? 1.0 : xcol[c] * scal;
         }
         if ((i % kCl) == (int)rank && tid == 0) d[i] = Al[(size_t)(i / kCl) * n + i];
         __syncthreads();
@@ -691,21 +692,27 @@ int syev_tri(const double* A, int64_t n, double* W, double* V, void* ws, int64_t
         return SKP_ERR_CUDA;
     }
     int nn = (int)n;
-    // whole matrix in a 16-CTA cluster's shared memory when it fits
-    bool clustered = false;
-    const size_t csm = sytrd_cluster_smem(nn);
-    if (csm <= 220 * 1024) {
+    // The trailing block of the reduction runs in a 16-CTA cluster's shared
+    // memory (DSMEM exchanges and mbarriers instead of grid syncs: ~2x faster
+    // per column): the whole matrix when it fits, else the grid kernel reduces
+    // the leading columns until the trailing block fits (C5's r2 = 1050: 410
+    // columns on the grid, the last 640 in the cluster).
+    int nc = 0;  // trailing block size for the cluster (0: none)
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    {
+        int cand = nn;
+        while (cand > 2 && sytrd_cluster_smem(cand) > 220 * 1024) --cand;
+        const size_t csm = sytrd_cluster_smem(cand);
         cudaError_t ea = cudaFuncSetAttribute(sytrd_cluster_kernel,
                                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaError_t eb = cudaFuncSetAttribute(sytrd_cluster_kernel,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-        if (ea == cudaSuccess && eb == cudaSuccess) {
-            cudaLaunchConfig_t cfg = {};
+        if (cand > 2 && ea == cudaSuccess && eb == cudaSuccess) {
             cfg.gridDim = dim3(kCl);
             cfg.blockDim = dim3(kClThreads);
             cfg.dynamicSmemBytes = csm;
             cfg.stream = st;
-            cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
             attr[0].val.clusterDim.x = kCl;
             attr[0].val.clusterDim.y = 1;
@@ -714,21 +721,25 @@ int syev_tri(const double* A, int64_t n, double* W, double* V, void* ws, int64_t
             cfg.numAttrs = 1;
             int ncl = 0;
             if (cudaOccupancyMaxActiveClusters(&ncl, sytrd_cluster_kernel, &cfg) == cudaSuccess &&
-                ncl >= 1) {
-                const int rpc = (nn + kCl - 1) / kCl;
-                SKP_CUDA(cudaLaunchKernelEx(&cfg, sytrd_cluster_kernel, (const double*)Ac, nn, rpc,
-                                            d, e, tau, Hv));
-                SKP_LAUNCHED(sytrd_cluster_kernel);
-                clustered = true;
-            }
+                ncl >= 1)
+                nc = cand;
         }
         cudaGetLastError();  // clear a refused attribute / occupancy query
     }
-    if (!clustered) {
-        void* args[] = {&Ac, &nn, &d, &e, &tau, &Hv, &pbuf};
+    const int i0 = nc ? nn - nc : nn;  // columns reduced by the grid kernel
+    if (i0 > 0) {
+        int iend = i0;
+        void* args[] = {&Ac, &nn, &iend, &d, &e, &tau, &Hv, &pbuf};
         SKP_CUDA(cudaLaunchCooperativeKernel((void*)sytrd_kernel, dim3(sms), dim3(kTriThreads), args,
                                              tsm, st));
         count_launch();
+    }
+    if (nc) {
+        const int rpc = (nc + kCl - 1) / kCl;
+        const int64_t off = (int64_t)i0 * nn + i0;
+        SKP_CUDA(cudaLaunchKernelEx(&cfg, sytrd_cluster_kernel, (const double*)(Ac + off), nn, nc,
+                                    rpc, d + i0, e + i0, tau + i0, Hv + off, nn));
+        SKP_LAUNCHED(sytrd_cluster_kernel);
     }
     const size_t bsm = 2 * (size_t)n * sizeof(double);
     SKP_CUDA(cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

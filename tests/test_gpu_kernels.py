@@ -605,7 +605,7 @@ def test_cholesky_reports_indefinite():
     assert int(info.item()) > 0
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 30, 111, 112, 113, 300, 520, 1050])
+@pytest.mark.parametrize("n", [1, 2, 3, 30, 111, 112, 113, 300, 520, 641, 700, 1050, 1500])
 def test_jacobi_eigensolver(n):
     from paper_2605_09755_b200._ops import CudaBackend
     rng = np.random.default_rng(n)
