@@ -59,3 +59,24 @@ def test_spec_validation_messages():
         skp.RangeFinderSpec(k=3, l=4, r1=10, r2=4, q=1, eps=0.7).validate(20, 20)
     assert skp.choose_q(0.5, 1) == 1
     assert skp.choose_q(0.1, 100) == 27
+
+
+def test_sketch_space_rule_on_the_configs():
+    """The power path each BASELINE config takes (CudaBackend.gram_ok's cost
+    rule; profiles/r02w_c5_sweep.txt measured the C5 cases)."""
+    from paper_2605_09755_b200._ops import gram_pays
+    assert gram_pays(4000, 520, 3)            # C3: sketch space
+    assert gram_pays(8000, 1050, 4)           # C5, the headline
+    assert gram_pays(8000, 1050, 2)           # C5 q = 2 (was the products: 747 vs 699 ms)
+    assert not gram_pays(8000, 1050, 1)       # C5 q = 1: three products are cheaper
+    assert gram_pays(4000, 1050, 1)           # C5 l = 4000, q = 1
+    assert not gram_pays(2000, 110, 3)        # C2: r2 small against l
+
+
+def test_bench_arms_share_the_config():
+    """Both bench arms print one config object (the driver compares them)."""
+    import bench
+    for name, cfg in bench.CONFIGS.items():
+        a = bench.workload_config(name, cfg, 2)
+        assert a == bench.workload_config(name, dict(cfg), 2)
+        assert a["workload"] == name and "l2" in a and "parallelism" in a
