@@ -91,6 +91,8 @@ def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: b
     t2 = _pass2_floor(be, f)
     g = comm.allreduce_(be.gram64(y))
     x1 = be.chol_inv64(g, 0.0, lazy=lazy, shift=SHIFT_REL[key])
+    if passes == 3 and hasattr(be, "save_pivots"):
+        be.save_pivots(c)      # Y's pivot range (see CudaBackend.piv)
     if x1 is None:
         # G is indefinite beyond the shift (all-zero or degenerate input):
         # truncate on G's own spectrum, dropping what lies under the shift
@@ -136,6 +138,10 @@ def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_t
     the 3xFP16 GEMM on the CUDA backend).  gram: G = A~^T A~ already formed
     for the sketch-space path (streamed uploads accumulate it per block)."""
     atil = be.prepare(atil)
+    # the power of A~'s spectrum in Y's: 1 for Y = A~ Omega (q = 0), else 2
+    # (both paths end with Y = A~ A~^T Q_prev, Q_prev orthonormal) -- read by
+    # the fp32 facade's promotion test on Y's pivot range
+    be.y_power = 1 if q == 0 else 2
     if lazy and stabilized and q > 0 and hasattr(be, "gram_ok") and be.gram_ok(atil, omega, q):
         return be.power_gram(comm, atil, omega, q, SHIFT_REL[_dtype_key(be)], g=gram)
     if lazy and stabilized and q > 0 and hasattr(be, "planes_ok") and be.planes_ok(atil, omega):
@@ -148,6 +154,9 @@ def power_iterate(be, comm, atil, omega, q: int, stabilized: bool = True, rows_t
         z = comm.allreduce_(be.mm(atil, y, ta=True))
         y = be.mm(atil, z)
     return y
+
+
+GRAM_SVD_FLOOR = 1.5e-3   # fp64 randsvd: below it, the SVD of B^T instead of eig(B B^T)
 
 
 def randsvd(be, comm, a, qb, check: bool = True, amax_hint=None, stats: dict | None = None):
@@ -211,8 +220,17 @@ def _randsvd_core(be, comm, bt, qb, gq=None, stats=None):
     w, v = be.eig_desc64(gb)
     p = min(c, n)
     sig, inv = be.sqrt_eigs(w)
-    vc = be.to_compute(be.cols(v, p))
     planes = hasattr(qb, "hi")          # Q given as the fp16 planes of Q^T
+    if (hasattr(be, "svd_cols") and _dtype_key(be) == "float64" and 1 < p == c
+            and float(sig[p - 1]) < GRAM_SVD_FLOOR * float(sig[0])):
+        # B B^T squares B's condition number: sigma_i below ~1.5e-3 sigma_1
+        # would miss the 1e-10 bar (eps (sigma_1 / sigma_i)^2); the one-sided
+        # Jacobi SVD of B^T itself keeps eps sigma_1 absolute (the reference's
+        # gesdd of B, linalg.py:84-88)
+        vb, s, ub = be.svd_cols(bt)     # B^T = Vb S Ub^T: B's left vectors Ub
+        u = be.mm(qb, be.to_compute(ub[:, :p]), ta=planes)
+        return u, s[:p], be.to_compute(vb[:, :p])
+    vc = be.to_compute(be.cols(v, p))
     u = be.mm(qb, vc, ta=planes)
     vv = be.mm(bt, vc)
     be.scale_cols_(vv, inv[:p])

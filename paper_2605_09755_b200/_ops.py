@@ -545,6 +545,11 @@ class CudaBackend:
         self.fail = torch.zeros(2, dtype=torch.int32, device=device)
         self._bsplit = {}
         self.overflow = torch.zeros(1, dtype=torch.int32, device=device)
+        # (min, max) Cholesky pivot of the last orthonormalisation's first,
+        # shifted pass: a lower bound of sigma_min(Y) / sigma_max(Y) (clipped
+        # by the shift) -- the facade promotes fp32 inputs whose spectrum the
+        # fp32 arithmetic cannot resolve (power._promote_range_finder)
+        self.piv = torch.ones(2, dtype=F64, device=device)
 
     # dense products in the compute dtype
     def mm(self, a, b, ta=False, tb=False, out=None, alpha=1.0, beta=0.0):
@@ -694,8 +699,28 @@ class CudaBackend:
             return None
         return x
 
+    def svd_cols(self, x):
+        """Thin SVD of x (rows >= cols) by the one-sided Jacobi kernel (K8),
+        fp64: (U, S, V) with x = U diag(S) V^T."""
+        return gesvj(x)
+
+    def save_pivots(self, n: int):
+        """Copy the last chol_inv64's pivot range (the 2 doubles the K5 kernel
+        leaves after its 4 np^2 workspace blocks, np = 32 ceil(n / 32)) into
+        self.piv: a device copy, read later with the other lazy checks."""
+        np_ = -(-n // 32) * 32
+        off = 4 * np_ * np_ * 8
+        ws = workspace(self.device, _lib.load().skp_cholinv_ws_bytes(n))
+        self.piv.copy_(ws.view(torch.uint8)[off:off + 16].view(F64))
+
+    def pivot_ratio(self) -> float:
+        """min / max pivot saved by save_pivots (host sync)."""
+        p = self.piv.cpu()
+        return float(p[0] / p[1]) if float(p[1]) > 0 else 1.0
+
     def lazy_reset(self):
         self.fail.zero_()
+        self.piv.fill_(1.0)
 
     def lazy_failed(self, comm=None) -> bool:
         """Any lazy failure (Cholesky pivot: fail[0], identical on every rank;
@@ -806,6 +831,7 @@ class CudaBackend:
         Returns Q (fp32, rows x c), or with planes_out the planes of Q^T (what
         randsvd consumes).  yt is consumed (its buffers are reused)."""
         x1 = self.chol_inv64(comm.allreduce_(self.gram64_planes(yt)), 0.0, lazy=True, shift=shift)
+        self.save_pivots(yt.rows)
         q1t = gemm_h3_emit_t(yt, split_h2(self.to_compute(x1)), ta=True, e_fixed=14,
                              overflow=self.fail[1:], b_lower=True)
         x2 = self.chol_inv64(comm.allreduce_(self.gram64_planes(q1t)), t2, lazy=True)

@@ -307,6 +307,8 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
         # for randsvd's in-kernel fp16 split of a: max|a| <~ sqrt(s) max|a S|
         # (a lone large entry lands in s outputs scaled 1/sqrt(s)); 2x slack
         hint_out["amax"] = (e_io, int(math.ceil(math.log2(2.0 * math.sqrt(spec.s or 1)))) + 1)
+    if hint_out is not None and hasattr(be, "pivot_ratio"):
+        hint_out["pivot_ratio"] = be.pivot_ratio() ** (1.0 / getattr(be, "y_power", 1))
     return qb
 
 
@@ -401,7 +403,44 @@ def _range_finder_blocked(a, spec, comm, rows_total, ph, fro2, name, streamed, h
             "shard A over more GPUs so that A~ stays resident")
     if hint_out is not None:
         hint_out["amax"] = (e_io, int(math.ceil(math.log2(2.0 * math.sqrt(spec.s or 1)))) + 1)
+        hint_out["pivot_ratio"] = be.pivot_ratio() ** 0.5   # (Y = A~ A~^T Q_prev: power 2)
     return qb
+
+
+# fp32 operands whose spectrum the fp32 arithmetic cannot resolve are
+# recomputed in fp64 -- the reference computes in fp64 for every input
+# (as_matrix, linalg.py:30-39).  The fp32 path keeps sigma within 1e-5 of it
+# while the returned sigma stay above ~1e-2 sigma_1 (3xFP16 products carry
+# ~2^-22 ||A|| ||Q||), and its CholeskyQR resolves Y's directions down to the
+# shift (~3e-3 sigma_1 after q >= 1 steps); below that the reference's
+# pivoted QR still keeps columns (tests/test_gpu_sweep.py found both).
+_PROMOTE_SIGMA_RATIO = 1e-2
+
+
+def _fp64_fits(a: torch.Tensor) -> bool:
+    """Room for an fp64 copy of a (plus the fp64 range finder's blocks)?"""
+    need = 2 * a.shape[0] * (a.shape[1] + 16) * 8 + (2 << 30)
+    return _ops._device_total(a.device) - torch.cuda.memory_allocated(a.device) >= need
+
+
+def _promote_range_finder(a: torch.Tensor, spec: RangeFinderSpec, qb, hint: dict,
+                          name: str = "a"):
+    """(a64, Q64) when the fp32 range finder met a spectrum it cannot resolve
+    -- its CholeskyQR truncated columns, or Y's first (shifted) pass saw pivots
+    below _PROMOTE_SIGMA_RATIO of the largest -- and an fp64 copy fits, else
+    None."""
+    if a.dtype != F32:
+        return None
+    ncols = qb.rows if isinstance(qb, _ops.SplitH2) else qb.shape[1]
+    wide = hint.get("pivot_ratio", 1.0) < _PROMOTE_SIGMA_RATIO
+    if (ncols >= min(spec.r2, a.shape[0], a.shape[1]) and not wide) or not _fp64_fits(a):
+        return None
+    a64 = _ops.cast(a, F64)
+    return a64, _range_finder_dev(a64, spec, name=name)
+
+
+def _sigma_too_wide(s: torch.Tensor) -> bool:
+    return s.numel() > 1 and float(s[-1]) < _PROMOTE_SIGMA_RATIO * float(s[0])
 
 
 def range_finder_sketched(a, spec: RangeFinderSpec, *, timings: dict | None = None, device=None):
@@ -410,7 +449,11 @@ def range_finder_sketched(a, spec: RangeFinderSpec, *, timings: dict | None = No
     m, n = op.t.shape
     spec.validate(m, n)
     ph = _Phases(timings is not None)
-    qb = _range_finder_dev(op.t, spec, phases=ph, streamed=streamed)
+    hint = {}
+    qb = _range_finder_dev(op.t, spec, phases=ph, streamed=streamed, hint_out=hint)
+    promoted = _promote_range_finder(op.t, spec, qb, hint)
+    if promoted is not None:
+        qb = promoted[1]
     if isinstance(a, _convert.DeviceMatrix):
         a.finite = True           # K2 counted every entry (none non-finite)
     ph.result(timings)
@@ -442,7 +485,12 @@ def randsvd(a, q_basis, *, timings: dict | None = None) -> SvdResult:
     dt = _convert.common_dtype(oa, oq)
     ph = _Phases(timings is not None)
     ph.mark("start", "randsvd")
-    u, s, v = _randsvd_dev(_convert.as_dtype(oa, dt), _convert.as_dtype(oq, dt))
+    at = _convert.as_dtype(oa, dt)
+    qt = _convert.as_dtype(oq, dt)
+    u, s, v = _randsvd_dev(at, qt)
+    if dt == F32 and _sigma_too_wide(s) and _fp64_fits(at):
+        # (Q passed the fp32 run's orthonormality check, at the fp32 tolerance)
+        u, s, v = _randsvd_dev(_ops.cast(at, F64), _ops.cast(qt, F64), check=False)
     ph.mark("randsvd")
     ph.result(timings)
     return SvdResult(_convert.download(u, oa.kind), _convert.download(s, oa.kind),
@@ -467,9 +515,18 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
                            planes_out=True)
     if isinstance(a, _convert.DeviceMatrix):
         a.finite = True
+    a_rs = op.t
+    promoted = _promote_range_finder(op.t, spec, qb, hint)
+    if promoted is not None:
+        a_rs, qb = promoted
+        hint = {}
     st = {}
     ph.begin("randsvd")
-    u, s, v = _randsvd_dev(op.t, qb, check=True, amax_hint=hint.get("amax"), stats=st)
+    u, s, v = _randsvd_dev(a_rs, qb, check=True, amax_hint=hint.get("amax"), stats=st)
+    if a_rs.dtype == F32 and _sigma_too_wide(s) and _fp64_fits(a_rs):
+        q32 = _ops.CudaBackend(a_rs.device, F32).dense(qb)
+        a_rs = _ops.cast(a_rs, F64)
+        u, s, v = _randsvd_dev(a_rs, _ops.cast(q32, F64), check=False, stats=st)
     ph.mark("randsvd")
     res = SvdResult(_convert.download(u, op.kind), _convert.download(s, op.kind),
                     _convert.download(v, op.kind))

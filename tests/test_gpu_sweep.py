@@ -1,0 +1,64 @@
+"""Seeded sweep of small, ragged configurations through the reference's own
+call sequence (range_finder_sketched, then randsvd) against the CPU oracle on
+the same bytes: odd m / n / l / r2, s in {1, 3, 8}, q in {0 .. 3}, fp32 and
+fp64, numpy and CUDA-tensor inputs.  Bar (BASELINE.json): sigma within 1e-10
+(fp64) / 1e-5 (fp32) relative over the top k, ||A - QQ^T A||_F / ||A||_F within
+1e-3 relative; Q keeps the reference's column count."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import skp_oracle as o
+
+pytestmark = pytest.mark.gpu
+
+SIG_TOL = {np.float64: 1e-10, np.float32: 1e-5}
+
+
+def _case(i):
+    rng = np.random.default_rng(1000 + i)
+    m = int(rng.integers(300, 5000))
+    n = int(rng.integers(100, 3000))
+    l = int(rng.integers(40, min(n, 700)))
+    r2 = int(rng.integers(8, max(9, min(l, 150))))
+    k = int(rng.integers(1, r2 + 1))
+    q = int(rng.integers(0, 4))
+    s = int(rng.choice([1, 3, 8]))
+    dtype = np.float64 if i % 3 == 0 else np.float32
+    cuda_in = i % 2 == 1
+    rank = int(rng.integers(r2 + 5, min(m, n) + 1)) if min(m, n) > r2 + 5 else min(m, n)
+    decay = float(rng.uniform(0.02, 0.2))
+    return m, n, l, r2, k, q, s, dtype, cuda_in, rank, decay
+
+
+def _matrix(m, n, rank, decay, seed, dtype):
+    rng = np.random.default_rng(seed)
+    u, _ = np.linalg.qr(rng.standard_normal((m, rank)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, rank)))
+    sv = np.exp(-decay * np.arange(rank))
+    return ((u * sv) @ v.T + 1e-7 * rng.standard_normal((m, n))).astype(dtype)
+
+
+@pytest.mark.parametrize("i", range(48))
+def test_random_small_configs_vs_oracle(i):
+    import paper_2605_09755_b200 as skp
+    m, n, l, r2, k, q, s, dtype, cuda_in, rank, decay = _case(i)
+    a = _matrix(m, n, rank, decay, i, dtype)
+    spec = skp.RangeFinderSpec(k=k, l=l, r1=l, r2=r2, q=q, eps=0.5, seed=i, s=s)
+    ospec = o.Spec(k=k, l=l, r1=l, r2=r2, q=q, seed=i, s=s)
+    qo = o.range_finder_sketched(a, ospec)
+    _, so, _ = o.randsvd(a, qo)
+    eo = o.proj_rel_error(a, qo)
+    x = torch.from_numpy(a).cuda() if cuda_in else a
+    qb = skp.range_finder_sketched(x, spec)
+    res = skp.randsvd(x, qb)
+    qn = qb.cpu().numpy() if cuda_in else qb
+    sig = res.sigma.cpu().numpy() if cuda_in else res.sigma
+    assert qn.shape[1] == qo.shape[1], (qn.shape, qo.shape)
+    kk = min(k, len(so))
+    np.testing.assert_allclose(sig[:kk], so[:kk], rtol=SIG_TOL[dtype],
+                               err_msg=f"case {_case(i)}")
+    a64 = a.astype(np.float64)
+    q64 = qn.astype(np.float64)
+    e = np.linalg.norm(a64 - q64 @ (q64.T @ a64)) / np.linalg.norm(a64)
+    assert abs(e - eo) <= 1e-3 * eo + 1e-12, (e, eo, _case(i))
