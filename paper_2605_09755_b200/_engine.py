@@ -65,6 +65,17 @@ def _pass2_floor(be, f: float) -> float:
     return min(1.0, f / SHIFT_REL[_dtype_key(be)] ** 0.5)
 
 
+def _svd_rank_basis(be, y, f: float):
+    """The reference's rank decision (linalg.py:57-81: keep |R_ii| >= f
+    max|R_ii|) on y's singular values from the one-sided Jacobi SVD (eps
+    sigma_1 absolute, no squaring); returns the leading left singular vectors."""
+    u, sv, _ = be.svd_cols(y)
+    k = int((sv > f * sv[0]).sum().item()) if float(sv[0]) > 0 else 0
+    if k == 0:
+        raise ValueError("cannot orthonormalize an all-zero matrix")
+    return be.to_compute(u[:, :k])
+
+
 def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: bool = False,
                    passes: int = 3, planes_out: bool = False):
     """Orthonormal basis of range(y), numerically rank-truncated (linalg.py:57-81),
@@ -89,10 +100,20 @@ def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: b
     key = _dtype_key(be)
     f = rank_floor(be, rows_total, c, tol)
     t2 = _pass2_floor(be, f)
+    y_in = y
+    # rank deficient in fp64 (eager): the Gram squares y's spectrum, so what
+    # the reference's pivoted QR keeps between its floor (max(m, c) eps) and
+    # ~sqrt(shift) -- an fp32 input's rounding noise on an exactly low-rank
+    # matrix, say -- lies under the shift (or breaks the shifted factor when
+    # max G_ii is far below ||G||): decide the rank on y's own singular values
+    svd_rank = (not lazy and key == "float64" and hasattr(be, "svd_cols")
+                and getattr(comm, "world", 1) == 1 and y.shape[0] >= c)
     g = comm.allreduce_(be.gram64(y))
     x1 = be.chol_inv64(g, 0.0, lazy=lazy, shift=SHIFT_REL[key])
     if passes == 3 and hasattr(be, "save_pivots"):
         be.save_pivots(c)      # Y's pivot range (see CudaBackend.piv)
+    if x1 is None and svd_rank:
+        return _svd_rank_basis(be, y_in, f)
     if x1 is None:
         # G is indefinite beyond the shift (all-zero or degenerate input):
         # truncate on G's own spectrum, dropping what lies under the shift
@@ -110,6 +131,8 @@ def orthonormalize(be, comm, y, tol=None, rows_total: int | None = None, lazy: b
         return q
     g2 = comm.allreduce_(be.gram64(q, accurate=True))
     x2 = be.chol_inv64(g2, t2, lazy=lazy)
+    if x2 is None and svd_rank:
+        return _svd_rank_basis(be, y_in, f)
     if x2 is None:
         # rank deficient: keep the directions of q whose pass-2 pivots clear
         # t2 (sigma_i(Y) >= f sigma_1(Y)), as the pivoted QR keeps |R_ii|

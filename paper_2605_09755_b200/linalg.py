@@ -59,10 +59,18 @@ def matmul(a, b):
 
 
 def orthonormalize(y, tol: float | None = None):
-    """Orthonormal basis for range(y), numerically rank-truncated (linalg.py:57-81)."""
+    """Orthonormal basis for range(y), numerically rank-truncated (linalg.py:57-81).
+
+    The reference's pivoted QR runs in fp64 for every input: an fp32 y whose
+    rank decision the fp32 CholeskyQR cuts short (it resolves ~2.8e-6 of
+    sigma_1, fp32 rounding noise included) is redone in fp64, so the column
+    count follows the reference (power._promote_range_finder's rule)."""
     op = _convert.upload(y, "y")
     be = _backend(op.t.dtype, op.t.device)
     q = _engine.orthonormalize(be, _engine.LOCAL, op.t, tol=tol)
+    if op.t.dtype == _ops.F32 and q.shape[1] < min(op.t.shape):
+        t64 = _ops.cast(op.t, _ops.F64)
+        q = _engine.orthonormalize(_backend(_ops.F64, op.t.device), _engine.LOCAL, t64, tol=tol)
     return _convert.download(q, op.kind)
 
 

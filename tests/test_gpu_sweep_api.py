@@ -1,0 +1,103 @@
+"""Seeded sweeps of the rest of the reference surface against the CPU oracle
+on the same bytes: orthonormalize (column count, span), thin_svd / pinv on
+graded and rank-deficient matrices, lowrank_factorize (the regression's
+error) and power_iterate (span).  fp32 and fp64, ragged shapes."""
+import numpy as np
+import pytest
+
+from oracle import skp_oracle as o
+
+pytestmark = pytest.mark.gpu
+
+
+def _graded(m, n, decades, rank, seed, dtype):
+    rng = np.random.default_rng(seed)
+    u, _ = np.linalg.qr(rng.standard_normal((m, rank)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, rank)))
+    return ((u * np.logspace(0, -decades, rank)) @ v.T).astype(dtype)
+
+
+def _proj_dist(q1, q2):
+    """|| Q1 Q1^T - Q2 Q2^T ||_2 (same-size orthonormal bases)."""
+    return float(np.linalg.norm(q1 @ (q1.T @ q2) - q2, 2)) if q1.shape == q2.shape else np.inf
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_orthonormalize_sweep(i):
+    import paper_2605_09755_b200 as skp
+    rng = np.random.default_rng(2000 + i)
+    m, c = int(rng.integers(50, 3000)), int(rng.integers(1, 120))
+    c = min(c, m)
+    rank = int(rng.integers(1, c + 1))
+    dtype = np.float64 if i % 2 else np.float32
+    decades = float(rng.uniform(0, 6 if dtype == np.float32 else 10))
+    y = _graded(m, c, decades, rank, i, dtype)
+    qo = o.orthonormalize(y)
+    qb = skp.orthonormalize(y)
+    assert np.abs(qb.T.astype(np.float64) @ qb - np.eye(qb.shape[1])).max() <= (
+        1e-5 if dtype == np.float32 else 1e-12)
+    # the reference's rank decision (fp32 inputs are decided in fp64, as the
+    # reference computes: their rounding noise counts as rank there too)
+    assert qb.shape[1] == qo.shape[1], (qb.shape, qo.shape, rank, decades)
+    if qb.shape[1] == rank or dtype == np.float64:
+        # same span, to the conditioning of y's kept part
+        tol = (1e-4 if dtype == np.float32 else 1e-13) * 10 ** decades
+        assert _proj_dist(qb.astype(np.float64), qo) <= tol
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_thin_svd_and_pinv_sweep(i):
+    import paper_2605_09755_b200 as skp
+    rng = np.random.default_rng(3000 + i)
+    m, n = int(rng.integers(2, 400)), int(rng.integers(2, 400))
+    rank = int(rng.integers(1, min(m, n) + 1))
+    a = _graded(m, n, float(rng.uniform(0, 12)), rank, i, np.float64)
+    uo, so, vo = o.thin_svd(a)
+    res = skp.thin_svd(a)
+    np.testing.assert_allclose(res.sigma, so, rtol=0, atol=1e-12 * so[0])
+    np.testing.assert_allclose((res.U * res.sigma) @ res.V.T, a, atol=1e-12 * so[0])
+    po, pg = o.pinv(a), skp.pinv(a)
+    # Moore-Penrose conditions to the accuracy of the kept singular values
+    # (entrywise the two pseudo-inverses agree only to eps sigma_1 / sigma_min,
+    # the accuracy of either SVD), and entrywise where that is tight
+    cut = so > max(m, n) * np.finfo(np.float64).eps * so[0]
+    kappa = so[0] / so[cut][-1]
+    assert np.linalg.norm(a @ pg @ a - a) <= 1e-12 * kappa * np.linalg.norm(a)
+    assert np.linalg.norm(pg @ a @ pg - pg) <= 1e-12 * kappa * np.linalg.norm(pg)
+    if kappa < 1e6:
+        assert np.abs(pg - po).max() <= 1e-13 * kappa ** 2 * max(1.0, np.abs(po).max())
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_lowrank_factorize_sweep(i):
+    import paper_2605_09755_b200 as skp
+    rng = np.random.default_rng(4000 + i)
+    m, n = int(rng.integers(300, 3000)), int(rng.integers(200, 2000))
+    l = int(rng.integers(40, min(n, 500)))
+    r2 = int(rng.integers(8, min(l, 80)))
+    q = int(rng.integers(0, 3))
+    dtype = np.float64 if i % 2 else np.float32
+    a = _graded(m, n, float(rng.uniform(0.5, 2.0)), min(m, n, 300), i, dtype)
+    spec = skp.RangeFinderSpec(k=max(1, r2 - 5), l=l, r1=l, r2=r2, q=q, eps=0.5, seed=i, s=8)
+    yo, xo = o.lowrank_factorize(a, o.Spec(k=max(1, r2 - 5), l=l, r1=l, r2=r2, q=q, seed=i, s=8))
+    res = skp.lowrank_factorize(a, spec)
+    a64 = a.astype(np.float64)
+    eo = np.linalg.norm(yo @ xo - a64) / np.linalg.norm(a64)
+    e = np.linalg.norm(res.Y.astype(np.float64) @ res.X - a64) / np.linalg.norm(a64)
+    assert abs(e - eo) <= 1e-3 * eo + (1e-6 if dtype == np.float32 else 1e-12), (e, eo)
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_power_iterate_span_sweep(i):
+    import paper_2605_09755_b200 as skp
+    rng = np.random.default_rng(5000 + i)
+    m, l = int(rng.integers(200, 3000)), int(rng.integers(20, 300))
+    r2 = int(rng.integers(2, min(l, 60)))
+    q = int(rng.integers(0, 4))
+    atil = _graded(m, l, float(rng.uniform(0.2, 1.5)), min(m, l), i, np.float64)
+    omega = np.random.default_rng(i).standard_normal((l, r2))
+    yo = o.power_iterate(atil, omega, q)
+    y = skp.power_iterate(atil, omega, q)
+    assert y.shape == yo.shape
+    d = _proj_dist(o.orthonormalize(y), o.orthonormalize(yo))
+    assert d <= 1e-6, d
