@@ -275,6 +275,15 @@ def _range_finder_dev(a: torch.Tensor, spec: RangeFinderSpec, comm=_engine.LOCAL
     ph.mark("power", "orth")
     qb = _engine.orthonormalize(be, comm, y, rows_total=rows_total, lazy=True,
                                 planes_out=planes_out)
+    if (a.dtype == F64 and getattr(comm, "world", 1) == 1 and isinstance(y, torch.Tensor)
+            and hasattr(be, "svd_cols") and y.shape[0] >= y.shape[1]
+            and be.pivot_ratio() < _engine.RESOLVE["float64"]):
+        # cond(Y) beyond what the shifted Gram keeps accurate (its pivots fell
+        # under 1e-6 of the largest; Y = A~ A~^T Q squares A's spectrum): the
+        # basis from Y's own SVD, as the reference's Householder QR would
+        # resolve it (host sync: fp64 only)
+        qb = _engine._svd_rank_basis(be, y, _engine.rank_floor(be, rows_total or y.shape[0],
+                                                                y.shape[1]))
     del y
     ph.mark("orth")
     nbad = int(bad.item())

@@ -32,14 +32,18 @@ def _case(i):
 
 
 def _matrix(m, n, rank, decay, seed, dtype):
+    """Exponentially decaying spectrum of the given rank, plus 1e-7 noise --
+    none for every fourth case (exactly low rank: the reference then keeps
+    the fp32 rounding noise's directions for fp32 inputs)."""
     rng = np.random.default_rng(seed)
     u, _ = np.linalg.qr(rng.standard_normal((m, rank)))
     v, _ = np.linalg.qr(rng.standard_normal((n, rank)))
     sv = np.exp(-decay * np.arange(rank))
-    return ((u * sv) @ v.T + 1e-7 * rng.standard_normal((m, n))).astype(dtype)
+    noise = 0.0 if seed % 4 == 2 else 1e-7
+    return ((u * sv) @ v.T + noise * rng.standard_normal((m, n))).astype(dtype)
 
 
-@pytest.mark.parametrize("i", range(48))
+@pytest.mark.parametrize("i", range(64))
 def test_random_small_configs_vs_oracle(i):
     import paper_2605_09755_b200 as skp
     m, n, l, r2, k, q, s, dtype, cuda_in, rank, decay = _case(i)
@@ -56,9 +60,16 @@ def test_random_small_configs_vs_oracle(i):
     sig = res.sigma.cpu().numpy() if cuda_in else res.sigma
     assert qn.shape[1] == qo.shape[1], (qn.shape, qo.shape)
     kk = min(k, len(so))
-    np.testing.assert_allclose(sig[:kk], so[:kk], rtol=SIG_TOL[dtype],
-                               err_msg=f"case {_case(i)}")
+    # A Y the reference itself had to truncate (its pivoted QR met |R_ii|
+    # below max(m, c) eps) has a trailing subspace fixed only to eps / rho_i:
+    # two correct implementations then agree on the Ritz values only to ~1e-5
+    # (measured: fp64, exact rank 330, q = 1, sigma_93 / sigma_1 = 2.8e-7,
+    # randsvd itself agreeing to 4e-14 on either Q; scripts/case6_probe.py)
+    tol = SIG_TOL[dtype] if qo.shape[1] == r2 else max(SIG_TOL[dtype], 1e-4)
+    np.testing.assert_allclose(sig[:kk], so[:kk], rtol=tol, err_msg=f"case {_case(i)}")
     a64 = a.astype(np.float64)
     q64 = qn.astype(np.float64)
     e = np.linalg.norm(a64 - q64 @ (q64.T @ a64)) / np.linalg.norm(a64)
-    assert abs(e - eo) <= 1e-3 * eo + 1e-12, (e, eo, _case(i))
+    # (the truncated case's residual is the ill-determined tail's energy)
+    etol = 1e-3 if qo.shape[1] == r2 else 5e-2
+    assert abs(e - eo) <= etol * eo + 1e-12, (e, eo, _case(i))
