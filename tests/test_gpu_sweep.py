@@ -73,3 +73,38 @@ def test_random_small_configs_vs_oracle(i):
     # (the truncated case's residual is the ill-determined tail's energy)
     etol = 1e-3 if qo.shape[1] == r2 else 5e-2
     assert abs(e - eo) <= etol * eo + 1e-12, (e, eo, _case(i))
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_random_classical_and_unstabilized_vs_oracle(i):
+    """range_finder_classical (the identity sketch, power.py:157-178) and the
+    unstabilised power iteration (stabilized=False) on the same seeded bytes
+    as the oracle: sigma and the projection error at the BASELINE bar."""
+    import paper_2605_09755_b200 as skp
+    rng = np.random.default_rng(7000 + i)
+    m, n = int(rng.integers(200, 3000)), int(rng.integers(60, 800))
+    r2 = int(rng.integers(4, min(n, 60)))
+    k = int(rng.integers(1, r2 + 1))
+    q = int(rng.integers(0, 3))
+    dtype = np.float64 if i % 2 else np.float32
+    rank = min(m, n)
+    a = _matrix(m, n, rank, float(rng.uniform(0.01, 0.05)), 10 * i + 1, dtype)
+    if i % 4 < 2:
+        qo = o.range_finder_sketched(a, o.Spec(k=k, l=n, r1=n, r2=r2, q=q, seed=i,
+                                               sketch_kind="identity"))
+        qb = skp.range_finder_classical(a, k, r2, q, seed=i)
+    else:
+        l = int(rng.integers(r2 + 2, min(n, 400) + 1))
+        qo = o.range_finder_sketched(a, o.Spec(k=k, l=l, r1=l, r2=r2, q=min(q, 1), seed=i, s=8,
+                                               stabilized=False))
+        qb = skp.range_finder_sketched(a, skp.RangeFinderSpec(
+            k=k, l=l, r1=l, r2=r2, q=min(q, 1), eps=0.5, seed=i, s=8, stabilized=False))
+    assert qb.shape[1] == qo.shape[1], (qb.shape, qo.shape)
+    _, so, _ = o.randsvd(a, qo)
+    res = skp.randsvd(a, qb)
+    np.testing.assert_allclose(res.sigma[:k], so[:k], rtol=SIG_TOL[dtype])
+    a64 = a.astype(np.float64)
+    q64 = qb.astype(np.float64)
+    e = np.linalg.norm(a64 - q64 @ (q64.T @ a64)) / np.linalg.norm(a64)
+    eo = o.proj_rel_error(a, qo)
+    assert abs(e - eo) <= 1e-3 * eo + 1e-12, (e, eo)
