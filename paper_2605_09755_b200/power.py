@@ -20,6 +20,7 @@ import math
 import threading
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import _convert, _engine, _ops
@@ -342,20 +343,22 @@ _BLOCK_BYTES = 2 << 30   # A~ row block of the blocked range finder (fp32)
 
 
 def _range_finder_blocked(a, spec, comm, rows_total, ph, fro2, name, streamed, hint_out,
-                          planes_out, be, sk, nonfinite, om_side, om_job, om_seed):
+                          planes_out, be, sk, nonfinite, om_side, om_job, om_seed, host=None):
     """Alg. 1 when A~ does not fit beside A: the sketch-space power iteration
     with A~ formed in row blocks twice -- pass 1 sketches each block (K2 v2),
     splits it and accumulates G = A~^T A~ (SYRK, beta = 1; behind a streamed
     upload, block by block as it lands); the q steps run in the l-dimensional
     space as in the resident path; pass 2 sketches each block again and forms
     its rows of Y = A~ W.  Only an A~ block, G (l x l) and Y (rows x r2) are
-    ever resident.  The rare eager fallbacks (a sketch plan or device Omega
-    that failed, a rank-deficient CholeskyQR) need A~ resident and raise."""
-    dev = a.device
-    m_loc = a.shape[0]
+    ever resident.  host (_HostBlocks): A itself does not fit either -- both
+    passes stream its row blocks from host memory (out of core).  The rare
+    eager fallbacks (a sketch plan or device Omega that failed, a
+    rank-deficient CholeskyQR) need A~ resident and raise."""
+    dev = host.dev if host is not None else a.device
+    m_loc = host.m if host is not None else a.shape[0]
     l, r2 = spec.r1, spec.r2
     ld = -(-l // 32) * 32
-    blk = int(max(1024, min(m_loc, _BLOCK_BYTES // (ld * 4))))
+    blk = host.rows if host is not None else int(max(1024, min(m_loc, _BLOCK_BYTES // (ld * 4))))
     e_io = torch.zeros(2, dtype=torch.int32, device=dev)
     buf = _ops.empty2d(blk, l, F32, dev)
     gram = _ops.empty2d(l, l, F32, dev)
@@ -365,11 +368,19 @@ def _range_finder_blocked(a, spec, comm, rows_total, ph, fro2, name, streamed, h
             for s0 in range(r0, r1, blk):
                 yield s0, min(r1, s0 + blk)
 
+    def blocks(first: bool):
+        """(r0, r1, the device rows of A) for one pass."""
+        if host is not None:
+            yield from host.blocks()
+            return
+        src = streamed.blocks() if (first and streamed is not None) else [(0, m_loc)]
+        for r0, r1 in ranges(src):
+            yield r0, r1, a[r0:r1]
+
     ph.mark("make_sketch", "apply_right")
     perm, first = None, True
-    src = streamed.blocks() if streamed is not None else [(0, m_loc)]
-    for r0, r1 in ranges(src):
-        got = sk.right_permuted(a[r0:r1], out=buf[:r1 - r0], fro2=fro2, nonfinite=nonfinite,
+    for r0, r1, ab in blocks(True):
+        got = sk.right_permuted(ab, out=buf[:r1 - r0], fro2=fro2, nonfinite=nonfinite,
                                 deferred=True, amax=e_io[1:])
         if got is None:
             raise RuntimeError("internal: the blocked range finder needs the row gather (K2 v2)")
@@ -381,7 +392,7 @@ def _range_finder_blocked(a, spec, comm, rows_total, ph, fro2, name, streamed, h
         torch.cuda.current_stream(dev).wait_event(om_side[1])
         omega = _ops.permute_rows(om_side[0], perm)
     elif om_job is None:
-        omega = omega_device(spec.omega_kind, l, r2, om_seed, a.dtype, dev, perm, nonfinite)
+        omega = omega_device(spec.omega_kind, l, r2, om_seed, F32, dev, perm, nonfinite)
     else:
         omega = om_job.to_device(dev, perm)
     ph.mark("omega", "power")
@@ -391,8 +402,8 @@ def _range_finder_blocked(a, spec, comm, rows_total, ph, fro2, name, streamed, h
     del gram, omega
     y = _ops.empty2d(m_loc, r2, F32, dev)
     scratch = torch.zeros(1, dtype=torch.int64, device=dev)
-    for r0, r1 in ranges([(0, m_loc)]):
-        sk.right_permuted(a[r0:r1], out=buf[:r1 - r0], nonfinite=scratch, deferred=True)
+    for r0, r1, ab in blocks(False):
+        sk.right_permuted(ab, out=buf[:r1 - r0], nonfinite=scratch, deferred=True)
         _ops.gemm_h3(_ops.split_h2(buf[:r1 - r0]), wt, out=y[r0:r1])     # A~_b W
     del buf, wt
     yt = _ops.split_h2(y, trans=True)
@@ -414,6 +425,112 @@ def _range_finder_blocked(a, spec, comm, rows_total, ph, fro2, name, streamed, h
         hint_out["amax"] = (e_io, int(math.ceil(math.log2(2.0 * math.sqrt(spec.s or 1)))) + 1)
         hint_out["pivot_ratio"] = be.pivot_ratio() ** 0.5   # (Y = A~ A~^T Q_prev: power 2)
     return qb
+
+
+_OOC_BLOCK_BYTES = 2 << 30   # host row block of an out-of-core A (fp32)
+
+
+class _HostBlocks:
+    """Row blocks of a host fp32 matrix staged into two device buffers: the
+    copy of block b + 1 runs on a side stream while the caller's stream works
+    on block b (each buffer is refilled only after the work queued on it)."""
+
+    def __init__(self, src: torch.Tensor, dev, rows: int | None = None):
+        self.src, self.dev = src, dev
+        self.m, n = src.shape
+        per = -(-n // 32) * 32 * 4
+        self.rows = int(rows or max(8, min(self.m, _OOC_BLOCK_BYTES // per) // 8 * 8))
+        self.bufs = [_ops.empty2d(min(self.rows, self.m), n, F32, dev) for _ in range(2)]
+
+    def blocks(self):
+        cur = torch.cuda.current_stream(self.dev)
+        side = _SIDE.get(self.dev)
+        free = [None, None]   # event: the caller's work on the buffer is queued before it
+        for bi, r0 in enumerate(range(0, self.m, self.rows)):
+            r1 = min(self.m, r0 + self.rows)
+            b = bi & 1
+            if free[b] is not None:
+                side.wait_event(free[b])
+            else:
+                side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                self.bufs[b][:r1 - r0].copy_(self.src[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            cur.wait_event(ev)
+            yield r0, r1, self.bufs[b][:r1 - r0]
+            free[b] = torch.cuda.Event()
+            free[b].record(cur)
+        for buf in self.bufs:
+            buf.record_stream(side)
+
+
+def _host_f32(a):
+    """A host 2-D float32 operand as a CPU tensor (else None)."""
+    if isinstance(a, _convert.DeviceMatrix):
+        return None
+    if isinstance(a, torch.Tensor):
+        return a if (not a.is_cuda and a.dim() == 2 and a.dtype == F32) else None
+    arr = np.asarray(a) if not isinstance(a, np.ndarray) else a
+    if arr.ndim != 2 or arr.dtype != np.float32 or not arr.size:
+        return None
+    return torch.from_numpy(np.ascontiguousarray(arr))
+
+
+def _needs_out_of_core(shape, spec_r2: int, spec_l: int, dev) -> bool:
+    """Does A (fp32) plus the range finder's least working set -- Y, Q and
+    their planes, the l x l Gram and its planes, an A~ block -- fail to fit?"""
+    m, n = shape
+    ld, ldr, ldl = (-(-x // 32) * 32 for x in (n, spec_r2, spec_l))
+    need = m * ld * 4 + 3 * m * ldr * 4 + 3 * ldl * ldl * 4 + (4 << 30)
+    return need > _ops._device_total(dev) - torch.cuda.memory_allocated(dev)
+
+
+def _range_finder_ooc(src: torch.Tensor, spec: RangeFinderSpec, dev, fro2=None,
+                      hint_out: dict | None = None, planes_out: bool = False, name: str = "a",
+                      rows: int | None = None):
+    """Alg. 1 for a host fp32 A that does not fit on the device: the blocked
+    sketch-space range finder with both passes streaming A's row blocks from
+    host memory (two trips over the link); Y, Q and G stay resident."""
+    if spec.sketch_kind != "countsketch" or not spec.stabilized or spec.q < 1:
+        raise ValueError("unsupported: a matrix larger than the device needs the stabilised "
+                         "countsketch range finder with q >= 1 (out of core)")
+    m, n = src.shape
+    be = _be(F32, dev)
+    ph = _Phases(False)
+    om_seed = substream(spec.seed, 1)
+    om_job = None if spec.omega_kind == "gaussian" else \
+        OmegaDraw(spec.omega_kind, spec.r1, spec.r2, om_seed, F32)
+    nonfinite = torch.zeros(1, dtype=torch.int64, device=dev)
+    sk = make_sketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s, device=dev)
+    om_side = _omega_side(spec, om_seed, F32, dev, nonfinite) if om_job is None else None
+    host = _HostBlocks(src, dev, rows)
+    return _range_finder_blocked(None, spec, _engine.LOCAL, m, ph, fro2, name, None, hint_out,
+                                 planes_out, be, sk, nonfinite, om_side, om_job, om_seed,
+                                 host=host)
+
+
+def _randsvd_ooc(src: torch.Tensor, qb, dev, stats: dict | None = None, rows: int | None = None):
+    """randsvd (power.py:181-199) for a host fp32 A that does not fit:
+    B^T = sum_b A_b^T Q_b over A's row blocks streamed from host memory
+    (3xFP16, each block split in the kernel with its own exponent), the rest
+    on the resident Q as usual; the reference's orthonormality check first."""
+    be = _be(F32, dev)
+    comm = _engine.LOCAL
+    gq = be.gram64_q(qb)
+    devn = be.orth_dev_t(gq)
+    sq = qb if isinstance(qb, _ops.SplitH2) else _ops.split_h2(qb, trans=True)
+    m, n = src.shape
+    bt = _ops.empty2d(n, sq.rows, F32, dev)
+    host = _HostBlocks(src, dev, rows)
+    first = True
+    for r0, r1, ab in host.blocks():
+        qs = _ops.SplitH2(sq.hi[:, r0:r1], sq.lo[:, r0:r1], sq.e, sq.rows, r1 - r0, sq.ld)
+        _ops.gemm_h3s_t(ab, _ops.h2_exponent(ab), qs, beta=0.0 if first else 1.0, out=bt)
+        first = False
+    out = _engine._randsvd_core(be, comm, bt, qb, gq, stats)
+    _engine._raise_if_not_orthonormal(be, be.scalar(devn))
+    return out
 
 
 # fp32 operands whose spectrum the fp32 arithmetic cannot resolve are
@@ -454,6 +571,13 @@ def _sigma_too_wide(s: torch.Tensor) -> bool:
 
 def range_finder_sketched(a, spec: RangeFinderSpec, *, timings: dict | None = None, device=None):
     """Orthonormal range finder from power iteration on the sketch A S (power.py:141-154)."""
+    src = _host_f32(a)
+    if src is not None:
+        dev = _ops.require_cuda(device)
+        if _needs_out_of_core(tuple(src.shape), spec.r2, spec.r1, dev):
+            spec.validate(*src.shape)
+            qb = _range_finder_ooc(src, spec, dev)
+            return _convert.download(qb, "cpu" if isinstance(a, torch.Tensor) else "numpy")
     op, streamed = _convert.upload_streamed(a, "a", device)
     m, n = op.t.shape
     spec.validate(m, n)
@@ -487,6 +611,20 @@ def _randsvd_dev(a: torch.Tensor, qb: torch.Tensor, comm=_engine.LOCAL, check: b
 
 def randsvd(a, q_basis, *, timings: dict | None = None) -> SvdResult:
     """U diag(sigma) V^T == Q Q^T a (power.py:181-199)."""
+    src = _host_f32(a)
+    if src is not None:
+        dev = _ops.require_cuda(None)
+        oq0 = np.asarray(q_basis) if not isinstance(q_basis, torch.Tensor) else q_basis
+        r2 = int(oq0.shape[1]) if getattr(oq0, "ndim", 2) == 2 else 1
+        if _needs_out_of_core(tuple(src.shape), r2, r2, dev):
+            oq = _convert.upload(q_basis, "q_basis", dev, dtype=F32)
+            if oq.t.shape[0] != src.shape[0]:
+                raise ValueError(f"dimension mismatch: Q has {oq.t.shape[0]} rows, "
+                                 f"a has {src.shape[0]}")
+            u, s, v = _randsvd_ooc(src, oq.t, dev)
+            kind = "cpu" if isinstance(a, torch.Tensor) else "numpy"
+            return SvdResult(_convert.download(u, kind), _convert.download(s, kind),
+                             _convert.download(v, kind))
     oa = _convert.upload(a, "a")
     oq = _convert.upload(q_basis, "q_basis", oa.t.device)
     if oq.t.shape[0] != oa.t.shape[0]:
@@ -514,6 +652,12 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
     rel_err = ||a - QQ^T a||_F / ||a||_F from ||a||_F^2 - sum(sigma^2)
     (Pythagorean identity, in the form that holds for any Q:
     _engine.randsvd's stats; ||a||_F^2 is fused into the sketch)."""
+    src = _host_f32(a)
+    if src is not None:
+        dev = _ops.require_cuda(None)
+        if _needs_out_of_core(tuple(src.shape), spec.r2, spec.r1, dev):
+            return _rsvd_ooc(src, spec, dev, with_error,
+                             "cpu" if isinstance(a, torch.Tensor) else "numpy")
     op, streamed = _convert.upload_streamed(a, "a")
     m, n = op.t.shape
     spec.validate(m, n)
@@ -545,6 +689,23 @@ def rsvd(a, spec: RangeFinderSpec, *, timings: dict | None = None, with_error: b
     a2 = float(fro2.item())
     rel = math.sqrt(max(a2 - float(st["qa2"]), 0.0) / a2) if a2 > 0 else 0.0
     return res, rel
+
+
+def _rsvd_ooc(src: torch.Tensor, spec: RangeFinderSpec, dev, with_error: bool, kind: str):
+    """rsvd for a host fp32 A larger than the device: three trips of A's row
+    blocks over the link (G, then Y = A~ W, then B^T = A^T Q)."""
+    m, n = src.shape
+    spec.validate(m, n)
+    fro2 = torch.zeros(1, dtype=torch.float64, device=dev) if with_error else None
+    qb = _range_finder_ooc(src, spec, dev, fro2=fro2, planes_out=True)
+    st = {}
+    u, s, v = _randsvd_ooc(src, qb, dev, stats=st)
+    res = SvdResult(_convert.download(u, kind), _convert.download(s, kind),
+                    _convert.download(v, kind))
+    if not with_error:
+        return res
+    a2 = float(fro2.item())
+    return res, (math.sqrt(max(a2 - float(st["qa2"]), 0.0) / a2) if a2 > 0 else 0.0)
 
 
 def lowrank_factorize(a, spec: RangeFinderSpec) -> FactorizationResult:

@@ -248,6 +248,41 @@ def test_blocked_range_finder_vs_live_oracle(skp, monkeypatch, name, m, n, l, r2
 @pytest.mark.parametrize("name,m,n,l,r2,k,q,rank,decay", [
     ("C3-structure", 16384, 4096, 1000, 120, 100, 3, 2048, "poly"),
     ("C5-structure", 32768, 2048, 1000, 210, 200, 2, 1024, "exp"),
+])
+def test_out_of_core_vs_live_oracle(skp, monkeypatch, name, m, n, l, r2, k, q, rank, decay):
+    """A host matrix larger than the device (forced here, with ~1000-row
+    blocks): the reference's two calls and rsvd stream A's row blocks from
+    host memory (G, Y = A~ W, B^T = A^T Q) -- against the live oracle on the
+    same bytes: sigma 1e-5, rel_err 1e-3."""
+    from paper_2605_09755_b200 import power
+    spec_v = np.arange(1.0, rank + 1.0) ** -0.5 if decay == "poly" else np.exp(-np.arange(1.0, rank + 1.0) / 200.0)
+    a = datagen.lowrank_plus_noise_gpu(m, n, spec_v, 1e-6 if decay == "poly" else 1e-8,
+                                       seed=3).cpu().numpy()
+    spec = skp.RangeFinderSpec(k=k, l=l, r1=l, r2=r2, q=q, eps=0.5, seed=3, s=8)
+    ospec = o.Spec(k=k, l=l, r1=l, r2=r2, q=q, seed=3, s=8)
+    qo = o.range_finder_sketched(a, ospec)
+    _, so, _ = o.randsvd(a, qo)
+    eo = o.proj_rel_error(a, qo)
+    calls = []
+    real_rf, real_rs = power._range_finder_ooc, power._randsvd_ooc
+    monkeypatch.setattr(power, "_needs_out_of_core", lambda *x: True)
+    monkeypatch.setattr(power, "_OOC_BLOCK_BYTES", 1000 * n * 4)
+    monkeypatch.setattr(power, "_range_finder_ooc", lambda *x, **kw: calls.append("rf") or real_rf(*x, **kw))
+    monkeypatch.setattr(power, "_randsvd_ooc", lambda *x, **kw: calls.append("rs") or real_rs(*x, **kw))
+    qb = skp.range_finder_sketched(a, spec)
+    assert isinstance(qb, np.ndarray) and qb.shape[1] == qo.shape[1]
+    res = skp.randsvd(a, qb)
+    np.testing.assert_allclose(res.sigma[:k], so[:k], rtol=SIG_TOL[np.float32])
+    assert abs(_rel_err(a, qb) - eo) <= ERR_TOL * eo
+    res_b, rel_b = skp.rsvd(a, spec, with_error=True)
+    np.testing.assert_allclose(res_b.sigma[:k], so[:k], rtol=SIG_TOL[np.float32])
+    assert abs(rel_b - eo) <= ERR_TOL * eo, (rel_b, eo)
+    assert calls == ["rf", "rs", "rf", "rs"]
+
+
+@pytest.mark.parametrize("name,m,n,l,r2,k,q,rank,decay", [
+    ("C3-structure", 16384, 4096, 1000, 120, 100, 3, 2048, "poly"),
+    ("C5-structure", 32768, 2048, 1000, 210, 200, 2, 1024, "exp"),
     ("graded", 16384, 2048, 500, 80, 60, 2, 400, "graded"),
 ])
 def test_sketch_space_power_matches_products(skp, monkeypatch, name, m, n, l, r2, k, q, rank,
