@@ -110,3 +110,59 @@ def test_two_ranks_on_cuda_match_one(tmp_path):
     app1 = one["c"][:512] @ np.linalg.pinv(one["w"], rcond=1e-10) @ one["c"][:512].T
     app2 = c2[:512] @ np.linalg.pinv(r0["w"], rcond=1e-10) @ c2[:512].T
     assert np.linalg.norm(app2 - app1) <= 1e-3 * np.linalg.norm(app1)
+
+
+# seeded ragged configurations of the sharded rsvd (the bench's driver):
+# odd row counts (uneven slabs), both power paths (sketch space / products),
+# q in {0, 1, 3}, s in {1, 8}
+SWEEP = [(30001, 1500, 600, 120, 100, 3, 8), (20011, 3000, 900, 40, 30, 1, 1),
+         (40003, 1024, 500, 200, 150, 0, 8), (12345, 2222, 333, 70, 60, 2, 8)]
+
+
+def _run_sweep(comm, rank, world):
+    import paper_2605_09755_b200 as skp
+    from paper_2605_09755_b200 import datagen, distributed as D
+    out = {}
+    for ci, (m, n, l, r2, k, q, s) in enumerate(SWEEP):
+        row0, rows = D.shard_rows(m, world, rank)
+        spec_v = np.exp(-np.arange(1.0, 601.0) / 150.0)
+        a = datagen.lowrank_plus_noise_gpu(m, n, spec_v, 1e-7, seed=ci, row0=row0, rows=rows)
+        spec = skp.RangeFinderSpec(k=k, l=l, r1=l, r2=r2, q=q, eps=0.5, seed=ci, s=s)
+        _, sv, _, rel = D.rsvd_sharded(a, spec, m, comm, with_error=True)
+        out[f"s{ci}"] = sv.double().cpu().numpy()
+        out[f"rel{ci}"] = np.array(rel)
+    return out
+
+
+def _worker_sweep(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_09755_b200 import distributed as D
+        np.savez(os.path.join(out_dir, f"sweep{rank}.npz"), **_run_sweep(D.TorchComm(), rank, world))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_sweep_match_one(tmp_path):
+    from paper_2605_09755_b200 import _engine
+    one = _run_sweep(_engine.LOCAL, 0, 1)
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_worker_sweep, args=(r, 2, port, str(tmp_path))) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(900)
+        assert p.exitcode == 0
+    r0, r1 = (dict(np.load(tmp_path / f"sweep{r}.npz")) for r in range(2))
+    for ci, (m, n, l, r2, k, q, s) in enumerate(SWEEP):
+        np.testing.assert_array_equal(r0[f"s{ci}"], r1[f"s{ci}"])
+        np.testing.assert_allclose(r0[f"s{ci}"][:k], one[f"s{ci}"][:k], rtol=1e-5,
+                                   err_msg=f"config {SWEEP[ci]}")
+        e1, e2 = float(one[f"rel{ci}"]), float(r0[f"rel{ci}"])
+        assert abs(e2 - e1) <= 1e-3 * e1, (SWEEP[ci], e1, e2)
