@@ -101,3 +101,31 @@ def test_power_iterate_span_sweep(i):
     assert y.shape == yo.shape
     d = _proj_dist(o.orthonormalize(y), o.orthonormalize(yo))
     assert d <= 1e-6, d
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_nystrom_sweep(i):
+    """nystrom_psd (power.py:258-298) on seeded PSD matrices against the
+    oracle's core on the same bytes: the orthonormalised power at the 1e-3
+    bar; the literal core (cond(W) up to ~1e15) at the documented 5e-3."""
+    import paper_2605_09755_b200 as skp
+    rng = np.random.default_rng(6000 + i)
+    n = int(rng.integers(300, 3000))
+    l = int(rng.integers(40, min(n, 500)))
+    r2 = int(rng.integers(8, min(l, 80)))
+    q = int(rng.integers(1, 3))
+    dtype = np.float64 if i % 2 else np.float32
+    rank = int(rng.integers(r2, min(n, 400)))
+    u, _ = np.linalg.qr(rng.standard_normal((n, rank)))
+    kmat = ((u * np.exp(-np.arange(rank) * float(rng.uniform(0.01, 0.1)))) @ u.T)
+    kmat = ((kmat + kmat.T) / 2).astype(dtype)
+    spec = skp.RangeFinderSpec(k=max(1, r2 - 4), l=l, r1=l, r2=r2, q=q, eps=0.5, seed=i, s=8)
+    ospec = o.Spec(k=max(1, r2 - 4), l=l, r1=l, r2=r2, q=q, seed=i, s=8)
+    for stab, tol in ((True, 1e-3), (False, 5e-3)):
+        res = skp.nystrom_psd(kmat, spec, stabilized=stab)
+        c = np.asarray(res.C.cpu() if hasattr(res.C, "cpu") else res.C, dtype=np.float64)
+        w = np.asarray(res.W.cpu() if hasattr(res.W, "cpu") else res.W, dtype=np.float64)
+        e = o.nystrom_rel_error(kmat, c, w)
+        co, wo = o.nystrom_core(kmat, ospec, stabilized=stab)
+        eo = o.nystrom_rel_error(kmat, co, wo)
+        assert abs(e - eo) <= tol * eo + 1e-12, (stab, e, eo, n, l, r2, q, dtype)
