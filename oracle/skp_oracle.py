@@ -131,16 +131,62 @@ class CountSketch:
             if r != n:
                 raise ValueError("identity sketch needs r == n")
             self.s = None
+        elif kind == "srht":              # sketching.py:125-130
+            rng = generator(self.seed)
+            self.n_pad = 1 << (int(n) - 1).bit_length()
+            self.srht_signs = rng.integers(0, 2, size=self.n_pad).astype(np.float64) * 2.0 - 1.0
+            self.subset = np.sort(rng.choice(self.n_pad, size=r, replace=False))
+            self.s = None
+        elif kind in ("gaussian", "sign"):  # sketching.py:131-136
+            rng = generator(self.seed)
+            if kind == "gaussian":
+                self.dense = rng.standard_normal((n, r)) / math.sqrt(r)
+            else:
+                self.dense = (rng.integers(0, 2, size=(n, r)).astype(np.float64) * 2.0 - 1.0)
+                self.dense /= math.sqrt(r)
+            self.s = None
         else:
-            raise ValueError(f"oracle covers countsketch/identity only, not {kind!r}")
+            raise ValueError(f"oracle covers countsketch/identity/srht/gaussian/sign, not {kind!r}")
+
+    @staticmethod
+    def fwht(a, axis: int = 0):
+        """sketching.py:65-90: unnormalised Sylvester-ordered Walsh-Hadamard."""
+        a = np.asarray(a, dtype=np.float64)
+        if axis == 1:
+            return CountSketch.fwht(a.T, 0).T
+        n = a.shape[0]
+        out = a.copy().reshape(n, -1)
+        cols = out.shape[1]
+        h = 1
+        while h < n:
+            out = out.reshape(n // (2 * h), 2, h, cols)
+            out = np.stack((out[:, 0] + out[:, 1], out[:, 0] - out[:, 1]), axis=1).reshape(n, cols)
+            h *= 2
+        return out.reshape(a.shape)
 
     def apply_right(self, a):            # sketching.py:158-174
         a = as_matrix(a)
-        return np.asarray(a @ self.csr) if self.kind == "countsketch" else a.copy()
+        if self.kind == "countsketch":
+            return np.asarray(a @ self.csr)
+        if self.kind == "srht":
+            padded = np.zeros((a.shape[0], self.n_pad))
+            padded[:, : self.n] = a
+            return self.fwht(padded * self.srht_signs, 1)[:, self.subset] / math.sqrt(self.r)
+        if self.kind in ("gaussian", "sign"):
+            return a @ self.dense
+        return a.copy()
 
     def apply_left_transpose(self, a):   # sketching.py:176-192
         a = as_matrix(a)
-        return np.asarray(self.csr.T @ a) if self.kind == "countsketch" else a.copy()
+        if self.kind == "countsketch":
+            return np.asarray(self.csr.T @ a)
+        if self.kind == "srht":
+            padded = np.zeros((self.n_pad, a.shape[1]))
+            padded[: self.n, :] = a
+            return self.fwht(padded * self.srht_signs[:, None], 0)[self.subset, :] / math.sqrt(self.r)
+        if self.kind in ("gaussian", "sign"):
+            return self.dense.T @ a
+        return a.copy()
 
     def densify(self):                   # sketching.py:194-213
         if self.kind == "identity":

@@ -108,3 +108,32 @@ def test_random_classical_and_unstabilized_vs_oracle(i):
     e = np.linalg.norm(a64 - q64 @ (q64.T @ a64)) / np.linalg.norm(a64)
     eo = o.proj_rel_error(a, qo)
     assert abs(e - eo) <= 1e-3 * eo + 1e-12, (e, eo)
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_random_other_sketch_kinds_vs_oracle(i):
+    """srht / gaussian / sign S (sketching.py:125-139; the oracle's draws are
+    pinned to the live reference in test_oracle_golden.py) through the
+    reference's two calls: sigma and the error at the BASELINE bar."""
+    import paper_2605_09755_b200 as skp
+    kind = ("srht", "gaussian", "sign")[i % 3]
+    rng = np.random.default_rng(8000 + i)
+    m, n = int(rng.integers(300, 2500)), int(rng.integers(100, 1500))
+    l = int(rng.integers(30, min(n, 300)))
+    r2 = int(rng.integers(6, min(l, 60)))
+    k = int(rng.integers(1, r2 + 1))
+    q = int(rng.integers(0, 3))
+    dtype = np.float64 if (i // 3) % 2 else np.float32
+    a = _matrix(m, n, min(m, n), float(rng.uniform(0.01, 0.06)), 10 * i + 3, dtype)
+    spec = skp.RangeFinderSpec(k=k, l=l, r1=l, r2=r2, q=q, eps=0.5, seed=i, sketch_kind=kind)
+    qo = o.range_finder_sketched(a, o.Spec(k=k, l=l, r1=l, r2=r2, q=q, seed=i, sketch_kind=kind))
+    qb = skp.range_finder_sketched(a, spec)
+    assert qb.shape[1] == qo.shape[1], (kind, qb.shape, qo.shape)
+    _, so, _ = o.randsvd(a, qo)
+    res = skp.randsvd(a, qb)
+    np.testing.assert_allclose(res.sigma[:k], so[:k], rtol=SIG_TOL[dtype], err_msg=kind)
+    a64 = a.astype(np.float64)
+    q64 = qb.astype(np.float64)
+    e = np.linalg.norm(a64 - q64 @ (q64.T @ a64)) / np.linalg.norm(a64)
+    eo = o.proj_rel_error(a, qo)
+    assert abs(e - eo) <= 1e-3 * eo + 1e-12, (kind, e, eo)

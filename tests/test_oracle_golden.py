@@ -5,11 +5,12 @@ both restatements (plain C and numpy) must reproduce them bit for bit
 (integer/index work) or to fp64 rounding (end-to-end C1).
 """
 import hashlib
+import os
 
 import numpy as np
 import pytest
 
-from conftest import small_cs_cases
+from conftest import GOLDEN, small_cs_cases
 from oracle import skp_oracle as o
 from paper_2605_09755_b200 import datagen
 
@@ -96,3 +97,26 @@ def test_ziggurat_restatement_matches_numpy(seed):
     ref = np.random.Generator(np.random.PCG64(seed)).standard_normal(n)
     raw = np.random.PCG64(seed).random_raw(n + n // 16 + 64)
     np.testing.assert_array_equal(ziggurat.standard_normal_from_raw(raw, n), ref)
+
+
+def test_oracle_srht_matches_live_reference():
+    """The oracle's SRHT (sketching.py:65-90, :125-130, :165-171, :183-189)
+    against values recorded from the live reference."""
+    g = np.load(os.path.join(GOLDEN, "srht_golden.npz"))
+    for key in sorted({k.split("_", 1)[1] for k in g.files if k.startswith("signs_")}):
+        n, r, seed = (int(v) for v in key.split("_"))
+        op = o.CountSketch("srht", n, r, seed)
+        np.testing.assert_array_equal(op.srht_signs, g[f"signs_{key}"])
+        np.testing.assert_array_equal(op.subset, g[f"subset_{key}"])
+        np.testing.assert_allclose(op.apply_right(g[f"a_{key}"]), g[f"right_{key}"], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(op.apply_left_transpose(g[f"x_{key}"]), g[f"left_{key}"], rtol=0,
+                                   atol=1e-12)
+
+
+def test_oracle_dense_sketches_match_live_reference():
+    """gaussian / sign S (sketching.py:131-136) drawn bit for bit as the reference."""
+    g = np.load(os.path.join(GOLDEN, "dense_sketch_golden.npz"))
+    for key in g.files:
+        kind, n, r, seed = key.split("_")
+        op = o.CountSketch(kind, int(n), int(r), int(seed))
+        np.testing.assert_array_equal(op.dense, g[key])
