@@ -129,3 +129,35 @@ def test_nystrom_sweep(i):
         co, wo = o.nystrom_core(kmat, ospec, stabilized=stab)
         eo = o.nystrom_rel_error(kmat, co, wo)
         assert abs(e - eo) <= tol * eo + 1e-12, (stab, e, eo, n, l, r2, q, dtype)
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_sketch_apply_sweep(i):
+    """SketchOperator.apply_right / apply_left_transpose (sketching.py:158-192)
+    for every kind against the oracle (whose draws are pinned to the live
+    reference): ragged n, r, s; fp32 and fp64; numpy and CUDA operands."""
+    import torch
+    import paper_2605_09755_b200 as skp
+    rng = np.random.default_rng(9000 + i)
+    kind = ("countsketch", "srht", "gaussian", "sign")[i % 4]
+    n = int(rng.integers(1, 3000))
+    r = int(rng.integers(1, min(n, 600) + 1)) if kind != "srht" else \
+        int(rng.integers(1, min(1 << (n - 1).bit_length(), 600) + 1))
+    s = int(rng.integers(1, min(r, 12) + 1)) if kind == "countsketch" else None
+    dtype = np.float64 if (i // 4) % 2 else np.float32
+    cuda = (i // 8) % 2 == 1
+    op = skp.make_sketch(kind, n, r, seed=i, s=s)
+    ref = o.CountSketch(kind, n, r, i, s=s)
+    a = rng.standard_normal((int(rng.integers(1, 300)), n)).astype(dtype)
+    x = rng.standard_normal((n, int(rng.integers(1, 40)))).astype(dtype)
+    ar = torch.from_numpy(a).cuda() if cuda else a
+    xr = torch.from_numpy(x).cuda() if cuda else x
+    got_r = op.apply_right(ar)
+    got_l = op.apply_left_transpose(xr)
+    got_r = got_r.cpu().numpy() if cuda else got_r
+    got_l = got_l.cpu().numpy() if cuda else got_l
+    tol = 1e-12 if dtype == np.float64 else 2e-6
+    want_r = ref.apply_right(a)
+    want_l = ref.apply_left_transpose(x)
+    assert np.abs(got_r - want_r).max() <= tol * max(1.0, np.abs(want_r).max()) * np.sqrt(n)
+    assert np.abs(got_l - want_l).max() <= tol * max(1.0, np.abs(want_l).max()) * np.sqrt(n)
