@@ -630,6 +630,10 @@ def randsvd(a, q_basis, *, timings: dict | None = None) -> SvdResult:
     if oq.t.shape[0] != oa.t.shape[0]:
         raise ValueError(f"dimension mismatch: Q has {oq.t.shape[0]} rows, a has {oa.t.shape[0]}")
     dt = _convert.common_dtype(oa, oq)
+    if dt == F64 and oa.t.dtype == F32 and not _fp64_fits(oa.t):
+        # an fp64 Q (e.g. a promoted range finder's) with an fp32 A too large
+        # for an fp64 copy: the fp32 product on Q rounded to fp32
+        dt = F32
     ph = _Phases(timings is not None)
     ph.mark("start", "randsvd")
     at = _convert.as_dtype(oa, dt)
