@@ -114,11 +114,14 @@ class ClockSampler:
 def make_input(cfg, row0, rows, device):
     import torch
     from paper_2605_09755_b200 import datagen
+    from paper_2605_09755_b200 import _ops
     g = cfg["gen"]
-    if g == "c1":
-        return torch.from_numpy(datagen.c1_matrix(1)[row0:row0 + rows]).to(device)
-    if g == "c2":
-        return torch.from_numpy(datagen.c2_matrix(2)[row0:row0 + rows]).to(device)
+    if g in ("c1", "c2"):
+        # host-generated: into 128-byte rows, as the public upload lays it out
+        h = (datagen.c1_matrix(1) if g == "c1" else datagen.c2_matrix(2))[row0:row0 + rows]
+        t = _ops.empty2d(h.shape[0], h.shape[1], torch.from_numpy(h[:1]).dtype, device)
+        t.copy_(torch.from_numpy(h))
+        return t
     if g == "c3":
         return datagen.c3_matrix_gpu(3, cfg["m"], cfg["n"], device=device, row0=row0, rows=rows)
     if g == "c5":
