@@ -191,14 +191,21 @@ class CountSketch:
     def densify(self):                   # sketching.py:194-213
         if self.kind == "identity":
             return np.eye(self.n)
+        if self.kind in ("gaussian", "sign"):
+            return self.dense.copy()
+        if self.kind == "srht":
+            return self.apply_right(np.eye(self.n))
         out = np.zeros((self.n, self.r))
         out[np.repeat(np.arange(self.n), self.s), self.cols.ravel()] = self.signs.ravel() / math.sqrt(self.s)
         return out
 
 
-def draw_omega(r1: int, r2: int, seed: int) -> np.ndarray:
-    """power.py:137-138 -> sketching.py:132-133: standard_normal((r1, r2)) / sqrt(r2)."""
-    return generator(seed).standard_normal((r1, r2)) / math.sqrt(r2)
+def draw_omega(r1: int, r2: int, seed: int, kind: str = "gaussian") -> np.ndarray:
+    """power.py:137-138: make_sketch(kind, r1, r2, seed).densify(); the
+    Gaussian default is sketching.py:132-133, standard_normal((r1, r2)) / sqrt(r2)."""
+    if kind == "gaussian":
+        return generator(seed).standard_normal((r1, r2)) / math.sqrt(r2)
+    return CountSketch(kind, r1, r2, seed).densify()
 
 
 # --------------------------------------------------------------------------
@@ -258,6 +265,7 @@ class Spec:
     seed: int = 0
     stabilized: bool = True
     s: int = 1
+    omega_kind: str = "gaussian"
 
 
 def power_iterate(atil, omega, q: int, stabilized: bool = True):
@@ -280,7 +288,7 @@ def range_finder_sketched(a, spec: Spec, timings: dict | None = None):
     m, n = a.shape
     sk = CountSketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s)
     t.append(time.perf_counter())
-    omega = draw_omega(spec.r1, spec.r2, substream(spec.seed, 1))
+    omega = draw_omega(spec.r1, spec.r2, substream(spec.seed, 1), spec.omega_kind)
     t.append(time.perf_counter())
     atil = sk.apply_right(a)
     t.append(time.perf_counter())
@@ -310,7 +318,7 @@ def lowrank_factorize(a, spec: Spec):
     m, n = a.shape
     s1 = CountSketch(spec.sketch_kind, n, spec.r1, substream(spec.seed, 0), s=spec.s)
     atil = s1.apply_right(a)
-    omega = draw_omega(spec.r1, spec.r2, substream(spec.seed, 1))
+    omega = draw_omega(spec.r1, spec.r2, substream(spec.seed, 1), spec.omega_kind)
     y = power_iterate(atil, omega, spec.q, stabilized=spec.stabilized)
     s2 = CountSketch(spec.sketch_kind, m, spec.r1, substream(spec.seed, 2), s=spec.s)
     return y, pinv(s2.apply_left_transpose(y)) @ s2.apply_left_transpose(a)
@@ -337,7 +345,7 @@ def nystrom_core(a, spec: Spec, stabilized: bool = False, timings: dict | None =
     wtil = sk.apply_left_transpose(ctil)
     wtil = (wtil + wtil.T) / 2.0
     t2 = time.perf_counter()
-    y = draw_omega(spec.r1, spec.r2, substream(spec.seed, 1))
+    y = draw_omega(spec.r1, spec.r2, substream(spec.seed, 1), spec.omega_kind)
     for _ in range(spec.q):
         if stabilized:
             y = orthonormalize(y)

@@ -250,8 +250,10 @@ def draw_omega(kind: str, rows: int, cols: int, seed: int) -> np.ndarray:
         if rows != cols:
             raise ValueError(f"identity sketch needs r == n, got n={rows}, r={cols}")
         return np.eye(rows)
-    if kind == "countsketch":
-        return make_sketch("countsketch", rows, cols, seed).densify()
+    if kind in ("countsketch", "srht"):
+        # (the reference's own route for every family: make_sketch(...).densify(),
+        # with its densify cap)
+        return make_sketch(kind, rows, cols, seed).densify()
     raise ValueError(f"unsupported omega kind {kind!r} on the B200 path")
 
 

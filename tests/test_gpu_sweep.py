@@ -137,3 +137,36 @@ def test_random_other_sketch_kinds_vs_oracle(i):
     e = np.linalg.norm(a64 - q64 @ (q64.T @ a64)) / np.linalg.norm(a64)
     eo = o.proj_rel_error(a, qo)
     assert abs(e - eo) <= 1e-3 * eo + 1e-12, (kind, e, eo)
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_random_r1_and_omega_kinds_vs_oracle(i):
+    """RangeFinderSpec beyond r1 == l: a primary sketch size r1 different
+    from l, and the start block drawn from another family (omega_kind, the
+    reference's ablation escape hatch, power.py:137-138)."""
+    import paper_2605_09755_b200 as skp
+    rng = np.random.default_rng(9500 + i)
+    omega_kind = ("gaussian", "sign", "countsketch", "srht")[i % 4]
+    m, n = int(rng.integers(300, 2500)), int(rng.integers(200, 1500))
+    l = int(rng.integers(20, min(n, 200)))
+    r1 = int(rng.integers(max(10, l // 2), min(n, 3 * l) + 1))
+    r2 = int(rng.integers(6, min(r1, 60)))
+    k = int(rng.integers(1, min(r2, l) + 1))
+    q = int(rng.integers(0, 3))
+    dtype = np.float64 if (i // 4) % 2 else np.float32
+    a = _matrix(m, n, min(m, n), float(rng.uniform(0.01, 0.06)), 10 * i + 7, dtype)
+    spec = skp.RangeFinderSpec(k=k, l=l, r1=r1, r2=r2, q=q, eps=0.5, seed=i, s=4,
+                               omega_kind=omega_kind)
+    qo = o.range_finder_sketched(a, o.Spec(k=k, l=l, r1=r1, r2=r2, q=q, seed=i, s=4,
+                                           omega_kind=omega_kind))
+    qb = skp.range_finder_sketched(a, spec)
+    assert qb.shape[1] == qo.shape[1], (omega_kind, qb.shape, qo.shape)
+    _, so, _ = o.randsvd(a, qo)
+    res = skp.randsvd(a, qb)
+    kk = min(k, len(so))
+    np.testing.assert_allclose(res.sigma[:kk], so[:kk], rtol=SIG_TOL[dtype], err_msg=omega_kind)
+    a64 = a.astype(np.float64)
+    q64 = qb.astype(np.float64)
+    e = np.linalg.norm(a64 - q64 @ (q64.T @ a64)) / np.linalg.norm(a64)
+    eo = o.proj_rel_error(a, qo)
+    assert abs(e - eo) <= 1e-3 * eo + 1e-12, (omega_kind, e, eo)
