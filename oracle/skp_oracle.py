@@ -266,6 +266,8 @@ class Spec:
     stabilized: bool = True
     s: int = 1
     omega_kind: str = "gaussian"
+    s2_kind: str | None = None
+    s2_r: int | None = None
 
 
 def power_iterate(atil, omega, q: int, stabilized: bool = True):
@@ -320,7 +322,8 @@ def lowrank_factorize(a, spec: Spec):
     atil = s1.apply_right(a)
     omega = draw_omega(spec.r1, spec.r2, substream(spec.seed, 1), spec.omega_kind)
     y = power_iterate(atil, omega, spec.q, stabilized=spec.stabilized)
-    s2 = CountSketch(spec.sketch_kind, m, spec.r1, substream(spec.seed, 2), s=spec.s)
+    s2 = CountSketch(spec.s2_kind or spec.sketch_kind, m, spec.s2_r or spec.r1,
+                     substream(spec.seed, 2), s=spec.s)
     return y, pinv(s2.apply_left_transpose(y)) @ s2.apply_left_transpose(a)
 
 

@@ -161,3 +161,29 @@ def test_sketch_apply_sweep(i):
     want_l = ref.apply_left_transpose(x)
     assert np.abs(got_r - want_r).max() <= tol * max(1.0, np.abs(want_r).max()) * np.sqrt(n)
     assert np.abs(got_l - want_l).max() <= tol * max(1.0, np.abs(want_l).max()) * np.sqrt(n)
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_lowrank_factorize_kinds_sweep(i):
+    """lowrank_factorize (power.py:202-239) with the secondary sketch's own
+    family and size (s2_kind, s2_r) and other primary families, vs the oracle."""
+    import paper_2605_09755_b200 as skp
+    rng = np.random.default_rng(9700 + i)
+    kind = ("countsketch", "srht", "gaussian", "sign")[i % 4]
+    s2_kind = ("srht", "countsketch", "sign", "gaussian")[(i // 4) % 4]
+    m, n = int(rng.integers(300, 2500)), int(rng.integers(200, 1500))
+    l = int(rng.integers(40, min(n, 300)))
+    r2 = int(rng.integers(8, min(l, 60)))
+    s2_r = int(rng.integers(r2 + 2, min(m, 4 * l) + 1))
+    q = int(rng.integers(0, 3))
+    dtype = np.float64 if i % 2 else np.float32
+    a = _graded(m, n, float(rng.uniform(0.5, 2.0)), min(m, n, 300), i + 50, dtype)
+    spec = skp.RangeFinderSpec(k=max(1, r2 - 5), l=l, r1=l, r2=r2, q=q, eps=0.5, seed=i, s=4,
+                               sketch_kind=kind, s2_kind=s2_kind, s2_r=s2_r)
+    yo, xo = o.lowrank_factorize(a, o.Spec(k=max(1, r2 - 5), l=l, r1=l, r2=r2, q=q, seed=i, s=4,
+                                           sketch_kind=kind, s2_kind=s2_kind, s2_r=s2_r))
+    res = skp.lowrank_factorize(a, spec)
+    a64 = a.astype(np.float64)
+    eo = np.linalg.norm(yo @ xo - a64) / np.linalg.norm(a64)
+    e = np.linalg.norm(res.Y.astype(np.float64) @ res.X - a64) / np.linalg.norm(a64)
+    assert abs(e - eo) <= 1e-3 * eo + (1e-6 if dtype == np.float32 else 1e-12), (kind, s2_kind, e, eo)
