@@ -187,3 +187,32 @@ def test_lowrank_factorize_kinds_sweep(i):
     eo = np.linalg.norm(yo @ xo - a64) / np.linalg.norm(a64)
     e = np.linalg.norm(res.Y.astype(np.float64) @ res.X - a64) / np.linalg.norm(a64)
     assert abs(e - eo) <= 1e-3 * eo + (1e-6 if dtype == np.float32 else 1e-12), (kind, s2_kind, e, eo)
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_nystrom_kinds_sweep(i):
+    """nystrom_psd with the other sketch families and start-block families
+    (orthonormalised core, the 1e-3 bar) vs the oracle."""
+    import paper_2605_09755_b200 as skp
+    rng = np.random.default_rng(9900 + i)
+    kind = ("srht", "gaussian", "sign", "countsketch")[i % 4]
+    omega_kind = ("gaussian", "sign")[(i // 4) % 2]
+    n = int(rng.integers(300, 2000))
+    l = int(rng.integers(40, min(n, 400)))
+    r2 = int(rng.integers(8, min(l, 60)))
+    dtype = np.float64 if i % 2 else np.float32
+    rank = int(rng.integers(r2, min(n, 300)))
+    u, _ = np.linalg.qr(rng.standard_normal((n, rank)))
+    kmat = (u * np.exp(-np.arange(rank) * float(rng.uniform(0.02, 0.1)))) @ u.T
+    kmat = ((kmat + kmat.T) / 2).astype(dtype)
+    spec = skp.RangeFinderSpec(k=max(1, r2 - 4), l=l, r1=l, r2=r2, q=2, eps=0.5, seed=i, s=4,
+                               sketch_kind=kind, omega_kind=omega_kind)
+    ospec = o.Spec(k=max(1, r2 - 4), l=l, r1=l, r2=r2, q=2, seed=i, s=4, sketch_kind=kind,
+                   omega_kind=omega_kind)
+    res = skp.nystrom_psd(kmat, spec, stabilized=True)
+    c = np.asarray(res.C.cpu() if hasattr(res.C, "cpu") else res.C, dtype=np.float64)
+    w = np.asarray(res.W.cpu() if hasattr(res.W, "cpu") else res.W, dtype=np.float64)
+    e = o.nystrom_rel_error(kmat, c, w)
+    co, wo = o.nystrom_core(kmat, ospec, stabilized=True)
+    eo = o.nystrom_rel_error(kmat, co, wo)
+    assert abs(e - eo) <= 1e-3 * eo + 1e-12, (kind, omega_kind, e, eo)
