@@ -170,3 +170,29 @@ def test_random_r1_and_omega_kinds_vs_oracle(i):
     e = np.linalg.norm(a64 - q64 @ (q64.T @ a64)) / np.linalg.norm(a64)
     eo = o.proj_rel_error(a, qo)
     assert abs(e - eo) <= 1e-3 * eo + 1e-12, (omega_kind, e, eo)
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_tiny_shapes_vs_oracle(i):
+    """Degenerate and tiny shapes through the reference's two calls: m or n
+    down to 1, l = 1, r2 = k = 1, s = r (every sketch column), q up to 3."""
+    import paper_2605_09755_b200 as skp
+    rng = np.random.default_rng(11000 + i)
+    m, n = int(rng.integers(1, 48)), int(rng.integers(1, 48))
+    l = int(rng.integers(1, min(m, n) + 1))
+    r1 = l
+    r2 = int(rng.integers(1, 12))
+    k = int(rng.integers(1, min(r2, l) + 1))
+    q = int(rng.integers(0, 4))
+    s = int(rng.integers(1, r1 + 1))
+    dtype = np.float64 if i % 2 else np.float32
+    a = rng.standard_normal((m, n)).astype(dtype)
+    spec = skp.RangeFinderSpec(k=k, l=l, r1=r1, r2=r2, q=q, eps=0.5, seed=i, s=s)
+    qo = o.range_finder_sketched(a, o.Spec(k=k, l=l, r1=r1, r2=r2, q=q, seed=i, s=s))
+    qb = skp.range_finder_sketched(a, spec)
+    assert qb.shape[1] == qo.shape[1], (m, n, l, r2, q, s, qb.shape, qo.shape)
+    _, so, _ = o.randsvd(a, qo)
+    res = skp.randsvd(a, qb)
+    kk = min(k, len(so))
+    np.testing.assert_allclose(res.sigma[:kk], so[:kk], rtol=SIG_TOL[dtype],
+                               err_msg=str((m, n, l, r2, q, s)))
