@@ -87,20 +87,22 @@ def test_lowrank_factorize_sweep(i):
     assert abs(e - eo) <= 1e-3 * eo + (1e-6 if dtype == np.float32 else 1e-12), (e, eo)
 
 
-@pytest.mark.parametrize("i", range(12))
+@pytest.mark.parametrize("i", range(16))
 def test_power_iterate_span_sweep(i):
     import paper_2605_09755_b200 as skp
     rng = np.random.default_rng(5000 + i)
     m, l = int(rng.integers(200, 3000)), int(rng.integers(20, 300))
     r2 = int(rng.integers(2, min(l, 60)))
     q = int(rng.integers(0, 4))
-    atil = _graded(m, l, float(rng.uniform(0.2, 1.5)), min(m, l), i, np.float64)
-    omega = np.random.default_rng(i).standard_normal((l, r2))
-    yo = o.power_iterate(atil, omega, q)
-    y = skp.power_iterate(atil, omega, q)
+    dtype = np.float64 if i < 12 else np.float32
+    stab = i % 3 != 2
+    atil = _graded(m, l, float(rng.uniform(0.2, 1.5)), min(m, l), i, dtype)
+    omega = np.random.default_rng(i).standard_normal((l, r2)).astype(dtype)
+    yo = o.power_iterate(atil, omega, q, stabilized=stab)
+    y = skp.power_iterate(atil, omega, q, stabilized=stab)
     assert y.shape == yo.shape
     d = _proj_dist(o.orthonormalize(y), o.orthonormalize(yo))
-    assert d <= 1e-6, d
+    assert d <= (1e-6 if dtype == np.float64 else 1e-3), (d, stab, q)
 
 
 @pytest.mark.parametrize("i", range(12))
