@@ -88,8 +88,8 @@ int skp_sketch_right_f64(const double* A, int64_t lda, int64_t m, int64_t n,
 
 /* K2 v2 (fp32, range-finder path): the same product written with PERMUTED
  * output columns, out = (A . S) P, by a row gather with a register-resident,
- * bank-conflict-free schedule.  The r columns are cut into ceil(r/768)
- * equal slices (one CTA each); P sorts the columns of each slice by entry
+ * bank-conflict-free schedule.  The r columns are cut into ceil(r/800)
+ * equal slices (rounded up to an even count; one or two per CTA); P sorts the columns of each slice by entry
  * count; its table is plan[0 .. r) (int32 column of S at each output
  * position; -1 from r to slices*768).  Build the plan once per sketch
  * (skp_sketch_gather_plan, from the
@@ -115,6 +115,11 @@ int skp_sketch_gather_plan(const int32_t* colptr, const int32_t* entries, int64_
 int skp_sketch_gather_f32(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
                           const void* plan, float scale, float* out, int64_t ldo, double* fro2,
                           int64_t* nonfinite, uint32_t* amax, void* stream);
+/* skp_sketch_gather_variant: which gather kernel skp_sketch_gather_f32 runs
+ * for (n, r) on the current device -- 3: two slices per CTA on a 16-bit
+ * schedule (an even slice count, column passes of <= 16384 words); 2: one
+ * slice per CTA.  Diagnostic only (same results either way).                 */
+int skp_sketch_gather_variant(int64_t n, int64_t r);
 /* skp_sketch_gather_f32_acc64: the same gather of fp32 A with fp64
  * accumulation and an fp64 output (the entries and their signs are exact in
  * fp64): the sketch C~ = K S of the psd Nystrom core (power.py:272-275),

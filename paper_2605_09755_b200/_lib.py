@@ -46,6 +46,7 @@ SIGNATURES = {
     "skp_sketch_gather_plan": (_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "skp_sketch_gather_f32": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, ctypes.c_float, _vp, _i64,
                                      _vp, _vp, _vp, _vp]),
+    "skp_sketch_gather_variant": (_int, [_i64, _i64]),
     "skp_sketch_gather_f32_acc64": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _f64, _vp, _i64, _vp,
                                            _vp, _vp]),
     "skp_sketch_left_t_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i32, _i64, _vp, _i64,

@@ -83,23 +83,29 @@ __device__ __forceinline__ uint32_t g_smem_u32(const void* p) {
 __device__ __forceinline__ void g_mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(g_smem_u32(bar)), "r"(count));
 }
+// try_wait with a suspend-time hint: a warp whose row has not landed sleeps in
+// the barrier unit until the phase completes (or ~1 ms) instead of spinning.
+// The spin form issued ~13 polls per row, each with the watchdog's clock
+// arithmetic if-converted into it: 37% of K2's instructions at C5 in an
+// issue-bound kernel (profiles/r02za_c5_pair_full.txt, before this change).
+__device__ __forceinline__ bool g_mbar_try(uint32_t a, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "n"(1000000)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void g_mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = g_smem_u32(bar);
-    long long t0 = 0;
-    for (int it = 0;; ++it) {
-        uint32_t ok;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(a), "r"(parity)
-            : "memory");
-        if (ok) return;
-        // watchdog: a protocol bug becomes a trap (error), never a hung GPU
-        if (it == 64) t0 = clock64();
-        if (it > 64 && (it & 1023) == 0 && clock64() - t0 > (long long)40e9) __trap();
-    }
+    if (g_mbar_try(a, parity)) return;
+    // watchdog (cold): a protocol bug becomes a trap (error), never a hung GPU
+    const long long t0 = clock64();
+    while (!g_mbar_try(a, parity))
+        if (clock64() - t0 > (long long)40e9) __trap();
 }
 __device__ __forceinline__ void g_mbar_arrive_e(uint64_t* bar) {
     asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\t"
@@ -655,6 +661,229 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
     }
 }
 
+// ---- K2 v3: two slices per CTA on a 16-bit schedule ----------------------------
+// What binds K2 at C5 is the row ingest: every one of the P slice CTAs of a
+// row group bulk-copies the whole row, and one SM receives ~150 GB/s however
+// many CTAs read the row (profiles/r02w_k2_ingest.txt: 40 ms of a 78 ms pass
+// at P = 10).  Here one CTA gathers two slices of the same plan from one copy
+// of the row, halving the ingest; the schedule of both fits the registers of
+// one because a pass of <= 16384 words needs 16-bit offsets: two entries per
+// register.  Entry at an even step: low half, byte offset - 128 in bits 2..15,
+// negate in bit 0; odd step: high half (bits 18..31), negate in bit 1.  Decode:
+//     even: LOP3 (w & 0xfffc) -> LDS -> LEA (x + (w << 31)) -> FADD
+//     odd:  SHR (w >> 16)     -> LDS -> SHL, LOP3 (sign)    -> FADD
+// (4.5 instructions per entry against 4; the LDS immediate carries the
+// buffer's absolute shared address SB + boff + 128, so SB -- the dynamic
+// shared memory base, after the reserved words -- is a template parameter,
+// probed once by the launcher).  The window [128, 128 + 65532] holds the row
+// from word 32 on and every zero word; an entry on one of the row's first 32
+// words is replaced by the zero word of its bank (no new conflict) and
+// gathered after the main steps (C3: ~1.5
+// such entries per warp and slice) from a per-lane table in shared memory.
+constexpr int kG3TR = 40;  // register-resident steps per slice (20 registers each)
+constexpr int kG3Heads = 8;  // head entries per lane (shared-memory table)
+constexpr size_t kG3Smem = GBuf<2>::smem + (size_t)kG3Heads * kGThreads * 4;
+template <uint32_t SB>
+__global__ void __maxnreg__(72)
+sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                          const int32_t* __restrict__ lanepos, int P2,
+                          const uint32_t* __restrict__ sched, const int32_t* __restrict__ tw,
+                          const int32_t* __restrict__ plan_fail, float scale,
+                          float* __restrict__ out, int64_t ldo, int64_t* nonfinite,
+                          uint32_t* __restrict__ amax, int accumulate, int mark_fail) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    if (*plan_fail) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && nonfinite && mark_fail)
+            atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), kGPlanFailMark);
+        return;
+    }
+    constexpr int TRK = kG3TR, RK = TRK / 2;
+    constexpr uint32_t kB = kGBufBytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * (size_t)kB);
+    uint32_t* done = reinterpret_cast<uint32_t*>(full + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sg = blockIdx.x % P2;
+    const int g = blockIdx.x / P2, G = gridDim.x / P2;
+    const uint32_t base = g_smem_u32(sm);  // == SB
+    const uint32_t zero_word = (uint32_t)((n + 31) / 32 * 32);
+    const uint32_t row_bytes = (uint32_t)((n + 3) / 4 * 16);
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            g_mbar_init(&full[b], 1);
+            done[b] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < 64) {
+        float* z = reinterpret_cast<float*>(sm + (threadIdx.x >> 5) * (size_t)kB);
+        z[zero_word + (threadIdx.x & 31)] = 0.f;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        for (int b = 0; b < 2; ++b)
+            if (g + b * (int64_t)G < m)
+                g_bulk_load_e(base + b * kB, A + (g + b * (int64_t)G) * lda, row_bytes, &full[b]);
+    }
+
+    // both slices' schedules -> packed registers; head entries -> this
+    // thread's column of the head table after the barriers (absolute
+    // address, bit 31 negate, bit 30 = slice 1; idle slots: a zero word)
+    const int wg0 = (2 * sg) * kGW + warp, wg1 = wg0 + kGW;
+    const int T0 = tw[wg0], T1 = tw[wg1];
+    uint32_t e[2 * RK];
+    uint32_t* heads = reinterpret_cast<uint32_t*>(sm + GBuf<2>::smem);
+#pragma unroll
+    for (int q = 0; q < kG3Heads; ++q) heads[q * kGThreads + threadIdx.x] = (zero_word + lane) * 4u + base;
+    int nhd = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int wgk = k ? wg1 : wg0, Tk = k ? T1 : T0;
+#pragma unroll
+        for (int t = 0; t < TRK; ++t) {
+            uint32_t v = t < Tk ? __ldg(sched + ((int64_t)wgk * kGTMax + t) * 32 + lane)
+                                : zero_word * 4u;
+            uint32_t off = v & 0x7fffffffu, neg = v >> 31;
+            if (t < Tk && off < 128u) {  // one of the row's first 32 words
+                const uint32_t h = (off + base) | (neg << 31) | ((uint32_t)k << 30);
+                if (nhd < kG3Heads) heads[nhd * kGThreads + threadIdx.x] = h;
+                ++nhd;
+                off = zero_word * 4u + off;  // the zero word of the same bank
+                neg = 0;
+            }
+            const uint32_t h16 = off - 128u;
+            if ((t & 1) == 0) e[k * RK + t / 2] = h16 | neg;
+            else e[k * RK + t / 2] |= (h16 << 16) | (neg << 1);
+        }
+    }
+    // heads: up to kG3Heads per lane from the table (C3/C5: at most 3; two
+    // columns of one lane share the ~256 head entries of a pass); a warp with
+    // more re-reads its schedule for them every row
+    const int HT = __reduce_max_sync(0xffffffffu, (unsigned)nhd);
+    const bool head_scan = HT > kG3Heads;
+    int lp = lanepos[(int64_t)wg0 * 32 + lane];
+    const int32_t v_out0 = lp & (kGPrimary - 1);
+    const bool valid0 = lp >= 0, primary0 = lp >= 0 && (lp & kGPrimary);
+    lp = lanepos[(int64_t)wg1 * 32 + lane];
+    const int32_t v_out1 = lp & (kGPrimary - 1);
+    const bool valid1 = lp >= 0, primary1 = lp >= 0 && (lp & kGPrimary);
+    bool bad = false;
+    uint32_t mx = 0;
+
+    auto do_row = [&](int64_t i, int b, uint32_t ph, auto boff_c) {
+        constexpr uint32_t boff = decltype(boff_c)::value;
+        constexpr uint32_t imm = SB + boff + 128u;
+        g_mbar_wait(&full[b], ph);
+#pragma unroll
+        for (int t = 0; t < 2 * RK; ++t) asm volatile("" : "+r"(e[t]));
+        float acc[2] = {0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int Tk = k ? T1 : T0;
+#pragma unroll
+            for (int t4 = 0; t4 < TRK; t4 += 4) {
+                if (t4 >= Tk) break;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint32_t w = e[k * RK + t4 / 2 + u];
+                    float x, y;
+                    asm("ld.shared.f32 %0, [%1+%2];" : "=f"(x) : "r"(w & 0xfffcu), "n"(imm));
+                    asm("ld.shared.f32 %0, [%1+%2];" : "=f"(y) : "r"(w >> 16), "n"(imm));
+                    acc[k] += __int_as_float(__float_as_int(x) + (int)(w << 31));
+                    acc[k] += __int_as_float(__float_as_int(y) ^ (int)((w << 30) & 0x80000000u));
+                }
+            }
+            const int wgk = k ? wg1 : wg0;
+            for (int t = TRK; t < Tk; ++t) {  // heavy warps: the rest from L1
+                const uint32_t ev = __ldg(sched + ((int64_t)wgk * kGTMax + t) * 32 + lane) + base;
+                float x;
+                asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(x) : "r"(ev & 0x7fffffffu), "n"(boff));
+                acc[k] += __int_as_float(__float_as_int(x) ^ (int)(ev & 0x80000000u));
+            }
+        }
+        if (!head_scan) {
+            for (int q = 0; q < HT; ++q) {
+                const uint32_t h = heads[q * kGThreads + threadIdx.x];
+                float x;
+                asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(x) : "r"(h & 0x3fffffffu), "n"(boff));
+                x = __int_as_float(__float_as_int(x) ^ (int)(h & 0x80000000u));
+                if (h & 0x40000000u) acc[1] += x;
+                else acc[0] += x;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int wgk = k ? wg1 : wg0, Tk = k ? T1 : T0;
+                for (int t = 0; t < min(Tk, TRK); ++t) {
+                    const uint32_t v = __ldg(sched + ((int64_t)wgk * kGTMax + t) * 32 + lane);
+                    if ((v & 0x7fffffffu) >= 128u) continue;
+                    float x;
+                    asm volatile("ld.shared.f32 %0, [%1+%2];"
+                                 : "=f"(x) : "r"((v & 0x7fffffffu) + base), "n"(boff));
+                    acc[k] += __int_as_float(__float_as_int(x) ^ (int)(v & 0x80000000u));
+                }
+            }
+        }
+        asm volatile("" : "+f"(acc[0]), "+f"(acc[1])::"memory");
+        __syncwarp();
+        if (lane == 0) {
+            if (atomicAdd(&done[b], 1u) == kGW - 1) {
+                done[b] = 0;
+                const int64_t nx = i + 2 * (int64_t)G;
+                if (nx < m) {
+                    asm volatile(
+                        "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                            g_smem_u32(&full[b])),
+                        "r"(row_bytes)
+                        : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+                        "[%1], %2, [%3];" ::"r"(base + (uint32_t)b * kB),
+                        "l"(reinterpret_cast<uint64_t>(A + nx * lda)), "r"(row_bytes),
+                        "r"(g_smem_u32(&full[b]))
+                        : "memory");
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const float part = __shfl_down_sync(0xffffffffu, acc[k], 1);
+            if (k ? primary1 : primary0) acc[k] += part;
+            if (k ? valid1 : valid0) {
+                float* po = out + i * ldo + (k ? v_out1 : v_out0);
+                const float o = accumulate ? fmaf(acc[k], scale, *po) : acc[k] * scale;
+                bad |= !isfinite(o);
+                mx = max(mx, __float_as_uint(fabsf(o)));
+                *po = o;
+            }
+        }
+    };
+
+    uint32_t ph = 0;
+    for (int64_t i = g; i < m; i += 2 * (int64_t)G, ph ^= 1u) {
+        do_row(i, 0, ph, std::integral_constant<uint32_t, 0>());
+        if (i + G < m) do_row(i + G, 1, ph, std::integral_constant<uint32_t, kB>());
+    }
+
+    if (amax) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0 && mx) atomicMax(amax, mx);
+    }
+    if (nonfinite) {
+        const unsigned nb = __popc(__ballot_sync(0xffffffffu, bad));
+        if (lane == 0 && nb)
+            atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), (unsigned long long)nb);
+    }
+}
+
+// the dynamic shared memory base of a kernel without static shared memory
+__global__ void smem_base_probe_kernel(uint32_t* out) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    if (threadIdx.x == 0) *out = g_smem_u32(sm);
+}
+
 // apply_right in the reference's column order: X[i, perm[v]] = X[i, v] in
 // place (X = the permuted A S P written by the gather).  One CTA holds the
 // inverse permutation and one row in shared memory: coalesced row read,
@@ -686,7 +915,11 @@ unpermute_cols_kernel(T* __restrict__ X, int64_t rows, int cols, int64_t ldx,
 // (with none, C3-like sketches put 56 steps on the heaviest warps, past the 44
 // register-resident ones); C3's 4000 columns -> 5 x 800
 constexpr int kGSpare = 96;
-int gather_slices(int64_t r) { return (int)cdiv(r, (int64_t)(kGCols - kGSpare)); }
+// (an even count above one slice: K2 v3 pairs the slices)
+int gather_slices(int64_t r) {
+    const int p = (int)cdiv(r, (int64_t)(kGCols - kGSpare));
+    return p > 1 ? (p + 1) / 2 * 2 : p;
+}
 // balanced slice width: the P slices share the r columns evenly (multiple of
 // 32), so no CTA carries a short last slice while its SM idles (C3: 6 x 672
 // instead of 5 x 768 + 160)
@@ -761,6 +994,28 @@ int gather_plan(const int32_t* colptr, const int32_t* entries, int64_t n, int64_
     return SKP_OK;
 }
 
+// dynamic shared memory base address on device `dev` (probed once; -1 on error)
+int smem_base(int dev, size_t smem) {
+    static int cached[64];
+    static bool have[64];
+    if (dev < 0 || dev >= 64) return -1;
+    if (have[dev]) return cached[dev];
+    uint32_t* d = nullptr;
+    uint32_t h = 0xffffffffu;
+    int rc = -1;
+    if (cudaFuncSetAttribute(smem_base_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) == cudaSuccess &&
+        cudaMalloc(&d, 4) == cudaSuccess) {
+        smem_base_probe_kernel<<<1, 32, smem>>>(d);
+        if (cudaMemcpy(&h, d, 4, cudaMemcpyDeviceToHost) == cudaSuccess) rc = (int)h;
+        cudaFree(d);
+    }
+    cudaGetLastError();
+    cached[dev] = rc;
+    have[dev] = true;
+    return rc;
+}
+
 template <typename Acc>
 int sketch_gather(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
                       const void* plan, Acc scale, Acc* out, int64_t ldo, double* fro2,
@@ -783,6 +1038,30 @@ int sketch_gather(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
     // output take two registers more)
     auto kern = sizeof(Acc) == 4 ? sketch_gather_kernel<2, Acc, kGTReg> : sketch_gather_kernel<2, Acc, 40>;
     const size_t smem = GBuf<2>::smem;
+    // K2 v3 (two slices per CTA) for fp32 passes of <= 16384 words
+    if constexpr (sizeof(Acc) == 4) {
+        const int sb = P % 2 == 0 && L.npass <= 16384 ? smem_base(dev, smem) : -1;
+        auto pk = sb == 0      ? sketch_gather_pair_kernel<0>
+                  : sb == 1024 ? sketch_gather_pair_kernel<1024>
+                               : nullptr;
+        if (pk) {
+            const int P2 = P / 2;
+            const int G2 = std::max(1, std::min<int>(sms / P2, (int)std::min<int64_t>(m, 1 << 20)));
+            SKP_CUDA(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kG3Smem));
+            for (int h = 0; h < L.H; ++h) {
+                const int64_t j0 = (int64_t)h * L.npass, nh = std::min<int64_t>(L.npass, n - j0);
+                const bool last = h + 1 == L.H;
+                pk<<<G2 * P2, kGThreads, kG3Smem, st>>>(
+                    A + j0, lda, m, nh, L.lanepos, P2, L.ps.sched[h], L.ps.tw[h], L.fail, scale,
+                    out, ldo, last ? nonfinite : (h == 0 ? nonfinite : nullptr),
+                    last ? amax : nullptr, h > 0, h == 0);
+                SKP_LAUNCHED(sketch_gather_pair_kernel);
+            }
+            if (fro2) return skp_sumsq_f32(A, m, n, lda, fro2, nullptr, st);
+            return SKP_OK;
+        }
+    }
     SKP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // one launch per column pass: pass h gathers A[:, h*npass ...] and adds
     // to what the earlier passes wrote; the checks ride on the last pass
@@ -859,4 +1138,11 @@ extern "C" int skp_unpermute_cols_f32(float* X, int64_t rows, int64_t cols, int6
 extern "C" int skp_unpermute_cols_f64(double* X, int64_t rows, int64_t cols, int64_t ldx,
                                       const int32_t* perm, void* stream) {
     return unpermute_cols<double>(X, rows, cols, ldx, perm, (cudaStream_t)stream);
+}
+extern "C" int skp_sketch_gather_variant(int64_t n, int64_t r) {
+    if (n < 1 || r < 1 || gather_passes(n) > kGMaxPass) return 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int sb = smem_base(dev, GBuf<2>::smem);
+    return gather_slices(r) % 2 == 0 && gather_npass(n) <= 16384 && (sb == 0 || sb == 1024) ? 3 : 2;
 }

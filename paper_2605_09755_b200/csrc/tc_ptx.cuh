@@ -22,32 +22,41 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, bool spin = false) {
+// mbarrier waits: try_wait with a suspend-time hint (the warp sleeps in the
+// barrier unit until the phase completes instead of polling) and the
+// watchdog in a cold path.  The earlier poll loop had the watchdog's clock
+// arithmetic if-converted into every poll: in K2 that was 37% of the issued
+// instructions (profiles/r02za_c5_pair_full.txt), and polling warps take
+// issue slots and power from the working ones.
+__device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "n"(1000000)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_cl(uint32_t a, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "n"(1000000)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
-    long long t0 = 0;
-    for (int it = 0;; ++it) {
-        uint32_t ok;
-        if (spin)
-            asm volatile(
-                "{\n\t.reg .pred p;\n\t"
-                "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                "selp.u32 %0, 1, 0, p;\n\t}"
-                : "=r"(ok)
-                : "r"(a), "r"(parity)
-                : "memory");
-        else
-            asm volatile(
-                "{\n\t.reg .pred p;\n\t"
-                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                "selp.u32 %0, 1, 0, p;\n\t}"
-                : "=r"(ok)
-                : "r"(a), "r"(parity)
-                : "memory");
-        if (ok) return;
-        // watchdog: a protocol bug becomes a trap (error), never a hung GPU
-        if (it == 64) t0 = clock64();
-        if (it > 64 && (it & 1023) == 0 && clock64() - t0 > (long long)40e9) __trap();
-    }
+    if (mbar_try(a, parity)) return;
+    // watchdog: a protocol bug becomes a trap (error), never a hung GPU
+    const long long t0 = clock64();
+    while (!mbar_try(a, parity))
+        if (clock64() - t0 > (long long)40e9) __trap();
 }
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
                                             int c0, int c1) {
@@ -124,20 +133,10 @@ __device__ __forceinline__ void cluster_sync_all() {
 // wait with cluster-scope acquire (barrier arrived on from the peer CTA)
 __device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
-    long long t0 = 0;
-    for (int it = 0;; ++it) {
-        uint32_t ok;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(a), "r"(parity)
-            : "memory");
-        if (ok) return;
-        if (it == 64) t0 = clock64();
-        if (it > 64 && (it & 1023) == 0 && clock64() - t0 > (long long)40e9) __trap();
-    }
+    if (mbar_try_cl(a, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_cl(a, parity))
+        if (clock64() - t0 > (long long)40e9) __trap();
 }
 template <bool kPair>
 __device__ __forceinline__ void mbar_wait_k(uint64_t* bar, uint32_t parity, bool cl_scope = false) {

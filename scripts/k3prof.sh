@@ -1,0 +1,6 @@
+# K2 v3 ncu captures: C3 (one launch) and C5 (one pass)
+O=gpurun_out
+timeout 900 python -m pytest tests/test_gpu_kernels.py -x -q -k "gather or sketch" > $O/k3_tests.log 2>&1; echo tests rc=$?
+tail -2 $O/k3_tests.log
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:pair -c 1 -o $O/r02za_c3_pair python scripts/sketch_time.py > $O/k3_ncu_c3.log 2>&1; echo ncu3 rc=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:pair -c 1 -o $O/r02za_c5_pair python scripts/sketch_time.py 1048576 32768 8000 > $O/k3_ncu_c5.log 2>&1; echo ncu5 rc=$?

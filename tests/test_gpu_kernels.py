@@ -177,7 +177,10 @@ def test_sketch_fused_norm_and_nonfinite(skp, ops):
                                      (40, 2050, 1600, 3), (1, 24576, 4000, 8),
                                      (9, 32768, 4000, 8), (3, 70001, 6000, 4),
                                      # the three-buffer ring wrapping several times
-                                     (300, 4096, 2000, 8), (1000, 8192, 768, 8)])
+                                     (300, 4096, 2000, 8), (1000, 8192, 768, 8),
+                                     # K2 v3 lanes with > 2 entries on the row's first
+                                     # 32 words (the re-read path), and an odd pass width
+                                     (50, 2000, 900, 32), (7, 16383, 1700, 5)])
 def test_sketch_gather_permuted(skp, ops, m, n, r, s):
     """K2 v2: (A S) P from the row-gather kernel == the oracle's A S with its
     columns taken in plan order; fused fp64 ||A||_F^2 and the non-finite test."""
@@ -210,6 +213,19 @@ def test_sketch_gather_permuted(skp, ops, m, n, r, s):
     bad.zero_()
     op.right_permuted(t, nonfinite=bad)
     assert int(bad.item()) >= 1
+
+
+def test_sketch_gather_variant(skp):
+    """The BASELINE sketch shapes run K2 v3 (two slices per CTA, 16-bit
+    schedule): C2 (n 10000, l 2000), C3 (16384, 4000), C5 (32768, 8000 in two
+    column passes); one slice per CTA where the slice count is one or a pass
+    is wider than 16384 words."""
+    from paper_2605_09755_b200 import _lib
+    v = _lib.load().skp_sketch_gather_variant
+    for n, r in [(10000, 2000), (16384, 4000), (32768, 8000), (32768, 16000)]:
+        assert v(n, r) == 3, (n, r)
+    # passes wider than 16384 words (C4's n = 65536: 3 x 21856) or one slice
+    assert v(24576, 4000) == 2 and v(65536, 4096) == 2 and v(16384, 700) == 2
 
 
 @pytest.mark.parametrize("m,n,r,s", [(67, 16384, 4000, 8), (9, 32768, 4000, 8), (3, 70001, 6000, 4),
