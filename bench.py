@@ -431,15 +431,22 @@ def run_ours(args, cfg, rank, world, local_rank):
     # entries/s at 1.95 GHz).  Work = the m n s gathered entries plus the row
     # ingest into each of the P slice CTAs (P n words per row), in entry units
     P_sl = -(-l // (896 - 96))
-    onchip_work = krows * (n * s_ + P_sl * n)
+    if v2:  # the plan's slice count (even where K2 v3 applies)
+        P_sl = int(_lib.load().skp_sketch_gather_plan_fail_offset(l)) // (896 * 4)
+    # K2 v3: one row copy feeds two slices (fp32, even slice count, column passes <= 16384 words)
+    n_pass = -(-n // 24576)
+    v3 = v2 and P_sl % 2 == 0 and -(-n // n_pass) <= 16384
+    copies = P_sl // 2 if v3 else P_sl
+    onchip_work = krows * (n * s_ + copies * n)
     onchip_ceiling = 148 * 32 * 0.957 * _SM_MAX_MHZ * 1e6
-    onchip = {"work_entries": onchip_work, "slices": P_sl,
+    onchip = {"work_entries": onchip_work, "slices": P_sl, "row_copies": copies,
               "achieved_entries_per_s": round(onchip_work / (sketch_ms * 1e-3), 1),
               "ceiling_entries_per_s": round(onchip_ceiling, 1),
               "frac_onchip": round(onchip_work / (sketch_ms * 1e-3) / onchip_ceiling, 4),
               "ceiling_source": "profiles/r02_smem_gather_ceiling.txt (scripts/micro/smem_gather.cu)"}
     kernels["sketch"] = {
-        "kernel": "sketch_gather (K2 v2)" if v2 else "sketch_right (K2 v1)", "bound": "hbm",
+        "kernel": ("sketch_gather_pair (K2 v3, two slices per CTA)" if v3 else "sketch_gather (K2 v2)") if v2
+        else "sketch_right (K2 v1)", "bound": "hbm",
         "onchip": onchip,
         "ms_per_launch": round(sketch_ms, 4),
         # (blocked: two passes over A, each timed here on krows rows)
