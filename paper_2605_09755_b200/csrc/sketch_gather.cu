@@ -848,8 +848,15 @@ sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, i
         asm volatile("" : "+f"(acc[0]), "+f"(acc[1])::"memory");
         __syncwarp();
         if (lane == 0) {
-            if (atomicAdd(&done[b], 1u) == kGW - 1) {
-                done[b] = 0;
+            // atom.inc wraps to 0 at the last warp by itself; an atom.add here
+            // (atomicAdd, or inline) is turned into a warp-aggregated add by
+            // ptxas, ~18 instructions per row and warp
+            uint32_t finished;
+            asm volatile("atom.shared.inc.u32 %0, [%1], %2;"
+                         : "=r"(finished)
+                         : "r"(base + 2u * kB + 16u + 4u * (uint32_t)b), "n"(kGW - 1)
+                         : "memory");
+            if (finished == kGW - 1) {
                 const int64_t nx = i + 2 * (int64_t)G;
                 if (nx < m) {
                     asm volatile(
@@ -866,12 +873,15 @@ sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, i
                 }
             }
         }
+        float* prow = out + i * ldo;  // one 64-bit product per row, not per slice
+        asm volatile("" : "+l"(prow));  // (opaque: or it is recomputed per slice)
+        __builtin_assume(__isGlobal(prow));
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const float part = __shfl_down_sync(0xffffffffu, acc[k], 1);
             if (k ? primary1 : primary0) acc[k] += part;
             if (k ? valid1 : valid0) {
-                float* po = out + i * ldo + (k ? v_out1 : v_out0);
+                float* po = prow + (k ? v_out1 : v_out0);
                 const float o = accumulate ? fmaf(acc[k], scale, *po) : acc[k] * scale;
                 mx = max(mx, __float_as_uint(fabsf(o)));  // (inf, nan: the largest patterns)
                 *po = o;
