@@ -99,6 +99,13 @@ __device__ __forceinline__ bool g_mbar_try(uint32_t a, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// (a = the barrier's shared address)
+__device__ __forceinline__ void g_mbar_wait_a(uint32_t a, uint32_t parity) {
+    if (g_mbar_try(a, parity)) return;
+    const long long t0 = clock64();
+    while (!g_mbar_try(a, parity))
+        if (clock64() - t0 > (long long)40e9) __trap();
+}
 __device__ __forceinline__ void g_mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = g_smem_u32(bar);
     if (g_mbar_try(a, parity)) return;
@@ -575,6 +582,9 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
 
     auto do_row = [&](int64_t i, int b, uint32_t ph, auto boff_c) {
         constexpr uint32_t boff = decltype(boff_c)::value;
+        // (column passes after the first: the earlier sums towards the L1 now,
+        // see the pair kernel)
+        if (accumulate && valid) asm volatile("prefetch.global.L1 [%0];" ::"l"(out + i * ldo + v_out));
         g_mbar_wait(&full[b], ph);
         // opaque per row: stops the compiler from hoisting the per-entry masks
         // out of the row loop (3x the registers, spills) and orders the loads
@@ -695,14 +705,15 @@ __device__ __forceinline__ void g_add2(float& a0, float& a1, float b0, float b1)
 constexpr int kG3TR = 40;  // register-resident steps per slice (20 registers each)
 constexpr int kG3Heads = 8;  // head entries per lane (shared-memory table)
 constexpr size_t kG3Smem = GBuf<2>::smem + (size_t)kG3Heads * kGThreads * 4;
-template <uint32_t SB>
+template <uint32_t SB, bool ACC>
 __global__ void __maxnreg__(72)
 sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                           const int32_t* __restrict__ lanepos, int P2,
                           const uint32_t* __restrict__ sched, const int32_t* __restrict__ tw,
                           const int32_t* __restrict__ plan_fail, float scale,
                           float* __restrict__ out, int64_t ldo, int64_t* nonfinite,
-                          uint32_t* __restrict__ amax, int accumulate, int mark_fail) {
+                          uint32_t* __restrict__ amax, int mark_fail) {
+    // ACC: a column pass after the first adds to what the earlier ones wrote
     extern __shared__ __align__(128) unsigned char sm[];
     if (*plan_fail) {
         if (blockIdx.x == 0 && threadIdx.x == 0 && nonfinite && mark_fail)
@@ -786,7 +797,21 @@ sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, i
     auto do_row = [&](int64_t i, int b, uint32_t ph, auto boff_c) {
         constexpr uint32_t boff = decltype(boff_c)::value;
         constexpr uint32_t imm = SB + boff + 128u;
-        g_mbar_wait(&full[b], ph);
+        // the barrier, the done count and the buffer of this row body at their
+        // absolute shared addresses (SB is a template parameter): no address
+        // arithmetic from the shared window base in the row loop
+        constexpr uint32_t kFull = SB + 2u * kB + (boff ? 8u : 0u);
+        constexpr uint32_t kDone = SB + 2u * kB + 16u + (boff ? 4u : 0u);
+        // a column pass after the first adds to the sums the earlier passes
+        // wrote: ask for them now, or every warp of the CTA meets their DRAM
+        // latency together at the end of the row (C5: pass 2 ran 89 ms against
+        // 63 ms for pass 1; K2 alone 131.3 -> 121.3 ms with the prefetch)
+        if constexpr (ACC) {
+            float* pr = out + i * ldo;  // (the next row's instead: the same, 121 ms)
+            if (valid0) asm volatile("prefetch.global.L1 [%0];" ::"l"(pr + v_out0));
+            if (valid1) asm volatile("prefetch.global.L1 [%0];" ::"l"(pr + v_out1));
+        }
+        g_mbar_wait_a(kFull, ph);
 #pragma unroll
         for (int t = 0; t < 2 * RK; ++t) asm volatile("" : "+r"(e[t]));
         float acc[2] = {0.f, 0.f};
@@ -854,21 +879,19 @@ sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, i
             uint32_t finished;
             asm volatile("atom.shared.inc.u32 %0, [%1], %2;"
                          : "=r"(finished)
-                         : "r"(base + 2u * kB + 16u + 4u * (uint32_t)b), "n"(kGW - 1)
+                         : "r"(kDone), "n"(kGW - 1)
                          : "memory");
             if (finished == kGW - 1) {
                 const int64_t nx = i + 2 * (int64_t)G;
                 if (nx < m) {
                     asm volatile(
-                        "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                            g_smem_u32(&full[b])),
+                        "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(kFull),
                         "r"(row_bytes)
                         : "memory");
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
-                        "[%1], %2, [%3];" ::"r"(base + (uint32_t)b * kB),
-                        "l"(reinterpret_cast<uint64_t>(A + nx * lda)), "r"(row_bytes),
-                        "r"(g_smem_u32(&full[b]))
+                        "[%1], %2, [%3];" ::"r"(SB + boff),
+                        "l"(reinterpret_cast<uint64_t>(A + nx * lda)), "r"(row_bytes), "r"(kFull)
                         : "memory");
                 }
             }
@@ -882,7 +905,7 @@ sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, i
             if (k ? primary1 : primary0) acc[k] += part;
             if (k ? valid1 : valid0) {
                 float* po = prow + (k ? v_out1 : v_out0);
-                const float o = accumulate ? fmaf(acc[k], scale, *po) : acc[k] * scale;
+                const float o = ACC ? fmaf(acc[k], scale, *po) : acc[k] * scale;
                 mx = max(mx, __float_as_uint(fabsf(o)));  // (inf, nan: the largest patterns)
                 *po = o;
             }
@@ -1073,21 +1096,24 @@ int sketch_gather(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
     // K2 v3 (two slices per CTA) for fp32 passes of <= 16384 words
     if constexpr (sizeof(Acc) == 4) {
         const int sb = P % 2 == 0 && L.npass <= 16384 ? smem_base(dev, smem) : -1;
-        auto pk = sb == 0      ? sketch_gather_pair_kernel<0>
-                  : sb == 1024 ? sketch_gather_pair_kernel<1024>
-                               : nullptr;
-        if (pk) {
+        auto pk0 = sb == 0      ? sketch_gather_pair_kernel<0, false>
+                   : sb == 1024 ? sketch_gather_pair_kernel<1024, false>
+                                : nullptr;
+        auto pk1 = sb == 0 ? sketch_gather_pair_kernel<0, true> : sketch_gather_pair_kernel<1024, true>;
+        if (pk0) {
             const int P2 = P / 2;
             const int G2 = std::max(1, std::min<int>(sms / P2, (int)std::min<int64_t>(m, 1 << 20)));
-            SKP_CUDA(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            SKP_CUDA(cudaFuncSetAttribute(pk0, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kG3Smem));
+            SKP_CUDA(cudaFuncSetAttribute(pk1, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)kG3Smem));
             for (int h = 0; h < L.H; ++h) {
                 const int64_t j0 = (int64_t)h * L.npass, nh = std::min<int64_t>(L.npass, n - j0);
                 const bool last = h + 1 == L.H;
-                pk<<<G2 * P2, kGThreads, kG3Smem, st>>>(
+                (h > 0 ? pk1 : pk0)<<<G2 * P2, kGThreads, kG3Smem, st>>>(
                     A + j0, lda, m, nh, L.lanepos, P2, L.ps.sched[h], L.ps.tw[h], L.fail, scale,
                     out, ldo, last ? nonfinite : (h == 0 ? nonfinite : nullptr),
-                    last ? amax : nullptr, h > 0, h == 0);
+                    last ? amax : nullptr, h == 0);
                 SKP_LAUNCHED(sketch_gather_pair_kernel);
             }
             if (fro2) return skp_sumsq_f32(A, m, n, lda, fro2, nullptr, st);
