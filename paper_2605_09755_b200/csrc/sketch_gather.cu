@@ -704,7 +704,13 @@ __device__ __forceinline__ void g_add2(float& a0, float& a1, float b0, float b1)
 // such entries per warp and slice) from a per-lane table in shared memory.
 constexpr int kG3TR = 40;  // register-resident steps per slice (20 registers each)
 constexpr int kG3Heads = 8;  // head entries per lane (shared-memory table)
-constexpr size_t kG3Smem = GBuf<2>::smem + (size_t)kG3Heads * kGThreads * 4;
+// two row buffers; three of 65664 bytes (16384 + 32 words) fit beside the
+// head table and were measured slower (C3 8.79 -> 9.24 ms, C5 121.0 -> 122.8
+// ms alone): the row loop is issue-bound, not waiting on the refill
+constexpr int kG3NB = 2;
+constexpr uint32_t kG3B = kGBufBytes;
+constexpr size_t kG3BufSmem = kG3NB * (size_t)kG3B + 64;
+constexpr size_t kG3Smem = kG3BufSmem + (size_t)kG3Heads * kGThreads * 4;
 template <uint32_t SB, bool ACC>
 __global__ void __maxnreg__(72)
 sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_t n,
@@ -721,9 +727,10 @@ sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, i
         return;
     }
     constexpr int TRK = kG3TR, RK = TRK / 2;
-    constexpr uint32_t kB = kGBufBytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * (size_t)kB);
-    uint32_t* done = reinterpret_cast<uint32_t*>(full + 2);
+    constexpr uint32_t kB = kG3B;
+    constexpr int NB = kG3NB;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + NB * (size_t)kB);
+    uint32_t* done = reinterpret_cast<uint32_t*>(full + NB);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sg = blockIdx.x % P2;
@@ -733,19 +740,19 @@ sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, i
     const uint32_t row_bytes = (uint32_t)((n + 3) / 4 * 16);
 
     if (threadIdx.x == 0) {
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NB; ++b) {
             g_mbar_init(&full[b], 1);
             done[b] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (threadIdx.x < 64) {
+    if (threadIdx.x < 32 * NB) {
         float* z = reinterpret_cast<float*>(sm + (threadIdx.x >> 5) * (size_t)kB);
         z[zero_word + (threadIdx.x & 31)] = 0.f;
     }
     __syncthreads();
     if (warp == 0) {
-        for (int b = 0; b < 2; ++b)
+        for (int b = 0; b < NB; ++b)
             if (g + b * (int64_t)G < m)
                 g_bulk_load_e(base + b * kB, A + (g + b * (int64_t)G) * lda, row_bytes, &full[b]);
     }
@@ -757,7 +764,7 @@ sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, i
     const int T0 = tw[wg0], T1 = tw[wg1];
     const int TM = max(T0, T1);
     uint32_t e[2 * RK];
-    uint32_t* heads = reinterpret_cast<uint32_t*>(sm + GBuf<2>::smem);
+    uint32_t* heads = reinterpret_cast<uint32_t*>(sm + kG3BufSmem);
 #pragma unroll
     for (int q = 0; q < kG3Heads; ++q) heads[q * kGThreads + threadIdx.x] = (zero_word + lane) * 4u + base;
     int nhd = 0;
@@ -800,8 +807,8 @@ sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, i
         // the barrier, the done count and the buffer of this row body at their
         // absolute shared addresses (SB is a template parameter): no address
         // arithmetic from the shared window base in the row loop
-        constexpr uint32_t kFull = SB + 2u * kB + (boff ? 8u : 0u);
-        constexpr uint32_t kDone = SB + 2u * kB + 16u + (boff ? 4u : 0u);
+        constexpr uint32_t kFull = SB + NB * kB + 8u * (boff / kB);
+        constexpr uint32_t kDone = SB + NB * kB + 8u * NB + 4u * (boff / kB);
         // a column pass after the first adds to the sums the earlier passes
         // wrote: ask for them now, or every warp of the CTA meets their DRAM
         // latency together at the end of the row (C5: pass 2 ran 89 ms against
@@ -882,7 +889,7 @@ sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, i
                          : "r"(kDone), "n"(kGW - 1)
                          : "memory");
             if (finished == kGW - 1) {
-                const int64_t nx = i + 2 * (int64_t)G;
+                const int64_t nx = i + NB * (int64_t)G;
                 if (nx < m) {
                     asm volatile(
                         "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(kFull),
@@ -913,9 +920,12 @@ sketch_gather_pair_kernel(const float* __restrict__ A, int64_t lda, int64_t m, i
     };
 
     uint32_t ph = 0;
-    for (int64_t i = g; i < m; i += 2 * (int64_t)G, ph ^= 1u) {
+    for (int64_t i = g; i < m; i += NB * (int64_t)G, ph ^= 1u) {
         do_row(i, 0, ph, std::integral_constant<uint32_t, 0>());
         if (i + G < m) do_row(i + G, 1, ph, std::integral_constant<uint32_t, kB>());
+        if constexpr (NB > 2)
+            if (i + 2 * (int64_t)G < m)
+                do_row(i + 2 * G, 2, ph, std::integral_constant<uint32_t, 2 * kB>());
     }
 
     // a non-finite output of this thread (iff a non-finite input): its |.|

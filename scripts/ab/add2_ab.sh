@@ -1,14 +1,10 @@
-# K2: T = tree, H = HEAD: C4 (K2 v2, fp64 accumulation, several column passes) and C5 in the step
-O=gpurun_out
-timeout 900 python -m pytest tests/test_gpu_kernels.py -q -m gpu -x -k "gather or sketch" 2>&1 | tail -2
-for v in T H; do
+# K2 v3: T = tree (two row buffers), NB3 = three row buffers of 65664 bytes
+for v in T NB3; do
   lib=scripts/ab/libskp_$v.so; [ $v = T ] && lib=paper_2605_09755_b200/libskp.so
-  timeout 600 python scripts/ab/run_lib.py $lib bench.py --config C4 --steps 5 --warmup 3 --no-e2e --no-cpu > $O/pf_c4_$v.json 2>/dev/null
-  python -c "
-import json; d=json.loads(open('$O/pf_c4_$v.json').read().strip().splitlines()[-1])
-print('$v c4', d['value'], d.get('phases_ms'), d['roofline'].get('ms_per_launch'))"
-  timeout 900 python scripts/ab/run_lib.py $lib bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > $O/pf_c5_$v.json 2>/dev/null
-  python -c "
-import json; d=json.loads(open('$O/pf_c5_$v.json').read().strip().splitlines()[-1])
-print('$v c5', d['value'], d['phases_ms']['apply_right'], {k: round(v['ms_per_launch'],2) for k, v in d['kernels'].items()}, d['clocks']['sm_mhz'])"
+  timeout 300 python scripts/ab/run_lib.py $lib scripts/ab/k2_sum.py 2>&1 | tail -3 | sed "s/^/$v digest: /"
 done
+for rep in 1 2; do for v in T NB3; do
+  lib=scripts/ab/libskp_$v.so; [ $v = T ] && lib=paper_2605_09755_b200/libskp.so
+  timeout 300 python scripts/ab/run_lib.py $lib scripts/sketch_time.py 2>&1 | tail -1 | sed "s/^/$v alone C3: /"
+  timeout 600 python scripts/ab/run_lib.py $lib scripts/sketch_time.py 1048576 32768 8000 2>&1 | tail -1 | sed "s/^/$v alone C5: /"
+done; done
