@@ -619,8 +619,13 @@ sketch_gather_kernel(const float* __restrict__ A, int64_t lda, int64_t m, int64_
         __syncwarp();
         if (lane == 0) {
             // the last warp done with this buffer refills it with row i + NB*G
-            if (atomicAdd(&done[b], 1u) == kGW - 1) {
-                done[b] = 0;
+            // (atom.inc wraps to 0 by itself; see the pair kernel)
+            uint32_t finished;
+            asm volatile("atom.shared.inc.u32 %0, [%1], %2;"
+                         : "=r"(finished)
+                         : "r"(g_smem_u32(&done[b])), "n"(kGW - 1)
+                         : "memory");
+            if (finished == kGW - 1) {
                 const int64_t nx = i + NB * (int64_t)G;
                 if (nx < m) {
                     asm volatile(
