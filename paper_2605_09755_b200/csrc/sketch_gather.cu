@@ -1141,14 +1141,27 @@ int sketch_gather(const float* A, int64_t lda, int64_t m, int64_t n, int64_t r,
                                           (int)kG3Smem));
             SKP_CUDA(cudaFuncSetAttribute(pk1, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)kG3Smem));
+            // Row chunks: the P2 CTAs of a row group copy the same rows, and only
+            // the first copy of a row should come from DRAM; left to themselves
+            // they drift apart by more rows than the L2 holds (C5: 253 GB read
+            // per pass for 69 GB of A).  Any coupling inside the kernel cost
+            // more than it saved (profiles/r02zc_k2_pacing_ab.txt); a kernel
+            // boundary every 512 row steps re-aligns them for ~15 us: C5 118.0
+            // -> 113.3 ms (flat from 384 to 1024 row steps; 128: 122.4 ms).  With
+            // P2 = 3 (C3) there is nothing to gain (8.75 -> 8.90 ms): one launch.
+            const int64_t chunk_rows = (int64_t)G2 * 512;
+            const int64_t chunk = (P2 >= 4 && m >= 8 * chunk_rows) ? chunk_rows : m;
             for (int h = 0; h < L.H; ++h) {
                 const int64_t j0 = (int64_t)h * L.npass, nh = std::min<int64_t>(L.npass, n - j0);
                 const bool last = h + 1 == L.H;
-                (h > 0 ? pk1 : pk0)<<<G2 * P2, kGThreads, kG3Smem, st>>>(
-                    A + j0, lda, m, nh, L.lanepos, P2, L.ps.sched[h], L.ps.tw[h], L.fail, scale,
-                    out, ldo, last ? nonfinite : (h == 0 ? nonfinite : nullptr),
-                    last ? amax : nullptr, h == 0);
-                SKP_LAUNCHED(sketch_gather_pair_kernel);
+                for (int64_t r0 = 0; r0 < m; r0 += chunk) {
+                    (h > 0 ? pk1 : pk0)<<<G2 * P2, kGThreads, kG3Smem, st>>>(
+                        A + j0 + r0 * lda, lda, std::min(chunk, m - r0), nh, L.lanepos, P2,
+                        L.ps.sched[h], L.ps.tw[h], L.fail, scale, out + r0 * ldo, ldo,
+                        last ? nonfinite : (h == 0 ? nonfinite : nullptr), last ? amax : nullptr,
+                        h == 0 && r0 == 0);
+                    SKP_LAUNCHED(sketch_gather_pair_kernel);
+                }
             }
             if (fro2) return skp_sumsq_f32(A, m, n, lda, fro2, nullptr, st);
             return SKP_OK;
