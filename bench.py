@@ -445,7 +445,7 @@ def run_ours(args, cfg, rank, world, local_rank):
               "frac_onchip": round(onchip_work / (sketch_ms * 1e-3) / onchip_ceiling, 4),
               "ceiling_source": "profiles/r02_smem_gather_ceiling.txt (scripts/micro/smem_gather.cu)"}
     kernels["sketch"] = {
-        "kernel": ("sketch_gather_pair (K2 v3, two slices per CTA)" if v3 else "sketch_gather (K2 v2)") if v2
+        "kernel": ("sketch_gather_pair (K2 v3, two slices per CTA; one launch here = one call: its column passes x row chunks)" if v3 else "sketch_gather (K2 v2)") if v2
         else "sketch_right (K2 v1)", "bound": "hbm",
         "onchip": onchip,
         "ms_per_launch": round(sketch_ms, 4),
